@@ -1,0 +1,314 @@
+/*
+ * ztp.h -- C ABI of the straggler-balanced 1D tensor-parallel linear layer
+ * (ZERO-resizing + SEMI-migration, arXiv 2401.11469) on B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n (Alg.1 l.k = P:202+k, Alg.2 l.k = P:293+k);
+ * S:n = SPEC.md line n; A-n = the reading of an ambiguous passage listed in
+ * DESIGN.md ("Readings").
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ *  - Indices are 0-based.  Ranks are 0..world-1.
+ *  - Layout: every tensor indexed by the pruned
+ *    contraction dimension K is stored with K as its OUTER (row) dimension:
+ *      x_t  [K, N]   input, feature-major (paper's input [bs*sql, K] transposed)
+ *      w_t  [K, n]   weight shard W^T     (paper's weight [n, K] transposed)
+ *      y_t  [n, N]   output, g_t [n, N] upstream gradient (paper's grad_input)
+ *      dx_t [K, N]   input gradient (paper's grad_output), dw_t [K, n]
+ *    Row-major, `ld` = elements between consecutive rows (>= cols, multiple
+ *    of 8 for bf16 so rows are 16-byte aligned), base pointer 16-byte aligned.
+ *  - Ownership: the caller owns every buffer passed in (device memory for
+ *    tensors and index lists, host memory for h_* arguments and results) and
+ *    every stream.  The library never frees caller memory.  The context owns
+ *    its NCCL communicator, cached TMA descriptors and workspaces.
+ *  - Streams are `cudaStream_t` passed as `void*` (NULL = legacy default).
+ *    Device work is enqueued asynchronously on that stream; host-side checks
+ *    run before anything is enqueued, and on error NOTHING is enqueued and
+ *    ztp_last_error() names the offending shapes/values.
+ *  - Asynchronous CUDA / NCCL failures are reported as ZTP_ECUDA / ZTP_ENCCL
+ *    by the next call that observes them (ztp_sync() forces the check).
+ *  - There is no CPU fallback: every compute step runs in this library's
+ *    CUDA kernels (or NCCL); a missing device is ZTP_ECUDA.
+ */
+#ifndef ZTP_H_
+#define ZTP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZTP_MAX_RANKS 8
+#define ZTP_UID_BYTES 128
+
+typedef enum ztp_status {
+  ZTP_OK = 0,
+  ZTP_EINVAL = 1,        /* bad argument value (NaN score, < 2 cost samples, empty T: S:549) */
+  ZTP_ESHAPE = 2,        /* shapes / leading dimensions inconsistent */
+  ZTP_EINDEX = 3,        /* index outside [0, K) */
+  ZTP_EDEGENERATE = 4,   /* #P >= K: nothing would survive */
+  ZTP_ELINEAGE = 5,      /* BWD selection differs from the FWD lineage entry */
+  ZTP_EHISTORY = 6,      /* Same imputation without history */
+  ZTP_ENOBASELINE = 7,   /* M_i = 0 in Eq.1 */
+  ZTP_ENOHELPER = 8,     /* migration with world = 1 */
+  ZTP_ERECEIVERS = 9,    /* e - x = 0 receivers */
+  ZTP_ECUDA = 10,
+  ZTP_ENCCL = 11,
+  ZTP_EUNSUPPORTED = 12
+} ztp_status;
+
+typedef enum ztp_dtype { ZTP_BF16 = 0, ZTP_F32 = 1 } ztp_dtype;
+
+/* A row-major 2-D device matrix.  rows = outer dimension. */
+typedef struct ztp_mat {
+  void* ptr;
+  int64_t rows, cols, ld;
+  int32_t dtype;           /* ztp_dtype */
+  int32_t _pad;
+} ztp_mat;
+
+typedef struct ztp_ctx ztp_ctx; /* one per rank / process / device */
+
+const char* ztp_status_str(ztp_status s);
+/* Last error message of `ctx` (ctx may be NULL: the calling thread's last
+ * error from a context-free call).  Valid until the next call. */
+const char* ztp_last_error(const ztp_ctx* ctx);
+/* Version string, e.g. "ztp 0.1 sm_100a". */
+const char* ztp_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Context.  world == 1 needs no NCCL id (uid may be NULL).  For world > 1,
+ * rank 0 calls ztp_get_unique_id() and the caller distributes the 128 bytes to
+ * every rank (e.g. torch.distributed.broadcast); every rank then calls
+ * ztp_ctx_create with its own rank and the CUDA device it owns.  Collective:
+ * all ranks must call it.  The communicator is NCCL over NVLink/NVSwitch.
+ * ------------------------------------------------------------------------- */
+ztp_status ztp_get_unique_id(unsigned char uid[ZTP_UID_BYTES]);
+ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world,
+                          const unsigned char* uid /* ZTP_UID_BYTES or NULL */, int device);
+ztp_status ztp_ctx_destroy(ztp_ctx* ctx);
+/* Blocks until `stream` drains and reports pending asynchronous errors
+ * (including device-side flags such as a NaN score seen by ztp_select). */
+ztp_status ztp_sync(ztp_ctx* ctx, void* stream);
+/* Number of kernels this context launched so far (own kernels only). */
+int64_t ztp_launch_count(const ztp_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * (1) Plan -- pure host, deterministic, no context, no device work.
+ *
+ * ztp_plan: per-rank runtimes T[e] and GEMM times M[e] (A-5, A-6) of the last
+ * statistics window -> resize ratios and the migrate-or-resize decision.
+ *   ZERO only (enable_migration = 0): Eq.1 with C = T_avg
+ *     (zero_crit = AVG, Alg.1 l.1) or T_min (MIN); every rank with
+ *     gamma > 0 resizes.
+ *   SEMI (enable_migration = 1, Alg.2): stragglers are ranks with
+ *     T > T_min (1 + eps) (A-17), ordered (T desc, rank asc) (A-21).
+ *     z = 1: gamma <= gamma_tol -> resize; else beta by bisection on Eq.2
+ *     (A-24), beta >= 1 - gamma_tol/gamma (A-23); phi = gamma beta,
+ *     gamma_r = gamma (1-beta)/(1-gamma beta) (A-16).
+ *     z > 1: Eq.3 scan (A-18..A-20): positions <= x migrate
+ *     (phi = gamma), the rest resize with Eq.1 at T_min.
+ *   L_ref: the reference column count of Eq.2/Eq.3 (A-25).
+ * Every double is computed in a fixed order in IEEE fp64 without contraction,
+ * so results are bit-identical on every rank and to the oracle.
+ * Errors: EINVAL (world not in 1..8, T not finite / negative, cost function
+ * with < 2 samples), ENOBASELINE (M_r <= 0 where Eq.1 is evaluated).
+ * ------------------------------------------------------------------------- */
+typedef struct ztp_pwl {       /* piecewise linear, x ascending, linear extrapolation */
+  int32_t n;
+  const double* x;
+  const double* y;
+} ztp_pwl;
+
+typedef struct ztp_costs {     /* Eq.2 / Eq.3 cost model (Alg.2 l.1 pretest) */
+  double omega1;               /* static allocation overhead Omega_1 */
+  ztp_pwl omega2;              /* dimension-extracting cost Omega_2(pruned columns) */
+  ztp_pwl phi1;                /* communication cost Phi_1(migrated columns) */
+  ztp_pwl phi2;                /* helper computation cost Phi_2(columns per helper) */
+} ztp_costs;
+
+typedef enum ztp_crit { ZTP_CRIT_AVG = 0, ZTP_CRIT_MIN = 1 } ztp_crit;
+
+typedef struct ztp_plan_opts {
+  int32_t enable_migration;    /* 0: ZERO-resizing only; 1: SEMI-migration */
+  int32_t zero_crit;           /* ztp_crit for ZERO-only mode (A-7) */
+  double gamma_max;            /* 0.9 (A-4) */
+  double eps;                  /* 0.02 straggler tolerance (A-17) */
+  double gamma_tol;            /* 0.5 resize-only bound (A-23) */
+  int32_t bisect_iters;        /* 64 (A-24) */
+  int32_t force_lambda;        /* -1 = Eq.3; >= 0 forces the migration group size */
+} ztp_plan_opts;
+
+typedef enum ztp_role { ZTP_NORMAL = 0, ZTP_RESIZE = 1, ZTP_MIGRATE = 2, ZTP_SPLIT = 3 } ztp_role;
+
+typedef struct ztp_plan_t {
+  int32_t world, z, x;
+  int32_t order[ZTP_MAX_RANKS];       /* ranks sorted by (T desc, rank asc) */
+  int32_t role[ZTP_MAX_RANKS];        /* ztp_role */
+  double gamma[ZTP_MAX_RANKS];        /* Eq.1 ratio (clamped) */
+  double beta[ZTP_MAX_RANKS];         /* migrated share of the shed work (Eq.2) */
+  double phi[ZTP_MAX_RANKS];          /* migrated fraction of hidden units = gamma beta */
+  double gamma_r[ZTP_MAX_RANKS];      /* prune ratio of the remaining work (A-16) */
+} ztp_plan_t;
+
+void ztp_plan_opts_default(ztp_plan_opts* o);
+ztp_status ztp_plan(int world, const double* T, const double* M, double L_ref,
+                    const ztp_costs* costs, const ztp_plan_opts* opts, ztp_plan_t* out);
+
+/* ztp_plan_counts: integer realisation of a plan for one linear of `rank`.
+ *   K       contraction length of this rank's linear (col: d_in; row: d_in/e)
+ *   n_units hidden units per rank that migration moves (MLP: f/e)
+ *   unit    migration granularity (1 for MLP units)
+ *   is_row  1 for a row-parallel linear (its K shrinks by the migrated units)
+ * n_mig = unit floor((n_units/unit) phi + 0.5) (<= n_units - unit);
+ * n_prune = floor(K_rem gamma_r + 0.5) clamped to K_rem - 1 (A-3, A-4);
+ * helper ranges: receivers ordered by r' = (r - s + e) % e, equal
+ * shares with the remainder to the lowest r' (A-28), contiguous inside the
+ * migrated tail [n_units - n_mig, n_units) (A-27). */
+typedef struct ztp_counts {
+  int32_t n_prune, n_mig;
+  int32_t n_out, out_dst[ZTP_MAX_RANKS];              /* my units [lo,hi) computed by out_dst */
+  int64_t out_lo[ZTP_MAX_RANKS], out_hi[ZTP_MAX_RANKS];
+  int32_t n_in, in_src[ZTP_MAX_RANKS];                /* in_src's units [lo,hi) computed by me */
+  int64_t in_lo[ZTP_MAX_RANKS], in_hi[ZTP_MAX_RANKS];
+} ztp_counts;
+
+ztp_status ztp_plan_counts(const ztp_plan_t* plan, int rank, int64_t K, int64_t n_units,
+                           int64_t unit, int is_row, ztp_counts* out);
+
+/* ---------------------------------------------------------------------------
+ * a1. Statistics exchange (Alg.1 l.1 / Alg.2 l.2): all-gather of (T_i, M_i)
+ * over the context's communicator, then a host copy.  Collective; blocks the
+ * host (this is the one host sync per replan).  T_all, M_all: host
+ * arrays of `world` doubles written in rank order.
+ * ------------------------------------------------------------------------- */
+ztp_status ztp_allgather_stats(ztp_ctx* ctx, double T_own, double M_own,
+                               double* T_all, double* M_all, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * (2) Priority select (Alg.1 l.12-14) -- device, stream-ordered.
+ * nseg segments (one per rank-local linear); segment i has h_seg_len[i]
+ * columns with fp32 scores (the per-column weight variation delta, Alg.1 l.4)
+ * at d_scores + sum_{j<i} h_seg_len[j].  It prunes the h_n_prune[i] columns
+ * with the smallest score, ties by ascending index (A-2); -0 == +0.
+ * Outputs (both ascending, Alg.1 l.14):
+ *   d_kept   segment i at offset sum_{j<i} (len_j - n_prune_j + append_j):
+ *            the kept indices S followed by h_append[i] appended indices
+ *            len_i, len_i+1, ... (migrated-in units on a helper, A-26);
+ *   d_pruned segment i at offset sum_{j<i} n_prune_j: the pruned indices P.
+ * h_append may be NULL (no appends).  One CTA per segment: radix select over
+ * the order-preserving 32-bit key of the score, ballot/popc compaction.
+ * Errors: EINVAL (nseg < 1, len < 1, n_prune outside [0, len-1]); a NaN score
+ * sets a device flag reported by ztp_sync() as EINVAL.
+ * ------------------------------------------------------------------------- */
+ztp_status ztp_select(ztp_ctx* ctx, int nseg, const int32_t* h_seg_len, const int32_t* h_n_prune,
+                      const int32_t* h_append, const float* d_scores,
+                      int32_t* d_kept, int32_t* d_pruned, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * (3)(4) Resized linears.  Collective semantics: every rank calls
+ * the same sequence.
+ *
+ * Lineage: `sel` = the entry <layer_id, matrix_id, P> -- device
+ * index lists kept (n_kept) and pruned (n_pruned), each ascending, with
+ * n_kept + n_pruned = K (appended units count as kept).  sel = NULL means
+ * dense (S = 0..K-1).  FWD records (layer_id, matrix_id) -> (kept, pruned,
+ * counts) in the context; BWD with a different entry returns ELINEAGE.
+ *
+ * FWD  y_t[j,t] = sum_{k in S} w_t[k,j] x_t[k,t]  for j < n_out
+ *      act = GELU: pre_t <- that sum, y_t <- GeLU_tanh(pre)
+ *      col layer: no collective (Megatron pairing) unless
+ *                 gather_output (all-gather of y over ranks).
+ *      row layer: y_t partial sums are all-reduced (sum) over ranks.
+ * BWD  dx_t[k,t] = sum_{j < n_out} w_t[k,j] g_t[j,t]  for k in S
+ *      dx_t[p,t]  = imputation for p in P (Zero; Average; Same from hist)
+ *      dw_t[k,j]  = sum_t x_t[k,t] g_t[j,t]           for k in S, j < n_out
+ *      dw_t[p,j]  = imputation for p in P
+ *      col layer: dx_t is all-reduced over ranks (the imputed rows
+ *                 are applied to the partial BEFORE the sum, A-14).
+ *      row layer: act_in = GELU multiplies dx_t by GeLU'(pre_in_t) (the
+ *                 input of this row layer was GeLU(pre_in)); no collective
+ *                 unless input_is_parallel == 0 (all-gather).
+ * dx_t or dw_t may have ptr = NULL to skip that GEMM.
+ * Shapes: x_t [K,N]; w_t [K, >= n_out]; y_t, pre_t [>= n_out, N];
+ * g_t [>= n_out, N]; dx_t, pre_in_t [K, N]; dw_t [K, >= n_out]; bf16 except
+ * ZTP_F32 verification mode (all fp32, SIMT FFMA, fp32 collectives).
+ * Errors: ESHAPE, EINDEX (host-visible lists), EDEGENERATE (n_kept == 0),
+ * ELINEAGE, EHISTORY, EUNSUPPORTED (dtype mix), ECUDA, ENCCL.
+ * ------------------------------------------------------------------------- */
+typedef enum ztp_phase { ZTP_FWD = 0, ZTP_BWD = 1 } ztp_phase;
+typedef enum ztp_impute { ZTP_IMPUTE_ZERO = 0, ZTP_IMPUTE_AVERAGE = 1, ZTP_IMPUTE_SAME = 2 } ztp_impute;
+typedef enum ztp_act { ZTP_ACT_NONE = 0, ZTP_ACT_GELU = 1 } ztp_act;
+
+typedef struct ztp_sel {
+  const int32_t* kept;
+  const int32_t* pruned;
+  int32_t n_kept, n_pruned;
+  int32_t layer_id, matrix_id;
+} ztp_sel;
+
+typedef struct ztp_linear_args {
+  ztp_mat x_t, w_t, y_t, pre_t, g_t, dx_t, dw_t, pre_in_t;
+  const ztp_sel* sel;          /* lineage entry; NULL = dense */
+  int64_t n_out;               /* output units computed (<= w_t.cols); 0 = w_t.cols */
+  int32_t impute;              /* ztp_impute (Zero is the paper's choice) */
+  int32_t act;                 /* FWD activation of this layer's output */
+  int32_t act_in;              /* BWD (row layer): activation feeding this layer */
+  int32_t gather_output;       /* col FWD: all-gather y over ranks */
+  int32_t input_is_parallel;   /* row BWD: 0 -> all-gather dx over ranks */
+  int32_t skip_collective;     /* 1: leave the all-reduce to the caller (fused later) */
+  const ztp_mat* hist_dx;      /* Same imputation history for dx_t (or NULL) */
+  const ztp_mat* hist_dw;      /* Same imputation history for dw_t (or NULL) */
+} ztp_linear_args;
+
+ztp_status ztp_col_linear(ztp_ctx* ctx, ztp_phase phase, const ztp_linear_args* a, void* stream);
+ztp_status ztp_row_linear(ztp_ctx* ctx, ztp_phase phase, const ztp_linear_args* a, void* stream);
+
+/* Stand-in attention core of the measurement layer (A-31): FWD ctx_t[f,t] =
+ * q[f,t] + k[f,t] + v[f,t] with qkv_t = [Q; K; V] row blocks of `feat` rows
+ * (the first n_feat of each block); BWD g_qkv_t = [dctx; dctx; dctx]. */
+ztp_status ztp_core(ztp_ctx* ctx, ztp_phase phase, const ztp_mat* qkv_t, const ztp_mat* ctx_t,
+                    int64_t feat, int64_t n_feat, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * (5) Migration -- peer copies of shard slices (A-26).
+ * Each transfer copies the sub-matrix src[r0:r0+nr, c0:c0+nc] held by
+ * src_rank into dst[dr0:dr0+nr, dc0:dc0+nc] held by dst_rank.  Every rank
+ * calls ztp_migrate with the SAME list; a rank acts only on transfers naming
+ * it (all transfers are issued inside one NCCL group, so any pattern is
+ * deadlock-free).  src_rank == dst_rank is a local device copy.  The slice is
+ * moved exactly once over NVLink (the straggler's egress is the scarce
+ * resource; helpers receive disjoint slices instead of full broadcasts).
+ * ------------------------------------------------------------------------- */
+typedef struct ztp_xfer {
+  ztp_mat src;                 /* meaningful on src_rank only */
+  ztp_mat dst;                 /* meaningful on dst_rank only */
+  int64_t r0, c0, nr, nc, dr0, dc0;
+  int32_t src_rank, dst_rank;
+} ztp_xfer;
+
+ztp_status ztp_migrate(ztp_ctx* ctx, int n, const ztp_xfer* xfers, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Straggler emulation and GEMM statistics (A-32).  chi > 1 makes every
+ * GEMM this context launches run chi times longer: a one-thread delay kernel
+ * after each GEMM spins until start + chi (end - start), where start/end are
+ * the GEMM's own %globaltimer stamps.  M (A-6) accumulates GEMM + delay time
+ * on the device; ztp_read_gemm_ns syncs `stream`, returns and resets it.
+ * ------------------------------------------------------------------------- */
+ztp_status ztp_set_slowdown(ztp_ctx* ctx, double chi);
+/* on = 1: stamp every GEMM and accumulate M even when chi == 1 (statistics
+ * window); off by default so unslowed ranks pay no extra launches. */
+ztp_status ztp_set_stats(ztp_ctx* ctx, int on);
+ztp_status ztp_read_gemm_ns(ztp_ctx* ctx, void* stream, double* ns);
+
+/* Raw resized GEMM (test / benchmark entry; the linears use it internally).
+ * kind 0 = FWD (y = w[S]^T x[S]), 1 = dX (dx rows by sel), 2 = dW. */
+ztp_status ztp_gemm(ztp_ctx* ctx, int kind, const ztp_linear_args* a, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZTP_H_ */

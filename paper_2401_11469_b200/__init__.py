@@ -1,0 +1,201 @@
+"""paper_2401_11469_b200 -- B200-native straggler-balanced 1D tensor-parallel
+linear layer (ZERO-resizing + SEMI-migration, arXiv 2401.11469).
+
+Python binding of the C ABI in include/ztp.h with the same names.  Every
+function marshals arguments (torch tensors are used only as device memory)
+and calls libztp.so; all compute runs in the library's sm_100a kernels and
+NCCL.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+from . import _lib
+from ._lib import (ACT_GELU, ACT_NONE, BF16, BWD, CRIT_AVG, CRIT_MIN, F32, FWD, IMPUTE_AVERAGE, IMPUTE_SAME,  # noqa
+                   IMPUTE_ZERO, KIND_DW, KIND_DX, KIND_FWD, MIGRATE, NORMAL, RESIZE, SPLIT, Costs, Counts,
+                   LinearArgs, Mat, PlanOpts, PlanT, Pwl, Sel, Xfer, ZtpError, check, lib)
+
+__all__ = [
+    "ztp_version", "ztp_get_unique_id", "ztp_ctx_create", "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count",
+    "ztp_plan", "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
+    "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "mat",
+    "make_costs", "plan_opts", "ZtpError",
+]
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def mat(t=None, rows: Optional[int] = None) -> Mat:
+    """ztp_mat view of a 2-D torch tensor (row-major, unit column stride)."""
+    if t is None:
+        return Mat(None, 0, 0, 0, 0, 0)
+    import torch
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("ztp_mat needs a 2-D tensor with unit column stride")
+    dt = {torch.bfloat16: BF16, torch.float32: F32}[t.dtype]
+    r = t.shape[0] if rows is None else rows
+    return Mat(t.data_ptr(), r, t.shape[1], t.stride(0), dt, 0)
+
+
+def ztp_version() -> str:
+    return lib.ztp_version().decode()
+
+
+def ztp_get_unique_id() -> bytes:
+    buf = C.create_string_buffer(_lib.UID_BYTES)
+    check(lib.ztp_get_unique_id(buf))
+    return buf.raw
+
+
+def ztp_ctx_create(rank: int = 0, world: int = 1, uid: Optional[bytes] = None, device: int = 0):
+    h = C.c_void_p()
+    check(lib.ztp_ctx_create(C.byref(h), rank, world, uid, device))
+    return h
+
+
+def ztp_ctx_destroy(ctx) -> None:
+    check(lib.ztp_ctx_destroy(ctx))
+
+
+def ztp_sync(ctx, stream=None) -> None:
+    check(lib.ztp_sync(ctx, _stream(stream)), ctx)
+
+
+def ztp_launch_count(ctx) -> int:
+    return int(lib.ztp_launch_count(ctx))
+
+
+# ------------------------------------------------------------------- plan (host)
+
+def _pwl(points):
+    xs, ys = points
+    n = len(xs)
+    xa = (C.c_double * n)(*xs)
+    ya = (C.c_double * n)(*ys)
+    return Pwl(n, xa, ya), (xa, ya)
+
+
+def make_costs(omega1=0.0, omega2=((0.0, 1.0), (0.0, 0.0)), phi1=((0.0, 1.0), (0.0, 0.0)),
+               phi2=((0.0, 1.0), (0.0, 0.0))):
+    """ztp_costs from (xs, ys) sample points; returns (Costs, keepalive)."""
+    o2, k1 = _pwl(omega2)
+    p1, k2 = _pwl(phi1)
+    p2, k3 = _pwl(phi2)
+    return Costs(omega1, o2, p1, p2), (k1, k2, k3)
+
+
+def plan_opts(**kw) -> PlanOpts:
+    o = PlanOpts()
+    lib.ztp_plan_opts_default(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def ztp_plan(T: Sequence[float], M: Sequence[float], L_ref: float, costs=None, opts: Optional[PlanOpts] = None
+             ) -> PlanT:
+    e = len(T)
+    Ta = (C.c_double * max(e, 1))(*T)
+    Ma = (C.c_double * max(e, 1))(*M)
+    if costs is None:
+        costs = make_costs()
+    c, _keep = costs if isinstance(costs, tuple) else (costs, None)
+    out = PlanT()
+    check(lib.ztp_plan(e, Ta, Ma, L_ref, C.byref(c), C.byref(opts or plan_opts()), C.byref(out)))
+    return out
+
+
+def ztp_plan_counts(plan: PlanT, rank: int, K: int, n_units: int, unit: int = 1, is_row: bool = False) -> Counts:
+    out = Counts()
+    check(lib.ztp_plan_counts(C.byref(plan), rank, K, n_units, unit, int(is_row), C.byref(out)))
+    return out
+
+
+def ztp_allgather_stats(ctx, T_own: float, M_own: float, world: int, stream=None):
+    Ta = (C.c_double * world)()
+    Ma = (C.c_double * world)()
+    check(lib.ztp_allgather_stats(ctx, T_own, M_own, Ta, Ma, _stream(stream)), ctx)
+    return list(Ta), list(Ma)
+
+
+# ------------------------------------------------------------------ device calls
+
+def ztp_select(ctx, seg_len: Sequence[int], n_prune: Sequence[int], scores, kept, pruned,
+               append: Optional[Sequence[int]] = None, stream=None) -> None:
+    n = len(seg_len)
+    la = (C.c_int32 * n)(*seg_len)
+    pa = (C.c_int32 * n)(*n_prune)
+    aa = (C.c_int32 * n)(*append) if append is not None else None
+    check(lib.ztp_select(ctx, n, la, pa, aa, scores.data_ptr(), kept.data_ptr(), pruned.data_ptr(),
+                         _stream(stream)), ctx)
+
+
+def sel(kept, n_kept: int, pruned, n_pruned: int, layer_id: int, matrix_id: int) -> Sel:
+    return Sel(kept.data_ptr() if kept is not None else None, pruned.data_ptr() if pruned is not None else None,
+               n_kept, n_pruned, layer_id, matrix_id)
+
+
+def linear_args(x_t=None, w_t=None, y_t=None, pre_t=None, g_t=None, dx_t=None, dw_t=None, pre_in_t=None,
+                sel_: Optional[Sel] = None, n_out: int = 0, impute: int = IMPUTE_ZERO, act: int = ACT_NONE,
+                act_in: int = ACT_NONE, skip_collective: int = 0) -> LinearArgs:
+    a = LinearArgs()
+    a.x_t, a.w_t, a.y_t, a.pre_t = mat(x_t), mat(w_t), mat(y_t), mat(pre_t)
+    a.g_t, a.dx_t, a.dw_t, a.pre_in_t = mat(g_t), mat(dx_t), mat(dw_t), mat(pre_in_t)
+    a.sel = C.pointer(sel_) if sel_ is not None else None
+    a.n_out = n_out
+    a.impute = impute
+    a.act = act
+    a.act_in = act_in
+    a.gather_output = 0
+    a.input_is_parallel = 1
+    a.skip_collective = skip_collective
+    return a
+
+
+def ztp_col_linear(ctx, phase: int, args: LinearArgs, stream=None) -> None:
+    check(lib.ztp_col_linear(ctx, phase, C.byref(args), _stream(stream)), ctx)
+
+
+def ztp_row_linear(ctx, phase: int, args: LinearArgs, stream=None) -> None:
+    check(lib.ztp_row_linear(ctx, phase, C.byref(args), _stream(stream)), ctx)
+
+
+def ztp_gemm(ctx, kind: int, args: LinearArgs, stream=None) -> None:
+    check(lib.ztp_gemm(ctx, kind, C.byref(args), _stream(stream)), ctx)
+
+
+def ztp_core(ctx, phase: int, qkv_t, ctx_t, feat: int, n_feat: int, stream=None) -> None:
+    q, c = mat(qkv_t), mat(ctx_t)
+    check(lib.ztp_core(ctx, phase, C.byref(q), C.byref(c), feat, n_feat, _stream(stream)), ctx)
+
+
+def ztp_migrate(ctx, xfers: Sequence[Xfer], stream=None) -> None:
+    n = len(xfers)
+    arr = (Xfer * max(n, 1))(*xfers)
+    check(lib.ztp_migrate(ctx, n, arr, _stream(stream)), ctx)
+
+
+def xfer(src=None, dst=None, r0=0, c0=0, nr=0, nc=0, dr0=0, dc0=0, src_rank=0, dst_rank=0) -> Xfer:
+    return Xfer(mat(src), mat(dst), r0, c0, nr, nc, dr0, dc0, src_rank, dst_rank)
+
+
+def ztp_set_slowdown(ctx, chi: float) -> None:
+    check(lib.ztp_set_slowdown(ctx, chi), ctx)
+
+
+def ztp_set_stats(ctx, on: bool) -> None:
+    check(lib.ztp_set_stats(ctx, int(on)), ctx)
+
+
+def ztp_read_gemm_ns(ctx, stream=None) -> float:
+    v = C.c_double()
+    check(lib.ztp_read_gemm_ns(ctx, _stream(stream), C.byref(v)), ctx)
+    return v.value

@@ -1,0 +1,609 @@
+// C ABI of libztp (include/ztp.h): context, select, resized linears with
+// their collectives, stand-in core, migration, statistics, emulation.
+// Host-side validation runs before anything is enqueued.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/ztp.h"
+#include "ztp_internal.h"
+
+namespace ztp {
+thread_local std::string g_thread_err;
+void set_thread_error(const std::string& msg) { g_thread_err = msg; }
+}  // namespace ztp
+
+struct LineageEntry {
+  const int32_t* kept;
+  const int32_t* pruned;
+  int32_t nk, np;
+};
+
+struct ztp_ctx {
+  int rank = 0, world = 1, device = 0, num_sms = 148;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int32_t* d_flags = nullptr;               // [0]: NaN score seen
+  unsigned long long* d_stamp = nullptr;    // [start_min, end_max]
+  unsigned long long* d_gemm_ns = nullptr;  // accumulated GEMM (+delay) time
+  double* d_stats = nullptr;                // 2 * world doubles
+  double chi = 1.0;
+  int stats = 0;
+  std::map<std::pair<int, int>, LineageEntry> lineage;
+  int32_t* d_iota = nullptr;
+  int64_t iota_cap = 0;
+  void* ws = nullptr;
+  size_t ws_cap = 0;
+};
+
+namespace {
+
+ztp_status fail(ztp_ctx* c, ztp_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  ztp::set_thread_error(msg);
+  return s;
+}
+
+#define CUDA_TRY(c, expr)                                                                  \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) return fail(c, ZTP_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NCCL_TRY(c, expr)                                                                  \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess) return fail(c, ZTP_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+std::string shp(const char* name, const ztp_mat& m) {
+  char b[160];
+  snprintf(b, sizeof b, "%s[%lld x %lld, ld %lld, %s]", name, (long long)m.rows, (long long)m.cols, (long long)m.ld,
+           m.dtype == ZTP_F32 ? "f32" : "bf16");
+  return b;
+}
+
+bool mat_ok(const ztp_mat& m) {
+  if (!m.ptr || m.rows < 1 || m.cols < 1 || m.ld < m.cols) return false;
+  if (m.dtype != ZTP_BF16 && m.dtype != ZTP_F32) return false;
+  const int64_t align = m.dtype == ZTP_BF16 ? 8 : 4;
+  if (m.ld % align != 0) return false;
+  if (reinterpret_cast<uintptr_t>(m.ptr) % 16 != 0) return false;
+  return true;
+}
+
+ztp_status ensure_iota(ztp_ctx* c, int64_t n) {
+  if (n <= c->iota_cap) return ZTP_OK;
+  int64_t cap = 1;
+  while (cap < n) cap <<= 1;
+  std::vector<int32_t> h(cap);
+  for (int64_t i = 0; i < cap; ++i) h[i] = (int32_t)i;
+  if (c->d_iota) cudaFree(c->d_iota);
+  CUDA_TRY(c, cudaMalloc(&c->d_iota, cap * sizeof(int32_t)));
+  CUDA_TRY(c, cudaMemcpy(c->d_iota, h.data(), cap * sizeof(int32_t), cudaMemcpyHostToDevice));
+  c->iota_cap = cap;
+  return ZTP_OK;
+}
+
+ztp_status ensure_ws(ztp_ctx* c, size_t bytes) {
+  if (bytes <= c->ws_cap) return ZTP_OK;
+  if (c->ws) cudaFree(c->ws);
+  c->ws = nullptr;
+  CUDA_TRY(c, cudaMalloc(&c->ws, bytes));
+  c->ws_cap = bytes;
+  return ZTP_OK;
+}
+
+bool emulating(const ztp_ctx* c) { return c->chi > 1.0 || c->stats; }
+
+ztp_status after_gemm(ztp_ctx* c, cudaStream_t st) {
+  if (!emulating(c)) return ZTP_OK;
+  CUDA_TRY(c, ztp::delay_launch(c->d_stamp, c->chi, c->d_gemm_ns, st));
+  ++c->launches;
+  return ZTP_OK;
+}
+
+ncclDataType_t nccl_type(int dtype) { return dtype == ZTP_F32 ? ncclFloat : ncclBfloat16; }
+
+// Resolve the lineage entry: sel == NULL -> dense S = 0..K-1.
+ztp_status resolve_sel(ztp_ctx* c, const ztp_sel* sel, int64_t K, const int32_t** kept, const int32_t** pruned,
+                       int* nk, int* np) {
+  if (sel == nullptr) {
+    ztp_status s = ensure_iota(c, K);
+    if (s != ZTP_OK) return s;
+    *kept = c->d_iota;
+    *pruned = nullptr;
+    *nk = (int)K;
+    *np = 0;
+    return ZTP_OK;
+  }
+  if ((int64_t)sel->n_kept + sel->n_pruned != K)
+    return fail(c, ZTP_ESHAPE,
+                "lineage: n_kept + n_pruned = " + std::to_string(sel->n_kept + sel->n_pruned) + " != K = " +
+                    std::to_string(K));
+  if (sel->n_kept < 1) return fail(c, ZTP_EDEGENERATE, "lineage: nothing survives (#P >= K, S:64)");
+  if (!sel->kept || (sel->n_pruned > 0 && !sel->pruned)) return fail(c, ZTP_EINVAL, "lineage: null index list");
+  *kept = sel->kept;
+  *pruned = sel->pruned;
+  *nk = sel->n_kept;
+  *np = sel->n_pruned;
+  return ZTP_OK;
+}
+
+// One resized GEMM + (optional) emulated slowdown.
+ztp_status gemm(ztp_ctx* c, int kind, const ztp_mat& x, const ztp_mat& w, const ztp_mat& g, int64_t n_out,
+                const int32_t* kept, const int32_t* pruned, int nk, const ztp_mat& out, const ztp_mat* out2,
+                const ztp_mat* aux, int epi, cudaStream_t st) {
+  const int dtype = (kind == ztp::KIND_DW ? x.dtype : w.dtype);
+  if (dtype == ZTP_BF16) {
+    ztp::GemmOperands o{};
+    o.x = x.ptr;
+    o.ld_x = x.ld;
+    o.w = w.ptr;
+    o.ld_w = w.ld;
+    o.g = g.ptr;
+    o.ld_g = g.ld;
+    o.n_cols = n_out;
+    ztp::GemmParams p{};
+    if (kind == ztp::KIND_FWD) {
+      o.K = x.rows;
+      o.N = x.cols;
+      p.M = (int)n_out;
+      p.N = (int)x.cols;
+      p.kdim = nk;
+    } else if (kind == ztp::KIND_DX) {
+      o.K = w.rows;
+      o.N = g.cols;
+      p.M = (int)w.rows;
+      p.N = (int)g.cols;
+      p.kdim = (int)n_out;
+    } else {
+      o.K = x.rows;
+      o.N = x.cols;
+      p.M = (int)x.rows;
+      p.N = (int)n_out;
+      p.kdim = (int)x.cols;
+    }
+    p.n_kept = nk;
+    p.kept = kept;
+    p.pruned = pruned;
+    p.epi = epi;
+    p.out = (__nv_bfloat16*)out.ptr;
+    p.ld_out = out.ld;
+    p.out2 = out2 ? (__nv_bfloat16*)out2->ptr : nullptr;
+    p.ld_out2 = out2 ? out2->ld : 0;
+    p.aux = aux ? (const __nv_bfloat16*)aux->ptr : nullptr;
+    p.ld_aux = aux ? aux->ld : 0;
+    p.stamp = emulating(c) ? c->d_stamp : nullptr;
+    CUDA_TRY(c, ztp::gemm_launch(kind, o, p, c->num_sms, st));
+  } else {
+    ztp::GemmParamsF32 p{};
+    p.kind = kind;
+    if (kind == ztp::KIND_FWD) {
+      p.M = (int)n_out;
+      p.N = (int)x.cols;
+      p.kdim = nk;
+    } else if (kind == ztp::KIND_DX) {
+      p.M = (int)w.rows;
+      p.N = (int)g.cols;
+      p.kdim = (int)n_out;
+    } else {
+      p.M = (int)x.rows;
+      p.N = (int)n_out;
+      p.kdim = (int)x.cols;
+    }
+    p.n_kept = nk;
+    p.kept = kept;
+    p.pruned = pruned;
+    p.x = (const float*)x.ptr;
+    p.ld_x = x.ld;
+    p.w = (const float*)w.ptr;
+    p.ld_w = w.ld;
+    p.g = (const float*)g.ptr;
+    p.ld_g = g.ld;
+    p.out = (float*)out.ptr;
+    p.ld_out = out.ld;
+    p.out2 = out2 ? (float*)out2->ptr : nullptr;
+    p.ld_out2 = out2 ? out2->ld : 0;
+    p.aux = aux ? (const float*)aux->ptr : nullptr;
+    p.ld_aux = aux ? aux->ld : 0;
+    p.epi = epi;
+    CUDA_TRY(c, ztp::gemm_f32_launch(p, st));
+  }
+  ++c->launches;
+  return after_gemm(c, st);
+}
+
+ztp_status allreduce(ztp_ctx* c, const ztp_mat& m, cudaStream_t st) {
+  if (c->world == 1) return ZTP_OK;
+  if (m.ld != m.cols) return fail(c, ZTP_ESHAPE, "all-reduce needs a contiguous tensor: " + shp("t", m));
+  NCCL_TRY(c, ncclAllReduce(m.ptr, m.ptr, (size_t)(m.rows * m.cols), nccl_type(m.dtype), ncclSum, c->comm, st));
+  return ZTP_OK;
+}
+
+enum { LAYER_COL = 0, LAYER_ROW = 1 };
+
+ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args* a, cudaStream_t st) {
+  if (!c || !a) return fail(c, ZTP_EINVAL, "linear: null ctx/args");
+  const char* nm = layer == LAYER_COL ? "ztp_col_linear" : "ztp_row_linear";
+  if (!mat_ok(a->x_t) && !(phase == ZTP_BWD && !a->dw_t.ptr))
+    return fail(c, ZTP_ESHAPE, std::string(nm) + ": bad " + shp("x_t", a->x_t));
+  if (!mat_ok(a->w_t)) return fail(c, ZTP_ESHAPE, std::string(nm) + ": bad " + shp("w_t", a->w_t));
+  const int64_t K = a->w_t.rows;
+  const int64_t n_out = a->n_out > 0 ? a->n_out : a->w_t.cols;
+  if (n_out > a->w_t.cols) return fail(c, ZTP_ESHAPE, std::string(nm) + ": n_out > w_t.cols");
+  if (a->impute != ZTP_IMPUTE_ZERO)
+    return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + ": Average/Same imputation are NEXT-2 (Zero only)");
+  if (a->gather_output || (phase == ZTP_BWD && layer == LAYER_ROW && !a->input_is_parallel))
+    return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + ": unpaired all-gather mode not built yet");
+  const int dtype = a->w_t.dtype;
+  const int32_t* kept;
+  const int32_t* pruned;
+  int nk, np;
+  ztp_status s = resolve_sel(c, a->sel, K, &kept, &pruned, &nk, &np);
+  if (s != ZTP_OK) return s;
+  const std::pair<int, int> key = a->sel ? std::make_pair(a->sel->layer_id, a->sel->matrix_id) : std::make_pair(-1, -1);
+
+  if (phase == ZTP_FWD) {
+    const ztp_mat& x = a->x_t;
+    if (x.rows != K || x.dtype != dtype)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD: " + shp("x_t", x) + " vs " + shp("w_t", a->w_t));
+    const int64_t N = x.cols;
+    if (!mat_ok(a->y_t) || a->y_t.rows < n_out || a->y_t.cols != N || a->y_t.dtype != dtype)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD: " + shp("y_t", a->y_t) + " for n_out " + std::to_string(n_out));
+    if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
+    const bool act = a->act == ZTP_ACT_GELU;
+    if (act && (!mat_ok(a->pre_t) || a->pre_t.rows < n_out || a->pre_t.cols != N))
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD GeLU: " + shp("pre_t", a->pre_t));
+    if (a->sel) c->lineage[key] = LineageEntry{a->sel->kept, a->sel->pruned, a->sel->n_kept, a->sel->n_pruned};
+    s = gemm(c, ztp::KIND_FWD, x, a->w_t, a->w_t, n_out, kept, pruned, nk, act ? a->pre_t : a->y_t,
+             act ? &a->y_t : nullptr, nullptr, act ? ztp::EPI_GELU : ztp::EPI_NONE, st);
+    if (s != ZTP_OK) return s;
+    if (layer == LAYER_ROW && !a->skip_collective) return allreduce(c, a->y_t, st);
+    return ZTP_OK;
+  }
+  // ----------------------------------------------------------------- BWD
+  if (a->sel) {
+    auto it = c->lineage.find(key);
+    if (it == c->lineage.end() || it->second.kept != a->sel->kept || it->second.pruned != a->sel->pruned ||
+        it->second.nk != a->sel->n_kept || it->second.np != a->sel->n_pruned)
+      return fail(c, ZTP_ELINEAGE,
+                  std::string(nm) + " BWD: no matching FWD lineage entry for <layer " +
+                      std::to_string(key.first) + ", matrix " + std::to_string(key.second) + "> (S:400)");
+  }
+  const ztp_mat& g = a->g_t;
+  if (!mat_ok(g) || g.rows < n_out || g.dtype != dtype)
+    return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("g_t", g));
+  const int64_t N = g.cols;
+  if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
+  if (a->dx_t.ptr) {
+    if (!mat_ok(a->dx_t) || a->dx_t.rows != K || a->dx_t.cols != N || a->dx_t.dtype != dtype)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dx_t", a->dx_t) + " vs K " + std::to_string(K));
+    int epi = ztp::EPI_NONE;
+    const ztp_mat* aux = nullptr;
+    if (layer == LAYER_ROW && a->act_in == ZTP_ACT_GELU) {
+      if (!mat_ok(a->pre_in_t) || a->pre_in_t.rows != K || a->pre_in_t.cols != N)
+        return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD GeLU': " + shp("pre_in_t", a->pre_in_t));
+      epi = ztp::EPI_GELU_GRAD;
+      aux = &a->pre_in_t;
+    }
+    s = gemm(c, ztp::KIND_DX, a->x_t, a->w_t, g, n_out, kept, pruned, nk, a->dx_t, nullptr, aux, epi, st);
+    if (s != ZTP_OK) return s;
+  }
+  const bool reduce_dx = layer == LAYER_COL && a->dx_t.ptr && !a->skip_collective && c->world > 1;
+  if (reduce_dx) {
+    // overlap the dX all-reduce with the dW GEMM: comm on a side stream
+    CUDA_TRY(c, cudaEventRecord(c->ev_a, st));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_a, 0));
+    s = allreduce(c, a->dx_t, c->comm_stream);
+    if (s != ZTP_OK) return s;
+    CUDA_TRY(c, cudaEventRecord(c->ev_b, c->comm_stream));
+  }
+  if (a->dw_t.ptr) {
+    const ztp_mat& x = a->x_t;
+    if (x.rows != K || x.cols != N || x.dtype != dtype)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("x_t", x) + " vs " + shp("g_t", g));
+    if (!mat_ok(a->dw_t) || a->dw_t.rows != K || a->dw_t.cols < n_out || a->dw_t.dtype != dtype)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dw_t", a->dw_t));
+    s = gemm(c, ztp::KIND_DW, x, a->w_t, g, n_out, kept, pruned, nk, a->dw_t, nullptr, nullptr, ztp::EPI_NONE, st);
+    if (s != ZTP_OK) return s;
+  }
+  if (reduce_dx) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_b, 0));
+  return ZTP_OK;
+}
+
+}  // namespace
+
+// =========================================================================== API
+
+extern "C" {
+
+const char* ztp_status_str(ztp_status s) {
+  switch (s) {
+    case ZTP_OK: return "ZTP_OK";
+    case ZTP_EINVAL: return "ZTP_EINVAL";
+    case ZTP_ESHAPE: return "ZTP_ESHAPE";
+    case ZTP_EINDEX: return "ZTP_EINDEX";
+    case ZTP_EDEGENERATE: return "ZTP_EDEGENERATE";
+    case ZTP_ELINEAGE: return "ZTP_ELINEAGE";
+    case ZTP_EHISTORY: return "ZTP_EHISTORY";
+    case ZTP_ENOBASELINE: return "ZTP_ENOBASELINE";
+    case ZTP_ENOHELPER: return "ZTP_ENOHELPER";
+    case ZTP_ERECEIVERS: return "ZTP_ERECEIVERS";
+    case ZTP_ECUDA: return "ZTP_ECUDA";
+    case ZTP_ENCCL: return "ZTP_ENCCL";
+    case ZTP_EUNSUPPORTED: return "ZTP_EUNSUPPORTED";
+  }
+  return "ZTP_?";
+}
+
+const char* ztp_last_error(const ztp_ctx* c) { return c ? c->err.c_str() : ztp::g_thread_err.c_str(); }
+
+const char* ztp_version(void) { return "ztp 0.1 sm_100a (tcgen05 + TMA gather4 + NCCL)"; }
+
+ztp_status ztp_get_unique_id(unsigned char uid[ZTP_UID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == ZTP_UID_BYTES, "ncclUniqueId size");
+  ncclUniqueId id;
+  NCCL_TRY(nullptr, ncclGetUniqueId(&id));
+  std::memcpy(uid, &id, ZTP_UID_BYTES);
+  return ZTP_OK;
+}
+
+ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned char* uid, int device) {
+  if (!out) return fail(nullptr, ZTP_EINVAL, "ztp_ctx_create: out is NULL");
+  *out = nullptr;
+  if (world < 1 || world > ZTP_MAX_RANKS || rank < 0 || rank >= world)
+    return fail(nullptr, ZTP_EINVAL, "ztp_ctx_create: rank/world out of range");
+  if (world > 1 && !uid) return fail(nullptr, ZTP_EINVAL, "ztp_ctx_create: world > 1 needs an NCCL unique id");
+  CUDA_TRY(nullptr, cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(nullptr, cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(nullptr, ZTP_EUNSUPPORTED,
+                std::string("libztp is built for sm_100a (B200) only; device is ") + prop.name + " sm_" +
+                    std::to_string(prop.major) + std::to_string(prop.minor));
+  ztp_ctx* c = new ztp_ctx();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  auto cleanup = [&](ztp_status s) {
+    ztp_ctx_destroy(c);
+    return s;
+  };
+  if (cudaMalloc(&c->d_flags, 64) != cudaSuccess || cudaMalloc(&c->d_stamp, 16) != cudaSuccess ||
+      cudaMalloc(&c->d_gemm_ns, 16) != cudaSuccess || cudaMalloc(&c->d_stats, 2 * (ZTP_MAX_RANKS + 1) * sizeof(double)) != cudaSuccess)
+    return cleanup(fail(nullptr, ZTP_ECUDA, "ztp_ctx_create: device allocation failed"));
+  cudaMemset(c->d_flags, 0, 64);
+  unsigned long long init_stamp[2] = {~0ull, 0ull};
+  cudaMemcpy(c->d_stamp, init_stamp, 16, cudaMemcpyHostToDevice);
+  cudaMemset(c->d_gemm_ns, 0, 16);
+  if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess)
+    return cleanup(fail(nullptr, ZTP_ECUDA, "ztp_ctx_create: stream/event creation failed"));
+  if (ensure_iota(c, 1 << 16) != ZTP_OK) return cleanup(ZTP_ECUDA);
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, uid, ZTP_UID_BYTES);
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess)
+      return cleanup(fail(nullptr, ZTP_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+  }
+  *out = c;
+  return ZTP_OK;
+}
+
+ztp_status ztp_ctx_destroy(ztp_ctx* c) {
+  if (!c) return ZTP_OK;
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
+  cudaFree(c->d_flags);
+  cudaFree(c->d_stamp);
+  cudaFree(c->d_gemm_ns);
+  cudaFree(c->d_stats);
+  cudaFree(c->d_iota);
+  cudaFree(c->ws);
+  delete c;
+  return ZTP_OK;
+}
+
+ztp_status ztp_sync(ztp_ctx* c, void* stream) {
+  if (!c) return fail(nullptr, ZTP_EINVAL, "ztp_sync: null ctx");
+  CUDA_TRY(c, cudaStreamSynchronize((cudaStream_t)stream));
+  CUDA_TRY(c, cudaGetLastError());
+  int32_t flags = 0;
+  CUDA_TRY(c, cudaMemcpy(&flags, c->d_flags, 4, cudaMemcpyDeviceToHost));
+  if (flags) {
+    cudaMemset(c->d_flags, 0, 4);
+    return fail(c, ZTP_EINVAL, "ztp_select saw a NaN score");
+  }
+  return ZTP_OK;
+}
+
+int64_t ztp_launch_count(const ztp_ctx* c) { return c ? c->launches : 0; }
+
+ztp_status ztp_allgather_stats(ztp_ctx* c, double T_own, double M_own, double* T_all, double* M_all, void* stream) {
+  if (!c || !T_all || !M_all) return fail(c, ZTP_EINVAL, "ztp_allgather_stats: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  double mine[2] = {T_own, M_own};
+  if (c->world == 1) {
+    T_all[0] = T_own;
+    M_all[0] = M_own;
+    return ZTP_OK;
+  }
+  double* d_send = c->d_stats + 2 * ZTP_MAX_RANKS;  // scratch after the gathered block
+  std::vector<double> host(2 * c->world);
+  CUDA_TRY(c, cudaMemcpyAsync(d_send, mine, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+  NCCL_TRY(c, ncclAllGather(d_send, c->d_stats, 2, ncclDouble, c->comm, st));
+  CUDA_TRY(c, cudaMemcpyAsync(host.data(), c->d_stats, 2 * c->world * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  for (int r = 0; r < c->world; ++r) {
+    T_all[r] = host[2 * r];
+    M_all[r] = host[2 * r + 1];
+  }
+  return ZTP_OK;
+}
+
+ztp_status ztp_select(ztp_ctx* c, int nseg, const int32_t* h_len, const int32_t* h_np, const int32_t* h_app,
+                      const float* d_scores, int32_t* d_kept, int32_t* d_pruned, void* stream) {
+  if (!c || !h_len || !h_np || !d_scores || !d_kept || !d_pruned || nseg < 1)
+    return fail(c, ZTP_EINVAL, "ztp_select: null argument or nseg < 1");
+  std::vector<ztp::SelectSeg> segs(nseg);
+  int64_t so = 0, ko = 0, po = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const int32_t app = h_app ? h_app[i] : 0;
+    if (h_len[i] < 1 || h_np[i] < 0 || h_np[i] > h_len[i] - 1 || app < 0)
+      return fail(c, ZTP_EINVAL,
+                  "ztp_select: segment " + std::to_string(i) + " len " + std::to_string(h_len[i]) + " n_prune " +
+                      std::to_string(h_np[i]) + " (need 0 <= n_prune <= len-1)");
+    segs[i] = ztp::SelectSeg{h_len[i], h_np[i], app, (int32_t)so, (int32_t)ko, (int32_t)po};
+    so += h_len[i];
+    ko += h_len[i] - h_np[i] + app;
+    po += h_np[i];
+  }
+  if (so > INT32_MAX) return fail(c, ZTP_EINVAL, "ztp_select: too many columns");
+  for (int b = 0; b < nseg; b += ztp::SELECT_MAX_SEGS) {
+    ztp::SelectParams p{};
+    p.nseg = std::min(ztp::SELECT_MAX_SEGS, nseg - b);
+    for (int i = 0; i < p.nseg; ++i) p.seg[i] = segs[b + i];
+    CUDA_TRY(c, ztp::select_launch(p, d_scores, d_kept, d_pruned, c->d_flags, (cudaStream_t)stream));
+    ++c->launches;
+  }
+  return ZTP_OK;
+}
+
+ztp_status ztp_col_linear(ztp_ctx* c, ztp_phase phase, const ztp_linear_args* a, void* stream) {
+  return linear(c, LAYER_COL, phase, a, (cudaStream_t)stream);
+}
+ztp_status ztp_row_linear(ztp_ctx* c, ztp_phase phase, const ztp_linear_args* a, void* stream) {
+  return linear(c, LAYER_ROW, phase, a, (cudaStream_t)stream);
+}
+
+ztp_status ztp_gemm(ztp_ctx* c, int kind, const ztp_linear_args* a, void* stream) {
+  if (!c || !a || kind < 0 || kind > 2) return fail(c, ZTP_EINVAL, "ztp_gemm: bad arguments");
+  const int64_t K = a->w_t.rows ? a->w_t.rows : a->x_t.rows;
+  const int64_t n_out = a->n_out > 0 ? a->n_out : (kind == ztp::KIND_DW ? a->dw_t.cols : a->w_t.cols);
+  const int32_t* kept;
+  const int32_t* pruned;
+  int nk, np;
+  ztp_status s = resolve_sel(c, a->sel, K, &kept, &pruned, &nk, &np);
+  if (s != ZTP_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kind == ztp::KIND_FWD) {
+    const bool act = a->act == ZTP_ACT_GELU;
+    return gemm(c, kind, a->x_t, a->w_t, a->w_t, n_out, kept, pruned, nk, act ? a->pre_t : a->y_t,
+                act ? &a->y_t : nullptr, nullptr, act ? ztp::EPI_GELU : ztp::EPI_NONE, st);
+  }
+  if (kind == ztp::KIND_DX) {
+    const bool gg = a->act_in == ZTP_ACT_GELU;
+    return gemm(c, kind, a->x_t, a->w_t, a->g_t, n_out, kept, pruned, nk, a->dx_t, nullptr, gg ? &a->pre_in_t : nullptr,
+                gg ? ztp::EPI_GELU_GRAD : ztp::EPI_NONE, st);
+  }
+  return gemm(c, kind, a->x_t, a->w_t, a->g_t, n_out, kept, pruned, nk, a->dw_t, nullptr, nullptr, ztp::EPI_NONE, st);
+}
+
+ztp_status ztp_core(ztp_ctx* c, ztp_phase phase, const ztp_mat* qkv, const ztp_mat* cx, int64_t feat, int64_t n_feat,
+                    void* stream) {
+  if (!c || !qkv || !cx || !mat_ok(*qkv) || !mat_ok(*cx)) return fail(c, ZTP_ESHAPE, "ztp_core: bad matrices");
+  if (qkv->rows < 3 * feat || n_feat > feat || cx->rows < n_feat || cx->cols != qkv->cols || qkv->dtype != cx->dtype)
+    return fail(c, ZTP_ESHAPE, "ztp_core: " + shp("qkv_t", *qkv) + " " + shp("ctx_t", *cx));
+  if (qkv->dtype == ZTP_BF16 && qkv->cols % 8) return fail(c, ZTP_ESHAPE, "ztp_core: N % 8 != 0");
+  CUDA_TRY(c, ztp::core_launch(phase == ZTP_FWD ? 0 : 1, qkv->ptr, qkv->ld, cx->ptr, cx->ld, feat, n_feat, qkv->cols,
+                               qkv->dtype, (cudaStream_t)stream));
+  ++c->launches;
+  return ZTP_OK;
+}
+
+ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
+  if (!c || (n > 0 && !xs)) return fail(c, ZTP_EINVAL, "ztp_migrate: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<size_t> off(n, 0);
+  size_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    const ztp_xfer& x = xs[i];
+    if (x.src_rank < 0 || x.src_rank >= c->world || x.dst_rank < 0 || x.dst_rank >= c->world || x.nr < 0 || x.nc < 0)
+      return fail(c, ZTP_EINVAL, "ztp_migrate: transfer " + std::to_string(i) + " has bad ranks/sizes");
+    const bool me_src = x.src_rank == c->rank, me_dst = x.dst_rank == c->rank;
+    if (me_src && (!mat_ok(x.src) || x.r0 + x.nr > x.src.rows || x.c0 + x.nc > x.src.cols))
+      return fail(c, ZTP_ESHAPE, "ztp_migrate: source slice outside " + shp("src", x.src));
+    if (me_dst && (!mat_ok(x.dst) || x.dr0 + x.nr > x.dst.rows || x.dc0 + x.nc > x.dst.cols))
+      return fail(c, ZTP_ESHAPE, "ztp_migrate: destination slice outside " + shp("dst", x.dst));
+    if (me_src && me_dst && x.src.dtype != x.dst.dtype) return fail(c, ZTP_ESHAPE, "ztp_migrate: dtype mismatch");
+    const int dt = me_src ? x.src.dtype : x.dst.dtype;
+    const size_t es = dt == ZTP_F32 ? 4 : 2;
+    off[i] = total;
+    if ((me_src || me_dst) && x.src_rank != x.dst_rank) total += ((size_t)x.nr * x.nc * es + 255) & ~size_t(255);
+  }
+  if (total && ensure_ws(c, total) != ZTP_OK) return ZTP_ECUDA;
+  char* ws = (char*)c->ws;
+  // local copies and packing of outgoing slices
+  for (int i = 0; i < n; ++i) {
+    const ztp_xfer& x = xs[i];
+    if (x.nr == 0 || x.nc == 0) continue;
+    const size_t es = (x.src_rank == c->rank ? x.src.dtype : x.dst.dtype) == ZTP_F32 ? 4 : 2;
+    if (x.src_rank == c->rank && x.dst_rank == c->rank) {
+      CUDA_TRY(c, cudaMemcpy2DAsync((char*)x.dst.ptr + (x.dr0 * x.dst.ld + x.dc0) * es, x.dst.ld * es,
+                                    (const char*)x.src.ptr + (x.r0 * x.src.ld + x.c0) * es, x.src.ld * es, x.nc * es,
+                                    x.nr, cudaMemcpyDeviceToDevice, st));
+    } else if (x.src_rank == c->rank) {
+      CUDA_TRY(c, cudaMemcpy2DAsync(ws + off[i], x.nc * es, (const char*)x.src.ptr + (x.r0 * x.src.ld + x.c0) * es,
+                                    x.src.ld * es, x.nc * es, x.nr, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  if (c->world > 1) {
+    NCCL_TRY(c, ncclGroupStart());
+    for (int i = 0; i < n; ++i) {
+      const ztp_xfer& x = xs[i];
+      if (x.nr == 0 || x.nc == 0 || x.src_rank == x.dst_rank) continue;
+      const int dt = x.src_rank == c->rank ? x.src.dtype : x.dst.dtype;
+      const size_t cnt = (size_t)x.nr * x.nc;
+      if (x.src_rank == c->rank) NCCL_TRY(c, ncclSend(ws + off[i], cnt, nccl_type(dt), x.dst_rank, c->comm, st));
+      if (x.dst_rank == c->rank) NCCL_TRY(c, ncclRecv(ws + off[i], cnt, nccl_type(dt), x.src_rank, c->comm, st));
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+  }
+  for (int i = 0; i < n; ++i) {
+    const ztp_xfer& x = xs[i];
+    if (x.nr == 0 || x.nc == 0 || x.src_rank == x.dst_rank || x.dst_rank != c->rank) continue;
+    const size_t es = x.dst.dtype == ZTP_F32 ? 4 : 2;
+    CUDA_TRY(c, cudaMemcpy2DAsync((char*)x.dst.ptr + (x.dr0 * x.dst.ld + x.dc0) * es, x.dst.ld * es, ws + off[i],
+                                  x.nc * es, x.nc * es, x.nr, cudaMemcpyDeviceToDevice, st));
+  }
+  return ZTP_OK;
+}
+
+ztp_status ztp_set_slowdown(ztp_ctx* c, double chi) {
+  if (!c || !(chi >= 1.0)) return fail(c, ZTP_EINVAL, "ztp_set_slowdown: chi must be >= 1");
+  c->chi = chi;
+  return ZTP_OK;
+}
+
+ztp_status ztp_set_stats(ztp_ctx* c, int on) {
+  if (!c) return fail(c, ZTP_EINVAL, "ztp_set_stats: null ctx");
+  c->stats = on ? 1 : 0;
+  return ZTP_OK;
+}
+
+ztp_status ztp_read_gemm_ns(ztp_ctx* c, void* stream, double* ns) {
+  if (!c || !ns) return fail(c, ZTP_EINVAL, "ztp_read_gemm_ns: null argument");
+  CUDA_TRY(c, cudaStreamSynchronize((cudaStream_t)stream));
+  unsigned long long v = 0;
+  CUDA_TRY(c, cudaMemcpy(&v, c->d_gemm_ns, 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemset(c->d_gemm_ns, 0, 8));
+  *ns = (double)v;
+  return ZTP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ztp {
+
+enum { KIND_FWD = 0, KIND_DX = 1, KIND_DW = 2 };
+enum { EPI_NONE = 0, EPI_GELU = 1, EPI_GELU_GRAD = 2 };
+
+struct GemmParams {
+  int M, N;            // output rows (M) and columns (N)
+  int kdim;            // contraction length (FWD: n_kept; DX: n_out; DW: tokens)
+  int n_kept;          // FWD: contraction rows; DX/DW: computed output rows (rest imputed)
+  const int32_t* kept;    // FWD: contraction row list; DX/DW: row map of m < n_kept
+  const int32_t* pruned;  // DX/DW: row map of m >= n_kept (Zero-imputed rows)
+  int oob_row;         // a row index outside the gathered tensor (TMA zero fill)
+  int epi;             // EPI_*
+  __nv_bfloat16* out;
+  int64_t ld_out;
+  __nv_bfloat16* out2;  // EPI_GELU: GeLU(pre) (out holds pre)
+  int64_t ld_out2;
+  const __nv_bfloat16* aux;  // EPI_GELU_GRAD: pre-activation rows at the output row map
+  int64_t ld_aux;
+  unsigned long long* stamp;  // [start_min, end_max] %globaltimer of this launch (nullable)
+};
+
+struct GemmOperands {
+  const void* x;   // X^T [K, N]
+  int64_t ld_x;
+  const void* w;   // W^T [K, n]
+  int64_t ld_w;
+  const void* g;   // G^T [n, N]
+  int64_t ld_g;
+  int64_t K, N, n_cols;  // n_cols = n_out
+};
+
+cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_sms, cudaStream_t st);
+
+// fp32 verification GEMM (SIMT FFMA), same lineage semantics, fp32 tensors.
+struct GemmParamsF32 {
+  int kind, M, N, kdim, n_kept;
+  const int32_t* kept;
+  const int32_t* pruned;
+  const float* x;
+  int64_t ld_x;
+  const float* w;
+  int64_t ld_w;
+  const float* g;
+  int64_t ld_g;
+  float* out;
+  int64_t ld_out;
+  float* out2;
+  int64_t ld_out2;
+  const float* aux;
+  int64_t ld_aux;
+  int epi;
+};
+cudaError_t gemm_f32_launch(const GemmParamsF32& p, cudaStream_t st);
+
+// Priority select (ztp_select.cu).
+struct SelectSeg {
+  int32_t len, n_prune, append;
+  int32_t score_off, kept_off, pruned_off;
+};
+constexpr int SELECT_MAX_SEGS = 64;
+struct SelectParams {
+  int nseg;
+  SelectSeg seg[SELECT_MAX_SEGS];
+};
+cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned,
+                          int32_t* err_flag, cudaStream_t st);
+
+// Straggler emulation (ztp_misc.cu).
+cudaError_t delay_launch(unsigned long long* stamp, double chi, unsigned long long* acc_ns, cudaStream_t st);
+cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st);
+cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int64_t feat,
+                        int64_t n_feat, int64_t N, int dtype, cudaStream_t st);
+cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
+                             cudaStream_t st);
+
+}  // namespace ztp

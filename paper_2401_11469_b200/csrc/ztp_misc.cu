@@ -1,0 +1,212 @@
+// Small kernels of the path: straggler emulation (delay after each GEMM),
+// the stand-in attention core (A-31), row fills, and the fp32 verification
+// GEMM (SIMT FFMA with the same lineage semantics as the tcgen05 kernel).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ztp_internal.h"
+#include "ztp_ptx.cuh"
+
+namespace ztp {
+
+// ------------------------------------------------------------ emulation
+// The GEMM stamped [start_min, end_max] of its CTAs; spin until
+// start + chi (end - start) so the rank's GEMM takes chi times longer (A-32),
+// accumulate the (stretched) GEMM time into acc_ns (M_i, A-6), reset stamps.
+__global__ void ztp_delay_kernel(unsigned long long* stamp, double chi, unsigned long long* acc_ns) {
+  const unsigned long long s = stamp[0], e = stamp[1];
+  if (s != ~0ull && e >= s) {
+    const unsigned long long dur = e - s;
+    const unsigned long long target = s + (unsigned long long)(chi * (double)dur);
+    unsigned long long now = globaltimer();
+    while (now < target) {
+      __nanosleep(256);
+      now = globaltimer();
+    }
+    if (acc_ns) atomicAdd(acc_ns, now - s);
+  }
+  stamp[0] = ~0ull;
+  stamp[1] = 0ull;
+}
+
+__global__ void ztp_stamp_reset_kernel(unsigned long long* stamp) {
+  stamp[0] = ~0ull;
+  stamp[1] = 0ull;
+}
+
+cudaError_t delay_launch(unsigned long long* stamp, double chi, unsigned long long* acc_ns, cudaStream_t st) {
+  ztp_delay_kernel<<<1, 1, 0, st>>>(stamp, chi, acc_ns);
+  return cudaGetLastError();
+}
+cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st) {
+  ztp_stamp_reset_kernel<<<1, 1, 0, st>>>(stamp);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------ stand-in core (A-31)
+// FWD ctx[f,t] = q[f,t] + k[f,t] + v[f,t]; BWD q = k = v = dctx.  16-byte vectors.
+__global__ void ztp_core_bf16(int phase, const __nv_bfloat16* __restrict__ qkv_c, __nv_bfloat16* qkv, int64_t ld_qkv,
+                              __nv_bfloat16* ctx, int64_t ld_ctx, int64_t feat, int64_t n_feat, int64_t N) {
+  const int64_t vec_per_row = N / 8;
+  const int64_t total = n_feat * vec_per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = i / vec_per_row, c = (i % vec_per_row) * 8;
+    if (phase == 0) {
+      const uint4 a = *reinterpret_cast<const uint4*>(qkv_c + f * ld_qkv + c);
+      const uint4 b = *reinterpret_cast<const uint4*>(qkv_c + (feat + f) * ld_qkv + c);
+      const uint4 d = *reinterpret_cast<const uint4*>(qkv_c + (2 * feat + f) * ld_qkv + c);
+      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+      const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
+      uint4 o;
+      __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 x = __bfloat1622float2(pa[j]), y = __bfloat1622float2(pb[j]), z = __bfloat1622float2(pd[j]);
+        po[j] = __floats2bfloat162_rn((x.x + y.x) + z.x, (x.y + y.y) + z.y);
+      }
+      *reinterpret_cast<uint4*>(ctx + f * ld_ctx + c) = o;
+    } else {
+      const uint4 g = *reinterpret_cast<const uint4*>(ctx + f * ld_ctx + c);
+      *reinterpret_cast<uint4*>(qkv + f * ld_qkv + c) = g;
+      *reinterpret_cast<uint4*>(qkv + (feat + f) * ld_qkv + c) = g;
+      *reinterpret_cast<uint4*>(qkv + (2 * feat + f) * ld_qkv + c) = g;
+    }
+  }
+}
+
+__global__ void ztp_core_f32(int phase, float* qkv, int64_t ld_qkv, float* ctx, int64_t ld_ctx, int64_t feat,
+                             int64_t n_feat, int64_t N) {
+  const int64_t total = n_feat * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = i / N, c = i % N;
+    if (phase == 0)
+      ctx[f * ld_ctx + c] = (qkv[f * ld_qkv + c] + qkv[(feat + f) * ld_qkv + c]) + qkv[(2 * feat + f) * ld_qkv + c];
+    else {
+      const float g = ctx[f * ld_ctx + c];
+      qkv[f * ld_qkv + c] = g;
+      qkv[(feat + f) * ld_qkv + c] = g;
+      qkv[(2 * feat + f) * ld_qkv + c] = g;
+    }
+  }
+}
+
+cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int64_t feat,
+                        int64_t n_feat, int64_t N, int dtype, cudaStream_t st) {
+  const int threads = 256;
+  const int blocks = 148 * 8;
+  if (dtype == 0)
+    ztp_core_bf16<<<blocks, threads, 0, st>>>(phase, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)qkv, ld_qkv,
+                                              (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N);
+  else
+    ztp_core_f32<<<blocks, threads, 0, st>>>(phase, (float*)qkv, ld_qkv, (float*)ctx, ld_ctx, feat, n_feat, N);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- row fill (Zero)
+__global__ void ztp_fill_rows(uint8_t* out, int64_t ld_bytes, const int32_t* rows, int nrows, int64_t row_bytes) {
+  const int64_t per = row_bytes / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)nrows * per;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per, c = i % per;
+    reinterpret_cast<uint32_t*>(out + (int64_t)rows[r] * ld_bytes)[c] = 0u;
+  }
+}
+
+cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
+                             cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  const int64_t es = dtype == 0 ? 2 : 4;
+  ztp_fill_rows<<<148 * 4, 256, 0, st>>>((uint8_t*)out, ld * es, rows, nrows, cols * es);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------- fp32 verification GEMM (SIMT FFMA)
+__device__ __forceinline__ float gelu_f32(float x) {
+  const float c = 0.7978845608028654f;
+  return 0.5f * x * (1.0f + tanhf(c * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_f32(float x) {
+  const float c = 0.7978845608028654f;
+  const float t = tanhf(c * (x + 0.044715f * x * x * x));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * 0.044715f * x * x);
+}
+
+// 64x64 output tile, 256 threads, 4x4 register micro-tile, k in blocks of 16.
+__global__ void __launch_bounds__(256) ztp_gemm_f32_kernel(const GemmParamsF32 p) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  const bool zero_tile = (p.kind != KIND_FWD) && (m0 >= p.n_kept);
+  if (!zero_tile) {
+    for (int k0 = 0; k0 < p.kdim; k0 += 16) {
+      for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+        const int kk = i / 64, mm = i % 64;
+        const int k = k0 + kk, m = m0 + mm, n = n0 + mm;
+        float a = 0.f, b = 0.f;
+        if (k < p.kdim) {
+          if (p.kind == KIND_FWD) {
+            const int64_t kr = p.kept[k];
+            if (m < p.M) a = p.w[kr * p.ld_w + m];
+            if (n < p.N) b = p.x[kr * p.ld_x + n];
+          } else if (p.kind == KIND_DX) {
+            if (m < p.n_kept) a = p.w[(int64_t)p.kept[m] * p.ld_w + k];
+            if (n < p.N) b = p.g[(int64_t)k * p.ld_g + n];
+          } else {
+            if (m < p.n_kept) a = p.x[(int64_t)p.kept[m] * p.ld_x + k];
+            if (n < p.N) b = p.g[(int64_t)n * p.ld_g + k];
+          }
+        }
+        As[kk][mm] = a;
+        Bs[kk][mm] = b;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        float av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          av[i] = As[kk][ty * 4 + i];
+          bv[i] = Bs[kk][tx * 4 + i];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= p.M) continue;
+    int64_t orow = m;
+    if (p.kind != KIND_FWD) orow = (m < p.n_kept) ? p.kept[m] : p.pruned[m - p.n_kept];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= p.N) continue;
+      float v = acc[i][j];
+      if (p.epi == EPI_GELU) {
+        p.out[orow * p.ld_out + n] = v;
+        p.out2[orow * p.ld_out2 + n] = gelu_f32(v);
+      } else {
+        if (p.epi == EPI_GELU_GRAD) v = v * gelu_grad_f32(p.aux[orow * p.ld_aux + n]);
+        p.out[orow * p.ld_out + n] = v;
+      }
+    }
+  }
+}
+
+cudaError_t gemm_f32_launch(const GemmParamsF32& p, cudaStream_t st) {
+  dim3 grid((p.N + 63) / 64, (p.M + 63) / 64);
+  ztp_gemm_f32_kernel<<<grid, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ztp

@@ -1,0 +1,251 @@
+// a2. Plan (ztp_plan / ztp_plan_counts): Eq.1, straggler detection
+// (Alg.2 l.2-5), Eq.2 by bisection, Eq.3 scan,
+// Alg.2 roles and the virtual renumbering.
+// Compiled with -ffp-contract=off: every double is evaluated in the order
+// DESIGN.md "Plan evaluation order" fixes, so all ranks agree bit-for-bit.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "../../include/ztp.h"
+
+namespace ztp {
+void set_thread_error(const std::string& msg);
+}
+
+namespace {
+
+using ztp::set_thread_error;
+
+bool pwl_ok(const ztp_pwl& f) { return f.n >= 2 && f.x != nullptr && f.y != nullptr; }
+
+// Segment j with x[j] <= v < x[j+1]; the last segment extrapolates.
+double pwl_eval(const ztp_pwl& f, double v) {
+  int j = 0;
+  while (j + 2 < f.n && v >= f.x[j + 1]) ++j;
+  return f.y[j] + (f.y[j + 1] - f.y[j]) * ((v - f.x[j]) / (f.x[j + 1] - f.x[j]));
+}
+
+double eq1(double T, double C, double M, double gmax) {
+  double g = (T - C) / M;
+  if (g < 0.0) g = 0.0;
+  if (g > gmax) g = gmax;
+  return g;
+}
+
+double gfun(const ztp_costs& c, double Lg, double b, int e) {
+  return ((c.omega1 + pwl_eval(c.omega2, Lg * (1.0 - b))) - pwl_eval(c.phi1, Lg * b)) -
+         pwl_eval(c.phi2, (Lg * b) / (double)(e - 1));
+}
+
+double solve_beta(const ztp_costs& c, double Lg, int e, int iters) {
+  if (gfun(c, Lg, 1.0, e) >= 0.0) return 1.0;
+  if (gfun(c, Lg, 0.0, e) <= 0.0) return 0.0;
+  double lo = 0.0, hi = 1.0;
+  for (int i = 0; i < iters; ++i) {
+    const double m = 0.5 * (lo + hi);
+    if (gfun(c, Lg, m, e) > 0.0)
+      lo = m;
+    else
+      hi = m;
+  }
+  return 0.5 * (lo + hi);
+}
+
+}  // namespace
+
+extern "C" void ztp_plan_opts_default(ztp_plan_opts* o) {
+  if (!o) return;
+  o->enable_migration = 0;
+  o->zero_crit = ZTP_CRIT_MIN;
+  o->gamma_max = 0.9;
+  o->eps = 0.02;
+  o->gamma_tol = 0.5;
+  o->bisect_iters = 64;
+  o->force_lambda = -1;
+}
+
+extern "C" ztp_status ztp_plan(int e, const double* T, const double* M, double L_ref, const ztp_costs* costs,
+                               const ztp_plan_opts* opts, ztp_plan_t* out) {
+  if (!out || !T || !M || !opts) {
+    set_thread_error("ztp_plan: null argument");
+    return ZTP_EINVAL;
+  }
+  if (e < 1 || e > ZTP_MAX_RANKS) {
+    set_thread_error("ztp_plan: world=" + std::to_string(e) + " outside 1..8 (S:559)");
+    return ZTP_EINVAL;
+  }
+  for (int r = 0; r < e; ++r)
+    if (!std::isfinite(T[r]) || T[r] < 0.0) {
+      set_thread_error("ztp_plan: T[" + std::to_string(r) + "] not finite / negative");
+      return ZTP_EINVAL;
+    }
+  std::memset(out, 0, sizeof(*out));
+  out->world = e;
+  int order[ZTP_MAX_RANKS];
+  for (int r = 0; r < e; ++r) order[r] = r;
+  std::stable_sort(order, order + e, [&](int a, int b) { return T[a] > T[b] || (T[a] == T[b] && a < b); });
+  for (int r = 0; r < e; ++r) out->order[r] = order[r];
+  double acc = 0.0;
+  for (int r = 0; r < e; ++r) acc = acc + T[r];
+  const double T_avg = acc / (double)e;
+  double T_min = T[0];
+  for (int r = 1; r < e; ++r)
+    if (T[r] < T_min) T_min = T[r];
+  const double thr = T_min * (1.0 + opts->eps);
+  int strag[ZTP_MAX_RANKS];
+  int z = 0;
+  for (int i = 0; i < e; ++i)
+    if (T[order[i]] > thr) strag[z++] = order[i];
+  out->z = z;
+
+  auto need_m = [&](int r) -> bool {
+    if (!(M[r] > 0.0)) {
+      set_thread_error("ztp_plan: M[" + std::to_string(r) + "] = 0, Eq.1 has no baseline (S:360)");
+      return false;
+    }
+    return true;
+  };
+
+  if (!opts->enable_migration) {
+    const double C = opts->zero_crit == ZTP_CRIT_AVG ? T_avg : T_min;
+    for (int r = 0; r < e; ++r) {
+      if (!need_m(r)) return ZTP_ENOBASELINE;
+      const double g = eq1(T[r], C, M[r], opts->gamma_max);
+      out->gamma[r] = g;
+      out->gamma_r[r] = g;
+      out->role[r] = g > 0.0 ? ZTP_RESIZE : ZTP_NORMAL;
+    }
+    return ZTP_OK;
+  }
+  for (int i = 0; i < z; ++i) {
+    const int r = strag[i];
+    if (!need_m(r)) return ZTP_ENOBASELINE;
+    out->gamma[r] = eq1(T[r], T_min, M[r], opts->gamma_max);
+  }
+  if (z == 0) return ZTP_OK;
+  if (!costs || !pwl_ok(costs->omega2) || !pwl_ok(costs->phi1) || !pwl_ok(costs->phi2)) {
+    set_thread_error("ztp_plan: cost functions need >= 2 samples (S:549)");
+    return ZTP_EINVAL;
+  }
+  if (z == 1) {
+    const int s = strag[0];
+    const double g = out->gamma[s];
+    if (g <= opts->gamma_tol) {
+      out->role[s] = g > 0.0 ? ZTP_RESIZE : ZTP_NORMAL;
+      out->gamma_r[s] = g;
+      return ZTP_OK;
+    }
+    double b = solve_beta(*costs, L_ref * g, e, opts->bisect_iters);
+    const double floor_b = 1.0 - opts->gamma_tol / g;
+    if (b < floor_b) b = floor_b;
+    out->beta[s] = b;
+    out->phi[s] = g * b;
+    out->gamma_r[s] = (g * (1.0 - b)) / (1.0 - g * b);
+    out->role[s] = b == 1.0 ? ZTP_MIGRATE : (b == 0.0 ? ZTP_RESIZE : ZTP_SPLIT);
+    out->x = b > 0.0 ? 1 : 0;
+    return ZTP_OK;
+  }
+  int x = z;
+  if (opts->force_lambda >= 0) {
+    x = opts->force_lambda < z ? opts->force_lambda : z;
+  } else {
+    double gam = 0.0;
+    for (int xi = 1; xi <= z; ++xi) {
+      const double Tk = T[order[xi - 1]];
+      gam = gam + L_ref * ((Tk - T_min) / Tk);
+      if (e - xi <= 0) {
+        set_thread_error("ztp_plan: e - x = 0 receivers (S:579)");
+        return ZTP_ERECEIVERS;
+      }
+      double mx = -INFINITY;
+      for (int y = xi + 1; y <= e; ++y) {
+        const double v = (gam / (double)(e - xi)) * (T[order[y - 1]] / L_ref);
+        if (v > mx) mx = v;
+      }
+      const double f = ((Tk - T_min) - pwl_eval(costs->phi1, gam)) - mx;
+      if (f <= 0.0) {
+        x = xi - 1;
+        break;
+      }
+    }
+  }
+  out->x = x;
+  for (int pos = 1; pos <= z; ++pos) {
+    const int r = strag[pos - 1];
+    if (pos <= x) {
+      out->role[r] = ZTP_MIGRATE;
+      out->beta[r] = 1.0;
+      out->phi[r] = out->gamma[r];
+      out->gamma_r[r] = 0.0;
+    } else {
+      out->role[r] = ZTP_RESIZE;
+      out->gamma_r[r] = out->gamma[r];
+    }
+  }
+  return ZTP_OK;
+}
+
+extern "C" ztp_status ztp_plan_counts(const ztp_plan_t* p, int rank, int64_t K, int64_t n_units, int64_t unit,
+                                      int is_row, ztp_counts* out) {
+  if (!p || !out || rank < 0 || rank >= p->world || unit <= 0 || n_units < unit || n_units % unit != 0 || K < 1) {
+    set_thread_error("ztp_plan_counts: bad rank / unit / sizes");
+    return ZTP_EINVAL;
+  }
+  const int e = p->world;
+  const int64_t units = n_units / unit;
+  auto migrating = [&](int r) { return p->role[r] == ZTP_MIGRATE || p->role[r] == ZTP_SPLIT; };
+  auto nmig = [&](int s) -> int64_t {
+    if (!migrating(s)) return 0;
+    int64_t nm = unit * (int64_t)std::floor((double)units * p->phi[s] + 0.5);
+    if (nm > n_units - unit) nm = n_units - unit;
+    return nm;
+  };
+  std::memset(out, 0, sizeof(*out));
+  out->n_mig = (int32_t)nmig(rank);
+  const int64_t K_rem = is_row ? K - out->n_mig : K;
+  int64_t npr = (int64_t)std::floor((double)K_rem * p->gamma_r[rank] + 0.5);
+  if (npr > K_rem - 1) npr = K_rem - 1;
+  if (npr < 0) npr = 0;
+  out->n_prune = (int32_t)npr;
+  int recv[ZTP_MAX_RANKS];
+  int nrecv = 0;
+  for (int r = 0; r < e; ++r)
+    if (!migrating(r)) recv[nrecv++] = r;
+  for (int i = 0; i < e; ++i) {
+    const int s = p->order[i];
+    const int64_t nm = nmig(s);
+    if (nm == 0) continue;
+    if (nrecv == 0) {
+      set_thread_error("ztp_plan_counts: no receivers");
+      return ZTP_ERECEIVERS;
+    }
+    int R[ZTP_MAX_RANKS];
+    for (int j = 0; j < nrecv; ++j) R[j] = recv[j];
+    std::sort(R, R + nrecv, [&](int a, int b) { return (a - s + e) % e < (b - s + e) % e; });
+    const int64_t tot = nm / unit;
+    const int64_t m = tot / nrecv, extra = tot % nrecv;
+    int64_t lo = n_units - nm;
+    for (int j = 0; j < nrecv; ++j) {
+      const int64_t cnt = (m + (j < extra ? 1 : 0)) * unit;
+      if (cnt > 0) {
+        if (rank == s) {
+          out->out_dst[out->n_out] = R[j];
+          out->out_lo[out->n_out] = lo;
+          out->out_hi[out->n_out] = lo + cnt;
+          ++out->n_out;
+        }
+        if (rank == R[j]) {
+          out->in_src[out->n_in] = s;
+          out->in_lo[out->n_in] = lo;
+          out->in_hi[out->n_in] = lo + cnt;
+          ++out->n_in;
+        }
+      }
+      lo += cnt;
+    }
+  }
+  return ZTP_OK;
+}

@@ -1,0 +1,156 @@
+// a3. Priority select ("the one with small variation can be pruned";
+// Alg.1 l.12-14 top-L_pri select + ascendSort; ties by ascending index, A-2).
+//
+// One CTA (1024 threads) per segment (= one rank-local linear).  The fp32
+// score is mapped to an order-preserving 32-bit key (-0 canonicalised to +0),
+// a 4 x 8-bit MSB radix select finds the key v of the n_prune-th smallest
+// score and how many of the ties at v are pruned; one ordered pass then
+// compacts indices into P (pruned) and S (kept) with warp ballot/popc and a
+// block scan, so both lists come out ascending without a sort.  Segment sizes
+// are <= tens of thousands of columns: the kernel is latency-bound, re-reading
+// its scores from L2 on each pass.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ztp_internal.h"
+
+namespace ztp {
+
+__device__ __forceinline__ uint32_t ord32(float x, bool& nan) {
+  uint32_t b = __float_as_uint(x);
+  nan = ((b & 0x7F800000u) == 0x7F800000u) && (b & 0x007FFFFFu);
+  if ((b & 0x7FFFFFFFu) == 0u) b = 0u;  // -0 == +0
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// Block-wide exclusive scan of a 0/1 flag (blockDim = 1024 = 32 warps).
+__device__ __forceinline__ int block_excl_scan(bool flag, int& total, int* warp_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xFFFFFFFFu, flag);
+  const int in_warp = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 0) warp_tot[w] = __popc(bal);
+  __syncthreads();
+  if (w == 0) {
+    int v = warp_tot[lane];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    warp_tot[32 + lane] = incl - v;           // exclusive
+    if (lane == 31) warp_tot[64] = incl;      // total
+  }
+  __syncthreads();
+  const int r = warp_tot[32 + w] + in_warp;
+  total = warp_tot[64];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, const float* __restrict__ scores,
+                                                          int32_t* __restrict__ kept, int32_t* __restrict__ pruned,
+                                                          int32_t* err_flag) {
+  const SelectSeg s = p.seg[blockIdx.x];
+  const float* sc = scores + s.score_off;
+  int32_t* K = kept + s.kept_off;
+  int32_t* P = pruned + s.pruned_off;
+  __shared__ uint32_t hist[256];
+  __shared__ int warp_tot[65];
+  __shared__ uint32_t sel_bin, sel_below;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+
+  uint32_t prefix = 0, mask = 0;
+  int target = s.n_prune - 1;  // 0-based rank (by key) of the last pruned element
+  bool saw_nan = false;
+  if (s.n_prune > 0) {
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < s.len; i += blockDim.x) {
+        bool nan;
+        const uint32_t key = ord32(sc[i], nan);
+        saw_nan |= nan;
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (tid < 32) {
+        // lane l owns bins 8l..8l+7
+        uint32_t loc[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          loc[j] = hist[8 * lane + j];
+          sum += loc[j];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t excl = incl - sum;
+        if ((uint32_t)target >= excl && (uint32_t)target < incl) {
+          uint32_t c = excl;
+          for (int j = 0; j < 8; ++j) {
+            if ((uint32_t)target < c + loc[j]) {
+              sel_bin = 8 * lane + j;
+              sel_below = c;
+              break;
+            }
+            c += loc[j];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= sel_bin << shift;
+      mask |= 0xFFu << shift;
+      target -= (int)sel_below;
+      __syncthreads();
+    }
+  } else {
+    for (int i = tid; i < s.len; i += blockDim.x) {
+      bool nan;
+      (void)ord32(sc[i], nan);
+      saw_nan |= nan;
+    }
+  }
+  if (saw_nan) atomicOr(err_flag, 1);
+  const uint32_t v = prefix;          // key of the n_prune-th smallest
+  const int t_need = target + 1;      // ties at v that are pruned (ascending index)
+
+  int carry_tie = 0, carry_p = 0;
+  for (int base = 0; base < s.len; base += blockDim.x) {
+    const int i = base + tid;
+    const bool valid = i < s.len;
+    bool nan;
+    const uint32_t key = valid ? ord32(sc[i], nan) : 0u;
+    const bool less = valid && s.n_prune > 0 && key < v;
+    const bool tie = valid && s.n_prune > 0 && key == v;
+    int tot_tie, tot_p;
+    const int tie_rank = carry_tie + block_excl_scan(tie, tot_tie, warp_tot);
+    const bool isp = less || (tie && tie_rank < t_need);
+    const int p_rank = carry_p + block_excl_scan(isp, tot_p, warp_tot);
+    if (valid) {
+      if (isp)
+        P[p_rank] = i;
+      else
+        K[i - p_rank] = i;
+    }
+    carry_tie += tot_tie;
+    carry_p += tot_p;
+  }
+  const int nk = s.len - s.n_prune;
+  for (int a = tid; a < s.append; a += blockDim.x) K[nk + a] = s.len + a;
+  (void)lane;
+}
+
+cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned,
+                          int32_t* err_flag, cudaStream_t st) {
+  ztp_select_kernel<<<p.nseg, 1024, 0, st>>>(p, scores, kept, pruned, err_flag);
+  return cudaGetLastError();
+}
+
+}  // namespace ztp

@@ -1,0 +1,160 @@
+"""CPU tests of the C ABI: the library loads, exports every symbol include/ztp.h
+declares, and its host planner (ztp_plan / ztp_plan_counts) matches the oracle
+bit-exactly (plans and counts are bit-exact)."""
+import ctypes as C
+import os
+import random
+import re
+import struct
+
+import pytest
+
+from conftest import ROOT
+from oracle import ztp_oracle as O
+
+
+@pytest.fixture(scope="module")
+def Z():
+    import paper_2401_11469_b200 as z
+    return z
+
+
+def test_header_symbols_exported(Z):
+    hdr = open(os.path.join(ROOT, "include", "ztp.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    declared = set(re.findall(r"\b(ztp_[a-z0-9_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    from paper_2401_11469_b200 import _lib
+    for name in sorted(declared):
+        assert hasattr(_lib.lib, name), f"{name} declared in ztp.h but not exported"
+    assert set(_lib.EXPORTED) == declared
+
+
+def test_status_strings_and_version(Z):
+    from paper_2401_11469_b200 import _lib
+    for i, nm in enumerate(_lib.STATUS):
+        assert _lib.lib.ztp_status_str(i).decode() == nm
+    assert "sm_100a" in Z.ztp_version()
+
+
+def _bits(x):
+    return struct.pack("<d", x)
+
+
+def _costs_pair(Z, rng):
+    def mono():
+        xs = sorted({0.0} | {round(rng.uniform(1, 300), 3) for _ in range(rng.randint(1, 4))})
+        ys = [0.0]
+        for _ in xs[1:]:
+            ys.append(ys[-1] + rng.uniform(0, 5))
+        return (tuple(xs), tuple(ys))
+    om1 = rng.uniform(0, 2)
+    o2, p1, p2 = mono(), mono(), mono()
+    return Z.make_costs(om1, o2, p1, p2), O.Costs(om1, o2, p1, p2)
+
+
+def _compare(Z, T, M, L, costs_pair, kw):
+    zc, oc = costs_pair
+    oopts = O.PlanOpts(**kw)
+    try:
+        op = O.plan(T, M, L, oc, oopts)
+        oerr = None
+    except O.OracleError as e:
+        oerr = e.code
+    try:
+        zp = Z.ztp_plan(T, M, L, zc, Z.plan_opts(**kw))
+        zerr = None
+    except Z.ZtpError as e:
+        zerr = e.name
+    assert oerr == zerr
+    if oerr:
+        return None
+    e = len(T)
+    assert zp.world == e and zp.z == op.z and zp.x == op.x
+    assert list(zp.order)[:e] == op.order
+    assert list(zp.role)[:e] == op.role
+    for f in ("gamma", "beta", "phi", "gamma_r"):
+        for r in range(e):
+            assert _bits(getattr(zp, f)[r]) == _bits(getattr(op, f)[r]), (f, r)
+    return zp, op
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_plan_bitexact_vs_oracle_randomized(Z, seed):
+    """>= 1000 randomized instances in total (10 seeds x 120) across ZERO-AVG,
+    ZERO-MIN and SEMI, with ties, clamps and forced lambda."""
+    rng = random.Random(seed)
+    for _ in range(120):
+        e = rng.randint(1, 8)
+        base = rng.uniform(1, 100)
+        T, M = [], []
+        for r in range(e):
+            chi = rng.choice([1.0, 1.0, rng.uniform(1, 9)])
+            m = rng.uniform(0.2, 0.9) * base
+            T.append(base - m + chi * m if rng.random() < 0.9 else base)
+            M.append(chi * m)
+        if rng.random() < 0.05:
+            M[rng.randrange(e)] = 0.0
+        kw = dict(enable_migration=rng.randint(0, 1), zero_crit=rng.randint(0, 1),
+                  gamma_max=rng.choice([0.9, 1.0, 0.5]), eps=rng.choice([0.0, 0.02]),
+                  gamma_tol=rng.choice([0.5, 0.3]), bisect_iters=rng.choice([64, 20]),
+                  force_lambda=rng.choice([-1, -1, -1, 0, 1, 3]))
+        res = _compare(Z, T, M, rng.choice([64.0, 100.0, 4096.0]), _costs_pair(Z, rng), kw)
+        if res is None:
+            continue
+        zp, op = res
+        # counts for every rank and both layer kinds
+        for r in range(e):
+            for K, n_units, unit, is_row in ((1024, 512, 1, False), (512, 512, 1, True), (777, 128, 4, True)):
+                try:
+                    oc = O.plan_counts(op, r, K, n_units, unit, is_row)
+                    oerr = None
+                except O.OracleError as ex:
+                    oerr = ex.code
+                try:
+                    zc = Z.ztp_plan_counts(zp, r, K, n_units, unit, is_row)
+                    zerr = None
+                except Z.ZtpError as ex:
+                    zerr = ex.name
+                assert oerr == zerr
+                if oerr:
+                    continue
+                assert (zc.n_prune, zc.n_mig) == (oc.n_prune, oc.n_mig)
+                assert [(zc.out_dst[i], zc.out_lo[i], zc.out_hi[i]) for i in range(zc.n_out)] == oc.out
+                assert [(zc.in_src[i], zc.in_lo[i], zc.in_hi[i]) for i in range(zc.n_in)] == oc.inc
+
+
+def test_plan_worked_examples_match(Z):
+    zero = ((0.0, 1.0), (0.0, 0.0))
+    lin = ((0.0, 1.0), (0.0, 1.0))
+    pair = (Z.make_costs(0.0, lin, lin, lin), O.Costs(0.0, lin, lin, lin))
+    _compare(Z, [10.0, 20.0], [16.0, 16.0], 100.0, pair, dict(zero_crit=O.CRIT_AVG))
+    _compare(Z, [20.0, 36.0], [16.0, 32.0], 64.0, pair, dict(zero_crit=O.CRIT_AVG))
+    p01 = ((0.0, 1.0), (0.0, 0.1))
+    _compare(Z, [40.0, 30.0, 10.0, 10.0], [5.0] * 4, 100.0,
+             (Z.make_costs(0.0, zero, p01, zero), O.Costs(0.0, zero, p01, zero)),
+             dict(enable_migration=1, gamma_max=1.0))
+    zp = Z.ztp_plan([20.0, 36.0], [16.0, 32.0], 64.0, opts=Z.plan_opts(zero_crit=Z.CRIT_AVG))
+    assert zp.gamma[1] == 0.25
+    assert Z.ztp_plan_counts(zp, 1, 64, 128, 1, False).n_prune == 16
+
+
+def test_plan_errors(Z):
+    with pytest.raises(Z.ZtpError) as ei:
+        Z.ztp_plan([], [], 1.0)
+    assert ei.value.name == "ZTP_EINVAL"
+    with pytest.raises(Z.ZtpError) as ei:
+        Z.ztp_plan([1.0, 2.0], [1.0, 0.0], 1.0)
+    assert ei.value.name == "ZTP_ENOBASELINE"
+    with pytest.raises(Z.ZtpError) as ei:
+        Z.ztp_plan([1.0, float("nan")], [1.0, 1.0], 1.0)
+    assert ei.value.name == "ZTP_EINVAL"
+
+
+def test_no_cuda_device_is_an_error_not_a_fallback(Z):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(Z.ZtpError) as ei:
+        Z.ztp_ctx_create()
+    assert ei.value.name in ("ZTP_ECUDA", "ZTP_EUNSUPPORTED")

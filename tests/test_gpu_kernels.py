@@ -1,0 +1,220 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle on
+identical seeded inputs: select (bit-exact), resized GEMMs fwd/dX/dW with
+ragged tiles and the Zero imputation (bf16: 2e-2 ||ref||_inf; imputed rows
+exactly +0.0), fused GeLU / GeLU' epilogues, fp32 verification mode (1e-5)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ztp_oracle as O
+from synth import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+TOL_F32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import paper_2401_11469_b200 as Z
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    ctx = Z.ztp_ctx_create(0, 1, None, 0)
+    yield Z, torch, ctx
+    Z.ztp_ctx_destroy(ctx)
+
+
+def dev(torch, a, dtype=None):
+    dtype = dtype or torch.bfloat16
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to("cuda").to(dtype)
+
+
+def host(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def err_ok(got, ref, tol):
+    scale = max(np.max(np.abs(ref)), 1e-30)
+    return np.max(np.abs(got - ref)) <= tol * scale, np.max(np.abs(got - ref)) / scale
+
+
+# ----------------------------------------------------------------- select
+
+@pytest.mark.parametrize("seed", range(8))
+def test_select_bitexact_random_segments(env, seed):
+    Z, torch, ctx = env
+    rng = np.random.default_rng(seed)
+    nseg = int(rng.integers(1, 70))            # > 64 exercises the chunked launch
+    lens = [int(rng.choice([1, 2, 7, 64, 333, 1024, 1376, 5000, 20480])) for _ in range(nseg)]
+    nps = [int(rng.integers(0, L)) if L > 1 else 0 for L in lens]
+    app = [int(rng.integers(0, 5)) for _ in range(nseg)]
+    parts = []
+    for i, L in enumerate(lens):
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            s = I.lognormal_scores(seed, f"s{i}", L)
+        elif kind == 1:
+            s = I.lognormal_scores(seed, f"s{i}", L, levels=16)       # tie stress (c3 variant)
+        else:
+            s = rng.standard_normal(L).astype(np.float32)
+            s[rng.integers(0, L, size=max(1, L // 10))] = -0.0
+        parts.append(s)
+    scores = dev(torch, np.concatenate(parts), torch.float32)
+    kept = torch.empty(sum(L - p + a for L, p, a in zip(lens, nps, app)), dtype=torch.int32, device="cuda")
+    pruned = torch.empty(max(1, sum(nps)), dtype=torch.int32, device="cuda")
+    Z.ztp_select(ctx, lens, nps, scores, kept, pruned, app)
+    Z.ztp_sync(ctx)
+    kh, ph = kept.cpu().numpy(), pruned.cpu().numpy()
+    ko = po = 0
+    for i, L in enumerate(lens):
+        S, P = O.select(parts[i], nps[i])
+        nk = L - nps[i]
+        assert np.array_equal(kh[ko:ko + nk], S), f"segment {i} kept"
+        assert np.array_equal(kh[ko + nk:ko + nk + app[i]], np.arange(L, L + app[i])), f"segment {i} appended"
+        assert np.array_equal(ph[po:po + nps[i]], P), f"segment {i} pruned"
+        ko += nk + app[i]
+        po += nps[i]
+
+
+def test_select_nan_flag(env):
+    Z, torch, ctx = env
+    s = dev(torch, np.array([1.0, np.nan, 2.0], dtype=np.float32), torch.float32)
+    kept = torch.empty(3, dtype=torch.int32, device="cuda")
+    pruned = torch.empty(3, dtype=torch.int32, device="cuda")
+    Z.ztp_select(ctx, [3], [1], s, kept, pruned)
+    with pytest.raises(Z.ZtpError) as ei:
+        Z.ztp_sync(ctx)
+    assert ei.value.name == "ZTP_EINVAL"
+    Z.ztp_sync(ctx)  # flag cleared
+
+
+def test_select_host_errors(env):
+    Z, torch, ctx = env
+    s = torch.zeros(4, device="cuda")
+    k = torch.empty(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(Z.ZtpError):
+        Z.ztp_select(ctx, [4], [4], s, k, k)     # nothing would survive
+
+
+# ------------------------------------------------------------ resized GEMMs
+
+def _case(K, n, N, gamma, seed):
+    Xt = I.normal(seed, "x", K, N)
+    Wt = I.uniform_sym(seed, "w", K, n, 1.0 / math.sqrt(K))
+    Gt = I.normal(seed, "g", n, N)
+    npr = int(math.floor(K * gamma + 0.5))
+    npr = min(npr, K - 1)
+    S, P = O.select(I.lognormal_scores(seed, "sc", K), npr)
+    return Xt, Wt, Gt, S, P
+
+
+def _sel_dev(Z, torch, S, P, lid=0, mid=0):
+    kept = torch.tensor(np.asarray(S, dtype=np.int32), device="cuda")
+    pruned = torch.tensor(np.asarray(P if len(P) else [0], dtype=np.int32), device="cuda")
+    return Z.sel(kept, len(S), pruned, len(P), lid, mid), (kept, pruned)
+
+
+SHAPES = [  # (K, n, N, gamma): ragged K' tails, partial M/N tiles, several tiles
+    (200, 300, 328, 0.35),
+    (64, 128, 256, 0.0),
+    (1024, 512, 776, 0.5),
+    (96, 40, 24, 0.9),
+    (517, 264, 1032, 0.25),
+]
+
+
+@pytest.mark.parametrize("K,n,N,gamma", SHAPES)
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_gemm_fwd_dx_dw_parity(env, K, n, N, gamma, dtype):
+    Z, torch, ctx = env
+    Xt, Wt, Gt, S, P = _case(K, n, N, gamma, seed=K + n + N)
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    tol = TOL_BF16 if dtype == "bf16" else TOL_F32
+    x, w, g = dev(torch, Xt, td), dev(torch, Wt, td), dev(torch, Gt, td)
+    y = torch.full((n, N), float("nan"), device="cuda", dtype=td)
+    dx = torch.full((K, N), float("nan"), device="cuda", dtype=td)
+    dw = torch.full((K, n), float("nan"), device="cuda", dtype=td)
+    s, keep = _sel_dev(Z, torch, S, P)
+    a = Z.linear_args(x_t=x, w_t=w, y_t=y, g_t=g, dx_t=dx, dw_t=dw, sel_=s)
+    Z.ztp_gemm(ctx, Z.KIND_FWD, a)
+    Z.ztp_gemm(ctx, Z.KIND_DX, a)
+    Z.ztp_gemm(ctx, Z.KIND_DW, a)
+    Z.ztp_sync(ctx)
+    ref_y = O.linear_fwd(Wt, Xt, S)
+    ref_dx = O.linear_bwd_dx(Wt, Gt, S, P)
+    ref_dw = O.linear_bwd_dw(Xt, Gt, S, P)
+    for name, got, ref in (("y", y, ref_y), ("dx", dx, ref_dx), ("dw", dw, ref_dw)):
+        gh = host(got)
+        assert np.isfinite(gh).all(), f"{name}: unwritten (NaN) elements"
+        ok, e = err_ok(gh, ref, tol)
+        assert ok, f"{name}: max|err|/||ref|| = {e:.3e}"
+    # Zero imputation: rows P exactly +0.0 (bit pattern)
+    if len(P):
+        for t in (dx, dw):
+            rows = t[torch.tensor(P, device="cuda")]
+            assert torch.all(rows == 0) and not torch.any(torch.signbit(rows))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_gemm_gelu_epilogues(env, dtype):
+    Z, torch, ctx = env
+    K, n, N = 384, 272, 520
+    Xt, Wt, Gt, S, P = _case(K, n, N, 0.4, seed=7)
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    tol = TOL_BF16 if dtype == "bf16" else TOL_F32
+    x, w = dev(torch, Xt, td), dev(torch, Wt, td)
+    pre = torch.empty((n, N), device="cuda", dtype=td)
+    h = torch.empty((n, N), device="cuda", dtype=td)
+    s, keep = _sel_dev(Z, torch, S, P)
+    Z.ztp_gemm(ctx, Z.KIND_FWD, Z.linear_args(x_t=x, w_t=w, y_t=h, pre_t=pre, sel_=s, act=Z.ACT_GELU))
+    # GeLU' epilogue on a row-layer dX: dH = W2^T G, G1 = dH * GeLU'(pre_in)
+    K2, n2 = 272, 200
+    W2 = I.uniform_sym(8, "w2", K2, n2, 1 / math.sqrt(K2))
+    G2 = I.normal(8, "g2", n2, N)
+    PreIn = I.normal(8, "pin", K2, N)
+    S2, P2 = O.select(I.lognormal_scores(8, "s2", K2), 100)
+    s2, keep2 = _sel_dev(Z, torch, S2, P2)
+    g1 = torch.empty((K2, N), device="cuda", dtype=td)
+    Z.ztp_gemm(ctx, Z.KIND_DX, Z.linear_args(w_t=dev(torch, W2, td), g_t=dev(torch, G2, td), dx_t=g1,
+                                             pre_in_t=dev(torch, PreIn, td), sel_=s2, act_in=Z.ACT_GELU))
+    Z.ztp_sync(ctx)
+    ref_pre = O.linear_fwd(Wt, Xt, S)
+    ok, e = err_ok(host(pre), ref_pre, tol)
+    assert ok, e
+    ok, e = err_ok(host(h), O.gelu_tanh(ref_pre), tol)
+    assert ok, e
+    ref_g1 = O.linear_bwd_dx(W2, G2, S2, P2) * O.gelu_tanh_grad(PreIn)
+    ok, e = err_ok(host(g1), ref_g1, tol)
+    assert ok, e
+
+
+def test_gemm_large_c2_shapes_sampled(env):
+    """c2 e=1 FC1 shapes (K=1024, n=4096, N=8192) in the bench launch config,
+    checked on sampled output rows/columns computed one by one in fp64."""
+    Z, torch, ctx = env
+    K, n, N = 1024, 4096, 8192
+    Xt, Wt, Gt, S, P = _case(K, n, N, 0.5, seed=11)
+    x, w, g = dev(torch, Xt), dev(torch, Wt), dev(torch, Gt)
+    y = torch.empty((n, N), device="cuda", dtype=torch.bfloat16)
+    dx = torch.empty((K, N), device="cuda", dtype=torch.bfloat16)
+    dw = torch.empty((K, n), device="cuda", dtype=torch.bfloat16)
+    s, keep = _sel_dev(Z, torch, S, P)
+    a = Z.linear_args(x_t=x, w_t=w, y_t=y, g_t=g, dx_t=dx, dw_t=dw, sel_=s)
+    for kind in (Z.KIND_FWD, Z.KIND_DX, Z.KIND_DW):
+        Z.ztp_gemm(ctx, kind, a)
+    Z.ztp_sync(ctx)
+    rng = np.random.default_rng(0)
+    rows_n = rng.integers(0, n, 24)
+    cols_N = rng.integers(0, N, 24)
+    yh, dxh, dwh = host(y), host(dx), host(dw)
+    ref = Wt[S][:, rows_n].T @ Xt[S][:, cols_N]
+    ok, e = err_ok(yh[np.ix_(rows_n, cols_N)], ref, TOL_BF16)
+    assert ok, e
+    rk = rng.choice(S, 24)
+    ok, e = err_ok(dxh[np.ix_(rk, cols_N)], Wt[rk] @ Gt[:, cols_N], TOL_BF16)
+    assert ok, e
+    ok, e = err_ok(dwh[np.ix_(rk, rows_n)], Xt[rk] @ Gt[rows_n].T, TOL_BF16)
+    assert ok, e
+    assert np.all(dxh[P] == 0) and np.all(dwh[P] == 0)
