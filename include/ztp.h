@@ -198,6 +198,9 @@ ztp_status ztp_allgather_stats(ztp_ctx* ctx, double T_own, double M_own,
  *            the kept indices S followed by h_append[i] appended indices
  *            len_i, len_i+1, ... (migrated-in units on a helper, A-26);
  *   d_pruned segment i at offset sum_{j<i} n_prune_j: the pruned indices P.
+ *   d_pos    (optional) segment i at offset sum_{j<i} (len_j + append_j):
+ *            the inverse map -- pos[k] = position of column k in the kept
+ *            list, -1 if pruned (used as the producer-side row map y_pos).
  * h_append may be NULL (no appends).  One CTA per segment: radix select over
  * the order-preserving 32-bit key of the score, ballot/popc compaction.
  * Errors: EINVAL (nseg < 1, len < 1, n_prune outside [0, len-1]); a NaN score
@@ -205,7 +208,7 @@ ztp_status ztp_allgather_stats(ztp_ctx* ctx, double T_own, double M_own,
  * ------------------------------------------------------------------------- */
 ztp_status ztp_select(ztp_ctx* ctx, int nseg, const int32_t* h_seg_len, const int32_t* h_n_prune,
                       const int32_t* h_append, const float* d_scores,
-                      int32_t* d_kept, int32_t* d_pruned, void* stream);
+                      int32_t* d_kept, int32_t* d_pruned, int32_t* d_pos, void* stream);
 
 /* ---------------------------------------------------------------------------
  * (3)(4) Resized linears.  Collective semantics: every rank calls
@@ -251,7 +254,18 @@ typedef struct ztp_sel {
 
 typedef struct ztp_linear_args {
   ztp_mat x_t, w_t, y_t, pre_t, g_t, dx_t, dw_t, pre_in_t;
+  /* Compact operand copies.  xs_t
+   * [>= n_kept, N] receives x_t rows S in lineage order, ws_t [>= n_kept, n]
+   * receives w_t rows S: FWD writes them, BWD of the same lineage entry reads
+   * them (ptr NULL: context workspace, BWD re-gathers).  The GEMM mainloop
+   * then streams dense TMA boxes. */
+  ztp_mat xs_t, ws_t;
   const ztp_sel* sel;          /* lineage entry; NULL = dense */
+  const int32_t* y_pos;        /* FWD, optional: output unit j is written to row y_pos[j] of y_t / pre_t
+                                  and dropped if y_pos[j] < 0 -- the next layer's compaction done by this
+                                  epilogue (device array of n_out entries) */
+  int32_t x_compact;           /* x_t (and pre_in_t) already hold only rows S, in lineage order */
+  int32_t _pad0;
   int64_t n_out;               /* output units computed (<= w_t.cols); 0 = w_t.cols */
   int32_t impute;              /* ztp_impute (Zero is the paper's choice) */
   int32_t act;                 /* FWD activation of this layer's output */
@@ -268,9 +282,11 @@ ztp_status ztp_row_linear(ztp_ctx* ctx, ztp_phase phase, const ztp_linear_args* 
 
 /* Stand-in attention core of the measurement layer (A-31): FWD ctx_t[f,t] =
  * q[f,t] + k[f,t] + v[f,t] with qkv_t = [Q; K; V] row blocks of `feat` rows
- * (the first n_feat of each block); BWD g_qkv_t = [dctx; dctx; dctx]. */
+ * (the first n_feat of each block); BWD g_qkv_t = [dctx; dctx; dctx].
+ * FWD with rows != NULL writes only features rows[0..n_rows) as compact rows
+ * 0..n_rows-1 of ctx_t (the O projection's kept rows S, producer-side). */
 ztp_status ztp_core(ztp_ctx* ctx, ztp_phase phase, const ztp_mat* qkv_t, const ztp_mat* ctx_t,
-                    int64_t feat, int64_t n_feat, void* stream);
+                    int64_t feat, int64_t n_feat, const int32_t* rows, int64_t n_rows, void* stream);
 
 /* ---------------------------------------------------------------------------
  * (5) Migration -- peer copies of shard slices (A-26).

@@ -521,11 +521,15 @@ def layer_step(Xt, Gt, sh: LayerShards, sel=None, mig=None, merged=True, policy=
     preJ, HJ = {}, {}
     extra_to_straggler = [np.zeros((h, N)) for _ in range(e)]
     for (s, r, lo, hi) in mig:
-        pj = sh.w1_t[s][:, lo:hi].T @ Y1          # received slices are never pruned
+        # received units extend the helper's FC1 output columns, contracted over
+        # the helper's own kept rows S_c (reading A-33), and are appended to its
+        # FC2 contraction unpruned (A-26)
+        Sr, _ = S_of(r, "fc1")
+        pj = linear_fwd(sh.w1_t[s][:, lo:hi], Y1, Sr)
         preJ[(s, r)] = pj
         HJ[(s, r)] = gelu_tanh(pj)
         contrib = sh.w2_t[s][lo:hi].T @ HJ[(s, r)]
-        flops[r] += 2.0 * (hi - lo) * N * h * 2
+        flops[r] += 2.0 * (hi - lo) * N * (kept_count(r, "fc1", h) + h)
         if merged:
             y_parts[r] = y_parts[r] + contrib          # local reduce merged
         else:
@@ -556,9 +560,10 @@ def layer_step(Xt, Gt, sh: LayerShards, sel=None, mig=None, merged=True, policy=
         dHJ = sh.w2_t[s][lo:hi] @ Gt
         dW2[s][lo:hi] = HJ[(s, r)] @ Gt.T                  # returned to the owner
         G1J = dHJ * gelu_tanh_grad(preJ[(s, r)])
-        contrib = sh.w1_t[s][:, lo:hi] @ G1J
-        dW1[s][:, lo:hi] = Y1 @ G1J.T                      # returned to the owner
-        flops[r] += 2.0 * (hi - lo) * N * h * 4
+        Sr, Pr = S_of(r, "fc1")
+        contrib = linear_bwd_dx(sh.w1_t[s][:, lo:hi], G1J, Sr, Pr, policy)
+        dW1[s][:, lo:hi] = linear_bwd_dw(Y1, G1J, Sr, Pr, policy)   # returned to the owner
+        flops[r] += 2.0 * (hi - lo) * N * (2.0 * h + 2.0 * kept_count(r, "fc1", h))
         if merged:
             dy1_parts[r] = dy1_parts[r] + contrib            # merged into the all-reduce
         else:

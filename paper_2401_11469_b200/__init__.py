@@ -129,13 +129,13 @@ def ztp_allgather_stats(ctx, T_own: float, M_own: float, world: int, stream=None
 # ------------------------------------------------------------------ device calls
 
 def ztp_select(ctx, seg_len: Sequence[int], n_prune: Sequence[int], scores, kept, pruned,
-               append: Optional[Sequence[int]] = None, stream=None) -> None:
+               append: Optional[Sequence[int]] = None, pos=None, stream=None) -> None:
     n = len(seg_len)
     la = (C.c_int32 * n)(*seg_len)
     pa = (C.c_int32 * n)(*n_prune)
     aa = (C.c_int32 * n)(*append) if append is not None else None
     check(lib.ztp_select(ctx, n, la, pa, aa, scores.data_ptr(), kept.data_ptr(), pruned.data_ptr(),
-                         _stream(stream)), ctx)
+                         pos.data_ptr() if pos is not None else None, _stream(stream)), ctx)
 
 
 def sel(kept, n_kept: int, pruned, n_pruned: int, layer_id: int, matrix_id: int) -> Sel:
@@ -145,10 +145,14 @@ def sel(kept, n_kept: int, pruned, n_pruned: int, layer_id: int, matrix_id: int)
 
 def linear_args(x_t=None, w_t=None, y_t=None, pre_t=None, g_t=None, dx_t=None, dw_t=None, pre_in_t=None,
                 sel_: Optional[Sel] = None, n_out: int = 0, impute: int = IMPUTE_ZERO, act: int = ACT_NONE,
-                act_in: int = ACT_NONE, skip_collective: int = 0) -> LinearArgs:
+                act_in: int = ACT_NONE, skip_collective: int = 0, xs_t=None, ws_t=None, y_pos=None,
+                x_compact: bool = False) -> LinearArgs:
     a = LinearArgs()
     a.x_t, a.w_t, a.y_t, a.pre_t = mat(x_t), mat(w_t), mat(y_t), mat(pre_t)
     a.g_t, a.dx_t, a.dw_t, a.pre_in_t = mat(g_t), mat(dx_t), mat(dw_t), mat(pre_in_t)
+    a.xs_t, a.ws_t = mat(xs_t), mat(ws_t)
+    a.y_pos = y_pos.data_ptr() if y_pos is not None else None
+    a.x_compact = int(x_compact)
     a.sel = C.pointer(sel_) if sel_ is not None else None
     a.n_out = n_out
     a.impute = impute
@@ -172,9 +176,11 @@ def ztp_gemm(ctx, kind: int, args: LinearArgs, stream=None) -> None:
     check(lib.ztp_gemm(ctx, kind, C.byref(args), _stream(stream)), ctx)
 
 
-def ztp_core(ctx, phase: int, qkv_t, ctx_t, feat: int, n_feat: int, stream=None) -> None:
+def ztp_core(ctx, phase: int, qkv_t, ctx_t, feat: int, n_feat: int, rows=None, n_rows: int = 0,
+             stream=None) -> None:
     q, c = mat(qkv_t), mat(ctx_t)
-    check(lib.ztp_core(ctx, phase, C.byref(q), C.byref(c), feat, n_feat, _stream(stream)), ctx)
+    check(lib.ztp_core(ctx, phase, C.byref(q), C.byref(c), feat, n_feat,
+                       rows.data_ptr() if rows is not None else None, n_rows, _stream(stream)), ctx)
 
 
 def ztp_migrate(ctx, xfers: Sequence[Xfer], stream=None) -> None:

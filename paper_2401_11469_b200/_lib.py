@@ -71,7 +71,8 @@ class Sel(C.Structure):
 
 class LinearArgs(C.Structure):
     _fields_ = [("x_t", Mat), ("w_t", Mat), ("y_t", Mat), ("pre_t", Mat), ("g_t", Mat), ("dx_t", Mat),
-                ("dw_t", Mat), ("pre_in_t", Mat), ("sel", C.POINTER(Sel)), ("n_out", C.c_int64),
+                ("dw_t", Mat), ("pre_in_t", Mat), ("xs_t", Mat), ("ws_t", Mat), ("sel", C.POINTER(Sel)),
+                ("y_pos", C.c_void_p), ("x_compact", C.c_int32), ("_pad0", C.c_int32), ("n_out", C.c_int64),
                 ("impute", C.c_int32), ("act", C.c_int32), ("act_in", C.c_int32), ("gather_output", C.c_int32),
                 ("input_is_parallel", C.c_int32), ("skip_collective", C.c_int32),
                 ("hist_dx", C.POINTER(Mat)), ("hist_dw", C.POINTER(Mat))]
@@ -107,10 +108,10 @@ def _load():
         "ztp_allgather_stats": (st, [vp, C.c_double, C.c_double, C.POINTER(C.c_double),
                                      C.POINTER(C.c_double), vp]),
         "ztp_select": (st, [vp, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
-                            vp, vp, vp, vp]),
+                            vp, vp, vp, vp, vp]),
         "ztp_col_linear": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
         "ztp_row_linear": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
-        "ztp_core": (st, [vp, C.c_int, C.POINTER(Mat), C.POINTER(Mat), C.c_int64, C.c_int64, vp]),
+        "ztp_core": (st, [vp, C.c_int, C.POINTER(Mat), C.POINTER(Mat), C.c_int64, C.c_int64, vp, C.c_int64, vp]),
         "ztp_migrate": (st, [vp, C.c_int, C.POINTER(Xfer), vp]),
         "ztp_set_slowdown": (st, [vp, C.c_double]),
         "ztp_set_stats": (st, [vp, C.c_int]),

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -43,6 +44,9 @@ struct ztp_ctx {
   int64_t iota_cap = 0;
   void* ws = nullptr;
   size_t ws_cap = 0;
+  void* cws[2] = {nullptr, nullptr};   // compact-operand workspaces (x, w)
+  size_t cws_cap[2] = {0, 0};
+  int use_gather4 = 0;                 // 1: gather rows in the GEMM producer with TMA gather4
 };
 
 namespace {
@@ -139,40 +143,70 @@ ztp_status resolve_sel(ztp_ctx* c, const ztp_sel* sel, int64_t K, const int32_t*
   return ZTP_OK;
 }
 
+// Operand source of a GEMM: the full tensor (rows reached through the lineage
+// list) or a compact tensor holding exactly the kept rows in lineage order.
+struct Src {
+  const ztp_mat* m;
+  bool compact;
+};
+
 // One resized GEMM + (optional) emulated slowdown.
-ztp_status gemm(ztp_ctx* c, int kind, const ztp_mat& x, const ztp_mat& w, const ztp_mat& g, int64_t n_out,
-                const int32_t* kept, const int32_t* pruned, int nk, const ztp_mat& out, const ztp_mat* out2,
-                const ztp_mat* aux, int epi, cudaStream_t st) {
-  const int dtype = (kind == ztp::KIND_DW ? x.dtype : w.dtype);
+//   FWD: A = W^T source, B = X^T source     DX: A = W^T source, B = G^T
+//   DW : A = X^T source, B = G^T
+ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t* kept, const int32_t* pruned,
+                int nk, const ztp_mat& out, const ztp_mat* out2, const ztp_mat* aux, int aux_by_m,
+                const int32_t* out_pos, int epi, cudaStream_t st) {
+  const int dtype = A.m->dtype;
+  {
+    const ztp_mat* need[3] = {A.m, B.m, &out};
+    for (const ztp_mat* m : need)
+      if (!mat_ok(*m) || m->dtype != dtype)
+        return fail(c, ZTP_ESHAPE, "gemm: operand " + shp("m", *m) +
+                                       " must be non-empty, 16-byte aligned with ld a multiple of 16 bytes, dtype "
+                                       "matching");
+    if (out2 && (!mat_ok(*out2) || out2->dtype != dtype)) return fail(c, ZTP_ESHAPE, "gemm: bad " + shp("out2", *out2));
+    if (aux && (!mat_ok(*aux) || aux->dtype != dtype)) return fail(c, ZTP_ESHAPE, "gemm: bad " + shp("aux", *aux));
+    if ((A.compact && A.m->rows < nk) || (kind == ztp::KIND_FWD && B.compact && B.m->rows < nk))
+      return fail(c, ZTP_ESHAPE, "gemm: compact operand has fewer rows than n_kept");
+  }
+  const ztp_mat& a = *A.m;
+  const ztp_mat& b = *B.m;
+  int M, N, kdim;
+  if (kind == ztp::KIND_FWD) {
+    M = (int)n_out;
+    N = (int)b.cols;
+    kdim = nk;
+  } else if (kind == ztp::KIND_DX) {
+    M = (int)out.rows;
+    N = (int)b.cols;
+    kdim = (int)n_out;
+  } else {
+    M = (int)out.rows;
+    N = (int)n_out;
+    kdim = (int)a.cols;
+  }
   if (dtype == ZTP_BF16) {
     ztp::GemmOperands o{};
-    o.x = x.ptr;
-    o.ld_x = x.ld;
-    o.w = w.ptr;
-    o.ld_w = w.ld;
-    o.g = g.ptr;
-    o.ld_g = g.ld;
-    o.n_cols = n_out;
-    ztp::GemmParams p{};
+    o.a = a.ptr;
+    o.a_ld = a.ld;
+    o.a_gather = !A.compact;
+    o.a_rows = A.compact ? nk : a.rows;
+    o.a_cols = kind == ztp::KIND_DW ? a.cols : n_out;
+    o.b = b.ptr;
+    o.b_ld = b.ld;
     if (kind == ztp::KIND_FWD) {
-      o.K = x.rows;
-      o.N = x.cols;
-      p.M = (int)n_out;
-      p.N = (int)x.cols;
-      p.kdim = nk;
-    } else if (kind == ztp::KIND_DX) {
-      o.K = w.rows;
-      o.N = g.cols;
-      p.M = (int)w.rows;
-      p.N = (int)g.cols;
-      p.kdim = (int)n_out;
+      o.b_gather = !B.compact;
+      o.b_rows = B.compact ? nk : b.rows;
+      o.b_cols = b.cols;
     } else {
-      o.K = x.rows;
-      o.N = x.cols;
-      p.M = (int)x.rows;
-      p.N = (int)n_out;
-      p.kdim = (int)x.cols;
+      o.b_gather = false;
+      o.b_rows = n_out;
+      o.b_cols = b.cols;
     }
+    ztp::GemmParams p{};
+    p.M = M;
+    p.N = N;
+    p.kdim = kdim;
     p.n_kept = nk;
     p.kept = kept;
     p.pruned = pruned;
@@ -183,39 +217,47 @@ ztp_status gemm(ztp_ctx* c, int kind, const ztp_mat& x, const ztp_mat& w, const 
     p.ld_out2 = out2 ? out2->ld : 0;
     p.aux = aux ? (const __nv_bfloat16*)aux->ptr : nullptr;
     p.ld_aux = aux ? aux->ld : 0;
+    p.aux_by_m = aux_by_m;
+    p.out_pos = out_pos;
     p.stamp = emulating(c) ? c->d_stamp : nullptr;
     CUDA_TRY(c, ztp::gemm_launch(kind, o, p, c->num_sms, st));
   } else {
     ztp::GemmParamsF32 p{};
     p.kind = kind;
-    if (kind == ztp::KIND_FWD) {
-      p.M = (int)n_out;
-      p.N = (int)x.cols;
-      p.kdim = nk;
-    } else if (kind == ztp::KIND_DX) {
-      p.M = (int)w.rows;
-      p.N = (int)g.cols;
-      p.kdim = (int)n_out;
-    } else {
-      p.M = (int)x.rows;
-      p.N = (int)n_out;
-      p.kdim = (int)x.cols;
-    }
+    p.M = M;
+    p.N = N;
+    p.kdim = kdim;
     p.n_kept = nk;
     p.kept = kept;
     p.pruned = pruned;
-    p.x = (const float*)x.ptr;
-    p.ld_x = x.ld;
-    p.w = (const float*)w.ptr;
-    p.ld_w = w.ld;
-    p.g = (const float*)g.ptr;
-    p.ld_g = g.ld;
+    if (kind == ztp::KIND_FWD) {
+      if (A.compact && kept != c->d_iota) return fail(c, ZTP_EUNSUPPORTED, "f32 path: compact weights");
+      p.w = (const float*)a.ptr;
+      p.ld_w = a.ld;
+      p.x = (const float*)b.ptr;
+      p.ld_x = b.ld;
+      p.x_compact = B.compact ? 1 : 0;
+    } else if (kind == ztp::KIND_DX) {
+      if (A.compact && kept != c->d_iota) return fail(c, ZTP_EUNSUPPORTED, "f32 path: compact weights");
+      p.w = (const float*)a.ptr;
+      p.ld_w = a.ld;
+      p.g = (const float*)b.ptr;
+      p.ld_g = b.ld;
+    } else {
+      p.x = (const float*)a.ptr;
+      p.ld_x = a.ld;
+      p.x_compact = A.compact ? 1 : 0;
+      p.g = (const float*)b.ptr;
+      p.ld_g = b.ld;
+    }
     p.out = (float*)out.ptr;
     p.ld_out = out.ld;
     p.out2 = out2 ? (float*)out2->ptr : nullptr;
     p.ld_out2 = out2 ? out2->ld : 0;
     p.aux = aux ? (const float*)aux->ptr : nullptr;
     p.ld_aux = aux ? aux->ld : 0;
+    p.aux_by_m = aux_by_m;
+    p.out_pos = out_pos;
     p.epi = epi;
     CUDA_TRY(c, ztp::gemm_f32_launch(p, st));
   }
@@ -230,13 +272,66 @@ ztp_status allreduce(ztp_ctx* c, const ztp_mat& m, cudaStream_t st) {
   return ZTP_OK;
 }
 
+// Compact copy of the kept rows of `full` into `dst` (caller buffer or ctx
+// workspace slot `slot`).  Returns the compact matrix in *out.
+ztp_status compact_rows(ztp_ctx* c, const ztp_mat& full, const int32_t* kept, int nk, const ztp_mat& dst_in,
+                        int slot, ztp_mat* out, cudaStream_t st) {
+  ztp_mat d = dst_in;
+  if (!d.ptr) {
+    const size_t es = full.dtype == ZTP_F32 ? 4 : 2;
+    const int64_t ld = (full.cols + 7) / 8 * 8;
+    const size_t bytes = ((size_t)nk * ld * es + 1023) & ~size_t(1023);
+    if (c->cws_cap[slot] < bytes) {
+      if (c->cws[slot]) cudaFree(c->cws[slot]);
+      c->cws[slot] = nullptr;
+      c->cws_cap[slot] = 0;
+      CUDA_TRY(c, cudaMalloc(&c->cws[slot], bytes));
+      c->cws_cap[slot] = bytes;
+    }
+    d = ztp_mat{c->cws[slot], nk, full.cols, ld, full.dtype, 0};
+  }
+  if (!mat_ok(d) || d.rows < nk || d.cols < full.cols || d.dtype != full.dtype)
+    return fail(c, ZTP_ESHAPE, "compact buffer " + shp("dst", d) + " too small for " + shp("src", full));
+  CUDA_TRY(c, ztp::gather_rows_launch(full.ptr, full.ld, kept, nk, full.cols, d.ptr, d.ld, full.dtype, st));
+  ++c->launches;
+  d.rows = nk;
+  d.cols = full.cols;
+  *out = d;
+  return ZTP_OK;
+}
+
 enum { LAYER_COL = 0, LAYER_ROW = 1 };
+
+// Source of the weight (or input) operand for this call.
+ztp_status operand_src(ztp_ctx* c, bool dense_sel, bool caller_compact, const ztp_mat& full, const ztp_mat& cbuf,
+                       bool refill, const int32_t* kept, int nk, int slot, ztp_mat* tmp, Src* out, cudaStream_t st) {
+  if (dense_sel) {
+    *out = Src{&full, true};
+    return ZTP_OK;
+  }
+  if (caller_compact) {
+    *out = Src{&full, true};
+    return ZTP_OK;
+  }
+  if (full.dtype == ZTP_F32 || c->use_gather4) {
+    *out = Src{&full, false};
+    return ZTP_OK;
+  }
+  if (!refill && cbuf.ptr) {  // BWD: reuse the compact copy written by FWD (same lineage entry)
+    *tmp = cbuf;
+    tmp->rows = nk;
+    *out = Src{tmp, true};
+    return ZTP_OK;
+  }
+  ztp_status s = compact_rows(c, full, kept, nk, cbuf, slot, tmp, st);
+  if (s != ZTP_OK) return s;
+  *out = Src{tmp, true};
+  return ZTP_OK;
+}
 
 ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args* a, cudaStream_t st) {
   if (!c || !a) return fail(c, ZTP_EINVAL, "linear: null ctx/args");
   const char* nm = layer == LAYER_COL ? "ztp_col_linear" : "ztp_row_linear";
-  if (!mat_ok(a->x_t) && !(phase == ZTP_BWD && !a->dw_t.ptr))
-    return fail(c, ZTP_ESHAPE, std::string(nm) + ": bad " + shp("x_t", a->x_t));
   if (!mat_ok(a->w_t)) return fail(c, ZTP_ESHAPE, std::string(nm) + ": bad " + shp("w_t", a->w_t));
   const int64_t K = a->w_t.rows;
   const int64_t n_out = a->n_out > 0 ? a->n_out : a->w_t.cols;
@@ -251,22 +346,33 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
   int nk, np;
   ztp_status s = resolve_sel(c, a->sel, K, &kept, &pruned, &nk, &np);
   if (s != ZTP_OK) return s;
+  const bool dense_sel = a->sel == nullptr;
   const std::pair<int, int> key = a->sel ? std::make_pair(a->sel->layer_id, a->sel->matrix_id) : std::make_pair(-1, -1);
+  const bool xc = a->x_compact != 0;
+  const int64_t x_rows_need = xc ? nk : K;
+  ztp_mat tmpx{}, tmpw{};
+  Src X{nullptr, false}, W{nullptr, false};
 
   if (phase == ZTP_FWD) {
     const ztp_mat& x = a->x_t;
-    if (x.rows != K || x.dtype != dtype)
-      return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD: " + shp("x_t", x) + " vs " + shp("w_t", a->w_t));
+    if (!mat_ok(x) || x.rows < x_rows_need || x.dtype != dtype || (!xc && x.rows != K))
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD: " + shp("x_t", x) + " vs " + shp("w_t", a->w_t) +
+                                     (xc ? " (compact x: needs n_kept rows)" : ""));
     const int64_t N = x.cols;
-    if (!mat_ok(a->y_t) || a->y_t.rows < n_out || a->y_t.cols != N || a->y_t.dtype != dtype)
+    const bool act = a->act == ZTP_ACT_GELU;
+    const int64_t out_rows_need = a->y_pos ? 1 : n_out;
+    if (!mat_ok(a->y_t) || a->y_t.rows < out_rows_need || a->y_t.cols != N || a->y_t.dtype != dtype)
       return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD: " + shp("y_t", a->y_t) + " for n_out " + std::to_string(n_out));
     if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
-    const bool act = a->act == ZTP_ACT_GELU;
-    if (act && (!mat_ok(a->pre_t) || a->pre_t.rows < n_out || a->pre_t.cols != N))
+    if (act && (!mat_ok(a->pre_t) || a->pre_t.rows < out_rows_need || a->pre_t.cols != N))
       return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD GeLU: " + shp("pre_t", a->pre_t));
     if (a->sel) c->lineage[key] = LineageEntry{a->sel->kept, a->sel->pruned, a->sel->n_kept, a->sel->n_pruned};
-    s = gemm(c, ztp::KIND_FWD, x, a->w_t, a->w_t, n_out, kept, pruned, nk, act ? a->pre_t : a->y_t,
-             act ? &a->y_t : nullptr, nullptr, act ? ztp::EPI_GELU : ztp::EPI_NONE, st);
+    s = operand_src(c, dense_sel, xc, x, a->xs_t, true, kept, nk, 0, &tmpx, &X, st);
+    if (s != ZTP_OK) return s;
+    s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, true, kept, nk, 1, &tmpw, &W, st);
+    if (s != ZTP_OK) return s;
+    s = gemm(c, ztp::KIND_FWD, W, X, n_out, kept, pruned, nk, act ? a->pre_t : a->y_t, act ? &a->y_t : nullptr,
+             nullptr, 0, a->y_pos, act ? ztp::EPI_GELU : ztp::EPI_NONE, st);
     if (s != ZTP_OK) return s;
     if (layer == LAYER_ROW && !a->skip_collective) return allreduce(c, a->y_t, st);
     return ZTP_OK;
@@ -291,12 +397,15 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     int epi = ztp::EPI_NONE;
     const ztp_mat* aux = nullptr;
     if (layer == LAYER_ROW && a->act_in == ZTP_ACT_GELU) {
-      if (!mat_ok(a->pre_in_t) || a->pre_in_t.rows != K || a->pre_in_t.cols != N)
+      if (!mat_ok(a->pre_in_t) || a->pre_in_t.rows < x_rows_need || a->pre_in_t.cols != N)
         return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD GeLU': " + shp("pre_in_t", a->pre_in_t));
       epi = ztp::EPI_GELU_GRAD;
       aux = &a->pre_in_t;
     }
-    s = gemm(c, ztp::KIND_DX, a->x_t, a->w_t, g, n_out, kept, pruned, nk, a->dx_t, nullptr, aux, epi, st);
+    s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, false, kept, nk, 1, &tmpw, &W, st);
+    if (s != ZTP_OK) return s;
+    s = gemm(c, ztp::KIND_DX, W, Src{&g, true}, n_out, kept, pruned, nk, a->dx_t, nullptr, aux, xc ? 1 : 0,
+             nullptr, epi, st);
     if (s != ZTP_OK) return s;
   }
   const bool reduce_dx = layer == LAYER_COL && a->dx_t.ptr && !a->skip_collective && c->world > 1;
@@ -310,11 +419,14 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
   }
   if (a->dw_t.ptr) {
     const ztp_mat& x = a->x_t;
-    if (x.rows != K || x.cols != N || x.dtype != dtype)
+    if (!mat_ok(x) || x.rows < x_rows_need || x.cols != N || x.dtype != dtype || (!xc && x.rows != K))
       return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("x_t", x) + " vs " + shp("g_t", g));
     if (!mat_ok(a->dw_t) || a->dw_t.rows != K || a->dw_t.cols < n_out || a->dw_t.dtype != dtype)
       return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dw_t", a->dw_t));
-    s = gemm(c, ztp::KIND_DW, x, a->w_t, g, n_out, kept, pruned, nk, a->dw_t, nullptr, nullptr, ztp::EPI_NONE, st);
+    s = operand_src(c, dense_sel, xc, x, a->xs_t, false, kept, nk, 0, &tmpx, &X, st);
+    if (s != ZTP_OK) return s;
+    s = gemm(c, ztp::KIND_DW, X, Src{&g, true}, n_out, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
+             ztp::EPI_NONE, st);
     if (s != ZTP_OK) return s;
   }
   if (reduce_dx) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_b, 0));
@@ -376,6 +488,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   c->world = world;
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
+  if (const char* g4 = getenv("ZTP_GATHER4")) c->use_gather4 = atoi(g4) != 0;
   auto cleanup = [&](ztp_status s) {
     ztp_ctx_destroy(c);
     return s;
@@ -415,6 +528,8 @@ ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   cudaFree(c->d_stats);
   cudaFree(c->d_iota);
   cudaFree(c->ws);
+  cudaFree(c->cws[0]);
+  cudaFree(c->cws[1]);
   delete c;
   return ZTP_OK;
 }
@@ -457,19 +572,20 @@ ztp_status ztp_allgather_stats(ztp_ctx* c, double T_own, double M_own, double* T
 }
 
 ztp_status ztp_select(ztp_ctx* c, int nseg, const int32_t* h_len, const int32_t* h_np, const int32_t* h_app,
-                      const float* d_scores, int32_t* d_kept, int32_t* d_pruned, void* stream) {
+                      const float* d_scores, int32_t* d_kept, int32_t* d_pruned, int32_t* d_pos, void* stream) {
   if (!c || !h_len || !h_np || !d_scores || !d_kept || !d_pruned || nseg < 1)
     return fail(c, ZTP_EINVAL, "ztp_select: null argument or nseg < 1");
   std::vector<ztp::SelectSeg> segs(nseg);
-  int64_t so = 0, ko = 0, po = 0;
+  int64_t so = 0, ko = 0, po = 0, qo = 0;
   for (int i = 0; i < nseg; ++i) {
     const int32_t app = h_app ? h_app[i] : 0;
     if (h_len[i] < 1 || h_np[i] < 0 || h_np[i] > h_len[i] - 1 || app < 0)
       return fail(c, ZTP_EINVAL,
                   "ztp_select: segment " + std::to_string(i) + " len " + std::to_string(h_len[i]) + " n_prune " +
                       std::to_string(h_np[i]) + " (need 0 <= n_prune <= len-1)");
-    segs[i] = ztp::SelectSeg{h_len[i], h_np[i], app, (int32_t)so, (int32_t)ko, (int32_t)po};
+    segs[i] = ztp::SelectSeg{h_len[i], h_np[i], app, (int32_t)so, (int32_t)ko, (int32_t)po, (int32_t)qo};
     so += h_len[i];
+    qo += h_len[i] + app;
     ko += h_len[i] - h_np[i] + app;
     po += h_np[i];
   }
@@ -478,7 +594,7 @@ ztp_status ztp_select(ztp_ctx* c, int nseg, const int32_t* h_len, const int32_t*
     ztp::SelectParams p{};
     p.nseg = std::min(ztp::SELECT_MAX_SEGS, nseg - b);
     for (int i = 0; i < p.nseg; ++i) p.seg[i] = segs[b + i];
-    CUDA_TRY(c, ztp::select_launch(p, d_scores, d_kept, d_pruned, c->d_flags, (cudaStream_t)stream));
+    CUDA_TRY(c, ztp::select_launch(p, d_scores, d_kept, d_pruned, d_pos, c->d_flags, (cudaStream_t)stream));
     ++c->launches;
   }
   return ZTP_OK;
@@ -493,35 +609,51 @@ ztp_status ztp_row_linear(ztp_ctx* c, ztp_phase phase, const ztp_linear_args* a,
 
 ztp_status ztp_gemm(ztp_ctx* c, int kind, const ztp_linear_args* a, void* stream) {
   if (!c || !a || kind < 0 || kind > 2) return fail(c, ZTP_EINVAL, "ztp_gemm: bad arguments");
-  const int64_t K = a->w_t.rows ? a->w_t.rows : a->x_t.rows;
+  cudaStream_t st = (cudaStream_t)stream;
+  const ztp_mat& full_src = kind == ztp::KIND_DW ? a->x_t : a->w_t;
+  const int64_t K = a->x_compact && kind == ztp::KIND_DW ? a->dw_t.rows : full_src.rows;
   const int64_t n_out = a->n_out > 0 ? a->n_out : (kind == ztp::KIND_DW ? a->dw_t.cols : a->w_t.cols);
   const int32_t* kept;
   const int32_t* pruned;
   int nk, np;
-  ztp_status s = resolve_sel(c, a->sel, K, &kept, &pruned, &nk, &np);
+  ztp_status s = resolve_sel(c, a->sel, kind == ztp::KIND_FWD ? a->w_t.rows : (kind == ztp::KIND_DX ? a->w_t.rows : K),
+                             &kept, &pruned, &nk, &np);
   if (s != ZTP_OK) return s;
-  cudaStream_t st = (cudaStream_t)stream;
+  const bool dense_sel = a->sel == nullptr;
+  ztp_mat tx{}, tw{};
+  Src X{nullptr, false}, W{nullptr, false};
   if (kind == ztp::KIND_FWD) {
     const bool act = a->act == ZTP_ACT_GELU;
-    return gemm(c, kind, a->x_t, a->w_t, a->w_t, n_out, kept, pruned, nk, act ? a->pre_t : a->y_t,
-                act ? &a->y_t : nullptr, nullptr, act ? ztp::EPI_GELU : ztp::EPI_NONE, st);
+    s = operand_src(c, dense_sel, a->x_compact != 0, a->x_t, a->xs_t, true, kept, nk, 0, &tx, &X, st);
+    if (s == ZTP_OK) s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, true, kept, nk, 1, &tw, &W, st);
+    if (s != ZTP_OK) return s;
+    return gemm(c, kind, W, X, n_out, kept, pruned, nk, act ? a->pre_t : a->y_t, act ? &a->y_t : nullptr, nullptr,
+                0, a->y_pos, act ? ztp::EPI_GELU : ztp::EPI_NONE, st);
   }
   if (kind == ztp::KIND_DX) {
     const bool gg = a->act_in == ZTP_ACT_GELU;
-    return gemm(c, kind, a->x_t, a->w_t, a->g_t, n_out, kept, pruned, nk, a->dx_t, nullptr, gg ? &a->pre_in_t : nullptr,
-                gg ? ztp::EPI_GELU_GRAD : ztp::EPI_NONE, st);
+    s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, true, kept, nk, 1, &tw, &W, st);
+    if (s != ZTP_OK) return s;
+    return gemm(c, kind, W, Src{&a->g_t, true}, n_out, kept, pruned, nk, a->dx_t, nullptr,
+                gg ? &a->pre_in_t : nullptr, a->x_compact ? 1 : 0, nullptr, gg ? ztp::EPI_GELU_GRAD : ztp::EPI_NONE,
+                st);
   }
-  return gemm(c, kind, a->x_t, a->w_t, a->g_t, n_out, kept, pruned, nk, a->dw_t, nullptr, nullptr, ztp::EPI_NONE, st);
+  s = operand_src(c, dense_sel, a->x_compact != 0, a->x_t, a->xs_t, true, kept, nk, 0, &tx, &X, st);
+  if (s != ZTP_OK) return s;
+  return gemm(c, kind, X, Src{&a->g_t, true}, n_out, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
+              ztp::EPI_NONE, st);
 }
 
 ztp_status ztp_core(ztp_ctx* c, ztp_phase phase, const ztp_mat* qkv, const ztp_mat* cx, int64_t feat, int64_t n_feat,
-                    void* stream) {
+                    const int32_t* rows, int64_t n_rows, void* stream) {
   if (!c || !qkv || !cx || !mat_ok(*qkv) || !mat_ok(*cx)) return fail(c, ZTP_ESHAPE, "ztp_core: bad matrices");
-  if (qkv->rows < 3 * feat || n_feat > feat || cx->rows < n_feat || cx->cols != qkv->cols || qkv->dtype != cx->dtype)
+  const int64_t n_out = (phase == ZTP_FWD && rows) ? n_rows : n_feat;
+  if (qkv->rows < 3 * feat || n_feat > feat || cx->rows < n_out || cx->cols != qkv->cols || qkv->dtype != cx->dtype ||
+      (rows && (n_rows < 1 || n_rows > n_feat)))
     return fail(c, ZTP_ESHAPE, "ztp_core: " + shp("qkv_t", *qkv) + " " + shp("ctx_t", *cx));
   if (qkv->dtype == ZTP_BF16 && qkv->cols % 8) return fail(c, ZTP_ESHAPE, "ztp_core: N % 8 != 0");
-  CUDA_TRY(c, ztp::core_launch(phase == ZTP_FWD ? 0 : 1, qkv->ptr, qkv->ld, cx->ptr, cx->ld, feat, n_feat, qkv->cols,
-                               qkv->dtype, (cudaStream_t)stream));
+  CUDA_TRY(c, ztp::core_launch(phase == ZTP_FWD ? 0 : 1, qkv->ptr, qkv->ld, cx->ptr, cx->ld, feat, n_out, qkv->cols,
+                               qkv->dtype, phase == ZTP_FWD ? rows : nullptr, (cudaStream_t)stream));
   ++c->launches;
   return ZTP_OK;
 }

@@ -74,7 +74,10 @@ __device__ __forceinline__ int gather_row_mk(const GemmParams& p, int m) {
   return (m < p.n_kept) ? __ldg(p.kept + m) : p.oob_row;
 }
 
-template <int KIND, int BN>
+// AG / BG: operand A / B gathered row-by-row with TMA gather4 through the
+// lineage list (true) or loaded as dense TMA boxes from a compact, already
+// row-selected tensor (false; rows past the compact extent are zero-filled).
+template <int KIND, int BN, bool AG, bool BG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ztp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParams p) {
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int n0 = (tile / m_tiles) * BN;
       if (zero_tile(m0)) continue;
       int ar0 = 0, ar1 = 0, ar2 = 0, ar3 = 0;
-      if (KIND != KIND_FWD) {
+      if (KIND != KIND_FWD && AG) {
         const int mb = m0 + 4 * lane;
         ar0 = gather_row_mk<KIND>(p, mb + 0);
         ar1 = gather_row_mk<KIND>(p, mb + 1);
@@ -145,24 +148,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) mbar_expect_tx(&full[stage], SM::STAGE_BYTES);
         __syncwarp();
         if (KIND == KIND_FWD) {
-          // both operands MN-major, gathered along the contraction (rows S)
-          const int g = lane & 15, half = lane >> 4;
-          const int kbase = kb * BK + 4 * g;
-          int r[4];
+          // both operands MN-major (contraction rows outer)
+          if (AG || BG) {
+            const int g = lane & 15, half = lane >> 4;
+            const int kbase = kb * BK + 4 * g;
+            int r[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int k = kbase + i;
-            r[i] = (k < p.n_kept) ? __ldg(p.kept + k) : p.oob_row;
+            for (int i = 0; i < 4; ++i) {
+              const int k = kbase + i;
+              r[i] = (k < p.n_kept) ? __ldg(p.kept + k) : p.oob_row;
+            }
+            if (AG)
+              tma_gather4(&tmA, &full[stage], sa + half * 8192 + g * 512, m0 + 64 * half, r[0], r[1], r[2], r[3]);
+            if (BG) {
+#pragma unroll
+              for (int b = 2 * half; b < 2 * half + 2; ++b)
+                if (b < BN / 64)
+                  tma_gather4(&tmB, &full[stage], sb + b * 8192 + g * 512, n0 + 64 * b, r[0], r[1], r[2], r[3]);
+            }
           }
-          tma_gather4(&tmA, &full[stage], sa + half * 8192 + g * 512, m0 + 64 * half, r[0], r[1], r[2], r[3]);
-#pragma unroll
-          for (int b = 2 * half; b < 2 * half + 2; ++b)
-            if (b < BN / 64)
-              tma_gather4(&tmB, &full[stage], sb + b * 8192 + g * 512, n0 + 64 * b, r[0], r[1], r[2], r[3]);
-        } else {
-          // A: K-major rows gathered by the lineage row map
-          tma_gather4(&tmA, &full[stage], sa + lane * 512, kb * BK, ar0, ar1, ar2, ar3);
           if (lane == 0) {
+            if (!AG) {
+              tma_load_2d(&tmA, &full[stage], sa, m0, kb * BK);
+              tma_load_2d(&tmA, &full[stage], sa + 8192, m0 + 64, kb * BK);
+            }
+            if (!BG) {
+#pragma unroll
+              for (int b = 0; b < BN / 64; ++b) tma_load_2d(&tmB, &full[stage], sb + b * 8192, n0 + 64 * b, kb * BK);
+            }
+          }
+        } else {
+          // A: K-major rows (m) x 64 contraction columns
+          if (AG) tma_gather4(&tmA, &full[stage], sa + lane * 512, kb * BK, ar0, ar1, ar2, ar3);
+          if (lane == 0) {
+            if (!AG) tma_load_2d(&tmA, &full[stage], sa, kb * BK, m0);
             if (KIND == KIND_DX) {
               // B = G^T [n, N] MN-major dense: 64 contraction rows x BN columns
 #pragma unroll
@@ -238,18 +257,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int n0 = (tile / m_tiles) * BN;
       const bool zt = zero_tile(m0);
       // output rows this lane stores: r = 4 i + lane / 8, i = 0..7
-      int orow[8];
+      int orow[8], arow[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int m = m0 + ew * 32 + 4 * i + (lane >> 3);
         int o = -1;
         if (m < p.M) {
           if (KIND == KIND_FWD)
-            o = m;
+            o = p.out_pos ? __ldg(p.out_pos + m) : m;   // producer-side compaction for the next layer
           else
             o = (m < p.n_kept) ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
         }
         orow[i] = o;
+        arow[i] = p.aux_by_m ? m : o;
       }
       if (!zt) {
         mbar_wait(&tfull[acc], aphase);
@@ -304,7 +324,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint4 w = *reinterpret_cast<const uint4*>(stg + off);
             if (p.epi == EPI_GELU_GRAD && !zt) {
               // G1 = dH * GeLU'(pre_in) at the same (row, col) (row layer BWD)
-              const uint4 pin = *reinterpret_cast<const uint4*>(p.aux + (int64_t)orow[i] * p.ld_aux + col);
+              const uint4 pin = *reinterpret_cast<const uint4*>(p.aux + (int64_t)arow[i] * p.ld_aux + col);
               w.x = pack_bf16(bf16_lo(w.x) * gelu_grad_f(bf16_lo(pin.x)), bf16_hi(w.x) * gelu_grad_f(bf16_hi(pin.x)));
               w.y = pack_bf16(bf16_lo(w.y) * gelu_grad_f(bf16_lo(pin.y)), bf16_hi(w.y) * gelu_grad_f(bf16_hi(pin.y)));
               w.z = pack_bf16(bf16_lo(w.z) * gelu_grad_f(bf16_lo(pin.z)), bf16_hi(w.z) * gelu_grad_f(bf16_hi(pin.z)));
@@ -367,46 +387,60 @@ static bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols
   return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BN>
+template <int KIND, int BN, bool AG, bool BG>
 static cudaError_t launch_kind(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int num_sms,
                                cudaStream_t st) {
   static bool attr_set = false;
   const int smem = Smem<BN>::TOTAL;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(ztp_gemm_kernel<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(ztp_gemm_kernel<KIND, BN, AG, BG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
-  ztp_gemm_kernel<KIND, BN><<<grid, NUM_THREADS, smem, st>>>(a, b, p);
+  ztp_gemm_kernel<KIND, BN, AG, BG><<<grid, NUM_THREADS, smem, st>>>(a, b, p);
   return cudaGetLastError();
 }
 
-// A/B tensor maps per kind (see header comment of this file).
+// Operand A / B tensor maps per kind (see the header comment of this file).
 cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_sms, cudaStream_t st) {
   CUtensorMap ta, tb;
   bool ok = true;
+  const bool ag = o.a_gather, bg = o.b_gather;
+  p.oob_row = (int)(o.a_rows > o.b_rows ? o.a_rows : o.b_rows);  // outside every gathered tensor
   if (kind == KIND_FWD) {
-    // A = W^T [K, n] rows gathered (box 64 cols x 1 row); B = X^T [K, N] rows gathered
-    ok &= make_map(&ta, o.w, o.K, o.n_cols, o.ld_w, 64, 1);
-    ok &= make_map(&tb, o.x, o.K, o.N, o.ld_x, 64, 1);
-    p.oob_row = (int)o.K;
+    // A = W^T [K|K', n] MN-major; B = X^T [K|K', N] MN-major (same rows)
+    ok &= make_map(&ta, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : 64);
+    ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, bg ? 1 : 64);
   } else if (kind == KIND_DX) {
-    // A = W^T [K, n_out] K-major rows gathered; B = G^T [n_out, N] MN-major 64x64 boxes
-    ok &= make_map(&ta, o.w, o.K, o.n_cols, o.ld_w, 64, 1);
-    ok &= make_map(&tb, o.g, o.n_cols, o.N, o.ld_g, 64, 64);
-    p.oob_row = (int)o.K;
+    // A = W^T [K|K', n_out] K-major; B = G^T [n_out, N] MN-major 64 x 64 boxes
+    ok &= make_map(&ta, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : BM);
+    ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, 64);
   } else {
-    // A = X^T [K, N] K-major rows gathered; B = G^T [n_out, N] K-major box 64 x 256
-    ok &= make_map(&ta, o.x, o.K, o.N, o.ld_x, 64, 1);
-    ok &= make_map(&tb, o.g, o.n_cols, o.N, o.ld_g, 64, 256);
-    p.oob_row = (int)o.K;
+    // A = X^T [K|K', N] K-major; B = G^T [n_out, N] K-major box 64 x 256
+    ok &= make_map(&ta, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : BM);
+    ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, 256);
   }
   if (!ok) return cudaErrorInvalidValue;
-  if (kind == KIND_FWD) return launch_kind<KIND_FWD, 256>(ta, tb, p, num_sms, st);
-  if (kind == KIND_DX) return launch_kind<KIND_DX, 256>(ta, tb, p, num_sms, st);
-  return launch_kind<KIND_DW, 256>(ta, tb, p, num_sms, st);
+#define ZTP_DISPATCH(K_)                                                          \
+  if (ag && bg) return launch_kind<K_, 256, true, true>(ta, tb, p, num_sms, st);   \
+  if (ag) return launch_kind<K_, 256, true, false>(ta, tb, p, num_sms, st);        \
+  if (bg) return launch_kind<K_, 256, false, true>(ta, tb, p, num_sms, st);        \
+  return launch_kind<K_, 256, false, false>(ta, tb, p, num_sms, st);
+  if (kind == KIND_FWD) {
+    ZTP_DISPATCH(KIND_FWD)
+  }
+  if (kind == KIND_DX) {
+    if (bg) return cudaErrorInvalidValue;
+    if (ag) return launch_kind<KIND_DX, 256, true, false>(ta, tb, p, num_sms, st);
+    return launch_kind<KIND_DX, 256, false, false>(ta, tb, p, num_sms, st);
+  }
+  if (bg) return cudaErrorInvalidValue;
+  if (ag) return launch_kind<KIND_DW, 256, true, false>(ta, tb, p, num_sms, st);
+  return launch_kind<KIND_DW, 256, false, false>(ta, tb, p, num_sms, st);
+#undef ZTP_DISPATCH
 }
 
 }  // namespace ztp

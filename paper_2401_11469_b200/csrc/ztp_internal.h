@@ -22,19 +22,23 @@ struct GemmParams {
   int64_t ld_out;
   __nv_bfloat16* out2;  // EPI_GELU: GeLU(pre) (out holds pre)
   int64_t ld_out2;
-  const __nv_bfloat16* aux;  // EPI_GELU_GRAD: pre-activation rows at the output row map
+  const __nv_bfloat16* aux;  // EPI_GELU_GRAD: pre-activation rows (row = output row, or m if aux_by_m)
   int64_t ld_aux;
+  int aux_by_m;               // aux is compact (row m of the tile order) instead of at the output row
+  const int32_t* out_pos;     // FWD: output row map (unit j -> row out_pos[j], dropped if < 0); NULL = identity
   unsigned long long* stamp;  // [start_min, end_max] %globaltimer of this launch (nullable)
 };
 
+// Operand tensors of one launch: row-major bf16 [rows, cols], pitch ld.
+// *_gather: rows are fetched through the lineage list with TMA gather4;
+// otherwise the tensor is compact (already row-selected) and loaded as boxes.
 struct GemmOperands {
-  const void* x;   // X^T [K, N]
-  int64_t ld_x;
-  const void* w;   // W^T [K, n]
-  int64_t ld_w;
-  const void* g;   // G^T [n, N]
-  int64_t ld_g;
-  int64_t K, N, n_cols;  // n_cols = n_out
+  const void* a;
+  int64_t a_rows, a_cols, a_ld;
+  bool a_gather;
+  const void* b;
+  int64_t b_rows, b_cols, b_ld;
+  bool b_gather;
 };
 
 cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_sms, cudaStream_t st);
@@ -42,6 +46,9 @@ cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_s
 // fp32 verification GEMM (SIMT FFMA), same lineage semantics, fp32 tensors.
 struct GemmParamsF32 {
   int kind, M, N, kdim, n_kept;
+  int x_compact;            // X^T holds only the kept rows (row k / m instead of kept[.])
+  int aux_by_m;
+  const int32_t* out_pos;
   const int32_t* kept;
   const int32_t* pruned;
   const float* x;
@@ -63,21 +70,23 @@ cudaError_t gemm_f32_launch(const GemmParamsF32& p, cudaStream_t st);
 // Priority select (ztp_select.cu).
 struct SelectSeg {
   int32_t len, n_prune, append;
-  int32_t score_off, kept_off, pruned_off;
+  int32_t score_off, kept_off, pruned_off, pos_off;
 };
 constexpr int SELECT_MAX_SEGS = 64;
 struct SelectParams {
   int nseg;
   SelectSeg seg[SELECT_MAX_SEGS];
 };
-cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned,
+cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned, int32_t* pos,
                           int32_t* err_flag, cudaStream_t st);
 
 // Straggler emulation (ztp_misc.cu).
 cudaError_t delay_launch(unsigned long long* stamp, double chi, unsigned long long* acc_ns, cudaStream_t st);
 cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st);
 cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int64_t feat,
-                        int64_t n_feat, int64_t N, int dtype, cudaStream_t st);
+                        int64_t n_feat, int64_t N, int dtype, const int32_t* rows, cudaStream_t st);
+cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* idx, int n, int64_t cols, void* dst,
+                               int64_t ld_dst, int dtype, cudaStream_t st);
 cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
                              cudaStream_t st);
 

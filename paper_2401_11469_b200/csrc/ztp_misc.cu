@@ -48,15 +48,17 @@ cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st) {
 // ------------------------------------------------------ stand-in core (A-31)
 // FWD ctx[f,t] = q[f,t] + k[f,t] + v[f,t]; BWD q = k = v = dctx.  16-byte vectors.
 __global__ void ztp_core_bf16(int phase, const __nv_bfloat16* __restrict__ qkv_c, __nv_bfloat16* qkv, int64_t ld_qkv,
-                              __nv_bfloat16* ctx, int64_t ld_ctx, int64_t feat, int64_t n_feat, int64_t N) {
+                              __nv_bfloat16* ctx, int64_t ld_ctx, int64_t feat, int64_t n_feat, int64_t N,
+                              const int32_t* __restrict__ rows) {
   const int64_t vec_per_row = N / 8;
   const int64_t total = n_feat * vec_per_row;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = i / vec_per_row, c = (i % vec_per_row) * 8;
     if (phase == 0) {
-      const uint4 a = *reinterpret_cast<const uint4*>(qkv_c + f * ld_qkv + c);
-      const uint4 b = *reinterpret_cast<const uint4*>(qkv_c + (feat + f) * ld_qkv + c);
-      const uint4 d = *reinterpret_cast<const uint4*>(qkv_c + (2 * feat + f) * ld_qkv + c);
+      const int64_t sf = rows ? (int64_t)__ldg(rows + f) : f;  // compact output row f <- feature sf
+      const uint4 a = *reinterpret_cast<const uint4*>(qkv_c + sf * ld_qkv + c);
+      const uint4 b = *reinterpret_cast<const uint4*>(qkv_c + (feat + sf) * ld_qkv + c);
+      const uint4 d = *reinterpret_cast<const uint4*>(qkv_c + (2 * feat + sf) * ld_qkv + c);
       const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
       const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
       const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
@@ -78,13 +80,14 @@ __global__ void ztp_core_bf16(int phase, const __nv_bfloat16* __restrict__ qkv_c
 }
 
 __global__ void ztp_core_f32(int phase, float* qkv, int64_t ld_qkv, float* ctx, int64_t ld_ctx, int64_t feat,
-                             int64_t n_feat, int64_t N) {
+                             int64_t n_feat, int64_t N, const int32_t* __restrict__ rows) {
   const int64_t total = n_feat * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = i / N, c = i % N;
-    if (phase == 0)
-      ctx[f * ld_ctx + c] = (qkv[f * ld_qkv + c] + qkv[(feat + f) * ld_qkv + c]) + qkv[(2 * feat + f) * ld_qkv + c];
-    else {
+    if (phase == 0) {
+      const int64_t sf = rows ? (int64_t)rows[f] : f;
+      ctx[f * ld_ctx + c] = (qkv[sf * ld_qkv + c] + qkv[(feat + sf) * ld_qkv + c]) + qkv[(2 * feat + sf) * ld_qkv + c];
+    } else {
       const float g = ctx[f * ld_ctx + c];
       qkv[f * ld_qkv + c] = g;
       qkv[(feat + f) * ld_qkv + c] = g;
@@ -94,14 +97,43 @@ __global__ void ztp_core_f32(int phase, float* qkv, int64_t ld_qkv, float* ctx, 
 }
 
 cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int64_t feat,
-                        int64_t n_feat, int64_t N, int dtype, cudaStream_t st) {
+                        int64_t n_feat, int64_t N, int dtype, const int32_t* rows, cudaStream_t st) {
   const int threads = 256;
   const int blocks = 148 * 8;
   if (dtype == 0)
     ztp_core_bf16<<<blocks, threads, 0, st>>>(phase, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)qkv, ld_qkv,
-                                              (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N);
+                                              (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N, rows);
   else
-    ztp_core_f32<<<blocks, threads, 0, st>>>(phase, (float*)qkv, ld_qkv, (float*)ctx, ld_ctx, feat, n_feat, N);
+    ztp_core_f32<<<blocks, threads, 0, st>>>(phase, (float*)qkv, ld_qkv, (float*)ctx, ld_ctx, feat, n_feat, N, rows);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------- row compaction (a4 gather)
+// dst[i, :] = src[idx[i], :] for i < n: the kept rows S of a feature-major
+// tensor packed contiguously (producer-side "dimension extracting"), so
+// the GEMM mainloop streams dense TMA boxes.  HBM-bound, 16-byte vectors.
+__global__ void ztp_gather_rows(const uint8_t* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ idx,
+                                int n, int64_t vec_per_row, uint8_t* __restrict__ dst, int64_t ld_dst) {
+  const int64_t total = (int64_t)n * vec_per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / vec_per_row, c = i % vec_per_row;
+    const int64_t sr = __ldg(idx + r);
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + sr * ld_src) + c);
+    reinterpret_cast<uint4*>(dst + r * ld_dst)[c] = v;
+  }
+}
+
+cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* idx, int n, int64_t cols, void* dst,
+                               int64_t ld_dst, int dtype, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t es = dtype == 0 ? 2 : 4;
+  const int64_t row_bytes = cols * es;
+  if (row_bytes % 16) return cudaErrorInvalidValue;
+  const int64_t total = (int64_t)n * (row_bytes / 16);
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  ztp_gather_rows<<<blocks, 256, 0, st>>>((const uint8_t*)src, ld_src * es, idx, n, row_bytes / 16, (uint8_t*)dst,
+                                          ld_dst * es);
   return cudaGetLastError();
 }
 
@@ -152,12 +184,12 @@ __global__ void __launch_bounds__(256) ztp_gemm_f32_kernel(const GemmParamsF32 p
           if (p.kind == KIND_FWD) {
             const int64_t kr = p.kept[k];
             if (m < p.M) a = p.w[kr * p.ld_w + m];
-            if (n < p.N) b = p.x[kr * p.ld_x + n];
+            if (n < p.N) b = p.x[(p.x_compact ? (int64_t)k : kr) * p.ld_x + n];
           } else if (p.kind == KIND_DX) {
             if (m < p.n_kept) a = p.w[(int64_t)p.kept[m] * p.ld_w + k];
             if (n < p.N) b = p.g[(int64_t)k * p.ld_g + n];
           } else {
-            if (m < p.n_kept) a = p.x[(int64_t)p.kept[m] * p.ld_x + k];
+            if (m < p.n_kept) a = p.x[(p.x_compact ? (int64_t)m : (int64_t)p.kept[m]) * p.ld_x + k];
             if (n < p.N) b = p.g[(int64_t)n * p.ld_g + k];
           }
         }
@@ -186,7 +218,12 @@ __global__ void __launch_bounds__(256) ztp_gemm_f32_kernel(const GemmParamsF32 p
     const int m = m0 + ty * 4 + i;
     if (m >= p.M) continue;
     int64_t orow = m;
-    if (p.kind != KIND_FWD) orow = (m < p.n_kept) ? p.kept[m] : p.pruned[m - p.n_kept];
+    if (p.kind != KIND_FWD)
+      orow = (m < p.n_kept) ? p.kept[m] : p.pruned[m - p.n_kept];
+    else if (p.out_pos)
+      orow = p.out_pos[m];
+    if (orow < 0) continue;
+    const int64_t arow = p.aux_by_m ? (int64_t)m : orow;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tx * 4 + j;
@@ -196,7 +233,7 @@ __global__ void __launch_bounds__(256) ztp_gemm_f32_kernel(const GemmParamsF32 p
         p.out[orow * p.ld_out + n] = v;
         p.out2[orow * p.ld_out2 + n] = gelu_f32(v);
       } else {
-        if (p.epi == EPI_GELU_GRAD) v = v * gelu_grad_f32(p.aux[orow * p.ld_aux + n]);
+        if (p.epi == EPI_GELU_GRAD) v = v * gelu_grad_f32(p.aux[arow * p.ld_aux + n]);
         p.out[orow * p.ld_out + n] = v;
       }
     }

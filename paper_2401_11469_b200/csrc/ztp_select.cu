@@ -51,11 +51,12 @@ __device__ __forceinline__ int block_excl_scan(bool flag, int& total, int* warp_
 
 __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, const float* __restrict__ scores,
                                                           int32_t* __restrict__ kept, int32_t* __restrict__ pruned,
-                                                          int32_t* err_flag) {
+                                                          int32_t* __restrict__ pos, int32_t* err_flag) {
   const SelectSeg s = p.seg[blockIdx.x];
   const float* sc = scores + s.score_off;
   int32_t* K = kept + s.kept_off;
   int32_t* P = pruned + s.pruned_off;
+  int32_t* Q = pos ? pos + s.pos_off : nullptr;
   __shared__ uint32_t hist[256];
   __shared__ int warp_tot[65];
   __shared__ uint32_t sel_bin, sel_below;
@@ -138,18 +139,22 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
         P[p_rank] = i;
       else
         K[i - p_rank] = i;
+      if (Q) Q[i] = isp ? -1 : i - p_rank;
     }
     carry_tie += tot_tie;
     carry_p += tot_p;
   }
   const int nk = s.len - s.n_prune;
-  for (int a = tid; a < s.append; a += blockDim.x) K[nk + a] = s.len + a;
+  for (int a = tid; a < s.append; a += blockDim.x) {
+    K[nk + a] = s.len + a;
+    if (Q) Q[s.len + a] = nk + a;
+  }
   (void)lane;
 }
 
-cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned,
+cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned, int32_t* pos,
                           int32_t* err_flag, cudaStream_t st) {
-  ztp_select_kernel<<<p.nseg, 1024, 0, st>>>(p, scores, kept, pruned, err_flag);
+  ztp_select_kernel<<<p.nseg, 1024, 0, st>>>(p, scores, kept, pruned, pos, err_flag);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,245 @@
+"""One transformer layer of 1D tensor parallelism on this rank, driven through
+the C ABI (SURVEY §8(a) "Layer definition used for measurement"):
+
+  attention-projection block: QKV (col) -> stand-in core ctx = Q+K+V (A-31)
+                              -> O (row) -> all-reduce
+  MLP block:                  FC1 (col) -> GeLU -> FC2 (row) -> all-reduce
+
+Every tensor is feature-major ([features, tokens]) and every weight is stored
+W^T [K, n].  This module only allocates device buffers
+(torch, as plumbing), builds the ztp_linear_args structs once, and issues the
+call sequence of a step; all arithmetic runs in libztp.so kernels and NCCL.
+
+Producer-side compaction: the core writes ctx only for O's kept
+rows S_o (compact), FC1's epilogue writes pre/H only for FC2's kept rows S_w
+(compact, through FC2's inverse map), and the col layers' inputs X / Y1 are
+compacted once in FWD (xs buffers) and reused in BWD.  So every GEMM mainloop
+streams dense TMA boxes.
+
+Migration (SEMI, A-26): a helper holds W1^T / W2^T with spare capacity; the
+straggler's hidden units J are pulled into the appended columns / rows
+(ztp_migrate) and simply extend the helper's FC1 output and FC2 contraction
+(kept list S_w + appended indices) -- the local reduce is the same TMEM
+accumulator, merged into the existing all-reduces.  dW slices of J
+are pushed back to the owner after BWD.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import torch
+
+import paper_2401_11469_b200 as Z
+
+SEGS = ("qkv", "o", "fc1", "fc2")
+
+
+def _buf(r, c, dtype=torch.bfloat16, fill=0.0):
+    """Row pitch padded to 16 bytes (TMA stride rule)."""
+    ld = (c + 7) // 8 * 8
+    t = torch.full((max(r, 1), ld), fill, dtype=dtype, device="cuda")
+    return t[:, :c]
+
+
+@dataclass
+class MigrationIO:
+    """This rank's migration ranges from ztp_plan_counts (FC1/FC2 units)."""
+    n_mig: int = 0                                     # my units shed (tail)
+    out: List[tuple] = field(default_factory=list)     # (dst, lo, hi)
+    inc: List[tuple] = field(default_factory=list)     # (src, lo, hi)
+    all_xfers: List[tuple] = field(default_factory=list)  # (src, dst, lo, hi, dst_off) for every pair
+
+
+class ZtpLayer:
+    def __init__(self, ctx, h: int, f: int, N: int, rank: int, world: int, shards: Dict[str, torch.Tensor],
+                 mig_cap: int = 0, dtype=torch.bfloat16, layer_id: int = 0):
+        self.ctx, self.h, self.f, self.N = ctx, h, f, N
+        self.rank, self.world = rank, world
+        self.a = h // world                  # attention features per rank
+        self.u = f // world                  # MLP hidden units per rank
+        self.cap = mig_cap
+        self.dtype = dtype
+        self.layer_id = layer_id
+        a, u, cap = self.a, self.u, mig_cap
+        # weights (W^T), MLP ones with migration capacity
+        self.qkv_t = _buf(h, 3 * a, dtype)
+        self.o_t = _buf(a, h, dtype)
+        self.w1_t = _buf(h, u + cap, dtype)
+        self.w2_t = _buf(u + cap, h, dtype)
+        self.qkv_t.copy_(shards["qkv"])
+        self.o_t.copy_(shards["o"])
+        self.w1_t[:, :u].copy_(shards["w1"])
+        self.w2_t[:u].copy_(shards["w2"])
+        # activations
+        self.X = _buf(h, N, dtype)
+        self.Xc = _buf(h, N, dtype)              # compact X rows S_qkv
+        self.QKV = _buf(3 * a, N, dtype)
+        self.ctxC = _buf(a, N, dtype)            # compact ctx rows S_o
+        self.Y1 = _buf(h, N, dtype)
+        self.Y1c = _buf(h, N, dtype)             # compact Y1 rows S_fc1
+        self.PreC = _buf(u + cap, N, dtype)      # compact pre rows S_fc2
+        self.HC = _buf(u + cap, N, dtype)        # compact H rows S_fc2
+        self.Y = _buf(h, N, dtype)
+        # gradients
+        self.G = _buf(h, N, dtype)
+        self.G1 = _buf(u + cap, N, dtype)        # dH * GeLU'(pre), full layout, rows P zero
+        self.dY1 = _buf(h, N, dtype)
+        self.dctx = _buf(a, N, dtype)
+        self.gQKV = _buf(3 * a, N, dtype)
+        self.dX = _buf(h, N, dtype)
+        self.dqkv = _buf(h, 3 * a, dtype)
+        self.do = _buf(a, h, dtype)
+        self.dw1 = _buf(h, u + cap, dtype)
+        self.dw2 = _buf(u + cap, h, dtype)
+        # compact weights
+        self.Wqkv_c = _buf(h, 3 * a, dtype)
+        self.Wo_c = _buf(a, h, dtype)
+        self.W1_c = _buf(h, u + cap, dtype)
+        self.W2_c = _buf(u + cap, h, dtype)
+        # selection buffers (lineage)
+        self.K = {"qkv": h, "o": a, "fc1": h, "fc2": u + cap}
+        total = sum(self.K.values())
+        self.kept = torch.zeros(total, dtype=torch.int32, device="cuda")
+        self.pruned = torch.zeros(total, dtype=torch.int32, device="cuda")
+        self.pos = torch.zeros(total + cap, dtype=torch.int32, device="cuda")
+        self.mig = MigrationIO()
+        self.n_fc = u                            # FC1 output units computed / FC2 K
+        self.set_selection({s: 0 for s in SEGS}, None)
+
+    # ------------------------------------------------------------------ plan
+    def set_migration(self, mio: MigrationIO):
+        """Apply this rank's migration ranges (from ztp_plan_counts)."""
+        self.mig = mio
+        n_in = sum(hi - lo for (_, lo, hi) in mio.inc)
+        if n_in > self.cap:
+            raise ValueError(f"migration needs {n_in} units of capacity, have {self.cap}")
+        self.n_fc = self.u - mio.n_mig + n_in
+
+    def set_selection(self, n_prune: Dict[str, int], scores: Optional[Dict[str, torch.Tensor]],
+                      stream=None):
+        """Run ztp_select for the four segments (one launch) and rebuild the
+        lineage entries and argument structs.  n_prune['fc2'] counts only my own
+        (non-migrated) units; received units are appended (never pruned)."""
+        own_fc2 = self.u - self.mig.n_mig
+        n_in = self.n_fc - own_fc2
+        self.seg_len = {"qkv": self.h, "o": self.a, "fc1": self.h, "fc2": own_fc2}
+        self.append = {"qkv": 0, "o": 0, "fc1": 0, "fc2": n_in}
+        self.n_prune = dict(n_prune)
+        lens = [self.seg_len[s] for s in SEGS]
+        nps = [self.n_prune[s] for s in SEGS]
+        apps = [self.append[s] for s in SEGS]
+        if scores is None:
+            sc = torch.zeros(sum(lens), dtype=torch.float32, device="cuda")
+        else:
+            sc = torch.cat([scores[s][: self.seg_len[s]].float() for s in SEGS])
+        self._scores = sc
+        self._sel_args = (lens, nps, apps)
+        self.run_select(stream)
+        # slices of the lineage buffers
+        ko = po = qo = 0
+        self.S, self.P, self.POS, self.nk = {}, {}, {}, {}
+        for s in SEGS:
+            nk = self.seg_len[s] - self.n_prune[s] + self.append[s]
+            self.S[s] = self.kept[ko:ko + nk]
+            self.P[s] = self.pruned[po:po + max(self.n_prune[s], 0)]
+            self.POS[s] = self.pos[qo:qo + self.seg_len[s] + self.append[s]]
+            self.nk[s] = nk
+            ko += nk
+            po += self.n_prune[s]
+            qo += self.seg_len[s] + self.append[s]
+        self._build_args()
+
+    def run_select(self, stream=None):
+        lens, nps, apps = self._sel_args
+        Z.ztp_select(self.ctx, lens, nps, self._scores, self.kept, self.pruned, apps, self.pos, stream)
+
+    def _sel(self, s, mid):
+        if self.n_prune[s] == 0 and self.append[s] == 0:
+            return None            # dense: no lineage entry, operands used in place
+        p = self.P[s] if self.n_prune[s] > 0 else self.kept
+        return Z.sel(self.S[s], self.nk[s], p, self.n_prune[s], self.layer_id, mid)
+
+    def _build_args(self):
+        h, a, N, nfc = self.h, self.a, self.N, self.n_fc
+        self.sels = {s: self._sel(s, i) for i, s in enumerate(SEGS)}
+        L = Z.linear_args
+        nk = self.nk
+        # forward
+        self.f_qkv = L(x_t=self.X, w_t=self.qkv_t, y_t=self.QKV, xs_t=self.Xc, ws_t=self.Wqkv_c,
+                       sel_=self.sels["qkv"])
+        self.f_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, y_t=self.Y1, ws_t=self.Wo_c, sel_=self.sels["o"],
+                     x_compact=True)
+        self.f_fc1 = L(x_t=self.Y1, w_t=self.w1_t, y_t=self.HC, pre_t=self.PreC, xs_t=self.Y1c, ws_t=self.W1_c,
+                       sel_=self.sels["fc1"], n_out=nfc, act=Z.ACT_GELU, y_pos=self.POS["fc2"])
+        self.f_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], y_t=self.Y, ws_t=self.W2_c,
+                       sel_=self.sels["fc2"], x_compact=True)
+        # backward
+        self.b_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], g_t=self.G, dx_t=self.G1[:nfc],
+                       dw_t=self.dw2[:nfc], pre_in_t=self.PreC[:nk["fc2"]], ws_t=self.W2_c,
+                       sel_=self.sels["fc2"], act_in=Z.ACT_GELU, x_compact=True)
+        self.b_fc1 = L(x_t=self.Y1, w_t=self.w1_t, g_t=self.G1[:nfc], dx_t=self.dY1, dw_t=self.dw1, xs_t=self.Y1c,
+                       ws_t=self.W1_c, sel_=self.sels["fc1"], n_out=nfc)
+        self.b_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx, dw_t=self.do,
+                     ws_t=self.Wo_c, sel_=self.sels["o"], x_compact=True)
+        self.b_qkv = L(x_t=self.X, w_t=self.qkv_t, g_t=self.gQKV, dx_t=self.dX, dw_t=self.dqkv, xs_t=self.Xc,
+                       ws_t=self.Wqkv_c, sel_=self.sels["qkv"])
+
+    # --------------------------------------------------------------- migration
+    def _xfers(self, grads: bool):
+        xs = []
+        for (src, dst, lo, hi, off) in self.mig.all_xfers:
+            n = hi - lo
+            if not grads:   # weights: owner's units [lo,hi) -> helper's appended slots [u+off, ...)
+                xs.append(Z.xfer(self.w1_t if self.rank == src else None, self.w1_t if self.rank == dst else None,
+                                 r0=0, c0=lo, nr=self.h, nc=n, dr0=0, dc0=self.u + off, src_rank=src, dst_rank=dst))
+                xs.append(Z.xfer(self.w2_t if self.rank == src else None, self.w2_t if self.rank == dst else None,
+                                 r0=lo, c0=0, nr=n, nc=self.h, dr0=self.u + off, dc0=0, src_rank=src, dst_rank=dst))
+            else:           # gradients back: helper's appended slots -> owner's [lo, hi)
+                xs.append(Z.xfer(self.dw1 if self.rank == dst else None, self.dw1 if self.rank == src else None,
+                                 r0=0, c0=self.u + off, nr=self.h, nc=n, dr0=0, dc0=lo, src_rank=dst, dst_rank=src))
+                xs.append(Z.xfer(self.dw2 if self.rank == dst else None, self.dw2 if self.rank == src else None,
+                                 r0=self.u + off, c0=0, nr=n, nc=self.h, dr0=lo, dc0=0, src_rank=dst, dst_rank=src))
+        return xs
+
+    def migrate_weights(self, stream=None):
+        if self.mig.all_xfers:
+            Z.ztp_migrate(self.ctx, self._xfers(False), stream)
+
+    def return_grads(self, stream=None):
+        if self.mig.all_xfers:
+            Z.ztp_migrate(self.ctx, self._xfers(True), stream)
+
+    # -------------------------------------------------------------------- step
+    def forward(self, stream=None):
+        c = self.ctx
+        Z.ztp_col_linear(c, Z.FWD, self.f_qkv, stream)
+        Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, self.S["o"], self.nk["o"], stream)
+        Z.ztp_row_linear(c, Z.FWD, self.f_o, stream)          # + all-reduce of Y1
+        Z.ztp_col_linear(c, Z.FWD, self.f_fc1, stream)        # GeLU epilogue, compact rows S_fc2
+        Z.ztp_row_linear(c, Z.FWD, self.f_fc2, stream)        # + all-reduce of Y
+
+    def backward(self, stream=None):
+        c = self.ctx
+        Z.ztp_row_linear(c, Z.BWD, self.b_fc2, stream)        # dH -> G1 = dH * GeLU'(pre), dW2
+        Z.ztp_col_linear(c, Z.BWD, self.b_fc1, stream)        # dY1 (+ all-reduce), dW1
+        Z.ztp_row_linear(c, Z.BWD, self.b_o, stream)          # dctx, dWo
+        Z.ztp_core(c, Z.BWD, self.gQKV, self.dctx, self.a, self.a, None, 0, stream)
+        Z.ztp_col_linear(c, Z.BWD, self.b_qkv, stream)        # dX (+ all-reduce), dWqkv
+
+    def step(self, stream=None, select: bool = True):
+        """One pass of the hot path: (select) + migrate weights + FWD + BWD +
+        return migrated weight gradients."""
+        if select:
+            self.run_select(stream)
+        self.migrate_weights(stream)
+        self.forward(stream)
+        self.backward(stream)
+        self.return_grads(stream)
+
+    # ------------------------------------------------------------ accounting
+    def executed_flops(self) -> float:
+        """6 N n K' per linear (fwd + dX + dW), SURVEY §8(d)."""
+        N, a, h = self.N, self.a, self.h
+        nk = self.nk
+        return 6.0 * N * (3 * a * nk["qkv"] + h * nk["o"] + self.n_fc * nk["fc1"] + h * nk["fc2"])

@@ -27,8 +27,22 @@ def env():
 
 
 def dev(torch, a, dtype=None):
+    """Device copy with the row pitch padded to a multiple of 8 elements (16 B);
+    returns a view of the logical shape (exercises ld != cols)."""
     dtype = dtype or torch.bfloat16
-    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to("cuda").to(dtype)
+    a = np.asarray(a, dtype=np.float32)
+    if a.ndim == 1:
+        return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
+    r, c = a.shape
+    ld = (c + 7) // 8 * 8
+    buf = torch.full((r, ld), float("nan"), device="cuda", dtype=dtype)
+    buf[:, :c] = torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
+    return buf[:, :c]
+
+
+def empty(torch, r, c, dtype):
+    ld = (c + 7) // 8 * 8
+    return torch.full((r, ld), float("nan"), device="cuda", dtype=dtype)[:, :c]
 
 
 def host(t):
@@ -133,9 +147,9 @@ def test_gemm_fwd_dx_dw_parity(env, K, n, N, gamma, dtype):
     td = torch.bfloat16 if dtype == "bf16" else torch.float32
     tol = TOL_BF16 if dtype == "bf16" else TOL_F32
     x, w, g = dev(torch, Xt, td), dev(torch, Wt, td), dev(torch, Gt, td)
-    y = torch.full((n, N), float("nan"), device="cuda", dtype=td)
-    dx = torch.full((K, N), float("nan"), device="cuda", dtype=td)
-    dw = torch.full((K, n), float("nan"), device="cuda", dtype=td)
+    y = empty(torch, n, N, td)
+    dx = empty(torch, K, N, td)
+    dw = empty(torch, K, n, td)
     s, keep = _sel_dev(Z, torch, S, P)
     a = Z.linear_args(x_t=x, w_t=w, y_t=y, g_t=g, dx_t=dx, dw_t=dw, sel_=s)
     Z.ztp_gemm(ctx, Z.KIND_FWD, a)
@@ -165,8 +179,8 @@ def test_gemm_gelu_epilogues(env, dtype):
     td = torch.bfloat16 if dtype == "bf16" else torch.float32
     tol = TOL_BF16 if dtype == "bf16" else TOL_F32
     x, w = dev(torch, Xt, td), dev(torch, Wt, td)
-    pre = torch.empty((n, N), device="cuda", dtype=td)
-    h = torch.empty((n, N), device="cuda", dtype=td)
+    pre = empty(torch, n, N, td)
+    h = empty(torch, n, N, td)
     s, keep = _sel_dev(Z, torch, S, P)
     Z.ztp_gemm(ctx, Z.KIND_FWD, Z.linear_args(x_t=x, w_t=w, y_t=h, pre_t=pre, sel_=s, act=Z.ACT_GELU))
     # GeLU' epilogue on a row-layer dX: dH = W2^T G, G1 = dH * GeLU'(pre_in)
@@ -176,7 +190,7 @@ def test_gemm_gelu_epilogues(env, dtype):
     PreIn = I.normal(8, "pin", K2, N)
     S2, P2 = O.select(I.lognormal_scores(8, "s2", K2), 100)
     s2, keep2 = _sel_dev(Z, torch, S2, P2)
-    g1 = torch.empty((K2, N), device="cuda", dtype=td)
+    g1 = empty(torch, K2, N, td)
     Z.ztp_gemm(ctx, Z.KIND_DX, Z.linear_args(w_t=dev(torch, W2, td), g_t=dev(torch, G2, td), dx_t=g1,
                                              pre_in_t=dev(torch, PreIn, td), sel_=s2, act_in=Z.ACT_GELU))
     Z.ztp_sync(ctx)

@@ -4,8 +4,13 @@ import argparse
 import json
 import math
 
+import os
+import sys
+
 import numpy as np
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2401_11469_b200 as Z
 
