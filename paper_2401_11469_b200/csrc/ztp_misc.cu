@@ -123,12 +123,33 @@ __global__ void ztp_gather_rows(const uint8_t* __restrict__ src, int64_t ld_src,
   }
 }
 
+// Rows whose width is not a multiple of 16 bytes: element-wise copy.
+__global__ void ztp_gather_rows_elem(const uint8_t* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ idx,
+                                     int n, int64_t cols, int64_t es, uint8_t* __restrict__ dst, int64_t ld_dst) {
+  const int64_t total = (int64_t)n * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const int64_t sr = __ldg(idx + r);
+    if (es == 2)
+      reinterpret_cast<uint16_t*>(dst + r * ld_dst)[c] = reinterpret_cast<const uint16_t*>(src + sr * ld_src)[c];
+    else
+      reinterpret_cast<uint32_t*>(dst + r * ld_dst)[c] = reinterpret_cast<const uint32_t*>(src + sr * ld_src)[c];
+  }
+}
+
 cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* idx, int n, int64_t cols, void* dst,
                                int64_t ld_dst, int dtype, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t es = dtype == 0 ? 2 : 4;
   const int64_t row_bytes = cols * es;
-  if (row_bytes % 16) return cudaErrorInvalidValue;
+  if (row_bytes % 16) {
+    const int64_t total = (int64_t)n * cols;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    ztp_gather_rows_elem<<<blocks, 256, 0, st>>>((const uint8_t*)src, ld_src * es, idx, n, cols, es, (uint8_t*)dst,
+                                                 ld_dst * es);
+    return cudaGetLastError();
+  }
   const int64_t total = (int64_t)n * (row_bytes / 16);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;

@@ -211,21 +211,35 @@ class ZtpLayer:
             Z.ztp_migrate(self.ctx, self._xfers(True), stream)
 
     # -------------------------------------------------------------------- step
-    def forward(self, stream=None):
+    def fwd_attn(self, stream=None):
         c = self.ctx
         Z.ztp_col_linear(c, Z.FWD, self.f_qkv, stream)
         Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, self.S["o"], self.nk["o"], stream)
         Z.ztp_row_linear(c, Z.FWD, self.f_o, stream)          # + all-reduce of Y1
+
+    def fwd_mlp(self, stream=None):
+        c = self.ctx
         Z.ztp_col_linear(c, Z.FWD, self.f_fc1, stream)        # GeLU epilogue, compact rows S_fc2
         Z.ztp_row_linear(c, Z.FWD, self.f_fc2, stream)        # + all-reduce of Y
 
-    def backward(self, stream=None):
+    def bwd_mlp(self, stream=None):
         c = self.ctx
         Z.ztp_row_linear(c, Z.BWD, self.b_fc2, stream)        # dH -> G1 = dH * GeLU'(pre), dW2
         Z.ztp_col_linear(c, Z.BWD, self.b_fc1, stream)        # dY1 (+ all-reduce), dW1
+
+    def bwd_attn(self, stream=None):
+        c = self.ctx
         Z.ztp_row_linear(c, Z.BWD, self.b_o, stream)          # dctx, dWo
         Z.ztp_core(c, Z.BWD, self.gQKV, self.dctx, self.a, self.a, None, 0, stream)
         Z.ztp_col_linear(c, Z.BWD, self.b_qkv, stream)        # dX (+ all-reduce), dWqkv
+
+    def forward(self, stream=None):
+        self.fwd_attn(stream)
+        self.fwd_mlp(stream)
+
+    def backward(self, stream=None):
+        self.bwd_mlp(stream)
+        self.bwd_attn(stream)
 
     def step(self, stream=None, select: bool = True):
         """One pass of the hot path: (select) + migrate weights + FWD + BWD +

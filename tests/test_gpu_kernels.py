@@ -16,12 +16,17 @@ TOL_BF16 = 2e-2
 TOL_F32 = 1e-5
 
 
-@pytest.fixture(scope="module")
-def env():
+@pytest.fixture(scope="module", params=["compact", "gather4"])
+def env(request):
+    """Both producer modes: compact operand copies + dense TMA boxes (default)
+    and in-GEMM TMA gather4 of the lineage rows (ZTP_GATHER4=1)."""
+    import os
     import torch
     import paper_2401_11469_b200 as Z
     assert torch.cuda.is_available(), "GPU tests need a B200"
+    os.environ["ZTP_GATHER4"] = "1" if request.param == "gather4" else "0"
     ctx = Z.ztp_ctx_create(0, 1, None, 0)
+    os.environ.pop("ZTP_GATHER4")
     yield Z, torch, ctx
     Z.ztp_ctx_destroy(ctx)
 

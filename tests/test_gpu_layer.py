@@ -1,0 +1,203 @@
+"""GPU parity of the whole TP layer step (attention-projection block + MLP
+block, fwd + bwd) through the C ABI against the oracle's layer_step, on the
+same seeded inputs: ZERO-resizing at several ratios, Zero imputation, the
+producer-side compaction path, and SEMI migration (hidden units appended on
+helpers).  Multi-rank runs are simulated on one GPU with one context per rank;
+the test itself sums the partials where NCCL would (test plumbing only)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ztp_oracle as O
+from synth import inputs as I
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def make_inputs(h, f, N, e, seed):
+    Wq, Wk, Wv, Wo = (I.uniform_sym(seed, n, h, h, 1 / math.sqrt(h)) for n in ("wq", "wk", "wv", "wo"))
+    W1 = I.uniform_sym(seed, "w1", h, f, 1 / math.sqrt(h))
+    W2 = I.uniform_sym(seed, "w2", f, h, 1 / math.sqrt(f))
+    X = I.normal(seed, "x", h, N)
+    G = I.normal(seed, "g", h, N)
+    return X, G, O.shard_layer(Wq, Wk, Wv, Wo, W1, W2, e)
+
+
+def to_dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda().to(torch.bfloat16)
+
+
+def host(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def close(got, ref, name):
+    sc = max(np.max(np.abs(ref)), 1e-30)
+    err = np.max(np.abs(got - ref)) / sc
+    assert np.isfinite(got).all() and err <= TOL, f"{name}: max|err|/||ref||inf = {err:.3e}"
+
+
+def selections(e, h, f, N, seed, gam, own_fc2=None):
+    """Oracle-side selections from the same seeded scores the device gets."""
+    a, u = h // e, f // e
+    sel, scores, nps = [], [], []
+    for r in range(e):
+        lens = {"qkv": h, "o": a, "fc1": h, "fc2": (own_fc2[r] if own_fc2 else u)}
+        d, sc, npr = {}, {}, {}
+        for s, L in lens.items():
+            sc[s] = I.lognormal_scores(seed, f"score.{s}", L, rank=r)
+            npr[s] = min(int(math.floor(L * gam[r][s] + 0.5)), L - 1)
+            d[s] = O.select(sc[s], npr[s])
+        sel.append(d)
+        scores.append(sc)
+        nps.append(npr)
+    return sel, scores, nps
+
+
+@pytest.fixture(scope="module")
+def tz():
+    import torch
+    import paper_2401_11469_b200 as Z
+    from paper_2401_11469_b200.layer import ZtpLayer, MigrationIO
+    assert torch.cuda.is_available()
+    return torch, Z, ZtpLayer, MigrationIO
+
+
+def build(tz, sh, r, e, h, f, N, cap=0):
+    torch, Z, ZtpLayer, _ = tz
+    ctx = Z.ztp_ctx_create(0, 1, None, 0)
+    L = ZtpLayer(ctx, h, f, N, r, e, {"qkv": to_dev(torch, sh.qkv_t[r]), "o": to_dev(torch, sh.o_t[r]),
+                                      "w1": to_dev(torch, sh.w1_t[r]), "w2": to_dev(torch, sh.w2_t[r])},
+                 mig_cap=cap)
+    return ctx, L
+
+
+@pytest.mark.parametrize("h,f,N,g", [(256, 1024, 328, (0.5, 0.3, 0.5, 0.4)),
+                                     (128, 512, 256, (0.0, 0.0, 0.0, 0.0)),
+                                     (192, 768, 520, (0.9, 0.25, 0.1, 0.75))])
+def test_layer_world1_real_context(tz, h, f, N, g):
+    """TP = 1 through the real single-rank context (collectives are no-ops)."""
+    torch, Z, ZtpLayer, _ = tz
+    seed = 99 + h
+    X, G, sh = make_inputs(h, f, N, 1, seed)
+    gam = [dict(zip(("qkv", "o", "fc1", "fc2"), g))]
+    sel, scores, nps = selections(1, h, f, N, seed, gam)
+    ref = O.layer_step(X, G, sh, sel)
+    ctx, L = build(tz, sh, 0, 1, h, f, N)
+    L.set_selection(nps[0], {s: torch.from_numpy(v).cuda() for s, v in scores[0].items()})
+    L.X.copy_(to_dev(torch, X))
+    L.G.copy_(to_dev(torch, G))
+    L.step(select=True)
+    Z.ztp_sync(ctx)
+    close(host(L.Y), ref["Y"], "Y")
+    close(host(L.dX), ref["dX"], "dX")
+    close(host(L.dqkv), ref["dWqkv"][0], "dWqkv")
+    close(host(L.do), ref["dWo"][0], "dWo")
+    close(host(L.dw1[:, :f]), ref["dW1"][0], "dW1")
+    close(host(L.dw2[:f]), ref["dW2"][0], "dW2")
+    for seg, t in (("qkv", L.dqkv), ("o", L.do), ("fc1", L.dw1), ("fc2", L.dw2)):
+        P = sel[0][seg][1]
+        if len(P):
+            assert torch.all(t[torch.tensor(P, device="cuda")] == 0)          # Zero imputation
+    # executed FLOPs accounting matches the oracle's audit
+    assert L.executed_flops() == pytest.approx(ref["flops"][0], rel=1e-12)
+    Z.ztp_ctx_destroy(ctx)
+
+
+def _simulate(tz, e, h, f, N, gam, mig=None, seed=7):
+    """e ranks on one GPU; the test sums partials where NCCL all-reduces."""
+    torch, Z, ZtpLayer, MigrationIO = tz
+    u = f // e
+    X, G, sh = make_inputs(h, f, N, e, seed)
+    mig = mig or []
+    own = [u] * e
+    inc = {r: [] for r in range(e)}
+    for (s, r, lo, hi) in mig:
+        own[s] = min(own[s], lo)
+        inc[r].append((s, lo, hi))
+    sel, scores, nps = selections(e, h, f, N, seed, gam, own_fc2=own)
+    ref = O.layer_step(X, G, sh, sel, mig)
+    cap = max([sum(hi - lo for (_, lo, hi) in inc[r]) for r in range(e)] + [0])
+    ranks = [build(tz, sh, r, e, h, f, N, cap) for r in range(e)]
+    offs = {}
+    for r, (ctx, L) in enumerate(ranks):
+        off = 0
+        for (s, lo, hi) in inc[r]:
+            offs[(s, r, lo)] = off
+            off += hi - lo
+        L.set_migration(MigrationIO(n_mig=u - own[r], inc=inc[r]))
+        L.set_selection(nps[r], {s: torch.from_numpy(v).cuda() for s, v in scores[r].items()})
+        L.X.copy_(to_dev(torch, X))
+        L.G.copy_(to_dev(torch, G))
+    # weight migration (ztp_migrate's job on a multi-GPU box)
+    for (s, r, lo, hi) in mig:
+        Ls, Lr = ranks[s][1], ranks[r][1]
+        o = u + offs[(s, r, lo)]
+        Lr.w1_t[:, o:o + hi - lo].copy_(Ls.w1_t[:, lo:hi])
+        Lr.w2_t[o:o + hi - lo].copy_(Ls.w2_t[lo:hi])
+
+    def allreduce(name):
+        tot = sum(getattr(L, name).float() for _, L in ranks)
+        for _, L in ranks:
+            getattr(L, name).copy_(tot.to(torch.bfloat16))
+    for _, L in ranks:
+        L.fwd_attn()
+    allreduce("Y1")
+    for _, L in ranks:
+        L.fwd_mlp()
+    allreduce("Y")
+    for _, L in ranks:
+        L.bwd_mlp()
+    allreduce("dY1")
+    for _, L in ranks:
+        L.bwd_attn()
+    allreduce("dX")
+    for (s, r, lo, hi) in mig:     # dW slices back to the owner
+        Ls, Lr = ranks[s][1], ranks[r][1]
+        o = u + offs[(s, r, lo)]
+        Ls.dw1[:, lo:hi].copy_(Lr.dw1[:, o:o + hi - lo])
+        Ls.dw2[lo:hi].copy_(Lr.dw2[o:o + hi - lo])
+    torch.cuda.synchronize()
+    L0 = ranks[0][1]
+    close(host(L0.Y), ref["Y"], "Y")
+    close(host(L0.dX), ref["dX"], "dX")
+    for r, (ctx, L) in enumerate(ranks):
+        close(host(L.dqkv), ref["dWqkv"][r], f"dWqkv[{r}]")
+        close(host(L.do), ref["dWo"][r], f"dWo[{r}]")
+        close(host(L.dw1[:, :u]), ref["dW1"][r], f"dW1[{r}]")
+        close(host(L.dw2[:u]), ref["dW2"][r], f"dW2[{r}]")
+        assert L.executed_flops() == pytest.approx(ref["flops"][r], rel=1e-12)
+        Z.ztp_ctx_destroy(ctx)
+
+
+def test_layer_tp2_straggler_resized(tz):
+    """c1-like: TP=2, rank 1 resized at gamma = 0.25 (Zero imputation)."""
+    g0 = dict(qkv=0.0, o=0.0, fc1=0.0, fc2=0.0)
+    g1 = dict(qkv=0.25, o=0.25, fc1=0.25, fc2=0.25)
+    _simulate(tz, 2, 128, 512, 264, [g0, g1])
+
+
+def test_layer_tp4_semi_migration(tz):
+    """TP=4, straggler 3 sheds its tail units to helpers ranked by
+    r' = (r - 3 + 4) % 4 and resizes the rest."""
+    e, h, f = 4, 256, 1024
+    u = f // e
+    g = [dict(qkv=0.0, o=0.0, fc1=0.0, fc2=0.0) for _ in range(e)]
+    g[3] = dict(qkv=0.5, o=0.5, fc1=0.3, fc2=0.3)
+    n_mig = 96
+    lo = u - n_mig
+    mig = [(3, 0, lo, lo + 32), (3, 1, lo + 32, lo + 64), (3, 2, lo + 64, lo + 96)]
+    _simulate(tz, e, h, f, 328, g, mig)
+
+
+def test_layer_tp4_migration_receiver_resizes(tz):
+    """Multi-straggler plan: a resize-group straggler (rank 1) also receives
+    migrated units (A-22) and prunes them along K with its own S_c (A-33)."""
+    e, h, f = 4, 128, 512
+    u = f // e
+    g = [dict(qkv=0.0, o=0.0, fc1=0.0, fc2=0.0) for _ in range(e)]
+    g[1] = dict(qkv=0.25, o=0.25, fc1=0.4, fc2=0.25)
+    mig = [(0, 1, u - 40, u - 16), (0, 2, u - 16, u - 8), (0, 3, u - 8, u)]
+    _simulate(tz, e, h, f, 136, g, mig)
