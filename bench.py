@@ -1,0 +1,435 @@
+"""bench.py -- resized-TP layer step on B200 (BASELINE.json metric).
+
+python bench.py --gpus N --steps K --warmup W [--impl ztp|reference]
+(N > 1: launched by torchrun, one rank per GPU, NCCL over NVLink.)
+
+Workload (BASELINE.json configs[1]): one GPT-2-medium layer
+(h=1024, 16 heads, ffn=4096, seq 1024 x batch 8 = 8192 tokens): attention-
+projection block + MLP block, fwd + bwd, 1D TP over N ranks.
+  N = 1: homogeneous ZERO-Pri resizing at gamma = 0.5 on every linear (the
+         paper's homogeneous evaluation point) vs the dense step.
+  N > 1: rank N-1 emulates a 2x straggler: T_free (chi=1, dense) ->
+         T_unbal (chi=2, dense; statistics window -> T_i, M_i) -> ztp_plan
+         (Eq.1, T_min criterion, A-7) -> ztp_select -> T_bal (timed headline).
+A step = select + FWD + BWD of the layer through the C ABI (every kernel is
+libztp's; collectives are NCCL).  value = executed GEMM TFLOP/s of the whole
+job (sum over ranks of 6 N n K' per linear / step time, max over ranks).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "resized-TP layer step ms & TFLOP/s at TP=1/2/4/8 w/ 2× straggler; % of roofline"
+NVLINK_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), d.get("hbm_gbs", 6650.0), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        cmd = ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
+               "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        while not self._stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append(parts)
+        p.kill()
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
+        load = [s for s in self.samples if s[6].isdigit() and int(s[6]) > 0] or self.samples
+        sm = [float(s[0]) for s in load if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in load if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in load for i in range(4) if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(load)}
+
+
+# ------------------------------------------------------------ inputs (synth)
+def rank_shards(cfg, e, r):
+    """This rank's shards of the seeded dense layer weights (synth blocks)."""
+    from synth import inputs as I
+    h, f, seed = cfg.h, cfg.f, cfg.seed
+    a, u = h // e, f // e
+    F0, F1 = r * a, (r + 1) * a
+    U0, U1 = r * u, (r + 1) * u
+    bq = 1 / math.sqrt(h)
+    qkv = np.concatenate([I.uniform_sym(seed, n, h, h, bq, c0=F0, c1=F1) for n in ("wq", "wk", "wv")], axis=1)
+    o = I.uniform_sym(seed, "wo", h, h, bq, r0=F0, r1=F1)
+    w1 = I.uniform_sym(seed, "w1", h, f, bq, c0=U0, c1=U1)
+    w2 = I.uniform_sym(seed, "w2", f, h, 1 / math.sqrt(f), r0=U0, r1=U1)
+    return {"qkv": qkv, "o": o, "w1": w1, "w2": w2}
+
+
+def scores_for(cfg, r, lens):
+    from synth import inputs as I
+    return {s: I.lognormal_scores(cfg.seed, f"score.{s}", L, rank=r) for s, L in lens.items()}
+
+
+# ------------------------------------------------------------ distributed
+class Dist:
+    def __init__(self, n_gpus: int):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != n_gpus:
+            raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={self.world} (launch N>1 with torchrun)")
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+
+    def barrier(self):
+        if self.world > 1:
+            t = self.torch.ones(1, device="cuda")
+            self.dist.all_reduce(t)
+        self.torch.cuda.synchronize()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], device="cuda", dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], device="cuda", dtype=self.torch.float64)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes | None) -> bytes:
+        if self.world == 1:
+            return b
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+
+def timed(D, fn, steps: int, stream) -> float:
+    """Device time of `steps` calls of fn (CUDA events on the launching stream,
+    barrier + synchronize on both sides), max over ranks, ms per step."""
+    torch = D.torch
+    D.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    D.barrier()
+    return D.max(e0.elapsed_time(e1)) / steps
+
+
+# ------------------------------------------------------------- oracle legs
+_ORACLE_INPUTS = {}
+
+
+def oracle_inputs(cfg, gamma: float, tokens: int):
+    """Seeded inputs of the sampled workload, prepared once (not timed)."""
+    key = (cfg.name, gamma, tokens)
+    if key not in _ORACLE_INPUTS:
+        from oracle import ztp_oracle as O
+        from synth import inputs as I
+        h, f = cfg.h, cfg.f
+        d = rank_shards(cfg, 1, 0)
+        sh = O.LayerShards([d["qkv"]], [d["o"]], [d["w1"]], [d["w2"]])
+        X = I.normal(cfg.seed, "x", h, cfg.N, c1=tokens)
+        G = I.normal(cfg.seed, "g", h, cfg.N, c1=tokens)
+        lens = {"qkv": h, "o": h, "fc1": h, "fc2": f}
+        sc = scores_for(cfg, 0, lens)
+        _ORACLE_INPUTS[key] = (X, G, sh, lens, sc)
+    return _ORACLE_INPUTS[key]
+
+
+def oracle_sample(cfg, gamma: float, tokens: int, budget_s: float):
+    """The fp64 oracle (as it stands) on a token sample of the same workload --
+    select + layer step per run; returns (TFLOP/s, seconds, runs, FLOPs per
+    run).  Baseline leg only."""
+    from oracle import ztp_oracle as O
+    X, G, sh, lens, sc = oracle_inputs(cfg, gamma, tokens)
+    t0 = time.perf_counter()
+    flops, runs = 0.0, 0
+    while True:
+        sel = [{s: O.select(sc[s], min(int(math.floor(L * gamma + 0.5)), L - 1)) for s, L in lens.items()}]
+        out = O.layer_step(X, G, sh, sel)
+        flops += sum(out["flops"])
+        runs += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return flops / dt / 1e12, dt, runs, flops / runs
+
+
+def reference_arm(args):
+    """--impl reference: the oracle on the box's host cores, rank 0 only; each
+    step is the layer step on a bounded token sample of the same workload."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    from synth.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    tokens = args.ref_tokens
+    for _ in range(args.warmup):
+        oracle_sample(cfg, args.gamma, tokens, 0.0)
+    t0 = time.perf_counter()
+    fl = 0.0
+    for _ in range(args.steps):
+        _, _, _, f1 = oracle_sample(cfg, args.gamma, tokens, 0.0)
+        fl += f1
+    total = time.perf_counter() - t0
+    value = fl / total / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded splitmix64, bf16-rounded values)",
+            "config": {"workload": f"{cfg.note}: 1 transformer layer fwd+bwd, TP=1, gamma={args.gamma} "
+                                   f"(fp64 oracle on {tokens} of {cfg.N} tokens per step)",
+                       "tokens_per_step": tokens},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": f"fp64 numpy oracle layer_step, {tokens} tokens x {args.steps} steps"},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ztp", choices=["ztp", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--gamma", type=float, default=0.5, help="N=1 homogeneous prune ratio")
+    ap.add_argument("--chi", type=float, default=2.0, help="straggler slowdown (N>1)")
+    ap.add_argument("--ref-tokens", type=int, default=256)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import paper_2401_11469_b200 as Z
+    from paper_2401_11469_b200.layer import ZtpLayer, SEGS
+    from synth.configs import CONFIGS
+    from synth import inputs as I
+
+    D = Dist(args.gpus)
+    e, r = D.world, D.rank
+    cfg = CONFIGS[args.config]
+    h, f, N = cfg.h, cfg.f, cfg.N
+    a, u = h // e, f // e
+    peak_burst, peak_sus, hbm, peak_src = load_peaks()
+    sampler = ClockSampler(D.local)
+    sampler.start()
+
+    uid = Z.ztp_get_unique_id() if (e > 1 and r == 0) else None
+    uid = D.bcast_bytes(uid)
+    ctx = Z.ztp_ctx_create(r, e, uid, D.local)
+    sh = rank_shards(cfg, e, r)
+    dev = {k: torch.from_numpy(v.astype(np.float32)).cuda().to(torch.bfloat16) for k, v in sh.items()}
+    L = ZtpLayer(ctx, h, f, N, r, e, dev)
+    Xh = I.normal(cfg.seed, "x", h, N)
+    Gh = I.normal(cfg.seed, "g", h, N)
+    L.X.copy_(torch.from_numpy(Xh.astype(np.float32)).cuda().to(torch.bfloat16))
+    L.G.copy_(torch.from_numpy(Gh.astype(np.float32)).cuda().to(torch.bfloat16))
+    lens = {"qkv": h, "o": a, "fc1": h, "fc2": u}
+    sc = {s: torch.from_numpy(v).cuda() for s, v in scores_for(cfg, r, lens).items()}
+    stream = torch.cuda.current_stream()
+    step = lambda: L.step(stream)   # noqa: E731
+
+    def run_phase(steps, warm):
+        for _ in range(warm):
+            step()
+        return timed(D, step, steps, stream)
+
+    # ---- phase A: straggler-free dense step (T_free)
+    L.set_selection({s: 0 for s in SEGS}, sc)
+    ms_free = run_phase(args.steps, args.warmup)
+    flops_dense = D.sum(L.executed_flops())
+
+    plan_info = {}
+    ms_unbal = None
+    if e > 1:
+        # ---- phase B: unbalanced (chi on the last rank), statistics window
+        strag = e - 1
+        Z.ztp_set_slowdown(ctx, args.chi if r == strag else 1.0)
+        Z.ztp_set_stats(ctx, True)
+        for _ in range(args.warmup):
+            step()
+        Z.ztp_read_profile(ctx, stream)
+        Z.ztp_set_profile(ctx, True)
+        win = 10
+        for _ in range(win):
+            step()
+        prof = Z.ztp_read_profile(ctx, stream)
+        Z.ztp_set_profile(ctx, False)
+        Z.ztp_set_stats(ctx, False)
+        T_own = (prof["gemm_ms"] + prof["other_ms"]) / win
+        M_own = prof["gemm_ms"] / win
+        ms_unbal = run_phase(args.steps, 0)
+        T_all, M_all = Z.ztp_allgather_stats(ctx, T_own, M_own, e, stream)
+        plan = Z.ztp_plan(T_all, M_all, float(h), None, Z.plan_opts(enable_migration=0, zero_crit=Z.CRIT_MIN))
+        n_prune = {}
+        for s, K, is_row in (("qkv", h, False), ("o", a, True), ("fc1", h, False), ("fc2", u, True)):
+            n_prune[s] = Z.ztp_plan_counts(plan, r, K, u, 1, is_row).n_prune
+        plan_info = {"T_ms": T_all, "M_ms": M_all, "gamma": list(plan.gamma)[:e], "role": list(plan.role)[:e],
+                     "z": plan.z, "criterion": "T_min (A-7)"}
+    else:
+        # N = 1: homogeneous resize at gamma (P:344 E2 analog); counts by the library
+        p = Z.PlanT()
+        p.world = 1
+        p.role[0] = Z.RESIZE
+        p.gamma[0] = p.gamma_r[0] = args.gamma
+        n_prune = {s: Z.ztp_plan_counts(p, 0, K, u, 1, s in ("o", "fc2")).n_prune
+                   for s, K in (("qkv", h), ("o", a), ("fc1", h), ("fc2", u))}
+        plan_info = {"gamma": [args.gamma], "mode": "homogeneous ZERO-Pri"}
+    L.set_selection(n_prune, sc)
+
+    # ---- phase C: balanced / resized step (headline), profiled
+    for _ in range(args.warmup):
+        step()
+    Z.ztp_read_profile(ctx, stream)
+    Z.ztp_set_profile(ctx, True)
+    n0 = Z.ztp_launch_count(ctx)
+    ms_bal = timed(D, step, args.steps, stream)
+    launches = Z.ztp_launch_count(ctx) - n0
+    prof = Z.ztp_read_profile(ctx, stream)
+    Z.ztp_set_profile(ctx, False)
+    flops_exec = D.sum(L.executed_flops())
+    value = flops_exec / (ms_bal * 1e-3) / 1e12
+
+    # ---- e2e: host buffers through the public API (pinned H2D of X, G; D2H of dX)
+    Xp = torch.empty((h, N), dtype=torch.bfloat16).pin_memory()
+    Gp = torch.empty((h, N), dtype=torch.bfloat16).pin_memory()
+    Xp.copy_(L.X.cpu())
+    Gp.copy_(L.G.cpu())
+    dXp = torch.empty((h, N), dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        L.X.copy_(Xp, non_blocking=True)
+        L.G.copy_(Gp, non_blocking=True)
+        L.step(stream)
+        dXp.copy_(L.dX, non_blocking=True)
+    for _ in range(3):
+        e2e_step()
+    e2e_steps = max(10, args.steps // 4)
+    ms_e2e = timed(D, e2e_step, e2e_steps, stream)
+    clocks = sampler.stop()
+
+    # ---- roofline of the dominant kernel (the resized tcgen05 GEMM)
+    gemm_ms = prof["gemm_ms"]
+    achieved = prof["gemm_flops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    timed_s = ms_bal * args.steps * 1e-3
+    peak = peak_sus if timed_s >= 1.0 else peak_burst
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "tensor", "kernel": "ztp_gemm_kernel (tcgen05 kind::f16, TMEM accum)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "peak_source": f"{peak_src} {'sustained' if peak is peak_sus else 'burst'} bf16 (MEASURED_PEAKS.json)",
+            "gemm_share_of_step": (gemm_ms / args.steps) / ms_bal if ms_bal else None,
+            "n_gemm_launches": prof["n_gemm"]}
+    # step roofline: max(GEMM at peak, collective bytes at NVLink) per rank
+    per_rank_flops = L.executed_flops()
+    comm_bytes = 4 * 2 * N * h * 2 * (e - 1) / e if e > 1 else 0.0   # 4 all-reduces, ring bus bytes
+    t_ideal = max(per_rank_flops / (peak_burst * 1e12), comm_bytes / (NVLINK_GBS * 1e9))
+    cpu = None
+    if r == 0 and e == 1 and not args.no_cpu:
+        v, dt, runs, _ = oracle_sample(cfg, args.gamma, 512, args.cpu_budget)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"fp64 numpy oracle layer_step (TP=1, gamma={args.gamma}) on 512 of {N} tokens, "
+                         f"{runs} runs in {dt:.1f} s"}
+    h2d = 2 * h * N * 2
+    d2h = h * N * 2
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": e, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_bal, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 inputs, random-init weights)",
+        "config": {"workload": f"{cfg.note}: 1 transformer layer (attn-proj + MLP) fwd+bwd, TP={e}",
+                   "tp": e, "tokens": N, "hidden": h, "ffn": f,
+                   "mode": ("homogeneous ZERO-Pri gamma=%.2f" % args.gamma) if e == 1 else
+                           f"rank {e - 1} slowed {args.chi}x, ZERO-resizing (T_min)",
+                   "l2": "no flush: per-step working set > 126 MB L2 (activations ~%d MB)" %
+                         int((2 * h * N * 2 * 6 + 2 * (f // e) * N * 2 * 2) / 1e6)},
+        "e2e": {"value": flops_exec / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "step_roofline": {"ideal_ms": t_ideal * 1e3, "frac": (t_ideal * 1e3) / ms_bal,
+                          "rule": "max(rank GEMM FLOPs / burst peak, all-reduce ring bytes / 770 GB/s)"},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "ms_dense_free": ms_free, "dense_tflops": flops_dense / (ms_free * 1e-3) / 1e12,
+        "plan": plan_info,
+    }
+    if e > 1:
+        line["ms_unbal"] = ms_unbal
+        line["recovery"] = ms_free / ms_bal
+        line["speedup"] = ms_unbal / ms_bal
+    else:
+        line["speedup_vs_dense"] = ms_free / ms_bal
+    if r == 0:
+        print(json.dumps(line), flush=True)
+    Z.ztp_ctx_destroy(ctx)
+    if e > 1:
+        D.dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

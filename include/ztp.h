@@ -320,6 +320,22 @@ ztp_status ztp_set_slowdown(ztp_ctx* ctx, double chi);
 ztp_status ztp_set_stats(ztp_ctx* ctx, int on);
 ztp_status ztp_read_gemm_ns(ztp_ctx* ctx, void* stream, double* ns);
 
+/* Profiling with CUDA events recorded on the launching stream around every
+ * kernel class this context issues (on = 1).  ztp_read_profile syncs `stream`,
+ * returns the totals since the last read and resets them:
+ *   gemm_ms     resized GEMM kernels (+ the emulated-slowdown delay after each)
+ *   other_ms    select, row compaction, stand-in core
+ *   comm_ms     collectives (NCCL) as seen on their stream
+ *   gemm_flops  algorithmic FLOPs of the GEMMs: 2 n_kept n_out N per launch
+ * T_i (A-5) = gemm_ms + other_ms (busy time, collective waits excluded) and
+ * M_i (A-6) = gemm_ms of the statistics window. */
+typedef struct ztp_profile {
+  double gemm_ms, other_ms, comm_ms, gemm_flops;
+  int64_t n_gemm, n_other, n_comm;
+} ztp_profile;
+ztp_status ztp_set_profile(ztp_ctx* ctx, int on);
+ztp_status ztp_read_profile(ztp_ctx* ctx, void* stream, ztp_profile* out);
+
 /* Raw resized GEMM (test / benchmark entry; the linears use it internally).
  * kind 0 = FWD (y = w[S]^T x[S]), 1 = dX (dx rows by sel), 2 = dW. */
 ztp_status ztp_gemm(ztp_ctx* ctx, int kind, const ztp_linear_args* a, void* stream);

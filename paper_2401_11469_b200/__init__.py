@@ -201,6 +201,16 @@ def ztp_set_stats(ctx, on: bool) -> None:
     check(lib.ztp_set_stats(ctx, int(on)), ctx)
 
 
+def ztp_set_profile(ctx, on: bool) -> None:
+    check(lib.ztp_set_profile(ctx, int(on)), ctx)
+
+
+def ztp_read_profile(ctx, stream=None) -> dict:
+    p = _lib.Profile()
+    check(lib.ztp_read_profile(ctx, _stream(stream), C.byref(p)), ctx)
+    return {k: getattr(p, k) for k, _ in _lib.Profile._fields_}
+
+
 def ztp_read_gemm_ns(ctx, stream=None) -> float:
     v = C.c_double()
     check(lib.ztp_read_gemm_ns(ctx, _stream(stream), C.byref(v)), ctx)

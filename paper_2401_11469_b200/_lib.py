@@ -78,6 +78,11 @@ class LinearArgs(C.Structure):
                 ("hist_dx", C.POINTER(Mat)), ("hist_dw", C.POINTER(Mat))]
 
 
+class Profile(C.Structure):
+    _fields_ = [("gemm_ms", C.c_double), ("other_ms", C.c_double), ("comm_ms", C.c_double),
+                ("gemm_flops", C.c_double), ("n_gemm", C.c_int64), ("n_other", C.c_int64), ("n_comm", C.c_int64)]
+
+
 class Xfer(C.Structure):
     _fields_ = [("src", Mat), ("dst", Mat), ("r0", C.c_int64), ("c0", C.c_int64), ("nr", C.c_int64),
                 ("nc", C.c_int64), ("dr0", C.c_int64), ("dc0", C.c_int64), ("src_rank", C.c_int32),
@@ -117,6 +122,8 @@ def _load():
         "ztp_set_stats": (st, [vp, C.c_int]),
         "ztp_read_gemm_ns": (st, [vp, vp, C.POINTER(C.c_double)]),
         "ztp_gemm": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
+        "ztp_set_profile": (st, [vp, C.c_int]),
+        "ztp_read_profile": (st, [vp, vp, C.POINTER(Profile)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -131,7 +138,8 @@ lib = _load()
 EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_id", "ztp_ctx_create",
             "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count", "ztp_plan_opts_default", "ztp_plan",
             "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
-            "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm")
+            "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm",
+            "ztp_set_profile", "ztp_read_profile")
 
 
 def check(code: int, ctx=None):

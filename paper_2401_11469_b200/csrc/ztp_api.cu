@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -47,7 +48,40 @@ struct ztp_ctx {
   void* cws[2] = {nullptr, nullptr};   // compact-operand workspaces (x, w)
   size_t cws_cap[2] = {0, 0};
   int use_gather4 = 0;                 // 1: gather rows in the GEMM producer with TMA gather4
+  int allow_splitk = 1;                // split-K for few-tile GEMMs (ZTP_SPLITK=0 disables)
+  void* skws = nullptr;                // split-K fp32 partials
+  size_t skws_cap = 0;
+  // profiling (ztp_set_profile): event pairs around every kernel class
+  struct ProfEv {
+    cudaEvent_t a, b;
+    int cat;
+    double flops;
+  };
+  int prof_on = 0;
+  std::vector<ProfEv> prof;
+  size_t prof_used = 0;
 };
+
+enum { PROF_GEMM = 0, PROF_OTHER = 1, PROF_COMM = 2 };
+
+namespace {
+int prof_begin(ztp_ctx* c, cudaStream_t st, int cat, double flops) {
+  if (!c->prof_on) return -1;
+  if (c->prof_used == c->prof.size()) {
+    ztp_ctx::ProfEv e{};
+    if (cudaEventCreate(&e.a) != cudaSuccess || cudaEventCreate(&e.b) != cudaSuccess) return -1;
+    c->prof.push_back(e);
+  }
+  const int i = (int)c->prof_used++;
+  c->prof[i].cat = cat;
+  c->prof[i].flops = flops;
+  cudaEventRecord(c->prof[i].a, st);
+  return i;
+}
+void prof_end(ztp_ctx* c, int i, cudaStream_t st) {
+  if (i >= 0) cudaEventRecord(c->prof[i].b, st);
+}
+}  // namespace
 
 namespace {
 
@@ -185,6 +219,8 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     N = (int)n_out;
     kdim = (int)a.cols;
   }
+  const double tokens = (double)(kind == ztp::KIND_DW ? a.cols : b.cols);
+  const int pe = prof_begin(c, st, PROF_GEMM, 2.0 * (double)nk * (double)n_out * tokens);
   if (dtype == ZTP_BF16) {
     ztp::GemmOperands o{};
     o.a = a.ptr;
@@ -220,6 +256,27 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     p.aux_by_m = aux_by_m;
     p.out_pos = out_pos;
     p.stamp = emulating(c) ? c->d_stamp : nullptr;
+    // split-K over the contraction when the output has too few tiles for 148 SMs
+    p.splits = c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, c->num_sms) : 1;
+    if (p.splits > 1) {
+      const int num_kb = (kdim + 63) / 64;
+      p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
+      p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
+      const size_t bytes = ztp::gemm_ws_bytes(kind, M, N, nk, p.splits);
+      if (c->skws_cap < bytes) {
+        if (c->skws) cudaFree(c->skws);
+        c->skws = nullptr;
+        c->skws_cap = 0;
+        CUDA_TRY(c, cudaMalloc(&c->skws, bytes));
+        c->skws_cap = bytes;
+      }
+      p.ws = (float*)c->skws;
+      p.ld_ws = (N + 7) / 8 * 8;
+      p.ws_split_stride = (int64_t)(kind == ztp::KIND_FWD ? M : std::min(M, nk)) * p.ld_ws;
+    } else {
+      p.splits = 1;
+      p.kb_per_split = (kdim + 63) / 64;
+    }
     CUDA_TRY(c, ztp::gemm_launch(kind, o, p, c->num_sms, st));
   } else {
     ztp::GemmParamsF32 p{};
@@ -262,13 +319,17 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     CUDA_TRY(c, ztp::gemm_f32_launch(p, st));
   }
   ++c->launches;
-  return after_gemm(c, st);
+  const ztp_status s = after_gemm(c, st);
+  prof_end(c, pe, st);
+  return s;
 }
 
 ztp_status allreduce(ztp_ctx* c, const ztp_mat& m, cudaStream_t st) {
   if (c->world == 1) return ZTP_OK;
   if (m.ld != m.cols) return fail(c, ZTP_ESHAPE, "all-reduce needs a contiguous tensor: " + shp("t", m));
+  const int pe = prof_begin(c, st, PROF_COMM, 0.0);
   NCCL_TRY(c, ncclAllReduce(m.ptr, m.ptr, (size_t)(m.rows * m.cols), nccl_type(m.dtype), ncclSum, c->comm, st));
+  prof_end(c, pe, st);
   return ZTP_OK;
 }
 
@@ -292,7 +353,9 @@ ztp_status compact_rows(ztp_ctx* c, const ztp_mat& full, const int32_t* kept, in
   }
   if (!mat_ok(d) || d.rows < nk || d.cols < full.cols || d.dtype != full.dtype)
     return fail(c, ZTP_ESHAPE, "compact buffer " + shp("dst", d) + " too small for " + shp("src", full));
+  const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
   CUDA_TRY(c, ztp::gather_rows_launch(full.ptr, full.ld, kept, nk, full.cols, d.ptr, d.ld, full.dtype, st));
+  prof_end(c, pe, st);
   ++c->launches;
   d.rows = nk;
   d.cols = full.cols;
@@ -489,6 +552,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
   if (const char* g4 = getenv("ZTP_GATHER4")) c->use_gather4 = atoi(g4) != 0;
+  if (const char* sk = getenv("ZTP_SPLITK")) c->allow_splitk = atoi(sk) != 0;
   auto cleanup = [&](ztp_status s) {
     ztp_ctx_destroy(c);
     return s;
@@ -528,8 +592,13 @@ ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   cudaFree(c->d_stats);
   cudaFree(c->d_iota);
   cudaFree(c->ws);
+  cudaFree(c->skws);
   cudaFree(c->cws[0]);
   cudaFree(c->cws[1]);
+  for (auto& e : c->prof) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
   delete c;
   return ZTP_OK;
 }
@@ -594,7 +663,9 @@ ztp_status ztp_select(ztp_ctx* c, int nseg, const int32_t* h_len, const int32_t*
     ztp::SelectParams p{};
     p.nseg = std::min(ztp::SELECT_MAX_SEGS, nseg - b);
     for (int i = 0; i < p.nseg; ++i) p.seg[i] = segs[b + i];
+    const int pe = prof_begin(c, (cudaStream_t)stream, PROF_OTHER, 0.0);
     CUDA_TRY(c, ztp::select_launch(p, d_scores, d_kept, d_pruned, d_pos, c->d_flags, (cudaStream_t)stream));
+    prof_end(c, pe, (cudaStream_t)stream);
     ++c->launches;
   }
   return ZTP_OK;
@@ -652,8 +723,10 @@ ztp_status ztp_core(ztp_ctx* c, ztp_phase phase, const ztp_mat* qkv, const ztp_m
       (rows && (n_rows < 1 || n_rows > n_feat)))
     return fail(c, ZTP_ESHAPE, "ztp_core: " + shp("qkv_t", *qkv) + " " + shp("ctx_t", *cx));
   if (qkv->dtype == ZTP_BF16 && qkv->cols % 8) return fail(c, ZTP_ESHAPE, "ztp_core: N % 8 != 0");
+  const int pe = prof_begin(c, (cudaStream_t)stream, PROF_OTHER, 0.0);
   CUDA_TRY(c, ztp::core_launch(phase == ZTP_FWD ? 0 : 1, qkv->ptr, qkv->ld, cx->ptr, cx->ld, feat, n_out, qkv->cols,
                                qkv->dtype, phase == ZTP_FWD ? rows : nullptr, (cudaStream_t)stream));
+  prof_end(c, pe, (cudaStream_t)stream);
   ++c->launches;
   return ZTP_OK;
 }
@@ -713,6 +786,36 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
     CUDA_TRY(c, cudaMemcpy2DAsync((char*)x.dst.ptr + (x.dr0 * x.dst.ld + x.dc0) * es, x.dst.ld * es, ws + off[i],
                                   x.nc * es, x.nc * es, x.nr, cudaMemcpyDeviceToDevice, st));
   }
+  return ZTP_OK;
+}
+
+ztp_status ztp_set_profile(ztp_ctx* c, int on) {
+  if (!c) return fail(c, ZTP_EINVAL, "ztp_set_profile: null ctx");
+  c->prof_on = on ? 1 : 0;
+  return ZTP_OK;
+}
+
+ztp_status ztp_read_profile(ztp_ctx* c, void* stream, ztp_profile* out) {
+  if (!c || !out) return fail(c, ZTP_EINVAL, "ztp_read_profile: null argument");
+  CUDA_TRY(c, cudaStreamSynchronize((cudaStream_t)stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->comm_stream));
+  std::memset(out, 0, sizeof(*out));
+  for (size_t i = 0; i < c->prof_used; ++i) {
+    float ms = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, c->prof[i].a, c->prof[i].b));
+    if (c->prof[i].cat == PROF_GEMM) {
+      out->gemm_ms += ms;
+      out->gemm_flops += c->prof[i].flops;
+      ++out->n_gemm;
+    } else if (c->prof[i].cat == PROF_OTHER) {
+      out->other_ms += ms;
+      ++out->n_other;
+    } else {
+      out->comm_ms += ms;
+      ++out->n_comm;
+    }
+  }
+  c->prof_used = 0;
   return ZTP_OK;
 }
 

@@ -4,24 +4,29 @@
 //   DW   dW^T[k,j] = sum_t       X^T[k,t] G^T[j,t], k in S
 // with rows P of dX^T / dW^T imputed by Zero in the same kernel.
 //
-// Design: persistent, warp-specialised, 1-CTA
-// tcgen05 kind::f16 128x256x16 MMAs accumulating in TMEM (2 x 256 columns,
-// double-buffered so the epilogue of tile i overlaps the mainloop of i+1).
-//   warp 0      TMA producer.  The pruned contraction rows are gathered
-//               straight from HBM into the 128B-swizzled smem ring with
-//               cp.async.bulk.tensor...tile::gather4 (4 rows per instruction,
-//               32 lanes issuing in parallel) -- no compacted copy of X or W
-//               is ever materialised (a4: "dimension extracting").
-//   warp 1      MMA issuer (one thread), tcgen05.commit -> smem-slot release.
-//   warp 2      TMEM allocator.
+// Design: persistent, warp-specialised tcgen05
+// kind::f16 GEMM accumulating in TMEM (2 x 256 fp32 columns, double-buffered so
+// the epilogue of tile i overlaps the mainloop of tile i+1).
+//   CG = 2 (default): a CTA pair (cluster of 2 on one TPC) computes a 256x256
+//          tile with tcgen05.mma.cta_group::2 -- each CTA stages its 128 rows
+//          of A and half (128 columns) of B, so L2->SM operand traffic per
+//          FLOP is 2/3 of a 128x256 single-CTA tile.
+//   CG = 1: a CTA computes a 128x256 tile (small-M problems).
+//   warp 0      TMA producer (dense boxes from compact operands, or
+//               tile::gather4 of the lineage rows in gather mode)
+//   warp 1      MMA issuer (one thread of the even CTA), tcgen05.commit
+//               multicast -> smem-slot release in both CTAs
+//   warp 2      TMEM allocator
 //   warps 4-7   epilogue: tcgen05.ld -> (GeLU | GeLU' | none) -> bf16 ->
 //               swizzled smem staging -> 128-bit coalesced row stores at the
-//               lineage row map (a6: scatter + Zero imputation).
+//               lineage row map (a6: scatter + Zero imputation), or fp32
+//               split-K partials reduced by ztp_splitk_reduce.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "ztp_internal.h"
@@ -29,17 +34,20 @@
 
 namespace ztp {
 
-constexpr int BM = 128;
+constexpr int BM = 128;   // rows per CTA
+constexpr int BN = 256;   // tile columns (per CTA pair when CG = 2)
 constexpr int BK = 64;
-constexpr int STAGES = 4;
 constexpr int NUM_THREADS = 256;
-constexpr int A_BYTES = BM * BK * 2;              // 16 KB
-constexpr int STAGING_PER_WARP = 32 * 128 * 2;    // two 32x64 bf16 planes (pre and H)
+constexpr int A_BYTES = BM * BK * 2;           // 16 KB
+constexpr int STAGING_PER_WARP = 32 * 128 * 2;  // two 32x64 bf16 planes (pre and H)
 
-template <int BN>
-struct Smem {
-  static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+template <int CG>
+struct Cfg {
+  static constexpr int BNL = BN / CG;                    // B columns staged by one CTA
+  static constexpr int TM = BM * CG;                     // tile rows
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int B_BYTES = BNL * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
   static constexpr int RING = STAGES * STAGE_BYTES;
   static constexpr int STAGING = 4 * STAGING_PER_WARP;
   static constexpr int BARS = (2 * STAGES + 4) * 8 + 16;
@@ -67,26 +75,91 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
 }
 
-template <int KIND>
-__device__ __forceinline__ int gather_row_mk(const GemmParams& p, int m) {
-  // K-major gathered operand (DX: W^T rows, DW: X^T rows): row m of the tile
-  // is lineage row kept[m]; pruned rows read as zeros (OOB row -> TMA zero fill).
-  return (m < p.n_kept) ? __ldg(p.kept + m) : p.oob_row;
+// 8 bf16 (16 B) at p; a ragged last chunk (nv < 8 valid columns) is stored
+// element-wise so nothing past the logical width is written.
+__device__ __forceinline__ void store_bf16x8(__nv_bfloat16* p, const uint4& w, int nv) {
+  if (nv >= 8) {
+    st_global_v4(p, w);
+    return;
+  }
+  const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < nv) reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)(x[i >> 1] >> (16 * (i & 1)));
 }
+
+__device__ __forceinline__ uint4 gelu_grad_mul(uint4 w, uint4 pin) {
+  w.x = pack_bf16(bf16_lo(w.x) * gelu_grad_f(bf16_lo(pin.x)), bf16_hi(w.x) * gelu_grad_f(bf16_hi(pin.x)));
+  w.y = pack_bf16(bf16_lo(w.y) * gelu_grad_f(bf16_lo(pin.y)), bf16_hi(w.y) * gelu_grad_f(bf16_hi(pin.y)));
+  w.z = pack_bf16(bf16_lo(w.z) * gelu_grad_f(bf16_lo(pin.z)), bf16_hi(w.z) * gelu_grad_f(bf16_hi(pin.z)));
+  w.w = pack_bf16(bf16_lo(w.w) * gelu_grad_f(bf16_lo(pin.w)), bf16_hi(w.w) * gelu_grad_f(bf16_hi(pin.w)));
+  return w;
+}
+
+// Work units: computed tiles x K-splits first, then (unsplit launches only)
+// the DX / DW tiles whose rows are all pruned -- they skip the MMA and write
+// Zero.  Split launches leave pruned rows to the reduce kernel.
+struct Work {
+  int m0, n0, kb0, kb1, split;
+  bool zero;
+};
+
+template <int KIND, int TM>
+struct Sched {
+  int m_tiles, n_tiles, mc, tiles_c, units_c, zero_m, num_units, num_kb, S, kbs;
+  __device__ __forceinline__ Sched(const GemmParams& p) {
+    m_tiles = (p.M + TM - 1) / TM;
+    n_tiles = (p.N + BN - 1) / BN;
+    num_kb = (p.kdim + BK - 1) / BK;
+    mc = m_tiles;
+    if (KIND != KIND_FWD) {
+      const int mk = (p.n_kept + TM - 1) / TM;
+      mc = mk < m_tiles ? mk : m_tiles;
+    }
+    tiles_c = mc * n_tiles;
+    S = p.splits;
+    kbs = p.kb_per_split;
+    units_c = tiles_c * S;
+    zero_m = m_tiles - mc;
+    num_units = units_c + (S == 1 ? zero_m * n_tiles : 0);
+  }
+  __device__ __forceinline__ Work get(int u) const {
+    Work w;
+    if (u < units_c) {
+      const int s = u / tiles_c, t = u - s * tiles_c;
+      w.m0 = (t % mc) * TM;
+      w.n0 = (t / mc) * BN;
+      w.split = s;
+      w.kb0 = s * kbs;
+      w.kb1 = min(num_kb, w.kb0 + kbs);
+      w.zero = false;
+    } else {
+      const int v = u - units_c;
+      w.m0 = (mc + v % zero_m) * TM;
+      w.n0 = (v / zero_m) * BN;
+      w.split = 0;
+      w.kb0 = w.kb1 = 0;
+      w.zero = true;
+    }
+    return w;
+  }
+};
 
 // AG / BG: operand A / B gathered row-by-row with TMA gather4 through the
 // lineage list (true) or loaded as dense TMA boxes from a compact, already
 // row-selected tensor (false; rows past the compact extent are zero-filled).
-template <int KIND, int BN, bool AG, bool BG>
+template <int KIND, int CG, bool AG, bool BG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ztp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParams p) {
-  using SM = Smem<BN>;
+  using C = Cfg<CG>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int BNL = C::BNL;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
-  uint8_t* staging = smem + SM::RING;
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + SM::STAGING);
+  uint8_t* staging = smem + C::RING;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::STAGING);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -94,6 +167,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;   // CTA rank in the pair
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
 
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMin(p.stamp, (unsigned long long)globaltimer());
 
@@ -104,7 +180,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], 4 * CG);
     }
     fence_barrier_init();
   }
@@ -112,41 +188,57 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) {
+    if (CG == 2)
+      tmem_alloc_cg2(tmem_slot, 512);
+    else
+      tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int m_tiles = (p.M + BM - 1) / BM;
-  const int n_tiles = (p.N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
-  const int num_kb = (p.kdim + BK - 1) / BK;
-  // DX / DW: tiles whose rows are all pruned skip the MMA and write Zero.
-  auto zero_tile = [&](int m0) { return (KIND != KIND_FWD) && (m0 >= p.n_kept); };
+  const Sched<KIND, C::TM> sc(p);
 
   if (warp == 0) {
     // ============================ TMA producer ============================
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile % m_tiles) * BM;
-      const int n0 = (tile / m_tiles) * BN;
-      if (zero_tile(m0)) continue;
+    for (int u = pair; u < sc.num_units; u += npairs) {
+      const Work wk = sc.get(u);
+      if (wk.zero) continue;
+      const int am0 = wk.m0 + BM * rank;   // this CTA's 128 rows of the tile (A)
+      const int bn0 = wk.n0 + BNL * rank;  // this CTA's columns of B
       int ar0 = 0, ar1 = 0, ar2 = 0, ar3 = 0;
       if (KIND != KIND_FWD && AG) {
-        const int mb = m0 + 4 * lane;
-        ar0 = gather_row_mk<KIND>(p, mb + 0);
-        ar1 = gather_row_mk<KIND>(p, mb + 1);
-        ar2 = gather_row_mk<KIND>(p, mb + 2);
-        ar3 = gather_row_mk<KIND>(p, mb + 3);
+        const int mb = am0 + 4 * lane;
+        ar0 = (mb + 0 < p.n_kept) ? __ldg(p.kept + mb + 0) : p.oob_row;
+        ar1 = (mb + 1 < p.n_kept) ? __ldg(p.kept + mb + 1) : p.oob_row;
+        ar2 = (mb + 2 < p.n_kept) ? __ldg(p.kept + mb + 2) : p.oob_row;
+        ar3 = (mb + 3 < p.n_kept) ? __ldg(p.kept + mb + 3) : p.oob_row;
       }
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = ring + stage * SM::STAGE_BYTES;
+        uint8_t* sa = ring + stage * C::STAGE_BYTES;
         uint8_t* sb = sa + A_BYTES;
-        if (lane == 0) mbar_expect_tx(&full[stage], SM::STAGE_BYTES);
+        if (leader && lane == 0) mbar_expect_tx(&full[stage], CG * C::STAGE_BYTES);
         __syncwarp();
+        auto load = [&](const CUtensorMap* tm, void* dst, int c0, int c1) {
+          if (CG == 2)
+            tma_load_2d_cg2(tm, &full[stage], dst, c0, c1);
+          else
+            tma_load_2d(tm, &full[stage], dst, c0, c1);
+        };
+        auto gather = [&](const CUtensorMap* tm, void* dst, int col, int r0, int r1, int r2, int r3) {
+          if (CG == 2)
+            tma_gather4_cg2(tm, &full[stage], dst, col, r0, r1, r2, r3);
+          else
+            tma_gather4(tm, &full[stage], dst, col, r0, r1, r2, r3);
+        };
         if (KIND == KIND_FWD) {
           // both operands MN-major (contraction rows outer)
           if (AG || BG) {
@@ -158,37 +250,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int k = kbase + i;
               r[i] = (k < p.n_kept) ? __ldg(p.kept + k) : p.oob_row;
             }
-            if (AG)
-              tma_gather4(&tmA, &full[stage], sa + half * 8192 + g * 512, m0 + 64 * half, r[0], r[1], r[2], r[3]);
+            if (AG) gather(&tmA, sa + half * 8192 + g * 512, am0 + 64 * half, r[0], r[1], r[2], r[3]);
             if (BG) {
+              constexpr int NB = BNL / 64, PER = NB / 2;
 #pragma unroll
-              for (int b = 2 * half; b < 2 * half + 2; ++b)
-                if (b < BN / 64)
-                  tma_gather4(&tmB, &full[stage], sb + b * 8192 + g * 512, n0 + 64 * b, r[0], r[1], r[2], r[3]);
+              for (int b = half * PER; b < (half + 1) * PER; ++b)
+                gather(&tmB, sb + b * 8192 + g * 512, bn0 + 64 * b, r[0], r[1], r[2], r[3]);
             }
           }
           if (lane == 0) {
             if (!AG) {
-              tma_load_2d(&tmA, &full[stage], sa, m0, kb * BK);
-              tma_load_2d(&tmA, &full[stage], sa + 8192, m0 + 64, kb * BK);
+              load(&tmA, sa, am0, kb * BK);
+              load(&tmA, sa + 8192, am0 + 64, kb * BK);
             }
             if (!BG) {
 #pragma unroll
-              for (int b = 0; b < BN / 64; ++b) tma_load_2d(&tmB, &full[stage], sb + b * 8192, n0 + 64 * b, kb * BK);
+              for (int b = 0; b < BNL / 64; ++b) load(&tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
             }
           }
         } else {
           // A: K-major rows (m) x 64 contraction columns
-          if (AG) tma_gather4(&tmA, &full[stage], sa + lane * 512, kb * BK, ar0, ar1, ar2, ar3);
+          if (AG) gather(&tmA, sa + lane * 512, kb * BK, ar0, ar1, ar2, ar3);
           if (lane == 0) {
-            if (!AG) tma_load_2d(&tmA, &full[stage], sa, kb * BK, m0);
+            if (!AG) load(&tmA, sa, kb * BK, am0);
             if (KIND == KIND_DX) {
-              // B = G^T [n, N] MN-major dense: 64 contraction rows x BN columns
+              // B = G^T [n, N] MN-major dense: 64 contraction rows x BNL columns
 #pragma unroll
-              for (int b = 0; b < BN / 64; ++b) tma_load_2d(&tmB, &full[stage], sb + b * 8192, n0 + 64 * b, kb * BK);
+              for (int b = 0; b < BNL / 64; ++b) load(&tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
             } else {
-              // B = G^T [n, N] K-major dense: BN rows (output cols j) x 64 tokens
-              tma_load_2d(&tmB, &full[stage], sb, kb * BK, n0);
+              // B = G^T [n, N] K-major dense: BNL rows (output cols j) x 64 tokens
+              load(&tmB, sb, kb * BK, bn0);
             }
           }
         }
@@ -198,24 +289,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // ============================ MMA issuer ==============================
-    constexpr uint32_t IDESC = make_idesc_bf16(BM, BN, KIND == KIND_FWD ? 1 : 0, KIND == KIND_DW ? 0 : 1);
+    constexpr uint32_t IDESC = make_idesc_bf16(C::TM, BN, KIND == KIND_FWD ? 1 : 0, KIND == KIND_DW ? 0 : 1);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile % m_tiles) * BM;
-      if (zero_tile(m0)) continue;
+    for (int u = pair; u < sc.num_units; u += npairs) {
+      const Work wk = sc.get(u);
+      if (wk.zero) continue;
       mbar_wait(&tempty[acc], aphase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t sa = smem_u32(ring + stage * SM::STAGE_BYTES);
+          const uint32_t sa = smem_u32(ring + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
@@ -228,9 +319,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               bd = make_sdesc_sw128(sb + kk * 32, 16, 1024);
             else
               bd = make_sdesc_sw128(sb + kk * 2048, 8192, 1024);
-            umma_bf16(d_tmem, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            const uint32_t accum = (kb > wk.kb0 || kk > 0) ? 1u : 0u;
+            if (CG == 2)
+              umma_bf16_cg2(d_tmem, ad, bd, IDESC, accum);
+            else
+              umma_bf16(d_tmem, ad, bd, IDESC, accum);
           }
-          umma_commit(&empty[stage]);
+          if (CG == 2)
+            umma_commit_mc(&empty[stage], 0x3);
+          else
+            umma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -238,7 +336,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           phase ^= 1;
         }
       }
-      if (lane == 0) umma_commit(&tfull[acc]);
+      if (lane == 0) {
+        if (CG == 2)
+          umma_commit_mc(&tfull[acc], 0x3);
+        else
+          umma_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
@@ -252,10 +355,58 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint8_t* stg2 = stg + 32 * 128;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile % m_tiles) * BM;
-      const int n0 = (tile / m_tiles) * BN;
-      const bool zt = zero_tile(m0);
+    auto release = [&]() {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2)
+          mbar_arrive_leader(&tempty[acc]);
+        else
+          mbar_arrive(&tempty[acc]);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    };
+    for (int u = pair; u < sc.num_units; u += npairs) {
+      const Work wk = sc.get(u);
+      const int m0 = wk.m0 + BM * rank, n0 = wk.n0;
+      const bool zt = wk.zero;
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      if (sc.S > 1) {
+        // ---- split-K partial: fp32 tile -> ws[split] (computed rows only, no row map)
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+        float* wsp = p.ws + (int64_t)wk.split * p.ws_split_stride;
+        const int mlim = KIND == KIND_FWD ? p.M : p.n_kept;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tbase + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint4 w = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) = w;
+          }
+          __syncwarp();
+          const int q = lane & 7;
+          const int col = n0 + c * 32 + q * 4;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + (lane >> 3);
+            const int m = m0 + ew * 32 + rr;
+            if (m < mlim && col < p.N) {
+              const uint4 w = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
+              st_global_v4(wsp + (int64_t)m * p.ld_ws + col, w);
+            }
+          }
+          __syncwarp();
+        }
+        release();
+        continue;
+      }
       // output rows this lane stores: r = 4 i + lane / 8, i = 0..7
       int orow[8], arow[8];
 #pragma unroll
@@ -275,7 +426,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
       }
-      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = 0; c < BN / 64; ++c) {
         uint32_t v0[32], v1[32];
@@ -288,7 +438,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0u;
         }
         // thread `lane` owns tile row ew*32 + lane: 64 fp32 -> 8 x 16B chunks
-        const int r = lane;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           float f[8];
@@ -302,7 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           w.y = pack_bf16(f[2], f[3]);
           w.z = pack_bf16(f[4], f[5]);
           w.w = pack_bf16(f[6], f[7]);
-          const int off = r * 128 + ((q ^ (r & 7)) << 4);
+          const int off = lane * 128 + ((q ^ (lane & 7)) << 4);
           *reinterpret_cast<uint4*>(stg + off) = w;
           if (p.epi == EPI_GELU) {
             uint4 g;
@@ -325,37 +474,91 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (p.epi == EPI_GELU_GRAD && !zt) {
               // G1 = dH * GeLU'(pre_in) at the same (row, col) (row layer BWD)
               const uint4 pin = *reinterpret_cast<const uint4*>(p.aux + (int64_t)arow[i] * p.ld_aux + col);
-              w.x = pack_bf16(bf16_lo(w.x) * gelu_grad_f(bf16_lo(pin.x)), bf16_hi(w.x) * gelu_grad_f(bf16_hi(pin.x)));
-              w.y = pack_bf16(bf16_lo(w.y) * gelu_grad_f(bf16_lo(pin.y)), bf16_hi(w.y) * gelu_grad_f(bf16_hi(pin.y)));
-              w.z = pack_bf16(bf16_lo(w.z) * gelu_grad_f(bf16_lo(pin.z)), bf16_hi(w.z) * gelu_grad_f(bf16_hi(pin.z)));
-              w.w = pack_bf16(bf16_lo(w.w) * gelu_grad_f(bf16_lo(pin.w)), bf16_hi(w.w) * gelu_grad_f(bf16_hi(pin.w)));
+              w = gelu_grad_mul(w, pin);
             }
-            st_global_v4(p.out + (int64_t)orow[i] * p.ld_out + col, w);
+            const int nv = p.N - col;
+            store_bf16x8(p.out + (int64_t)orow[i] * p.ld_out + col, w, nv);
             if (p.epi == EPI_GELU) {
               const uint4 g = *reinterpret_cast<const uint4*>(stg2 + off);
-              st_global_v4(p.out2 + (int64_t)orow[i] * p.ld_out2 + col, g);
+              store_bf16x8(p.out2 + (int64_t)orow[i] * p.ld_out2 + col, g, nv);
             }
           }
         }
         __syncwarp();
       }
-      if (!zt) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          aphase ^= 1;
-        }
-      }
+      if (!zt) release();
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, 512);
+  if (warp == 2) {
+    if (CG == 2)
+      tmem_dealloc_cg2(tmem_base, 512);
+    else
+      tmem_dealloc(tmem_base, 512);
+  }
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMax(p.stamp + 1, (unsigned long long)globaltimer());
+}
+
+// Split-K reduction (fixed split order -> deterministic) fused with the
+// epilogue the unsplit kernel applies: GeLU / GeLU', bf16 RNE, lineage row map
+// and the Zero imputation of pruned rows.
+template <int KIND>
+__global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
+  const int cpr = (p.N + 7) / 8;
+  const int64_t total = (int64_t)p.M * cpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / cpr);
+    const int col = (int)(i % cpr) * 8;
+    const int nv = p.N - col;
+    const bool computed = (KIND == KIND_FWD) || (m < p.n_kept);
+    int orow;
+    if (KIND == KIND_FWD)
+      orow = p.out_pos ? __ldg(p.out_pos + m) : m;
+    else
+      orow = computed ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
+    if (orow < 0) continue;
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (computed) {
+      const float* src = p.ws + (int64_t)m * p.ld_ws + col;
+      for (int s = 0; s < p.splits; ++s) {
+        const float4 a = *reinterpret_cast<const float4*>(src);
+        const float4 b = *reinterpret_cast<const float4*>(src + 4);
+        v[0] += a.x;
+        v[1] += a.y;
+        v[2] += a.z;
+        v[3] += a.w;
+        v[4] += b.x;
+        v[5] += b.y;
+        v[6] += b.z;
+        v[7] += b.w;
+        src += p.ws_split_stride;
+      }
+    }
+    uint4 w;
+    w.x = pack_bf16(v[0], v[1]);
+    w.y = pack_bf16(v[2], v[3]);
+    w.z = pack_bf16(v[4], v[5]);
+    w.w = pack_bf16(v[6], v[7]);
+    if (p.epi == EPI_GELU_GRAD && computed) {
+      const int ar = p.aux_by_m ? m : orow;
+      w = gelu_grad_mul(w, *reinterpret_cast<const uint4*>(p.aux + (int64_t)ar * p.ld_aux + col));
+    }
+    store_bf16x8(p.out + (int64_t)orow * p.ld_out + col, w, nv);
+    if (p.epi == EPI_GELU) {
+      uint4 g;
+      g.x = pack_bf16(gelu_f(v[0]), gelu_f(v[1]));
+      g.y = pack_bf16(gelu_f(v[2]), gelu_f(v[3]));
+      g.z = pack_bf16(gelu_f(v[4]), gelu_f(v[5]));
+      g.w = pack_bf16(gelu_f(v[6]), gelu_f(v[7]));
+      store_bf16x8(p.out2 + (int64_t)orow * p.ld_out2 + col, g, nv);
+    }
+  }
 }
 
 // ----------------------------------------------------------------- host side
@@ -387,21 +590,82 @@ static bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols
   return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BN, bool AG, bool BG>
+static int units_of(int kind, int cg, const GemmParams& p) {
+  const int tm = BM * cg;
+  const int m_tiles = (p.M + tm - 1) / tm, n_tiles = (p.N + BN - 1) / BN;
+  int mc = m_tiles;
+  if (kind != KIND_FWD) mc = std::min(m_tiles, (p.n_kept + tm - 1) / tm);
+  return mc * n_tiles * p.splits + (p.splits == 1 ? (m_tiles - mc) * n_tiles : 0);
+}
+
+template <int KIND, int CG, bool AG, bool BG>
 static cudaError_t launch_kind(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int num_sms,
                                cudaStream_t st) {
   static bool attr_set = false;
-  const int smem = Smem<BN>::TOTAL;
+  const int smem = Cfg<CG>::TOTAL;
+  auto kern = ztp_gemm_kernel<KIND, CG, AG, BG>;
   if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(ztp_gemm_kernel<KIND, BN, AG, BG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  ztp_gemm_kernel<KIND, BN, AG, BG><<<grid, NUM_THREADS, smem, st>>>(a, b, p);
+  const int units = units_of(KIND, CG, p);
+  const int pairs = std::min(units, num_sms / CG);
+  if (pairs > 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(pairs * CG);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, p);
+    if (e != cudaSuccess) return e;
+  }
+  if (p.splits == 1) return cudaSuccess;
+  const int64_t chunks = (int64_t)p.M * ((p.N + 7) / 8);
+  const int blocks = (int)std::min<int64_t>((chunks + 255) / 256, (int64_t)num_sms * 8);
+  ztp_splitk_reduce<KIND><<<blocks, 256, 0, st>>>(p);
   return cudaGetLastError();
+}
+
+int gemm_choose_cg(int kind, int M, int n_kept) {
+  const int rows = kind == KIND_FWD ? M : std::min(M, n_kept);
+  return rows > BM ? 2 : 1;
+}
+
+int gemm_choose_splits(int kind, int M, int N, int kdim, int n_kept, int num_sms) {
+  const int cg = gemm_choose_cg(kind, M, n_kept);
+  const int tm = BM * cg;
+  const int m_tiles = (M + tm - 1) / tm, n_tiles = (N + BN - 1) / BN;
+  int mc = m_tiles;
+  if (kind != KIND_FWD) mc = std::min(m_tiles, (n_kept + tm - 1) / tm);
+  const int tiles_c = std::max(1, mc * n_tiles);
+  const int num_kb = (kdim + BK - 1) / BK;
+  const int s = std::min((num_sms / cg) / tiles_c, num_kb / 16);  // each split keeps >= 1024 contraction elements
+  return std::max(1, s);
+}
+
+size_t gemm_ws_bytes(int kind, int M, int N, int n_kept, int splits) {
+  if (splits <= 1) return 0;
+  const int64_t rows = kind == KIND_FWD ? M : std::min(M, n_kept);
+  const int64_t ld = (N + 7) / 8 * 8;
+  return (size_t)splits * rows * ld * sizeof(float);
+}
+
+template <int KIND, int CG>
+static cudaError_t dispatch(bool ag, bool bg, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                            int num_sms, cudaStream_t st) {
+  if (KIND != KIND_FWD && bg) return cudaErrorInvalidValue;
+  if (ag && bg) return launch_kind<KIND, CG, true, true>(ta, tb, p, num_sms, st);
+  if (ag) return launch_kind<KIND, CG, true, false>(ta, tb, p, num_sms, st);
+  if (bg) return launch_kind<KIND, CG, false, true>(ta, tb, p, num_sms, st);
+  return launch_kind<KIND, CG, false, false>(ta, tb, p, num_sms, st);
 }
 
 // Operand A / B tensor maps per kind (see the header comment of this file).
@@ -409,6 +673,8 @@ cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_s
   CUtensorMap ta, tb;
   bool ok = true;
   const bool ag = o.a_gather, bg = o.b_gather;
+  const int cg = gemm_choose_cg(kind, p.M, p.n_kept);
+  const uint32_t bnl = BN / cg;
   p.oob_row = (int)(o.a_rows > o.b_rows ? o.a_rows : o.b_rows);  // outside every gathered tensor
   if (kind == KIND_FWD) {
     // A = W^T [K|K', n] MN-major; B = X^T [K|K', N] MN-major (same rows)
@@ -419,28 +685,19 @@ cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_s
     ok &= make_map(&ta, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : BM);
     ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, 64);
   } else {
-    // A = X^T [K|K', N] K-major; B = G^T [n_out, N] K-major box 64 x 256
+    // A = X^T [K|K', N] K-major; B = G^T [n_out, N] K-major box 64 x BN/cg
     ok &= make_map(&ta, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : BM);
-    ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, 256);
+    ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, bnl);
   }
   if (!ok) return cudaErrorInvalidValue;
-#define ZTP_DISPATCH(K_)                                                          \
-  if (ag && bg) return launch_kind<K_, 256, true, true>(ta, tb, p, num_sms, st);   \
-  if (ag) return launch_kind<K_, 256, true, false>(ta, tb, p, num_sms, st);        \
-  if (bg) return launch_kind<K_, 256, false, true>(ta, tb, p, num_sms, st);        \
-  return launch_kind<K_, 256, false, false>(ta, tb, p, num_sms, st);
-  if (kind == KIND_FWD) {
-    ZTP_DISPATCH(KIND_FWD)
-  }
-  if (kind == KIND_DX) {
-    if (bg) return cudaErrorInvalidValue;
-    if (ag) return launch_kind<KIND_DX, 256, true, false>(ta, tb, p, num_sms, st);
-    return launch_kind<KIND_DX, 256, false, false>(ta, tb, p, num_sms, st);
-  }
-  if (bg) return cudaErrorInvalidValue;
-  if (ag) return launch_kind<KIND_DW, 256, true, false>(ta, tb, p, num_sms, st);
-  return launch_kind<KIND_DW, 256, false, false>(ta, tb, p, num_sms, st);
-#undef ZTP_DISPATCH
+  if (kind == KIND_FWD)
+    return cg == 2 ? dispatch<KIND_FWD, 2>(ag, bg, ta, tb, p, num_sms, st)
+                   : dispatch<KIND_FWD, 1>(ag, bg, ta, tb, p, num_sms, st);
+  if (kind == KIND_DX)
+    return cg == 2 ? dispatch<KIND_DX, 2>(ag, bg, ta, tb, p, num_sms, st)
+                   : dispatch<KIND_DX, 1>(ag, bg, ta, tb, p, num_sms, st);
+  return cg == 2 ? dispatch<KIND_DW, 2>(ag, bg, ta, tb, p, num_sms, st)
+                 : dispatch<KIND_DW, 1>(ag, bg, ta, tb, p, num_sms, st);
 }
 
 }  // namespace ztp

@@ -27,7 +27,16 @@ struct GemmParams {
   int aux_by_m;               // aux is compact (row m of the tile order) instead of at the output row
   const int32_t* out_pos;     // FWD: output row map (unit j -> row out_pos[j], dropped if < 0); NULL = identity
   unsigned long long* stamp;  // [start_min, end_max] %globaltimer of this launch (nullable)
+  // split-K (set by gemm_launch): splits > 1 writes fp32 partials to ws and a
+  // fixed-order reduce kernel applies the epilogue and the row map.
+  int splits, kb_per_split;
+  float* ws;
+  int64_t ld_ws, ws_split_stride;
 };
+
+// Split-K choice for a launch and the fp32 workspace it needs (bytes).
+int gemm_choose_splits(int kind, int M, int N, int kdim, int n_kept, int num_sms);
+size_t gemm_ws_bytes(int kind, int M, int N, int n_kept, int splits);
 
 // Operand tensors of one launch: row-major bf16 [rows, cols], pitch ld.
 // *_gather: rows are fetched through the lineage list with TMA gather4;

@@ -209,6 +209,47 @@ def test_gemm_gelu_epilogues(env, dtype):
     assert ok, e
 
 
+@pytest.mark.parametrize("case", ["fwd_gelu", "dx_gelu_grad", "dw"])
+def test_gemm_splitk_paths(env, case):
+    """Few output tiles + long contraction -> split-K partials + the fixed-order
+    reduce kernel (epilogue, row map and Zero rows applied there)."""
+    Z, torch, ctx = env
+    if case == "fwd_gelu":
+        K, n, N, gamma = 8192, 128, 256, 0.5            # 1 tile, 64 k-blocks
+    elif case == "dx_gelu_grad":
+        K, n, N, gamma = 256, 2048, 256, 0.6            # 1 computed m-tile, kdim 2048
+    else:
+        K, n, N, gamma = 256, 200, 4096, 0.5            # 1 x 1 tiles, 64 token k-blocks
+    Xt, Wt, Gt, S, P = _case(K, n, N, gamma, seed=31)
+    x, w, g = dev(torch, Xt), dev(torch, Wt), dev(torch, Gt)
+    s, keep = _sel_dev(Z, torch, S, P)
+    if case == "fwd_gelu":
+        pre, h = empty(torch, n, N, torch.bfloat16), empty(torch, n, N, torch.bfloat16)
+        Z.ztp_gemm(ctx, Z.KIND_FWD, Z.linear_args(x_t=x, w_t=w, y_t=h, pre_t=pre, sel_=s, act=Z.ACT_GELU))
+        Z.ztp_sync(ctx)
+        ref = O.linear_fwd(Wt, Xt, S)
+        for got, want in ((pre, ref), (h, O.gelu_tanh(ref))):
+            ok, e = err_ok(host(got), want, TOL_BF16)
+            assert ok, e
+    elif case == "dx_gelu_grad":
+        pin = I.normal(31, "pin", K, N)
+        dx = empty(torch, K, N, torch.bfloat16)
+        Z.ztp_gemm(ctx, Z.KIND_DX, Z.linear_args(w_t=w, g_t=g, dx_t=dx, pre_in_t=dev(torch, pin), sel_=s,
+                                                 act_in=Z.ACT_GELU))
+        Z.ztp_sync(ctx)
+        ref = O.linear_bwd_dx(Wt, Gt, S, P) * O.gelu_tanh_grad(pin)
+        ok, e = err_ok(host(dx), ref, TOL_BF16)
+        assert ok, e
+        assert torch.all(dx[torch.tensor(P, device="cuda")] == 0)
+    else:
+        dw = empty(torch, K, n, torch.bfloat16)
+        Z.ztp_gemm(ctx, Z.KIND_DW, Z.linear_args(x_t=x, w_t=w, g_t=g, dw_t=dw, sel_=s))
+        Z.ztp_sync(ctx)
+        ok, e = err_ok(host(dw), O.linear_bwd_dw(Xt, Gt, S, P), TOL_BF16)
+        assert ok, e
+        assert torch.all(dw[torch.tensor(P, device="cuda")] == 0)
+
+
 def test_gemm_large_c2_shapes_sampled(env):
     """c2 e=1 FC1 shapes (K=1024, n=4096, N=8192) in the bench launch config,
     checked on sampled output rows/columns computed one by one in fp64."""

@@ -31,22 +31,18 @@ def run(K, n, N, gamma, iters=20, kinds=(0, 1, 2)):
     s = Z.sel(S, K - npr, P, npr, 0, 0)
     a = Z.linear_args(x_t=x, w_t=w, y_t=y, g_t=gt, dx_t=dx, dw_t=dw, sel_=s)
     out = {}
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for kind in kinds:
         for _ in range(3):
             Z.ztp_gemm(ctx, kind, a)
         torch.cuda.synchronize()
-        times = []
+        Z.ztp_read_profile(ctx)
+        Z.ztp_set_profile(ctx, True)
         for _ in range(iters):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
             Z.ztp_gemm(ctx, kind, a)
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-        t = float(np.median(times)) * 1e-3
-        flops = 2.0 * n * N * (K - npr)
+        prof = Z.ztp_read_profile(ctx)
+        Z.ztp_set_profile(ctx, False)
+        t = prof["gemm_ms"] / iters * 1e-3           # GEMM kernel(s) only, CUDA events
+        flops = prof["gemm_flops"] / iters
         out[["fwd", "dx", "dw"][kind]] = dict(ms=t * 1e3, tflops=flops / t / 1e12)
     Z.ztp_ctx_destroy(ctx)
     return out
