@@ -51,6 +51,42 @@ class MigrationIO:
     all_xfers: List[tuple] = field(default_factory=list)  # (src, dst, lo, hi, dst_off) for every pair
 
 
+def migration_io(plan, rank: int, world: int, u: int, h: int, unit: int = 1) -> MigrationIO:
+    """This rank's migration I/O from a plan, via ztp_plan_counts (host only).
+    all_xfers lists every (src, dst, lo, hi, dst_off) pair of the layer so all
+    ranks issue the same ztp_migrate list; dst_off is the offset of the range
+    inside the helper's appended slots [u, u + cap)."""
+    counts = [Z.ztp_plan_counts(plan, r, u, u, unit, True) for r in range(world)]
+    me = counts[rank]
+    mio = MigrationIO(n_mig=me.n_mig,
+                      out=[(me.out_dst[i], me.out_lo[i], me.out_hi[i]) for i in range(me.n_out)],
+                      inc=[(me.in_src[i], me.in_lo[i], me.in_hi[i]) for i in range(me.n_in)])
+    for r in range(world):
+        off = 0
+        c = counts[r]
+        for i in range(c.n_in):
+            lo, hi = c.in_lo[i], c.in_hi[i]
+            mio.all_xfers.append((c.in_src[i], r, lo, hi, off))
+            off += hi - lo
+    return mio
+
+
+def xfer_specs(mio: MigrationIO, u: int, h: int, grads: bool) -> List[dict]:
+    """Peer copies of one layer's migration (pure host logic).  Weights: the
+    owner's units [lo, hi) -> the helper's appended slots [u+off, ...) of W1^T
+    (columns) and W2^T (rows).  Gradients: the reverse, into dW1^T / dW2^T."""
+    out = []
+    for (src, dst, lo, hi, off) in mio.all_xfers:
+        n = hi - lo
+        if not grads:
+            out.append(dict(t="w1", src=src, dst=dst, r0=0, c0=lo, nr=h, nc=n, dr0=0, dc0=u + off))
+            out.append(dict(t="w2", src=src, dst=dst, r0=lo, c0=0, nr=n, nc=h, dr0=u + off, dc0=0))
+        else:
+            out.append(dict(t="dw1", src=dst, dst=src, r0=0, c0=u + off, nr=h, nc=n, dr0=0, dc0=lo))
+            out.append(dict(t="dw2", src=dst, dst=src, r0=u + off, c0=0, nr=n, nc=h, dr0=lo, dc0=0))
+    return out
+
+
 class ZtpLayer:
     def __init__(self, ctx, h: int, f: int, N: int, rank: int, world: int, shards: Dict[str, torch.Tensor],
                  mig_cap: int = 0, dtype=torch.bfloat16, layer_id: int = 0):
@@ -187,19 +223,13 @@ class ZtpLayer:
 
     # --------------------------------------------------------------- migration
     def _xfers(self, grads: bool):
+        tens = {"w1": self.w1_t, "w2": self.w2_t, "dw1": self.dw1, "dw2": self.dw2}
         xs = []
-        for (src, dst, lo, hi, off) in self.mig.all_xfers:
-            n = hi - lo
-            if not grads:   # weights: owner's units [lo,hi) -> helper's appended slots [u+off, ...)
-                xs.append(Z.xfer(self.w1_t if self.rank == src else None, self.w1_t if self.rank == dst else None,
-                                 r0=0, c0=lo, nr=self.h, nc=n, dr0=0, dc0=self.u + off, src_rank=src, dst_rank=dst))
-                xs.append(Z.xfer(self.w2_t if self.rank == src else None, self.w2_t if self.rank == dst else None,
-                                 r0=lo, c0=0, nr=n, nc=self.h, dr0=self.u + off, dc0=0, src_rank=src, dst_rank=dst))
-            else:           # gradients back: helper's appended slots -> owner's [lo, hi)
-                xs.append(Z.xfer(self.dw1 if self.rank == dst else None, self.dw1 if self.rank == src else None,
-                                 r0=0, c0=self.u + off, nr=self.h, nc=n, dr0=0, dc0=lo, src_rank=dst, dst_rank=src))
-                xs.append(Z.xfer(self.dw2 if self.rank == dst else None, self.dw2 if self.rank == src else None,
-                                 r0=self.u + off, c0=0, nr=n, nc=self.h, dr0=lo, dc0=0, src_rank=dst, dst_rank=src))
+        for d in xfer_specs(self.mig, self.u, self.h, grads):
+            t = tens[d["t"]]
+            xs.append(Z.xfer(t if self.rank == d["src"] else None, t if self.rank == d["dst"] else None,
+                             r0=d["r0"], c0=d["c0"], nr=d["nr"], nc=d["nc"], dr0=d["dr0"], dc0=d["dc0"],
+                             src_rank=d["src"], dst_rank=d["dst"]))
         return xs
 
     def migrate_weights(self, stream=None):
