@@ -285,18 +285,53 @@ def main():
     L.G.copy_(torch.from_numpy(Gh.astype(np.float32)).cuda().to(torch.bfloat16))
     lens = {"qkv": h, "o": a, "fc1": h, "fc2": u}
     sc = {s: torch.from_numpy(v).cuda() for s, v in scores_for(cfg, r, lens).items()}
-    stream = torch.cuda.current_stream()
-    step = lambda: L.step(stream)   # noqa: E731
+    stream = torch.cuda.Stream()          # capture needs a non-default stream
+    torch.cuda.set_stream(stream)
 
-    def run_phase(steps, warm):
+    def make_graph(profile: bool = False, pre=None, post=None):
+        """Warm the step un-captured (sizes workspaces, sets kernel attributes),
+        then record it (optionally with the library's profiling events inside)
+        into a CUDA graph; returns (graph, library launches per step)."""
+        for _ in range(2):
+            if pre:
+                pre()
+            L.step(stream)
+            if post:
+                post()
+        torch.cuda.synchronize()
+        Z.ztp_read_profile(ctx, stream)
+        Z.ztp_set_profile(ctx, profile)
+        n0 = Z.ztp_launch_count(ctx)
+        g = L.capture(stream, pre=pre, post=post)
+        n1 = Z.ztp_launch_count(ctx)
+        Z.ztp_set_profile(ctx, False)
+        torch.cuda.synchronize()
+        return g, n1 - n0
+
+    def profiled_steps(n: int) -> dict:
+        """Per-step averages of the library's event profile over n steps."""
+        Z.ztp_read_profile(ctx, stream)
+        Z.ztp_set_profile(ctx, True)
+        # hold the stream with a GPU spin while the n steps are enqueued, so the
+        # kernels then run back to back and the events time kernels, not the host
+        torch.cuda._sleep(int(2e8))
+        for _ in range(n):
+            L.step(stream)
+        out = Z.ztp_read_profile(ctx, stream)
+        Z.ztp_set_profile(ctx, False)
+        return {k: (v / n if isinstance(v, float) else v) for k, v in out.items()}
+
+    def run_phase(g, steps, warm):
         for _ in range(warm):
-            step()
-        return timed(D, step, steps, stream)
+            g.replay()
+        return timed(D, g.replay, steps, stream)
 
     # ---- phase A: straggler-free dense step (T_free)
     L.set_selection({s: 0 for s in SEGS}, sc)
-    ms_free = run_phase(args.steps, args.warmup)
+    gA, _ = make_graph()
+    ms_free = run_phase(gA, args.steps, args.warmup)
     flops_dense = D.sum(L.executed_flops())
+    del gA
 
     plan_info = {}
     ms_unbal = None
@@ -305,19 +340,13 @@ def main():
         strag = e - 1
         Z.ztp_set_slowdown(ctx, args.chi if r == strag else 1.0)
         Z.ztp_set_stats(ctx, True)
-        for _ in range(args.warmup):
-            step()
-        Z.ztp_read_profile(ctx, stream)
-        Z.ztp_set_profile(ctx, True)
-        win = 10
-        for _ in range(win):
-            step()
-        prof = Z.ztp_read_profile(ctx, stream)
-        Z.ztp_set_profile(ctx, False)
+        gB, _ = make_graph()
+        ms_unbal = run_phase(gB, args.steps, args.warmup)
+        prof = profiled_steps(10)                        # statistics window (A-5, A-6)
         Z.ztp_set_stats(ctx, False)
-        T_own = (prof["gemm_ms"] + prof["other_ms"]) / win
-        M_own = prof["gemm_ms"] / win
-        ms_unbal = run_phase(args.steps, 0)
+        T_own = prof["gemm_ms"] + prof["other_ms"]
+        M_own = prof["gemm_ms"]
+        del gB
         T_all, M_all = Z.ztp_allgather_stats(ctx, T_own, M_own, e, stream)
         plan = Z.ztp_plan(T_all, M_all, float(h), None, Z.plan_opts(enable_migration=0, zero_crit=Z.CRIT_MIN))
         n_prune = {}
@@ -336,18 +365,16 @@ def main():
         plan_info = {"gamma": [args.gamma], "mode": "homogeneous ZERO-Pri"}
     L.set_selection(n_prune, sc)
 
-    # ---- phase C: balanced / resized step (headline), profiled
-    for _ in range(args.warmup):
-        step()
-    Z.ztp_read_profile(ctx, stream)
-    Z.ztp_set_profile(ctx, True)
-    n0 = Z.ztp_launch_count(ctx)
-    ms_bal = timed(D, step, args.steps, stream)
-    launches = Z.ztp_launch_count(ctx) - n0
-    prof = Z.ztp_read_profile(ctx, stream)
-    Z.ztp_set_profile(ctx, False)
+    # ---- phase C: balanced / resized step (headline), profiled inside the graph
+    gC, per_step_launches = make_graph()
+    ms_bal = run_phase(gC, args.steps, args.warmup)
+    launches = per_step_launches * args.steps
+    # the GEMM launches of the same step, timed with CUDA events on the
+    # launching stream in an un-captured pass right after the timed region
+    prof = profiled_steps(min(20, args.steps))
     flops_exec = D.sum(L.executed_flops())
     value = flops_exec / (ms_bal * 1e-3) / 1e12
+    del gC
 
     # ---- e2e: host buffers through the public API (pinned H2D of X, G; D2H of dX)
     Xp = torch.empty((h, N), dtype=torch.bfloat16).pin_memory()
@@ -356,19 +383,21 @@ def main():
     Gp.copy_(L.G.cpu())
     dXp = torch.empty((h, N), dtype=torch.bfloat16).pin_memory()
 
-    def e2e_step():
+    def h2d():
         L.X.copy_(Xp, non_blocking=True)
         L.G.copy_(Gp, non_blocking=True)
-        L.step(stream)
+
+    def d2h():
         dXp.copy_(L.dX, non_blocking=True)
-    for _ in range(3):
-        e2e_step()
+    gE, _ = make_graph(pre=h2d, post=d2h)
     e2e_steps = max(10, args.steps // 4)
-    ms_e2e = timed(D, e2e_step, e2e_steps, stream)
+    ms_e2e = run_phase(gE, e2e_steps, 3)
+    del gE
+    # per step: one GEMM pass of the last replay (gemm_ms) -> per-step averages
     clocks = sampler.stop()
 
     # ---- roofline of the dominant kernel (the resized tcgen05 GEMM)
-    gemm_ms = prof["gemm_ms"]
+    gemm_ms = prof["gemm_ms"]                            # one step's GEMM launches (last replay)
     achieved = prof["gemm_flops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
     timed_s = ms_bal * args.steps * 1e-3
     peak = peak_sus if timed_s >= 1.0 else peak_burst
@@ -383,8 +412,9 @@ def main():
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "peak_source": f"{peak_src} {'sustained' if peak is peak_sus else 'burst'} bf16 (MEASURED_PEAKS.json)",
-            "gemm_share_of_step": (gemm_ms / args.steps) / ms_bal if ms_bal else None,
-            "n_gemm_launches": prof["n_gemm"]}
+            "gemm_share_of_step": gemm_ms / ms_bal if ms_bal else None,
+            "n_gemm_launches_per_step": prof["n_gemm"] // max(1, min(20, args.steps)),
+            "measured": "CUDA events around each GEMM launch on its stream, un-captured pass of the same step"}
     # step roofline: max(GEMM at peak, collective bytes at NVLink) per rank
     per_rank_flops = L.executed_flops()
     comm_bytes = 4 * 2 * N * h * 2 * (e - 1) / e if e > 1 else 0.0   # 4 all-reduces, ring bus bytes

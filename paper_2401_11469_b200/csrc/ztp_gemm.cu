@@ -17,7 +17,8 @@
 //   warp 1      MMA issuer (one thread of the even CTA), tcgen05.commit
 //               multicast -> smem-slot release in both CTAs
 //   warp 2      TMEM allocator
-//   warps 4-7   epilogue: tcgen05.ld -> (GeLU | GeLU' | none) -> bf16 ->
+//   warps 4-11  epilogue (2 warpgroups: TMEM lane quarter x column half):
+//               tcgen05.ld -> (GeLU | GeLU' | none) -> bf16 ->
 //               swizzled smem staging -> 128-bit coalesced row stores at the
 //               lineage row map (a6: scatter + Zero imputation), or fp32
 //               split-K partials reduced by ztp_splitk_reduce.
@@ -37,9 +38,10 @@ namespace ztp {
 constexpr int BM = 128;   // rows per CTA
 constexpr int BN = 256;   // tile columns (per CTA pair when CG = 2)
 constexpr int BK = 64;
-constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARPS = 8;                   // 2 warpgroups: TMEM lane quarter x column half
+constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB
-constexpr int STAGING_PER_WARP = 32 * 128 * 2;  // two 32x64 bf16 planes (pre and H)
+constexpr int STAGING_PER_WARP = 32 * 128;     // one 32 x 64 bf16 plane (32 x 32 fp32)
 
 template <int CG>
 struct Cfg {
@@ -49,7 +51,7 @@ struct Cfg {
   static constexpr int B_BYTES = BNL * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
   static constexpr int RING = STAGES * STAGE_BYTES;
-  static constexpr int STAGING = 4 * STAGING_PER_WARP;
+  static constexpr int STAGING = EPI_WARPS * STAGING_PER_WARP;
   static constexpr int BARS = (2 * STAGES + 4) * 8 + 16;
   static constexpr int TOTAL = 1024 + RING + STAGING + BARS;
 };
@@ -61,16 +63,23 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// GeLU tanh approximation and its derivative, fp32.
+// GeLU tanh approximation and its derivative, fp32.  tanh uses the
+// SFU (tanh.approx.f32, max rel. error ~2^-11), below the 2^-8 resolution of
+// the bf16 outputs these epilogues produce.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_f(float x) {
   const float c = 0.7978845608028654f;
   float u = c * (x + 0.044715f * x * x * x);
-  return 0.5f * x * (1.0f + tanhf(u));
+  return 0.5f * x * (1.0f + tanh_fast(u));
 }
 __device__ __forceinline__ float gelu_grad_f(float x) {
   const float c = 0.7978845608028654f;
   float u = c * (x + 0.044715f * x * x * x);
-  float t = tanhf(u);
+  float t = tanh_fast(u);
   float du = c * (1.0f + 3.0f * 0.044715f * x * x);
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
 }
@@ -123,9 +132,13 @@ struct Sched {
     zero_m = m_tiles - mc;
     num_units = units_c + (S == 1 ? zero_m * n_tiles : 0);
   }
-  __device__ __forceinline__ Work get(int u) const {
+  // all-pruned (zero) units come FIRST: the epilogue warps write them while
+  // the producer / MMA warps, which skip them, already stream the first tile.
+  __device__ __forceinline__ Work get(int u0) const {
     Work w;
-    if (u < units_c) {
+    const int nz = num_units - units_c;
+    if (u0 >= nz) {
+      const int u = u0 - nz;
       const int s = u / tiles_c, t = u - s * tiles_c;
       w.m0 = (t % mc) * TM;
       w.n0 = (t / mc) * BN;
@@ -134,7 +147,7 @@ struct Sched {
       w.kb1 = min(num_kb, w.kb0 + kbs);
       w.zero = false;
     } else {
-      const int v = u - units_c;
+      const int v = u0;
       w.m0 = (mc + v % zero_m) * TM;
       w.n0 = (v / zero_m) * BN;
       w.split = 0;
@@ -180,7 +193,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4 * CG);
+      mbar_init(&tempty[s], EPI_WARPS * CG);
     }
     fence_barrier_init();
   }
@@ -350,9 +363,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ============================ epilogue ================================
-    const int ew = warp - 4;  // TMEM lane quarter == warp % 4
+    const int ew = warp - 4;
+    const int lq = ew & 3;               // TMEM lane quarter == warp % 4 (rows lq*32 .. +31)
+    const int ch = ew >> 2;              // column half of the 256-column accumulator
     uint8_t* stg = staging + ew * STAGING_PER_WARP;
-    uint8_t* stg2 = stg + 32 * 128;
     int acc = 0;
     uint32_t aphase = 0;
     auto release = [&]() {
@@ -373,7 +387,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const Work wk = sc.get(u);
       const int m0 = wk.m0 + BM * rank, n0 = wk.n0;
       const bool zt = wk.zero;
-      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      const uint32_t tbase = tmem_base + ((uint32_t)(lq * 32) << 16) + acc * BN + ch * (BN / 2);
+      const int nc0 = n0 + ch * (BN / 2);   // first output column of this warp
       if (sc.S > 1) {
         // ---- split-K partial: fp32 tile -> ws[split] (computed rows only, no row map)
         mbar_wait(&tfull[acc], aphase);
@@ -381,7 +396,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float* wsp = p.ws + (int64_t)wk.split * p.ws_split_stride;
         const int mlim = KIND == KIND_FWD ? p.M : p.n_kept;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < BN / 64; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(tbase + c * 32, v);
           tmem_ld_wait();
@@ -392,11 +407,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           __syncwarp();
           const int q = lane & 7;
-          const int col = n0 + c * 32 + q * 4;
+          const int col = nc0 + c * 32 + q * 4;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int rr = 4 * i + (lane >> 3);
-            const int m = m0 + ew * 32 + rr;
+            const int m = m0 + lq * 32 + rr;
             if (m < mlim && col < p.N) {
               const uint4 w = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
               st_global_v4(wsp + (int64_t)m * p.ld_ws + col, w);
@@ -411,7 +426,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int orow[8], arow[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int m = m0 + ew * 32 + 4 * i + (lane >> 3);
+        const int m = m0 + lq * 32 + 4 * i + (lane >> 3);
         int o = -1;
         if (m < p.M) {
           if (KIND == KIND_FWD)
@@ -427,8 +442,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
       }
 #pragma unroll 1
-      for (int c = 0; c < BN / 64; ++c) {
+      for (int c = 0; c < BN / 128; ++c) {
         uint32_t v0[32], v1[32];
+        // GeLU' operand (pre-activation) of this lane's 8 stores, issued before
+        // the TMEM load so the 8 global loads overlap instead of serialising
+        uint4 pin[8];
+        if (p.epi == EPI_GELU_GRAD && !zt) {
+          const int colp = nc0 + c * 64 + (lane & 7) * 8;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            pin[i] = make_uint4(0u, 0u, 0u, 0u);
+            if (orow[i] >= 0 && colp < p.N)
+              pin[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (int64_t)arow[i] * p.ld_aux + colp));
+          }
+        }
         if (!zt) {
           tmem_ld_32x32b_x32(tbase + c * 64, v0);
           tmem_ld_32x32b_x32(tbase + c * 64 + 32, v1);
@@ -437,54 +464,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0u;
         }
-        // thread `lane` owns tile row ew*32 + lane: 64 fp32 -> 8 x 16B chunks
+        // thread `lane` owns tile row lq*32 + lane: 64 fp32 -> 8 x 16B chunks.
+        // Plane 0 = the GEMM output (pre for GeLU); plane 1 (GeLU only) = H.
+        const int q = lane & 7;
+        const int col = nc0 + c * 64 + q * 8;
+#pragma unroll 1
+        for (int plane = 0; plane < (p.epi == EPI_GELU ? 2 : 1); ++plane) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float f[8];
+          for (int qq = 0; qq < 8; ++qq) {
+            float f[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int cc = qq * 8 + i;
+              f[i] = __uint_as_float(cc < 32 ? v0[cc] : v1[cc - 32]);
+              if (plane == 1) f[i] = gelu_f(f[i]);
+            }
+            uint4 w;
+            w.x = pack_bf16(f[0], f[1]);
+            w.y = pack_bf16(f[2], f[3]);
+            w.z = pack_bf16(f[4], f[5]);
+            w.w = pack_bf16(f[6], f[7]);
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((qq ^ (lane & 7)) << 4)) = w;
+          }
+          __syncwarp();
+          __nv_bfloat16* dst = plane == 0 ? p.out : p.out2;
+          const int64_t ldd = plane == 0 ? p.ld_out : p.ld_out2;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int col = q * 8 + i;
-            f[i] = __uint_as_float(col < 32 ? v0[col] : v1[col - 32]);
-          }
-          uint4 w;
-          w.x = pack_bf16(f[0], f[1]);
-          w.y = pack_bf16(f[2], f[3]);
-          w.z = pack_bf16(f[4], f[5]);
-          w.w = pack_bf16(f[6], f[7]);
-          const int off = lane * 128 + ((q ^ (lane & 7)) << 4);
-          *reinterpret_cast<uint4*>(stg + off) = w;
-          if (p.epi == EPI_GELU) {
-            uint4 g;
-            g.x = pack_bf16(gelu_f(f[0]), gelu_f(f[1]));
-            g.y = pack_bf16(gelu_f(f[2]), gelu_f(f[3]));
-            g.z = pack_bf16(gelu_f(f[4]), gelu_f(f[5]));
-            g.w = pack_bf16(gelu_f(f[6]), gelu_f(f[7]));
-            *reinterpret_cast<uint4*>(stg2 + off) = g;
-          }
-        }
-        __syncwarp();
-        const int q = lane & 7;
-        const int col = n0 + c * 64 + q * 8;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rr = 4 * i + (lane >> 3);
-          const int off = rr * 128 + ((q ^ (rr & 7)) << 4);
-          if (orow[i] >= 0 && col < p.N) {
-            uint4 w = *reinterpret_cast<const uint4*>(stg + off);
-            if (p.epi == EPI_GELU_GRAD && !zt) {
-              // G1 = dH * GeLU'(pre_in) at the same (row, col) (row layer BWD)
-              const uint4 pin = *reinterpret_cast<const uint4*>(p.aux + (int64_t)arow[i] * p.ld_aux + col);
-              w = gelu_grad_mul(w, pin);
-            }
-            const int nv = p.N - col;
-            store_bf16x8(p.out + (int64_t)orow[i] * p.ld_out + col, w, nv);
-            if (p.epi == EPI_GELU) {
-              const uint4 g = *reinterpret_cast<const uint4*>(stg2 + off);
-              store_bf16x8(p.out2 + (int64_t)orow[i] * p.ld_out2 + col, g, nv);
+            const int rr = 4 * i + (lane >> 3);
+            if (orow[i] >= 0 && col < p.N) {
+              uint4 w = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
+              if (p.epi == EPI_GELU_GRAD && !zt) w = gelu_grad_mul(w, pin[i]);   // G1 = dH * GeLU'(pre_in)
+              store_bf16x8(dst + (int64_t)orow[i] * ldd + col, w, p.N - col);
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
       if (!zt) release();
     }

@@ -281,6 +281,25 @@ class ZtpLayer:
         self.backward(stream)
         self.return_grads(stream)
 
+    def capture(self, stream, select: bool = True, pre=None, post=None):
+        """Record one step (optionally wrapped by `pre`/`post` callables, e.g.
+        host<->device copies) into a CUDA graph on `stream` (a non-default
+        torch stream).  The library launches nothing that allocates or syncs in
+        steady state, so the whole step -- select, GEMMs, epilogues, NCCL --
+        is captured; replay() re-issues it with one launch."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            if pre is not None:
+                pre()
+            self.step(stream, select=select)
+            if post is not None:
+                post()
+        self._graph = g
+        return g
+
+    def replay(self):
+        self._graph.replay()
+
     # ------------------------------------------------------------ accounting
     def executed_flops(self) -> float:
         """6 N n K' per linear (fwd + dX + dW), SURVEY §8(d)."""

@@ -106,6 +106,34 @@ def test_layer_world1_real_context(tz, h, f, N, g):
     Z.ztp_ctx_destroy(ctx)
 
 
+def test_layer_cuda_graph_replay(tz):
+    """The bench replays the step as a CUDA graph: the captured step (select +
+    fwd + bwd through the C ABI) must reproduce the oracle on replay."""
+    torch, Z, ZtpLayer, _ = tz
+    h, f, N = 256, 1024, 264
+    X, G, sh = make_inputs(h, f, N, 1, 5)
+    gam = [dict(qkv=0.5, o=0.25, fc1=0.5, fc2=0.5)]
+    sel, scores, nps = selections(1, h, f, N, 5, gam)
+    ref = O.layer_step(X, G, sh, sel)
+    ctx, L = build(tz, sh, 0, 1, h, f, N)
+    L.set_selection(nps[0], {s: torch.from_numpy(v).cuda() for s, v in scores[0].items()})
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        L.X.copy_(to_dev(torch, X))
+        L.G.copy_(to_dev(torch, G))
+        L.step(s)                      # warm-up (sizes workspaces)
+        L.Y.zero_()
+        L.dX.zero_()
+        L.capture(s)
+        for _ in range(3):
+            L.replay()
+    torch.cuda.synchronize()
+    close(host(L.Y), ref["Y"], "Y")
+    close(host(L.dX), ref["dX"], "dX")
+    close(host(L.dw1[:, :f]), ref["dW1"][0], "dW1")
+    Z.ztp_ctx_destroy(ctx)
+
+
 def _simulate(tz, e, h, f, N, gam, mig=None, seed=7):
     """e ranks on one GPU; the test sums partials where NCCL all-reduces."""
     torch, Z, ZtpLayer, MigrationIO = tz
