@@ -49,6 +49,7 @@ struct ztp_ctx {
   size_t cws_cap[2] = {0, 0};
   int use_gather4 = 0;                 // 1: gather rows in the GEMM producer with TMA gather4
   int allow_splitk = 1;                // split-K for few-tile GEMMs (ZTP_SPLITK=0 disables)
+  int dbg_epi = 0;                     // ZTP_DEBUG_EPI (performance experiments; results invalid)
   void* skws = nullptr;                // split-K fp32 partials
   size_t skws_cap = 0;
   // profiling (ztp_set_profile): event pairs around every kernel class
@@ -249,6 +250,9 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     p.epi = epi;
     p.out = (__nv_bfloat16*)out.ptr;
     p.ld_out = out.ld;
+    p.out_rows = (int)out.rows;
+    if (out2 && out2->rows != out.rows)
+      return fail(c, ZTP_ESHAPE, "gemm: " + shp("out2", *out2) + " must have the rows of " + shp("out", out));
     p.out2 = out2 ? (__nv_bfloat16*)out2->ptr : nullptr;
     p.ld_out2 = out2 ? out2->ld : 0;
     p.aux = aux ? (const __nv_bfloat16*)aux->ptr : nullptr;
@@ -256,6 +260,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     p.aux_by_m = aux_by_m;
     p.out_pos = out_pos;
     p.stamp = emulating(c) ? c->d_stamp : nullptr;
+    p.dbg = c->dbg_epi;
     // split-K over the contraction when the output has too few tiles for 148 SMs
     p.splits = c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, c->num_sms) : 1;
     if (p.splits > 1) {
@@ -553,6 +558,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   c->num_sms = prop.multiProcessorCount;
   if (const char* g4 = getenv("ZTP_GATHER4")) c->use_gather4 = atoi(g4) != 0;
   if (const char* sk = getenv("ZTP_SPLITK")) c->allow_splitk = atoi(sk) != 0;
+  if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   auto cleanup = [&](ztp_status s) {
     ztp_ctx_destroy(c);
     return s;

@@ -47,11 +47,11 @@ template <int CG>
 struct Cfg {
   static constexpr int BNL = BN / CG;                    // B columns staged by one CTA
   static constexpr int TM = BM * CG;                     // tile rows
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int STAGES = CG == 2 ? 5 : 3;
   static constexpr int B_BYTES = BNL * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
   static constexpr int RING = STAGES * STAGE_BYTES;
-  static constexpr int STAGING = EPI_WARPS * STAGING_PER_WARP;
+  static constexpr int STAGING = EPI_WARPS * 2 * STAGING_PER_WARP;   // ping-pong per warp
   static constexpr int BARS = (2 * STAGES + 4) * 8 + 16;
   static constexpr int TOTAL = 1024 + RING + STAGING + BARS;
 };
@@ -164,7 +164,8 @@ struct Sched {
 template <int KIND, int CG, bool AG, bool BG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ztp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmParams p) {
+                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
+                    const __grid_constant__ CUtensorMap tmW, const GemmParams p) {
   using C = Cfg<CG>;
   constexpr int STAGES = C::STAGES;
   constexpr int BNL = C::BNL;
@@ -366,7 +367,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp - 4;
     const int lq = ew & 3;               // TMEM lane quarter == warp % 4 (rows lq*32 .. +31)
     const int ch = ew >> 2;              // column half of the 256-column accumulator
-    uint8_t* stg = staging + ew * STAGING_PER_WARP;
+    uint8_t* const stg_base = staging + ew * 2 * STAGING_PER_WARP;
+    uint8_t* stg = stg_base;
+    int sk = 0;                          // staging buffers used so far (ping-pong)
     int acc = 0;
     uint32_t aphase = 0;
     auto release = [&]() {
@@ -389,87 +392,94 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool zt = wk.zero;
       const uint32_t tbase = tmem_base + ((uint32_t)(lq * 32) << 16) + acc * BN + ch * (BN / 2);
       const int nc0 = n0 + ch * (BN / 2);   // first output column of this warp
+      // Two staging buffers per warp alternate: before refilling one, the
+      // lanes that issued TMA stores wait until at most the other buffer's
+      // store is still reading (bulk wait_group.read 1).
+      auto staging_free = [&]() {
+        if (lane < 8) bulk_wait_read1();
+        __syncwarp();
+        stg = stg_base + (sk & 1) * STAGING_PER_WARP;
+        ++sk;
+      };
       if (sc.S > 1) {
-        // ---- split-K partial: fp32 tile -> ws[split] (computed rows only, no row map)
+        // ---- split-K partial: fp32 tile -> ws[split] via TMA box stores
+        //      (rows >= n_kept / cols >= N are outside the ws map: not written)
         mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
-        float* wsp = p.ws + (int64_t)wk.split * p.ws_split_stride;
-        const int mlim = KIND == KIND_FWD ? p.M : p.n_kept;
 #pragma unroll 1
         for (int c = 0; c < BN / 64; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(tbase + c * 32, v);
           tmem_ld_wait();
+          if (c == BN / 64 - 1) release();   // accumulator fully in registers: TMEM free
+          staging_free();
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const uint4 w = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) = w;
-          }
+          for (int q = 0; q < 8; ++q)
+            st_shared_v4(stg + lane * 128 + ((q ^ (lane & 7)) << 4),
+                         make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+          fence_proxy_async_smem();
           __syncwarp();
-          const int q = lane & 7;
-          const int col = nc0 + c * 32 + q * 4;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = 4 * i + (lane >> 3);
-            const int m = m0 + lq * 32 + rr;
-            if (m < mlim && col < p.N) {
-              const uint4 w = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
-              st_global_v4(wsp + (int64_t)m * p.ld_ws + col, w);
-            }
+          if (lane == 0) {
+            tma_store_3d(&tmW, stg, nc0 + c * 32, m0 + lq * 32, wk.split);
+            bulk_commit();
           }
-          __syncwarp();
         }
-        release();
         continue;
       }
-      // output rows this lane stores: r = 4 i + lane / 8, i = 0..7
-      int orow[8], arow[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int m = m0 + lq * 32 + 4 * i + (lane >> 3);
-        int o = -1;
-        if (m < p.M) {
-          if (KIND == KIND_FWD)
-            o = p.out_pos ? __ldg(p.out_pos + m) : m;   // producer-side compaction for the next layer
-          else
-            o = (m < p.n_kept) ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
-        }
-        orow[i] = o;
-        arow[i] = p.aux_by_m ? m : o;
+      // this lane owns tile row m = m0 + lq*32 + lane; its output row index
+      const int m = m0 + lq * 32 + lane;
+      int orow = p.oob_out;                       // rows outside the output are not written
+      int arow = 0;
+      if (m < p.M) {
+        int o;
+        if (KIND == KIND_FWD)
+          o = p.out_pos ? __ldg(p.out_pos + m) : m;   // producer-side compaction for the next layer
+        else
+          o = (m < p.n_kept) ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
+        if (o >= 0) orow = o;
+        arow = p.aux_by_m ? m : o;
       }
+      const bool dense_out = KIND == KIND_FWD && p.out_pos == nullptr;
+      // rows of the 4-row scatter group this lane issues (lanes 0..7)
+      int sr[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sr[j] = __shfl_sync(0xFFFFFFFFu, orow, (4 * lane + j) & 31);
       if (!zt) {
         mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
       }
+      if (p.dbg & 2) {
+        if (!zt) release();
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN / 128; ++c) {
+        const int col0 = nc0 + c * 64;
         uint32_t v0[32], v1[32];
-        // GeLU' operand (pre-activation) of this lane's 8 stores, issued before
-        // the TMEM load so the 8 global loads overlap instead of serialising
+        // GeLU' operand: this lane's row of the pre-activation, loaded before
+        // the TMEM load so the global loads overlap it
         uint4 pin[8];
         if (p.epi == EPI_GELU_GRAD && !zt) {
-          const int colp = nc0 + c * 64 + (lane & 7) * 8;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             pin[i] = make_uint4(0u, 0u, 0u, 0u);
-            if (orow[i] >= 0 && colp < p.N)
-              pin[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (int64_t)arow[i] * p.ld_aux + colp));
+            if (m < p.n_kept && col0 + 8 * i < p.N)
+              pin[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (int64_t)arow * p.ld_aux + col0 + 8 * i));
           }
         }
         if (!zt) {
           tmem_ld_32x32b_x32(tbase + c * 64, v0);
           tmem_ld_32x32b_x32(tbase + c * 64 + 32, v1);
           tmem_ld_wait();
+          if (c == BN / 128 - 1) release();   // accumulator fully in registers: TMEM free for tile i+2
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0u;
         }
-        // thread `lane` owns tile row lq*32 + lane: 64 fp32 -> 8 x 16B chunks.
         // Plane 0 = the GEMM output (pre for GeLU); plane 1 (GeLU only) = H.
-        const int q = lane & 7;
-        const int col = nc0 + c * 64 + q * 8;
 #pragma unroll 1
         for (int plane = 0; plane < (p.epi == EPI_GELU ? 2 : 1); ++plane) {
+          staging_free();
 #pragma unroll
           for (int qq = 0; qq < 8; ++qq) {
             float f[8];
@@ -484,25 +494,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             w.y = pack_bf16(f[2], f[3]);
             w.z = pack_bf16(f[4], f[5]);
             w.w = pack_bf16(f[6], f[7]);
-            *reinterpret_cast<uint4*>(stg + lane * 128 + ((qq ^ (lane & 7)) << 4)) = w;
+            if (p.epi == EPI_GELU_GRAD && !zt) w = gelu_grad_mul(w, pin[qq]);   // G1 = dH * GeLU'(pre_in)
+            st_shared_v4(stg + lane * 128 + ((qq ^ (lane & 7)) << 4), w);
           }
+          fence_proxy_async_smem();
           __syncwarp();
-          __nv_bfloat16* dst = plane == 0 ? p.out : p.out2;
-          const int64_t ldd = plane == 0 ? p.ld_out : p.ld_out2;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = 4 * i + (lane >> 3);
-            if (orow[i] >= 0 && col < p.N) {
-              uint4 w = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
-              if (p.epi == EPI_GELU_GRAD && !zt) w = gelu_grad_mul(w, pin[i]);   // G1 = dH * GeLU'(pre_in)
-              store_bf16x8(dst + (int64_t)orow[i] * ldd + col, w, p.N - col);
+          if (!(p.dbg & 1)) {
+            const CUtensorMap* tm = plane == 0 ? &tmO : &tmO2;
+            if (dense_out) {
+              if (lane == 0) {
+                tma_store_2d(tm, stg, col0, m0 + lq * 32);
+                bulk_commit();
+              }
+            } else if (lane < 8) {
+              tma_scatter4(tm, stg + lane * 512, col0, sr[0], sr[1], sr[2], sr[3]);
+              bulk_commit();
             }
           }
-          __syncwarp();
         }
       }
-      if (!zt) release();
     }
+    if (lane < 8) bulk_wait0();   // all output writes performed before the CTA exits
   }
 
   tc_fence_before();
@@ -590,20 +602,39 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// bf16 row-major [rows, cols] with leading dimension ld (elements); box = box_cols x box_rows.
+// Row-major [rows, cols] with leading dimension ld (elements); box = box_cols x box_rows.
 static bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, uint32_t box_cols,
-                     uint32_t box_rows) {
+                     uint32_t box_rows, bool f32 = false) {
   auto enc = get_encode();
   if (!enc) return false;
+  const int64_t es = f32 ? 4 : 2;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
   cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// fp32 split-K workspace [splits][rows][ld]: box 32 x 32 x 1 (128-byte rows).
+static bool make_ws_map(CUtensorMap* m, const float* ptr, int64_t splits, int64_t rows, int64_t cols, int64_t ld) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)splits};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(rows * ld * 4)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+struct Maps {
+  CUtensorMap a, b, o, o2, w;
+};
 
 static int units_of(int kind, int cg, const GemmParams& p) {
   const int tm = BM * cg;
@@ -614,8 +645,7 @@ static int units_of(int kind, int cg, const GemmParams& p) {
 }
 
 template <int KIND, int CG, bool AG, bool BG>
-static cudaError_t launch_kind(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int num_sms,
-                               cudaStream_t st) {
+static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms, cudaStream_t st) {
   static bool attr_set = false;
   const int smem = Cfg<CG>::TOTAL;
   auto kern = ztp_gemm_kernel<KIND, CG, AG, BG>;
@@ -639,7 +669,7 @@ static cudaError_t launch_kind(const CUtensorMap& a, const CUtensorMap& b, const
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, mp.w, p);
     if (e != cudaSuccess) return e;
   }
   if (p.splits == 1) return cudaSuccess;
@@ -674,45 +704,55 @@ size_t gemm_ws_bytes(int kind, int M, int N, int n_kept, int splits) {
 }
 
 template <int KIND, int CG>
-static cudaError_t dispatch(bool ag, bool bg, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                            int num_sms, cudaStream_t st) {
+static cudaError_t dispatch(bool ag, bool bg, const Maps& mp, const GemmParams& p, int num_sms, cudaStream_t st) {
   if (KIND != KIND_FWD && bg) return cudaErrorInvalidValue;
-  if (ag && bg) return launch_kind<KIND, CG, true, true>(ta, tb, p, num_sms, st);
-  if (ag) return launch_kind<KIND, CG, true, false>(ta, tb, p, num_sms, st);
-  if (bg) return launch_kind<KIND, CG, false, true>(ta, tb, p, num_sms, st);
-  return launch_kind<KIND, CG, false, false>(ta, tb, p, num_sms, st);
+  if (ag && bg) return launch_kind<KIND, CG, true, true>(mp, p, num_sms, st);
+  if (ag) return launch_kind<KIND, CG, true, false>(mp, p, num_sms, st);
+  if (bg) return launch_kind<KIND, CG, false, true>(mp, p, num_sms, st);
+  return launch_kind<KIND, CG, false, false>(mp, p, num_sms, st);
 }
 
-// Operand A / B tensor maps per kind (see the header comment of this file).
+// Operand, output and workspace tensor maps per kind (see the file header).
 cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_sms, cudaStream_t st) {
-  CUtensorMap ta, tb;
+  Maps mp;
   bool ok = true;
   const bool ag = o.a_gather, bg = o.b_gather;
   const int cg = gemm_choose_cg(kind, p.M, p.n_kept);
   const uint32_t bnl = BN / cg;
   p.oob_row = (int)(o.a_rows > o.b_rows ? o.a_rows : o.b_rows);  // outside every gathered tensor
+  p.oob_out = p.out_rows;                                        // TMA stores skip this row
   if (kind == KIND_FWD) {
     // A = W^T [K|K', n] MN-major; B = X^T [K|K', N] MN-major (same rows)
-    ok &= make_map(&ta, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : 64);
-    ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, bg ? 1 : 64);
+    ok &= make_map(&mp.a, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : 64);
+    ok &= make_map(&mp.b, o.b, o.b_rows, o.b_cols, o.b_ld, 64, bg ? 1 : 64);
   } else if (kind == KIND_DX) {
     // A = W^T [K|K', n_out] K-major; B = G^T [n_out, N] MN-major 64 x 64 boxes
-    ok &= make_map(&ta, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : BM);
-    ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, 64);
+    ok &= make_map(&mp.a, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : BM);
+    ok &= make_map(&mp.b, o.b, o.b_rows, o.b_cols, o.b_ld, 64, 64);
   } else {
     // A = X^T [K|K', N] K-major; B = G^T [n_out, N] K-major box 64 x BN/cg
-    ok &= make_map(&ta, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : BM);
-    ok &= make_map(&tb, o.b, o.b_rows, o.b_cols, o.b_ld, 64, bnl);
+    ok &= make_map(&mp.a, o.a, o.a_rows, o.a_cols, o.a_ld, 64, ag ? 1 : BM);
+    ok &= make_map(&mp.b, o.b, o.b_rows, o.b_cols, o.b_ld, 64, bnl);
+  }
+  // outputs: dense box stores (32 rows x 64 columns) or 4-row scatters at the row map
+  const bool dense_out = kind == KIND_FWD && p.out_pos == nullptr;
+  ok &= make_map(&mp.o, p.out, p.out_rows, p.N, p.ld_out, 64, dense_out ? 32 : 1);
+  if (p.epi == EPI_GELU)
+    ok &= make_map(&mp.o2, p.out2, p.out_rows, p.N, p.ld_out2, 64, dense_out ? 32 : 1);
+  else
+    mp.o2 = mp.o;
+  if (p.splits > 1) {
+    const int64_t rows = kind == KIND_FWD ? p.M : std::min(p.M, p.n_kept);
+    ok &= make_ws_map(&mp.w, p.ws, p.splits, rows, p.N, p.ld_ws);
+  } else {
+    mp.w = mp.o;
   }
   if (!ok) return cudaErrorInvalidValue;
   if (kind == KIND_FWD)
-    return cg == 2 ? dispatch<KIND_FWD, 2>(ag, bg, ta, tb, p, num_sms, st)
-                   : dispatch<KIND_FWD, 1>(ag, bg, ta, tb, p, num_sms, st);
+    return cg == 2 ? dispatch<KIND_FWD, 2>(ag, bg, mp, p, num_sms, st) : dispatch<KIND_FWD, 1>(ag, bg, mp, p, num_sms, st);
   if (kind == KIND_DX)
-    return cg == 2 ? dispatch<KIND_DX, 2>(ag, bg, ta, tb, p, num_sms, st)
-                   : dispatch<KIND_DX, 1>(ag, bg, ta, tb, p, num_sms, st);
-  return cg == 2 ? dispatch<KIND_DW, 2>(ag, bg, ta, tb, p, num_sms, st)
-                 : dispatch<KIND_DW, 1>(ag, bg, ta, tb, p, num_sms, st);
+    return cg == 2 ? dispatch<KIND_DX, 2>(ag, bg, mp, p, num_sms, st) : dispatch<KIND_DX, 1>(ag, bg, mp, p, num_sms, st);
+  return cg == 2 ? dispatch<KIND_DW, 2>(ag, bg, mp, p, num_sms, st) : dispatch<KIND_DW, 1>(ag, bg, mp, p, num_sms, st);
 }
 
 }  // namespace ztp

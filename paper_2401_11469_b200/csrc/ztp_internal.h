@@ -32,6 +32,9 @@ struct GemmParams {
   int splits, kb_per_split;
   float* ws;
   int64_t ld_ws, ws_split_stride;
+  int dbg;   // performance experiments only (ZTP_DEBUG_EPI): 1 skip stores, 2 skip the epilogue body
+  int oob_out;   // a row index outside the output tensor (TMA stores skip it)
+  int out_rows;  // rows of the output tensor(s)
 };
 
 // Split-K choice for a launch and the fp32 workspace it needs (bytes).

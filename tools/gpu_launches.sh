@@ -2,4 +2,3 @@
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 timeout -s KILL 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1
-tail -3 gpurun_out/ncu_bench.log

@@ -25,7 +25,14 @@ P = torch.sort(perm[:npr]).values.int().cuda() if npr else torch.zeros(1, dtype=
 xs = torch.empty(K - npr, N, device="cuda", dtype=torch.bfloat16)
 ws = torch.empty(K - npr, n, device="cuda", dtype=torch.bfloat16)
 s = Z.sel(S, K - npr, P, npr, 0, 0)
-a = Z.linear_args(x_t=x, w_t=w, y_t=y, g_t=g, dx_t=dx, dw_t=dw, sel_=s, xs_t=xs, ws_t=ws)
+act = os.environ.get("ACT", "")
+pre = torch.empty(n, N, device="cuda", dtype=torch.bfloat16)
+pin = torch.randn(K, N, device="cuda").bfloat16()
+if act == "gelu":
+    a = Z.linear_args(x_t=x, w_t=w, y_t=y, pre_t=pre, g_t=g, dx_t=dx, dw_t=dw, sel_=s, xs_t=xs, ws_t=ws,
+                      act=Z.ACT_GELU, act_in=Z.ACT_GELU, pre_in_t=pin)
+else:
+    a = Z.linear_args(x_t=x, w_t=w, y_t=y, g_t=g, dx_t=dx, dw_t=dw, sel_=s, xs_t=xs, ws_t=ws)
 for it in range(2):
     for kind in (Z.KIND_FWD, Z.KIND_DX, Z.KIND_DW):
         Z.ztp_gemm(ctx, kind, a)
