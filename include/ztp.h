@@ -243,7 +243,12 @@ ztp_status ztp_select(ztp_ctx* ctx, int nseg, const int32_t* h_seg_len, const in
  * ------------------------------------------------------------------------- */
 typedef enum ztp_phase { ZTP_FWD = 0, ZTP_BWD = 1 } ztp_phase;
 typedef enum ztp_impute { ZTP_IMPUTE_ZERO = 0, ZTP_IMPUTE_AVERAGE = 1, ZTP_IMPUTE_SAME = 2 } ztp_impute;
-typedef enum ztp_act { ZTP_ACT_NONE = 0, ZTP_ACT_GELU = 1 } ztp_act;
+/* GELU: FWD pre_t <- pre, BWD (act_in) dx *= GeLU'(pre_in_t).
+ * GELU_D: FWD pre_t <- GeLU'(pre) -- the derivative the consumer's backward
+ * needs, computed from the fp32 accumulator with the tanh the GeLU already
+ * evaluates -- and BWD (act_in) dx *= pre_in_t.  Same results as GELU
+ * (A-34); the backward epilogue is one multiply. */
+typedef enum ztp_act { ZTP_ACT_NONE = 0, ZTP_ACT_GELU = 1, ZTP_ACT_GELU_D = 2 } ztp_act;
 
 typedef struct ztp_sel {
   const int32_t* kept;
@@ -263,9 +268,20 @@ typedef struct ztp_linear_args {
   const ztp_sel* sel;          /* lineage entry; NULL = dense */
   const int32_t* y_pos;        /* FWD, optional: output unit j is written to row y_pos[j] of y_t / pre_t
                                   and dropped if y_pos[j] < 0 -- the next layer's compaction done by this
-                                  epilogue (device array of n_out entries) */
+                                  epilogue (device array of n_out entries).  With out_sel: required, the
+                                  inverse of out_sel->kept (ztp_select's `pos` of that segment). */
   int32_t x_compact;           /* x_t (and pre_in_t) already hold only rows S, in lineage order */
-  int32_t _pad0;
+  int32_t dx_compact;          /* row BWD: dx_t receives only rows S, row i <- unit kept[i]; the Zero
+                                  rows P are implied, not written (consumed by the producer's out_sel) */
+  /* Output-side lineage (col layer feeding a row layer, DESIGN.md "Output
+   * pruning"): the consumer's entry over this layer's n_out outputs (its
+   * kept S' and pruned P' units, S' + P' = n_out).  The consumer contracts
+   * only over S' and Zero-imputes the gradient of P', so:
+   *  FWD computes y / pre only for j in S' (row i <- unit S'[i], compact);
+   *  BWD reads g_t compact (row i <- unit S'[i], the consumer's dx_compact),
+   *      contracts dX over S' only, and writes dw_t[k, p] = 0 for p in P'.
+   * Results are identical to the full-output computation.  NULL = off. */
+  const ztp_sel* out_sel;
   int64_t n_out;               /* output units computed (<= w_t.cols); 0 = w_t.cols */
   int32_t impute;              /* ztp_impute (Zero is the paper's choice) */
   int32_t act;                 /* FWD activation of this layer's output */

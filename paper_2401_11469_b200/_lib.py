@@ -18,7 +18,7 @@ STATUS = ["ZTP_OK", "ZTP_EINVAL", "ZTP_ESHAPE", "ZTP_EINDEX", "ZTP_EDEGENERATE",
 BF16, F32 = 0, 1
 FWD, BWD = 0, 1
 IMPUTE_ZERO, IMPUTE_AVERAGE, IMPUTE_SAME = 0, 1, 2
-ACT_NONE, ACT_GELU = 0, 1
+ACT_NONE, ACT_GELU, ACT_GELU_D = 0, 1, 2
 CRIT_AVG, CRIT_MIN = 0, 1
 NORMAL, RESIZE, MIGRATE, SPLIT = 0, 1, 2, 3
 KIND_FWD, KIND_DX, KIND_DW = 0, 1, 2
@@ -72,7 +72,8 @@ class Sel(C.Structure):
 class LinearArgs(C.Structure):
     _fields_ = [("x_t", Mat), ("w_t", Mat), ("y_t", Mat), ("pre_t", Mat), ("g_t", Mat), ("dx_t", Mat),
                 ("dw_t", Mat), ("pre_in_t", Mat), ("xs_t", Mat), ("ws_t", Mat), ("sel", C.POINTER(Sel)),
-                ("y_pos", C.c_void_p), ("x_compact", C.c_int32), ("_pad0", C.c_int32), ("n_out", C.c_int64),
+                ("y_pos", C.c_void_p), ("x_compact", C.c_int32), ("dx_compact", C.c_int32),
+                ("out_sel", C.POINTER(Sel)), ("n_out", C.c_int64),
                 ("impute", C.c_int32), ("act", C.c_int32), ("act_in", C.c_int32), ("gather_output", C.c_int32),
                 ("input_is_parallel", C.c_int32), ("skip_collective", C.c_int32),
                 ("hist_dx", C.POINTER(Mat)), ("hist_dw", C.POINTER(Mat))]

@@ -190,7 +190,7 @@ struct Src {
 //   DW : A = X^T source, B = G^T
 ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t* kept, const int32_t* pruned,
                 int nk, const ztp_mat& out, const ztp_mat* out2, const ztp_mat* aux, int aux_by_m,
-                const int32_t* out_pos, int epi, cudaStream_t st) {
+                const int32_t* out_pos, int epi, cudaStream_t st, bool out_compact = false) {
   const int dtype = A.m->dtype;
   {
     const ztp_mat* need[3] = {A.m, B.m, &out};
@@ -259,6 +259,9 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     p.ld_aux = aux ? aux->ld : 0;
     p.aux_by_m = aux_by_m;
     p.out_pos = out_pos;
+    // identity row map: compact outputs, or a dense lineage (S = 0..K-1)
+    p.out_dense = out_compact || (kind == ztp::KIND_FWD ? out_pos == nullptr
+                                                        : (kept == c->d_iota && pruned == nullptr && M <= nk));
     p.stamp = emulating(c) ? c->d_stamp : nullptr;
     p.dbg = c->dbg_epi;
     // split-K over the contraction when the output has too few tiles for 148 SMs
@@ -312,6 +315,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.g = (const float*)b.ptr;
       p.ld_g = b.ld;
     }
+    if (out_compact) return fail(c, ZTP_EUNSUPPORTED, "f32 path: compact outputs");
     p.out = (float*)out.ptr;
     p.ld_out = out.ld;
     p.out2 = out2 ? (float*)out2->ptr : nullptr;
@@ -368,6 +372,42 @@ ztp_status compact_rows(ztp_ctx* c, const ztp_mat& full, const int32_t* kept, in
   return ZTP_OK;
 }
 
+// W^T[S, S'] (rows = this layer's kept S, or all rows when dense; columns =
+// the consumer's kept S') into ws_t or ctx workspace slot 1 (output pruning).
+// BWD (refill = false) reuses the copy FWD wrote into a caller ws_t.
+ztp_status weight_2d(ztp_ctx* c, const ztp_mat& w, const int32_t* rows, int nk, const int32_t* cols, int n_y,
+                     const ztp_mat& cbuf, bool refill, ztp_mat* tmp, Src* out, cudaStream_t st) {
+  ztp_mat d = cbuf;
+  if (d.ptr) {
+    if (!mat_ok(d) || d.rows < nk || d.cols < n_y || d.dtype != w.dtype)
+      return fail(c, ZTP_ESHAPE, "out_sel: compact weight " + shp("ws_t", d) + " needs [" + std::to_string(nk) +
+                                     ", " + std::to_string(n_y) + "]");
+  } else {
+    const int64_t ld = (n_y + 7) / 8 * 8;
+    const size_t bytes = ((size_t)nk * ld * 2 + 1023) & ~size_t(1023);
+    if (c->cws_cap[1] < bytes) {
+      if (c->cws[1]) cudaFree(c->cws[1]);
+      c->cws[1] = nullptr;
+      c->cws_cap[1] = 0;
+      CUDA_TRY(c, cudaMalloc(&c->cws[1], bytes));
+      c->cws_cap[1] = bytes;
+    }
+    d = ztp_mat{c->cws[1], nk, n_y, ld, w.dtype, 0};
+    refill = true;
+  }
+  d.rows = nk;
+  d.cols = n_y;
+  if (refill) {
+    const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
+    CUDA_TRY(c, ztp::gather_2d_launch(w.ptr, w.ld, rows, nk, cols, n_y, d.ptr, d.ld, st));
+    prof_end(c, pe, st);
+    ++c->launches;
+  }
+  *tmp = d;
+  *out = Src{tmp, true};
+  return ZTP_OK;
+}
+
 enum { LAYER_COL = 0, LAYER_ROW = 1 };
 
 // Source of the weight (or input) operand for this call.
@@ -415,6 +455,18 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
   ztp_status s = resolve_sel(c, a->sel, K, &kept, &pruned, &nk, &np);
   if (s != ZTP_OK) return s;
   const bool dense_sel = a->sel == nullptr;
+  // output pruning: only the consumer's kept outputs S' are computed / consumed
+  const ztp_sel* os = a->out_sel;
+  int64_t n_y = n_out;
+  if (os) {
+    if (dtype != ZTP_BF16) return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + ": out_sel needs bf16");
+    if ((int64_t)os->n_kept + os->n_pruned != n_out)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + ": out_sel n_kept + n_pruned != n_out " + std::to_string(n_out));
+    if (os->n_kept < 1) return fail(c, ZTP_EDEGENERATE, std::string(nm) + ": out_sel keeps no output");
+    if (!os->kept || !a->y_pos) return fail(c, ZTP_EINVAL, std::string(nm) + ": out_sel needs its kept list and y_pos");
+    n_y = os->n_kept;
+  }
+  const bool dxc = a->dx_compact != 0 && !dense_sel;
   const std::pair<int, int> key = a->sel ? std::make_pair(a->sel->layer_id, a->sel->matrix_id) : std::make_pair(-1, -1);
   const bool xc = a->x_compact != 0;
   const int64_t x_rows_need = xc ? nk : K;
@@ -427,8 +479,9 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
       return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD: " + shp("x_t", x) + " vs " + shp("w_t", a->w_t) +
                                      (xc ? " (compact x: needs n_kept rows)" : ""));
     const int64_t N = x.cols;
-    const bool act = a->act == ZTP_ACT_GELU;
-    const int64_t out_rows_need = a->y_pos ? 1 : n_out;
+    const bool act = a->act == ZTP_ACT_GELU || a->act == ZTP_ACT_GELU_D;
+    const int act_epi = a->act == ZTP_ACT_GELU_D ? ztp::EPI_GELU_D : ztp::EPI_GELU;
+    const int64_t out_rows_need = os ? n_y : (a->y_pos ? 1 : n_out);
     if (!mat_ok(a->y_t) || a->y_t.rows < out_rows_need || a->y_t.cols != N || a->y_t.dtype != dtype)
       return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD: " + shp("y_t", a->y_t) + " for n_out " + std::to_string(n_out));
     if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
@@ -437,10 +490,13 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     if (a->sel) c->lineage[key] = LineageEntry{a->sel->kept, a->sel->pruned, a->sel->n_kept, a->sel->n_pruned};
     s = operand_src(c, dense_sel, xc, x, a->xs_t, true, kept, nk, 0, &tmpx, &X, st);
     if (s != ZTP_OK) return s;
-    s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, true, kept, nk, 1, &tmpw, &W, st);
+    if (os)
+      s = weight_2d(c, a->w_t, dense_sel ? nullptr : kept, nk, os->kept, (int)n_y, a->ws_t, true, &tmpw, &W, st);
+    else
+      s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, true, kept, nk, 1, &tmpw, &W, st);
     if (s != ZTP_OK) return s;
-    s = gemm(c, ztp::KIND_FWD, W, X, n_out, kept, pruned, nk, act ? a->pre_t : a->y_t, act ? &a->y_t : nullptr,
-             nullptr, 0, a->y_pos, act ? ztp::EPI_GELU : ztp::EPI_NONE, st);
+    s = gemm(c, ztp::KIND_FWD, W, X, n_y, kept, pruned, nk, act ? a->pre_t : a->y_t, act ? &a->y_t : nullptr,
+             nullptr, 0, os ? nullptr : a->y_pos, act ? act_epi : ztp::EPI_NONE, st);
     if (s != ZTP_OK) return s;
     if (layer == LAYER_ROW && !a->skip_collective) return allreduce(c, a->y_t, st);
     return ZTP_OK;
@@ -455,25 +511,34 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
                       std::to_string(key.first) + ", matrix " + std::to_string(key.second) + "> (S:400)");
   }
   const ztp_mat& g = a->g_t;
-  if (!mat_ok(g) || g.rows < n_out || g.dtype != dtype)
+  if (!mat_ok(g) || g.rows < n_y || g.dtype != dtype)
     return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("g_t", g));
   const int64_t N = g.cols;
   if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
   if (a->dx_t.ptr) {
-    if (!mat_ok(a->dx_t) || a->dx_t.rows != K || a->dx_t.cols != N || a->dx_t.dtype != dtype)
-      return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dx_t", a->dx_t) + " vs K " + std::to_string(K));
+    if (!mat_ok(a->dx_t) || (dxc ? a->dx_t.rows < nk : a->dx_t.rows != K) || a->dx_t.cols != N ||
+        a->dx_t.dtype != dtype)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dx_t", a->dx_t) + " vs K " + std::to_string(K) +
+                                     (dxc ? " (compact dx: n_kept rows)" : ""));
+    if (dxc && a->act_in != ZTP_ACT_NONE && !xc)
+      return fail(c, ZTP_EINVAL, std::string(nm) + " BWD: dx_compact with GeLU' needs x_compact pre_in_t");
     int epi = ztp::EPI_NONE;
     const ztp_mat* aux = nullptr;
-    if (layer == LAYER_ROW && a->act_in == ZTP_ACT_GELU) {
+    if (layer == LAYER_ROW && (a->act_in == ZTP_ACT_GELU || a->act_in == ZTP_ACT_GELU_D)) {
       if (!mat_ok(a->pre_in_t) || a->pre_in_t.rows < x_rows_need || a->pre_in_t.cols != N)
         return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD GeLU': " + shp("pre_in_t", a->pre_in_t));
-      epi = ztp::EPI_GELU_GRAD;
+      epi = a->act_in == ZTP_ACT_GELU_D ? ztp::EPI_MUL : ztp::EPI_GELU_GRAD;
       aux = &a->pre_in_t;
     }
-    s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, false, kept, nk, 1, &tmpw, &W, st);
+    if (os)
+      s = weight_2d(c, a->w_t, dense_sel ? nullptr : kept, nk, os->kept, (int)n_y, a->ws_t, false, &tmpw, &W, st);
+    else
+      s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, false, kept, nk, 1, &tmpw, &W, st);
     if (s != ZTP_OK) return s;
-    s = gemm(c, ztp::KIND_DX, W, Src{&g, true}, n_out, kept, pruned, nk, a->dx_t, nullptr, aux, xc ? 1 : 0,
-             nullptr, epi, st);
+    ztp_mat dx = a->dx_t;
+    if (dxc) dx.rows = nk;   // rows P implied Zero, not written
+    s = gemm(c, ztp::KIND_DX, W, Src{&g, true}, n_y, kept, dxc ? nullptr : pruned, nk, dx, nullptr, aux, xc ? 1 : 0,
+             nullptr, epi, st, dxc);
     if (s != ZTP_OK) return s;
   }
   const bool reduce_dx = layer == LAYER_COL && a->dx_t.ptr && !a->skip_collective && c->world > 1;
@@ -493,9 +558,16 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
       return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dw_t", a->dw_t));
     s = operand_src(c, dense_sel, xc, x, a->xs_t, false, kept, nk, 0, &tmpx, &X, st);
     if (s != ZTP_OK) return s;
-    s = gemm(c, ztp::KIND_DW, X, Src{&g, true}, n_out, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
+    s = gemm(c, ztp::KIND_DW, X, Src{&g, true}, n_y, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
              ztp::EPI_NONE, st);
     if (s != ZTP_OK) return s;
+    if (os) {
+      // columns S' were written compact; spread them to their units, P' <- Zero
+      const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
+      CUDA_TRY(c, ztp::expand_cols_launch(a->dw_t.ptr, a->dw_t.ld, (int)K, a->y_pos, (int)n_y, (int)n_out, st));
+      prof_end(c, pe, st);
+      ++c->launches;
+    }
   }
   if (reduce_dx) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_b, 0));
   return ZTP_OK;
@@ -700,19 +772,21 @@ ztp_status ztp_gemm(ztp_ctx* c, int kind, const ztp_linear_args* a, void* stream
   ztp_mat tx{}, tw{};
   Src X{nullptr, false}, W{nullptr, false};
   if (kind == ztp::KIND_FWD) {
-    const bool act = a->act == ZTP_ACT_GELU;
+    const bool act = a->act == ZTP_ACT_GELU || a->act == ZTP_ACT_GELU_D;
+    const int act_epi = a->act == ZTP_ACT_GELU_D ? ztp::EPI_GELU_D : ztp::EPI_GELU;
     s = operand_src(c, dense_sel, a->x_compact != 0, a->x_t, a->xs_t, true, kept, nk, 0, &tx, &X, st);
     if (s == ZTP_OK) s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, true, kept, nk, 1, &tw, &W, st);
     if (s != ZTP_OK) return s;
     return gemm(c, kind, W, X, n_out, kept, pruned, nk, act ? a->pre_t : a->y_t, act ? &a->y_t : nullptr, nullptr,
-                0, a->y_pos, act ? ztp::EPI_GELU : ztp::EPI_NONE, st);
+                0, a->y_pos, act ? act_epi : ztp::EPI_NONE, st);
   }
   if (kind == ztp::KIND_DX) {
-    const bool gg = a->act_in == ZTP_ACT_GELU;
+    const bool gg = a->act_in == ZTP_ACT_GELU || a->act_in == ZTP_ACT_GELU_D;
+    const int gepi = a->act_in == ZTP_ACT_GELU_D ? ztp::EPI_MUL : ztp::EPI_GELU_GRAD;
     s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, true, kept, nk, 1, &tw, &W, st);
     if (s != ZTP_OK) return s;
     return gemm(c, kind, W, Src{&a->g_t, true}, n_out, kept, pruned, nk, a->dx_t, nullptr,
-                gg ? &a->pre_in_t : nullptr, a->x_compact ? 1 : 0, nullptr, gg ? ztp::EPI_GELU_GRAD : ztp::EPI_NONE,
+                gg ? &a->pre_in_t : nullptr, a->x_compact ? 1 : 0, nullptr, gg ? gepi : ztp::EPI_NONE,
                 st);
   }
   s = operand_src(c, dense_sel, a->x_compact != 0, a->x_t, a->xs_t, true, kept, nk, 0, &tx, &X, st);

@@ -71,19 +71,6 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float gelu_f(float x) {
-  const float c = 0.7978845608028654f;
-  float u = c * (x + 0.044715f * x * x * x);
-  return 0.5f * x * (1.0f + tanh_fast(u));
-}
-__device__ __forceinline__ float gelu_grad_f(float x) {
-  const float c = 0.7978845608028654f;
-  float u = c * (x + 0.044715f * x * x * x);
-  float t = tanh_fast(u);
-  float du = c * (1.0f + 3.0f * 0.044715f * x * x);
-  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
-}
-
 // 8 bf16 (16 B) at p; a ragged last chunk (nv < 8 valid columns) is stored
 // element-wise so nothing past the logical width is written.
 __device__ __forceinline__ void store_bf16x8(__nv_bfloat16* p, const uint4& w, int nv) {
@@ -97,13 +84,28 @@ __device__ __forceinline__ void store_bf16x8(__nv_bfloat16* p, const uint4& w, i
     if (i < nv) reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)(x[i >> 1] >> (16 * (i & 1)));
 }
 
-__device__ __forceinline__ uint4 gelu_grad_mul(uint4 w, uint4 pin) {
-  w.x = pack_bf16(bf16_lo(w.x) * gelu_grad_f(bf16_lo(pin.x)), bf16_hi(w.x) * gelu_grad_f(bf16_hi(pin.x)));
-  w.y = pack_bf16(bf16_lo(w.y) * gelu_grad_f(bf16_lo(pin.y)), bf16_hi(w.y) * gelu_grad_f(bf16_hi(pin.y)));
-  w.z = pack_bf16(bf16_lo(w.z) * gelu_grad_f(bf16_lo(pin.z)), bf16_hi(w.z) * gelu_grad_f(bf16_hi(pin.z)));
-  w.w = pack_bf16(bf16_lo(w.w) * gelu_grad_f(bf16_lo(pin.w)), bf16_hi(w.w) * gelu_grad_f(bf16_hi(pin.w)));
-  return w;
+// Packed (f32x2, FFMA2 / FMUL2) GeLU of two values and, when want_d, its
+// derivative, sharing one tanh:
+//   u = c (x + a x^3),  t = tanh(u),  GeLU = x/2 (1 + t),
+//   GeLU' = (1 + t)/2 + x/2 (1 - t^2) c (1 + 3 a x^2).
+__device__ __forceinline__ void gelu2(float2 x, float2& h, float2& d, bool want_d) {
+  constexpr float C = 0.7978845608028654f, CA = 0.7978845608028654f * 0.044715f;
+  const float2 x2 = __fmul2_rn(x, x);
+  const float2 s = __ffma2_rn(x2, make_float2(CA, CA), make_float2(C, C));
+  const float2 u = __fmul2_rn(x, s);
+  const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 hx = __fmul2_rn(x, make_float2(0.5f, 0.5f));
+  h = __ffma2_rn(hx, t, hx);
+  if (want_d) {
+    const float2 A = __ffma2_rn(t, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
+    const float2 B = __ffma2_rn(make_float2(-t.x, -t.y), t, make_float2(1.0f, 1.0f));
+    const float2 du = __ffma2_rn(x2, make_float2(3.0f * CA, 3.0f * CA), make_float2(C, C));
+    d = __ffma2_rn(__fmul2_rn(hx, B), du, A);
+  }
 }
+__device__ __forceinline__ uint32_t pack2(float2 v) { return pack_bf16(v.x, v.y); }
+__device__ __forceinline__ float2 unpack2(uint32_t u) { return make_float2(bf16_lo(u), bf16_hi(u)); }
+
 
 // Work units: computed tiles x K-splits first, then (unsplit launches only)
 // the DX / DW tiles whose rows are all pruned -- they skip the MMA and write
@@ -432,14 +434,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int arow = 0;
       if (m < p.M) {
         int o;
-        if (KIND == KIND_FWD)
+        if (p.out_dense)
+          o = m;                                      // compact output (row i <- unit i of the list)
+        else if (KIND == KIND_FWD)
           o = p.out_pos ? __ldg(p.out_pos + m) : m;   // producer-side compaction for the next layer
         else
           o = (m < p.n_kept) ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
         if (o >= 0) orow = o;
         arow = p.aux_by_m ? m : o;
       }
-      const bool dense_out = KIND == KIND_FWD && p.out_pos == nullptr;
+      const bool dense_out = p.out_dense;
       // rows of the 4-row scatter group this lane issues (lanes 0..7)
       int sr[4];
 #pragma unroll
@@ -452,14 +456,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (!zt) release();
         continue;
       }
+      // one TMA store of a staged 32 x 64 bf16 plane (dense box or 4-row scatter)
+      auto store_plane = [&](const CUtensorMap* tm, uint8_t* buf, int col0) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (p.dbg & 1) return;
+        if (dense_out) {
+          if (lane == 0) {
+            tma_store_2d(tm, buf, col0, m0 + lq * 32);
+            bulk_commit();
+          }
+        } else if (lane < 8) {
+          tma_scatter4(tm, buf + lane * 512, col0, sr[0], sr[1], sr[2], sr[3]);
+          bulk_commit();
+        }
+      };
+      const bool two_planes = p.epi == EPI_GELU || p.epi == EPI_GELU_D;
+      const bool has_aux = (p.epi == EPI_GELU_GRAD || p.epi == EPI_MUL) && !zt;
 #pragma unroll 1
       for (int c = 0; c < BN / 128; ++c) {
         const int col0 = nc0 + c * 64;
-        uint32_t v0[32], v1[32];
-        // GeLU' operand: this lane's row of the pre-activation, loaded before
-        // the TMEM load so the global loads overlap it
+        uint32_t v[64];
+        // GeLU' operand (pre-activation, or GeLU'(pre) itself for EPI_MUL):
+        // this lane's row, loaded before the TMEM load so the two overlap
         uint4 pin[8];
-        if (p.epi == EPI_GELU_GRAD && !zt) {
+        if (has_aux) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             pin[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -468,49 +489,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         if (!zt) {
-          tmem_ld_32x32b_x32(tbase + c * 64, v0);
-          tmem_ld_32x32b_x32(tbase + c * 64 + 32, v1);
+          tmem_ld_32x32b_x32(tbase + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+          tmem_ld_32x32b_x32(tbase + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
           tmem_ld_wait();
           if (c == BN / 128 - 1) release();   // accumulator fully in registers: TMEM free for tile i+2
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0u;
+          for (int i = 0; i < 64; ++i) v[i] = 0u;
         }
-        // Plane 0 = the GEMM output (pre for GeLU); plane 1 (GeLU only) = H.
-#pragma unroll 1
-        for (int plane = 0; plane < (p.epi == EPI_GELU ? 2 : 1); ++plane) {
+        if (two_planes) {
+          // out <- pre (EPI_GELU) or GeLU'(pre) (EPI_GELU_D); out2 <- GeLU(pre).
+          // Both staging buffers are filled in one pass (tanh shared).
+          if (lane < 8) bulk_wait_read0();
+          __syncwarp();
+          uint8_t* const b0 = stg_base;
+          uint8_t* const b1 = stg_base + STAGING_PER_WARP;
+          const bool want_d = p.epi == EPI_GELU_D;
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq) {
+            uint32_t w0[4], w1[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 x = make_float2(__uint_as_float(v[qq * 8 + 2 * j]), __uint_as_float(v[qq * 8 + 2 * j + 1]));
+              float2 hv, dv;
+              gelu2(x, hv, dv, want_d);
+              w0[j] = want_d ? pack2(dv) : pack2(x);
+              w1[j] = pack2(hv);
+            }
+            const uint32_t off = lane * 128 + ((qq ^ (lane & 7)) << 4);
+            st_shared_v4(b0 + off, make_uint4(w0[0], w0[1], w0[2], w0[3]));
+            st_shared_v4(b1 + off, make_uint4(w1[0], w1[1], w1[2], w1[3]));
+          }
+          store_plane(&tmO, b0, col0);
+          store_plane(&tmO2, b1, col0);
+        } else {
           staging_free();
 #pragma unroll
           for (int qq = 0; qq < 8; ++qq) {
-            float f[8];
+            uint32_t w[4];
+            const uint32_t a4[4] = {pin[qq].x, pin[qq].y, pin[qq].z, pin[qq].w};
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int cc = qq * 8 + i;
-              f[i] = __uint_as_float(cc < 32 ? v0[cc] : v1[cc - 32]);
-              if (plane == 1) f[i] = gelu_f(f[i]);
-            }
-            uint4 w;
-            w.x = pack_bf16(f[0], f[1]);
-            w.y = pack_bf16(f[2], f[3]);
-            w.z = pack_bf16(f[4], f[5]);
-            w.w = pack_bf16(f[6], f[7]);
-            if (p.epi == EPI_GELU_GRAD && !zt) w = gelu_grad_mul(w, pin[qq]);   // G1 = dH * GeLU'(pre_in)
-            st_shared_v4(stg + lane * 128 + ((qq ^ (lane & 7)) << 4), w);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (!(p.dbg & 1)) {
-            const CUtensorMap* tm = plane == 0 ? &tmO : &tmO2;
-            if (dense_out) {
-              if (lane == 0) {
-                tma_store_2d(tm, stg, col0, m0 + lq * 32);
-                bulk_commit();
+            for (int j = 0; j < 4; ++j) {
+              float2 x = make_float2(__uint_as_float(v[qq * 8 + 2 * j]), __uint_as_float(v[qq * 8 + 2 * j + 1]));
+              if (has_aux) {
+                // G1 = dH * GeLU'(pre_in)  (EPI_MUL: aux already holds GeLU'(pre))
+                const float2 a = unpack2(a4[j]);
+                if (p.epi == EPI_GELU_GRAD) {
+                  float2 hv, dv;
+                  gelu2(a, hv, dv, true);
+                  x = __fmul2_rn(x, dv);
+                } else {
+                  x = __fmul2_rn(x, a);
+                }
               }
-            } else if (lane < 8) {
-              tma_scatter4(tm, stg + lane * 512, col0, sr[0], sr[1], sr[2], sr[3]);
-              bulk_commit();
+              w[j] = pack2(x);
             }
+            st_shared_v4(stg + lane * 128 + ((qq ^ (lane & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
           }
+          store_plane(&tmO, stg, col0);
         }
       }
     }
@@ -545,7 +581,9 @@ __global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
     const int nv = p.N - col;
     const bool computed = (KIND == KIND_FWD) || (m < p.n_kept);
     int orow;
-    if (KIND == KIND_FWD)
+    if (p.out_dense)
+      orow = m;
+    else if (KIND == KIND_FWD)
       orow = p.out_pos ? __ldg(p.out_pos + m) : m;
     else
       orow = computed ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
@@ -572,19 +610,38 @@ __global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
     w.y = pack_bf16(v[2], v[3]);
     w.z = pack_bf16(v[4], v[5]);
     w.w = pack_bf16(v[6], v[7]);
-    if (p.epi == EPI_GELU_GRAD && computed) {
-      const int ar = p.aux_by_m ? m : orow;
-      w = gelu_grad_mul(w, *reinterpret_cast<const uint4*>(p.aux + (int64_t)ar * p.ld_aux + col));
+    const int ar = p.aux_by_m ? m : orow;
+    if ((p.epi == EPI_GELU_GRAD || p.epi == EPI_MUL) && computed) {
+      const uint4 a = *reinterpret_cast<const uint4*>(p.aux + (int64_t)ar * p.ld_aux + col);
+      const uint32_t a4[4] = {a.x, a.y, a.z, a.w};
+      uint32_t o4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 x = make_float2(v[2 * j], v[2 * j + 1]);
+        float2 g = unpack2(a4[j]), hv, dv;
+        if (p.epi == EPI_GELU_GRAD) {
+          gelu2(g, hv, dv, true);
+          g = dv;
+        }
+        o4[j] = pack2(__fmul2_rn(x, g));
+      }
+      w = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+    }
+    uint4 g = w;
+    if (p.epi == EPI_GELU || p.epi == EPI_GELU_D) {
+      uint32_t h4[4], d4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 hv, dv;
+        gelu2(make_float2(v[2 * j], v[2 * j + 1]), hv, dv, p.epi == EPI_GELU_D);
+        h4[j] = pack2(hv);
+        d4[j] = pack2(dv);
+      }
+      g = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+      if (p.epi == EPI_GELU_D) w = make_uint4(d4[0], d4[1], d4[2], d4[3]);
     }
     store_bf16x8(p.out + (int64_t)orow * p.ld_out + col, w, nv);
-    if (p.epi == EPI_GELU) {
-      uint4 g;
-      g.x = pack_bf16(gelu_f(v[0]), gelu_f(v[1]));
-      g.y = pack_bf16(gelu_f(v[2]), gelu_f(v[3]));
-      g.z = pack_bf16(gelu_f(v[4]), gelu_f(v[5]));
-      g.w = pack_bf16(gelu_f(v[6]), gelu_f(v[7]));
-      store_bf16x8(p.out2 + (int64_t)orow * p.ld_out2 + col, g, nv);
-    }
+    if (p.epi == EPI_GELU || p.epi == EPI_GELU_D) store_bf16x8(p.out2 + (int64_t)orow * p.ld_out2 + col, g, nv);
   }
 }
 
@@ -735,9 +792,9 @@ cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_s
     ok &= make_map(&mp.b, o.b, o.b_rows, o.b_cols, o.b_ld, 64, bnl);
   }
   // outputs: dense box stores (32 rows x 64 columns) or 4-row scatters at the row map
-  const bool dense_out = kind == KIND_FWD && p.out_pos == nullptr;
+  const bool dense_out = p.out_dense;
   ok &= make_map(&mp.o, p.out, p.out_rows, p.N, p.ld_out, 64, dense_out ? 32 : 1);
-  if (p.epi == EPI_GELU)
+  if (p.epi == EPI_GELU || p.epi == EPI_GELU_D)
     ok &= make_map(&mp.o2, p.out2, p.out_rows, p.N, p.ld_out2, 64, dense_out ? 32 : 1);
   else
     mp.o2 = mp.o;

@@ -8,7 +8,9 @@
 namespace ztp {
 
 enum { KIND_FWD = 0, KIND_DX = 1, KIND_DW = 2 };
-enum { EPI_NONE = 0, EPI_GELU = 1, EPI_GELU_GRAD = 2 };
+// EPI_GELU: out <- pre, out2 <- GeLU(pre).  EPI_GELU_D: out <- GeLU'(pre), out2 <- GeLU(pre).
+// EPI_GELU_GRAD: out <- acc * GeLU'(aux).  EPI_MUL: out <- acc * aux (aux = GeLU'(pre)).
+enum { EPI_NONE = 0, EPI_GELU = 1, EPI_GELU_GRAD = 2, EPI_GELU_D = 3, EPI_MUL = 4 };
 
 struct GemmParams {
   int M, N;            // output rows (M) and columns (N)
@@ -35,6 +37,7 @@ struct GemmParams {
   int dbg;   // performance experiments only (ZTP_DEBUG_EPI): 1 skip stores, 2 skip the epilogue body
   int oob_out;   // a row index outside the output tensor (TMA stores skip it)
   int out_rows;  // rows of the output tensor(s)
+  int out_dense; // the row map is the identity on m < M (set by the host): dense TMA box stores
 };
 
 // Split-K choice for a launch and the fp32 workspace it needs (bytes).
@@ -99,6 +102,9 @@ cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, i
                         int64_t n_feat, int64_t N, int dtype, const int32_t* rows, cudaStream_t st);
 cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* idx, int n, int64_t cols, void* dst,
                                int64_t ld_dst, int dtype, cudaStream_t st);
+cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* rows, int n, const int32_t* cols, int nc,
+                             void* dst, int64_t ld_dst, cudaStream_t st);
+cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, int nc, int n_full, cudaStream_t st);
 cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
                              cudaStream_t st);
 

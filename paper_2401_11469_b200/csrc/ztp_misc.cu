@@ -158,6 +158,91 @@ cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* i
   return cudaGetLastError();
 }
 
+// ------------------------------------ 2D compaction (output pruning, bf16)
+// dst[r, c] = src[rows ? rows[r] : r, cols[c]] for r < n, c < nc: the weight
+// block W^T[S, S'] a col layer needs when its consumer keeps only S' of its
+// outputs.  Each thread builds 8 output columns (one 16-byte store) from the
+// source row, which stays in L1 across the warp (cols ascending).
+__global__ void ztp_gather_2d(const uint16_t* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ rows,
+                              int n, const int32_t* __restrict__ cols, int nc, uint16_t* __restrict__ dst,
+                              int64_t ld_dst) {
+  const int vpr = (nc + 7) / 8;
+  const int64_t total = (int64_t)n * vpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / vpr), c0 = (int)(i % vpr) * 8;
+    const uint16_t* s = src + (int64_t)(rows ? __ldg(rows + r) : r) * ld_src;
+    uint16_t* d = dst + (int64_t)r * ld_dst + c0;
+    if (c0 + 8 <= nc) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = (uint32_t)__ldg(s + __ldg(cols + c0 + 2 * q)) | ((uint32_t)__ldg(s + __ldg(cols + c0 + 2 * q + 1)) << 16);
+      *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      for (int c = c0; c < nc; ++c) d[c - c0] = __ldg(s + __ldg(cols + c));
+    }
+  }
+}
+
+cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* rows, int n, const int32_t* cols, int nc,
+                             void* dst, int64_t ld_dst, cudaStream_t st) {
+  if (n <= 0 || nc <= 0) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) != 0 || ld_dst % 8 != 0) return cudaErrorMisalignedAddress;
+  const int64_t total = (int64_t)n * ((nc + 7) / 8);
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  ztp_gather_2d<<<blocks, 256, 0, st>>>((const uint16_t*)src, ld_src, rows, n, cols, nc, (uint16_t*)dst, ld_dst);
+  return cudaGetLastError();
+}
+
+// In-place column expansion (output pruning, bf16): row r of t holds nc
+// compact columns; afterwards t[r, j] = pos[j] >= 0 ? old[r, pos[j]] : 0 for
+// j < n_full (the Zero gradient of the consumer-pruned units).  One CTA
+// per row at a time: the compact row is staged in shared memory first, so the
+// in-place overwrite never reads a written element.
+__global__ void ztp_expand_cols(uint16_t* t, int64_t ld, int n, const int32_t* __restrict__ pos, int nc, int n_full) {
+  extern __shared__ uint16_t row[];
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    uint16_t* p = t + (int64_t)r * ld;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) row[c] = p[c];
+    __syncthreads();
+    for (int j0 = threadIdx.x * 8; j0 < n_full; j0 += blockDim.x * 8) {
+      if (j0 + 8 <= n_full) {
+        auto g = [&](int j) -> uint32_t {
+          const int q = __ldg(pos + j);
+          return q >= 0 ? (uint32_t)row[q] : 0u;
+        };
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = g(j0 + 2 * q) | (g(j0 + 2 * q + 1) << 16);
+        *reinterpret_cast<uint4*>(p + j0) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        for (int j = j0; j < n_full; ++j) {
+          const int q = __ldg(pos + j);
+          p[j] = q >= 0 ? row[q] : (uint16_t)0;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, int nc, int n_full, cudaStream_t st) {
+  if (n <= 0 || n_full <= 0) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(t) & 15) != 0 || ld % 8 != 0)
+    return cudaErrorMisalignedAddress;
+  const size_t smem = (size_t)nc * 2;
+  static int max_set = 48 * 1024;
+  if ((int)smem > max_set) {
+    cudaError_t e = cudaFuncSetAttribute(ztp_expand_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    max_set = (int)smem;
+  }
+  const int blocks = n < 148 * 8 ? n : 148 * 8;
+  ztp_expand_cols<<<blocks, 256, smem, st>>>((uint16_t*)t, ld, n, pos, nc, n_full);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- row fill (Zero)
 __global__ void ztp_fill_rows(uint8_t* out, int64_t ld_bytes, const int32_t* rows, int nrows, int64_t row_bytes) {
   const int64_t per = row_bytes / 4;
@@ -250,11 +335,12 @@ __global__ void __launch_bounds__(256) ztp_gemm_f32_kernel(const GemmParamsF32 p
       const int n = n0 + tx * 4 + j;
       if (n >= p.N) continue;
       float v = acc[i][j];
-      if (p.epi == EPI_GELU) {
-        p.out[orow * p.ld_out + n] = v;
+      if (p.epi == EPI_GELU || p.epi == EPI_GELU_D) {
+        p.out[orow * p.ld_out + n] = p.epi == EPI_GELU ? v : gelu_grad_f32(v);
         p.out2[orow * p.ld_out2 + n] = gelu_f32(v);
       } else {
         if (p.epi == EPI_GELU_GRAD) v = v * gelu_grad_f32(p.aux[arow * p.ld_aux + n]);
+        if (p.epi == EPI_MUL) v = v * p.aux[arow * p.ld_aux + n];
         p.out[orow * p.ld_out + n] = v;
       }
     }

@@ -114,12 +114,12 @@ class ZtpLayer:
         self.ctxC = _buf(a, N, dtype)            # compact ctx rows S_o
         self.Y1 = _buf(h, N, dtype)
         self.Y1c = _buf(h, N, dtype)             # compact Y1 rows S_fc1
-        self.PreC = _buf(u + cap, N, dtype)      # compact pre rows S_fc2
+        self.PreC = _buf(u + cap, N, dtype)      # compact GeLU'(pre) rows S_fc2 (ACT_GELU_D)
         self.HC = _buf(u + cap, N, dtype)        # compact H rows S_fc2
         self.Y = _buf(h, N, dtype)
         # gradients
         self.G = _buf(h, N, dtype)
-        self.G1 = _buf(u + cap, N, dtype)        # dH * GeLU'(pre), full layout, rows P zero
+        self.G1 = _buf(u + cap, N, dtype)        # dH * GeLU'(pre), compact rows S_fc2 (P_fc2 Zero, implied)
         self.dY1 = _buf(h, N, dtype)
         self.dctx = _buf(a, N, dtype)
         self.gQKV = _buf(3 * a, N, dtype)
@@ -206,16 +206,22 @@ class ZtpLayer:
                        sel_=self.sels["qkv"])
         self.f_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, y_t=self.Y1, ws_t=self.Wo_c, sel_=self.sels["o"],
                      x_compact=True)
+        # output pruning: FC1 computes only the hidden units FC2 keeps (S_fc2)
+        # and its backward reads the compact G1 FC2's dX writes (rows P_fc2
+        # are Zero) -- same results as the full FC1, half the work at
+        # gamma = 0.5.  DESIGN.md "Output pruning".
+        osel = self.sels["fc2"]
+        ng = nk["fc2"] if osel is not None else nfc
         self.f_fc1 = L(x_t=self.Y1, w_t=self.w1_t, y_t=self.HC, pre_t=self.PreC, xs_t=self.Y1c, ws_t=self.W1_c,
-                       sel_=self.sels["fc1"], n_out=nfc, act=Z.ACT_GELU, y_pos=self.POS["fc2"])
+                       sel_=self.sels["fc1"], n_out=nfc, act=Z.ACT_GELU_D, y_pos=self.POS["fc2"], out_sel=osel)
         self.f_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], y_t=self.Y, ws_t=self.W2_c,
                        sel_=self.sels["fc2"], x_compact=True)
         # backward
-        self.b_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], g_t=self.G, dx_t=self.G1[:nfc],
+        self.b_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], g_t=self.G, dx_t=self.G1[:ng],
                        dw_t=self.dw2[:nfc], pre_in_t=self.PreC[:nk["fc2"]], ws_t=self.W2_c,
-                       sel_=self.sels["fc2"], act_in=Z.ACT_GELU, x_compact=True)
-        self.b_fc1 = L(x_t=self.Y1, w_t=self.w1_t, g_t=self.G1[:nfc], dx_t=self.dY1, dw_t=self.dw1, xs_t=self.Y1c,
-                       ws_t=self.W1_c, sel_=self.sels["fc1"], n_out=nfc)
+                       sel_=self.sels["fc2"], act_in=Z.ACT_GELU_D, x_compact=True, dx_compact=osel is not None)
+        self.b_fc1 = L(x_t=self.Y1, w_t=self.w1_t, g_t=self.G1[:ng], dx_t=self.dY1, dw_t=self.dw1, xs_t=self.Y1c,
+                       ws_t=self.W1_c, sel_=self.sels["fc1"], n_out=nfc, y_pos=self.POS["fc2"], out_sel=osel)
         self.b_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx, dw_t=self.do,
                      ws_t=self.Wo_c, sel_=self.sels["o"], x_compact=True)
         self.b_qkv = L(x_t=self.X, w_t=self.qkv_t, g_t=self.gQKV, dx_t=self.dX, dw_t=self.dqkv, xs_t=self.Xc,
@@ -302,7 +308,9 @@ class ZtpLayer:
 
     # ------------------------------------------------------------ accounting
     def executed_flops(self) -> float:
-        """6 N n K' per linear (fwd + dX + dW), SURVEY §8(d)."""
+        """FLOPs of the resized layer: 6 N n K' per linear (fwd + dX + dW),
+        SURVEY §8(d).  The method's count -- output pruning (FC1 computing only
+        FC2's kept units) executes fewer for the same result."""
         N, a, h = self.N, self.a, self.h
         nk = self.nk
         return 6.0 * N * (3 * a * nk["qkv"] + h * nk["o"] + self.n_fc * nk["fc1"] + h * nk["fc2"])

@@ -176,19 +176,23 @@ def test_gemm_fwd_dx_dw_parity(env, K, n, N, gamma, dtype):
             assert torch.all(rows == 0) and not torch.any(torch.signbit(rows))
 
 
+@pytest.mark.parametrize("act", ["gelu", "gelu_d"])
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-def test_gemm_gelu_epilogues(env, dtype):
+def test_gemm_gelu_epilogues(env, dtype, act):
+    """FWD: pre_t <- pre (GELU) or GeLU'(pre) (GELU_D), y <- GeLU(pre).
+    Row-layer dX: G1 = dH * GeLU'(pre_in) (GELU) or dH * pre_in (GELU_D, where
+    pre_in already holds GeLU'(pre))."""
     Z, torch, ctx = env
     K, n, N = 384, 272, 520
     Xt, Wt, Gt, S, P = _case(K, n, N, 0.4, seed=7)
     td = torch.bfloat16 if dtype == "bf16" else torch.float32
     tol = TOL_BF16 if dtype == "bf16" else TOL_F32
+    A = Z.ACT_GELU if act == "gelu" else Z.ACT_GELU_D
     x, w = dev(torch, Xt, td), dev(torch, Wt, td)
     pre = empty(torch, n, N, td)
     h = empty(torch, n, N, td)
     s, keep = _sel_dev(Z, torch, S, P)
-    Z.ztp_gemm(ctx, Z.KIND_FWD, Z.linear_args(x_t=x, w_t=w, y_t=h, pre_t=pre, sel_=s, act=Z.ACT_GELU))
-    # GeLU' epilogue on a row-layer dX: dH = W2^T G, G1 = dH * GeLU'(pre_in)
+    Z.ztp_gemm(ctx, Z.KIND_FWD, Z.linear_args(x_t=x, w_t=w, y_t=h, pre_t=pre, sel_=s, act=A))
     K2, n2 = 272, 200
     W2 = I.uniform_sym(8, "w2", K2, n2, 1 / math.sqrt(K2))
     G2 = I.normal(8, "g2", n2, N)
@@ -196,11 +200,12 @@ def test_gemm_gelu_epilogues(env, dtype):
     S2, P2 = O.select(I.lognormal_scores(8, "s2", K2), 100)
     s2, keep2 = _sel_dev(Z, torch, S2, P2)
     g1 = empty(torch, K2, N, td)
+    aux = PreIn if act == "gelu" else O.gelu_tanh_grad(PreIn)
     Z.ztp_gemm(ctx, Z.KIND_DX, Z.linear_args(w_t=dev(torch, W2, td), g_t=dev(torch, G2, td), dx_t=g1,
-                                             pre_in_t=dev(torch, PreIn, td), sel_=s2, act_in=Z.ACT_GELU))
+                                             pre_in_t=dev(torch, aux, td), sel_=s2, act_in=A))
     Z.ztp_sync(ctx)
     ref_pre = O.linear_fwd(Wt, Xt, S)
-    ok, e = err_ok(host(pre), ref_pre, tol)
+    ok, e = err_ok(host(pre), ref_pre if act == "gelu" else O.gelu_tanh_grad(ref_pre), tol)
     assert ok, e
     ok, e = err_ok(host(h), O.gelu_tanh(ref_pre), tol)
     assert ok, e
@@ -209,33 +214,37 @@ def test_gemm_gelu_epilogues(env, dtype):
     assert ok, e
 
 
-@pytest.mark.parametrize("case", ["fwd_gelu", "dx_gelu_grad", "dw"])
+@pytest.mark.parametrize("case", ["fwd_gelu", "fwd_gelu_d", "dx_gelu_grad", "dx_mul", "dw"])
 def test_gemm_splitk_paths(env, case):
     """Few output tiles + long contraction -> split-K partials + the fixed-order
     reduce kernel (epilogue, row map and Zero rows applied there)."""
     Z, torch, ctx = env
-    if case == "fwd_gelu":
+    if case.startswith("fwd_gelu"):
         K, n, N, gamma = 8192, 128, 256, 0.5            # 1 tile, 64 k-blocks
-    elif case == "dx_gelu_grad":
+    elif case.startswith("dx"):
         K, n, N, gamma = 256, 2048, 256, 0.6            # 1 computed m-tile, kdim 2048
     else:
         K, n, N, gamma = 256, 200, 4096, 0.5            # 1 x 1 tiles, 64 token k-blocks
     Xt, Wt, Gt, S, P = _case(K, n, N, gamma, seed=31)
     x, w, g = dev(torch, Xt), dev(torch, Wt), dev(torch, Gt)
     s, keep = _sel_dev(Z, torch, S, P)
-    if case == "fwd_gelu":
+    if case.startswith("fwd_gelu"):
+        gd = case == "fwd_gelu_d"
         pre, h = empty(torch, n, N, torch.bfloat16), empty(torch, n, N, torch.bfloat16)
-        Z.ztp_gemm(ctx, Z.KIND_FWD, Z.linear_args(x_t=x, w_t=w, y_t=h, pre_t=pre, sel_=s, act=Z.ACT_GELU))
+        Z.ztp_gemm(ctx, Z.KIND_FWD, Z.linear_args(x_t=x, w_t=w, y_t=h, pre_t=pre, sel_=s,
+                                                  act=Z.ACT_GELU_D if gd else Z.ACT_GELU))
         Z.ztp_sync(ctx)
         ref = O.linear_fwd(Wt, Xt, S)
-        for got, want in ((pre, ref), (h, O.gelu_tanh(ref))):
+        for got, want in ((pre, O.gelu_tanh_grad(ref) if gd else ref), (h, O.gelu_tanh(ref))):
             ok, e = err_ok(host(got), want, TOL_BF16)
             assert ok, e
-    elif case == "dx_gelu_grad":
+    elif case.startswith("dx"):
+        mul = case == "dx_mul"
         pin = I.normal(31, "pin", K, N)
         dx = empty(torch, K, N, torch.bfloat16)
-        Z.ztp_gemm(ctx, Z.KIND_DX, Z.linear_args(w_t=w, g_t=g, dx_t=dx, pre_in_t=dev(torch, pin), sel_=s,
-                                                 act_in=Z.ACT_GELU))
+        Z.ztp_gemm(ctx, Z.KIND_DX, Z.linear_args(w_t=w, g_t=g, dx_t=dx,
+                                                 pre_in_t=dev(torch, O.gelu_tanh_grad(pin) if mul else pin), sel_=s,
+                                                 act_in=Z.ACT_GELU_D if mul else Z.ACT_GELU))
         Z.ztp_sync(ctx)
         ref = O.linear_bwd_dx(Wt, Gt, S, P) * O.gelu_tanh_grad(pin)
         ok, e = err_ok(host(dx), ref, TOL_BF16)
@@ -248,6 +257,62 @@ def test_gemm_splitk_paths(env, case):
         ok, e = err_ok(host(dw), O.linear_bwd_dw(Xt, Gt, S, P), TOL_BF16)
         assert ok, e
         assert torch.all(dw[torch.tensor(P, device="cuda")] == 0)
+
+
+@pytest.mark.parametrize("g1,g2", [(0.3, 0.45), (0.0, 0.5), (0.5, 0.0)])
+def test_output_pruning_col_row_pair(env, g1, g2):
+    """FC1 (col, GeLU) -> FC2 (row) with out_sel = FC2's entry: FC1 computes
+    only the units S2 FC2 keeps, FC2's dX is written compact (dx_compact) and
+    FC1's backward contracts over S2 only and writes Zero columns P2 of dW1.
+    Every result equals the full-output computation of the oracle."""
+    Z, torch, ctx = env
+    h, f, N = 200, 520, 264
+    seed = 41 + int(10 * g1) + int(100 * g2)
+    X = I.normal(seed, "x", h, N)
+    W1 = I.uniform_sym(seed, "w1", h, f, 1 / math.sqrt(h))
+    W2 = I.uniform_sym(seed, "w2", f, h, 1 / math.sqrt(f))
+    G = I.normal(seed, "g", h, N)
+    S1, P1 = O.select(I.lognormal_scores(seed, "s1", h), min(int(h * g1 + 0.5), h - 1))
+    S2, P2 = O.select(I.lognormal_scores(seed, "s2", f), min(int(f * g2 + 0.5), f - 1))
+    nk2 = len(S2)
+    bf = torch.bfloat16
+    x, w1, w2, g = dev(torch, X), dev(torch, W1), dev(torch, W2), dev(torch, G)
+    s1, k1 = _sel_dev(Z, torch, S1, P1, 0, 2) if len(P1) else (None, None)
+    s2, k2 = _sel_dev(Z, torch, S2, P2, 0, 3)
+    pos = np.full(f, -1, dtype=np.int32)
+    pos[np.asarray(S2)] = np.arange(nk2, dtype=np.int32)
+    pos = torch.tensor(pos, device="cuda")
+    hc, prec = empty(torch, nk2, N, bf), empty(torch, nk2, N, bf)
+    y = empty(torch, h, N, bf)
+    g1c = empty(torch, nk2, N, bf)
+    dy1, dw1, dw2 = empty(torch, h, N, bf), empty(torch, h, f, bf), empty(torch, f, h, bf)
+    ws1 = empty(torch, h, f, bf)
+    a1 = Z.linear_args(x_t=x, w_t=w1, y_t=hc, pre_t=prec, ws_t=ws1, sel_=s1, act=Z.ACT_GELU, y_pos=pos,
+                       out_sel=s2)
+    a2 = Z.linear_args(x_t=hc, w_t=w2, y_t=y, g_t=g, dx_t=g1c, dw_t=dw2, pre_in_t=prec, sel_=s2,
+                       act_in=Z.ACT_GELU, x_compact=True, dx_compact=True)
+    b1 = Z.linear_args(x_t=x, w_t=w1, g_t=g1c, dx_t=dy1, dw_t=dw1, ws_t=ws1, sel_=s1, y_pos=pos, out_sel=s2)
+    Z.ztp_col_linear(ctx, Z.FWD, a1)
+    Z.ztp_row_linear(ctx, Z.FWD, a2)
+    Z.ztp_row_linear(ctx, Z.BWD, a2)
+    Z.ztp_col_linear(ctx, Z.BWD, b1)
+    Z.ztp_sync(ctx)
+    S2a = np.asarray(S2)
+    pre_ref = O.linear_fwd(W1, X, S1)                       # full FC1 output
+    H_ref = O.gelu_tanh(pre_ref)
+    y_ref = O.linear_fwd(W2, H_ref, S2)
+    G1_full = O.linear_bwd_dx(W2, G, S2, P2) * O.gelu_tanh_grad(pre_ref)   # rows P2 exactly 0
+    checks = [("pre", prec, pre_ref[S2a]), ("H", hc, H_ref[S2a]), ("y", y, y_ref), ("G1", g1c, G1_full[S2a]),
+              ("dW2", dw2, O.linear_bwd_dw(H_ref, G, S2, P2)), ("dY1", dy1, O.linear_bwd_dx(W1, G1_full, S1, P1)),
+              ("dW1", dw1, O.linear_bwd_dw(X, G1_full, S1, P1))]
+    for name, got, ref in checks:
+        gh = host(got)
+        assert np.isfinite(gh).all(), f"{name}: unwritten (NaN) elements"
+        ok, e = err_ok(gh, ref, TOL_BF16)
+        assert ok, f"{name}: max|err|/||ref|| = {e:.3e}"
+    if len(P2):   # Zero columns P2 of dW1, bit pattern +0.0
+        cols = dw1[:, torch.tensor(P2, device="cuda")]
+        assert torch.all(cols == 0) and not torch.any(torch.signbit(cols))
 
 
 def test_gemm_large_c2_shapes_sampled(env):
