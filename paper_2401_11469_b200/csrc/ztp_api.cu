@@ -575,6 +575,16 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
 
 }  // namespace
 
+namespace ztp {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ZTP_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+}  // namespace ztp
+
 // =========================================================================== API
 
 extern "C" {

@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool leader = rank == 0;
   const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
 
-  if (p.stamp != nullptr && threadIdx.x == 0) atomicMin(p.stamp, (unsigned long long)globaltimer());
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -217,6 +216,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done (barriers, TMEM, descriptor prefetch): wait for the
+  // preceding kernel's results, let the next kernel begin its own prologue
+  pdl_wait();
+  pdl_trigger();
+  if (p.stamp != nullptr && threadIdx.x == 0) atomicMin(p.stamp, (unsigned long long)globaltimer());
 
   const Sched<KIND, C::TM> sc(p);
 
@@ -573,6 +577,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // and the Zero imputation of pruned rows.
 template <int KIND>
 __global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
+  pdl_wait();
+  pdl_trigger();
   const int cpr = (p.N + 7) / 8;
   const int64_t total = (int64_t)p.M * cpr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -719,21 +725,22 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, mp.w, p);
     if (e != cudaSuccess) return e;
   }
   if (p.splits == 1) return cudaSuccess;
   const int64_t chunks = (int64_t)p.M * ((p.N + 7) / 8);
   const int blocks = (int)std::min<int64_t>((chunks + 255) / 256, (int64_t)num_sms * 8);
-  ztp_splitk_reduce<KIND><<<blocks, 256, 0, st>>>(p);
-  return cudaGetLastError();
+  return launch_k(ztp_splitk_reduce<KIND>, blocks, 256, 0, st, p);
 }
 
 int gemm_choose_cg(int kind, int M, int n_kept) {

@@ -4,8 +4,30 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 
 namespace ztp {
+
+// Programmatic dependent launch (PDL) for every kernel of the path: the next
+// kernel's CTAs start their prologue while this one drains; each kernel calls
+// griddepcontrol.wait before touching memory (ztp_ptx.cuh pdl_wait).  Kept in
+// CUDA graphs as programmatic edges.  ZTP_PDL=0 turns it off (A/B timing).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 enum { KIND_FWD = 0, KIND_DX = 1, KIND_DW = 2 };
 // EPI_GELU: out <- pre, out2 <- GeLU(pre).  EPI_GELU_D: out <- GeLU'(pre), out2 <- GeLU(pre).

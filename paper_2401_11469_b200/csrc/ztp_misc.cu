@@ -16,6 +16,8 @@ namespace ztp {
 // start + chi (end - start) so the rank's GEMM takes chi times longer (A-32),
 // accumulate the (stretched) GEMM time into acc_ns (M_i, A-6), reset stamps.
 __global__ void ztp_delay_kernel(unsigned long long* stamp, double chi, unsigned long long* acc_ns) {
+  pdl_wait();
+  pdl_trigger();
   const unsigned long long s = stamp[0], e = stamp[1];
   if (s != ~0ull && e >= s) {
     const unsigned long long dur = e - s;
@@ -32,17 +34,17 @@ __global__ void ztp_delay_kernel(unsigned long long* stamp, double chi, unsigned
 }
 
 __global__ void ztp_stamp_reset_kernel(unsigned long long* stamp) {
+  pdl_wait();
+  pdl_trigger();
   stamp[0] = ~0ull;
   stamp[1] = 0ull;
 }
 
 cudaError_t delay_launch(unsigned long long* stamp, double chi, unsigned long long* acc_ns, cudaStream_t st) {
-  ztp_delay_kernel<<<1, 1, 0, st>>>(stamp, chi, acc_ns);
-  return cudaGetLastError();
+  return launch_k(ztp_delay_kernel, 1, 1, 0, st, stamp, chi, acc_ns);
 }
 cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st) {
-  ztp_stamp_reset_kernel<<<1, 1, 0, st>>>(stamp);
-  return cudaGetLastError();
+  return launch_k(ztp_stamp_reset_kernel, 1, 1, 0, st, stamp);
 }
 
 // ------------------------------------------------------ stand-in core (A-31)
@@ -50,6 +52,8 @@ cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st) {
 __global__ void ztp_core_bf16(int phase, const __nv_bfloat16* __restrict__ qkv_c, __nv_bfloat16* qkv, int64_t ld_qkv,
                               __nv_bfloat16* ctx, int64_t ld_ctx, int64_t feat, int64_t n_feat, int64_t N,
                               const int32_t* __restrict__ rows) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t vec_per_row = N / 8;
   const int64_t total = n_feat * vec_per_row;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -81,6 +85,8 @@ __global__ void ztp_core_bf16(int phase, const __nv_bfloat16* __restrict__ qkv_c
 
 __global__ void ztp_core_f32(int phase, float* qkv, int64_t ld_qkv, float* ctx, int64_t ld_ctx, int64_t feat,
                              int64_t n_feat, int64_t N, const int32_t* __restrict__ rows) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = n_feat * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = i / N, c = i % N;
@@ -101,11 +107,10 @@ cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, i
   const int threads = 256;
   const int blocks = 148 * 8;
   if (dtype == 0)
-    ztp_core_bf16<<<blocks, threads, 0, st>>>(phase, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)qkv, ld_qkv,
-                                              (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N, rows);
-  else
-    ztp_core_f32<<<blocks, threads, 0, st>>>(phase, (float*)qkv, ld_qkv, (float*)ctx, ld_ctx, feat, n_feat, N, rows);
-  return cudaGetLastError();
+    return launch_k(ztp_core_bf16, blocks, threads, 0, st, phase, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)qkv,
+                    ld_qkv, (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N, rows);
+  return launch_k(ztp_core_f32, blocks, threads, 0, st, phase, (float*)qkv, ld_qkv, (float*)ctx, ld_ctx, feat, n_feat,
+                  N, rows);
 }
 
 // ------------------------------------------------- row compaction (a4 gather)
@@ -114,6 +119,8 @@ cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, i
 // the GEMM mainloop streams dense TMA boxes.  HBM-bound, 16-byte vectors.
 __global__ void ztp_gather_rows(const uint8_t* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ idx,
                                 int n, int64_t vec_per_row, uint8_t* __restrict__ dst, int64_t ld_dst) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)n * vec_per_row;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / vec_per_row, c = i % vec_per_row;
@@ -126,6 +133,8 @@ __global__ void ztp_gather_rows(const uint8_t* __restrict__ src, int64_t ld_src,
 // Rows whose width is not a multiple of 16 bytes: element-wise copy.
 __global__ void ztp_gather_rows_elem(const uint8_t* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ idx,
                                      int n, int64_t cols, int64_t es, uint8_t* __restrict__ dst, int64_t ld_dst) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)n * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / cols, c = i % cols;
@@ -146,16 +155,14 @@ cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* i
     const int64_t total = (int64_t)n * cols;
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    ztp_gather_rows_elem<<<blocks, 256, 0, st>>>((const uint8_t*)src, ld_src * es, idx, n, cols, es, (uint8_t*)dst,
-                                                 ld_dst * es);
-    return cudaGetLastError();
+    return launch_k(ztp_gather_rows_elem, blocks, 256, 0, st, (const uint8_t*)src, ld_src * es, idx, n, cols, es,
+                    (uint8_t*)dst, ld_dst * es);
   }
   const int64_t total = (int64_t)n * (row_bytes / 16);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  ztp_gather_rows<<<blocks, 256, 0, st>>>((const uint8_t*)src, ld_src * es, idx, n, row_bytes / 16, (uint8_t*)dst,
-                                          ld_dst * es);
-  return cudaGetLastError();
+  return launch_k(ztp_gather_rows, blocks, 256, 0, st, (const uint8_t*)src, ld_src * es, idx, n, row_bytes / 16,
+                  (uint8_t*)dst, ld_dst * es);
 }
 
 // ------------------------------------ 2D compaction (output pruning, bf16)
@@ -166,6 +173,8 @@ cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* i
 __global__ void ztp_gather_2d(const uint16_t* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ rows,
                               int n, const int32_t* __restrict__ cols, int nc, uint16_t* __restrict__ dst,
                               int64_t ld_dst) {
+  pdl_wait();
+  pdl_trigger();
   const int vpr = (nc + 7) / 8;
   const int64_t total = (int64_t)n * vpr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -191,8 +200,8 @@ cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* row
   const int64_t total = (int64_t)n * ((nc + 7) / 8);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  ztp_gather_2d<<<blocks, 256, 0, st>>>((const uint16_t*)src, ld_src, rows, n, cols, nc, (uint16_t*)dst, ld_dst);
-  return cudaGetLastError();
+  return launch_k(ztp_gather_2d, blocks, 256, 0, st, (const uint16_t*)src, ld_src, rows, n, cols, nc, (uint16_t*)dst,
+                  ld_dst);
 }
 
 // In-place column expansion (output pruning, bf16): row r of t holds nc
@@ -201,6 +210,8 @@ cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* row
 // per row at a time: the compact row is staged in shared memory first, so the
 // in-place overwrite never reads a written element.
 __global__ void ztp_expand_cols(uint16_t* t, int64_t ld, int n, const int32_t* __restrict__ pos, int nc, int n_full) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint16_t row[];
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     uint16_t* p = t + (int64_t)r * ld;
@@ -239,12 +250,13 @@ cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, i
     max_set = (int)smem;
   }
   const int blocks = n < 148 * 8 ? n : 148 * 8;
-  ztp_expand_cols<<<blocks, 256, smem, st>>>((uint16_t*)t, ld, n, pos, nc, n_full);
-  return cudaGetLastError();
+  return launch_k(ztp_expand_cols, blocks, 256, smem, st, (uint16_t*)t, ld, n, pos, nc, n_full);
 }
 
 // ------------------------------------------------------------- row fill (Zero)
 __global__ void ztp_fill_rows(uint8_t* out, int64_t ld_bytes, const int32_t* rows, int nrows, int64_t row_bytes) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t per = row_bytes / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)nrows * per;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -257,8 +269,7 @@ cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nro
                              cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
   const int64_t es = dtype == 0 ? 2 : 4;
-  ztp_fill_rows<<<148 * 4, 256, 0, st>>>((uint8_t*)out, ld * es, rows, nrows, cols * es);
-  return cudaGetLastError();
+  return launch_k(ztp_fill_rows, 148 * 4, 256, 0, st, (uint8_t*)out, ld * es, rows, nrows, cols * es);
 }
 
 // ------------------------------------------- fp32 verification GEMM (SIMT FFMA)
@@ -274,6 +285,8 @@ __device__ __forceinline__ float gelu_grad_f32(float x) {
 
 // 64x64 output tile, 256 threads, 4x4 register micro-tile, k in blocks of 16.
 __global__ void __launch_bounds__(256) ztp_gemm_f32_kernel(const GemmParamsF32 p) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
@@ -349,8 +362,7 @@ __global__ void __launch_bounds__(256) ztp_gemm_f32_kernel(const GemmParamsF32 p
 
 cudaError_t gemm_f32_launch(const GemmParamsF32& p, cudaStream_t st) {
   dim3 grid((p.N + 63) / 64, (p.M + 63) / 64);
-  ztp_gemm_f32_kernel<<<grid, 256, 0, st>>>(p);
-  return cudaGetLastError();
+  return launch_k(ztp_gemm_f32_kernel, grid, 256, 0, st, p);
 }
 
 }  // namespace ztp

@@ -14,6 +14,7 @@
 #include <cstdint>
 
 #include "ztp_internal.h"
+#include "ztp_ptx.cuh"
 
 namespace ztp {
 
@@ -52,6 +53,8 @@ __device__ __forceinline__ int block_excl_scan(bool flag, int& total, int* warp_
 __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, const float* __restrict__ scores,
                                                           int32_t* __restrict__ kept, int32_t* __restrict__ pruned,
                                                           int32_t* __restrict__ pos, int32_t* err_flag) {
+  pdl_wait();
+  pdl_trigger();
   const SelectSeg s = p.seg[blockIdx.x];
   const float* sc = scores + s.score_off;
   int32_t* K = kept + s.kept_off;
@@ -154,7 +157,8 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
 
 cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned, int32_t* pos,
                           int32_t* err_flag, cudaStream_t st) {
-  ztp_select_kernel<<<p.nseg, 1024, 0, st>>>(p, scores, kept, pruned, pos, err_flag);
+  cudaError_t e = launch_k(ztp_select_kernel, p.nseg, 1024, 0, st, p, scores, kept, pruned, pos, err_flag);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
