@@ -348,6 +348,10 @@ ztp_status ztp_read_gemm_ns(ztp_ctx* ctx, void* stream, double* ns);
 typedef struct ztp_profile {
   double gemm_ms, other_ms, comm_ms, gemm_flops;
   int64_t n_gemm, n_other, n_comm;
+  /* sum over GEMM launches of (last CTA end - first CTA start), from the
+   * kernels' own %globaltimer stamps (split-K reduce included): kernel time
+   * without event / launch overheads */
+  double gemm_kernel_ms;
 } ztp_profile;
 ztp_status ztp_set_profile(ztp_ctx* ctx, int on);
 ztp_status ztp_read_profile(ztp_ctx* ctx, void* stream, ztp_profile* out);

@@ -81,7 +81,8 @@ class LinearArgs(C.Structure):
 
 class Profile(C.Structure):
     _fields_ = [("gemm_ms", C.c_double), ("other_ms", C.c_double), ("comm_ms", C.c_double),
-                ("gemm_flops", C.c_double), ("n_gemm", C.c_int64), ("n_other", C.c_int64), ("n_comm", C.c_int64)]
+                ("gemm_flops", C.c_double), ("n_gemm", C.c_int64), ("n_other", C.c_int64), ("n_comm", C.c_int64),
+                ("gemm_kernel_ms", C.c_double)]
 
 
 class Xfer(C.Structure):

@@ -32,6 +32,13 @@ struct ztp_ctx {
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // BWD: the dW GEMM runs on side_stream concurrently with the dX GEMM (they
+  // are independent), so the two small-output GEMMs share the SMs
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_c = nullptr, ev_d = nullptr;
+  int conc_bwd = 0;                    // ZTP_CONC=1: dW on the side stream (measured: no gain)
+  void* skws_side = nullptr;           // split-K partials of side-stream GEMMs
+  size_t skws_side_cap = 0;
   std::string err;
   int64_t launches = 0;
   int32_t* d_flags = nullptr;               // [0]: NaN score seen
@@ -59,6 +66,9 @@ struct ztp_ctx {
     double flops;
   };
   int prof_on = 0;
+  unsigned long long* d_pstamp = nullptr;   // per-GEMM-launch kernel stamps while profiling
+  int pstamp_used = 0;
+  static constexpr int PSTAMP_CAP = 4096;
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
 };
@@ -190,7 +200,8 @@ struct Src {
 //   DW : A = X^T source, B = G^T
 ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t* kept, const int32_t* pruned,
                 int nk, const ztp_mat& out, const ztp_mat* out2, const ztp_mat* aux, int aux_by_m,
-                const int32_t* out_pos, int epi, cudaStream_t st, bool out_compact = false) {
+                const int32_t* out_pos, int epi, cudaStream_t st, bool out_compact = false,
+                const int32_t* col_pos = nullptr, int n_full = 0) {
   const int dtype = A.m->dtype;
   {
     const ztp_mat* need[3] = {A.m, B.m, &out};
@@ -264,6 +275,10 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
                                                         : (kept == c->d_iota && pruned == nullptr && M <= nk));
     p.stamp = emulating(c) ? c->d_stamp : nullptr;
     p.dbg = c->dbg_epi;
+    p.col_pos = col_pos;
+    p.n_full = n_full;
+    if (c->prof_on && c->d_pstamp && c->pstamp_used < ztp_ctx::PSTAMP_CAP)
+      p.prof_stamp = c->d_pstamp + 2 * (c->pstamp_used++);
     // split-K over the contraction when the output has too few tiles for 148 SMs
     p.splits = c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, c->num_sms) : 1;
     if (p.splits > 1) {
@@ -271,14 +286,17 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
       p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
       const size_t bytes = ztp::gemm_ws_bytes(kind, M, N, nk, p.splits);
-      if (c->skws_cap < bytes) {
-        if (c->skws) cudaFree(c->skws);
-        c->skws = nullptr;
-        c->skws_cap = 0;
-        CUDA_TRY(c, cudaMalloc(&c->skws, bytes));
-        c->skws_cap = bytes;
+      const bool side = st == c->side_stream;
+      void*& wsp = side ? c->skws_side : c->skws;
+      size_t& wcap = side ? c->skws_side_cap : c->skws_cap;
+      if (wcap < bytes) {
+        if (wsp) cudaFree(wsp);
+        wsp = nullptr;
+        wcap = 0;
+        CUDA_TRY(c, cudaMalloc(&wsp, bytes));
+        wcap = bytes;
       }
-      p.ws = (float*)c->skws;
+      p.ws = (float*)wsp;
       p.ld_ws = (N + 7) / 8 * 8;
       p.ws_split_stride = (int64_t)(kind == ztp::KIND_FWD ? M : std::min(M, nk)) * p.ld_ws;
     } else {
@@ -286,7 +304,9 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.kb_per_split = (kdim + 63) / 64;
     }
     CUDA_TRY(c, ztp::gemm_launch(kind, o, p, c->num_sms, st));
+    if (p.splits > 1 || p.col_pos) ++c->launches;   // split-K reduce or column expansion
   } else {
+    if (col_pos) return fail(c, ZTP_EUNSUPPORTED, "f32 path: output pruning");
     ztp::GemmParamsF32 p{};
     p.kind = kind;
     p.M = M;
@@ -515,6 +535,16 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("g_t", g));
   const int64_t N = g.cols;
   if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
+  // dW concurrently with dX on the side stream (not while emulating a
+  // straggler -- the slowdown stamps one GEMM at a time -- nor while profiling,
+  // which times each GEMM alone)
+  const bool conc = c->conc_bwd && !c->prof_on && a->dx_t.ptr && a->dw_t.ptr && !emulating(c);
+  cudaStream_t sw = st;
+  if (conc) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_c, st));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_c, 0));
+    sw = c->side_stream;
+  }
   if (a->dx_t.ptr) {
     if (!mat_ok(a->dx_t) || (dxc ? a->dx_t.rows < nk : a->dx_t.rows != K) || a->dx_t.cols != N ||
         a->dx_t.dtype != dtype)
@@ -556,18 +586,17 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
       return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("x_t", x) + " vs " + shp("g_t", g));
     if (!mat_ok(a->dw_t) || a->dw_t.rows != K || a->dw_t.cols < n_out || a->dw_t.dtype != dtype)
       return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dw_t", a->dw_t));
-    s = operand_src(c, dense_sel, xc, x, a->xs_t, false, kept, nk, 0, &tmpx, &X, st);
+    s = operand_src(c, dense_sel, xc, x, a->xs_t, false, kept, nk, 0, &tmpx, &X, sw);
     if (s != ZTP_OK) return s;
+    // output pruning: the GEMM computes the compact columns S'; its split-K
+    // reduce (or an expansion pass) spreads them to their units, P' <- Zero
     s = gemm(c, ztp::KIND_DW, X, Src{&g, true}, n_y, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
-             ztp::EPI_NONE, st);
+             ztp::EPI_NONE, sw, false, os ? a->y_pos : nullptr, (int)n_out);
     if (s != ZTP_OK) return s;
-    if (os) {
-      // columns S' were written compact; spread them to their units, P' <- Zero
-      const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
-      CUDA_TRY(c, ztp::expand_cols_launch(a->dw_t.ptr, a->dw_t.ld, (int)K, a->y_pos, (int)n_y, (int)n_out, st));
-      prof_end(c, pe, st);
-      ++c->launches;
-    }
+  }
+  if (conc) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_d, sw));
+    CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_d, 0));
   }
   if (reduce_dx) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_b, 0));
   return ZTP_OK;
@@ -640,6 +669,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   c->num_sms = prop.multiProcessorCount;
   if (const char* g4 = getenv("ZTP_GATHER4")) c->use_gather4 = atoi(g4) != 0;
   if (const char* sk = getenv("ZTP_SPLITK")) c->allow_splitk = atoi(sk) != 0;
+  if (const char* cc = getenv("ZTP_CONC")) c->conc_bwd = atoi(cc) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   auto cleanup = [&](ztp_status s) {
     ztp_ctx_destroy(c);
@@ -654,7 +684,10 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   cudaMemset(c->d_gemm_ns, 0, 16);
   if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_d, cudaEventDisableTiming) != cudaSuccess)
     return cleanup(fail(nullptr, ZTP_ECUDA, "ztp_ctx_create: stream/event creation failed"));
   if (ensure_iota(c, 1 << 16) != ZTP_OK) return cleanup(ZTP_ECUDA);
   if (world > 1) {
@@ -674,6 +707,11 @@ ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->ev_c) cudaEventDestroy(c->ev_c);
+  if (c->ev_d) cudaEventDestroy(c->ev_d);
+  if (c->skws_side) cudaFree(c->skws_side);
+  if (c->d_pstamp) cudaFree(c->d_pstamp);
   cudaFree(c->d_flags);
   cudaFree(c->d_stamp);
   cudaFree(c->d_gemm_ns);
@@ -882,6 +920,11 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
 ztp_status ztp_set_profile(ztp_ctx* c, int on) {
   if (!c) return fail(c, ZTP_EINVAL, "ztp_set_profile: null ctx");
   c->prof_on = on ? 1 : 0;
+  if (on && !c->d_pstamp) CUDA_TRY(c, cudaMalloc(&c->d_pstamp, 2 * ztp_ctx::PSTAMP_CAP * sizeof(unsigned long long)));
+  if (on) {
+    CUDA_TRY(c, cudaMemset(c->d_pstamp, 0, 2 * ztp_ctx::PSTAMP_CAP * sizeof(unsigned long long)));
+    c->pstamp_used = 0;
+  }
   return ZTP_OK;
 }
 
@@ -889,6 +932,7 @@ ztp_status ztp_read_profile(ztp_ctx* c, void* stream, ztp_profile* out) {
   if (!c || !out) return fail(c, ZTP_EINVAL, "ztp_read_profile: null argument");
   CUDA_TRY(c, cudaStreamSynchronize((cudaStream_t)stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->comm_stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->side_stream));
   std::memset(out, 0, sizeof(*out));
   for (size_t i = 0; i < c->prof_used; ++i) {
     float ms = 0.f;
@@ -906,6 +950,16 @@ ztp_status ztp_read_profile(ztp_ctx* c, void* stream, ztp_profile* out) {
     }
   }
   c->prof_used = 0;
+  if (c->pstamp_used > 0) {
+    std::vector<unsigned long long> h(2 * (size_t)c->pstamp_used);
+    CUDA_TRY(c, cudaMemcpy(h.data(), c->d_pstamp, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < c->pstamp_used; ++i) {
+      const unsigned long long t0 = ~h[2 * i], t1 = h[2 * i + 1];
+      if (h[2 * i] != 0 && t1 >= t0) out->gemm_kernel_ms += (double)(t1 - t0) * 1e-6;
+    }
+    CUDA_TRY(c, cudaMemset(c->d_pstamp, 0, h.size() * sizeof(unsigned long long)));
+    c->pstamp_used = 0;
+  }
   return ZTP_OK;
 }
 

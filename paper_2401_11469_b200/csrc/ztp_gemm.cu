@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   pdl_wait();
   pdl_trigger();
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMin(p.stamp, (unsigned long long)globaltimer());
+  if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp, ~(unsigned long long)globaltimer());
 
   const Sched<KIND, C::TM> sc(p);
 
@@ -570,21 +571,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tmem_dealloc(tmem_base, 512);
   }
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMax(p.stamp + 1, (unsigned long long)globaltimer());
+  if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp + 1, (unsigned long long)globaltimer());
 }
 
 // Split-K reduction (fixed split order -> deterministic) fused with the
 // epilogue the unsplit kernel applies: GeLU / GeLU', bf16 RNE, lineage row map
 // and the Zero imputation of pruned rows.
 template <int KIND>
-__global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
-  pdl_wait();
-  pdl_trigger();
-  const int cpr = (p.N + 7) / 8;
+__device__ __forceinline__ void splitk_reduce_body(const GemmParams& p) {
+  // col_pos (DW with output pruning): output column j <- compact column
+  // col_pos[j] of the partials, Zero where col_pos[j] < 0
+  const int width = p.col_pos ? p.n_full : p.N;
+  const int cpr = (width + 7) / 8;
   const int64_t total = (int64_t)p.M * cpr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int m = (int)(i / cpr);
     const int col = (int)(i % cpr) * 8;
-    const int nv = p.N - col;
+    const int nv = width - col;
     const bool computed = (KIND == KIND_FWD) || (m < p.n_kept);
     int orow;
     if (p.out_dense)
@@ -595,7 +598,17 @@ __global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
       orow = computed ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
     if (orow < 0) continue;
     float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (computed) {
+    if (computed && p.col_pos) {
+      int cc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cc[q] = q < nv ? __ldg(p.col_pos + col + q) : -1;
+      const float* src = p.ws + (int64_t)m * p.ld_ws;
+      for (int s = 0; s < p.splits; ++s, src += p.ws_split_stride) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (cc[q] >= 0) v[q] += __ldcg(src + cc[q]);
+      }
+    } else if (computed) {
       const float* src = p.ws + (int64_t)m * p.ld_ws + col;
       for (int s = 0; s < p.splits; ++s) {
         const float4 a = *reinterpret_cast<const float4*>(src);
@@ -649,6 +662,14 @@ __global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
     store_bf16x8(p.out + (int64_t)orow * p.ld_out + col, w, nv);
     if (p.epi == EPI_GELU || p.epi == EPI_GELU_D) store_bf16x8(p.out2 + (int64_t)orow * p.ld_out2 + col, g, nv);
   }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
+  pdl_wait();
+  pdl_trigger();
+  splitk_reduce_body<KIND>(p);
+  if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp + 1, (unsigned long long)globaltimer());
 }
 
 // ----------------------------------------------------------------- host side
@@ -737,8 +758,12 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, mp.w, p);
     if (e != cudaSuccess) return e;
   }
-  if (p.splits == 1) return cudaSuccess;
-  const int64_t chunks = (int64_t)p.M * ((p.N + 7) / 8);
+  if (p.splits == 1) {
+    if (p.col_pos)   // compact columns written by the epilogue: spread them, Zero the rest
+      return expand_cols_launch(p.out, p.ld_out, p.out_rows, p.col_pos, p.N, p.n_full, st);
+    return cudaSuccess;
+  }
+  const int64_t chunks = (int64_t)p.M * (((p.col_pos ? p.n_full : p.N) + 7) / 8);
   const int blocks = (int)std::min<int64_t>((chunks + 255) / 256, (int64_t)num_sms * 8);
   return launch_k(ztp_splitk_reduce<KIND>, blocks, 256, 0, st, p);
 }

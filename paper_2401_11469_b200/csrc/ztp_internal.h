@@ -60,6 +60,9 @@ struct GemmParams {
   int oob_out;   // a row index outside the output tensor (TMA stores skip it)
   int out_rows;  // rows of the output tensor(s)
   int out_dense; // the row map is the identity on m < M (set by the host): dense TMA box stores
+  unsigned long long* prof_stamp;  // profiling: [max ~start, max end] %globaltimer (nullable)
+  const int32_t* col_pos;  // DW output pruning: full column j <- compact column col_pos[j] (< 0: Zero)
+  int n_full;              // full output columns when col_pos is set (N = compact columns)
 };
 
 // Split-K choice for a launch and the fp32 workspace it needs (bytes).

@@ -66,7 +66,7 @@ def main():
                 Z.ztp_gemm(ctx, kind, a)
             prof = Z.ztp_read_profile(ctx)
             Z.ztp_set_profile(ctx, False)
-            t = prof["gemm_ms"] / 20
+            t = prof["gemm_kernel_ms"] / 20
             tf = prof["gemm_flops"] / 20 / (t * 1e-3) / 1e12
             print(f"dbg={dbg} {name:16s} {t * 1e3:7.1f} us {tf:7.1f} TF/s", flush=True)
         Z.ztp_ctx_destroy(ctx)
