@@ -282,6 +282,10 @@ typedef struct ztp_linear_args {
    *      contracts dX over S' only, and writes dw_t[k, p] = 0 for p in P'.
    * Results are identical to the full-output computation.  NULL = off. */
   const ztp_sel* out_sel;
+  /* FWD: compact copies already written by ztp_prepare for this lineage
+   * entry -- bit 0: xs_t, bit 1: ws_t -- so this call does not refill them. */
+  int32_t prepared;
+  int32_t _pad1;
   int64_t n_out;               /* output units computed (<= w_t.cols); 0 = w_t.cols */
   int32_t impute;              /* ztp_impute (Zero is the paper's choice) */
   int32_t act;                 /* FWD activation of this layer's output */
@@ -292,6 +296,15 @@ typedef struct ztp_linear_args {
   const ztp_mat* hist_dx;      /* Same imputation history for dx_t (or NULL) */
   const ztp_mat* hist_dw;      /* Same imputation history for dw_t (or NULL) */
 } ztp_linear_args;
+
+/* a4, batched: the compact operand copies of several linears in ONE launch
+ * (fewer kernel boundaries than one gather per linear).  For args[i] with a
+ * lineage entry: what[i] bit 0 -> xs_t <- rows S of x_t (not with x_compact),
+ * bit 1 -> ws_t <- rows S of w_t (with out_sel: W^T[S, S'], or W^T[:, S'] when
+ * sel is NULL).  xs_t / ws_t must be caller buffers of sufficient size.  The
+ * caller then sets args[i]->prepared to the same bits for the FWD call.
+ * n <= 16 copies in total.  Errors: EINVAL, ESHAPE, EUNSUPPORTED (f32). */
+ztp_status ztp_prepare(ztp_ctx* ctx, int n, const ztp_linear_args* const* args, const int32_t* what, void* stream);
 
 ztp_status ztp_col_linear(ztp_ctx* ctx, ztp_phase phase, const ztp_linear_args* a, void* stream);
 ztp_status ztp_row_linear(ztp_ctx* ctx, ztp_phase phase, const ztp_linear_args* a, void* stream);

@@ -174,6 +174,14 @@ def ztp_row_linear(ctx, phase: int, args: LinearArgs, stream=None) -> None:
     check(lib.ztp_row_linear(ctx, phase, C.byref(args), _stream(stream)), ctx)
 
 
+def ztp_prepare(ctx, items, stream=None) -> None:
+    """items: [(LinearArgs, what_bits)] -> one batched compaction launch."""
+    n = len(items)
+    arr = (C.POINTER(LinearArgs) * n)(*[C.pointer(a) for a, _ in items])
+    what = (C.c_int32 * n)(*[int(w) for _, w in items])
+    check(lib.ztp_prepare(ctx, n, arr, what, _stream(stream)), ctx)
+
+
 def ztp_gemm(ctx, kind: int, args: LinearArgs, stream=None) -> None:
     check(lib.ztp_gemm(ctx, kind, C.byref(args), _stream(stream)), ctx)
 

@@ -73,7 +73,7 @@ class LinearArgs(C.Structure):
     _fields_ = [("x_t", Mat), ("w_t", Mat), ("y_t", Mat), ("pre_t", Mat), ("g_t", Mat), ("dx_t", Mat),
                 ("dw_t", Mat), ("pre_in_t", Mat), ("xs_t", Mat), ("ws_t", Mat), ("sel", C.POINTER(Sel)),
                 ("y_pos", C.c_void_p), ("x_compact", C.c_int32), ("dx_compact", C.c_int32),
-                ("out_sel", C.POINTER(Sel)), ("n_out", C.c_int64),
+                ("out_sel", C.POINTER(Sel)), ("prepared", C.c_int32), ("_pad1", C.c_int32), ("n_out", C.c_int64),
                 ("impute", C.c_int32), ("act", C.c_int32), ("act_in", C.c_int32), ("gather_output", C.c_int32),
                 ("input_is_parallel", C.c_int32), ("skip_collective", C.c_int32),
                 ("hist_dx", C.POINTER(Mat)), ("hist_dw", C.POINTER(Mat))]
@@ -124,6 +124,7 @@ def _load():
         "ztp_set_stats": (st, [vp, C.c_int]),
         "ztp_read_gemm_ns": (st, [vp, vp, C.POINTER(C.c_double)]),
         "ztp_gemm": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
+        "ztp_prepare": (st, [vp, C.c_int, C.POINTER(C.POINTER(LinearArgs)), C.POINTER(C.c_int32), vp]),
         "ztp_set_profile": (st, [vp, C.c_int]),
         "ztp_read_profile": (st, [vp, vp, C.POINTER(Profile)]),
     }
@@ -140,7 +141,7 @@ lib = _load()
 EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_id", "ztp_ctx_create",
             "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count", "ztp_plan_opts_default", "ztp_plan",
             "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
-            "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm",
+            "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "ztp_prepare",
             "ztp_set_profile", "ztp_read_profile")
 
 

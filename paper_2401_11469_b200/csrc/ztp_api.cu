@@ -57,6 +57,8 @@ struct ztp_ctx {
   int use_gather4 = 0;                 // 1: gather rows in the GEMM producer with TMA gather4
   int allow_splitk = 1;                // split-K for few-tile GEMMs (ZTP_SPLITK=0 disables)
   int dbg_epi = 0;                     // ZTP_DEBUG_EPI (performance experiments; results invalid)
+  int dbg_skip = 0;                    // ZTP_DEBUG_SKIP bitmask (timing experiments only, results invalid):
+                                       // 1 select, 2 compaction copies, 4 core, 16 GEMMs
   void* skws = nullptr;                // split-K fp32 partials
   size_t skws_cap = 0;
   // profiling (ztp_set_profile): event pairs around every kernel class
@@ -303,7 +305,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.splits = 1;
       p.kb_per_split = (kdim + 63) / 64;
     }
-    CUDA_TRY(c, ztp::gemm_launch(kind, o, p, c->num_sms, st));
+    if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, c->num_sms, st));
     if (p.splits > 1 || p.col_pos) ++c->launches;   // split-K reduce or column expansion
   } else {
     if (col_pos) return fail(c, ZTP_EUNSUPPORTED, "f32 path: output pruning");
@@ -383,7 +385,8 @@ ztp_status compact_rows(ztp_ctx* c, const ztp_mat& full, const int32_t* kept, in
   if (!mat_ok(d) || d.rows < nk || d.cols < full.cols || d.dtype != full.dtype)
     return fail(c, ZTP_ESHAPE, "compact buffer " + shp("dst", d) + " too small for " + shp("src", full));
   const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
-  CUDA_TRY(c, ztp::gather_rows_launch(full.ptr, full.ld, kept, nk, full.cols, d.ptr, d.ld, full.dtype, st));
+  if (!(c->dbg_skip & 2))
+    CUDA_TRY(c, ztp::gather_rows_launch(full.ptr, full.ld, kept, nk, full.cols, d.ptr, d.ld, full.dtype, st));
   prof_end(c, pe, st);
   ++c->launches;
   d.rows = nk;
@@ -419,7 +422,7 @@ ztp_status weight_2d(ztp_ctx* c, const ztp_mat& w, const int32_t* rows, int nk, 
   d.cols = n_y;
   if (refill) {
     const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
-    CUDA_TRY(c, ztp::gather_2d_launch(w.ptr, w.ld, rows, nk, cols, n_y, d.ptr, d.ld, st));
+    if (!(c->dbg_skip & 2)) CUDA_TRY(c, ztp::gather_2d_launch(w.ptr, w.ld, rows, nk, cols, n_y, d.ptr, d.ld, st));
     prof_end(c, pe, st);
     ++c->launches;
   }
@@ -508,12 +511,14 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     if (act && (!mat_ok(a->pre_t) || a->pre_t.rows < out_rows_need || a->pre_t.cols != N))
       return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD GeLU: " + shp("pre_t", a->pre_t));
     if (a->sel) c->lineage[key] = LineageEntry{a->sel->kept, a->sel->pruned, a->sel->n_kept, a->sel->n_pruned};
-    s = operand_src(c, dense_sel, xc, x, a->xs_t, true, kept, nk, 0, &tmpx, &X, st);
+    const bool fill_x = !(a->prepared & 1) || !a->xs_t.ptr;   // ztp_prepare wrote the copies already
+    const bool fill_w = !(a->prepared & 2) || !a->ws_t.ptr;
+    s = operand_src(c, dense_sel, xc, x, a->xs_t, fill_x, kept, nk, 0, &tmpx, &X, st);
     if (s != ZTP_OK) return s;
     if (os)
-      s = weight_2d(c, a->w_t, dense_sel ? nullptr : kept, nk, os->kept, (int)n_y, a->ws_t, true, &tmpw, &W, st);
+      s = weight_2d(c, a->w_t, dense_sel ? nullptr : kept, nk, os->kept, (int)n_y, a->ws_t, fill_w, &tmpw, &W, st);
     else
-      s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, true, kept, nk, 1, &tmpw, &W, st);
+      s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, fill_w, kept, nk, 1, &tmpw, &W, st);
     if (s != ZTP_OK) return s;
     s = gemm(c, ztp::KIND_FWD, W, X, n_y, kept, pruned, nk, act ? a->pre_t : a->y_t, act ? &a->y_t : nullptr,
              nullptr, 0, os ? nullptr : a->y_pos, act ? act_epi : ztp::EPI_NONE, st);
@@ -671,6 +676,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* sk = getenv("ZTP_SPLITK")) c->allow_splitk = atoi(sk) != 0;
   if (const char* cc = getenv("ZTP_CONC")) c->conc_bwd = atoi(cc) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
+  if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
   auto cleanup = [&](ztp_status s) {
     ztp_ctx_destroy(c);
     return s;
@@ -790,10 +796,62 @@ ztp_status ztp_select(ztp_ctx* c, int nseg, const int32_t* h_len, const int32_t*
     p.nseg = std::min(ztp::SELECT_MAX_SEGS, nseg - b);
     for (int i = 0; i < p.nseg; ++i) p.seg[i] = segs[b + i];
     const int pe = prof_begin(c, (cudaStream_t)stream, PROF_OTHER, 0.0);
-    CUDA_TRY(c, ztp::select_launch(p, d_scores, d_kept, d_pruned, d_pos, c->d_flags, (cudaStream_t)stream));
+    if (!(c->dbg_skip & 1))
+      CUDA_TRY(c, ztp::select_launch(p, d_scores, d_kept, d_pruned, d_pos, c->d_flags, (cudaStream_t)stream));
     prof_end(c, pe, (cudaStream_t)stream);
     ++c->launches;
   }
+  return ZTP_OK;
+}
+
+ztp_status ztp_prepare(ztp_ctx* c, int n, const ztp_linear_args* const* args, const int32_t* what, void* stream) {
+  if (!c || n < 0 || (n > 0 && (!args || !what))) return fail(c, ZTP_EINVAL, "ztp_prepare: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  ztp::GatherJobs J{};
+  auto add = [&](const void* src, int64_t ld_src, const int32_t* rows, int nr, const int32_t* cols, int nc,
+                 const ztp_mat& dst) -> ztp_status {
+    if (J.njobs == ztp::GATHER_MAX_JOBS) return fail(c, ZTP_EINVAL, "ztp_prepare: more than 16 copies");
+    if (!mat_ok(dst) || dst.rows < nr || dst.cols < nc || dst.dtype != ZTP_BF16)
+      return fail(c, ZTP_ESHAPE, "ztp_prepare: destination " + shp("dst", dst) + " too small / not bf16");
+    ztp::GatherJob& g = J.job[J.njobs++];
+    g = ztp::GatherJob{(const uint16_t*)src, ld_src, rows, cols, (uint16_t*)dst.ptr, dst.ld, nr, nc, J.total};
+    J.total += (int64_t)nr * ((nc + 7) / 8);
+    return ZTP_OK;
+  };
+  for (int i = 0; i < n; ++i) {
+    const ztp_linear_args* a = args[i];
+    if (!a) return fail(c, ZTP_EINVAL, "ztp_prepare: null args");
+    if (a->w_t.dtype != ZTP_BF16) return fail(c, ZTP_EUNSUPPORTED, "ztp_prepare: bf16 only");
+    const int64_t K = a->w_t.rows;
+    const int32_t* kept;
+    const int32_t* pruned;
+    int nk, np;
+    ztp_status s = resolve_sel(c, a->sel, K, &kept, &pruned, &nk, &np);
+    if (s != ZTP_OK) return s;
+    const bool dense = a->sel == nullptr;
+    if ((what[i] & 1) && !dense && !a->x_compact) {
+      if (!mat_ok(a->x_t) || a->x_t.rows != K || a->x_t.dtype != ZTP_BF16)
+        return fail(c, ZTP_ESHAPE, "ztp_prepare: " + shp("x_t", a->x_t));
+      s = add(a->x_t.ptr, a->x_t.ld, kept, nk, nullptr, (int)a->x_t.cols, a->xs_t);
+      if (s != ZTP_OK) return s;
+    }
+    if (what[i] & 2) {
+      const int64_t n_out = a->n_out > 0 ? a->n_out : a->w_t.cols;
+      if (a->out_sel) {
+        if ((int64_t)a->out_sel->n_kept + a->out_sel->n_pruned != n_out || !a->out_sel->kept)
+          return fail(c, ZTP_ESHAPE, "ztp_prepare: out_sel does not cover n_out");
+        s = add(a->w_t.ptr, a->w_t.ld, dense ? nullptr : kept, nk, a->out_sel->kept, a->out_sel->n_kept, a->ws_t);
+      } else if (!dense) {
+        s = add(a->w_t.ptr, a->w_t.ld, kept, nk, nullptr, (int)a->w_t.cols, a->ws_t);
+      }
+      if (s != ZTP_OK) return s;
+    }
+  }
+  if (J.total == 0) return ZTP_OK;
+  const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
+  if (!(c->dbg_skip & 2)) CUDA_TRY(c, ztp::gather_multi_launch(J, st));
+  prof_end(c, pe, st);
+  ++c->launches;
   return ZTP_OK;
 }
 
@@ -852,8 +910,10 @@ ztp_status ztp_core(ztp_ctx* c, ztp_phase phase, const ztp_mat* qkv, const ztp_m
     return fail(c, ZTP_ESHAPE, "ztp_core: " + shp("qkv_t", *qkv) + " " + shp("ctx_t", *cx));
   if (qkv->dtype == ZTP_BF16 && qkv->cols % 8) return fail(c, ZTP_ESHAPE, "ztp_core: N % 8 != 0");
   const int pe = prof_begin(c, (cudaStream_t)stream, PROF_OTHER, 0.0);
-  CUDA_TRY(c, ztp::core_launch(phase == ZTP_FWD ? 0 : 1, qkv->ptr, qkv->ld, cx->ptr, cx->ld, feat, n_out, qkv->cols,
-                               qkv->dtype, phase == ZTP_FWD ? rows : nullptr, (cudaStream_t)stream));
+  if (!(c->dbg_skip & 4)) {
+    CUDA_TRY(c, ztp::core_launch(phase == ZTP_FWD ? 0 : 1, qkv->ptr, qkv->ld, cx->ptr, cx->ld, feat, n_out, qkv->cols,
+                                 qkv->dtype, phase == ZTP_FWD ? rows : nullptr, (cudaStream_t)stream));
+  }
   prof_end(c, pe, (cudaStream_t)stream);
   ++c->launches;
   return ZTP_OK;

@@ -129,6 +129,24 @@ cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* i
                                int64_t ld_dst, int dtype, cudaStream_t st);
 cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* rows, int n, const int32_t* cols, int nc,
                              void* dst, int64_t ld_dst, cudaStream_t st);
+// Batched compaction (ztp_prepare): dst[r, c] = src[rows ? rows[r] : r, cols ? cols[c] : c], bf16.
+struct GatherJob {
+  const uint16_t* src;
+  int64_t ld_src;
+  const int32_t* rows;   // nullable: identity
+  const int32_t* cols;   // nullable: identity (16-byte vector copies)
+  uint16_t* dst;
+  int64_t ld_dst;
+  int32_t n, nc;
+  int64_t vbegin;        // first 8-column vector of this job in the launch
+};
+constexpr int GATHER_MAX_JOBS = 16;
+struct GatherJobs {
+  int njobs;
+  int64_t total;         // vectors over all jobs
+  GatherJob job[GATHER_MAX_JOBS];
+};
+cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st);
 cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, int nc, int n_full, cudaStream_t st);
 cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
                              cudaStream_t st);

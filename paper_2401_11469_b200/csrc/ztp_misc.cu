@@ -204,6 +204,47 @@ cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* row
                   ld_dst);
 }
 
+// Batched compaction of several operands (ztp_prepare): one launch, each
+// thread one 8-column (16-byte) output vector of some job.
+__global__ void ztp_gather_multi(const GatherJobs J) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < J.total; v += (int64_t)gridDim.x * blockDim.x) {
+    int j = 0;
+#pragma unroll 1
+    while (j + 1 < J.njobs && v >= J.job[j + 1].vbegin) ++j;
+    const GatherJob& g = J.job[j];
+    const int vpr = (g.nc + 7) / 8;
+    const int64_t local = v - g.vbegin;
+    const int r = (int)(local / vpr), c0 = (int)(local % vpr) * 8;
+    const uint16_t* s = g.src + (int64_t)(g.rows ? __ldg(g.rows + r) : r) * g.ld_src;
+    uint16_t* d = g.dst + (int64_t)r * g.ld_dst + c0;
+    if (c0 + 8 <= g.nc) {
+      uint4 w;
+      if (g.cols) {
+        uint32_t q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          q[k] = (uint32_t)__ldg(s + __ldg(g.cols + c0 + 2 * k)) |
+                 ((uint32_t)__ldg(s + __ldg(g.cols + c0 + 2 * k + 1)) << 16);
+        w = make_uint4(q[0], q[1], q[2], q[3]);
+      } else {
+        w = __ldg(reinterpret_cast<const uint4*>(s + c0));
+      }
+      *reinterpret_cast<uint4*>(d) = w;
+    } else {
+      for (int c = c0; c < g.nc; ++c) d[c - c0] = __ldg(s + (g.cols ? __ldg(g.cols + c) : c));
+    }
+  }
+}
+
+cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st) {
+  if (j.total <= 0) return cudaSuccess;
+  int blocks = (int)((j.total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  return launch_k(ztp_gather_multi, blocks, 256, 0, st, j);
+}
+
 // In-place column expansion (output pruning, bf16): row r of t holds nc
 // compact columns; afterwards t[r, j] = pos[j] >= 0 ? old[r, pos[j]] : 0 for
 // j < n_full (the Zero gradient of the consumer-pruned units).  One CTA

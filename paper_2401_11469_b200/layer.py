@@ -216,6 +216,12 @@ class ZtpLayer:
                        sel_=self.sels["fc1"], n_out=nfc, act=Z.ACT_GELU_D, y_pos=self.POS["fc2"], out_sel=osel)
         self.f_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], y_t=self.Y, ws_t=self.W2_c,
                        sel_=self.sels["fc2"], x_compact=True)
+        # batched compaction (ztp_prepare): X + Wqkv, Wo, W1 (2D), W2
+        self._prep = []
+        for args, what in ((self.f_qkv, 3), (self.f_o, 2), (self.f_fc1, 2), (self.f_fc2, 2)):
+            if args.sel or args.out_sel:
+                args.prepared = what
+                self._prep.append((args, what))
         # backward
         self.b_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], g_t=self.G, dx_t=self.G1[:ng],
                        dw_t=self.dw2[:nfc], pre_in_t=self.PreC[:nk["fc2"]], ws_t=self.W2_c,
@@ -247,8 +253,16 @@ class ZtpLayer:
             Z.ztp_migrate(self.ctx, self._xfers(True), stream)
 
     # -------------------------------------------------------------------- step
+    def prepare(self, stream=None):
+        """All compact operand copies that depend only on the step's inputs,
+        weights and selection (X rows S_qkv, and the weight blocks of the four
+        linears) in one launch; the FWD calls then skip their own copies."""
+        if self._prep:
+            Z.ztp_prepare(self.ctx, self._prep, stream)
+
     def fwd_attn(self, stream=None):
         c = self.ctx
+        self.prepare(stream)
         Z.ztp_col_linear(c, Z.FWD, self.f_qkv, stream)
         Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, self.S["o"], self.nk["o"], stream)
         Z.ztp_row_linear(c, Z.FWD, self.f_o, stream)          # + all-reduce of Y1

@@ -343,3 +343,27 @@ def test_gemm_large_c2_shapes_sampled(env):
     ok, e = err_ok(dwh[np.ix_(rk, rows_n)], Xt[rk] @ Gt[rows_n].T, TOL_BF16)
     assert ok, e
     assert np.all(dxh[P] == 0) and np.all(dwh[P] == 0)
+
+
+def test_prepare_batched_compaction(env):
+    """ztp_prepare: one launch writes xs_t = x[S], ws_t = w[S] and the 2D block
+    W^T[S, S'] (out_sel), bit-exact copies; ragged widths use the scalar path."""
+    Z, torch, ctx = env
+    K, n, N = 300, 523, 264
+    X = I.normal(5, "x", K, N)
+    W = I.uniform_sym(5, "w", K, n, 0.1)
+    S, P = O.select(I.lognormal_scores(5, "s", K), 120)
+    S2, P2 = O.select(I.lognormal_scores(5, "s2", n), 200)
+    s, keep = _sel_dev(Z, torch, S, P)
+    s2, keep2 = _sel_dev(Z, torch, S2, P2, 0, 1)
+    x, w = dev(torch, X), dev(torch, W)
+    xs, ws, w2 = empty(torch, K, N, torch.bfloat16), empty(torch, K, n, torch.bfloat16), empty(torch, K, n, torch.bfloat16)
+    a1 = Z.linear_args(x_t=x, w_t=w, xs_t=xs, ws_t=ws, sel_=s)
+    a2 = Z.linear_args(x_t=x, w_t=w, ws_t=w2, sel_=s, out_sel=s2)
+    Z.ztp_prepare(ctx, [(a1, 3), (a2, 2)])
+    Z.ztp_sync(ctx)
+    Sa, S2a = np.asarray(S), np.asarray(S2)
+    xb, wb = host(x), host(w)
+    assert np.array_equal(host(xs[:len(S)]), xb[Sa])
+    assert np.array_equal(host(ws[:len(S)]), wb[Sa])
+    assert np.array_equal(host(w2[:len(S), :len(S2)]), wb[Sa][:, S2a])
