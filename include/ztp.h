@@ -226,9 +226,13 @@ ztp_status ztp_select(ztp_ctx* ctx, int nseg, const int32_t* h_seg_len, const in
  *                 gather_output (all-gather of y over ranks).
  *      row layer: y_t partial sums are all-reduced (sum) over ranks.
  * BWD  dx_t[k,t] = sum_{j < n_out} w_t[k,j] g_t[j,t]  for k in S
- *      dx_t[p,t]  = imputation for p in P (Zero; Average; Same from hist)
+ *      dx_t[p,t]  = imputation for p in P: Zero (0, the paper's choice);
+ *                   Average (per column t the mean of dx_t[k,t] over k in S,
+ *                   A-10); Same (hist_dx[p,t], the previous step's values,
+ *                   A-11; caller-owned [K, N]; missing -> ZTP_EHISTORY)
  *      dw_t[k,j]  = sum_t x_t[k,t] g_t[j,t]           for k in S, j < n_out
- *      dw_t[p,j]  = imputation for p in P
+ *      dw_t[p,j]  = imputation for p in P (as dx_t; Same from hist_dw [K, n])
+ *
  *      col layer: dx_t is all-reduced over ranks (the imputed rows
  *                 are applied to the partial BEFORE the sum, A-14).
  *      row layer: act_in = GELU multiplies dx_t by GeLU'(pre_in_t) (the

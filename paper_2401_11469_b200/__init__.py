@@ -146,7 +146,8 @@ def sel(kept, n_kept: int, pruned, n_pruned: int, layer_id: int, matrix_id: int)
 def linear_args(x_t=None, w_t=None, y_t=None, pre_t=None, g_t=None, dx_t=None, dw_t=None, pre_in_t=None,
                 sel_: Optional[Sel] = None, n_out: int = 0, impute: int = IMPUTE_ZERO, act: int = ACT_NONE,
                 act_in: int = ACT_NONE, skip_collective: int = 0, xs_t=None, ws_t=None, y_pos=None,
-                x_compact: bool = False, dx_compact: bool = False, out_sel: Optional[Sel] = None) -> LinearArgs:
+                x_compact: bool = False, dx_compact: bool = False, out_sel: Optional[Sel] = None,
+                hist_dx=None, hist_dw=None) -> LinearArgs:
     a = LinearArgs()
     a.x_t, a.w_t, a.y_t, a.pre_t = mat(x_t), mat(w_t), mat(y_t), mat(pre_t)
     a.g_t, a.dx_t, a.dw_t, a.pre_in_t = mat(g_t), mat(dx_t), mat(dw_t), mat(pre_in_t)
@@ -156,6 +157,8 @@ def linear_args(x_t=None, w_t=None, y_t=None, pre_t=None, g_t=None, dx_t=None, d
     a.dx_compact = int(dx_compact)
     a.sel = C.pointer(sel_) if sel_ is not None else None
     a.out_sel = C.pointer(out_sel) if out_sel is not None else None
+    a.hist_dx = C.pointer(mat(hist_dx)) if hist_dx is not None else None
+    a.hist_dw = C.pointer(mat(hist_dw)) if hist_dw is not None else None
     a.n_out = n_out
     a.impute = impute
     a.act = act

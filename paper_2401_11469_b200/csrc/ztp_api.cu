@@ -431,6 +431,25 @@ ztp_status weight_2d(ztp_ctx* c, const ztp_mat& w, const int32_t* rows, int nk, 
   return ZTP_OK;
 }
 
+// Average / Same imputation of rows P of a BWD output (NEXT-2; A-10,
+// A-11) after the GEMM wrote rows S (and Zero rows P).
+ztp_status impute(ztp_ctx* c, int policy, const ztp_mat& out, int64_t cols, const int32_t* kept, int nk,
+                  const int32_t* pruned, int np, const ztp_mat* hist, cudaStream_t st) {
+  if (policy == ZTP_IMPUTE_ZERO || np <= 0) return ZTP_OK;
+  if (policy == ZTP_IMPUTE_SAME) {
+    if (!hist || !hist->ptr) return fail(c, ZTP_EHISTORY, "Same imputation needs the previous step's values (S:74)");
+    if (!mat_ok(*hist) || hist->rows != out.rows || hist->cols < cols || hist->dtype != out.dtype)
+      return fail(c, ZTP_ESHAPE, "Same imputation: " + shp("hist", *hist) + " vs " + shp("out", out));
+  }
+  const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
+  CUDA_TRY(c, ztp::impute_rows_launch(out.ptr, out.ld, cols, kept, nk, pruned, np,
+                                      policy == ZTP_IMPUTE_AVERAGE ? 1 : 2, hist ? hist->ptr : nullptr,
+                                      hist ? hist->ld : 0, out.dtype, st));
+  prof_end(c, pe, st);
+  ++c->launches;
+  return ZTP_OK;
+}
+
 enum { LAYER_COL = 0, LAYER_ROW = 1 };
 
 // Source of the weight (or input) operand for this call.
@@ -467,8 +486,10 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
   const int64_t K = a->w_t.rows;
   const int64_t n_out = a->n_out > 0 ? a->n_out : a->w_t.cols;
   if (n_out > a->w_t.cols) return fail(c, ZTP_ESHAPE, std::string(nm) + ": n_out > w_t.cols");
-  if (a->impute != ZTP_IMPUTE_ZERO)
-    return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + ": Average/Same imputation are NEXT-2 (Zero only)");
+  if (a->impute < ZTP_IMPUTE_ZERO || a->impute > ZTP_IMPUTE_SAME)
+    return fail(c, ZTP_EINVAL, std::string(nm) + ": unknown imputation policy " + std::to_string(a->impute));
+  if (a->impute != ZTP_IMPUTE_ZERO && (a->dx_compact || a->out_sel))
+    return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + ": dx_compact / out_sel imply Zero imputation (A-35)");
   if (a->gather_output || (phase == ZTP_BWD && layer == LAYER_ROW && !a->input_is_parallel))
     return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + ": unpaired all-gather mode not built yet");
   const int dtype = a->w_t.dtype;
@@ -575,6 +596,9 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     s = gemm(c, ztp::KIND_DX, W, Src{&g, true}, n_y, kept, dxc ? nullptr : pruned, nk, dx, nullptr, aux, xc ? 1 : 0,
              nullptr, epi, st, dxc);
     if (s != ZTP_OK) return s;
+    // Average / Same on this rank's partial, before the all-reduce (A-14)
+    if (!dense_sel) s = impute(c, a->impute, a->dx_t, N, kept, nk, pruned, np, a->hist_dx, st);
+    if (s != ZTP_OK) return s;
   }
   const bool reduce_dx = layer == LAYER_COL && a->dx_t.ptr && !a->skip_collective && c->world > 1;
   if (reduce_dx) {
@@ -597,6 +621,8 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     // reduce (or an expansion pass) spreads them to their units, P' <- Zero
     s = gemm(c, ztp::KIND_DW, X, Src{&g, true}, n_y, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
              ztp::EPI_NONE, sw, false, os ? a->y_pos : nullptr, (int)n_out);
+    if (s != ZTP_OK) return s;
+    if (!dense_sel) s = impute(c, a->impute, a->dw_t, n_out, kept, nk, pruned, np, a->hist_dw, sw);
     if (s != ZTP_OK) return s;
   }
   if (conc) {

@@ -148,6 +148,10 @@ struct GatherJobs {
 };
 cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st);
 cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, int nc, int n_full, cudaStream_t st);
+// Average / Same imputation of rows P (NEXT-2): mode 1 = per-column
+// mean over rows S of `out` (A-10), mode 2 = rows P copied from `hist` (A-11).
+cudaError_t impute_rows_launch(void* out, int64_t ld, int64_t cols, const int32_t* kept, int nk, const int32_t* pruned,
+                               int np, int mode, const void* hist, int64_t ld_hist, int dtype, cudaStream_t st);
 cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
                              cudaStream_t st);
 

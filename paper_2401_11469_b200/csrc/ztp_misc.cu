@@ -294,6 +294,84 @@ cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, i
   return launch_k(ztp_expand_cols, blocks, 256, smem, st, (uint16_t*)t, ld, n, pos, nc, n_full);
 }
 
+// ------------------------------------------ Average / Same imputation (NEXT-2)
+// Average (A-10): one CTA per 8-column group; its threads stride over
+// the kept rows S, partial sums in fp32 are combined in a fixed tree order
+// (deterministic), mean = sum / |S|, written to every row p in P.  Zero rows
+// P written by the GEMM are overwritten.  Same (A-11): out[p] <- hist[p].
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+
+template <typename T>
+__global__ void __launch_bounds__(256) ztp_impute_average(T* out, int64_t ld, int64_t cols, const int32_t* kept, int nk,
+                                                          const int32_t* pruned, int np) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float part[8][256];
+  const int64_t c0 = (int64_t)blockIdx.x * 8;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+    const T* row = out + (int64_t)__ldg(kept + i) * ld + c0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (c0 + q < cols) acc[q] += to_f<T>(row[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) part[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) part[q][threadIdx.x] += part[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < np * 8; j += blockDim.x) {
+    const int r = j / 8, q = j % 8;
+    if (c0 + q < cols) out[(int64_t)__ldg(pruned + r) * ld + c0 + q] = from_f<T>(part[q][0] / (float)nk);
+  }
+}
+
+template <typename T>
+__global__ void ztp_impute_same(T* out, int64_t ld, int64_t cols, const int32_t* pruned, int np, const T* hist,
+                                int64_t ld_hist) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = (int64_t)np * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = __ldg(pruned + i / cols), c = i % cols;
+    out[r * ld + c] = hist[r * ld_hist + c];
+  }
+}
+
+cudaError_t impute_rows_launch(void* out, int64_t ld, int64_t cols, const int32_t* kept, int nk, const int32_t* pruned,
+                               int np, int mode, const void* hist, int64_t ld_hist, int dtype, cudaStream_t st) {
+  if (np <= 0 || cols <= 0) return cudaSuccess;
+  if (mode == 1) {
+    const int blocks = (int)((cols + 7) / 8);
+    if (dtype == 0)
+      return launch_k(ztp_impute_average<__nv_bfloat16>, blocks, 256, 0, st, (__nv_bfloat16*)out, ld, cols, kept, nk,
+                      pruned, np);
+    return launch_k(ztp_impute_average<float>, blocks, 256, 0, st, (float*)out, ld, cols, kept, nk, pruned, np);
+  }
+  int blocks = (int)(((int64_t)np * cols + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (dtype == 0)
+    return launch_k(ztp_impute_same<__nv_bfloat16>, blocks, 256, 0, st, (__nv_bfloat16*)out, ld, cols, pruned, np,
+                    (const __nv_bfloat16*)hist, ld_hist);
+  return launch_k(ztp_impute_same<float>, blocks, 256, 0, st, (float*)out, ld, cols, pruned, np, (const float*)hist,
+                  ld_hist);
+}
+
 // ------------------------------------------------------------- row fill (Zero)
 __global__ void ztp_fill_rows(uint8_t* out, int64_t ld_bytes, const int32_t* rows, int nrows, int64_t row_bytes) {
   pdl_wait();

@@ -367,3 +367,47 @@ def test_prepare_batched_compaction(env):
     assert np.array_equal(host(xs[:len(S)]), xb[Sa])
     assert np.array_equal(host(ws[:len(S)]), wb[Sa])
     assert np.array_equal(host(w2[:len(S), :len(S2)]), wb[Sa][:, S2a])
+
+
+@pytest.mark.parametrize("policy", ["average", "same"])
+@pytest.mark.parametrize("layer", ["col", "row"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_bwd_imputation_average_same(env, policy, layer, dtype):
+    """NEXT-2: rows P of dX and dW imputed by Average (per-column mean
+    over rows S, A-10) or Same (previous step's values, A-11); rows S as the
+    resized GEMM.  Same without history -> ZTP_EHISTORY."""
+    Z, torch, ctx = env
+    K, n, N = 300, 264, 520
+    Xt, Wt, Gt, S, P = _case(K, n, N, 0.35, seed=61)
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    tol = TOL_BF16 if dtype == "bf16" else TOL_F32
+    Hdx = I.normal(62, "hdx", K, N)
+    Hdw = I.normal(62, "hdw", K, n)
+    x, w, g = dev(torch, Xt, td), dev(torch, Wt, td), dev(torch, Gt, td)
+    y = empty(torch, n, N, td)
+    dx, dw = empty(torch, K, N, td), empty(torch, K, n, td)
+    s, keep = _sel_dev(Z, torch, S, P, 3, 0 if layer == "col" else 1)
+    pol = Z.IMPUTE_AVERAGE if policy == "average" else Z.IMPUTE_SAME
+    hx, hw = (dev(torch, Hdx, td), dev(torch, Hdw, td)) if policy == "same" else (None, None)
+    lin = Z.ztp_col_linear if layer == "col" else Z.ztp_row_linear
+    a = Z.linear_args(x_t=x, w_t=w, y_t=y, g_t=g, dx_t=dx, dw_t=dw, sel_=s, impute=pol, hist_dx=hx, hist_dw=hw)
+    lin(ctx, Z.FWD, a)
+    lin(ctx, Z.BWD, a)
+    Z.ztp_sync(ctx)
+    hist_x = host(hx) if hx is not None else None
+    hist_w = host(hw) if hw is not None else None
+    ref_dx = O.linear_bwd_dx(Wt, Gt, S, P, policy, hist_x)
+    ref_dw = O.linear_bwd_dw(Xt, Gt, S, P, policy, hist_w)
+    for name, got, ref in (("dx", dx, ref_dx), ("dw", dw, ref_dw)):
+        gh = host(got)
+        assert np.isfinite(gh).all(), name
+        ok, e = err_ok(gh, ref, tol)
+        assert ok, f"{name}: {e:.3e}"
+        Pa = np.asarray(P)
+        if policy == "same":
+            assert np.array_equal(gh[Pa], (hist_x if name == "dx" else hist_w)[Pa]), f"{name}: Same rows not copied"
+    if policy == "same":
+        b = Z.linear_args(x_t=x, w_t=w, y_t=y, g_t=g, dx_t=dx, dw_t=dw, sel_=s, impute=pol)
+        with pytest.raises(Z.ZtpError) as ei:
+            lin(ctx, Z.BWD, b)
+        assert ei.value.name == "ZTP_EHISTORY"
