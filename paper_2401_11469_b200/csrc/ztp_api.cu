@@ -203,7 +203,7 @@ struct Src {
 ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t* kept, const int32_t* pruned,
                 int nk, const ztp_mat& out, const ztp_mat* out2, const ztp_mat* aux, int aux_by_m,
                 const int32_t* out_pos, int epi, cudaStream_t st, bool out_compact = false,
-                const int32_t* col_pos = nullptr, int n_full = 0) {
+                const int32_t* col_pos = nullptr, int n_full = 0, bool indep_of_prev = false) {
   const int dtype = A.m->dtype;
   {
     const ztp_mat* need[3] = {A.m, B.m, &out};
@@ -279,6 +279,10 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     p.dbg = c->dbg_epi;
     p.col_pos = col_pos;
     p.n_full = n_full;
+    // early start (PDL wait at exit) only when nothing between the launches
+    // depends on stamps (emulation) and the workspaces are disjoint (dW uses
+    // its own split-K workspace)
+    p.pdl_late = indep_of_prev && !emulating(c) && ztp::pdl_enabled();
     if (c->prof_on && c->d_pstamp && c->pstamp_used < ztp_ctx::PSTAMP_CAP)
       p.prof_stamp = c->d_pstamp + 2 * (c->pstamp_used++);
     // split-K over the contraction when the output has too few tiles for 148 SMs
@@ -288,7 +292,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
       p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
       const size_t bytes = ztp::gemm_ws_bytes(kind, M, N, nk, p.splits);
-      const bool side = st == c->side_stream;
+      const bool side = st == c->side_stream || kind == ztp::KIND_DW;   // dW: its own workspace
       void*& wsp = side ? c->skws_side : c->skws;
       size_t& wcap = side ? c->skws_side_cap : c->skws_cap;
       if (wcap < bytes) {
@@ -615,12 +619,16 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
       return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("x_t", x) + " vs " + shp("g_t", g));
     if (!mat_ok(a->dw_t) || a->dw_t.rows != K || a->dw_t.cols < n_out || a->dw_t.dtype != dtype)
       return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dw_t", a->dw_t));
+    const int64_t l0 = c->launches;
     s = operand_src(c, dense_sel, xc, x, a->xs_t, false, kept, nk, 0, &tmpx, &X, sw);
     if (s != ZTP_OK) return s;
+    const bool copied = c->launches != l0;   // a compaction kernel now precedes the dW GEMM
     // output pruning: the GEMM computes the compact columns S'; its split-K
     // reduce (or an expansion pass) spreads them to their units, P' <- Zero
     s = gemm(c, ztp::KIND_DW, X, Src{&g, true}, n_y, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
-             ztp::EPI_NONE, sw, false, os ? a->y_pos : nullptr, (int)n_out);
+             ztp::EPI_NONE, sw, false, os ? a->y_pos : nullptr, (int)n_out,
+             /*indep_of_prev=*/a->dx_t.ptr != nullptr && !copied && !conc && !reduce_dx &&
+                 a->impute == ZTP_IMPUTE_ZERO);
     if (s != ZTP_OK) return s;
     if (!dense_sel) s = impute(c, a->impute, a->dw_t, n_out, kept, nk, pruned, np, a->hist_dw, sw);
     if (s != ZTP_OK) return s;

@@ -217,8 +217,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // prologue done (barriers, TMEM, descriptor prefetch): wait for the
-  // preceding kernel's results, let the next kernel begin its own prologue
-  pdl_wait();
+  // preceding kernel's results, let the next kernel begin its own prologue.
+  // pdl_late (a dW GEMM right after the dX GEMM it does not depend on): run
+  // now, wait for the predecessor only before exiting, so successors still
+  // see it complete (its own inputs were complete before the dX started).
+  if (!p.pdl_late) pdl_wait();
   pdl_trigger();
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMin(p.stamp, (unsigned long long)globaltimer());
   if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp, ~(unsigned long long)globaltimer());
@@ -570,6 +573,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     else
       tmem_dealloc(tmem_base, 512);
   }
+  if (p.pdl_late) pdl_wait();
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMax(p.stamp + 1, (unsigned long long)globaltimer());
   if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp + 1, (unsigned long long)globaltimer());
 }

@@ -63,6 +63,7 @@ struct GemmParams {
   unsigned long long* prof_stamp;  // profiling: [max ~start, max end] %globaltimer (nullable)
   const int32_t* col_pos;  // DW output pruning: full column j <- compact column col_pos[j] (< 0: Zero)
   int n_full;              // full output columns when col_pos is set (N = compact columns)
+  int pdl_late;            // inputs do not depend on the preceding kernel: PDL wait deferred to exit
 };
 
 // Split-K choice for a launch and the fp32 workspace it needs (bytes).
