@@ -535,6 +535,9 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
     if (act && (!mat_ok(a->pre_t) || a->pre_t.rows < out_rows_need || a->pre_t.cols != N))
       return fail(c, ZTP_ESHAPE, std::string(nm) + " FWD GeLU: " + shp("pre_t", a->pre_t));
+    if (layer == LAYER_ROW && a->y_pos && !a->skip_collective && c->world > 1)
+      return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + " FWD: an output row map (y_pos) needs TP = 1 or "
+                                                          "skip_collective (the all-reduce sums full outputs)");
     if (a->sel) c->lineage[key] = LineageEntry{a->sel->kept, a->sel->pruned, a->sel->n_kept, a->sel->n_pruned};
     const bool fill_x = !(a->prepared & 1) || !a->xs_t.ptr;   // ztp_prepare wrote the copies already
     const bool fill_w = !(a->prepared & 2) || !a->ws_t.ptr;

@@ -26,6 +26,7 @@ are pushed back to the owner after BWD.
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+import os
 from typing import Dict, List, Optional
 
 import torch
@@ -204,16 +205,29 @@ class ZtpLayer:
         # forward
         self.f_qkv = L(x_t=self.X, w_t=self.qkv_t, y_t=self.QKV, xs_t=self.Xc, ws_t=self.Wqkv_c,
                        sel_=self.sels["qkv"])
-        self.f_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, y_t=self.Y1, ws_t=self.Wo_c, sel_=self.sels["o"],
-                     x_compact=True)
+        # TP = 1 (no all-reduce of Y1): the O projection's epilogue writes Y1
+        # directly in FC1's kept order (rows S_fc1, through its inverse map),
+        # so no full Y1 and no compaction copy exist.  TP > 1 all-reduces the
+        # full Y1 first (ranks keep different S_fc1), then FC1 compacts.
+        self.y1_direct = (self.world == 1 and self.sels["fc1"] is not None
+                          and os.environ.get("ZTP_Y1_DIRECT", "1") != "0")   # A/B knob
+        if self.y1_direct:
+            y1, y1_kw = self.Y1c[:nk["fc1"]], {"x_compact": True}
+            self.f_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, y_t=self.Y1c, ws_t=self.Wo_c, sel_=self.sels["o"],
+                         x_compact=True, y_pos=self.POS["fc1"])
+        else:
+            y1, y1_kw = self.Y1, {"xs_t": self.Y1c}
+            self.f_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, y_t=self.Y1, ws_t=self.Wo_c, sel_=self.sels["o"],
+                         x_compact=True)
         # output pruning: FC1 computes only the hidden units FC2 keeps (S_fc2)
         # and its backward reads the compact G1 FC2's dX writes (rows P_fc2
         # are Zero) -- same results as the full FC1, half the work at
         # gamma = 0.5.  DESIGN.md "Output pruning".
         osel = self.sels["fc2"]
         ng = nk["fc2"] if osel is not None else nfc
-        self.f_fc1 = L(x_t=self.Y1, w_t=self.w1_t, y_t=self.HC, pre_t=self.PreC, xs_t=self.Y1c, ws_t=self.W1_c,
-                       sel_=self.sels["fc1"], n_out=nfc, act=Z.ACT_GELU_D, y_pos=self.POS["fc2"], out_sel=osel)
+        self.f_fc1 = L(x_t=y1, w_t=self.w1_t, y_t=self.HC, pre_t=self.PreC, ws_t=self.W1_c,
+                       sel_=self.sels["fc1"], n_out=nfc, act=Z.ACT_GELU_D, y_pos=self.POS["fc2"], out_sel=osel,
+                       **y1_kw)
         self.f_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], y_t=self.Y, ws_t=self.W2_c,
                        sel_=self.sels["fc2"], x_compact=True)
         # batched compaction (ztp_prepare): X + Wqkv, Wo, W1 (2D), W2
@@ -226,8 +240,9 @@ class ZtpLayer:
         self.b_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], g_t=self.G, dx_t=self.G1[:ng],
                        dw_t=self.dw2[:nfc], pre_in_t=self.PreC[:nk["fc2"]], ws_t=self.W2_c,
                        sel_=self.sels["fc2"], act_in=Z.ACT_GELU_D, x_compact=True, dx_compact=osel is not None)
-        self.b_fc1 = L(x_t=self.Y1, w_t=self.w1_t, g_t=self.G1[:ng], dx_t=self.dY1, dw_t=self.dw1, xs_t=self.Y1c,
-                       ws_t=self.W1_c, sel_=self.sels["fc1"], n_out=nfc, y_pos=self.POS["fc2"], out_sel=osel)
+        self.b_fc1 = L(x_t=y1, w_t=self.w1_t, g_t=self.G1[:ng], dx_t=self.dY1, dw_t=self.dw1,
+                       ws_t=self.W1_c, sel_=self.sels["fc1"], n_out=nfc, y_pos=self.POS["fc2"], out_sel=osel,
+                       **y1_kw)
         self.b_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx, dw_t=self.do,
                      ws_t=self.Wo_c, sel_=self.sels["o"], x_compact=True)
         self.b_qkv = L(x_t=self.X, w_t=self.qkv_t, g_t=self.gQKV, dx_t=self.dX, dw_t=self.dqkv, xs_t=self.Xc,
