@@ -114,8 +114,10 @@ struct SelectSeg {
   int32_t score_off, kept_off, pruned_off, pos_off;
 };
 constexpr int SELECT_MAX_SEGS = 64;
+constexpr int SELECT_SMEM_KEYS = 48 * 1024;
 struct SelectParams {
   int nseg;
+  int smem_keys;   // segments up to this length stage their keys in shared memory (set by select_launch)
   SelectSeg seg[SELECT_MAX_SEGS];
 };
 cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned, int32_t* pos,

@@ -57,6 +57,26 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
   pdl_trigger();
   const SelectSeg s = p.seg[blockIdx.x];
   const float* sc = scores + s.score_off;
+  // keys staged in shared memory once when the segment fits (every pass and
+  // the compaction then read smem instead of re-reading L2)
+  extern __shared__ uint32_t skey[];
+  const bool staged = s.len <= p.smem_keys;
+  bool saw_nan = false;
+  if (staged) {
+    for (int i = threadIdx.x; i < s.len; i += blockDim.x) {
+      bool nan;
+      skey[i] = ord32(sc[i], nan);
+      saw_nan |= nan;
+    }
+    __syncthreads();
+  }
+  auto key_at = [&](int i, bool& nan) -> uint32_t {
+    if (staged) {
+      nan = false;
+      return skey[i];
+    }
+    return ord32(sc[i], nan);
+  };
   int32_t* K = kept + s.kept_off;
   int32_t* P = pruned + s.pruned_off;
   int32_t* Q = pos ? pos + s.pos_off : nullptr;
@@ -68,17 +88,23 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
 
   uint32_t prefix = 0, mask = 0;
   int target = s.n_prune - 1;  // 0-based rank (by key) of the last pruned element
-  bool saw_nan = false;
   if (s.n_prune > 0) {
     for (int pass = 0; pass < 4; ++pass) {
       const int shift = 24 - 8 * pass;
       for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
       __syncthreads();
-      for (int i = tid; i < s.len; i += blockDim.x) {
-        bool nan;
-        const uint32_t key = ord32(sc[i], nan);
+      // warp-aggregated histogram: scores cluster in few exponent bins, so
+      // lanes with the same bin add once (__match_any_sync) instead of
+      // serialising on one shared-memory address
+      for (int base = 0; base < s.len; base += blockDim.x) {
+        const int i = base + tid;
+        bool nan = false;
+        const uint32_t key = i < s.len ? key_at(i, nan) : 0u;
         saw_nan |= nan;
-        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        const bool hit = i < s.len && (key & mask) == prefix;
+        const uint32_t bin = hit ? (key >> shift) & 255u : 256u;   // 256 = no bin
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+        if (hit && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
       }
       __syncthreads();
       if (tid < 32) {
@@ -114,7 +140,7 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
       target -= (int)sel_below;
       __syncthreads();
     }
-  } else {
+  } else if (!staged) {
     for (int i = tid; i < s.len; i += blockDim.x) {
       bool nan;
       (void)ord32(sc[i], nan);
@@ -130,7 +156,7 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
     const int i = base + tid;
     const bool valid = i < s.len;
     bool nan;
-    const uint32_t key = valid ? ord32(sc[i], nan) : 0u;
+    const uint32_t key = valid ? key_at(i, nan) : 0u;
     const bool less = valid && s.n_prune > 0 && key < v;
     const bool tie = valid && s.n_prune > 0 && key == v;
     int tot_tie, tot_p;
@@ -152,12 +178,23 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
     K[nk + a] = s.len + a;
     if (Q) Q[s.len + a] = nk + a;
   }
-  (void)lane;
 }
 
 cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned, int32_t* pos,
                           int32_t* err_flag, cudaStream_t st) {
-  cudaError_t e = launch_k(ztp_select_kernel, p.nseg, 1024, 0, st, p, scores, kept, pruned, pos, err_flag);
+  static int smem_set = 0;
+  SelectParams q = p;
+  int maxlen = 0;
+  for (int i = 0; i < p.nseg; ++i) maxlen = p.seg[i].len > maxlen ? p.seg[i].len : maxlen;
+  // stage keys in smem up to 48K keys (192 KB); longer segments re-read L2
+  q.smem_keys = maxlen <= SELECT_SMEM_KEYS ? maxlen : 0;
+  const int smem = q.smem_keys * 4;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(ztp_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  cudaError_t e = launch_k(ztp_select_kernel, p.nseg, 1024, smem, st, q, scores, kept, pruned, pos, err_flag);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
