@@ -326,6 +326,46 @@ def select(scores, n_prune: int):
 
 
 # ----------------------------------------------------------------------------
+# NEXT-1. Priority-score maintenance (Alg.1 l.4-11)
+# ----------------------------------------------------------------------------
+
+def column_delta(Wt_new, Wt_old):
+    """Alg.1 l.4: delta_i = sum_{j=1..R} |w_ji^t - w_ji^{t-1}| / R, the average
+    change of the paper's column i of the weight [R, L].  Here row i of Wt
+    [K=L, n=R].  Pinned: S:87 worked example, constant-shift closed form."""
+    a = np.asarray(Wt_new, dtype=np.float64)
+    b = np.asarray(Wt_old, dtype=np.float64)
+    if a.shape != b.shape:
+        raise OracleError("ZTP_ESHAPE", "weights differ in shape")
+    return np.abs(a - b).sum(axis=1) / a.shape[1]
+
+
+def priority_update(delta_prev, Wt_new, Wt_old, P_prev=None):
+    """Alg.1 l.4-8 with the incremental rule of P:190: every column's delta is
+    recomputed except the columns pruned in the previous epoch, which keep their
+    old value (their zero-imputed gradients would otherwise pin them as
+    'small variation' forever -- the endless loop of P:190; A-1: 'index not in
+    pri_list' = pruned).  P_prev None = first epoch (all recomputed)."""
+    d = column_delta(Wt_new, Wt_old)
+    if P_prev is not None and len(P_prev):
+        P = np.asarray(P_prev, dtype=np.int64)
+        d[P] = np.asarray(delta_prev, dtype=np.float64)[P]
+    return d
+
+
+def pridiff_gamma(delta, theta: float, gamma_t: float, alpha: float = 0.8) -> float:
+    """Alg.1 l.9-11 (Differentiated Pruning Ratios): L_uni = #{i:
+    delta_i > theta}; gamma_k = 1 - L_uni / L_k; de facto max(gamma_k,
+    alpha * gamma_t).  theta = N_iter * theta_iter (theta_iter = 1e-3)."""
+    d = np.asarray(delta, dtype=np.float64)
+    L = d.shape[0]
+    if L == 0:
+        raise OracleError("ZTP_EINVAL", "empty segment")
+    L_uni = int(np.count_nonzero(d > theta))
+    return max(1.0 - L_uni / L, alpha * gamma_t)
+
+
+# ----------------------------------------------------------------------------
 # a4-a6. One resized linear: dual pruning + imputation (P:142-156, Fig. 2)
 # ----------------------------------------------------------------------------
 

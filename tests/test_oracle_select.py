@@ -56,3 +56,57 @@ def test_nan_rejected():
     with pytest.raises(O.OracleError) as ei:
         O.select(np.array([1.0, np.nan], dtype=np.float32), 1)
     assert ei.value.code == "ZTP_EINVAL"
+
+
+# ------------------------------------------------ NEXT-1 priority maintenance
+
+def test_column_delta_worked_example():
+    """S:87 / Alg.1 l.4: paper-view weights [R, L]; our Wt is the transpose."""
+    g = golden("column_delta.json")
+    Wo = np.array(g["w_old"], dtype=np.float64).T
+    Wn = np.array(g["w_new"], dtype=np.float64).T
+    assert O.column_delta(Wn, Wo).tolist() == g["delta"]
+
+
+def test_column_delta_constant_shift_closed_form():
+    rng = np.random.default_rng(3)
+    W = rng.standard_normal((37, 19))
+    for c in (0.25, -3.0, 0.0):
+        d = O.column_delta(W + c, W)
+        assert np.allclose(d, abs(c), rtol=0, atol=1e-15)
+    # rows changed in a single element j: delta = |dw| / R exactly
+    W2 = W.copy()
+    W2[5, 7] += 0.5
+    d = O.column_delta(W2, W)
+    assert d[5] == pytest.approx(0.5 / 19, abs=1e-15) and np.count_nonzero(d) == 1
+
+
+def test_priority_update_carries_pruned_columns():
+    """P:190: pruned columns keep their old variation (no endless loop);
+    every other column is recomputed."""
+    rng = np.random.default_rng(4)
+    K, n = 50, 23
+    W0 = rng.standard_normal((K, n))
+    d0 = rng.random(K)
+    S, P = O.select(d0.astype(np.float32), 20)
+    W1 = W0 + 0.01 * rng.standard_normal((K, n))
+    W1[P] = W0[P]                       # pruned rows: zero-imputed grads -> unchanged
+    d1 = O.priority_update(d0, W1, W0, P)
+    assert np.array_equal(d1[P], d0[P])                           # carried over, bit-exact
+    assert np.allclose(d1[S], O.column_delta(W1, W0)[S], rtol=0, atol=0)
+    # without carry-over the pruned columns would collapse to 0 (the loop)
+    assert np.all(O.priority_update(d0, W1, W0, None)[P] == 0.0)
+    # first epoch: everything recomputed
+    assert np.array_equal(O.priority_update(d0, W1, W0, None), O.column_delta(W1, W0))
+
+
+def test_pridiff_gamma_rules():
+    """Alg.1 l.9-11: gamma_k = 1 - #{delta > theta}/L, floored at alpha*gamma."""
+    d = np.array([0.5, 0.001, 0.002, 0.3, 0.0, 0.001])
+    theta = 0.001                        # strict '>' : 0.001 is not above
+    assert O.pridiff_gamma(d, theta, 0.0) == pytest.approx(1 - 3 / 6)
+    assert O.pridiff_gamma(d, theta, 0.9) == pytest.approx(0.8 * 0.9)   # alpha floor wins
+    assert O.pridiff_gamma(np.full(8, 1.0), theta, 0.5) == pytest.approx(0.4)
+    assert O.pridiff_gamma(np.zeros(8), theta, 0.5) == 1.0
+    with pytest.raises(O.OracleError):
+        O.pridiff_gamma(np.zeros(0), theta, 0.5)
