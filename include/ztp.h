@@ -301,6 +301,23 @@ typedef struct ztp_linear_args {
   const ztp_mat* hist_dw;      /* Same imputation history for dw_t (or NULL) */
 } ztp_linear_args;
 
+/* ---------------------------------------------------------------------------
+ * NEXT-1 priority-score maintenance (Alg.1 l.4-11), once per epoch.
+ * ztp_priority_update: for every row i of w_t [K, n] (the paper's weight
+ * column i): delta[i] = sum_j |w_t[i,j] - w_old_t[i,j]| / n  (Alg.1 l.4; fp32,
+ * fixed summation order -> deterministic), EXCEPT rows pruned in the previous
+ * selection (pos_prev[i] < 0, the `pos` output of ztp_select), which keep
+ * their delta (incremental update).  pos_prev NULL = first epoch.
+ * If count_above != NULL, *count_above += #{i : delta[i] > theta} (L_uni,
+ * Alg.1 l.9; device int32, exact).  delta [K] fp32 device, in/out; it is the
+ * score array ztp_select consumes.  w_t, w_old_t bf16, same shape.
+ * Errors: EINVAL (null), ESHAPE (shape / dtype mismatch), ECUDA.
+ * ztp_pridiff_gamma (host): Alg.1 l.10-11, gamma_k = max(1 - L_uni / L,
+ * alpha * gamma_t) (alpha = 0.8 in the paper). */
+ztp_status ztp_priority_update(ztp_ctx* ctx, const ztp_mat* w_t, const ztp_mat* w_old_t, const int32_t* pos_prev,
+                               float* delta, int32_t* count_above, float theta, void* stream);
+double ztp_pridiff_gamma(int64_t L, int64_t L_uni, double gamma_t, double alpha);
+
 /* a4, batched: the compact operand copies of several linears in ONE launch
  * (fewer kernel boundaries than one gather per linear).  For args[i] with a
  * lineage entry: what[i] bit 0 -> xs_t <- rows S of x_t (not with x_compact),

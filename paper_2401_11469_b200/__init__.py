@@ -177,6 +177,21 @@ def ztp_row_linear(ctx, phase: int, args: LinearArgs, stream=None) -> None:
     check(lib.ztp_row_linear(ctx, phase, C.byref(args), _stream(stream)), ctx)
 
 
+def ztp_priority_update(ctx, w_t, w_old_t, delta, pos_prev=None, count_above=None, theta: float = 0.0,
+                        stream=None) -> None:
+    """NEXT-1 (Alg.1 l.4-9): delta <- column variation of W^T rows, rows pruned
+    last epoch (pos_prev < 0) carried over; count_above += #{delta > theta}."""
+    wm, om = mat(w_t), mat(w_old_t)
+    check(lib.ztp_priority_update(ctx, C.byref(wm), C.byref(om),
+                                  pos_prev.data_ptr() if pos_prev is not None else None, delta.data_ptr(),
+                                  count_above.data_ptr() if count_above is not None else None, float(theta),
+                                  _stream(stream)), ctx)
+
+
+def ztp_pridiff_gamma(L: int, L_uni: int, gamma_t: float, alpha: float = 0.8) -> float:
+    return float(lib.ztp_pridiff_gamma(L, L_uni, gamma_t, alpha))
+
+
 def ztp_prepare(ctx, items, stream=None) -> None:
     """items: [(LinearArgs, what_bits)] -> one batched compaction launch."""
     n = len(items)

@@ -841,6 +841,28 @@ ztp_status ztp_select(ztp_ctx* c, int nseg, const int32_t* h_len, const int32_t*
   return ZTP_OK;
 }
 
+ztp_status ztp_priority_update(ztp_ctx* c, const ztp_mat* w, const ztp_mat* wo, const int32_t* pos_prev, float* delta,
+                               int32_t* count_above, float theta, void* stream) {
+  if (!c || !w || !wo || !delta) return fail(c, ZTP_EINVAL, "ztp_priority_update: null argument");
+  if (!mat_ok(*w) || !mat_ok(*wo) || w->rows != wo->rows || w->cols != wo->cols || w->dtype != ZTP_BF16 ||
+      wo->dtype != ZTP_BF16)
+    return fail(c, ZTP_ESHAPE, "ztp_priority_update: " + shp("w_t", *w) + " vs " + shp("w_old_t", *wo) + " (bf16)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
+  CUDA_TRY(c, ztp::priority_update_launch(w->ptr, w->ld, wo->ptr, wo->ld, w->rows, w->cols, pos_prev, delta,
+                                          count_above, theta, st));
+  prof_end(c, pe, st);
+  ++c->launches;
+  return ZTP_OK;
+}
+
+double ztp_pridiff_gamma(int64_t L, int64_t L_uni, double gamma_t, double alpha) {
+  if (L <= 0) return 0.0;
+  const double g = 1.0 - (double)L_uni / (double)L;
+  const double f = alpha * gamma_t;
+  return g > f ? g : f;
+}
+
 ztp_status ztp_prepare(ztp_ctx* c, int n, const ztp_linear_args* const* args, const int32_t* what, void* stream) {
   if (!c || n < 0 || (n > 0 && (!args || !what))) return fail(c, ZTP_EINVAL, "ztp_prepare: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;

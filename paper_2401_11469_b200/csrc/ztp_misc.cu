@@ -372,6 +372,60 @@ cudaError_t impute_rows_launch(void* out, int64_t ld, int64_t cols, const int32_
                   ld_hist);
 }
 
+// ------------------------------------------- NEXT-1 priority maintenance
+// One warp per row i of W^T: lanes stride the row in 8-element (16-byte)
+// chunks, fp32 partial sums of |w - w_old| reduced by a fixed shuffle tree
+// (deterministic), divided by n.  Rows pruned last epoch keep delta.
+__global__ void ztp_priority_update_kernel(const uint16_t* __restrict__ w, int64_t ld_w,
+                                           const uint16_t* __restrict__ wo, int64_t ld_o, int64_t K, int64_t n,
+                                           const int32_t* __restrict__ pos_prev, float* delta, int32_t* count_above,
+                                           float theta) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < K; i += warps) {
+    float d;
+    if (pos_prev && __ldg(pos_prev + i) < 0) {
+      d = delta[i];                               // pruned last epoch: carried over
+    } else {
+      const uint16_t* a = w + i * ld_w;
+      const uint16_t* b = wo + i * ld_o;
+      float acc = 0.f;
+      for (int64_t c = (int64_t)lane * 8; c < n; c += 256) {
+        if (c + 8 <= n) {
+          const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + c));
+          const uint4 y = __ldg(reinterpret_cast<const uint4*>(b + c));
+          const uint32_t xa[4] = {x.x, x.y, x.z, x.w}, ya[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            acc += fabsf(__uint_as_float(xa[q] << 16) - __uint_as_float(ya[q] << 16));
+            acc += fabsf(__uint_as_float(xa[q] & 0xFFFF0000u) - __uint_as_float(ya[q] & 0xFFFF0000u));
+          }
+        } else {
+          for (int64_t e = c; e < n; ++e)
+            acc += fabsf(__uint_as_float((uint32_t)a[e] << 16) - __uint_as_float((uint32_t)b[e] << 16));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xFFFFFFFFu, acc, o);
+      d = __shfl_sync(0xFFFFFFFFu, acc, 0) / (float)n;
+      if (lane == 0) delta[i] = d;
+    }
+    if (count_above && lane == 0 && d > theta) atomicAdd(count_above, 1);
+  }
+}
+
+cudaError_t priority_update_launch(const void* w, int64_t ld_w, const void* w_old, int64_t ld_old, int64_t K,
+                                   int64_t n, const int32_t* pos_prev, float* delta, int32_t* count_above,
+                                   float theta, cudaStream_t st) {
+  if (K <= 0) return cudaSuccess;
+  int blocks = (int)((K + 7) / 8);                   // 8 warps per block, one row each
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  return launch_k(ztp_priority_update_kernel, blocks, 256, 0, st, (const uint16_t*)w, ld_w, (const uint16_t*)w_old,
+                  ld_old, K, n, pos_prev, delta, count_above, theta);
+}
+
 // ------------------------------------------------------------- row fill (Zero)
 __global__ void ztp_fill_rows(uint8_t* out, int64_t ld_bytes, const int32_t* rows, int nrows, int64_t row_bytes) {
   pdl_wait();

@@ -187,6 +187,43 @@ class ZtpLayer:
             qo += self.seg_len[s] + self.append[s]
         self._build_args()
 
+    def weight_rows(self) -> Dict[str, torch.Tensor]:
+        """W^T of each segment restricted to the rows the segment selects over
+        (own units only for FC2)."""
+        own = self.u - self.mig.n_mig
+        return {"qkv": self.qkv_t, "o": self.o_t, "fc1": self.w1_t[:, :self.u], "fc2": self.w2_t[:own]}
+
+    def priority_epoch(self, w_prev: Dict[str, torch.Tensor], gamma_t: float, theta: float,
+                       alpha: float = 0.8, stream=None) -> Dict[str, int]:
+        """NEXT-1, once per epoch (Alg.1 l.3-14): per segment, the column
+        variation of W^T against the previous epoch's weights (pruned rows keep
+        their score), the PriDiff ratio max(1 - L_uni/L, alpha gamma_t)
+        (l.9-11) and the new selection on the maintained scores (l.12-14).
+        Returns the per-segment prune counts."""
+        cur = self.weight_rows()
+        lens = {s: self.seg_len[s] for s in SEGS}
+        offs, o = {}, 0
+        for s in SEGS:
+            offs[s] = o
+            o += lens[s]
+        cnt = torch.zeros(len(SEGS), dtype=torch.int32, device="cuda")
+        first = not getattr(self, "_prio_init", False)
+        for i, s in enumerate(SEGS):
+            delta = self._scores[offs[s]:offs[s] + lens[s]]
+            pos = None if first else self.POS[s][:lens[s]]
+            Z.ztp_priority_update(self.ctx, cur[s], w_prev[s], delta, pos_prev=pos, count_above=cnt[i:i + 1],
+                                  theta=theta, stream=stream)
+        self._prio_init = True
+        l_uni = cnt.cpu().tolist()                 # epoch boundary: one host sync
+        n_prune = {}
+        for i, s in enumerate(SEGS):
+            L = lens[s]
+            g = min(Z.ztp_pridiff_gamma(L, l_uni[i], gamma_t, alpha), 0.9)        # A-4 clamp
+            n_prune[s] = min(int(g * L + 0.5), L - 1)                              # A-3 rounding
+        scores = {s: self._scores[offs[s]:offs[s] + lens[s]].clone() for s in SEGS}
+        self.set_selection(n_prune, scores, stream)
+        return n_prune
+
     def run_select(self, stream=None):
         lens, nps, apps = self._sel_args
         Z.ztp_select(self.ctx, lens, nps, self._scores, self.kept, self.pruned, apps, self.pos, stream)

@@ -158,3 +158,19 @@ def test_no_cuda_device_is_an_error_not_a_fallback(Z):
     with pytest.raises(Z.ZtpError) as ei:
         Z.ztp_ctx_create()
     assert ei.value.name in ("ZTP_ECUDA", "ZTP_EUNSUPPORTED")
+
+
+def test_pridiff_gamma_matches_oracle():
+    """Alg.1 l.10-11 host function, bit-exact vs the oracle's rule."""
+    import numpy as np
+    from oracle import ztp_oracle as O
+    import paper_2401_11469_b200 as Z
+    rng = np.random.default_rng(9)
+    for _ in range(300):
+        L = int(rng.integers(1, 5000))
+        d = rng.random(L) * 0.01
+        theta = float(rng.choice([0.001, 0.005, 0.0]))
+        g = float(rng.random() * 0.9)
+        a = float(rng.choice([0.8, 1.0, 0.5]))
+        L_uni = int(np.count_nonzero(d > theta))
+        assert Z.ztp_pridiff_gamma(L, L_uni, g, a) == O.pridiff_gamma(d, theta, g, a)

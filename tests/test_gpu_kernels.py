@@ -411,3 +411,42 @@ def test_bwd_imputation_average_same(env, policy, layer, dtype):
         with pytest.raises(Z.ZtpError) as ei:
             lin(ctx, Z.BWD, b)
         assert ei.value.name == "ZTP_EHISTORY"
+
+
+@pytest.mark.parametrize("K,n", [(1024, 4096), (300, 523), (17, 8)])
+def test_priority_update_next1(env, K, n):
+    """NEXT-1 (Alg.1 l.4-9): GPU column deltas vs the oracle (fp32 sum
+    of bf16 differences, 1e-4 relative: n * 2^-24 bound), pruned rows carried over bit-exactly,
+    L_uni exact for the GPU's deltas, and the next selection on them equals the
+    oracle's select on the same scores (bit-exact)."""
+    Z, torch, ctx = env
+    W0 = I.uniform_sym(71, "w0", K, n, 0.05)
+    W1 = W0 + I.normal(71, "dw", K, n) * 1e-3
+    W1 = I.round_bf16(W1)
+    d_prev = I.lognormal_scores(71, "d0", K)
+    S, P = O.select(d_prev, K // 3)
+    pos = np.full(K, 0, dtype=np.int32)
+    pos[np.asarray(P, dtype=np.int64)] = -1
+    w1, w0 = dev(torch, W1), dev(torch, W0)
+    delta = torch.tensor(d_prev, device="cuda", dtype=torch.float32)
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    theta = 1e-3
+    Z.ztp_priority_update(ctx, w1, w0, delta, pos_prev=torch.tensor(pos, device="cuda"), count_above=cnt,
+                          theta=theta)
+    Z.ztp_sync(ctx)
+    got = delta.cpu().numpy()
+    ref = O.priority_update(d_prev.astype(np.float64), host(w1), host(w0), P)
+    Pa = np.asarray(P, dtype=np.int64)
+    assert np.array_equal(got[Pa], d_prev[Pa])                     # carried over
+    assert np.allclose(got, ref, rtol=1e-4, atol=1e-12)
+    assert int(cnt.item()) == int(np.count_nonzero(got > np.float32(theta)))
+    # the epoch's selection on the maintained scores: GPU select == oracle select
+    npr = int(math.floor(K * O.pridiff_gamma(got, theta, 0.5) + 0.5))
+    npr = min(npr, K - 1)
+    kept = torch.empty(K, dtype=torch.int32, device="cuda")
+    pr = torch.empty(max(1, npr), dtype=torch.int32, device="cuda")
+    Z.ztp_select(ctx, [K], [npr], delta, kept, pr)
+    Z.ztp_sync(ctx)
+    S2, P2 = O.select(got, npr)
+    assert np.array_equal(kept.cpu().numpy()[:K - npr], S2)
+    assert np.array_equal(pr.cpu().numpy()[:npr], P2)

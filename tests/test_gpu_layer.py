@@ -229,3 +229,44 @@ def test_layer_tp4_migration_receiver_resizes(tz):
     g[1] = dict(qkv=0.25, o=0.25, fc1=0.4, fc2=0.25)
     mig = [(0, 1, u - 40, u - 16), (0, 2, u - 16, u - 8), (0, 3, u - 8, u)]
     _simulate(tz, e, h, f, 136, g, mig)
+
+
+def test_layer_priority_epoch_next1(tz):
+    """NEXT-1 at the layer level: two epochs of ZtpLayer.priority_epoch (column
+    variation with carry-over, PriDiff ratio, selection) give the oracle's
+    scores (1e-4), counts and index sets (bit-exact)."""
+    torch, Z, ZtpLayer, _ = tz
+    h, f, N = 128, 512, 264
+    seed = 301
+    X, G, sh = make_inputs(h, f, N, 1, seed)
+    ctx, L = build(tz, sh, 0, 1, h, f, N)
+    lens = {"qkv": h, "o": h, "fc1": h, "fc2": f}
+    sc0 = {s: I.lognormal_scores(seed, f"score.{s}", n) for s, n in lens.items()}
+    L.set_selection({s: 0 for s in lens}, {s: torch.from_numpy(v).cuda() for s, v in sc0.items()})
+    ref_delta = {s: sc0[s].astype(np.float64) for s in lens}
+    P_prev = {s: None for s in lens}
+    theta, gamma_t = 2e-4, 0.4
+    for epoch in range(2):
+        prev = {s: t.clone() for s, t in L.weight_rows().items()}
+        prev_h = {s: host(t) for s, t in prev.items()}
+        # "training": perturb the weights; rows pruned last epoch stay unchanged
+        for s, t in L.weight_rows().items():
+            upd = to_dev(torch, I.normal(seed + epoch, f"upd.{s}", t.shape[0], t.shape[1]) * 1e-3 *
+                         (1 + np.arange(t.shape[0])[:, None] % 7))
+            if P_prev[s] is not None and len(P_prev[s]):
+                upd[torch.tensor(P_prev[s], device="cuda")] = 0
+            t.add_(upd)
+        nps = L.priority_epoch(prev, gamma_t, theta)
+        torch.cuda.synchronize()
+        for s in lens:
+            cur_h = host(L.weight_rows()[s])
+            d = O.priority_update(ref_delta[s], cur_h, prev_h[s], P_prev[s])
+            got = L._scores[sum(lens[t] for t in list(lens)[:list(lens).index(s)]):][:lens[s]].cpu().numpy()
+            assert np.allclose(got, d, rtol=1e-4, atol=1e-12), s
+            g = min(O.pridiff_gamma(got, theta, gamma_t), 0.9)
+            npr = min(int(g * lens[s] + 0.5), lens[s] - 1)
+            assert nps[s] == npr, s
+            S, P = O.select(got, npr)
+            assert np.array_equal(L.S[s].cpu().numpy(), S) and np.array_equal(L.P[s][:npr].cpu().numpy(), P), s
+            ref_delta[s], P_prev[s] = got.astype(np.float64), P
+    Z.ztp_ctx_destroy(ctx)
