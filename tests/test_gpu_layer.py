@@ -134,8 +134,10 @@ def test_layer_cuda_graph_replay(tz):
     Z.ztp_ctx_destroy(ctx)
 
 
-def _simulate(tz, e, h, f, N, gam, mig=None, seed=7):
-    """e ranks on one GPU; the test sums partials where NCCL all-reduces."""
+def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None):
+    """e ranks on one GPU; the test sums partials where NCCL all-reduces.
+    sampled = k: full-size run checked on k token columns (Y, dX) against the
+    oracle computed for those columns only (layer_step_sampled)."""
     torch, Z, ZtpLayer, MigrationIO = tz
     u = f // e
     X, G, sh = make_inputs(h, f, N, e, seed)
@@ -146,7 +148,11 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7):
         own[s] = min(own[s], lo)
         inc[r].append((s, lo, hi))
     sel, scores, nps = selections(e, h, f, N, seed, gam, own_fc2=own)
-    ref = O.layer_step(X, G, sh, sel, mig)
+    if sampled:
+        cols = np.unique(np.concatenate([np.linspace(0, N - 1, sampled).astype(np.int64), [N - 1]]))
+        ref = O.layer_step_sampled(X, G, sh, sel, cols, mig)
+    else:
+        ref = O.layer_step(X, G, sh, sel, mig)
     cap = max([sum(hi - lo for (_, lo, hi) in inc[r]) for r in range(e)] + [0])
     ranks = [build(tz, sh, r, e, h, f, N, cap) for r in range(e)]
     offs = {}
@@ -189,6 +195,20 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7):
         Ls.dw2[lo:hi].copy_(Lr.dw2[o:o + hi - lo])
     torch.cuda.synchronize()
     L0 = ranks[0][1]
+    if sampled:
+        ct = torch.tensor(cols, device="cuda")
+        close(host(L0.Y[:, ct]), ref["Y"], "Y (sampled)")
+        close(host(L0.dX[:, ct]), ref["dX"], "dX (sampled)")
+        for r, (ctx, L) in enumerate(ranks):
+            # Zero imputation of the straggler's dW rows, exact -- on its own
+            # units (migrated units' dW comes back from helpers that contract
+            # over their own kept rows, A-33)
+            for seg, t in (("qkv", L.dqkv), ("o", L.do), ("fc1", L.dw1[:, :own[r]]), ("fc2", L.dw2)):
+                P = sel[r][seg][1]
+                if len(P):
+                    assert torch.all(t[torch.tensor(P, device="cuda")] == 0), (r, seg)
+            Z.ztp_ctx_destroy(ctx)
+        return
     close(host(L0.Y), ref["Y"], "Y")
     close(host(L0.dX), ref["dX"], "dX")
     for r, (ctx, L) in enumerate(ranks):
@@ -270,3 +290,55 @@ def test_layer_priority_epoch_next1(tz):
             assert np.array_equal(L.S[s].cpu().numpy(), S) and np.array_equal(L.P[s][:npr].cpu().numpy(), P), s
             ref_delta[s], P_prev[s] = got.astype(np.float64), P
     Z.ztp_ctx_destroy(ctx)
+
+
+# ---------------------------------------------- BASELINE.json configs, full size
+
+def _tail(u, n_mig, s, e):
+    """SEMI ranges of straggler s: tail [u - n_mig, u) split over the other
+    ranks in r' = (r - s + e) % e order, remainder to the lowest r' (A-28)."""
+    recv = sorted((r for r in range(e) if r != s), key=lambda r: (r - s + e) % e)
+    m, rem = divmod(n_mig, len(recv))
+    out, lo = [], u - n_mig
+    for i, r in enumerate(recv):
+        k = m + (1 if i < rem else 0)
+        if k:
+            out.append((s, r, lo, lo + k))
+        lo += k
+    return out
+
+
+def _zeros(e):
+    return [dict(qkv=0.0, o=0.0, fc1=0.0, fc2=0.0) for _ in range(e)]
+
+
+def test_config_c2_full_size_sampled(tz):
+    """c2 (GPT-2 medium, N = 8192) at TP = 1, gamma = 0.5 on every linear --
+    the bench workload -- Y and dX checked on sampled token columns."""
+    _simulate(tz, 1, 1024, 4096, 8192, [dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)], seed=241, sampled=24)
+
+
+def test_config_c3_full_size_sampled(tz):
+    """c3 (ViT-L, 197 x 64 = 12608 tokens) at TP = 4, rank 3 resized at 0.5."""
+    g = _zeros(4)
+    g[3] = dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)
+    _simulate(tz, 4, 1024, 4096, 12608, g, seed=242, sampled=16)
+
+
+def test_config_c4_full_size_semi_sampled(tz):
+    """c4 (Llama-2-7B-shaped, h = 4096, f = 11008, N = 2048) at TP = 8, rank 5
+    a 3x straggler: SEMI with beta = 0.25 -> 229 of its 1376 units migrate to
+    the 7 helpers (33,33,33,33,33,32,32 in r' order) and the rest resizes at
+    gamma_r = 0.6."""
+    e, f = 8, 11008
+    g = _zeros(e)
+    g[5] = dict(qkv=0.6, o=0.6, fc1=0.6, fc2=0.6)
+    _simulate(tz, e, 4096, f, 2048, g, mig=_tail(f // e, 229, 5, e), seed=243, sampled=12)
+
+
+def test_config_c5_layer_full_size_sampled(tz):
+    """c5 (GPT-13B-shaped layer, h = 5120, f = 20480, N = 2048) at TP = 8,
+    rank 0 resized at 0.5 (one layer of the 4-layer stack)."""
+    g = _zeros(8)
+    g[0] = dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)
+    _simulate(tz, 8, 5120, 20480, 2048, g, seed=244, sampled=8)
