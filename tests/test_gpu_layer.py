@@ -342,3 +342,12 @@ def test_config_c5_layer_full_size_sampled(tz):
     g = _zeros(8)
     g[0] = dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)
     _simulate(tz, 8, 5120, 20480, 2048, g, seed=244, sampled=8)
+
+
+def test_config_c1_exact_shape(tz):
+    """c1 (single FFN-block config of BASELINE.json: h = 64, f = 256, seq 16 x
+    batch 2 -> N = 32) at TP = 2, rank 1 slowed 2x -> T_avg ratio 0.25 on every
+    linear (the config's stated ratio, S:363 closed form), full comparison."""
+    g = _zeros(2)
+    g[1] = dict(qkv=0.25, o=0.25, fc1=0.25, fc2=0.25)
+    _simulate(tz, 2, 64, 256, 32, g, seed=240)
