@@ -50,6 +50,140 @@ __device__ __forceinline__ int block_excl_scan(bool flag, int& total, int* warp_
   return r;
 }
 
+// Block-wide exclusive scan of an int (blockDim = 1024): two barriers.
+__device__ __forceinline__ int block_excl_scan_int(int v, int& total, int* warp_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int x = warp_tot[lane];
+    int wi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    warp_tot[32 + lane] = wi - x;
+    if (lane == 31) warp_tot[64] = wi;
+  }
+  __syncthreads();
+  total = warp_tot[64];
+  return warp_tot[32 + w] + incl - v;
+}
+
+// Segments of up to 1024 * E columns: thread t holds keys [t E, t E + E) in
+// registers; 4 radix passes with warp-aggregated histograms, then ONE scan of
+// the per-thread tie counts and ONE of the per-thread prune counts give every
+// element its place (instead of two block scans per 1024 elements).  Same
+// result as the general path: prune (score asc, index asc), S and P ascending.
+template <int E>
+__device__ __forceinline__ void select_regs(const SelectSeg& s, const float* __restrict__ sc, int32_t* K, int32_t* P,
+                                            int32_t* Q, int32_t* err_flag, uint32_t* hist, int* warp_tot,
+                                            uint32_t* sel) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int i0 = tid * E;
+  uint32_t key[E];
+  bool saw_nan = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    bool nan = false;
+    key[e] = (i0 + e < s.len) ? ord32(__ldg(sc + i0 + e), nan) : 0u;
+    saw_nan |= nan;
+  }
+  if (saw_nan) atomicOr(err_flag, 1);
+  uint32_t prefix = 0, mask = 0;
+  int target = s.n_prune - 1;
+  if (s.n_prune > 0) {
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      if (tid < 256) hist[tid] = 0;
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const bool hit = i0 + e < s.len && (key[e] & mask) == prefix;
+        const uint32_t bin = hit ? (key[e] >> shift) & 255u : 256u;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+        if (hit && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+      }
+      __syncthreads();
+      if (tid < 32) {
+        uint32_t loc[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          loc[j] = hist[8 * lane + j];
+          sum += loc[j];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t excl = incl - sum;
+        if ((uint32_t)target >= excl && (uint32_t)target < incl) {
+          uint32_t c = excl;
+          for (int j = 0; j < 8; ++j) {
+            if ((uint32_t)target < c + loc[j]) {
+              sel[0] = 8 * lane + j;
+              sel[1] = c;
+              break;
+            }
+            c += loc[j];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= sel[0] << shift;
+      mask |= 0xFFu << shift;
+      target -= (int)sel[1];
+    }
+  }
+  const uint32_t v = prefix;
+  const int t_need = target + 1;
+  const bool any = s.n_prune > 0;
+  int c_tie = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) c_tie += (any && i0 + e < s.len && key[e] == v) ? 1 : 0;
+  int tot;
+  int tr = block_excl_scan_int(c_tie, tot, warp_tot);
+  bool isp[E];
+  int c_p = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const bool valid = i0 + e < s.len;
+    const bool tie = any && valid && key[e] == v;
+    isp[e] = any && valid && (key[e] < v || (tie && tr < t_need));
+    tr += tie ? 1 : 0;
+    c_p += isp[e] ? 1 : 0;
+  }
+  int pr = block_excl_scan_int(c_p, tot, warp_tot);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = i0 + e;
+    if (i < s.len) {
+      if (isp[e]) {
+        P[pr] = i;
+        if (Q) Q[i] = -1;
+        ++pr;
+      } else {
+        K[i - pr] = i;
+        if (Q) Q[i] = i - pr;
+      }
+    }
+  }
+  const int nk = s.len - s.n_prune;
+  for (int a = tid; a < s.append; a += blockDim.x) {
+    K[nk + a] = s.len + a;
+    if (Q) Q[s.len + a] = nk + a;
+  }
+}
+
 __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, const float* __restrict__ scores,
                                                           int32_t* __restrict__ kept, int32_t* __restrict__ pruned,
                                                           int32_t* __restrict__ pos, int32_t* err_flag) {
@@ -57,6 +191,23 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
   pdl_trigger();
   const SelectSeg s = p.seg[blockIdx.x];
   const float* sc = scores + s.score_off;
+  if (s.len <= 8 * 1024) {
+    __shared__ uint32_t rhist[256];
+    __shared__ int rwarp[65];
+    __shared__ uint32_t rsel[2];
+    int32_t* Kr = kept + s.kept_off;
+    int32_t* Pr = pruned + s.pruned_off;
+    int32_t* Qr = pos ? pos + s.pos_off : nullptr;
+    if (s.len <= 1024)
+      select_regs<1>(s, sc, Kr, Pr, Qr, err_flag, rhist, rwarp, rsel);
+    else if (s.len <= 2048)
+      select_regs<2>(s, sc, Kr, Pr, Qr, err_flag, rhist, rwarp, rsel);
+    else if (s.len <= 4096)
+      select_regs<4>(s, sc, Kr, Pr, Qr, err_flag, rhist, rwarp, rsel);
+    else
+      select_regs<8>(s, sc, Kr, Pr, Qr, err_flag, rhist, rwarp, rsel);
+    return;
+  }
   // keys staged in shared memory once when the segment fits (every pass and
   // the compaction then read smem instead of re-reading L2)
   extern __shared__ uint32_t skey[];
@@ -187,7 +338,7 @@ cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* k
   int maxlen = 0;
   for (int i = 0; i < p.nseg; ++i) maxlen = p.seg[i].len > maxlen ? p.seg[i].len : maxlen;
   // stage keys in smem up to 48K keys (192 KB); longer segments re-read L2
-  q.smem_keys = maxlen <= SELECT_SMEM_KEYS ? maxlen : 0;
+  q.smem_keys = (maxlen > 8 * 1024 && maxlen <= SELECT_SMEM_KEYS) ? maxlen : 0;   // <= 8K: register path
   const int smem = q.smem_keys * 4;
   if (smem > 48 * 1024 && smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(ztp_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -30,12 +30,12 @@ def cases():
         a = Z.linear_args(x_t=x, w_t=w, y_t=y, pre_t=pre if gelu else None, act=Z.ACT_GELU if gelu else Z.ACT_NONE)
         out[name] = (Z.KIND_FWD, a, (w, x, y, pre))
     # DX dx[K, N] = W^T[K, n] G^T[n, N]
-    for name, K, n, gg in (("fc2_dx_gelugrad", 2048, 1024, True), ("fc2_dx_plain", 2048, 1024, False),
-                           ("fc1_dx", 512, 2048, False)):
+    for name, K, n, gg in (("fc2_dx_gelugrad", 2048, 1024, 1), ("fc2_dx_mul", 2048, 1024, 2),
+                           ("fc2_dx_plain", 2048, 1024, 0), ("fc1_dx", 512, 2048, 0)):
         w, g = r(K, n), r(n, N)
         dx, pin = torch.empty(K, N, device="cuda", dtype=bf), r(K, N)
         a = Z.linear_args(w_t=w, g_t=g, dx_t=dx, pre_in_t=pin if gg else None,
-                          act_in=Z.ACT_GELU if gg else Z.ACT_NONE)
+                          act_in=[Z.ACT_NONE, Z.ACT_GELU, Z.ACT_GELU_D][gg])
         out[name] = (Z.KIND_DX, a, (w, g, dx, pin))
     # DW dw[K, n] = X^T[K, N] G^T[n, N]^T
     for name, K, n in (("fc2_dw", 2048, 1024), ("fc1_dw", 512, 2048), ("o_dw", 512, 1024), ("qkv_dw", 512, 3072)):
