@@ -334,9 +334,14 @@ ztp_status ztp_row_linear(ztp_ctx* ctx, ztp_phase phase, const ztp_linear_args* 
  * q[f,t] + k[f,t] + v[f,t] with qkv_t = [Q; K; V] row blocks of `feat` rows
  * (the first n_feat of each block); BWD g_qkv_t = [dctx; dctx; dctx].
  * FWD with rows != NULL writes only features rows[0..n_rows) as compact rows
- * 0..n_rows-1 of ctx_t (the O projection's kept rows S, producer-side). */
+ * 0..n_rows-1 of ctx_t (the O projection's kept rows S, producer-side).
+ * v_compact (A-36, output pruning of V): the V block of qkv_t holds only the
+ * features rows[0..n_rows), compact (V row i <- feature rows[i]); FWD reads
+ * it so, BWD writes dV compact (dQ, dK stay full).  qkv_t then has
+ * 2 feat + n_rows rows. */
 ztp_status ztp_core(ztp_ctx* ctx, ztp_phase phase, const ztp_mat* qkv_t, const ztp_mat* ctx_t,
-                    int64_t feat, int64_t n_feat, const int32_t* rows, int64_t n_rows, void* stream);
+                    int64_t feat, int64_t n_feat, const int32_t* rows, int64_t n_rows, int32_t v_compact,
+                    void* stream);
 
 /* ---------------------------------------------------------------------------
  * (5) Migration -- peer copies of shard slices (A-26).

@@ -205,10 +205,10 @@ def ztp_gemm(ctx, kind: int, args: LinearArgs, stream=None) -> None:
 
 
 def ztp_core(ctx, phase: int, qkv_t, ctx_t, feat: int, n_feat: int, rows=None, n_rows: int = 0,
-             stream=None) -> None:
+             stream=None, v_compact: bool = False) -> None:
     q, c = mat(qkv_t), mat(ctx_t)
     check(lib.ztp_core(ctx, phase, C.byref(q), C.byref(c), feat, n_feat,
-                       rows.data_ptr() if rows is not None else None, n_rows, _stream(stream)), ctx)
+                       rows.data_ptr() if rows is not None else None, n_rows, int(v_compact), _stream(stream)), ctx)
 
 
 def ztp_migrate(ctx, xfers: Sequence[Xfer], stream=None) -> None:

@@ -118,7 +118,8 @@ def _load():
                             vp, vp, vp, vp, vp]),
         "ztp_col_linear": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
         "ztp_row_linear": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
-        "ztp_core": (st, [vp, C.c_int, C.POINTER(Mat), C.POINTER(Mat), C.c_int64, C.c_int64, vp, C.c_int64, vp]),
+        "ztp_core": (st, [vp, C.c_int, C.POINTER(Mat), C.POINTER(Mat), C.c_int64, C.c_int64, vp, C.c_int64,
+                          C.c_int32, vp]),
         "ztp_migrate": (st, [vp, C.c_int, C.POINTER(Xfer), vp]),
         "ztp_set_slowdown": (st, [vp, C.c_double]),
         "ztp_set_stats": (st, [vp, C.c_int]),

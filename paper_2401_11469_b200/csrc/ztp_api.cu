@@ -961,17 +961,21 @@ ztp_status ztp_gemm(ztp_ctx* c, int kind, const ztp_linear_args* a, void* stream
 }
 
 ztp_status ztp_core(ztp_ctx* c, ztp_phase phase, const ztp_mat* qkv, const ztp_mat* cx, int64_t feat, int64_t n_feat,
-                    const int32_t* rows, int64_t n_rows, void* stream) {
+                    const int32_t* rows, int64_t n_rows, int32_t v_compact, void* stream) {
   if (!c || !qkv || !cx || !mat_ok(*qkv) || !mat_ok(*cx)) return fail(c, ZTP_ESHAPE, "ztp_core: bad matrices");
+  if (v_compact && (!rows || n_rows < 1)) return fail(c, ZTP_EINVAL, "ztp_core: v_compact needs the kept list rows");
   const int64_t n_out = (phase == ZTP_FWD && rows) ? n_rows : n_feat;
-  if (qkv->rows < 3 * feat || n_feat > feat || cx->rows < n_out || cx->cols != qkv->cols || qkv->dtype != cx->dtype ||
+  const int64_t n_v = v_compact ? n_rows : n_feat;
+  const int64_t qkv_rows = v_compact ? 2 * feat + n_v : 3 * feat;
+  if (qkv->rows < qkv_rows || n_feat > feat || cx->rows < n_out || cx->cols != qkv->cols || qkv->dtype != cx->dtype ||
       (rows && (n_rows < 1 || n_rows > n_feat)))
     return fail(c, ZTP_ESHAPE, "ztp_core: " + shp("qkv_t", *qkv) + " " + shp("ctx_t", *cx));
   if (qkv->dtype == ZTP_BF16 && qkv->cols % 8) return fail(c, ZTP_ESHAPE, "ztp_core: N % 8 != 0");
   const int pe = prof_begin(c, (cudaStream_t)stream, PROF_OTHER, 0.0);
   if (!(c->dbg_skip & 4)) {
     CUDA_TRY(c, ztp::core_launch(phase == ZTP_FWD ? 0 : 1, qkv->ptr, qkv->ld, cx->ptr, cx->ld, feat, n_out, qkv->cols,
-                                 qkv->dtype, phase == ZTP_FWD ? rows : nullptr, (cudaStream_t)stream));
+                                 qkv->dtype, (phase == ZTP_FWD || v_compact) ? rows : nullptr, n_v, v_compact ? 1 : 0,
+                                 (cudaStream_t)stream));
   }
   prof_end(c, pe, (cudaStream_t)stream);
   ++c->launches;

@@ -127,7 +127,8 @@ cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* k
 cudaError_t delay_launch(unsigned long long* stamp, double chi, unsigned long long* acc_ns, cudaStream_t st);
 cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st);
 cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int64_t feat,
-                        int64_t n_feat, int64_t N, int dtype, const int32_t* rows, cudaStream_t st);
+                        int64_t n_feat, int64_t N, int dtype, const int32_t* rows, int64_t n_v, int v_compact,
+                        cudaStream_t st);
 cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* idx, int n, int64_t cols, void* dst,
                                int64_t ld_dst, int dtype, cudaStream_t st);
 cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* rows, int n, const int32_t* cols, int nc,

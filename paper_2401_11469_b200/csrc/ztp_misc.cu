@@ -49,20 +49,24 @@ cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st) {
 
 // ------------------------------------------------------ stand-in core (A-31)
 // FWD ctx[f,t] = q[f,t] + k[f,t] + v[f,t]; BWD q = k = v = dctx.  16-byte vectors.
+// v_compact (A-36): the V block holds only the O projection's kept features
+// (V row i <- feature rows[i]), FWD reads it at i, BWD writes dV there.
+// BWD walks the 2 n_feat + n_v output rows once (each written once).
 __global__ void ztp_core_bf16(int phase, const __nv_bfloat16* __restrict__ qkv_c, __nv_bfloat16* qkv, int64_t ld_qkv,
                               __nv_bfloat16* ctx, int64_t ld_ctx, int64_t feat, int64_t n_feat, int64_t N,
-                              const int32_t* __restrict__ rows) {
+                              const int32_t* __restrict__ rows, int64_t n_v, int v_compact) {
   pdl_wait();
   pdl_trigger();
   const int64_t vec_per_row = N / 8;
-  const int64_t total = n_feat * vec_per_row;
+  const int64_t total = (phase == 0 ? n_feat : 2 * n_feat + n_v) * vec_per_row;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = i / vec_per_row, c = (i % vec_per_row) * 8;
     if (phase == 0) {
       const int64_t sf = rows ? (int64_t)__ldg(rows + f) : f;  // compact output row f <- feature sf
+      const int64_t vr = v_compact ? 2 * feat + f : 2 * feat + sf;
       const uint4 a = *reinterpret_cast<const uint4*>(qkv_c + sf * ld_qkv + c);
       const uint4 b = *reinterpret_cast<const uint4*>(qkv_c + (feat + sf) * ld_qkv + c);
-      const uint4 d = *reinterpret_cast<const uint4*>(qkv_c + (2 * feat + sf) * ld_qkv + c);
+      const uint4 d = *reinterpret_cast<const uint4*>(qkv_c + vr * ld_qkv + c);
       const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
       const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
       const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
@@ -75,42 +79,63 @@ __global__ void ztp_core_bf16(int phase, const __nv_bfloat16* __restrict__ qkv_c
       }
       *reinterpret_cast<uint4*>(ctx + f * ld_ctx + c) = o;
     } else {
-      const uint4 g = *reinterpret_cast<const uint4*>(ctx + f * ld_ctx + c);
-      *reinterpret_cast<uint4*>(qkv + f * ld_qkv + c) = g;
-      *reinterpret_cast<uint4*>(qkv + (feat + f) * ld_qkv + c) = g;
-      *reinterpret_cast<uint4*>(qkv + (2 * feat + f) * ld_qkv + c) = g;
+      // output row f of g_qkv: Q rows [0, n_feat), K rows [feat, feat + n_feat), V rows from 2 feat
+      int64_t orow, grow;
+      if (f < n_feat) {
+        orow = f;
+        grow = f;
+      } else if (f < 2 * n_feat) {
+        orow = feat + (f - n_feat);
+        grow = f - n_feat;
+      } else {
+        const int64_t j = f - 2 * n_feat;
+        orow = 2 * feat + j;
+        grow = v_compact ? (int64_t)__ldg(rows + j) : j;
+      }
+      *reinterpret_cast<uint4*>(qkv + orow * ld_qkv + c) = *reinterpret_cast<const uint4*>(ctx + grow * ld_ctx + c);
     }
   }
 }
 
 __global__ void ztp_core_f32(int phase, float* qkv, int64_t ld_qkv, float* ctx, int64_t ld_ctx, int64_t feat,
-                             int64_t n_feat, int64_t N, const int32_t* __restrict__ rows) {
+                             int64_t n_feat, int64_t N, const int32_t* __restrict__ rows, int64_t n_v, int v_compact) {
   pdl_wait();
   pdl_trigger();
-  const int64_t total = n_feat * N;
+  const int64_t total = (phase == 0 ? n_feat : 2 * n_feat + n_v) * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = i / N, c = i % N;
     if (phase == 0) {
       const int64_t sf = rows ? (int64_t)rows[f] : f;
-      ctx[f * ld_ctx + c] = (qkv[sf * ld_qkv + c] + qkv[(feat + sf) * ld_qkv + c]) + qkv[(2 * feat + sf) * ld_qkv + c];
+      const int64_t vr = v_compact ? 2 * feat + f : 2 * feat + sf;
+      ctx[f * ld_ctx + c] = (qkv[sf * ld_qkv + c] + qkv[(feat + sf) * ld_qkv + c]) + qkv[vr * ld_qkv + c];
     } else {
-      const float g = ctx[f * ld_ctx + c];
-      qkv[f * ld_qkv + c] = g;
-      qkv[(feat + f) * ld_qkv + c] = g;
-      qkv[(2 * feat + f) * ld_qkv + c] = g;
+      int64_t orow, grow;
+      if (f < n_feat) {
+        orow = f;
+        grow = f;
+      } else if (f < 2 * n_feat) {
+        orow = feat + (f - n_feat);
+        grow = f - n_feat;
+      } else {
+        const int64_t j = f - 2 * n_feat;
+        orow = 2 * feat + j;
+        grow = v_compact ? (int64_t)rows[j] : j;
+      }
+      qkv[orow * ld_qkv + c] = ctx[grow * ld_ctx + c];
     }
   }
 }
 
 cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int64_t feat,
-                        int64_t n_feat, int64_t N, int dtype, const int32_t* rows, cudaStream_t st) {
+                        int64_t n_feat, int64_t N, int dtype, const int32_t* rows, int64_t n_v, int v_compact,
+                        cudaStream_t st) {
   const int threads = 256;
   const int blocks = 148 * 8;
   if (dtype == 0)
     return launch_k(ztp_core_bf16, blocks, threads, 0, st, phase, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)qkv,
-                    ld_qkv, (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N, rows);
+                    ld_qkv, (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N, rows, n_v, v_compact);
   return launch_k(ztp_core_f32, blocks, threads, 0, st, phase, (float*)qkv, ld_qkv, (float*)ctx, ld_ctx, feat, n_feat,
-                  N, rows);
+                  N, rows, n_v, v_compact);
 }
 
 // ------------------------------------------------- row compaction (a4 gather)

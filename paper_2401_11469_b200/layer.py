@@ -136,7 +136,7 @@ class ZtpLayer:
         self.W2_c = _buf(u + cap, h, dtype)
         # selection buffers (lineage)
         self.K = {"qkv": h, "o": a, "fc1": h, "fc2": u + cap}
-        total = sum(self.K.values())
+        total = sum(self.K.values()) + 3 * a        # + the derived V-output segment (A-36)
         self.kept = torch.zeros(total, dtype=torch.int32, device="cuda")
         self.pruned = torch.zeros(total, dtype=torch.int32, device="cuda")
         self.pos = torch.zeros(total + cap, dtype=torch.int32, device="cuda")
@@ -163,20 +163,33 @@ class ZtpLayer:
         self.seg_len = {"qkv": self.h, "o": self.a, "fc1": self.h, "fc2": own_fc2}
         self.append = {"qkv": 0, "o": 0, "fc1": 0, "fc2": n_in}
         self.n_prune = dict(n_prune)
-        lens = [self.seg_len[s] for s in SEGS]
-        nps = [self.n_prune[s] for s in SEGS]
-        apps = [self.append[s] for s in SEGS]
+        # A-36: the V rows of the QKV output feed only ctx features S_o (the
+        # O projection's kept set), so QKV computes V for S_o only.  The V
+        # selection is a derived segment over the 3a QKV outputs -- Q and K
+        # scored +inf (never pruned), V scored like O's inputs -- selected in
+        # the same launch, so it is exactly O's (S_o, P_o) shifted by 2a.
+        self.v_prune = self.n_prune["o"] > 0 and os.environ.get("ZTP_V_PRUNE", "1") != "0"
+        segs = SEGS + (("vo",) if self.v_prune else ())
+        if self.v_prune:
+            self.seg_len["vo"], self.append["vo"], self.n_prune["vo"] = 3 * self.a, 0, self.n_prune["o"]
+        lens = [self.seg_len[s] for s in segs]
+        nps = [self.n_prune[s] for s in segs]
+        apps = [self.append[s] for s in segs]
         if scores is None:
-            sc = torch.zeros(sum(lens), dtype=torch.float32, device="cuda")
+            base = [torch.zeros(self.seg_len[s], dtype=torch.float32, device="cuda") for s in SEGS]
         else:
-            sc = torch.cat([scores[s][: self.seg_len[s]].float() for s in SEGS])
+            base = [scores[s][: self.seg_len[s]].float() for s in SEGS]
+        if self.v_prune:
+            inf = torch.full((2 * self.a,), float("inf"), dtype=torch.float32, device="cuda")
+            base = base + [inf, base[1]]
+        sc = torch.cat(base)
         self._scores = sc
         self._sel_args = (lens, nps, apps)
         self.run_select(stream)
         # slices of the lineage buffers
         ko = po = qo = 0
         self.S, self.P, self.POS, self.nk = {}, {}, {}, {}
-        for s in SEGS:
+        for s in segs:
             nk = self.seg_len[s] - self.n_prune[s] + self.append[s]
             self.S[s] = self.kept[ko:ko + nk]
             self.P[s] = self.pruned[po:po + max(self.n_prune[s], 0)]
@@ -237,11 +250,15 @@ class ZtpLayer:
     def _build_args(self):
         h, a, N, nfc = self.h, self.a, self.N, self.n_fc
         self.sels = {s: self._sel(s, i) for i, s in enumerate(SEGS)}
+        vsel = self._sel("vo", 4) if self.v_prune else None
+        self.vsel = vsel
         L = Z.linear_args
         nk = self.nk
+        ngq = 2 * a + nk["o"] if vsel is not None else 3 * a      # QKV output rows computed
         # forward
+        vkw = {"out_sel": vsel, "y_pos": self.POS["vo"]} if vsel is not None else {}
         self.f_qkv = L(x_t=self.X, w_t=self.qkv_t, y_t=self.QKV, xs_t=self.Xc, ws_t=self.Wqkv_c,
-                       sel_=self.sels["qkv"])
+                       sel_=self.sels["qkv"], n_out=3 * a, **vkw)
         # TP = 1 (no all-reduce of Y1): the O projection's epilogue writes Y1
         # directly in FC1's kept order (rows S_fc1, through its inverse map),
         # so no full Y1 and no compaction copy exist.  TP > 1 all-reduces the
@@ -282,8 +299,8 @@ class ZtpLayer:
                        **y1_kw)
         self.b_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx, dw_t=self.do,
                      ws_t=self.Wo_c, sel_=self.sels["o"], x_compact=True)
-        self.b_qkv = L(x_t=self.X, w_t=self.qkv_t, g_t=self.gQKV, dx_t=self.dX, dw_t=self.dqkv, xs_t=self.Xc,
-                       ws_t=self.Wqkv_c, sel_=self.sels["qkv"])
+        self.b_qkv = L(x_t=self.X, w_t=self.qkv_t, g_t=self.gQKV[:ngq], dx_t=self.dX, dw_t=self.dqkv, xs_t=self.Xc,
+                       ws_t=self.Wqkv_c, sel_=self.sels["qkv"], n_out=3 * a, **vkw)
 
     # --------------------------------------------------------------- migration
     def _xfers(self, grads: bool):
@@ -316,7 +333,8 @@ class ZtpLayer:
         c = self.ctx
         self.prepare(stream)
         Z.ztp_col_linear(c, Z.FWD, self.f_qkv, stream)
-        Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, self.S["o"], self.nk["o"], stream)
+        Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, self.S["o"], self.nk["o"], stream,
+                   v_compact=self.vsel is not None)
         Z.ztp_row_linear(c, Z.FWD, self.f_o, stream)          # + all-reduce of Y1
 
     def fwd_mlp(self, stream=None):
@@ -332,7 +350,11 @@ class ZtpLayer:
     def bwd_attn(self, stream=None):
         c = self.ctx
         Z.ztp_row_linear(c, Z.BWD, self.b_o, stream)          # dctx, dWo
-        Z.ztp_core(c, Z.BWD, self.gQKV, self.dctx, self.a, self.a, None, 0, stream)
+        if self.vsel is not None:
+            Z.ztp_core(c, Z.BWD, self.gQKV, self.dctx, self.a, self.a, self.S["o"], self.nk["o"], stream,
+                       v_compact=True)
+        else:
+            Z.ztp_core(c, Z.BWD, self.gQKV, self.dctx, self.a, self.a, None, 0, stream)
         Z.ztp_col_linear(c, Z.BWD, self.b_qkv, stream)        # dX (+ all-reduce), dWqkv
 
     def forward(self, stream=None):
