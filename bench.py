@@ -328,14 +328,18 @@ def main():
     def run_phase(g, steps, warm):
         """warm untimed replays (at least ~100 ms of them, so the timed steps
         start from the clock / power state of a running job, not from the idle
-        gap of graph capture), then `steps` timed replays."""
+        gap of graph capture), then `steps` timed replays.  The warm-up count
+        is agreed over ranks (max), since every replay runs collectives."""
         torch.cuda.synchronize()
         t0 = time.time()
-        n = 0
-        while n < warm or (time.time() - t0 < 0.1 and n < 2000):
+        for _ in range(3):
             g.replay()
-            n += 1
-            if n % 50 == 0:
+        torch.cuda.synchronize()
+        per = max((time.time() - t0) / 3, 1e-6)
+        n = int(D.max(float(max(warm, min(2000, math.ceil(0.1 / per))))))
+        for i in range(3, n):
+            g.replay()
+            if i % 50 == 0:
                 torch.cuda.synchronize()
         return timed(D, g.replay, steps, stream)
 
