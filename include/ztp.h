@@ -387,11 +387,17 @@ ztp_status ztp_read_gemm_ns(ztp_ctx* ctx, void* stream, double* ns);
 typedef struct ztp_profile {
   double gemm_ms, other_ms, comm_ms, gemm_flops;
   int64_t n_gemm, n_other, n_comm;
-  /* sum over GEMM launches of (last CTA end - first CTA start), from the
-   * kernels' own %globaltimer stamps (split-K reduce included): kernel time
-   * without event / launch overheads */
+  /* length of the union over GEMM launches of [first CTA start, last CTA
+   * end], from the kernels' own %globaltimer stamps (split-K reduce
+   * included): GEMM kernel time without event / launch overheads, overlaps
+   * between launches (PDL) counted once */
   double gemm_kernel_ms;
 } ztp_profile;
+/* on = 2: GEMM kernel stamps only (no events, no change to the launch
+ * schedule), capturable: a graph captured in this mode writes the same stamp
+ * slots on every replay, and each ztp_read_profile returns the GEMM kernel
+ * time and FLOPs of the replays since the last read (one replay per read
+ * gives per-step values).  on = 0 releases the slots. */
 ztp_status ztp_set_profile(ztp_ctx* ctx, int on);
 ztp_status ztp_read_profile(ztp_ctx* ctx, void* stream, ztp_profile* out);
 

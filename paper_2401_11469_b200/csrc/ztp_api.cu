@@ -70,6 +70,7 @@ struct ztp_ctx {
   int prof_on = 0;
   unsigned long long* d_pstamp = nullptr;   // per-GEMM-launch kernel stamps while profiling
   int pstamp_used = 0;
+  std::vector<double> pstamp_flops;         // algorithmic FLOPs of each stamped launch
   static constexpr int PSTAMP_CAP = 4096;
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
@@ -79,7 +80,7 @@ enum { PROF_GEMM = 0, PROF_OTHER = 1, PROF_COMM = 2 };
 
 namespace {
 int prof_begin(ztp_ctx* c, cudaStream_t st, int cat, double flops) {
-  if (!c->prof_on) return -1;
+  if (c->prof_on != 1) return -1;   // mode 2: kernel stamps only (capturable in CUDA graphs)
   if (c->prof_used == c->prof.size()) {
     ztp_ctx::ProfEv e{};
     if (cudaEventCreate(&e.a) != cudaSuccess || cudaEventCreate(&e.b) != cudaSuccess) return -1;
@@ -283,8 +284,11 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     // depends on stamps (emulation) and the workspaces are disjoint (dW uses
     // its own split-K workspace)
     p.pdl_late = indep_of_prev && !emulating(c) && ztp::pdl_enabled();
-    if (c->prof_on && c->d_pstamp && c->pstamp_used < ztp_ctx::PSTAMP_CAP)
+    if (c->prof_on && c->d_pstamp && c->pstamp_used < ztp_ctx::PSTAMP_CAP) {
+      c->pstamp_flops.resize((size_t)c->pstamp_used + 1);
+      c->pstamp_flops[c->pstamp_used] = 2.0 * (double)nk * (double)n_out * tokens;
       p.prof_stamp = c->d_pstamp + 2 * (c->pstamp_used++);
+    }
     // split-K over the contraction when the output has too few tiles for 148 SMs
     p.splits = c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, c->num_sms) : 1;
     if (p.splits > 1) {
@@ -571,7 +575,7 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
   // dW concurrently with dX on the side stream (not while emulating a
   // straggler -- the slowdown stamps one GEMM at a time -- nor while profiling,
   // which times each GEMM alone)
-  const bool conc = c->conc_bwd && !c->prof_on && a->dx_t.ptr && a->dw_t.ptr && !emulating(c);
+  const bool conc = c->conc_bwd && c->prof_on != 1 && a->dx_t.ptr && a->dw_t.ptr && !emulating(c);
   cudaStream_t sw = st;
   if (conc) {
     CUDA_TRY(c, cudaEventRecord(c->ev_c, st));
@@ -1042,7 +1046,8 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
 
 ztp_status ztp_set_profile(ztp_ctx* c, int on) {
   if (!c) return fail(c, ZTP_EINVAL, "ztp_set_profile: null ctx");
-  c->prof_on = on ? 1 : 0;
+  c->prof_on = (on == 2) ? 2 : (on ? 1 : 0);
+  if (!on) c->pstamp_used = 0;
   if (on && !c->d_pstamp) CUDA_TRY(c, cudaMalloc(&c->d_pstamp, 2 * ztp_ctx::PSTAMP_CAP * sizeof(unsigned long long)));
   if (on) {
     CUDA_TRY(c, cudaMemset(c->d_pstamp, 0, 2 * ztp_ctx::PSTAMP_CAP * sizeof(unsigned long long)));
@@ -1076,12 +1081,36 @@ ztp_status ztp_read_profile(ztp_ctx* c, void* stream, ztp_profile* out) {
   if (c->pstamp_used > 0) {
     std::vector<unsigned long long> h(2 * (size_t)c->pstamp_used);
     CUDA_TRY(c, cudaMemcpy(h.data(), c->d_pstamp, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    // GEMM kernel time = length of the UNION of the launches' [start, end]
+    // intervals (launches overlap under PDL; a sum would count it twice)
+    std::vector<std::pair<unsigned long long, unsigned long long>> iv;
     for (int i = 0; i < c->pstamp_used; ++i) {
       const unsigned long long t0 = ~h[2 * i], t1 = h[2 * i + 1];
-      if (h[2 * i] != 0 && t1 >= t0) out->gemm_kernel_ms += (double)(t1 - t0) * 1e-6;
+      if (h[2 * i] != 0 && t1 >= t0) {
+        iv.emplace_back(t0, t1);
+        if (c->prof_on == 2) {
+          out->gemm_flops += c->pstamp_flops[i];
+          ++out->n_gemm;
+        }
+      }
+    }
+    std::sort(iv.begin(), iv.end());
+    if (!iv.empty()) {
+      unsigned long long cs = iv[0].first, ce = iv[0].second;
+      for (size_t k = 1; k < iv.size(); ++k) {
+        if (iv[k].first > ce) {
+          out->gemm_kernel_ms += (double)(ce - cs) * 1e-6;
+          cs = iv[k].first;
+          ce = iv[k].second;
+        } else if (iv[k].second > ce) {
+          ce = iv[k].second;
+        }
+      }
+      out->gemm_kernel_ms += (double)(ce - cs) * 1e-6;
     }
     CUDA_TRY(c, cudaMemset(c->d_pstamp, 0, h.size() * sizeof(unsigned long long)));
-    c->pstamp_used = 0;
+    // mode 2 keeps its slots: a captured graph writes the same ones every replay
+    if (c->prof_on != 2) c->pstamp_used = 0;
   }
   return ZTP_OK;
 }
