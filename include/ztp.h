@@ -400,6 +400,10 @@ typedef struct ztp_profile {
  * gives per-step values).  on = 0 releases the slots. */
 ztp_status ztp_set_profile(ztp_ctx* ctx, int on);
 ztp_status ztp_read_profile(ztp_ctx* ctx, void* stream, ztp_profile* out);
+/* Diagnostics: the raw [start, end] %globaltimer stamps (ns) of the stamped
+ * GEMM launches (profiling on), in launch order, without resetting them;
+ * returns how many pairs were written to out[2 * max_launches], -1 on error. */
+int ztp_read_stamps(ztp_ctx* ctx, void* stream, unsigned long long* out, int max_launches);
 
 /* Raw resized GEMM (test / benchmark entry; the linears use it internally).
  * kind 0 = FWD (y = w[S]^T x[S]), 1 = dX (dx rows by sel), 2 = dW. */

@@ -239,6 +239,15 @@ def ztp_read_profile(ctx, stream=None) -> dict:
     return {k: getattr(p, k) for k, _ in _lib.Profile._fields_}
 
 
+def ztp_read_stamps(ctx, stream=None, max_launches: int = 256):
+    """[(start_ns, end_ns)] of the stamped GEMM launches (diagnostics)."""
+    buf = (C.c_uint64 * (2 * max_launches))()
+    n = lib.ztp_read_stamps(ctx, _stream(stream), buf, max_launches)
+    if n < 0:
+        raise ZtpError(-1, "ztp_read_stamps failed")
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(n)]
+
+
 def ztp_read_gemm_ns(ctx, stream=None) -> float:
     v = C.c_double()
     check(lib.ztp_read_gemm_ns(ctx, _stream(stream), C.byref(v)), ctx)

@@ -127,6 +127,7 @@ def _load():
         "ztp_gemm": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
         "ztp_prepare": (st, [vp, C.c_int, C.POINTER(C.POINTER(LinearArgs)), C.POINTER(C.c_int32), vp]),
         "ztp_priority_update": (st, [vp, C.POINTER(Mat), C.POINTER(Mat), vp, vp, vp, C.c_float, vp]),
+        "ztp_read_stamps": (C.c_int, [vp, vp, C.POINTER(C.c_uint64), C.c_int]),
         "ztp_pridiff_gamma": (C.c_double, [C.c_int64, C.c_int64, C.c_double, C.c_double]),
         "ztp_set_profile": (st, [vp, C.c_int]),
         "ztp_read_profile": (st, [vp, vp, C.POINTER(Profile)]),
@@ -145,7 +146,7 @@ EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_i
             "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count", "ztp_plan_opts_default", "ztp_plan",
             "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
             "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "ztp_prepare",
-            "ztp_priority_update", "ztp_pridiff_gamma",
+            "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",
             "ztp_set_profile", "ztp_read_profile")
 
 

@@ -1115,6 +1115,17 @@ ztp_status ztp_read_profile(ztp_ctx* c, void* stream, ztp_profile* out) {
   return ZTP_OK;
 }
 
+int ztp_read_stamps(ztp_ctx* c, void* stream, unsigned long long* out, int max_launches) {
+  if (!c || !out || max_launches < 0) return -1;
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return -1;
+  const int n = std::min(c->pstamp_used, max_launches);
+  if (n <= 0 || !c->d_pstamp) return 0;
+  if (cudaMemcpy(out, c->d_pstamp, 2 * (size_t)n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  for (int i = 0; i < n; ++i) out[2 * i] = ~out[2 * i];
+  return n;
+}
+
 ztp_status ztp_set_slowdown(ztp_ctx* c, double chi) {
   if (!c || !(chi >= 1.0)) return fail(c, ZTP_EINVAL, "ztp_set_slowdown: chi must be >= 1");
   c->chi = chi;
