@@ -676,6 +676,76 @@ __global__ void __launch_bounds__(256) ztp_splitk_reduce(const GemmParams p) {
   if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp + 1, (unsigned long long)globaltimer());
 }
 
+// Lean split-K reduce for dW (no epilogue math): S splits known at compile
+// time, so every partial of an 8-column group is loaded before the fixed-order
+// sum s = 0..S-1 (memory-level parallelism without predicated spare loads);
+// COLPOS spreads compact columns to their units (output pruning).
+template <int S, bool COLPOS>
+__global__ void __launch_bounds__(256) ztp_dw_reduce(const GemmParams p) {
+  pdl_wait();
+  pdl_trigger();
+  const int width = COLPOS ? p.n_full : p.N;
+  const int cpr = (width + 7) / 8;
+  const int64_t total = (int64_t)p.M * cpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / cpr);
+    const int col = (int)(i % cpr) * 8;
+    const int nv = width - col;
+    const bool computed = m < p.n_kept;
+    const int orow = p.out_dense ? m : (computed ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept)));
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (computed) {
+      const float* src = p.ws + (int64_t)m * p.ld_ws;
+      if constexpr (COLPOS) {
+        int cc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cc[q] = q < nv ? __ldg(p.col_pos + col + q) : -1;
+        float t[S][8];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) t[s][q] = cc[q] >= 0 ? __ldcg(src + s * p.ws_split_stride + cc[q]) : 0.f;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] += t[s][q];
+      } else {
+        float4 a[S], b[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const float* q = src + s * p.ws_split_stride + col;
+          a[s] = __ldcg(reinterpret_cast<const float4*>(q));
+          b[s] = __ldcg(reinterpret_cast<const float4*>(q + 4));
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          v[0] += a[s].x;
+          v[1] += a[s].y;
+          v[2] += a[s].z;
+          v[3] += a[s].w;
+          v[4] += b[s].x;
+          v[5] += b[s].y;
+          v[6] += b[s].z;
+          v[7] += b[s].w;
+        }
+      }
+    }
+    uint4 w;
+    w.x = pack_bf16(v[0], v[1]);
+    w.y = pack_bf16(v[2], v[3]);
+    w.z = pack_bf16(v[4], v[5]);
+    w.w = pack_bf16(v[6], v[7]);
+    store_bf16x8(p.out + (int64_t)orow * p.ld_out + col, w, nv);
+  }
+  if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp + 1, (unsigned long long)globaltimer());
+}
+
+template <int S>
+static cudaError_t dw_reduce_launch(const GemmParams& p, int blocks, cudaStream_t st) {
+  if (p.col_pos) return launch_k(ztp_dw_reduce<S, true>, blocks, 256, 0, st, p);
+  return launch_k(ztp_dw_reduce<S, false>, blocks, 256, 0, st, p);
+}
+
 // ----------------------------------------------------------------- host side
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -769,6 +839,14 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
   }
   const int64_t chunks = (int64_t)p.M * (((p.col_pos ? p.n_full : p.N) + 7) / 8);
   const int blocks = (int)std::min<int64_t>((chunks + 255) / 256, (int64_t)num_sms * 8);
+  if (KIND == KIND_DW && p.epi == EPI_NONE) {
+    switch (p.splits) {
+      case 2: return dw_reduce_launch<2>(p, blocks, st);
+      case 3: return dw_reduce_launch<3>(p, blocks, st);
+      case 4: return dw_reduce_launch<4>(p, blocks, st);
+      default: break;   // more splits: the generic loop (measured faster at S = 8)
+    }
+  }
   return launch_k(ztp_splitk_reduce<KIND>, blocks, 256, 0, st, p);
 }
 
