@@ -1,0 +1,118 @@
+"""GPU tests of the runtime side of the path through the C ABI: SEMI-migration
+peer copies at world 1 (local-copy path of ztp_migrate, a8), straggler
+emulation + statistics (a1: M_i from the GEMMs' own stamps, A-6, A-32), the
+statistics all-gather at world 1, and the profiling counters."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ztp_oracle as O
+from synth import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import paper_2401_11469_b200 as Z
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    ctx = Z.ztp_ctx_create(0, 1, None, 0)
+    yield Z, torch, ctx
+    Z.ztp_ctx_destroy(ctx)
+
+
+def padded(torch, r, c, dtype, fill):
+    ld = (c + 7) // 8 * 8 + 8
+    t = torch.full((r, ld), fill, device="cuda", dtype=dtype)
+    return t[:, :c]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_migrate_local_copies(env, dtype):
+    """Sub-matrix copies src[r0:r0+nr, c0:c0+nc] -> dst[dr0:.., dc0:..] (the
+    W1 column / W2 row slices SEMI moves, A-26), exact; untouched elements
+    keep their value; zero-size transfers are no-ops."""
+    Z, torch, ctx = env
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    src = padded(torch, 300, 264, td, 0.0)
+    src.copy_(torch.from_numpy(I.normal(3, "m", 300, 264).astype(np.float32)).cuda().to(td))
+    dst = padded(torch, 280, 200, td, -7.0)
+    xs = [Z.xfer(src, dst, r0=5, c0=8, nr=40, nc=64, dr0=0, dc0=16),
+          Z.xfer(src, dst, r0=100, c0=0, nr=120, nc=24, dr0=150, dc0=100),
+          Z.xfer(src, dst, r0=0, c0=0, nr=0, nc=10, dr0=0, dc0=0)]
+    Z.ztp_migrate(ctx, xs)
+    Z.ztp_sync(ctx)
+    s, d = src.float().cpu().numpy(), dst.float().cpu().numpy()
+    want = np.full((280, 200), -7.0, dtype=np.float32)
+    want[0:40, 16:80] = s[5:45, 8:72]
+    want[150:270, 100:124] = s[100:220, 0:24]
+    assert np.array_equal(d, want)
+
+
+def test_migrate_errors(env):
+    Z, torch, ctx = env
+    a = torch.zeros(64, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(Z.ZtpError) as e1:
+        Z.ztp_migrate(ctx, [Z.xfer(a, a, nr=8, nc=8, src_rank=0, dst_rank=1)])      # rank outside world 1
+    assert e1.value.name == "ZTP_EINVAL"
+    with pytest.raises(Z.ZtpError) as e2:
+        Z.ztp_migrate(ctx, [Z.xfer(a, a, r0=60, nr=8, nc=8)])                      # slice outside src
+    assert e2.value.name == "ZTP_ESHAPE"
+
+
+def _gemm_args(Z, torch, K, n, N):
+    x = (torch.rand(K, N, device="cuda") - 0.5).to(torch.bfloat16)
+    w = (torch.rand(K, n, device="cuda") - 0.5).to(torch.bfloat16)
+    y = torch.empty(n, N, device="cuda", dtype=torch.bfloat16)
+    return Z.linear_args(x_t=x, w_t=w, y_t=y), (x, w, y)
+
+
+def test_slowdown_emulation_and_statistics(env):
+    """chi = 2 stretches every GEMM to twice its own duration (delay kernel on
+    the GEMM's %globaltimer stamps, A-32) and M_i accumulates the stretched
+    time (A-6): M(chi=2) / M(chi=1) ~ 2.  The all-gather at world 1 returns
+    the rank's own (T, M)."""
+    Z, torch, ctx = env
+    a, keep = _gemm_args(Z, torch, 2048, 2048, 8192)
+    for _ in range(100):                             # clocks out of the idle state first
+        Z.ztp_gemm(ctx, Z.KIND_FWD, a)
+    Z.ztp_set_slowdown(ctx, 2.0)                     # load the delay kernel (lazy module loading)
+    Z.ztp_gemm(ctx, Z.KIND_FWD, a)
+    Z.ztp_sync(ctx)
+    res = {}
+    for chi in (1.0, 2.0):
+        Z.ztp_set_slowdown(ctx, chi)
+        Z.ztp_set_stats(ctx, True)
+        Z.ztp_read_gemm_ns(ctx)                      # reset
+        for _ in range(10):
+            Z.ztp_gemm(ctx, Z.KIND_FWD, a)
+        res[chi] = Z.ztp_read_gemm_ns(ctx)
+        Z.ztp_set_stats(ctx, False)
+    Z.ztp_set_slowdown(ctx, 1.0)
+    assert res[1.0] > 0
+    assert 1.7 < res[2.0] / res[1.0] < 2.3, res
+    T, M = Z.ztp_allgather_stats(ctx, 1.25, 0.75, 1)
+    assert T == [1.25] and M == [0.75]
+    with pytest.raises(Z.ZtpError):
+        Z.ztp_set_slowdown(ctx, 0.5)                 # chi < 1 is not a slowdown
+
+
+def test_profile_counters(env):
+    """ztp_read_profile: GEMM launch count and algorithmic FLOPs exact; the
+    kernel-stamp time is positive and within the event-bracketed time."""
+    Z, torch, ctx = env
+    K, n, N = 512, 1024, 4096
+    a, keep = _gemm_args(Z, torch, K, n, N)
+    Z.ztp_gemm(ctx, Z.KIND_FWD, a)
+    torch.cuda.synchronize()
+    Z.ztp_read_profile(ctx)
+    Z.ztp_set_profile(ctx, True)
+    for _ in range(3):
+        Z.ztp_gemm(ctx, Z.KIND_FWD, a)
+    p = Z.ztp_read_profile(ctx)
+    Z.ztp_set_profile(ctx, False)
+    assert p["n_gemm"] == 3
+    assert p["gemm_flops"] == pytest.approx(3 * 2.0 * K * n * N, rel=1e-12)
+    assert 0 < p["gemm_kernel_ms"] <= p["gemm_ms"] * 1.05
