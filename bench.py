@@ -264,7 +264,7 @@ def main():
 
     import torch
     import paper_2401_11469_b200 as Z
-    from paper_2401_11469_b200.layer import ZtpLayer, SEGS
+    from paper_2401_11469_b200.layer import ZtpLayer, SEGS, layer_prune_counts
     from synth.configs import CONFIGS
     from synth import inputs as I
 
@@ -366,9 +366,7 @@ def main():
         del gB
         T_all, M_all = Z.ztp_allgather_stats(ctx, T_own, M_own, e, stream)
         plan = Z.ztp_plan(T_all, M_all, float(h), None, Z.plan_opts(enable_migration=0, zero_crit=Z.CRIT_MIN))
-        n_prune = {}
-        for s, K, is_row in (("qkv", h, False), ("o", a, True), ("fc1", h, False), ("fc2", u, True)):
-            n_prune[s] = Z.ztp_plan_counts(plan, r, K, u, 1, is_row).n_prune
+        n_prune = layer_prune_counts(plan, r, h, a, u)
         plan_info = {"T_ms": T_all, "M_ms": M_all, "gamma": list(plan.gamma)[:e], "role": list(plan.role)[:e],
                      "z": plan.z, "criterion": "T_min (A-7)"}
     else:
@@ -377,8 +375,7 @@ def main():
         p.world = 1
         p.role[0] = Z.RESIZE
         p.gamma[0] = p.gamma_r[0] = args.gamma
-        n_prune = {s: Z.ztp_plan_counts(p, 0, K, u, 1, s in ("o", "fc2")).n_prune
-                   for s, K in (("qkv", h), ("o", a), ("fc1", h), ("fc2", u))}
+        n_prune = layer_prune_counts(p, 0, h, a, u)
         plan_info = {"gamma": [args.gamma], "mode": "homogeneous ZERO-Pri"}
     L.set_selection(n_prune, sc)
 

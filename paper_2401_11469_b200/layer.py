@@ -72,6 +72,25 @@ def migration_io(plan, rank: int, world: int, u: int, h: int, unit: int = 1) -> 
     return mio
 
 
+def layer_prune_counts(plan, rank: int, h: int, a: int, u: int) -> Dict[str, int]:
+    """Prune counts of the four linears of `rank` from a plan (host only).
+    MLP (A-26): FC1 prunes its input K = h by gamma_r, FC2 its K_rem = u -
+    n_mig own units by gamma_r (ztp_plan_counts).  Attention (A-37): heads do
+    not migrate in this build, so QKV / O prune K = h / a by gamma_r, and a
+    rank that sheds MLP units (MIGRATE / SPLIT) resizes its attention by its
+    Eq.1 gamma instead -- its remaining attention work is (1 - gamma), as is
+    the MLP's after migration."""
+    att = Z.PlanT.from_buffer_copy(plan)
+    if int(plan.role[rank]) in (Z.MIGRATE, Z.SPLIT):
+        att.gamma_r[rank] = plan.gamma[rank]
+    att.role[rank] = Z.RESIZE
+    att.phi[rank] = 0.0
+    return {"qkv": Z.ztp_plan_counts(att, rank, h, h, 1, False).n_prune,
+            "o": Z.ztp_plan_counts(att, rank, a, a, 1, False).n_prune,
+            "fc1": Z.ztp_plan_counts(plan, rank, h, u, 1, False).n_prune,
+            "fc2": Z.ztp_plan_counts(plan, rank, u, u, 1, True).n_prune}
+
+
 def xfer_specs(mio: MigrationIO, u: int, h: int, grads: bool) -> List[dict]:
     """Peer copies of one layer's migration (pure host logic).  Weights: the
     owner's units [lo, hi) -> the helper's appended slots [u+off, ...) of W1^T

@@ -174,3 +174,29 @@ def test_pridiff_gamma_matches_oracle():
         a = float(rng.choice([0.8, 1.0, 0.5]))
         L_uni = int(np.count_nonzero(d > theta))
         assert Z.ztp_pridiff_gamma(L, L_uni, g, a) == O.pridiff_gamma(d, theta, g, a)
+
+
+def test_layer_prune_counts_attention_rule():
+    """A-37: attention linears prune by gamma_r, except on ranks that shed MLP
+    units (MIGRATE / SPLIT), which resize attention by their Eq.1 gamma; the
+    MLP counts are ztp_plan_counts' (FC2 over its K_rem = u - n_mig)."""
+    import math
+    import paper_2401_11469_b200 as Z
+    from paper_2401_11469_b200.layer import layer_prune_counts
+    T = [10.0, 80.0, 10.0, 60.0, 10.0, 40.0, 10.0, 20.0]
+    M = [8.0, 78.0, 8.0, 58.0, 8.0, 38.0, 8.0, 18.0]
+    h, a, u = 4096, 512, 1376
+    for lam in range(5):
+        plan = Z.ztp_plan(T, M, float(u), None, Z.plan_opts(enable_migration=1, zero_crit=Z.CRIT_MIN,
+                                                               force_lambda=lam))
+        for r in range(8):
+            c = layer_prune_counts(plan, r, h, a, u)
+            role = int(plan.role[r])
+            g_att = plan.gamma[r] if role in (Z.MIGRATE, Z.SPLIT) else plan.gamma_r[r]
+            for s, K in (("qkv", h), ("o", a)):
+                want = min(max(int(math.floor(K * g_att + 0.5)), 0), K - 1)
+                assert c[s] == want, (lam, r, s)
+            assert c["fc1"] == Z.ztp_plan_counts(plan, r, h, u, 1, False).n_prune
+            assert c["fc2"] == Z.ztp_plan_counts(plan, r, u, u, 1, True).n_prune
+            if role == Z.MIGRATE:            # a migrating rank still sheds its attention excess
+                assert c["qkv"] > 0 and c["o"] > 0
