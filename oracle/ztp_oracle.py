@@ -198,10 +198,15 @@ def plan(T, M, L_ref: float, costs: Costs, opts: PlanOpts) -> Plan:
     stragglers = [r for r in p.order if T[r] > thr]
     p.z = len(stragglers)
     if not opts.enable_migration:
-        # ZERO-resizing only (Alg.1 l.1-2): every rank with gamma > 0 resizes.
+        # ZERO-resizing only (Alg.1 l.1-2): the detected stragglers (Alg.2
+        # l.4 with tolerance eps, A-17) with gamma > 0 resize; a rank within
+        # eps of T_min keeps its full shard (A-38).  eps = 0 is paper-literal:
+        # the only excluded ranks sit at T_min, where Eq.1 gives 0 anyway.
         C = T_avg if opts.zero_crit == CRIT_AVG else T_min
         for r in range(e):
-            g = eq1_gamma(T[r], C, M[r], opts.gamma_max)
+            g = eq1_gamma(T[r], C, M[r], opts.gamma_max)      # (raises on M_i = 0 for every rank)
+            if not T[r] > thr:
+                g = 0.0
             p.gamma[r] = g
             p.gamma_r[r] = g
             p.role[r] = RESIZE if g > 0.0 else NORMAL

@@ -113,7 +113,9 @@ extern "C" ztp_status ztp_plan(int e, const double* T, const double* M, double L
     const double C = opts->zero_crit == ZTP_CRIT_AVG ? T_avg : T_min;
     for (int r = 0; r < e; ++r) {
       if (!need_m(r)) return ZTP_ENOBASELINE;
-      const double g = eq1(T[r], C, M[r], opts->gamma_max);
+      // only detected stragglers resize (A-17 tolerance, A-38); eps = 0 is
+      // paper-literal (ranks at T_min get gamma = 0 from Eq.1 anyway)
+      const double g = T[r] > thr ? eq1(T[r], C, M[r], opts->gamma_max) : 0.0;
       out->gamma[r] = g;
       out->gamma_r[r] = g;
       out->role[r] = g > 0.0 ? ZTP_RESIZE : ZTP_NORMAL;

@@ -69,6 +69,21 @@ def test_detection_tolerance_S562():
     assert p.z == 1 and p.order[0] == 1
 
 
+def test_zero_resizes_only_detected_stragglers_A38():
+    """ZERO-only plans resize the ranks Alg.2 l.4 detects (T > T_min (1 + eps),
+    A-17, A-38); eps = 0 gives Eq.1 literally for every rank."""
+    T, M = [10.0, 10.1, 15.0], [5.0, 5.0, 10.0]
+    p = O.plan(T, M, 1.0, O.Costs(), O.PlanOpts(zero_crit=O.CRIT_MIN))
+    assert p.gamma == [0.0, 0.0, 0.5] and p.role == [O.NORMAL, O.NORMAL, O.RESIZE] and p.z == 1
+    p = O.plan(T, M, 1.0, O.Costs(), O.PlanOpts(zero_crit=O.CRIT_MIN, eps=0.0))
+    assert p.gamma[1] == pytest.approx(0.1 / 5.0, rel=1e-12) and p.gamma[2] == 0.5
+    assert p.role == [O.NORMAL, O.RESIZE, O.RESIZE]
+    # AVG criterion: the within-eps rank is below T_avg, so Eq.1 gives 0 anyway
+    p = O.plan(T, M, 1.0, O.Costs(), O.PlanOpts(zero_crit=O.CRIT_AVG))
+    T_avg = (10.0 + 10.1 + 15.0) / 3
+    assert p.gamma[:2] == [0.0, 0.0] and p.gamma[2] == pytest.approx((15.0 - T_avg) / 10.0, rel=1e-12)
+
+
 def test_eq2_worked_example_S572():
     g = golden("eq2_worked.json")
     c = O.Costs(g["omega1"], _costs_from(g, "omega2"), _costs_from(g, "phi1"), _costs_from(g, "phi2"))
