@@ -10,7 +10,8 @@ projection block + MLP block, fwd + bwd, 1D TP over N ranks.
          paper's homogeneous evaluation point) vs the dense step.
   N > 1: rank N-1 emulates a 2x straggler: T_free (chi=1, dense) ->
          T_unbal (chi=2, dense; statistics window -> T_i, M_i) -> ztp_plan
-         (Eq.1, T_min criterion, A-7) -> ztp_select -> T_bal (timed headline).
+         (Eq.1, T_min criterion, A-7) -> ztp_select -> statistics refresh
+         (10% trigger, ztp_plan_refine, A-39) -> T_bal (timed headline).
 A step = select + FWD + BWD of the layer through the C ABI (every kernel is
 libztp's; collectives are NCCL).  value = executed GEMM TFLOP/s of the whole
 job (sum over ranks of 6 N n K' per linear / step time, max over ranks).
@@ -378,6 +379,29 @@ def main():
         n_prune = layer_prune_counts(p, 0, h, a, u)
         plan_info = {"gamma": [args.gamma], "mode": "homogeneous ZERO-Pri"}
     L.set_selection(n_prune, sc)
+    if e > 1:
+        # statistics refresh ("over-10% change ... update on demand",
+        # A-8): a window with the plan in effect; if some rank's runtime moved
+        # by > 10%, Eq.1 on that window is composed with the plan (A-39).
+        plan_info["refresh"] = []
+        T_last = T_all
+        for _ in range(2):
+            Z.ztp_set_stats(ctx, True)
+            gR, _ = make_graph()
+            run_phase(gR, 20, 3)
+            prof = profiled_steps(10)
+            Z.ztp_set_stats(ctx, False)
+            del gR
+            T_cur, M_cur = Z.ztp_allgather_stats(ctx, prof["gemm_ms"] + prof["other_ms"], prof["gemm_ms"], e, stream)
+            if max(abs(T_cur[q] - T_last[q]) / T_last[q] for q in range(e)) <= 0.10:
+                break
+            fresh = Z.ztp_plan(T_cur, M_cur, float(h), None, Z.plan_opts(enable_migration=0, zero_crit=Z.CRIT_MIN))
+            if fresh.z == 0:
+                break
+            T_last = T_cur
+            plan = Z.ztp_plan_refine(plan, fresh)
+            L.set_selection(layer_prune_counts(plan, r, h, a, u), sc)
+            plan_info["refresh"].append({"T_ms": T_cur, "gamma": list(plan.gamma)[:e]})
 
     # ---- phase C: balanced / resized step (headline), profiled inside the graph
     gC, per_step_launches = make_graph()

@@ -129,6 +129,33 @@ def eq1_gamma(T_r: float, C: float, M_r: float, gamma_max: float) -> float:
     return g
 
 
+def plan_refine(prev: Plan, fresh: Plan, gamma_max: float = 0.9) -> Plan:
+    """Statistics refresh of a ZERO-only plan ("over-10% increase ...
+    update on demand", A-8; reading A-39).  `fresh` is Eq.1 on a window
+    measured with `prev` in effect, so its ratio is a fraction of the work the
+    rank still computes (the savings offset the remaining gap
+    T_i - T_avg): kept fractions multiply, 1 - gamma = (1 - gamma_prev)
+    (1 - gamma_fresh), clamped to gamma_max (A-4)."""
+    if prev.world != fresh.world:
+        raise OracleError("ZTP_EINVAL", "world mismatch")
+    e = fresh.world
+    if any(x in (MIGRATE, SPLIT) for x in list(prev.role[:e]) + list(fresh.role[:e])):
+        raise OracleError("ZTP_EUNSUPPORTED", "refine ZERO-only plans (A-39)")
+    out = Plan(world=e, z=fresh.z, x=0, order=list(fresh.order), role=[NORMAL] * e, gamma=[0.0] * e,
+               beta=[0.0] * e, phi=[0.0] * e, gamma_r=[0.0] * e)
+    for r in range(e):
+        keep = (1.0 - prev.gamma_r[r]) * (1.0 - fresh.gamma_r[r])
+        g = 1.0 - keep
+        if g > gamma_max:
+            g = gamma_max
+        if g < 0.0:
+            g = 0.0
+        out.gamma[r] = g
+        out.gamma_r[r] = g
+        out.role[r] = RESIZE if g > 0.0 else NORMAL
+    return out
+
+
 def solve_beta(Lg: float, costs: Costs, e: int, iters: int) -> float:
     """Eq.2: Omega1 + Omega2(L g (1-b)) = Phi1(L g b) + Phi2(L g b/(e-1)).
     g(b) = LHS - RHS is non-increasing; bisection with a fixed iteration count

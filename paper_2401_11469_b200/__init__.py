@@ -18,7 +18,7 @@ from ._lib import (ACT_GELU, ACT_GELU_D, ACT_NONE, BF16, BWD, CRIT_AVG, CRIT_MIN
 
 __all__ = [
     "ztp_version", "ztp_get_unique_id", "ztp_ctx_create", "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count",
-    "ztp_plan", "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
+    "ztp_plan", "ztp_plan_refine", "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
     "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "mat",
     "make_costs", "plan_opts", "ZtpError",
 ]
@@ -110,6 +110,12 @@ def ztp_plan(T: Sequence[float], M: Sequence[float], L_ref: float, costs=None, o
     c, _keep = costs if isinstance(costs, tuple) else (costs, None)
     out = PlanT()
     check(lib.ztp_plan(e, Ta, Ma, L_ref, C.byref(c), C.byref(opts or plan_opts()), C.byref(out)))
+    return out
+
+
+def ztp_plan_refine(prev: PlanT, fresh: PlanT, gamma_max: float = 0.9) -> PlanT:
+    out = PlanT()
+    check(lib.ztp_plan_refine(C.byref(prev), C.byref(fresh), gamma_max, C.byref(out)))
     return out
 
 

@@ -110,6 +110,7 @@ def _load():
         "ztp_plan_opts_default": (None, [C.POINTER(PlanOpts)]),
         "ztp_plan": (st, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double,
                           C.POINTER(Costs), C.POINTER(PlanOpts), C.POINTER(PlanT)]),
+        "ztp_plan_refine": (st, [C.POINTER(PlanT), C.POINTER(PlanT), C.c_double, C.POINTER(PlanT)]),
         "ztp_plan_counts": (st, [C.POINTER(PlanT), C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                  C.POINTER(Counts)]),
         "ztp_allgather_stats": (st, [vp, C.c_double, C.c_double, C.POINTER(C.c_double),
@@ -143,7 +144,7 @@ lib = _load()
 
 # every symbol include/ztp.h declares (checked by tests/test_abi.py)
 EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_id", "ztp_ctx_create",
-            "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count", "ztp_plan_opts_default", "ztp_plan",
+            "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count", "ztp_plan_opts_default", "ztp_plan", "ztp_plan_refine",
             "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
             "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "ztp_prepare",
             "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",

@@ -190,6 +190,35 @@ extern "C" ztp_status ztp_plan(int e, const double* T, const double* M, double L
   return ZTP_OK;
 }
 
+extern "C" ztp_status ztp_plan_refine(const ztp_plan_t* prev, const ztp_plan_t* fresh, double gamma_max,
+                                      ztp_plan_t* out) {
+  if (!prev || !fresh || !out || prev->world != fresh->world || fresh->world < 1 || fresh->world > ZTP_MAX_RANKS) {
+    set_thread_error("ztp_plan_refine: null plan or world mismatch");
+    return ZTP_EINVAL;
+  }
+  const int e = fresh->world;
+  for (int r = 0; r < e; ++r)
+    if (prev->role[r] > ZTP_RESIZE || fresh->role[r] > ZTP_RESIZE) {
+      set_thread_error("ztp_plan_refine: rank " + std::to_string(r) + " migrates; refine ZERO-only plans (A-39)");
+      return ZTP_EUNSUPPORTED;
+    }
+  ztp_plan_t o = *fresh;
+  o.x = 0;
+  for (int r = 0; r < e; ++r) {
+    const double keep = (1.0 - prev->gamma_r[r]) * (1.0 - fresh->gamma_r[r]);
+    double g = 1.0 - keep;
+    if (g > gamma_max) g = gamma_max;
+    if (g < 0.0) g = 0.0;
+    o.gamma[r] = g;
+    o.gamma_r[r] = g;
+    o.beta[r] = 0.0;
+    o.phi[r] = 0.0;
+    o.role[r] = g > 0.0 ? ZTP_RESIZE : ZTP_NORMAL;
+  }
+  *out = o;
+  return ZTP_OK;
+}
+
 extern "C" ztp_status ztp_plan_counts(const ztp_plan_t* p, int rank, int64_t K, int64_t n_units, int64_t unit,
                                       int is_row, ztp_counts* out) {
   if (!p || !out || rank < 0 || rank >= p->world || unit <= 0 || n_units < unit || n_units % unit != 0 || K < 1) {

@@ -151,6 +151,33 @@ def test_plan_errors(Z):
     assert ei.value.name == "ZTP_EINVAL"
 
 
+def test_plan_refine_matches_oracle(Z):
+    """ztp_plan_refine (A-39) bit-exact against the oracle on random ZERO
+    plan pairs; SEMI roles are rejected by both."""
+    import random
+    rng = random.Random(7)
+    for _ in range(300):
+        e = rng.randint(1, 8)
+        T1 = [rng.uniform(1, 3) for _ in range(e)]
+        T2 = [rng.uniform(1, 3) for _ in range(e)]
+        M = [rng.uniform(0.5, 2) for _ in range(e)]
+        kw = dict(zero_crit=rng.randint(0, 1), gamma_max=rng.choice([0.9, 1.0]))
+        zp1, zp2 = Z.ztp_plan(T1, M, 1.0, opts=Z.plan_opts(**kw)), Z.ztp_plan(T2, M, 1.0, opts=Z.plan_opts(**kw))
+        op1, op2 = O.plan(T1, M, 1.0, O.Costs(), O.PlanOpts(**kw)), O.plan(T2, M, 1.0, O.Costs(), O.PlanOpts(**kw))
+        zr = Z.ztp_plan_refine(zp1, zp2, kw["gamma_max"])
+        orf = O.plan_refine(op1, op2, kw["gamma_max"])
+        assert list(zr.role)[:e] == orf.role and zr.z == orf.z and list(zr.order)[:e] == orf.order
+        for r in range(e):
+            assert _bits(zr.gamma[r]) == _bits(orf.gamma[r]) and _bits(zr.gamma_r[r]) == _bits(orf.gamma_r[r])
+    lin = ((0.0, 1.0), (0.0, 1.0))
+    semi = Z.ztp_plan([10.0, 30.0], [10.0, 30.0], 100.0, Z.make_costs(0.0, lin, ((0.0, 1.0), (0.0, 0.0)), lin),
+                      Z.plan_opts(enable_migration=1))
+    assert semi.role[1] in (Z.MIGRATE, Z.SPLIT)
+    with pytest.raises(Z.ZtpError) as ei:
+        Z.ztp_plan_refine(semi, semi)
+    assert ei.value.name == "ZTP_EUNSUPPORTED"
+
+
 def test_no_cuda_device_is_an_error_not_a_fallback(Z):
     import torch
     if torch.cuda.is_available():

@@ -84,6 +84,40 @@ def test_zero_resizes_only_detected_stragglers_A38():
     assert p.gamma[:2] == [0.0, 0.0] and p.gamma[2] == pytest.approx((15.0 - T_avg) / 10.0, rel=1e-12)
 
 
+@pytest.mark.parametrize("seed", range(20))
+def test_refine_reaches_Tmin_under_resize_overhead_A39(seed):
+    """Eq.1 is exact for a rank whose GEMM time scales with the kept work
+    (T = C + chi m (1 - gamma)), so a first plan lands on T_min.  With a fixed
+    resize overhead kappa (select + compaction) the straggler overshoots by
+    kappa; ONE refresh on the resized window (A-39 composition) brings its
+    modelled runtime back to T_min exactly (algebra: keep = (1/chi)(1 - kappa/m))."""
+    rng = random.Random(seed)
+    e = rng.randint(2, 8)
+    s = rng.randrange(e)
+    m, C = rng.uniform(1, 10), rng.uniform(0, 5)
+    chi = rng.uniform(1.5, 3.0)
+    kappa = rng.uniform(0.05, 0.3) * m + 0.03 * (C + m)      # detectable (> eps T_min, A-17)
+    chis = [chi if r == s else 1.0 for r in range(e)]
+
+    def window(g):
+        T = [C + (kappa if g[r] > 0 else 0.0) + chis[r] * m * (1 - g[r]) for r in range(e)]
+        M = [chis[r] * m * (1 - g[r]) for r in range(e)]
+        return T, M
+
+    opts = O.PlanOpts(zero_crit=O.CRIT_MIN, gamma_max=1.0)
+    p1 = O.plan(*window([0.0] * e), 1.0, O.Costs(), opts)
+    assert p1.gamma[s] == pytest.approx(1 - 1 / chi, rel=1e-12)
+    T1, _ = window(p1.gamma_r)
+    assert T1[s] == pytest.approx(C + m + kappa, rel=1e-12)       # overshoot by the overhead
+    p2 = O.plan_refine(p1, O.plan(*window(p1.gamma_r), 1.0, O.Costs(), opts), 1.0)
+    T2, _ = window(p2.gamma_r)
+    assert T2[s] == pytest.approx(C + m, rel=1e-12)                # = T_min
+    assert [r for r in range(e) if p2.gamma[r] > 0] == [s]
+    # a further refresh finds no straggler and changes nothing
+    p3 = O.plan_refine(p2, O.plan(*window(p2.gamma_r), 1.0, O.Costs(), opts), 1.0)
+    assert p3.gamma == p2.gamma
+
+
 def test_eq2_worked_example_S572():
     g = golden("eq2_worked.json")
     c = O.Costs(g["omega1"], _costs_from(g, "omega2"), _costs_from(g, "phi1"), _costs_from(g, "phi2"))

@@ -18,7 +18,9 @@ Phases (each rank timed alone, same seeded inputs):
   unbal   chi on the straggler, dense; the statistics window gives T_i, M_i
           (A-5, A-6)
   bal     ztp_plan (ZERO with the T_min criterion, A-7; or SEMI) ->
-          layer_prune_counts -> ztp_select; chi kept.
+          layer_prune_counts -> ztp_select; chi kept.  Then up to REFRESH
+          statistics refreshes (P:178's 10% trigger, A-8): a new window with
+          the plan in effect, ztp_plan on it, ztp_plan_refine (A-39).
 Usage: CASES=c2:2:2,c2:4:2,c3:4:2,c4:8:2,c4:8:3s python tools/recovery_sim.py
 (cfg:e:chi, suffix s = SEMI plan with migration)."""
 import json
@@ -35,6 +37,7 @@ from synth.configs import CONFIGS  # noqa: E402
 import bench  # noqa: E402
 
 STEPS = int(os.environ.get("STEPS", "50"))
+REFRESH = int(os.environ.get("REFRESH", "3"))
 NVLINK_GBS = bench.NVLINK_GBS
 
 
@@ -109,6 +112,27 @@ def run_case(cfg_name, e, chi, semi):
     for r, L in enumerate(layers):
         L.set_selection(counts[r], scores[r])
     bal = [time_rank(L, ctxs[r], chis[r]) for r, L in enumerate(layers)]
+    # statistics refresh (A-8): a rank whose runtime moved > 10% since
+    # the window its plan came from triggers a new window; ZERO plans compose
+    # with the fresh Eq.1 ratio (ztp_plan_refine, A-39)
+    first = {"T_bal_ms": max(bal), "gamma": [round(g, 4) for g in list(plan.gamma)[:e]]}
+    refresh = []
+    T_last = T
+    for _ in range(REFRESH if not semi else 0):
+        if max(abs(bal[r] - T_last[r]) / T_last[r] for r in range(e)) <= 0.10:
+            break
+        M_cur = [gemm_ms(L, ctxs[r]) for r, L in enumerate(layers)]
+        fresh = Z.ztp_plan(bal, M_cur, float(u), None, Z.plan_opts(enable_migration=0, zero_crit=Z.CRIT_MIN))
+        if fresh.z == 0:
+            break
+        T_last = bal
+        plan = Z.ztp_plan_refine(plan, fresh)
+        counts = [layer_prune_counts(plan, r, h, a, u) for r in range(e)]
+        for r, L in enumerate(layers):
+            L.set_selection(counts[r], scores[r])
+        bal = [time_rank(L, ctxs[r], chis[r]) for r, L in enumerate(layers)]
+        refresh.append({"gamma": [round(g, 4) for g in list(plan.gamma)[:e]], "T_bal_ms": max(bal),
+                        "per_rank_ms": [round(x, 4) for x in bal]})
     t_comm = 4 * 2 * N * h * 2 * (e - 1) / e / (NVLINK_GBS * 1e9) * 1e3
     t_free, t_unbal, t_bal = max(free), max(T), max(bal)
     roles = "".join("NRMS"[int(x)] for x in list(plan.role)[:e])
@@ -122,7 +146,8 @@ def run_case(cfg_name, e, chi, semi):
            "recovery_with_comm": (t_free + t_comm) / (t_bal + t_comm),
            "speedup_with_comm": (t_unbal + t_comm) / (t_bal + t_comm),
            "per_rank_free_ms": [round(x, 4) for x in free], "per_rank_unbal_ms": [round(x, 4) for x in T],
-           "per_rank_bal_ms": [round(x, 4) for x in bal], "M_ms": [round(x, 4) for x in M]}
+           "per_rank_bal_ms": [round(x, 4) for x in bal], "M_ms": [round(x, 4) for x in M],
+           "first_plan": first, "refresh": refresh}
     for c in ctxs:
         Z.ztp_ctx_destroy(c)
     del layers
