@@ -293,6 +293,17 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     p.splits = c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, c->num_sms) : 1;
     if (p.splits > 1) {
       const int num_kb = (kdim + 63) / 64;
+      // dW: the K-slices of a tile as one cluster reduced through DSMEM
+      const int cs = ztp::gemm_cluster_splits(kind, epi, M, N, nk, p.splits, c->num_sms);
+      if (cs >= 2) p.splits = cs;
+      p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
+      p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
+      p.cs = (cs >= 2 && p.splits == cs) ? cs : 0;
+    }
+    if (p.splits > 1 && p.cs > 1) {
+      p.ws = nullptr;      // no workspace: partials never leave the cluster
+    } else if (p.splits > 1) {
+      const int num_kb = (kdim + 63) / 64;
       p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
       p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
       const size_t bytes = ztp::gemm_ws_bytes(kind, M, N, nk, p.splits);
@@ -314,7 +325,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.kb_per_split = (kdim + 63) / 64;
     }
     if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, c->num_sms, st));
-    if (p.splits > 1 || p.col_pos) ++c->launches;   // split-K reduce or column expansion
+    if ((p.splits > 1 && p.cs <= 1) || p.col_pos) ++c->launches;   // split-K reduce or column expansion
   } else {
     if (col_pos) return fail(c, ZTP_EUNSUPPORTED, "f32 path: output pruning");
     ztp::GemmParamsF32 p{};
@@ -872,13 +883,14 @@ ztp_status ztp_prepare(ztp_ctx* c, int n, const ztp_linear_args* const* args, co
   cudaStream_t st = (cudaStream_t)stream;
   ztp::GatherJobs J{};
   auto add = [&](const void* src, int64_t ld_src, const int32_t* rows, int nr, const int32_t* cols, int nc,
-                 const ztp_mat& dst) -> ztp_status {
+                 const ztp_mat& dst, int src_cols) -> ztp_status {
     if (J.njobs == ztp::GATHER_MAX_JOBS) return fail(c, ZTP_EINVAL, "ztp_prepare: more than 16 copies");
     if (!mat_ok(dst) || dst.rows < nr || dst.cols < nc || dst.dtype != ZTP_BF16)
       return fail(c, ZTP_ESHAPE, "ztp_prepare: destination " + shp("dst", dst) + " too small / not bf16");
     ztp::GatherJob& g = J.job[J.njobs++];
-    g = ztp::GatherJob{(const uint16_t*)src, ld_src, rows, cols, (uint16_t*)dst.ptr, dst.ld, nr, nc, J.total};
-    J.total += (int64_t)nr * ((nc + 7) / 8);
+    g = ztp::GatherJob{(const uint16_t*)src, ld_src, rows, cols, (uint16_t*)dst.ptr, dst.ld, nr, nc, J.total,
+                       src_cols};
+    J.total += nr;
     return ZTP_OK;
   };
   for (int i = 0; i < n; ++i) {
@@ -895,7 +907,7 @@ ztp_status ztp_prepare(ztp_ctx* c, int n, const ztp_linear_args* const* args, co
     if ((what[i] & 1) && !dense && !a->x_compact) {
       if (!mat_ok(a->x_t) || a->x_t.rows != K || a->x_t.dtype != ZTP_BF16)
         return fail(c, ZTP_ESHAPE, "ztp_prepare: " + shp("x_t", a->x_t));
-      s = add(a->x_t.ptr, a->x_t.ld, kept, nk, nullptr, (int)a->x_t.cols, a->xs_t);
+      s = add(a->x_t.ptr, a->x_t.ld, kept, nk, nullptr, (int)a->x_t.cols, a->xs_t, 0);
       if (s != ZTP_OK) return s;
     }
     if (what[i] & 2) {
@@ -903,9 +915,10 @@ ztp_status ztp_prepare(ztp_ctx* c, int n, const ztp_linear_args* const* args, co
       if (a->out_sel) {
         if ((int64_t)a->out_sel->n_kept + a->out_sel->n_pruned != n_out || !a->out_sel->kept)
           return fail(c, ZTP_ESHAPE, "ztp_prepare: out_sel does not cover n_out");
-        s = add(a->w_t.ptr, a->w_t.ld, dense ? nullptr : kept, nk, a->out_sel->kept, a->out_sel->n_kept, a->ws_t);
+        s = add(a->w_t.ptr, a->w_t.ld, dense ? nullptr : kept, nk, a->out_sel->kept, a->out_sel->n_kept, a->ws_t,
+                (int)n_out);
       } else if (!dense) {
-        s = add(a->w_t.ptr, a->w_t.ld, kept, nk, nullptr, (int)a->w_t.cols, a->ws_t);
+        s = add(a->w_t.ptr, a->w_t.ld, kept, nk, nullptr, (int)a->w_t.cols, a->ws_t, 0);
       }
       if (s != ZTP_OK) return s;
     }

@@ -183,8 +183,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;   // CTA rank in the pair
+  const uint32_t crank = (CG == 2 || p.cs > 1) ? cluster_ctarank() : 0u;   // rank in the cluster
+  const int rank = CG == 2 ? (int)(crank & 1u) : 0;                         // CTA rank in the pair
   const bool leader = rank == 0;
+  const uint16_t pmask = (uint16_t)(0x3u << (crank & ~1u));   // this pair's CTAs (commit multicast)
+  const int csplit = p.cs > 1 ? (int)crank / CG : 0;          // cluster split-K: this pair's K-slice
   const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
 
 
@@ -227,12 +230,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp, ~(unsigned long long)globaltimer());
 
   const Sched<KIND, C::TM> sc(p);
+  // persistent round-robin over work units; cluster split-K: exactly one unit,
+  // K-slice `csplit` of the cluster's tile
+  int u_first = pair, u_step = npairs;
+  if (p.cs > 1) {
+    u_first = csplit * sc.tiles_c + (int)(blockIdx.x / (CG * p.cs));
+    u_step = sc.num_units;
+  }
 
   if (warp == 0) {
     // ============================ TMA producer ============================
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = pair; u < sc.num_units; u += npairs) {
+    for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
       if (wk.zero) continue;
       const int am0 = wk.m0 + BM * rank;   // this CTA's 128 rows of the tile (A)
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int u = pair; u < sc.num_units; u += npairs) {
+    for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
       if (wk.zero) continue;
       mbar_wait(&tempty[acc], aphase ^ 1);
@@ -350,7 +360,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               umma_bf16(d_tmem, ad, bd, IDESC, accum);
           }
           if (CG == 2)
-            umma_commit_mc(&empty[stage], 0x3);
+            umma_commit_mc(&empty[stage], pmask);
           else
             umma_commit(&empty[stage]);
         }
@@ -362,7 +372,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (lane == 0) {
         if (CG == 2)
-          umma_commit_mc(&tfull[acc], 0x3);
+          umma_commit_mc(&tfull[acc], pmask);
         else
           umma_commit(&tfull[acc]);
       }
@@ -372,6 +382,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         aphase ^= 1;
       }
     }
+  } else if (warp >= 4 && p.cs > 1) {
+    // cluster split-K: this pair's K-slice is accumulated; reduced below
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
   } else if (warp >= 4) {
     // ============================ epilogue ================================
     const int ew = warp - 4;
@@ -396,7 +410,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         aphase ^= 1;
       }
     };
-    for (int u = pair; u < sc.num_units; u += npairs) {
+    for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
       const int m0 = wk.m0 + BM * rank, n0 = wk.n0;
       const bool zt = wk.zero;
@@ -559,6 +573,95 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
     if (lane < 8) bulk_wait0();   // all output writes performed before the CTA exits
+  }
+
+  if (p.cs > 1) {
+    // ============ cluster split-K reduce through distributed shared memory
+    // The S pairs of the cluster hold the S K-slice partials of one tile in
+    // TMEM.  The tile's 256 columns are 8 chunks of 32; chunk j is owned by
+    // split j % S.  Every CTA sends each chunk's fp32 partial (its 128 rows)
+    // to the same-half CTA of the owner, into slot [source split][chunk] of
+    // the owner's operand ring (idle once every slice is accumulated); the
+    // owner sums the S slots in split order 0..S-1 (fixed order: the result
+    // is deterministic), rounds to bf16 and stores its rows at the lineage
+    // row map (rows past n_kept hold exact zeros).
+    const int S = p.cs;
+    const int slots = (8 + S - 1) / S;
+    const int tile = (int)(blockIdx.x / (CG * S));
+    const int m0 = (tile % sc.mc) * C::TM + BM * rank;
+    const int n0 = (tile / sc.mc) * BN;
+    const uint32_t rbuf = smem_u32(ring);
+    const int ew = warp - 4, lq = ew & 3, ch = ew >> 2;
+    const uint32_t row_off = (uint32_t)(lq * 32 + lane) * 128u;
+    // #1: every slice of the cluster is accumulated (each epilogue waited its
+    // tfull before arriving): all rings are free to receive
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp >= 4) {
+      const uint32_t tb = tmem_base + ((uint32_t)(lq * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        const int j = ch * 4 + c;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tb + j * 32, v);
+        tmem_ld_wait();
+        const int owner = j % S, slot = j / S;
+        const uint32_t dst = mapa_shared(rbuf + (uint32_t)((csplit * slots + slot) * 128) * 128u + row_off,
+                                         (uint32_t)(owner * CG + rank));
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          st_cluster_v4(dst + ((uint32_t)(q ^ (lane & 7)) << 4), v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+    }
+    // #2: every slot delivered (cluster barrier release / acquire)
+    cluster_sync();
+    if (warp >= 4) {
+      const int m = m0 + lq * 32 + lane;
+      int orow = -1;
+      if (m < p.M) orow = p.out_dense ? m : (m < p.n_kept ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept)));
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        const int j = ch * 4 + c;
+        if (j % S != csplit) continue;
+        const int slot = j / S;
+        float a[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) a[i] = 0.f;
+#pragma unroll 1
+        for (int src = 0; src < S; ++src) {
+          const uint32_t base = rbuf + (uint32_t)((src * slots + slot) * 128) * 128u + row_off;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint4 x = ld_shared_v4(base + ((uint32_t)(q ^ (lane & 7)) << 4));
+            a[4 * q] += __uint_as_float(x.x);
+            a[4 * q + 1] += __uint_as_float(x.y);
+            a[4 * q + 2] += __uint_as_float(x.z);
+            a[4 * q + 3] += __uint_as_float(x.w);
+          }
+        }
+        if (orow >= 0 && !(p.dbg & 1)) {
+          __nv_bfloat16* o = p.out + (int64_t)orow * p.ld_out + n0 + j * 32;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int col = n0 + j * 32 + 8 * i;
+            if (col < p.N)
+              store_bf16x8(o + 8 * i,
+                           make_uint4(pack_bf16(a[8 * i], a[8 * i + 1]), pack_bf16(a[8 * i + 2], a[8 * i + 3]),
+                                      pack_bf16(a[8 * i + 4], a[8 * i + 5]), pack_bf16(a[8 * i + 6], a[8 * i + 7])),
+                           p.N - col);
+          }
+        }
+      }
+      // rows of fully pruned tiles: Zero, one warp per row over the grid
+      const int zr0 = sc.mc * C::TM;
+      const int gw = (int)blockIdx.x * EPI_WARPS + ew, nw = (int)gridDim.x * EPI_WARPS;
+      for (int zm = zr0 + gw; zm < p.M; zm += nw) {
+        const int zr = p.out_dense ? zm : __ldg(p.pruned + (zm - p.n_kept));
+        __nv_bfloat16* o = p.out + (int64_t)zr * p.ld_out;
+        for (int col = lane * 8; col < p.N; col += 256) store_bf16x8(o + col, make_uint4(0u, 0u, 0u, 0u), p.N - col);
+      }
+    }
   }
 
   tc_fence_before();
@@ -813,7 +916,7 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     attr_set = true;
   }
   const int units = units_of(KIND, CG, p);
-  const int pairs = std::min(units, num_sms / CG);
+  const int pairs = p.cs > 1 ? units : std::min(units, num_sms / CG);   // cluster split-K: one unit per pair
   if (pairs > 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(pairs * CG);
@@ -822,7 +925,7 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CG * (p.cs > 1 ? p.cs : 1);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -832,7 +935,7 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, mp.w, p);
     if (e != cudaSuccess) return e;
   }
-  if (p.splits == 1) {
+  if (p.splits == 1 || p.cs > 1) {
     if (p.col_pos)   // compact columns written by the epilogue: spread them, Zero the rest
       return expand_cols_launch(p.out, p.ld_out, p.out_rows, p.col_pos, p.N, p.n_full, st);
     return cudaSuccess;
@@ -865,6 +968,53 @@ int gemm_choose_splits(int kind, int M, int N, int kdim, int n_kept, int num_sms
   const int num_kb = (kdim + BK - 1) / BK;
   const int s = std::min((num_sms / cg) / tiles_c, num_kb / 16);  // each split keeps >= 1024 contraction elements
   return std::max(1, s);
+}
+
+// Cluster split-K (dW, no epilogue math): the `cs` K-slices of a tile run as
+// one cluster of CG x cs CTAs (<= 8, portable) and reduce through DSMEM.  It
+// needs every tile's cluster co-resident (one wave): checked against the
+// occupancy API for this kernel's shared memory.  Opt-in: ZTP_CSPLIT=1.
+int gemm_cluster_splits(int kind, int epi, int M, int N, int n_kept, int splits, int num_sms) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("ZTP_CSPLIT");
+    enabled = e ? atoi(e) != 0 : 0;   // measured slower in the step graph: opt-in
+  }
+  if (!enabled || kind != KIND_DW || epi != EPI_NONE || splits < 2) return 0;
+  const int cg = gemm_choose_cg(kind, M, n_kept);
+  const int tm = BM * cg;
+  const int m_tiles = (M + tm - 1) / tm, n_tiles = (N + BN - 1) / BN;
+  const int tiles_c = std::min(m_tiles, (n_kept + tm - 1) / tm) * n_tiles;
+  static int max_cl[3][9] = {};
+  for (int cs = std::min(splits, 8 / cg); cs >= 2; --cs) {
+    if (tiles_c * cs * cg > num_sms) continue;
+    int& mc = max_cl[cg][cs];
+    if (mc == 0) {
+      const int smem = cg == 2 ? Cfg<2>::TOTAL : Cfg<1>::TOTAL;
+      const void* kern = cg == 2 ? (const void*)ztp_gemm_kernel<KIND_DW, 2, false, false>
+                                 : (const void*)ztp_gemm_kernel<KIND_DW, 1, false, false>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cg * cs * 64);
+      cfg.blockDim = dim3(NUM_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cg * cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        n = -1;
+      }
+      mc = n > 0 ? n : -1;
+    }
+    if (mc > 0 && tiles_c <= mc) return cs;
+  }
+  return 0;
 }
 
 size_t gemm_ws_bytes(int kind, int M, int N, int n_kept, int splits) {
@@ -912,7 +1062,7 @@ cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_s
     ok &= make_map(&mp.o2, p.out2, p.out_rows, p.N, p.ld_out2, 64, dense_out ? 32 : 1);
   else
     mp.o2 = mp.o;
-  if (p.splits > 1) {
+  if (p.splits > 1 && p.cs <= 1) {
     const int64_t rows = kind == KIND_FWD ? p.M : std::min(p.M, p.n_kept);
     ok &= make_ws_map(&mp.w, p.ws, p.splits, rows, p.N, p.ld_ws);
   } else {

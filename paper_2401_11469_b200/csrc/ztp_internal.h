@@ -64,7 +64,13 @@ struct GemmParams {
   const int32_t* col_pos;  // DW output pruning: full column j <- compact column col_pos[j] (< 0: Zero)
   int n_full;              // full output columns when col_pos is set (N = compact columns)
   int pdl_late;            // inputs do not depend on the preceding kernel: PDL wait deferred to exit
+  int cs;                  // DW cluster split-K: the `splits` K-slices of a tile run as one cluster and
+                           // are reduced through distributed shared memory (no workspace, no reduce kernel)
 };
+// Cluster split-K choice for a dW launch with `splits` K-slices: the split
+// count to run as clusters (<= splits, cluster of cg x cs CTAs fits and every
+// tile gets a co-resident cluster), or 0 when the mode does not apply.
+int gemm_cluster_splits(int kind, int epi, int M, int N, int n_kept, int splits, int num_sms);
 
 // Split-K choice for a launch and the fp32 workspace it needs (bytes).
 int gemm_choose_splits(int kind, int M, int N, int kdim, int n_kept, int num_sms);
@@ -142,12 +148,13 @@ struct GatherJob {
   uint16_t* dst;
   int64_t ld_dst;
   int32_t n, nc;
-  int64_t vbegin;        // first 8-column vector of this job in the launch
+  int64_t rbegin;        // first row of this job in the launch's row space
+  int32_t src_cols;      // cols != NULL: logical width of the source rows (> every cols[c])
 };
 constexpr int GATHER_MAX_JOBS = 16;
 struct GatherJobs {
   int njobs;
-  int64_t total;         // vectors over all jobs
+  int64_t total;         // rows over all jobs
   GatherJob job[GATHER_MAX_JOBS];
 };
 cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st);

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "ztp_internal.h"
@@ -146,12 +147,27 @@ __global__ void ztp_gather_rows(const uint8_t* __restrict__ src, int64_t ld_src,
                                 int n, int64_t vec_per_row, uint8_t* __restrict__ dst, int64_t ld_dst) {
   pdl_wait();
   pdl_trigger();
+  constexpr int U = 4;   // independent vectors in flight per thread
   const int64_t total = (int64_t)n * vec_per_row;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / vec_per_row, c = i % vec_per_row;
-    const int64_t sr = __ldg(idx + r);
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + sr * ld_src) + c);
-    reinterpret_cast<uint4*>(dst + r * ld_dst)[c] = v;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < total; i0 += U * stride) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) {
+        const int64_t r = i / vec_per_row, c = i % vec_per_row;
+        v[u] = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)__ldg(idx + r) * ld_src) + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) {
+        const int64_t r = i / vec_per_row, c = i % vec_per_row;
+        reinterpret_cast<uint4*>(dst + r * ld_dst)[c] = v[u];
+      }
+    }
   }
 }
 
@@ -184,8 +200,8 @@ cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* i
                     (uint8_t*)dst, ld_dst * es);
   }
   const int64_t total = (int64_t)n * (row_bytes / 16);
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  int blocks = (int)((total + 1023) / 1024);
+  if (blocks > 148 * 8) blocks = 148 * 8;
   return launch_k(ztp_gather_rows, blocks, 256, 0, st, (const uint8_t*)src, ld_src * es, idx, n, row_bytes / 16,
                   (uint8_t*)dst, ld_dst * es);
 }
@@ -229,70 +245,134 @@ cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* row
                   ld_dst);
 }
 
-// Batched compaction of several operands (ztp_prepare): one launch, each
-// thread one 8-column (16-byte) output vector of some job.
-__global__ void ztp_gather_multi(const GatherJobs J) {
+// Batched compaction of several operands (ztp_prepare): one launch, one warp
+// per output row (rows of all jobs concatenated).  Row copies stream 16-byte
+// vectors, UNROLL in flight per lane.  2D jobs (a weight block W^T[S, S'],
+// output pruning) first stage the source row in the warp's shared-memory slot
+// with 16-byte loads, then pick the kept columns from shared memory, so HBM
+// sees only coalesced full-row reads.
+__global__ void ztp_gather_multi(const GatherJobs J, int slot_elems) {
   pdl_wait();
   pdl_trigger();
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < J.total; v += (int64_t)gridDim.x * blockDim.x) {
+  extern __shared__ __align__(16) uint16_t gm_slot[];
+  constexpr int UNROLL = 4;
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  uint16_t* slot = gm_slot + (int64_t)(threadIdx.x >> 5) * slot_elems;
+  const int64_t nw = (int64_t)gridDim.x * wpb;
+  for (int64_t row = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); row < J.total; row += nw) {
     int j = 0;
 #pragma unroll 1
-    while (j + 1 < J.njobs && v >= J.job[j + 1].vbegin) ++j;
+    while (j + 1 < J.njobs && row >= J.job[j + 1].rbegin) ++j;
     const GatherJob& g = J.job[j];
-    const int vpr = (g.nc + 7) / 8;
-    const int64_t local = v - g.vbegin;
-    const int r = (int)(local / vpr), c0 = (int)(local % vpr) * 8;
+    const int r = (int)(row - g.rbegin);
     const uint16_t* s = g.src + (int64_t)(g.rows ? __ldg(g.rows + r) : r) * g.ld_src;
-    uint16_t* d = g.dst + (int64_t)r * g.ld_dst + c0;
-    if (c0 + 8 <= g.nc) {
-      uint4 w;
-      if (g.cols) {
+    uint16_t* d = g.dst + (int64_t)r * g.ld_dst;
+    if (!g.cols) {
+      const int nv = g.nc / 8;
+      for (int v0 = lane; v0 < nv; v0 += 32 * UNROLL) {
+        uint4 w[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (v0 + 32 * u < nv) w[u] = __ldg(reinterpret_cast<const uint4*>(s) + v0 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (v0 + 32 * u < nv) reinterpret_cast<uint4*>(d)[v0 + 32 * u] = w[u];
+      }
+      for (int c = nv * 8 + lane; c < g.nc; c += 32) d[c] = __ldg(s + c);
+      continue;
+    }
+    const int sv = (g.src_cols + 7) / 8;            // source vectors staged (pitch is 16-byte padded)
+    for (int v0 = lane; v0 < sv; v0 += 32 * UNROLL) {
+      uint4 w[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (v0 + 32 * u < sv) w[u] = __ldg(reinterpret_cast<const uint4*>(s) + v0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (v0 + 32 * u < sv) reinterpret_cast<uint4*>(slot)[v0 + 32 * u] = w[u];
+    }
+    __syncwarp();
+    for (int c0 = lane * 8; c0 < g.nc; c0 += 256) {
+      if (c0 + 8 <= g.nc) {
         uint32_t q[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          q[k] = (uint32_t)__ldg(s + __ldg(g.cols + c0 + 2 * k)) |
-                 ((uint32_t)__ldg(s + __ldg(g.cols + c0 + 2 * k + 1)) << 16);
-        w = make_uint4(q[0], q[1], q[2], q[3]);
+          q[k] = (uint32_t)slot[__ldg(g.cols + c0 + 2 * k)] | ((uint32_t)slot[__ldg(g.cols + c0 + 2 * k + 1)] << 16);
+        *reinterpret_cast<uint4*>(d + c0) = make_uint4(q[0], q[1], q[2], q[3]);
       } else {
-        w = __ldg(reinterpret_cast<const uint4*>(s + c0));
+        for (int c = c0; c < g.nc; ++c) d[c] = slot[__ldg(g.cols + c)];
       }
-      *reinterpret_cast<uint4*>(d) = w;
-    } else {
-      for (int c = c0; c < g.nc; ++c) d[c - c0] = __ldg(s + (g.cols ? __ldg(g.cols + c) : c));
     }
+    __syncwarp();
   }
 }
 
 cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st) {
   if (j.total <= 0) return cudaSuccess;
-  int blocks = (int)((j.total + 255) / 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  return launch_k(ztp_gather_multi, blocks, 256, 0, st, j);
+  int slot = 0;                                   // elements per warp slot (largest 2D source row)
+  for (int i = 0; i < j.njobs; ++i) {
+    const GatherJob& g = j.job[i];
+    if ((reinterpret_cast<uintptr_t>(g.src) & 15) || (reinterpret_cast<uintptr_t>(g.dst) & 15) || g.ld_src % 8 ||
+        g.ld_dst % 8)
+      return cudaErrorMisalignedAddress;
+    if (g.cols) {
+      if (g.src_cols <= 0 || (g.src_cols + 7) / 8 * 8 > g.ld_src) return cudaErrorInvalidValue;
+      slot = std::max(slot, (g.src_cols + 7) / 8 * 8);
+    }
+  }
+  int wpb = 8;
+  while (wpb > 1 && (size_t)wpb * slot * 2 > 96 * 1024) wpb >>= 1;
+  const size_t smem = (size_t)wpb * slot * 2;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  static size_t max_set = 48 * 1024;
+  if (smem > max_set) {
+    cudaError_t e = cudaFuncSetAttribute(ztp_gather_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    max_set = smem;
+  }
+  const int64_t need = (j.total + wpb - 1) / wpb;
+  const int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / std::max<size_t>(smem, 1))));
+  const int blocks = (int)std::min<int64_t>(need, (int64_t)148 * per_sm);
+  return launch_k(ztp_gather_multi, blocks, 32 * wpb, smem, st, j, slot);
 }
 
 // In-place column expansion (output pruning, bf16): row r of t holds nc
 // compact columns; afterwards t[r, j] = pos[j] >= 0 ? old[r, pos[j]] : 0 for
-// j < n_full (the Zero gradient of the consumer-pruned units).  One CTA
-// per row at a time: the compact row is staged in shared memory first, so the
-// in-place overwrite never reads a written element.
-__global__ void ztp_expand_cols(uint16_t* t, int64_t ld, int n, const int32_t* __restrict__ pos, int nc, int n_full) {
+// j < n_full (the Zero gradient of the consumer-pruned units).  One
+// warp per row: the compact row is staged in the warp's shared-memory slot
+// with 16-byte loads first, so the in-place overwrite never reads a written
+// element; several rows per CTA are in flight at once.
+__global__ void ztp_expand_cols(uint16_t* t, int64_t ld, int n, const int32_t* __restrict__ pos, int nc, int n_full,
+                                int row_slot, int pos_vec) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ uint16_t row[];
-  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+  extern __shared__ __align__(16) uint16_t rows_s[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  uint16_t* row = rows_s + (int64_t)w * row_slot;
+  const int nv = nc / 8;
+  for (int r = blockIdx.x * wpb + w; r < n; r += gridDim.x * wpb) {
     uint16_t* p = t + (int64_t)r * ld;
-    for (int c = threadIdx.x; c < nc; c += blockDim.x) row[c] = p[c];
-    __syncthreads();
-    for (int j0 = threadIdx.x * 8; j0 < n_full; j0 += blockDim.x * 8) {
+    for (int c = lane; c < nv; c += 32)
+      reinterpret_cast<uint4*>(row)[c] = reinterpret_cast<const uint4*>(p)[c];
+    for (int c = nv * 8 + lane; c < nc; c += 32) row[c] = p[c];
+    __syncwarp();
+    for (int j0 = lane * 8; j0 < n_full; j0 += 256) {
       if (j0 + 8 <= n_full) {
-        auto g = [&](int j) -> uint32_t {
-          const int q = __ldg(pos + j);
-          return q >= 0 ? (uint32_t)row[q] : 0u;
-        };
-        uint32_t w[4];
+        int q[8];
+        if (pos_vec) {
+          const int4 q0 = __ldg(reinterpret_cast<const int4*>(pos + j0));
+          const int4 q1 = __ldg(reinterpret_cast<const int4*>(pos + j0 + 4));
+          q[0] = q0.x, q[1] = q0.y, q[2] = q0.z, q[3] = q0.w, q[4] = q1.x, q[5] = q1.y, q[6] = q1.z, q[7] = q1.w;
+        } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) w[q] = g(j0 + 2 * q) | (g(j0 + 2 * q + 1) << 16);
-        *reinterpret_cast<uint4*>(p + j0) = make_uint4(w[0], w[1], w[2], w[3]);
+          for (int k = 0; k < 8; ++k) q[k] = __ldg(pos + j0 + k);
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          o[k] = (q[2 * k] >= 0 ? (uint32_t)row[q[2 * k]] : 0u) |
+                 ((q[2 * k + 1] >= 0 ? (uint32_t)row[q[2 * k + 1]] : 0u) << 16);
+        *reinterpret_cast<uint4*>(p + j0) = make_uint4(o[0], o[1], o[2], o[3]);
       } else {
         for (int j = j0; j < n_full; ++j) {
           const int q = __ldg(pos + j);
@@ -300,23 +380,29 @@ __global__ void ztp_expand_cols(uint16_t* t, int64_t ld, int n, const int32_t* _
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
 cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, int nc, int n_full, cudaStream_t st) {
   if (n <= 0 || n_full <= 0) return cudaSuccess;
-  if ((reinterpret_cast<uintptr_t>(t) & 15) != 0 || ld % 8 != 0)
-    return cudaErrorMisalignedAddress;
-  const size_t smem = (size_t)nc * 2;
+  if ((reinterpret_cast<uintptr_t>(t) & 15) != 0 || ld % 8 != 0) return cudaErrorMisalignedAddress;
+  const int pos_vec = (reinterpret_cast<uintptr_t>(pos) & 15) == 0;
+  const int row_slot = (nc + 7) / 8 * 8;                    // elements per warp slot (16-byte multiple)
+  int wpb = 8;
+  while (wpb > 1 && (size_t)wpb * row_slot * 2 > 96 * 1024) wpb >>= 1;
+  const size_t smem = (size_t)wpb * row_slot * 2;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static int max_set = 48 * 1024;
   if ((int)smem > max_set) {
     cudaError_t e = cudaFuncSetAttribute(ztp_expand_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     max_set = (int)smem;
   }
-  const int blocks = n < 148 * 8 ? n : 148 * 8;
-  return launch_k(ztp_expand_cols, blocks, 256, smem, st, (uint16_t*)t, ld, n, pos, nc, n_full);
+  const int need = (n + wpb - 1) / wpb;
+  const int blocks = need < 148 * 4 ? need : 148 * 4;
+  return launch_k(ztp_expand_cols, blocks, 32 * wpb, smem, st, (uint16_t*)t, ld, n, pos, nc, n_full, row_slot,
+                  pos_vec);
 }
 
 // ------------------------------------------ Average / Same imputation (NEXT-2)

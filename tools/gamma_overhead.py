@@ -54,22 +54,21 @@ def run():
             per.append(Z.ztp_launch_count(ctx) - k0)
         torch.cuda.synchronize()
         meta.append({"gamma": g, "launches_before": n0, "per_step": per, "nk": dict(L.nk)})
-    json.dump({"cfg": CFG, "tp": TP, "meta": meta}, open("gpurun_out/gov_meta.json", "w"), indent=1)
+    json.dump({"cfg": CFG, "tp": TP, "meta": meta}, open(f"gpurun_out/gov_meta_{CFG}_{TP}.json", "w"), indent=1)
     Z.ztp_ctx_destroy(ctx)
 
 
 def parse(csv_path, out_path):
-    meta = json.load(open("gpurun_out/gov_meta.json"))
+    meta = json.load(open(f"gpurun_out/gov_meta_{CFG}_{TP}.json"))
     rows = [r for r in csv.DictReader(l for l in open(csv_path) if l.startswith('"'))
             if r.get("Metric Name") == "gpu__time_duration.sum"]
-    names = [(r["Kernel Name"], float(r["Metric Value"]) / (1e3 if r["Metric Unit"] == "nsecond" else 1.0))
+    names = [(r["Kernel Name"], float(r["Metric Value"]) / (1e3 if r["Metric Unit"] in ("nsecond", "ns") else 1.0))
              for r in rows]
     # ncu counts select/launch order exactly as ztp_launch_count (one ztp kernel per count)
     idx = 0
     out = []
-    first = meta["meta"][0]["launches_before"]
     for m in meta["meta"]:
-        start = m["launches_before"] - first + sum(m["per_step"][:-1])
+        start = m["launches_before"] + sum(m["per_step"][:-1])     # ncu index == library launch count
         n = m["per_step"][-1]
         ks = names[start:start + n]
         out.append({"gamma": m["gamma"], "nk": m["nk"], "total_us": sum(t for _, t in ks),
