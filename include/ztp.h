@@ -339,6 +339,15 @@ double ztp_pridiff_gamma(int64_t L, int64_t L_uni, double gamma_t, double alpha)
  * n <= 16 copies in total.  Errors: EINVAL, ESHAPE, EUNSUPPORTED (f32). */
 ztp_status ztp_prepare(ztp_ctx* ctx, int n, const ztp_linear_args* const* args, const int32_t* what, void* stream);
 
+/* ztp_join: make `stream` wait for the library's internal side-stream work.
+ * With ZTP_CONC=1 a BWD call runs its dW GEMM on an internal stream
+ * concurrently with the dX GEMM (the SMs split in proportion to their work)
+ * and returns without joining it, so the next linear's dX is not held back;
+ * call ztp_join before reading dW on `stream` (a FWD call and ztp_migrate
+ * join automatically; a step captured in a CUDA graph must end with it).
+ * Errors: ZTP_EINVAL (null ctx), ZTP_ECUDA. */
+ztp_status ztp_join(ztp_ctx* ctx, void* stream);
+
 ztp_status ztp_col_linear(ztp_ctx* ctx, ztp_phase phase, const ztp_linear_args* a, void* stream);
 ztp_status ztp_row_linear(ztp_ctx* ctx, ztp_phase phase, const ztp_linear_args* a, void* stream);
 

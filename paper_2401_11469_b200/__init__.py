@@ -18,7 +18,7 @@ from ._lib import (ACT_GELU, ACT_GELU_D, ACT_NONE, BF16, BWD, CRIT_AVG, CRIT_MIN
 
 __all__ = [
     "ztp_version", "ztp_get_unique_id", "ztp_ctx_create", "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count",
-    "ztp_plan", "ztp_plan_refine", "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
+    "ztp_plan", "ztp_plan_refine", "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_join", "ztp_col_linear", "ztp_row_linear",
     "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "mat",
     "make_costs", "plan_opts", "ZtpError",
 ]
@@ -133,6 +133,12 @@ def ztp_allgather_stats(ctx, T_own: float, M_own: float, world: int, stream=None
 
 
 # ------------------------------------------------------------------ device calls
+
+def ztp_join(ctx, stream=None) -> None:
+    """Order the library's side-stream work (concurrent dW, ZTP_CONC) before
+    later work on `stream`."""
+    check(lib.ztp_join(ctx, _stream(stream)), ctx)
+
 
 def ztp_select(ctx, seg_len: Sequence[int], n_prune: Sequence[int], scores, kept, pruned,
                append: Optional[Sequence[int]] = None, pos=None, stream=None) -> None:

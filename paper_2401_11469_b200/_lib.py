@@ -117,6 +117,7 @@ def _load():
                                      C.POINTER(C.c_double), vp]),
         "ztp_select": (st, [vp, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                             vp, vp, vp, vp, vp]),
+        "ztp_join": (st, [vp, vp]),
         "ztp_col_linear": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
         "ztp_row_linear": (st, [vp, C.c_int, C.POINTER(LinearArgs), vp]),
         "ztp_core": (st, [vp, C.c_int, C.POINTER(Mat), C.POINTER(Mat), C.c_int64, C.c_int64, vp, C.c_int64,
@@ -145,7 +146,7 @@ lib = _load()
 # every symbol include/ztp.h declares (checked by tests/test_abi.py)
 EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_id", "ztp_ctx_create",
             "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count", "ztp_plan_opts_default", "ztp_plan", "ztp_plan_refine",
-            "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_col_linear", "ztp_row_linear",
+            "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_join", "ztp_col_linear", "ztp_row_linear",
             "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "ztp_prepare",
             "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",
             "ztp_set_profile", "ztp_read_profile")

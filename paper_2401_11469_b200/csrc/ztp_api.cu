@@ -36,7 +36,9 @@ struct ztp_ctx {
   // are independent), so the two small-output GEMMs share the SMs
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_c = nullptr, ev_d = nullptr;
-  int conc_bwd = 0;                    // ZTP_CONC=1: dW on the side stream (measured: no gain)
+  int conc_bwd = 1;                    // ZTP_CONC (default 1): dW on the side stream, the SMs split by work
+  int sm_cap = 0;                      // > 0: SMs a GEMM launch may use (concurrent dX / dW partition)
+  bool side_pending = false;           // side-stream work not yet joined into a caller stream
   void* skws_side = nullptr;           // split-K partials of side-stream GEMMs
   size_t skws_side_cap = 0;
   std::string err;
@@ -290,11 +292,12 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.prof_stamp = c->d_pstamp + 2 * (c->pstamp_used++);
     }
     // split-K over the contraction when the output has too few tiles for 148 SMs
-    p.splits = c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, c->num_sms) : 1;
+    const int nsm = c->sm_cap > 0 ? c->sm_cap : c->num_sms;
+    p.splits = c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, nsm) : 1;
     if (p.splits > 1) {
       const int num_kb = (kdim + 63) / 64;
       // dW: the K-slices of a tile as one cluster reduced through DSMEM
-      const int cs = ztp::gemm_cluster_splits(kind, epi, M, N, nk, p.splits, c->num_sms);
+      const int cs = ztp::gemm_cluster_splits(kind, epi, M, N, nk, p.splits, nsm);
       if (cs >= 2) p.splits = cs;
       p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
       p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
@@ -324,7 +327,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.splits = 1;
       p.kb_per_split = (kdim + 63) / 64;
     }
-    if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, c->num_sms, st));
+    if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, nsm, st));
     if ((p.splits > 1 && p.cs <= 1) || p.col_pos) ++c->launches;   // split-K reduce or column expansion
   } else {
     if (col_pos) return fail(c, ZTP_EUNSUPPORTED, "f32 path: output pruning");
@@ -498,8 +501,21 @@ ztp_status operand_src(ztp_ctx* c, bool dense_sel, bool caller_compact, const zt
   return ZTP_OK;
 }
 
+ztp_status join_side(ztp_ctx* c, cudaStream_t st) {
+  if (c->side_pending) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_d, c->side_stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_d, 0));
+    c->side_pending = false;
+  }
+  return ZTP_OK;
+}
+
 ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args* a, cudaStream_t st) {
   if (!c || !a) return fail(c, ZTP_EINVAL, "linear: null ctx/args");
+  if (phase == ZTP_FWD) {
+    ztp_status js = join_side(c, st);   // a new step: earlier concurrent dW work is ordered before it
+    if (js != ZTP_OK) return js;
+  }
   const char* nm = layer == LAYER_COL ? "ztp_col_linear" : "ztp_row_linear";
   if (!mat_ok(a->w_t)) return fail(c, ZTP_ESHAPE, std::string(nm) + ": bad " + shp("w_t", a->w_t));
   const int64_t K = a->w_t.rows;
@@ -586,12 +602,26 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
   // dW concurrently with dX on the side stream (not while emulating a
   // straggler -- the slowdown stamps one GEMM at a time -- nor while profiling,
   // which times each GEMM alone)
-  const bool conc = c->conc_bwd && c->prof_on != 1 && a->dx_t.ptr && a->dw_t.ptr && !emulating(c);
+  const bool conc = c->conc_bwd && c->prof_on != 1 && a->dx_t.ptr && a->dw_t.ptr && !emulating(c) &&
+                    dtype == ZTP_BF16;
   cudaStream_t sw = st;
+  int cap_dx = 0, cap_dw = 0;
   if (conc) {
     CUDA_TRY(c, cudaEventRecord(c->ev_c, st));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_c, 0));
     sw = c->side_stream;
+    // partition the SMs (in CTA pairs) in proportion to the two GEMMs' MMA
+    // work (tiles x 64-deep k-blocks), so both run at once and each one's
+    // fill and tail overlap the other's mainloop
+    const double rows = (double)std::min<int64_t>(nk, dxc ? nk : K);
+    const double t_rows = std::ceil(rows / 256.0);
+    const double w_dx = t_rows * std::ceil((double)N / 256.0) * std::ceil((double)n_y / 64.0);
+    const double w_dw = t_rows * std::ceil((double)n_y / 256.0) * std::ceil((double)N / 64.0);
+    const int pairs = c->num_sms / 2;
+    int px = (int)std::lround(pairs * w_dx / (w_dx + w_dw));
+    px = std::max(1, std::min(pairs - 1, px));
+    cap_dx = 2 * px;
+    cap_dw = 2 * (pairs - px);
   }
   if (a->dx_t.ptr) {
     if (!mat_ok(a->dx_t) || (dxc ? a->dx_t.rows < nk : a->dx_t.rows != K) || a->dx_t.cols != N ||
@@ -615,8 +645,10 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     if (s != ZTP_OK) return s;
     ztp_mat dx = a->dx_t;
     if (dxc) dx.rows = nk;   // rows P implied Zero, not written
+    c->sm_cap = cap_dx;
     s = gemm(c, ztp::KIND_DX, W, Src{&g, true}, n_y, kept, dxc ? nullptr : pruned, nk, dx, nullptr, aux, xc ? 1 : 0,
              nullptr, epi, st, dxc);
+    c->sm_cap = 0;
     if (s != ZTP_OK) return s;
     // Average / Same on this rank's partial, before the all-reduce (A-14)
     if (!dense_sel) s = impute(c, a->impute, a->dx_t, N, kept, nk, pruned, np, a->hist_dx, st);
@@ -643,18 +675,20 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     const bool copied = c->launches != l0;   // a compaction kernel now precedes the dW GEMM
     // output pruning: the GEMM computes the compact columns S'; its split-K
     // reduce (or an expansion pass) spreads them to their units, P' <- Zero
+    c->sm_cap = cap_dw;
     s = gemm(c, ztp::KIND_DW, X, Src{&g, true}, n_y, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
              ztp::EPI_NONE, sw, false, os ? a->y_pos : nullptr, (int)n_out,
              /*indep_of_prev=*/a->dx_t.ptr != nullptr && !copied && !conc && !reduce_dx &&
                  a->impute == ZTP_IMPUTE_ZERO);
+    c->sm_cap = 0;
     if (s != ZTP_OK) return s;
     if (!dense_sel) s = impute(c, a->impute, a->dw_t, n_out, kept, nk, pruned, np, a->hist_dw, sw);
     if (s != ZTP_OK) return s;
   }
-  if (conc) {
-    CUDA_TRY(c, cudaEventRecord(c->ev_d, sw));
-    CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_d, 0));
-  }
+  // the dW outputs feed nothing later in the step: the side stream is joined
+  // by ztp_join (or the next FWD call), not here, so the next linear's dX
+  // does not wait for this dW
+  if (conc) c->side_pending = true;
   if (reduce_dx) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_b, 0));
   return ZTP_OK;
 }
@@ -931,6 +965,11 @@ ztp_status ztp_prepare(ztp_ctx* c, int n, const ztp_linear_args* const* args, co
   return ZTP_OK;
 }
 
+ztp_status ztp_join(ztp_ctx* c, void* stream) {
+  if (!c) return fail(c, ZTP_EINVAL, "ztp_join: null ctx");
+  return join_side(c, (cudaStream_t)stream);
+}
+
 ztp_status ztp_col_linear(ztp_ctx* c, ztp_phase phase, const ztp_linear_args* a, void* stream) {
   return linear(c, LAYER_COL, phase, a, (cudaStream_t)stream);
 }
@@ -1002,6 +1041,10 @@ ztp_status ztp_core(ztp_ctx* c, ztp_phase phase, const ztp_mat* qkv, const ztp_m
 ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
   if (!c || (n > 0 && !xs)) return fail(c, ZTP_EINVAL, "ztp_migrate: null argument");
   cudaStream_t st = (cudaStream_t)stream;
+  {
+    ztp_status js = join_side(c, st);   // returned dW slices must be complete
+    if (js != ZTP_OK) return js;
+  }
   std::vector<size_t> off(n, 0);
   size_t total = 0;
   for (int i = 0; i < n; ++i) {

@@ -375,6 +375,7 @@ class ZtpLayer:
         else:
             Z.ztp_core(c, Z.BWD, self.gQKV, self.dctx, self.a, self.a, None, 0, stream)
         Z.ztp_col_linear(c, Z.BWD, self.b_qkv, stream)        # dX (+ all-reduce), dWqkv
+        Z.ztp_join(c, stream)                                  # concurrent dW work (ZTP_CONC) ends the step
 
     def forward(self, stream=None):
         self.fwd_attn(stream)
