@@ -1,0 +1,205 @@
+"""Alg.2 l.1 "pretestDiffRatio(Omega_1, Omega_2, Phi_1)":
+measure, before training, the cost functions Eq.2 / Eq.3 weigh against each
+other, and hand them to ztp_plan as a ztp_costs (piecewise linear, SURVEY
+§8(a) row a2, §8(d) timing protocol step 6).
+
+  Omega_1     "static space allocation overhead for the submatrix with
+              reduced dimensions": the extra non-GEMM time a step
+              pays as soon as it resizes at all (select, compaction copies,
+              imputation launches) -- measured at the smallest ratio.
+  Omega_2(n)  "proportionally increased dimension extracting cost" of n
+              pruned units: the extra non-GEMM time at n = L gamma pruned
+              units, minus Omega_1.
+  Phi_1(n)    "communication cost" of migrating n units: the weight
+              slices out (W1^T columns, W2^T rows) and the dW slices back,
+              per step, through ztp_migrate.
+  Phi_2(m)    "computation cost" on a helper of m received units (P:258,
+              P:280 infers it from the receiver's speed): measured directly
+              as the step-time increase of a rank that appends m units.
+
+x axes are MLP hidden units (L = u, the rank's FFN units, A-25); times are
+milliseconds, the unit of the statistics T / M the plan receives.  Every
+sample comes from CUDA-graph replays of the rank's real step through the C
+ABI (select + GEMMs + epilogues), so the functions carry this box's fixed
+costs, not a model.
+
+Only host orchestration lives here (timing, sample bookkeeping); all work
+runs in libztp.so.  The pure-host part (`fit_costs`) is unit-tested on CPU.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import paper_2401_11469_b200 as Z
+
+GAMMAS = (0.0, 0.125, 0.25, 0.5, 0.75)
+FRACS = (0.0, 0.125, 0.25, 0.5, 1.0)
+
+
+def _monotone(points: Sequence[Tuple[float, float]]) -> Tuple[Tuple[float, ...], Tuple[float, ...]]:
+    """Samples -> a non-decreasing piecewise-linear function through (0, 0):
+    x ascending, duplicates dropped, y clamped at 0 and made non-decreasing
+    (running max) -- a cost cannot shrink when more units are moved or pruned,
+    so a dip is timing noise."""
+    pts = sorted((float(x), float(y)) for x, y in points)
+    xs, ys = [0.0], [0.0]
+    for x, y in pts:
+        if x <= xs[-1]:
+            continue
+        xs.append(x)
+        ys.append(max(ys[-1], y, 0.0))
+    if len(xs) < 2:                      # ztp_pwl needs >= 2 samples
+        xs.append(1.0)
+        ys.append(0.0)
+    return tuple(xs), tuple(ys)
+
+
+def fit_costs(omega: Sequence[Tuple[float, float]], phi1: Sequence[Tuple[float, float]],
+              phi2: Sequence[Tuple[float, float]]):
+    """Raw pretest samples -> (ztp_costs keepalive tuple, plain dict).
+    omega: (pruned units n, extra non-GEMM ms vs the dense step) for n >= 0;
+    Omega_1 = the extra at the smallest n > 0, Omega_2(n) = extra(n) - Omega_1
+    (a static part plus a part proportional to the pruned data).
+    phi1: (migrated units, ms); phi2: (units received by one helper, ms)."""
+    pos = sorted((x, y) for x, y in omega if x > 0)
+    omega1 = max(pos[0][1], 0.0) if pos else 0.0
+    o2 = _monotone([(x, y - omega1) for x, y in pos])
+    p1 = _monotone(phi1)
+    p2 = _monotone(phi2)
+    plain = {"omega1": omega1, "omega2": o2, "phi1": p1, "phi2": p2}
+    return Z.make_costs(omega1, o2, p1, p2), plain
+
+
+# ----------------------------------------------------------------- GPU side
+def time_step(L, ctx, chi: float = 1.0, steps: int = 30, reps: int = 3) -> float:
+    """Median over `reps` of the mean replay time (ms) of one captured step."""
+    import torch
+    stream = torch.cuda.Stream()
+    Z.ztp_set_slowdown(ctx, chi)
+    L.step(stream)
+    torch.cuda.synchronize()
+    g = L.capture(stream)
+    for _ in range(3):
+        g.replay()
+    out = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1) / steps)
+    del g
+    out.sort()
+    return out[len(out) // 2]
+
+
+def gemm_ms(L, ctx, steps: int = 5) -> float:
+    """M (A-6): GEMM (+ emulated delay) time per step from the kernels' own
+    stamps (statistics mode)."""
+    Z.ztp_set_stats(ctx, True)
+    Z.ztp_read_gemm_ns(ctx)
+    for _ in range(steps):
+        L.step()
+    m = Z.ztp_read_gemm_ns(ctx) / steps / 1e6
+    Z.ztp_set_stats(ctx, False)
+    return m
+
+
+def _homog_counts(L, g: float) -> Dict[str, int]:
+    """A-3 rounding, A-4 (at least one kept) of one ratio on all four linears."""
+    out = {}
+    for s in ("qkv", "o", "fc1", "fc2"):
+        K = {"qkv": L.h, "o": L.a, "fc1": L.h, "fc2": L.u}[s]
+        out[s] = min(int(K * g + 0.5), K - 1)
+    return out
+
+
+def pretest(L, ctx, scores: Dict, *, gammas: Sequence[float] = GAMMAS, fracs: Sequence[float] = FRACS,
+            steps: int = 30, peer: Optional[int] = None, link_gbs: Optional[float] = None, ctx_rank: int = 0):
+    """Run the pretest on this rank's layer `L` (a ZtpLayer built with
+    mig_cap >= L.u * max(fracs)) and return (costs, report).
+
+    peer: the rank Phi_1's copies go to (None: local device copies on this
+    GPU -- the one-GPU stand-in); ctx_rank: the rank of `ctx` (ztp_migrate
+    acts on transfers naming it).  link_gbs: if given, Phi_1 is
+    additionally modelled as bytes / link_gbs + the measured per-call fixed
+    cost, and the MODEL is what the returned costs use (a one-GPU run cannot
+    time NVLink; report["phi1_measured"] keeps the local copies).
+    The layer is left dense, without migration."""
+    import torch
+    from paper_2401_11469_b200.layer import MigrationIO
+
+    u, h = L.u, L.h
+    rep: Dict[str, List] = {"omega": [], "phi1_measured": [], "phi2": []}
+    L.set_migration(MigrationIO())
+    # ---- Omega: extra non-GEMM time of a resized step (gamma sweep)
+    base = None
+    for g in sorted(set([0.0] + list(gammas))):
+        L.set_selection(_homog_counts(L, g), scores)
+        T = time_step(L, ctx, 1.0, steps)
+        M = gemm_ms(L, ctx)
+        over = T - M
+        if base is None:
+            base = over
+        n = L.n_prune["fc2"]
+        rep["omega"].append({"gamma": g, "n_pruned": n, "T_ms": T, "M_ms": M, "extra_ms": over - base})
+    # ---- Phi_2: a helper appending m units (merged accumulation, A-26)
+    L.set_selection(_homog_counts(L, 0.0), scores)
+    t0 = None
+    src = (L.rank + 1) % max(L.world, 2)
+    for fr in sorted(set([0.0] + list(fracs))):
+        m = int(u * fr + 0.5)
+        if m > L.cap:
+            continue
+        L.set_migration(MigrationIO(inc=[(src, 0, m)] if m > 0 else []))
+        L.set_selection(_homog_counts(L, 0.0), scores)
+        T = time_step(L, ctx, 1.0, steps)
+        if t0 is None:
+            t0 = T
+        rep["phi2"].append({"units": m, "T_ms": T, "extra_ms": T - t0})
+    L.set_migration(MigrationIO())
+    L.set_selection(_homog_counts(L, 0.0), scores)
+    # ---- Phi_1: weight slices out + dW slices back for n units
+    dst = ctx_rank if peer is None else peer
+    stream = torch.cuda.Stream()
+    fixed = None
+    for fr in sorted(set(list(fracs))):
+        n = int(u * fr + 0.5)
+        if n == 0 or n > L.cap:
+            continue
+        xs = []
+        for t_src, t_dst, r0, c0, nr, nc, dr0, dc0 in (
+                (L.w1_t, L.w1_t, 0, 0, h, n, 0, u), (L.w2_t, L.w2_t, 0, 0, n, h, u, 0),
+                (L.dw1, L.dw1, 0, u, h, n, 0, 0), (L.dw2, L.dw2, u, 0, n, h, 0, 0)):
+            xs.append(Z.xfer(t_src, t_dst, r0=r0, c0=c0, nr=nr, nc=nc, dr0=dr0, dc0=dc0,
+                             src_rank=ctx_rank, dst_rank=dst))
+        for _ in range(3):
+            Z.ztp_migrate(ctx, xs, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(reps):
+                Z.ztp_migrate(ctx, xs, stream)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        nbytes = 4 * n * h * L.w1_t.element_size()
+        rep["phi1_measured"].append({"units": n, "ms": ms, "bytes": nbytes})
+        fixed = ms if fixed is None else min(fixed, ms)
+    if link_gbs:
+        # bandwidth model over the link, with the smallest measured call as
+        # its fixed cost (launch + latency), never below the measured copy
+        rep["phi1"] = [{"units": d["units"], "ms": max(d["ms"], 0.5 * fixed + d["bytes"] / (link_gbs * 1e9) * 1e3),
+                        "model": f"bytes / {link_gbs} GB/s + fixed"} for d in rep["phi1_measured"]]
+    else:
+        rep["phi1"] = rep["phi1_measured"]
+    costs, plain = fit_costs([(d["n_pruned"], d["extra_ms"]) for d in rep["omega"]],
+                             [(d["units"], d["ms"]) for d in rep["phi1"]],
+                             [(d["units"], d["extra_ms"]) for d in rep["phi2"]])
+    rep["costs"] = plain
+    return costs, rep

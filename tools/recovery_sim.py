@@ -35,6 +35,7 @@ import paper_2401_11469_b200 as Z  # noqa: E402
 from paper_2401_11469_b200.layer import ZtpLayer, migration_io, layer_prune_counts, SEGS  # noqa: E402
 from synth.configs import CONFIGS  # noqa: E402
 import bench  # noqa: E402
+from paper_2401_11469_b200.pretest import pretest  # noqa: E402
 
 STEPS = int(os.environ.get("STEPS", "50"))
 REFRESH = int(os.environ.get("REFRESH", "3"))
@@ -99,7 +100,13 @@ def run_case(cfg_name, e, chi, semi):
     free = [time_rank(L, ctxs[r], 1.0) for r, L in enumerate(layers)]
     T = [time_rank(L, ctxs[r], chis[r]) for r, L in enumerate(layers)]
     M = [gemm_ms(L, ctxs[r]) for r, L in enumerate(layers)]
-    plan = Z.ztp_plan(T, M, float(u), None, Z.plan_opts(enable_migration=1 if semi else 0, zero_crit=Z.CRIT_MIN))
+    costs, pre = None, None
+    if semi:
+        # Alg.2 l.1 pretest on a non-straggling rank (Phi_1 modelled over NVLink)
+        costs, pre = pretest(layers[0], ctxs[0], scores[0], steps=10, link_gbs=NVLINK_GBS)
+        for r, L in enumerate(layers):
+            L.set_selection({s: 0 for s in SEGS}, scores[r])
+    plan = Z.ztp_plan(T, M, float(u), costs, Z.plan_opts(enable_migration=1 if semi else 0, zero_crit=Z.CRIT_MIN))
     if semi:
         mios = [migration_io(plan, r, e, u, h) for r in range(e)]
         for r, L in enumerate(layers):
@@ -147,7 +154,7 @@ def run_case(cfg_name, e, chi, semi):
            "speedup_with_comm": (t_unbal + t_comm) / (t_bal + t_comm),
            "per_rank_free_ms": [round(x, 4) for x in free], "per_rank_unbal_ms": [round(x, 4) for x in T],
            "per_rank_bal_ms": [round(x, 4) for x in bal], "M_ms": [round(x, 4) for x in M],
-           "first_plan": first, "refresh": refresh}
+           "first_plan": first, "refresh": refresh, "pretest_costs": pre["costs"] if pre else None}
     for c in ctxs:
         Z.ztp_ctx_destroy(c)
     del layers
