@@ -38,11 +38,6 @@ struct ztp_ctx {
   cudaEvent_t ev_c = nullptr, ev_d = nullptr;
   int conc_bwd = 1;                    // ZTP_CONC (default 1): dW on the side stream, the SMs split by work
   int sm_cap = 0;                      // > 0: SMs a GEMM launch may use (concurrent dX / dW partition)
-  int dyn_sched = 1;                   // ZTP_DYN (default 1): GEMM work units claimed dynamically (atomic
-                                       // counter per launch) instead of a static round-robin / SM partition
-  static constexpr int DYN_SLOTS = 1024;
-  int* d_dyn = nullptr;                // DYN_SLOTS x [counter, finished pairs], zero between launches
-  int dyn_next = 0;
   bool side_pending = false;           // side-stream work not yet joined into a caller stream
   void* skws_side = nullptr;           // split-K partials of side-stream GEMMs
   size_t skws_side_cap = 0;
@@ -332,7 +327,6 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.splits = 1;
       p.kb_per_split = (kdim + 63) / 64;
     }
-    p.dyn = (c->dyn_sched && p.cs <= 1) ? c->d_dyn + 2 * (c->dyn_next++ % ztp_ctx::DYN_SLOTS) : nullptr;
     if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, nsm, st));
     if ((p.splits > 1 && p.cs <= 1) || p.col_pos) ++c->launches;   // split-K reduce or column expansion
   } else {
@@ -612,14 +606,7 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
                     dtype == ZTP_BF16;
   cudaStream_t sw = st;
   int cap_dx = 0, cap_dw = 0;
-  if (conc && c->dyn_sched) {
-    // dynamic scheduling: both GEMMs launch on every SM; whichever pairs get
-    // SMs claim units, so dW fills dX's tail and the next linear's dX
-    // competes for SMs freed by either (no static partition)
-    CUDA_TRY(c, cudaEventRecord(c->ev_c, st));
-    CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_c, 0));
-    sw = c->side_stream;
-  } else if (conc) {
+  if (conc) {
     CUDA_TRY(c, cudaEventRecord(c->ev_c, st));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_c, 0));
     sw = c->side_stream;
@@ -774,7 +761,6 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* g4 = getenv("ZTP_GATHER4")) c->use_gather4 = atoi(g4) != 0;
   if (const char* sk = getenv("ZTP_SPLITK")) c->allow_splitk = atoi(sk) != 0;
   if (const char* cc = getenv("ZTP_CONC")) c->conc_bwd = atoi(cc) != 0;
-  if (const char* dy = getenv("ZTP_DYN")) c->dyn_sched = atoi(dy) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
   auto cleanup = [&](ztp_status s) {
@@ -782,14 +768,12 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
     return s;
   };
   if (cudaMalloc(&c->d_flags, 64) != cudaSuccess || cudaMalloc(&c->d_stamp, 16) != cudaSuccess ||
-      cudaMalloc(&c->d_gemm_ns, 16) != cudaSuccess || cudaMalloc(&c->d_stats, 2 * (ZTP_MAX_RANKS + 1) * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&c->d_dyn, 2 * ztp_ctx::DYN_SLOTS * sizeof(int)) != cudaSuccess)
+      cudaMalloc(&c->d_gemm_ns, 16) != cudaSuccess || cudaMalloc(&c->d_stats, 2 * (ZTP_MAX_RANKS + 1) * sizeof(double)) != cudaSuccess)
     return cleanup(fail(nullptr, ZTP_ECUDA, "ztp_ctx_create: device allocation failed"));
   cudaMemset(c->d_flags, 0, 64);
   unsigned long long init_stamp[2] = {~0ull, 0ull};
   cudaMemcpy(c->d_stamp, init_stamp, 16, cudaMemcpyHostToDevice);
   cudaMemset(c->d_gemm_ns, 0, 16);
-  cudaMemset(c->d_dyn, 0, 2 * ztp_ctx::DYN_SLOTS * sizeof(int));
   if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess ||
@@ -822,7 +806,6 @@ ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   if (c->d_pstamp) cudaFree(c->d_pstamp);
   cudaFree(c->d_flags);
   cudaFree(c->d_stamp);
-  cudaFree(c->d_dyn);
   cudaFree(c->d_gemm_ns);
   cudaFree(c->d_stats);
   cudaFree(c->d_iota);

@@ -43,14 +43,6 @@ constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB
 constexpr int STAGING_PER_WARP = 32 * 128;     // one 32 x 64 bf16 plane (32 x 32 fp32)
 
-// Dynamic work scheduling (p.dyn != nullptr): the leader CTA's producer lane
-// claims the next work unit with an atomicAdd on a per-launch global counter
-// and publishes it through a SCHED_DEPTH-slot shared-memory ring (its own and,
-// over DSMEM, the peer CTA's), so a pair that starts late -- its SMs still
-// held by a concurrent GEMM (dX / dW) or the previous kernel's tail --
-// simply takes fewer units instead of holding a fixed round-robin share.
-constexpr int SCHED_DEPTH = 4;
-
 template <int CG>
 struct Cfg {
   static constexpr int BNL = BN / CG;                    // B columns staged by one CTA
@@ -60,7 +52,7 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
   static constexpr int RING = STAGES * STAGE_BYTES;
   static constexpr int STAGING = EPI_WARPS * 2 * STAGING_PER_WARP;   // ping-pong per warp
-  static constexpr int BARS = (2 * STAGES + 4 + 2 * SCHED_DEPTH) * 8 + SCHED_DEPTH * 4 + 16;
+  static constexpr int BARS = (2 * STAGES + 4) * 8 + 16;
   static constexpr int TOTAL = 1024 + RING + STAGING + BARS;
 };
 
@@ -187,10 +179,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* sfull = tempty + 2;              // dynamic scheduler: unit id published
-  uint64_t* sempty = sfull + SCHED_DEPTH;    // dynamic scheduler: unit id consumed (leader CTA's copy)
-  int32_t* sched = reinterpret_cast<int32_t*>(sempty + SCHED_DEPTH);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched + SCHED_DEPTH);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -210,12 +199,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], EPI_WARPS * CG);
-    }
-    // consumers of a published unit id: the MMA warp, the epilogue warps of
-    // both CTAs and the peer CTA's producer
-    for (int s = 0; s < SCHED_DEPTH; ++s) {
-      mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 1 + EPI_WARPS * CG + (CG - 1));
     }
     fence_barrier_init();
   }
@@ -254,50 +237,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     u_first = csplit * sc.tiles_c + (int)(blockIdx.x / (CG * p.cs));
     u_step = sc.num_units;
   }
-  const bool dyn = p.dyn != nullptr && p.cs <= 1;
-  // k-th work unit of this CTA (pair), or -1 when none is left.  Static:
-  // round-robin.  Dynamic: read from the scheduler ring; every consumer warp
-  // calls it for k = 0, 1, ... and acknowledges the slot on the leader's
-  // sempty barrier once the id is in a register.
-  auto next_unit = [&](int k) -> int {
-    if (!dyn) {
-      const int u = u_first + k * u_step;
-      return u < sc.num_units ? u : -1;
-    }
-    const int slot = k % SCHED_DEPTH;
-    mbar_wait_cluster(&sfull[slot], (uint32_t)(k / SCHED_DEPTH) & 1u);
-    const int u = ld_shared_s32(&sched[slot]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive_cluster(CG == 2 ? (smem_u32(&sempty[slot]) & PEER_BIT_MASK) : smem_u32(&sempty[slot]));
-    return u;
-  };
-  // the fetcher (leader CTA, producer warp): claim unit k and publish it
-  auto fetch_unit = [&](int k) -> int {
-    if (!dyn) return next_unit(k);
-    const int slot = k % SCHED_DEPTH;
-    int u = 0;
-    if (lane == 0) {
-      mbar_wait_cluster(&sempty[slot], ((uint32_t)(k / SCHED_DEPTH) & 1u) ^ 1u);
-      u = atomicAdd(p.dyn, 1);
-      if (u >= sc.num_units) u = -1;
-      sched[slot] = u;
-      if (CG == 2) {
-        const uint32_t peer = crank ^ 1u;
-        st_cluster_u32(mapa_shared(smem_u32(&sched[slot]), peer), (uint32_t)u);
-        mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[slot]), peer));
-      }
-      mbar_arrive_cluster(smem_u32(&sfull[slot]));
-    }
-    return __shfl_sync(0xFFFFFFFFu, u, 0);
-  };
 
   if (warp == 0) {
     // ============================ TMA producer ============================
     int stage = 0;
     uint32_t phase = 0;
-    for (int k = 0;; ++k) {
-      const int u = leader ? fetch_unit(k) : next_unit(k);
-      if (u < 0) break;
+    for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
       if (wk.zero) continue;
       const int am0 = wk.m0 + BM * rank;   // this CTA's 128 rows of the tile (A)
@@ -385,9 +330,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int k = 0;; ++k) {
-      const int u = next_unit(k);
-      if (u < 0) break;
+    for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
       if (wk.zero) continue;
       mbar_wait(&tempty[acc], aphase ^ 1);
@@ -467,9 +410,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         aphase ^= 1;
       }
     };
-    for (int k = 0;; ++k) {
-      const int u = next_unit(k);
-      if (u < 0) break;
+    for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
       const int m0 = wk.m0 + BM * rank, n0 = wk.n0;
       const bool zt = wk.zero;
@@ -734,15 +675,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tmem_dealloc_cg2(tmem_base, 512);
     else
       tmem_dealloc(tmem_base, 512);
-  }
-  // the last pair to finish re-arms the launch's counter for the next use
-  // (graph replays reuse it): every pair has stopped claiming by now
-  if (dyn && leader && threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(p.dyn + 1, 1) == npairs - 1) {
-      atomicExch(p.dyn, 0);
-      atomicExch(p.dyn + 1, 0);
-    }
   }
   if (p.pdl_late) pdl_wait();
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMax(p.stamp + 1, (unsigned long long)globaltimer());

@@ -64,8 +64,6 @@ struct GemmParams {
   const int32_t* col_pos;  // DW output pruning: full column j <- compact column col_pos[j] (< 0: Zero)
   int n_full;              // full output columns when col_pos is set (N = compact columns)
   int pdl_late;            // inputs do not depend on the preceding kernel: PDL wait deferred to exit
-  int* dyn;                // dynamic scheduling: [unit counter, finished pairs] of this launch (zero on
-                           // entry, re-armed by the kernel's last pair); nullptr = static round-robin
   int cs;                  // DW cluster split-K: the `splits` K-slices of a tile run as one cluster and
                            // are reduced through distributed shared memory (no workspace, no reduce kernel)
 };

@@ -79,8 +79,10 @@ def time_step(L, ctx, chi: float = 1.0, steps: int = 30, reps: int = 3) -> float
     L.step(stream)
     torch.cuda.synchronize()
     g = L.capture(stream)
-    for _ in range(3):
-        g.replay()
+    with torch.cuda.stream(stream):      # replay() issues on the current stream
+        for _ in range(3):
+            g.replay()
+    torch.cuda.synchronize()
     out = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -87,7 +87,10 @@ def test_pretest_on_gpu():
         p2 = rep["phi2"]
         assert p2[-1]["extra_ms"] > 0.0 and p2[-1]["T_ms"] > p2[0]["T_ms"]
         p1 = rep["phi1_measured"]
-        assert p1[-1]["ms"] > p1[0]["ms"] > 0.0
+        # copies of 1/8 .. all units: launch-dominated at this size, so only
+        # positivity and a non-shrinking trend within timing noise
+        assert all(d["ms"] > 0.0 for d in p1) and p1[-1]["ms"] >= 0.9 * p1[0]["ms"]
+        assert p1[-1]["bytes"] == 8 * p1[0]["bytes"]
         plan = Z.ztp_plan([1.0, 3.0], [0.8, 2.4], float(f), costs,
                           Z.plan_opts(enable_migration=1, zero_crit=Z.CRIT_MIN))
         assert plan.z == 1 and 0.0 <= plan.beta[1] <= 1.0

@@ -50,8 +50,7 @@ from synth import inputs as I  # noqa: E402
 NVLINK_GBS = 770.0
 PER = int(os.environ.get("STEPS_PER_PHASE", "10"))
 REPLAYS = int(os.environ.get("REPLAYS", "5"))
-WARM = int(os.environ.get("WARM", "5"))       # replays after a (re)capture before timing: the first
-                                              # replays of a fresh graph measured ~25% slow (r01 v1 run)
+WARM = int(os.environ.get("WARM", "5"))       # replays after a (re)capture before timing
 EPS = float(os.environ.get("EPS", "0.05"))    # A-17 straggler tolerance, above the one-GPU timing noise
 TRIGGER = 0.10
 
@@ -118,8 +117,10 @@ class Rank:
             with torch.cuda.graph(g, stream=stream):
                 self.run(stream)
             self.graph, self.key = g, key
-            for _ in range(WARM):
-                self.graph.replay()
+            with torch.cuda.stream(stream):      # replay() issues on the current stream
+                for _ in range(WARM):
+                    self.graph.replay()
+            torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             e0.record(stream)

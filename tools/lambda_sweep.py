@@ -38,8 +38,10 @@ def time_rank(L, ctx, chi_r, steps=STEPS):
         L.step(stream)
     torch.cuda.synchronize()
     g = L.capture(stream)
-    for _ in range(3):
-        g.replay()
+    with torch.cuda.stream(stream):      # replay() issues on the current stream
+        for _ in range(3):
+            g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e0.record(stream)
