@@ -409,6 +409,21 @@ def main():
     for _ in range(int(os.environ.get("BENCH_REPEAT", "0"))):   # diagnostics: run-to-run spread
         print(f"[bench] repeat ms_per_step {run_phase(gC, args.steps, 2):.4f}", file=sys.stderr, flush=True)
     launches = per_step_launches * args.steps
+    # per-step distribution (median / p10 / p90 over 50 steps):
+    # each replay bracketed by its own events, max over ranks per step; a
+    # separate pass after the timed region (the headline is the timed mean)
+    n_dist = 50
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_dist)]
+    torch.cuda.synchronize()
+    D.barrier()
+    for a0, a1 in evs:
+        a0.record(stream)
+        gC.replay()
+        a1.record(stream)
+    torch.cuda.synchronize()
+    per_step = sorted(D.max(a0.elapsed_time(a1)) for a0, a1 in evs)
+    step_dist = {"p10": per_step[n_dist // 10], "p50": per_step[n_dist // 2], "p90": per_step[(9 * n_dist) // 10],
+                 "n": n_dist, "how": "one event pair per replay (launch gaps included), max over ranks"}
     # the GEMM launches of the same step, timed with CUDA events on the
     # launching stream in an un-captured pass right after the timed region
     prof = profiled_steps(min(20, args.steps))
@@ -552,6 +567,7 @@ def main():
                           "rule": "max(rank GEMM FLOPs / burst peak, all-reduce ring bytes / 770 GB/s)"},
         "cpu_baseline": cpu,
         "clocks": clocks,
+        "step_ms_dist": step_dist,
         "ms_dense_free": ms_free, "dense_tflops": flops_dense / (ms_free * 1e-3) / 1e12,
         "plan": plan_info,
     }

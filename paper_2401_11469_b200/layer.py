@@ -261,8 +261,12 @@ class ZtpLayer:
         Z.ztp_select(self.ctx, lens, nps, self._scores, self.kept, self.pruned, apps, self.pos, stream)
 
     def _sel(self, s, mid):
-        if self.n_prune[s] == 0 and self.append[s] == 0:
-            return None            # dense: no lineage entry, operands used in place
+        if self.n_prune[s] == 0 and (self.append[s] == 0 or s == "fc2"):
+            # dense: no lineage entry, operands used in place.  A helper's
+            # received MLP units sit right after its own ones (W1^T columns /
+            # W2^T rows u .. u + n_in), so an unpruned FC2 with appended units
+            # is the dense prefix of length n_fc -- no compaction copies
+            return None
         p = self.P[s] if self.n_prune[s] > 0 else self.kept
         return Z.sel(self.S[s], self.nk[s], p, self.n_prune[s], self.layer_id, mid)
 
@@ -299,7 +303,8 @@ class ZtpLayer:
         osel = self.sels["fc2"]
         ng = nk["fc2"] if osel is not None else nfc
         self.f_fc1 = L(x_t=y1, w_t=self.w1_t, y_t=self.HC, pre_t=self.PreC, ws_t=self.W1_c,
-                       sel_=self.sels["fc1"], n_out=nfc, act=Z.ACT_GELU_D, y_pos=self.POS["fc2"], out_sel=osel,
+                       sel_=self.sels["fc1"], n_out=nfc, act=Z.ACT_GELU_D, y_pos=self.POS["fc2"] if osel is not None else None,
+                       out_sel=osel,
                        **y1_kw)
         self.f_fc2 = L(x_t=self.HC[:nk["fc2"]], w_t=self.w2_t[:nfc], y_t=self.Y, ws_t=self.W2_c,
                        sel_=self.sels["fc2"], x_compact=True)
@@ -314,7 +319,8 @@ class ZtpLayer:
                        dw_t=self.dw2[:nfc], pre_in_t=self.PreC[:nk["fc2"]], ws_t=self.W2_c,
                        sel_=self.sels["fc2"], act_in=Z.ACT_GELU_D, x_compact=True, dx_compact=osel is not None)
         self.b_fc1 = L(x_t=y1, w_t=self.w1_t, g_t=self.G1[:ng], dx_t=self.dY1, dw_t=self.dw1,
-                       ws_t=self.W1_c, sel_=self.sels["fc1"], n_out=nfc, y_pos=self.POS["fc2"], out_sel=osel,
+                       ws_t=self.W1_c, sel_=self.sels["fc1"], n_out=nfc, y_pos=self.POS["fc2"] if osel is not None else None,
+                       out_sel=osel,
                        **y1_kw)
         self.b_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx, dw_t=self.do,
                      ws_t=self.Wo_c, sel_=self.sels["o"], x_compact=True)

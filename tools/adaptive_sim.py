@@ -140,6 +140,18 @@ class Rank:
         return m
 
 
+def measure(ranks, chis, version):
+    """Per-rank step times, each the mean of a forward (0..e-1) and a
+    reverse pass: a rank's place in the sweep otherwise biases it by the
+    board's power/clock drift (~10% over one sweep measured)."""
+    e = len(ranks)
+    fwd = [R.time(chis[r], version) for r, R in enumerate(ranks)]
+    rev = [0.0] * e
+    for r in reversed(range(e)):
+        rev[r] = ranks[r].time(chis[r], version)
+    return [(a + b) / 2 for a, b in zip(fwd, rev)]
+
+
 def apply_plan(ranks, plan, e, h, a, u):
     """plan -> every rank's migration ranges and prune counts on all layers;
     the weight slices are copied locally (one GPU) once per plan."""
@@ -197,7 +209,7 @@ def main():
     # ---- T_free: everyone dense at chi = 1
     apply_plan(ranks, None, e, h, a, u)
     version = 0
-    t_free = max(R.time(1.0, version) for R in ranks) + t_comm
+    t_free = max(measure(ranks, [1.0] * e, version)) + t_comm
 
     plan, mios = None, [MigrationIO() for _ in range(e)]
     window, T_ref, refined = True, None, False
@@ -210,7 +222,7 @@ def main():
                 apply_plan(ranks, None, e, h, a, u)
                 version += 1
                 plan, mios = None, [MigrationIO() for _ in range(e)]
-            T = [R.time(chis[r], version) for r, R in enumerate(ranks)]
+            T = measure(ranks, chis, version)
             M = [R.gemm_ms(chis[r]) for r, R in enumerate(ranks)]
             rec.update(mode="window", per_rank_ms=[round(x, 4) for x in T], M_ms=[round(x, 4) for x in M])
             rec["step_ms"] = max(T) + t_comm
@@ -222,7 +234,7 @@ def main():
             window, T_ref, refined = False, None, False
             rec["plan_after"] = plan_summary(plan, e)
         else:
-            T = [R.time(chis[r], version) for r, R in enumerate(ranks)]
+            T = measure(ranks, chis, version)
             rec.update(mode="plan", per_rank_ms=[round(x, 4) for x in T])
             rec["step_ms"] = max(T) + t_comm + mig_model_ms(mios, h, n_layers)
             if T_ref is None:
@@ -261,7 +273,7 @@ def main():
     version += 1
     for ph in range(4):
         _, chis = schedule(ph * PER, e)
-        unbal[ph] = max(R.time(chis[r], version) for r, R in enumerate(ranks)) + t_comm
+        unbal[ph] = max(measure(ranks, chis, version)) + t_comm
         phases[ph]["unbal_step_ms"] = round(unbal[ph], 4)
         phases[ph]["speedup_planned_vs_unbal"] = (round(unbal[ph] / phases[ph]["mean_planned_step_ms"], 4)
                                                   if phases[ph]["mean_planned_step_ms"] else None)

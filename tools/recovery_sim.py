@@ -64,6 +64,17 @@ def time_rank(L, ctx, chi_r, steps=STEPS):
     return e0.elapsed_time(e1) / steps
 
 
+def time_all(layers, ctxs, chis):
+    """Per-rank step times, each the mean of a forward and a reverse sweep
+    over the ranks (cancels the power/clock drift along one sweep)."""
+    e = len(layers)
+    fwd = [time_rank(L, ctxs[r], chis[r]) for r, L in enumerate(layers)]
+    rev = [0.0] * e
+    for r in reversed(range(e)):
+        rev[r] = time_rank(layers[r], ctxs[r], chis[r])
+    return [(a + b) / 2 for a, b in zip(fwd, rev)]
+
+
 def gemm_ms(L, ctx):
     """M_i: GEMM time per step incl. the emulated slowdown (A-6)."""
     Z.ztp_set_stats(ctx, True)
@@ -99,8 +110,8 @@ def run_case(cfg_name, e, chi, semi):
         scores.append({s: torch.from_numpy(v).cuda() for s, v in bench.scores_for(cfg, r, lens).items()})
     for r, L in enumerate(layers):
         L.set_selection({s: 0 for s in SEGS}, scores[r])
-    free = [time_rank(L, ctxs[r], 1.0) for r, L in enumerate(layers)]
-    T = [time_rank(L, ctxs[r], chis[r]) for r, L in enumerate(layers)]
+    free = time_all(layers, ctxs, [1.0] * e)
+    T = time_all(layers, ctxs, chis)
     M = [gemm_ms(L, ctxs[r]) for r, L in enumerate(layers)]
     costs, pre = None, None
     if semi:
@@ -120,7 +131,7 @@ def run_case(cfg_name, e, chi, semi):
     counts = [layer_prune_counts(plan, r, h, a, u) for r in range(e)]
     for r, L in enumerate(layers):
         L.set_selection(counts[r], scores[r])
-    bal = [time_rank(L, ctxs[r], chis[r]) for r, L in enumerate(layers)]
+    bal = time_all(layers, ctxs, chis)
     # statistics refresh (A-8): a rank whose runtime moved > 10% since
     # the window its plan came from triggers a new window; ZERO plans compose
     # with the fresh Eq.1 ratio (ztp_plan_refine, A-39)
@@ -139,7 +150,7 @@ def run_case(cfg_name, e, chi, semi):
         counts = [layer_prune_counts(plan, r, h, a, u) for r in range(e)]
         for r, L in enumerate(layers):
             L.set_selection(counts[r], scores[r])
-        bal = [time_rank(L, ctxs[r], chis[r]) for r, L in enumerate(layers)]
+        bal = time_all(layers, ctxs, chis)
         refresh.append({"gamma": [round(g, 4) for g in list(plan.gamma)[:e]], "T_bal_ms": max(bal),
                         "per_rank_ms": [round(x, 4) for x in bal]})
     t_comm = 4 * 2 * N * h * 2 * (e - 1) / e / (NVLINK_GBS * 1e9) * 1e3
