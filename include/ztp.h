@@ -157,16 +157,20 @@ void ztp_plan_opts_default(ztp_plan_opts* o);
 ztp_status ztp_plan(int world, const double* T, const double* M, double L_ref,
                     const ztp_costs* costs, const ztp_plan_opts* opts, ztp_plan_t* out);
 
-/* ztp_plan_refine: statistics refresh of a ZERO-only plan (A-8, A-39).
+/* ztp_plan_refine: statistics refresh of a plan (A-8, A-39, A-42).
  * When a rank's runtime moves by > 10% after `prev` was applied, the new
- * window (T, M measured WITH prev's resizing in effect) gives `fresh` =
- * ztp_plan(...) whose Eq.1 ratio is a fraction of the work the rank still
+ * window (T, M measured WITH prev in effect) gives `fresh` = ztp_plan(...)
+ * (ZERO-only) whose Eq.1 ratio is a fraction of the work the rank still
  * computes, so the kept fractions compose:
- *   gamma = gamma_r = min(1 - (1 - prev.gamma_r[r]) (1 - fresh.gamma_r[r]), gamma_max),
- * role RESIZE iff gamma > 0; z and order are fresh's.  Host-only, bit-
- * deterministic.  Errors: ZTP_EINVAL (null, world mismatch),
- * ZTP_EUNSUPPORTED (either plan has a MIGRATE / SPLIT role -- a SEMI plan is
- * recomputed by ztp_plan from a dense window instead). */
+ *   resizing ranks: gamma = gamma_r = min(1 - (1 - prev.gamma_r[r]) (1 - fresh.gamma_r[r]), gamma_max),
+ *                   role RESIZE iff gamma > 0;
+ *   MIGRATE / SPLIT ranks of prev (A-42): their whole shed fraction composes,
+ *                   gamma = min(1 - (1 - prev.gamma[r]) (1 - fresh.gamma_r[r]), gamma_max), beta kept,
+ *                   phi = gamma beta, gamma_r = gamma (1 - beta) / (1 - gamma beta), role kept;
+ * z is fresh's; order and x are prev's when prev migrates (same sender order),
+ * else fresh's order and x = 0.  Host-only, bit-deterministic.
+ * Errors: ZTP_EINVAL (null, world mismatch), ZTP_EUNSUPPORTED (fresh has a
+ * MIGRATE / SPLIT role: the refresh plan must be ZERO-only). */
 ztp_status ztp_plan_refine(const ztp_plan_t* prev, const ztp_plan_t* fresh, double gamma_max, ztp_plan_t* out);
 
 /* ztp_plan_counts: integer realisation of a plan for one linear of `rank`.

@@ -130,29 +130,42 @@ def eq1_gamma(T_r: float, C: float, M_r: float, gamma_max: float) -> float:
 
 
 def plan_refine(prev: Plan, fresh: Plan, gamma_max: float = 0.9) -> Plan:
-    """Statistics refresh of a ZERO-only plan ("over-10% increase ...
-    update on demand", A-8; reading A-39).  `fresh` is Eq.1 on a window
-    measured with `prev` in effect, so its ratio is a fraction of the work the
-    rank still computes (the savings offset the remaining gap
+    """Statistics refresh of a plan ("over-10% increase ... update on
+    demand", A-8; readings A-39, A-42).  `fresh` is Eq.1 (ZERO-only) on a
+    window measured with `prev` in effect, so its ratio is a fraction of the
+    work the rank still computes (the savings offset the remaining gap
     T_i - T_avg): kept fractions multiply, 1 - gamma = (1 - gamma_prev)
-    (1 - gamma_fresh), clamped to gamma_max (A-4)."""
+    (1 - gamma_fresh), clamped to gamma_max (A-4).
+    A-42: a rank that sheds work by migration (MIGRATE / SPLIT) composes its
+    whole shed fraction gamma the same way and keeps its Eq.2 split beta:
+    phi = gamma beta, gamma_r = gamma (1 - beta) / (1 - gamma beta) (A-16);
+    the plan keeps prev's migration group (x) and sender order."""
     if prev.world != fresh.world:
         raise OracleError("ZTP_EINVAL", "world mismatch")
     e = fresh.world
-    if any(x in (MIGRATE, SPLIT) for x in list(prev.role[:e]) + list(fresh.role[:e])):
-        raise OracleError("ZTP_EUNSUPPORTED", "refine ZERO-only plans (A-39)")
-    out = Plan(world=e, z=fresh.z, x=0, order=list(fresh.order), role=[NORMAL] * e, gamma=[0.0] * e,
-               beta=[0.0] * e, phi=[0.0] * e, gamma_r=[0.0] * e)
+    if any(x in (MIGRATE, SPLIT) for x in list(fresh.role[:e])):
+        raise OracleError("ZTP_EUNSUPPORTED", "the refresh plan must be ZERO-only (A-39, A-42)")
+    semi = any(x in (MIGRATE, SPLIT) for x in list(prev.role[:e]))
+    out = Plan(world=e, z=fresh.z, x=prev.x if semi else 0, order=list(prev.order if semi else fresh.order),
+               role=[NORMAL] * e, gamma=[0.0] * e, beta=[0.0] * e, phi=[0.0] * e, gamma_r=[0.0] * e)
     for r in range(e):
-        keep = (1.0 - prev.gamma_r[r]) * (1.0 - fresh.gamma_r[r])
+        sheds = prev.role[r] in (MIGRATE, SPLIT)
+        keep = (1.0 - (prev.gamma[r] if sheds else prev.gamma_r[r])) * (1.0 - fresh.gamma_r[r])
         g = 1.0 - keep
         if g > gamma_max:
             g = gamma_max
         if g < 0.0:
             g = 0.0
         out.gamma[r] = g
-        out.gamma_r[r] = g
-        out.role[r] = RESIZE if g > 0.0 else NORMAL
+        if sheds:
+            b = prev.beta[r]
+            out.beta[r] = b
+            out.phi[r] = g * b
+            out.gamma_r[r] = 0.0 if b >= 1.0 else (g * (1.0 - b)) / (1.0 - g * b)
+            out.role[r] = prev.role[r]
+        else:
+            out.gamma_r[r] = g
+            out.role[r] = RESIZE if g > 0.0 else NORMAL
     return out
 
 

@@ -197,14 +197,36 @@ extern "C" ztp_status ztp_plan_refine(const ztp_plan_t* prev, const ztp_plan_t* 
     return ZTP_EINVAL;
   }
   const int e = fresh->world;
-  for (int r = 0; r < e; ++r)
-    if (prev->role[r] > ZTP_RESIZE || fresh->role[r] > ZTP_RESIZE) {
-      set_thread_error("ztp_plan_refine: rank " + std::to_string(r) + " migrates; refine ZERO-only plans (A-39)");
+  bool semi = false;
+  for (int r = 0; r < e; ++r) {
+    if (fresh->role[r] > ZTP_RESIZE) {
+      set_thread_error("ztp_plan_refine: fresh plan of rank " + std::to_string(r) +
+                       " migrates; the refresh plan must be ZERO-only (A-39, A-42)");
       return ZTP_EUNSUPPORTED;
     }
+    if (prev->role[r] == ZTP_MIGRATE || prev->role[r] == ZTP_SPLIT) semi = true;
+  }
   ztp_plan_t o = *fresh;
   o.x = 0;
+  if (semi) {   // keep the migration group and its sender order (A-42)
+    o.x = prev->x;
+    for (int i = 0; i < ZTP_MAX_RANKS; ++i) o.order[i] = prev->order[i];
+  }
   for (int r = 0; r < e; ++r) {
+    if (prev->role[r] == ZTP_MIGRATE || prev->role[r] == ZTP_SPLIT) {
+      // A-42: compose the rank's whole shed fraction, keep its Eq.2 split
+      const double keep = (1.0 - prev->gamma[r]) * (1.0 - fresh->gamma_r[r]);
+      double g = 1.0 - keep;
+      if (g > gamma_max) g = gamma_max;
+      if (g < 0.0) g = 0.0;
+      const double b = prev->beta[r];
+      o.gamma[r] = g;
+      o.beta[r] = b;
+      o.phi[r] = g * b;
+      o.gamma_r[r] = b >= 1.0 ? 0.0 : (g * (1.0 - b)) / (1.0 - g * b);
+      o.role[r] = prev->role[r];
+      continue;
+    }
     const double keep = (1.0 - prev->gamma_r[r]) * (1.0 - fresh->gamma_r[r]);
     double g = 1.0 - keep;
     if (g > gamma_max) g = gamma_max;

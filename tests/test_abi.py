@@ -173,9 +173,42 @@ def test_plan_refine_matches_oracle(Z):
     semi = Z.ztp_plan([10.0, 30.0], [10.0, 30.0], 100.0, Z.make_costs(0.0, lin, ((0.0, 1.0), (0.0, 0.0)), lin),
                       Z.plan_opts(enable_migration=1))
     assert semi.role[1] in (Z.MIGRATE, Z.SPLIT)
-    with pytest.raises(Z.ZtpError) as ei:
+    with pytest.raises(Z.ZtpError) as ei:     # the refresh plan itself must be ZERO-only
         Z.ztp_plan_refine(semi, semi)
     assert ei.value.name == "ZTP_EUNSUPPORTED"
+
+
+def test_plan_refine_semi_matches_oracle(Z):
+    """A-42: refreshing a SEMI plan (MIGRATE / SPLIT ranks compose their shed
+    fraction, keep beta) is bit-exact against the oracle on random plans."""
+    import random
+    rng = random.Random(11)
+    seen = set()
+    for _ in range(300):
+        e = rng.randint(2, 8)
+        T1 = [rng.uniform(1, 1.3) for _ in range(e)]
+        for s in rng.sample(range(e), rng.randint(1, min(3, e - 1))):
+            T1[s] = rng.uniform(2, 4)
+        M = [rng.uniform(0.5, 1.0) * t for t in T1]
+        T2 = [rng.uniform(1, 1.6) for _ in range(e)]
+        xs = (0.0, 1.0)
+        om2, p1, p2 = ((xs, (0.0, rng.uniform(0, 2))) for _ in range(3))
+        om1 = rng.uniform(0, 0.2)
+        zc, oc = Z.make_costs(om1, om2, p1, p2), O.Costs(om1, om2, p1, p2)
+        kw = dict(enable_migration=1, zero_crit=1, gamma_max=rng.choice([0.9, 1.0]))
+        zp1 = Z.ztp_plan(T1, M, 1.0, zc, Z.plan_opts(**kw))
+        op1 = O.plan(T1, M, 1.0, oc, O.PlanOpts(**kw))
+        kz = dict(zero_crit=1, gamma_max=kw["gamma_max"])
+        zp2 = Z.ztp_plan(T2, M, 1.0, opts=Z.plan_opts(**kz))
+        op2 = O.plan(T2, M, 1.0, O.Costs(), O.PlanOpts(**kz))
+        zr = Z.ztp_plan_refine(zp1, zp2, kw["gamma_max"])
+        orf = O.plan_refine(op1, op2, kw["gamma_max"])
+        seen.update(orf.role)
+        assert list(zr.role)[:e] == orf.role and zr.x == orf.x and list(zr.order)[:e] == orf.order[:e]
+        for r in range(e):
+            for k in ("gamma", "beta", "phi", "gamma_r"):
+                assert _bits(getattr(zr, k)[r]) == _bits(getattr(orf, k)[r]), (k, r)
+    assert {O.MIGRATE, O.RESIZE} <= seen or {O.SPLIT, O.RESIZE} <= seen
 
 
 def test_no_cuda_device_is_an_error_not_a_fallback(Z):

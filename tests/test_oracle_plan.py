@@ -118,6 +118,49 @@ def test_refine_reaches_Tmin_under_resize_overhead_A39(seed):
     assert p3.gamma == p2.gamma
 
 
+@pytest.mark.parametrize("seed", range(20))
+def test_refine_semi_reaches_Tmin_A42(seed):
+    """A-42: a migrating straggler whose remaining work (1 - gamma) runs at
+    chi x (T = C + kappa + chi m (1 - gamma), kappa the fixed overhead of
+    shedding) overshoots T_min by kappa under the first plan; ONE refresh
+    composing its shed fraction lands it on T_min exactly, keeps beta, and the
+    A-16 identity (1 - phi)(1 - gamma_r) = 1 - gamma holds for the new plan."""
+    rng = random.Random(100 + seed)
+    e = rng.randint(3, 8)
+    s = rng.randrange(e)
+    m, C = rng.uniform(1, 10), rng.uniform(0, 5)
+    chi = rng.uniform(2.2, 4.0)                         # gamma > gamma_tol: SEMI migrates
+    kappa = rng.uniform(0.05, 0.3) * m + 0.03 * (C + m)
+    chis = [chi if r == s else 1.0 for r in range(e)]
+
+    def window(gam):
+        T = [C + (kappa if gam[r] > 0 else 0.0) + chis[r] * m * (1 - gam[r]) for r in range(e)]
+        M = [chis[r] * m * (1 - gam[r]) for r in range(e)]
+        return T, M
+
+    lin = ((0.0, 1.0), (0.0, 0.0))
+    costs = O.Costs(0.0, ((0.0, 1.0), (0.0, 1.0)), lin, lin)     # resizing costs, migration free: beta = 1
+    p1 = O.plan(*window([0.0] * e), 1.0, costs, O.PlanOpts(enable_migration=1, zero_crit=O.CRIT_MIN, gamma_max=1.0))
+    assert p1.role[s] == O.MIGRATE and p1.beta[s] == 1.0
+    assert p1.gamma[s] == pytest.approx(1 - 1 / chi, rel=1e-12)
+    zopts = O.PlanOpts(zero_crit=O.CRIT_MIN, gamma_max=1.0)
+    T1, M1 = window(p1.gamma)
+    assert T1[s] == pytest.approx(C + m + kappa, rel=1e-12)
+    p2 = O.plan_refine(p1, O.plan(T1, M1, 1.0, O.Costs(), zopts), 1.0)
+    T2, _ = window(p2.gamma)
+    assert T2[s] == pytest.approx(C + m, rel=1e-12)
+    assert p2.role[s] == O.MIGRATE and p2.beta[s] == 1.0 and p2.phi[s] == p2.gamma[s] and p2.gamma_r[s] == 0.0
+    assert p2.x == p1.x and p2.order == p1.order
+    # SPLIT: the A-16 identity for a fractional beta
+    q = O.Plan(world=2, z=1, x=1, order=[1, 0], role=[O.NORMAL, O.SPLIT], gamma=[0.0, 0.6], beta=[0.0, 0.25],
+               phi=[0.0, 0.15], gamma_r=[0.0, 0.6 * 0.75 / (1 - 0.15)])
+    f = O.plan([1.0, 1.3], [1.0, 1.0], 1.0, O.Costs(), zopts)
+    r2 = O.plan_refine(q, f, 1.0)
+    assert r2.role[1] == O.SPLIT and r2.beta[1] == 0.25
+    assert (1 - r2.phi[1]) * (1 - r2.gamma_r[1]) == pytest.approx(1 - r2.gamma[1], rel=1e-14)
+    assert 1 - r2.gamma[1] == pytest.approx((1 - 0.6) * (1 - f.gamma_r[1]), rel=1e-14)
+
+
 def test_eq2_worked_example_S572():
     g = golden("eq2_worked.json")
     c = O.Costs(g["omega1"], _costs_from(g, "omega2"), _costs_from(g, "phi1"), _costs_from(g, "phi2"))

@@ -27,8 +27,9 @@ Controller (host, per step; Alg.2):
     the Alg.2 l.1 pretest (paper_2401_11469_b200/pretest.py, measured here at
     start-up, Phi_1 modelled over NVLink);
   * the first step under a new plan is the monitoring reference T_ref; a
-    ZERO-only plan whose straggler is still detectably slower is refined once
-    per window (A-39, ztp_plan_refine);
+    plan whose straggler is still detectably slower is refined once per
+    window (ztp_plan_refine: A-39 for resizing ranks, A-42 for migrating
+    ones -- their shed fraction composes, beta kept);
   * trigger: any rank's runtime moving > 10% from T_ref (A-8).
 Output: per-step JSON (phase, mode, roles, gamma/beta, per-rank ms, step ms)
 and per-phase means vs T_free.  Env: STEPS_PER_PHASE (10), REPLAYS (5), WARM (5), EPS (0.05),
@@ -239,8 +240,7 @@ def main():
             rec["step_ms"] = max(T) + t_comm + mig_model_ms(mios, h, n_layers)
             if T_ref is None:
                 T_ref = T
-                zero_only = plan is not None and all(int(x) in (0, 1) for x in list(plan.role)[:e])
-                if zero_only and not refined:
+                if plan is not None and not refined:
                     M = [R.gemm_ms(chis[r]) for r, R in enumerate(ranks)]
                     fresh = Z.ztp_plan(T, M, float(u), None, zopts)
                     if int(fresh.z) > 0:

@@ -120,17 +120,23 @@ def run_case(cfg_name, e, chi, semi):
         for r, L in enumerate(layers):
             L.set_selection({s: 0 for s in SEGS}, scores[r])
     plan = Z.ztp_plan(T, M, float(u), costs, Z.plan_opts(enable_migration=1 if semi else 0, zero_crit=Z.CRIT_MIN))
-    if semi:
-        mios = [migration_io(plan, r, e, u, h) for r in range(e)]
+    last_mios = []
+
+    def apply(plan):
+        if semi:
+            mios = [migration_io(plan, r, e, u, h) for r in range(e)]
+            last_mios[:] = mios
+            for r, L in enumerate(layers):
+                L.set_migration(mios[r])
+            for (src, dst, lo, hi, off) in mios[0].all_xfers:      # local stand-in for ztp_migrate
+                Ls, Ld = layers[src], layers[dst]
+                Ld.w1_t[:, u + off:u + off + hi - lo].copy_(Ls.w1_t[:, lo:hi])
+                Ld.w2_t[u + off:u + off + hi - lo].copy_(Ls.w2_t[lo:hi])
+        cnt = [layer_prune_counts(plan, r, h, a, u) for r in range(e)]
         for r, L in enumerate(layers):
-            L.set_migration(mios[r])
-        for (src, dst, lo, hi, off) in mios[0].all_xfers:      # local stand-in for ztp_migrate
-            Ls, Ld = layers[src], layers[dst]
-            Ld.w1_t[:, u + off:u + off + hi - lo].copy_(Ls.w1_t[:, lo:hi])
-            Ld.w2_t[u + off:u + off + hi - lo].copy_(Ls.w2_t[lo:hi])
-    counts = [layer_prune_counts(plan, r, h, a, u) for r in range(e)]
-    for r, L in enumerate(layers):
-        L.set_selection(counts[r], scores[r])
+            L.set_selection(cnt[r], scores[r])
+        return cnt
+    counts = apply(plan)
     bal = time_all(layers, ctxs, chis)
     # statistics refresh (A-8): a rank whose runtime moved > 10% since
     # the window its plan came from triggers a new window; ZERO plans compose
@@ -138,7 +144,7 @@ def run_case(cfg_name, e, chi, semi):
     first = {"T_bal_ms": max(bal), "gamma": [round(g, 4) for g in list(plan.gamma)[:e]]}
     refresh = []
     T_last = T
-    for _ in range(REFRESH if not semi else 0):
+    for _ in range(REFRESH):
         if max(abs(bal[r] - T_last[r]) / T_last[r] for r in range(e)) <= 0.10:
             break
         M_cur = [gemm_ms(L, ctxs[r]) for r, L in enumerate(layers)]
@@ -146,15 +152,16 @@ def run_case(cfg_name, e, chi, semi):
         if fresh.z == 0:
             break
         T_last = bal
-        plan = Z.ztp_plan_refine(plan, fresh)
-        counts = [layer_prune_counts(plan, r, h, a, u) for r in range(e)]
-        for r, L in enumerate(layers):
-            L.set_selection(counts[r], scores[r])
+        plan = Z.ztp_plan_refine(plan, fresh)          # A-39 / A-42 (SEMI: shed fraction composes)
+        counts = apply(plan)
         bal = time_all(layers, ctxs, chis)
         refresh.append({"gamma": [round(g, 4) for g in list(plan.gamma)[:e]], "T_bal_ms": max(bal),
                         "per_rank_ms": [round(x, 4) for x in bal]})
     t_comm = 4 * 2 * N * h * 2 * (e - 1) / e / (NVLINK_GBS * 1e9) * 1e3
-    t_free, t_unbal, t_bal = max(free), max(T), max(bal)
+    # per-step migration copies of a SEMI plan (weights out + dW back) from
+    # the busiest sender's egress, modelled at NVLINK_GBS like the all-reduces
+    t_mig = max([4 * m.n_mig * h * 2 / (NVLINK_GBS * 1e9) * 1e3 for m in last_mios] + [0.0])
+    t_free, t_unbal, t_bal = max(free), max(T), max(bal) + t_mig
     roles = "".join("NRMS"[int(x)] for x in list(plan.role)[:e])
     out = {"config": cfg_name, "tp": e, "chi": chi, "straggler": strag, "plan": "SEMI" if semi else "ZERO (T_min)",
            "roles": roles, "gamma": [round(g, 4) for g in list(plan.gamma)[:e]],
@@ -162,7 +169,7 @@ def run_case(cfg_name, e, chi, semi):
            "n_prune_straggler": counts[strag],
            "T_free_ms": t_free, "T_unbal_ms": t_unbal, "T_bal_ms": t_bal,
            "recovery_compute": t_free / t_bal, "speedup_compute": t_unbal / t_bal,
-           "t_allreduce_model_ms": t_comm,
+           "t_allreduce_model_ms": t_comm, "t_migration_model_ms": t_mig,
            "recovery_with_comm": (t_free + t_comm) / (t_bal + t_comm),
            "speedup_with_comm": (t_unbal + t_comm) / (t_bal + t_comm),
            "per_rank_free_ms": [round(x, 4) for x in free], "per_rank_unbal_ms": [round(x, 4) for x in T],
