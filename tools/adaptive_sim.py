@@ -30,7 +30,9 @@ Controller (host, per step; Alg.2):
     plan whose straggler is still detectably slower is refined once per
     window (ztp_plan_refine: A-39 for resizing ranks, A-42 for migrating
     ones -- their shed fraction composes, beta kept);
-  * trigger: any rank's runtime moving > 10% from T_ref (A-8).
+  * trigger: any rank's runtime moving > 10% from T_ref (A-8), or,
+    on the first step under a plan, a rank running > 10% below the T_min the
+    plan aimed at (its slowdown changed while the plan was being applied).
 Output: per-step JSON (phase, mode, roles, gamma/beta, per-rank ms, step ms)
 and per-phase means vs T_free.  Env: STEPS_PER_PHASE (10), REPLAYS (5), WARM (5), EPS (0.05),
 OUT (gpurun_out/adaptive_sim.json), CFG (c5), TP (8)."""
@@ -214,6 +216,7 @@ def main():
 
     plan, mios = None, [MigrationIO() for _ in range(e)]
     window, T_ref, refined = True, None, False
+    T_target = T_window_max = 0.0
     series = []
     for step in range(4 * PER):
         ph, chis = schedule(step, e)
@@ -233,17 +236,34 @@ def main():
                 mios = apply_plan(ranks, plan, e, h, a, u)
                 version += 1
             window, T_ref, refined = False, None, False
+            T_target = min(T)                       # the plan aims every rank at T_min
+            T_window_max = max(T)
             rec["plan_after"] = plan_summary(plan, e)
         else:
             T = measure(ranks, chis, version)
             rec.update(mode="plan", per_rank_ms=[round(x, 4) for x in T])
             rec["step_ms"] = max(T) + t_comm + mig_model_ms(mios, h, n_layers)
-            if T_ref is None:
+            if T_ref is None and plan is not None and (min(T) < (1.0 - TRIGGER) * T_target or
+                                                       max(T) > (1.0 + TRIGGER) * T_window_max):
+                # on the first step under a plan, a rank runs > 10% below the
+                # T_min the plan aimed at, or > 10% above the unbalanced window's
+                # slowest rank: the slowdowns changed while the plan was being
+                # applied -- a new window, not a refine
+                window = True
+                rec["trigger"] = "off target"
+            elif T_ref is None:
                 T_ref = T
                 if plan is not None and not refined:
                     M = [R.gemm_ms(chis[r]) for r, R in enumerate(ranks)]
                     fresh = Z.ztp_plan(T, M, float(u), None, zopts)
-                    if int(fresh.z) > 0:
+                    # refine the plan's stragglers only: a normal task that is
+                    # now slower carries received units (Alg.2 keeps normal
+                    # tasks unpruned)
+                    for r in range(e):
+                        if int(plan.role[r]) == Z.NORMAL:
+                            fresh.gamma[r] = fresh.gamma_r[r] = 0.0
+                            fresh.role[r] = Z.NORMAL
+                    if any(fresh.gamma_r[r] > 0.0 for r in range(e)):
                         plan = Z.ztp_plan_refine(plan, fresh)
                         mios = apply_plan(ranks, plan, e, h, a, u)
                         version += 1
