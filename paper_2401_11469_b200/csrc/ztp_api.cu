@@ -37,6 +37,11 @@ struct ztp_ctx {
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_c = nullptr, ev_d = nullptr;
   int conc_bwd = 1;                    // ZTP_CONC (default 1): dW on the side stream, the SMs split by work
+  // ZTP_DW_SHARE: weight of the dW GEMM's MMA work in that split.  dW carries
+  // fixed costs dX does not (split-K partials + reduce, one unit per pair), so
+  // it gets more SMs than its MMA share: 1.2 measured best (1.0 / 1.2 / 1.3 /
+  // 1.4 / 1.5 / 1.6 / 0.8 swept, profiles/r01_dw_share_sweep_v*.txt)
+  double dw_share = 1.2;
   int sm_cap = 0;                      // > 0: SMs a GEMM launch may use (concurrent dX / dW partition)
   bool side_pending = false;           // side-stream work not yet joined into a caller stream
   void* skws_side = nullptr;           // split-K partials of side-stream GEMMs
@@ -611,14 +616,14 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_c, 0));
     sw = c->side_stream;
     // partition the SMs (in CTA pairs) in proportion to the two GEMMs' MMA
-    // work (tiles x 64-deep k-blocks), so both run at once and each one's
-    // fill and tail overlap the other's mainloop
+    // work (tiles x 64-deep k-blocks; dW's weighted by dw_share), so both run
+    // at once and each one's fill and tail overlap the other's mainloop
     const double rows = (double)std::min<int64_t>(nk, dxc ? nk : K);
     const double t_rows = std::ceil(rows / 256.0);
     const double w_dx = t_rows * std::ceil((double)N / 256.0) * std::ceil((double)n_y / 64.0);
     const double w_dw = t_rows * std::ceil((double)n_y / 256.0) * std::ceil((double)N / 64.0);
     const int pairs = c->num_sms / 2;
-    int px = (int)std::lround(pairs * w_dx / (w_dx + w_dw));
+    int px = (int)std::lround(pairs * w_dx / (w_dx + c->dw_share * w_dw));
     px = std::max(1, std::min(pairs - 1, px));
     cap_dx = 2 * px;
     cap_dw = 2 * (pairs - px);
@@ -761,6 +766,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* g4 = getenv("ZTP_GATHER4")) c->use_gather4 = atoi(g4) != 0;
   if (const char* sk = getenv("ZTP_SPLITK")) c->allow_splitk = atoi(sk) != 0;
   if (const char* cc = getenv("ZTP_CONC")) c->conc_bwd = atoi(cc) != 0;
+  if (const char* ds = getenv("ZTP_DW_SHARE")) c->dw_share = atof(ds);
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
   auto cleanup = [&](ztp_status s) {
