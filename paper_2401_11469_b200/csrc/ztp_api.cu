@@ -42,6 +42,12 @@ struct ztp_ctx {
   // it gets more SMs than its MMA share: 1.2 measured best (1.0 / 1.2 / 1.3 /
   // 1.4 / 1.5 / 1.6 / 0.8 swept, profiles/r01_dw_share_sweep_v*.txt)
   double dw_share = 1.2;
+  // While a concurrent dW is pending, the (non-persistent) core kernel is
+  // launched in plain stream order: under PDL its CTAs would sit resident on
+  // every free SM waiting for the dX GEMM, and the side-stream dW GEMM could
+  // not start on the SMs its predecessor frees (ZTP_SQUAT_GUARD=0: PDL anyway;
+  // the same guard on the side stream's split-K reduces measured no better)
+  int squat_guard = 1;
   int sm_cap = 0;                      // > 0: SMs a GEMM launch may use (concurrent dX / dW partition)
   bool side_pending = false;           // side-stream work not yet joined into a caller stream
   void* skws_side = nullptr;           // split-K partials of side-stream GEMMs
@@ -767,6 +773,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* sk = getenv("ZTP_SPLITK")) c->allow_splitk = atoi(sk) != 0;
   if (const char* cc = getenv("ZTP_CONC")) c->conc_bwd = atoi(cc) != 0;
   if (const char* ds = getenv("ZTP_DW_SHARE")) c->dw_share = atof(ds);
+  if (const char* sg = getenv("ZTP_SQUAT_GUARD")) c->squat_guard = atoi(sg) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
   auto cleanup = [&](ztp_status s) {
@@ -1037,7 +1044,7 @@ ztp_status ztp_core(ztp_ctx* c, ztp_phase phase, const ztp_mat* qkv, const ztp_m
   if (!(c->dbg_skip & 4)) {
     CUDA_TRY(c, ztp::core_launch(phase == ZTP_FWD ? 0 : 1, qkv->ptr, qkv->ld, cx->ptr, cx->ld, feat, n_out, qkv->cols,
                                  qkv->dtype, (phase == ZTP_FWD || v_compact) ? rows : nullptr, n_v, v_compact ? 1 : 0,
-                                 (cudaStream_t)stream));
+                                 (cudaStream_t)stream, !(c->side_pending && c->squat_guard)));
   }
   prof_end(c, pe, (cudaStream_t)stream);
   ++c->launches;

@@ -13,6 +13,24 @@ namespace ztp {
 // griddepcontrol.wait before touching memory (ztp_ptx.cuh pdl_wait).  Kept in
 // CUDA graphs as programmatic edges.  ZTP_PDL=0 turns it off (A/B timing).
 bool pdl_enabled();
+// launch_k_pdl(pdl = false): plain stream order.  Used where an early-
+// launched elementwise kernel would occupy (squat) SMs while it waits: its
+// CTAs would take the SMs a concurrent side-stream GEMM is waiting for.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Args&&... args) {
@@ -134,7 +152,7 @@ cudaError_t delay_launch(unsigned long long* stamp, double chi, unsigned long lo
 cudaError_t stamp_reset_launch(unsigned long long* stamp, cudaStream_t st);
 cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int64_t feat,
                         int64_t n_feat, int64_t N, int dtype, const int32_t* rows, int64_t n_v, int v_compact,
-                        cudaStream_t st);
+                        cudaStream_t st, bool pdl = true);
 cudaError_t gather_rows_launch(const void* src, int64_t ld_src, const int32_t* idx, int n, int64_t cols, void* dst,
                                int64_t ld_dst, int dtype, cudaStream_t st);
 cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* rows, int n, const int32_t* cols, int nc,

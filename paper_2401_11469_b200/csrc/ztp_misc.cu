@@ -129,14 +129,14 @@ __global__ void ztp_core_f32(int phase, float* qkv, int64_t ld_qkv, float* ctx, 
 
 cudaError_t core_launch(int phase, const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int64_t feat,
                         int64_t n_feat, int64_t N, int dtype, const int32_t* rows, int64_t n_v, int v_compact,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool pdl) {
   const int threads = 256;
   const int blocks = 148 * 8;
   if (dtype == 0)
-    return launch_k(ztp_core_bf16, blocks, threads, 0, st, phase, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)qkv,
-                    ld_qkv, (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N, rows, n_v, v_compact);
-  return launch_k(ztp_core_f32, blocks, threads, 0, st, phase, (float*)qkv, ld_qkv, (float*)ctx, ld_ctx, feat, n_feat,
-                  N, rows, n_v, v_compact);
+    return launch_k_pdl(pdl, ztp_core_bf16, blocks, threads, 0, st, phase, (const __nv_bfloat16*)qkv,
+                        (__nv_bfloat16*)qkv, ld_qkv, (__nv_bfloat16*)ctx, ld_ctx, feat, n_feat, N, rows, n_v, v_compact);
+  return launch_k_pdl(pdl, ztp_core_f32, blocks, threads, 0, st, phase, (float*)qkv, ld_qkv, (float*)ctx, ld_ctx, feat,
+                      n_feat, N, rows, n_v, v_compact);
 }
 
 // ------------------------------------------------- row compaction (a4 gather)
