@@ -220,6 +220,47 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None):
         Z.ztp_ctx_destroy(ctx)
 
 
+@pytest.mark.parametrize("env", [{"ZTP_CONC": "0"},
+                                 {"ZTP_SQUAT_GUARD": "0"},
+                                 {"ZTP_DW_SHARE": "0.8"},
+                                 {"ZTP_DW_SHARE": "1.6"}])
+def test_layer_schedule_variants_graph(tz, monkeypatch, env):
+    """The scheduling choices (concurrent vs serial dX / dW, the SM split
+    weight -- it changes the dW split-K counts -- and the core's stream-order
+    guard) change launch order and summation splits only: a captured step
+    under each still matches the oracle.  The knobs are read when a context
+    is created."""
+    torch, Z, ZtpLayer, _ = tz
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    h, f, N = 512, 2048, 1032
+    X, G, sh = make_inputs(h, f, N, 1, 17)
+    gam = [dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)]
+    sel, scores, nps = selections(1, h, f, N, 17, gam)
+    ref = O.layer_step(X, G, sh, sel)
+    ctx, L = build(tz, sh, 0, 1, h, f, N)
+    L.set_selection(nps[0], {s: torch.from_numpy(v).cuda() for s, v in scores[0].items()})
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        L.X.copy_(to_dev(torch, X))
+        L.G.copy_(to_dev(torch, G))
+        L.step(s)
+        L.Y.zero_()
+        L.dX.zero_()
+        L.dqkv.zero_()
+        L.capture(s)
+        for _ in range(2):
+            L.replay()
+    torch.cuda.synchronize()
+    close(host(L.Y), ref["Y"], "Y")
+    close(host(L.dX), ref["dX"], "dX")
+    close(host(L.dqkv), ref["dWqkv"][0], "dWqkv")
+    close(host(L.do), ref["dWo"][0], "dWo")
+    close(host(L.dw1[:, :f]), ref["dW1"][0], "dW1")
+    close(host(L.dw2[:f]), ref["dW2"][0], "dW2")
+    Z.ztp_ctx_destroy(ctx)
+
+
 def test_layer_tp2_straggler_resized(tz):
     """c1-like: TP=2, rank 1 resized at gamma = 0.25 (Zero imputation)."""
     g0 = dict(qkv=0.0, o=0.0, fc1=0.0, fc2=0.0)
