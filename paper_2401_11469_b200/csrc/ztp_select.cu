@@ -340,7 +340,10 @@ cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* k
   // stage keys in smem up to 48K keys (192 KB); longer segments re-read L2
   q.smem_keys = (maxlen > 8 * 1024 && maxlen <= SELECT_SMEM_KEYS) ? maxlen : 0;   // <= 8K: register path
   const int smem = q.smem_keys * 4;
-  if (smem > 48 * 1024 && smem > smem_set) {
+  // the opt-in covers dynamic + static shared memory: raise it for any staged
+  // launch (a 12288-key segment is exactly 48 KB dynamic, over the default
+  // 48 KB limit once the kernel's static arrays are added)
+  if (smem > 0 && smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(ztp_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     smem_set = smem;

@@ -97,6 +97,30 @@ def test_select_bitexact_random_segments(env, seed):
         po += nps[i]
 
 
+@pytest.mark.parametrize("L", [8193, 12000, 12288, 49152, 49153])
+def test_select_staging_boundaries(env, L):
+    """Segment lengths around the shared-memory staging limits of the select
+    kernel (register path <= 8K keys; staged keys up to 48K; 12288 keys =
+    exactly 48 KB of dynamic smem, the c4 TP=1 derived V segment), each as
+    the longest segment of its launch, bit-exact vs the oracle."""
+    Z, torch, ctx = env
+    lens = [L, 333]
+    parts = [I.lognormal_scores(7, f"b{L}", L, levels=16), I.lognormal_scores(7, "small", 333)]
+    nps = [L // 3, 100]
+    scores = dev(torch, np.concatenate(parts), torch.float32)
+    kept = torch.empty(sum(n - p for n, p in zip(lens, nps)), dtype=torch.int32, device="cuda")
+    pruned = torch.empty(sum(nps), dtype=torch.int32, device="cuda")
+    Z.ztp_select(ctx, lens, nps, scores, kept, pruned)
+    Z.ztp_sync(ctx)
+    kh, ph = kept.cpu().numpy(), pruned.cpu().numpy()
+    ko = po = 0
+    for i, n in enumerate(lens):
+        S, P = O.select(parts[i], nps[i])
+        assert np.array_equal(kh[ko:ko + n - nps[i]], S) and np.array_equal(ph[po:po + nps[i]], P), i
+        ko += n - nps[i]
+        po += nps[i]
+
+
 def test_select_nan_flag(env):
     Z, torch, ctx = env
     s = dev(torch, np.array([1.0, np.nan, 2.0], dtype=np.float32), torch.float32)
