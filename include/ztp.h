@@ -344,9 +344,13 @@ double ztp_pridiff_gamma(int64_t L, int64_t L_uni, double gamma_t, double alpha)
 ztp_status ztp_prepare(ztp_ctx* ctx, int n, const ztp_linear_args* const* args, const int32_t* what, void* stream);
 
 /* ztp_join: make `stream` wait for the library's internal side-stream work.
- * With ZTP_CONC=1 a BWD call runs its dW GEMM on an internal stream
- * concurrently with the dX GEMM (the SMs split in proportion to their work)
- * and returns without joining it, so the next linear's dX is not held back;
+ * With ZTP_CONC=1 (default) a BWD call runs its dW GEMM on an internal
+ * stream concurrently with the dX GEMM (the SMs split in proportion to their
+ * MMA work, dW's weighted by ZTP_DW_SHARE = 1.2 for its split-K costs) and
+ * returns without joining it, so the next linear's dX is not held back;
+ * while such work is pending, ztp_core launches in plain stream order (no
+ * programmatic early launch that would hold SMs the dW needs;
+ * ZTP_SQUAT_GUARD=0 disables that);
  * call ztp_join before reading dW on `stream` (a FWD call and ztp_migrate
  * join automatically; a step captured in a CUDA graph must end with it).
  * Errors: ZTP_EINVAL (null ctx), ZTP_ECUDA. */
