@@ -120,13 +120,13 @@ def _homog_counts(L, g: float) -> Dict[str, int]:
 
 
 def pretest(L, ctx, scores: Dict, *, gammas: Sequence[float] = GAMMAS, fracs: Sequence[float] = FRACS,
-            steps: int = 30, peer: Optional[int] = None, link_gbs: Optional[float] = None, ctx_rank: int = 0):
+            steps: int = 30, link_gbs: Optional[float] = None, ctx_rank: int = 0):
     """Run the pretest on this rank's layer `L` (a ZtpLayer built with
     mig_cap >= L.u * max(fracs)) and return (costs, report).
 
-    peer: the rank Phi_1's copies go to (None: local device copies on this
-    GPU -- the one-GPU stand-in); ctx_rank: the rank of `ctx` (ztp_migrate
-    acts on transfers naming it).  link_gbs: if given, Phi_1 is
+    Phi_1's copies are local device copies through ztp_migrate (src = dst =
+    ctx_rank, the rank of `ctx`): the one-GPU stand-in for the peer pulls of
+    a multi-GPU box.  link_gbs: if given, Phi_1 is
     additionally modelled as bytes / link_gbs + the measured per-call fixed
     cost, and the MODEL is what the returned costs use (a one-GPU run cannot
     time NVLink; report["phi1_measured"] keeps the local copies).
@@ -165,7 +165,6 @@ def pretest(L, ctx, scores: Dict, *, gammas: Sequence[float] = GAMMAS, fracs: Se
     L.set_migration(MigrationIO())
     L.set_selection(_homog_counts(L, 0.0), scores)
     # ---- Phi_1: weight slices out + dW slices back for n units
-    dst = ctx_rank if peer is None else peer
     stream = torch.cuda.Stream()
     fixed = None
     for fr in sorted(set(list(fracs))):
@@ -177,7 +176,7 @@ def pretest(L, ctx, scores: Dict, *, gammas: Sequence[float] = GAMMAS, fracs: Se
                 (L.w1_t, L.w1_t, 0, 0, h, n, 0, u), (L.w2_t, L.w2_t, 0, 0, n, h, u, 0),
                 (L.dw1, L.dw1, 0, u, h, n, 0, 0), (L.dw2, L.dw2, u, 0, n, h, 0, 0)):
             xs.append(Z.xfer(t_src, t_dst, r0=r0, c0=c0, nr=nr, nc=nc, dr0=dr0, dc0=dc0,
-                             src_rank=ctx_rank, dst_rank=dst))
+                             src_rank=ctx_rank, dst_rank=ctx_rank))
         for _ in range(3):
             Z.ztp_migrate(ctx, xs, stream)
         torch.cuda.synchronize()
