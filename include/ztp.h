@@ -157,21 +157,72 @@ void ztp_plan_opts_default(ztp_plan_opts* o);
 ztp_status ztp_plan(int world, const double* T, const double* M, double L_ref,
                     const ztp_costs* costs, const ztp_plan_opts* opts, ztp_plan_t* out);
 
-/* ztp_plan_refine: statistics refresh of a plan (A-8, A-39, A-42).
- * When a rank's runtime moves by > 10% after `prev` was applied, the new
- * window (T, M measured WITH prev in effect) gives `fresh` = ztp_plan(...)
+/* ztp_plan_refine: statistics refresh of a plan (A-8, A-39, A-42, A-43).
+ * The window (T, M measured WITH prev in effect) gives `fresh` = ztp_plan(...)
  * (ZERO-only) whose Eq.1 ratio is a fraction of the work the rank still
- * computes, so the kept fractions compose:
- *   resizing ranks: gamma = gamma_r = min(1 - (1 - prev.gamma_r[r]) (1 - fresh.gamma_r[r]), gamma_max),
+ * computes, so the kept fractions of prev's STRAGGLERS compose:
+ *   RESIZE ranks of prev: gamma = gamma_r = min(1 - (1 - prev.gamma_r[r]) (1 - fresh.gamma_r[r]), gamma_max),
  *                   role RESIZE iff gamma > 0;
  *   MIGRATE / SPLIT ranks of prev (A-42): their whole shed fraction composes,
  *                   gamma = min(1 - (1 - prev.gamma[r]) (1 - fresh.gamma_r[r]), gamma_max), beta kept,
  *                   phi = gamma beta, gamma_r = gamma (1 - beta) / (1 - gamma beta), role kept;
- * z is fresh's; order and x are prev's when prev migrates (same sender order),
- * else fresh's order and x = 0.  Host-only, bit-deterministic.
+ *   NORMAL ranks of prev (A-43): stay NORMAL with gamma = 0, whatever fresh
+ *                   says -- Alg.2 resizes only the plan's stragglers
+ *                   and a receiver's extra time is received, loss-free work
+ *                   (P:233); only a new statistics window re-plans them.
+ * fresh's tolerance eps is the dead band: a straggler within T_min (1 + eps)
+ * of the fresh window has fresh.gamma_r = 0 and keeps its ratio.
+ * z and x are prev's; order is prev's when prev migrates (same sender order),
+ * else fresh's.  Host-only, bit-deterministic.
  * Errors: ZTP_EINVAL (null, world mismatch), ZTP_EUNSUPPORTED (fresh has a
  * MIGRATE / SPLIT role: the refresh plan must be ZERO-only). */
 ztp_status ztp_plan_refine(const ztp_plan_t* prev, const ztp_plan_t* fresh, double gamma_max, ztp_plan_t* out);
+
+/* ---------------------------------------------------------------------------
+ * a1/a2 controller: the statistics-driven re-planning loop of P:171-178 and
+ * Alg.2 l.2 (reading A-41), one call per step on every rank with the
+ * all-gathered T, M of the step just run under ctl->plan.  Pure host state
+ * machine (plain struct, copyable, bit-deterministic), so every rank holds the
+ * same plan without further communication.
+ *   WINDOW  the step ran un-resized (plan all NORMAL): ctl->plan = ztp_plan(T,
+ *           M, L_ref, costs, opts->plan) (Eq.1 / Alg.2 are defined on
+ *           un-resized runtimes); T_target = min T, T_wmax = max T -> FIRST.
+ *   FIRST   first step under a plan: if it is off target (some rank below
+ *           (1 - trigger) T_target or above (1 + trigger) T_wmax: the
+ *           slowdowns changed while it was applied) the plan is lifted ->
+ *           WINDOW.  Else, up to max_refines times, ztp_plan_refine(plan,
+ *           ztp_plan(T, M, ZERO-only, T_min criterion)) (A-39, A-42, A-43);
+ *           a changed plan stays in FIRST, an unchanged one sets T_ref = T
+ *           -> MONITOR.
+ *   MONITOR any rank with |T_r - T_ref_r| > trigger T_ref_r (P:178's "over-10%
+ *           increase", either direction, A-8) lifts the plan -> WINDOW (a
+ *           rank whose slowdown vanished must return to gamma = 0).
+ * *action = ZTP_CTL_APPLY when ctl->plan changed (the caller applies it before
+ * the next step: ztp_plan_counts, ztp_select, ztp_migrate), else KEEP.
+ * Errors: EINVAL (null, T not finite or <= 0), and ztp_plan's errors. */
+enum { ZTP_CTL_WINDOW = 0, ZTP_CTL_FIRST = 1, ZTP_CTL_MONITOR = 2 };
+enum { ZTP_CTL_KEEP = 0, ZTP_CTL_APPLY = 1 };
+
+typedef struct ztp_ctl_opts {
+  ztp_plan_opts plan;          /* window plan (SEMI or ZERO-only, criterion, eps, gamma_max, ...) */
+  double L_ref;                /* Eq.2 / Eq.3 reference column count (A-25) */
+  double trigger;              /* 0.10 */
+  int32_t max_refines;         /* refreshes of one plan before monitoring (1) */
+  int32_t _pad;
+} ztp_ctl_opts;
+
+typedef struct ztp_ctl {
+  int32_t world, state, refines, _pad;
+  ztp_plan_t plan;             /* the plan in effect for the next step */
+  double T_ref[ZTP_MAX_RANKS]; /* monitoring reference */
+  double T_target, T_wmax;     /* the window's T_min and T_max */
+  int64_t steps, windows, replans, refine_count, triggers;
+} ztp_ctl;
+
+void ztp_ctl_opts_default(ztp_ctl_opts* o);
+ztp_status ztp_ctl_init(ztp_ctl* ctl, int world);
+ztp_status ztp_ctl_step(ztp_ctl* ctl, const ztp_ctl_opts* opts, const ztp_costs* costs, const double* T,
+                        const double* M, int32_t* action);
 
 /* ztp_plan_counts: integer realisation of a plan for one linear of `rank`.
  *   K       contraction length of this rank's linear (col: d_in; row: d_in/e)
@@ -193,6 +244,45 @@ typedef struct ztp_counts {
 
 ztp_status ztp_plan_counts(const ztp_plan_t* plan, int rank, int64_t K, int64_t n_units,
                            int64_t unit, int is_row, ztp_counts* out);
+
+/* ztp_layer_prune_counts: the four prune counts of one transformer layer of
+ * `rank` (h hidden, a = h/e attention features, u = f/e MLP units per rank),
+ * out = {QKV (K = h), O (K = a), FC1 (K = h), FC2 (K_rem = u - n_mig)}.
+ * MLP: ztp_plan_counts with gamma_r (FC2 is a row layer).  Attention (A-37):
+ * heads do not migrate in this build (A-26), so a MIGRATE / SPLIT rank
+ * resizes QKV and O by its Eq.1 gamma -- its remaining attention work is
+ * (1 - gamma), like its MLP's after migration; other ranks by gamma_r.
+ * Host-only.  Errors: EINVAL (null, rank, sizes). */
+ztp_status ztp_layer_prune_counts(const ztp_plan_t* plan, int rank, int64_t h, int64_t a, int64_t u,
+                                  int32_t out[4]);
+
+/* ztp_plan_uniform: every rank RESIZE with gamma (homogeneous resizing, the
+ * paper's E2 setting P:344; NORMAL if gamma = 0).  EINVAL for gamma outside
+ * [0, 1) or world outside 1..8. */
+ztp_status ztp_plan_uniform(int world, double gamma, ztp_plan_t* out);
+
+/* ztp_pridiff_counts: NEXT-1 PriDiff prune count of a segment of L columns
+ * with L_uni columns above the variation threshold (Alg.1 l.9-11):
+ * gamma_k = max(1 - L_uni / L, alpha gamma_t), clamped to [0, gamma_max]
+ * (A-4), n_prune = floor(L gamma_k + 0.5) <= L - 1 (A-3, >= 1 survives).
+ * Returns 0 for L < 1. */
+int32_t ztp_pridiff_counts(int64_t L, int64_t L_uni, double gamma_t, double alpha, double gamma_max);
+
+/* ztp_costs_fit: Alg.2 l.1 pretest samples -> the Eq.2 / Eq.3 cost model
+ * (A-40).  omega: (pruned units n, extra non-GEMM time vs the dense step);
+ * Omega_1 = the extra at the smallest n > 0 ("static space allocation
+ * overhead", clamped >= 0), Omega_2(n) = extra(n) - Omega_1.  phi1: (migrated
+ * units, time); phi2: (units received by one helper, time).  Each function
+ * becomes non-decreasing piecewise linear through (0, 0): x ascending, x <= 0
+ * and repeated x dropped, y the running max clamped at 0 (a cost cannot
+ * shrink with more units; a dip is timing noise); a function without samples
+ * is the zero line through (0,0), (1,0).  xs / ys: caller arrays of 3 cap
+ * doubles that receive the points (function k at offset k cap); out's
+ * ztp_pwl pointers point into them.  Errors: EINVAL (null, non-finite
+ * sample, cap < max(n) + 2). */
+ztp_status ztp_costs_fit(int n_omega, const double* omega_x, const double* omega_y, int n_phi1,
+                         const double* phi1_x, const double* phi1_y, int n_phi2, const double* phi2_x,
+                         const double* phi2_y, int cap, double* xs, double* ys, ztp_costs* out);
 
 /* ---------------------------------------------------------------------------
  * a1. Statistics exchange (Alg.1 l.1 / Alg.2 l.2): all-gather of (T_i, M_i)
@@ -351,8 +441,11 @@ ztp_status ztp_prepare(ztp_ctx* ctx, int n, const ztp_linear_args* const* args, 
  * while such work is pending, ztp_core launches in plain stream order (no
  * programmatic early launch that would hold SMs the dW needs;
  * ZTP_SQUAT_GUARD=0 disables that);
- * call ztp_join before reading dW on `stream` (a FWD call and ztp_migrate
- * join automatically; a step captured in a CUDA graph must end with it).
+ * call ztp_join before reading dW on `stream` (a FWD call, ztp_migrate,
+ * ztp_select, ztp_prepare and ztp_priority_update join automatically; a step
+ * captured in a CUDA graph must end with it).  Until then the caller must not
+ * modify a BWD call's inputs (x_t / xs_t, g_t) nor its lineage lists by
+ * other means than these calls.
  * Errors: ZTP_EINVAL (null ctx), ZTP_ECUDA. */
 ztp_status ztp_join(ztp_ctx* ctx, void* stream);
 
@@ -395,8 +488,11 @@ ztp_status ztp_migrate(ztp_ctx* ctx, int n, const ztp_xfer* xfers, void* stream)
  * Straggler emulation and GEMM statistics (A-32).  chi > 1 makes every
  * GEMM this context launches run chi times longer: a one-thread delay kernel
  * after each GEMM spins until start + chi (end - start), where start/end are
- * the GEMM's own %globaltimer stamps.  M (A-6) accumulates GEMM + delay time
- * on the device; ztp_read_gemm_ns syncs `stream`, returns and resets it.
+ * the GEMM's own %globaltimer stamps (the side stream's concurrent dW GEMM
+ * has its own stamp slot, so a slowed rank runs the same concurrent dX / dW
+ * schedule as an unslowed one).  M (A-6) accumulates GEMM + delay time on the
+ * device, overlapping GEMMs counted once (union of their intervals);
+ * ztp_read_gemm_ns syncs `stream`, returns and resets it.
  * ------------------------------------------------------------------------- */
 ztp_status ztp_set_slowdown(ztp_ctx* ctx, double chi);
 /* on = 1: stamp every GEMM and accumulate M even when chi == 1 (statistics

@@ -139,16 +139,23 @@ def plan_refine(prev: Plan, fresh: Plan, gamma_max: float = 0.9) -> Plan:
     A-42: a rank that sheds work by migration (MIGRATE / SPLIT) composes its
     whole shed fraction gamma the same way and keeps its Eq.2 split beta:
     phi = gamma beta, gamma_r = gamma (1 - beta) / (1 - gamma beta) (A-16);
-    the plan keeps prev's migration group (x) and sender order."""
+    the plan keeps prev's migration group (x) and sender order.
+    A-43: only prev's stragglers are refined.  A NORMAL task of prev stays
+    NORMAL with gamma 0 whatever the fresh window says: Alg.2 resizes only the
+    z - x stragglers, and a receiver's extra runtime is received work
+    that migration makes loss-free.  The fresh plan's tolerance eps is
+    the dead band (a straggler within T_min (1 + eps) gets fresh gamma 0)."""
     if prev.world != fresh.world:
         raise OracleError("ZTP_EINVAL", "world mismatch")
     e = fresh.world
     if any(x in (MIGRATE, SPLIT) for x in list(fresh.role[:e])):
         raise OracleError("ZTP_EUNSUPPORTED", "the refresh plan must be ZERO-only (A-39, A-42)")
     semi = any(x in (MIGRATE, SPLIT) for x in list(prev.role[:e]))
-    out = Plan(world=e, z=fresh.z, x=prev.x if semi else 0, order=list(prev.order if semi else fresh.order),
+    out = Plan(world=e, z=prev.z, x=prev.x if semi else 0, order=list(prev.order if semi else fresh.order),
                role=[NORMAL] * e, gamma=[0.0] * e, beta=[0.0] * e, phi=[0.0] * e, gamma_r=[0.0] * e)
     for r in range(e):
+        if prev.role[r] == NORMAL:
+            continue                                   # A-43: stays NORMAL, gamma 0
         sheds = prev.role[r] in (MIGRATE, SPLIT)
         keep = (1.0 - (prev.gamma[r] if sheds else prev.gamma_r[r])) * (1.0 - fresh.gamma_r[r])
         g = 1.0 - keep
@@ -291,6 +298,119 @@ def plan(T, M, L_ref: float, costs: Costs, opts: PlanOpts) -> Plan:
     return p
 
 
+CTL_WINDOW, CTL_FIRST, CTL_MONITOR = 0, 1, 2
+CTL_KEEP, CTL_APPLY = 0, 1
+
+
+def dense_plan(e: int) -> Plan:
+    return Plan(world=e, order=list(range(e)), role=[NORMAL] * e, gamma=[0.0] * e, beta=[0.0] * e,
+                phi=[0.0] * e, gamma_r=[0.0] * e)
+
+
+@dataclass
+class CtlOpts:
+    plan: PlanOpts = field(default_factory=PlanOpts)
+    L_ref: float = 1.0
+    trigger: float = 0.10          # P:178 "over-10% increase"
+    max_refines: int = 1
+
+
+class Controller:
+    """The statistics-driven re-planning loop (Alg.2 l.2; reading
+    A-41), written as the three-state machine it is:
+
+    WINDOW   the step ran un-resized: plan = Alg.1/Alg.2 on its T, M (Eq.1 and
+             Alg.2 are defined on un-resized runtimes); remember the window's
+             T_min (the plan's target) and T_max.
+    FIRST    first step under the plan.  Off target -- some rank below
+             (1 - trigger) T_min or above (1 + trigger) T_max of the window: the
+             slowdowns changed while the plan was applied -- lift it (WINDOW).
+             Otherwise refresh it once (plan_refine on a ZERO-only T_min plan of
+             this step, A-39/A-42/A-43); if the plan changed judge its first step
+             again, else this step is the monitoring reference.
+    MONITOR  a relative runtime change > trigger of any rank against the
+             reference, in either direction (A-8), lifts the plan.
+
+    step() returns CTL_APPLY when the plan for the next step changed."""
+
+    def __init__(self, world: int):
+        if not 1 <= world <= 8:
+            raise OracleError("ZTP_EINVAL", "world outside 1..8")
+        self.world = world
+        self.state = CTL_WINDOW
+        self.refines = 0
+        self.plan = dense_plan(world)
+        self.T_ref = [0.0] * world
+        self.T_target = 0.0
+        self.T_wmax = 0.0
+        self.steps = self.windows = self.replans = self.refine_count = self.triggers = 0
+
+    @staticmethod
+    def _dense(p: Plan) -> bool:
+        return all(x == NORMAL for x in p.role[:p.world])
+
+    @staticmethod
+    def _same(a: Plan, b: Plan) -> bool:
+        e = a.world
+        return (a.x == b.x and a.role[:e] == b.role[:e] and a.gamma[:e] == b.gamma[:e]
+                and a.gamma_r[:e] == b.gamma_r[:e] and a.beta[:e] == b.beta[:e] and a.phi[:e] == b.phi[:e])
+
+    def step(self, T, M, opts: CtlOpts, costs: Costs = None) -> int:
+        e = self.world
+        for t in T[:e]:
+            if not (math.isfinite(t) and t > 0.0):
+                raise OracleError("ZTP_EINVAL", "T must be finite and > 0")
+        trig = opts.trigger
+        self.steps += 1
+        Tmin = min(T[:e])
+        Tmax = max(T[:e])
+        action = CTL_KEEP
+
+        def lift():
+            nonlocal action
+            if not self._dense(self.plan):
+                action = CTL_APPLY
+            self.plan = dense_plan(e)
+            self.state = CTL_WINDOW
+
+        if self.state == CTL_WINDOW:
+            p = plan(list(T[:e]), list(M[:e]), opts.L_ref, costs if costs is not None else Costs(), opts.plan)
+            self.windows += 1
+            if not self._dense(p):
+                self.plan = p
+                self.replans += 1
+                action = CTL_APPLY
+            self.T_target, self.T_wmax = Tmin, Tmax
+            self.refines = 0
+            self.state = CTL_FIRST
+            return action
+        if self.state == CTL_FIRST:
+            if not self._dense(self.plan) and (Tmin < (1.0 - trig) * self.T_target or
+                                               Tmax > (1.0 + trig) * self.T_wmax):
+                lift()
+                return action
+            if not self._dense(self.plan) and self.refines < opts.max_refines:
+                zo = PlanOpts(enable_migration=0, zero_crit=CRIT_MIN, gamma_max=opts.plan.gamma_max,
+                              eps=opts.plan.eps, gamma_tol=opts.plan.gamma_tol, bisect_iters=opts.plan.bisect_iters,
+                              force_lambda=opts.plan.force_lambda)
+                fresh = plan(list(T[:e]), list(M[:e]), opts.L_ref, Costs(), zo)
+                ref = plan_refine(self.plan, fresh, opts.plan.gamma_max)
+                self.refines += 1
+                if not self._same(ref, self.plan):
+                    self.plan = ref
+                    self.refine_count += 1
+                    return CTL_APPLY
+            self.T_ref = list(T[:e])
+            self.state = CTL_MONITOR
+            return action
+        for r in range(e):
+            if abs(T[r] - self.T_ref[r]) / self.T_ref[r] > trig:
+                self.triggers += 1
+                lift()
+                return action
+        return action
+
+
 @dataclass
 class Counts:
     n_prune: int = 0
@@ -348,6 +468,68 @@ def plan_counts(p: Plan, rank: int, K: int, n_units: int, unit: int, is_row: boo
                     c.inc.append((s, lo, lo + cnt))
             lo += cnt
     return c
+
+
+def layer_prune_counts(p: Plan, rank: int, h: int, a: int, u: int) -> dict:
+    """The four prune counts of one layer (SURVEY §8(a) layer): MLP by
+    plan_counts (FC1 col over K = h, FC2 row over K_rem = u - n_mig).
+    Attention, reading A-37: heads never migrate (A-26), so a rank that sheds
+    MLP units (MIGRATE / SPLIT) keeps (1 - gamma) of its attention work by
+    resizing QKV (K = h) and O (K = a) with its Eq.1 gamma; other ranks use
+    gamma_r, as for FC1."""
+    g_att = p.gamma[rank] if p.role[rank] in (MIGRATE, SPLIT) else p.gamma_r[rank]
+
+    def att(K):
+        n = int(math.floor(float(K) * g_att + 0.5))
+        return max(0, min(n, K - 1))
+    return {"qkv": att(h), "o": att(a),
+            "fc1": plan_counts(p, rank, h, u, 1, False).n_prune,
+            "fc2": plan_counts(p, rank, u, u, 1, True).n_prune}
+
+
+def plan_uniform(e: int, gamma: float) -> Plan:
+    """Homogeneous resizing (E2): every rank RESIZE with gamma."""
+    if not (0.0 <= gamma < 1.0):
+        raise OracleError("ZTP_EINVAL", "gamma outside [0, 1)")
+    return Plan(world=e, order=list(range(e)), role=[RESIZE if gamma > 0 else NORMAL] * e, gamma=[gamma] * e,
+                beta=[0.0] * e, phi=[0.0] * e, gamma_r=[gamma] * e)
+
+
+def pridiff_counts(L: int, L_uni: int, gamma_t: float, alpha: float = 0.8, gamma_max: float = 0.9) -> int:
+    """Alg.1 l.10-11 ratio max(1 - L_uni/L, alpha gamma_t), clamped to
+    [0, gamma_max] (A-4), as a prune count floor(L g + 0.5) <= L - 1 (A-3)."""
+    if L < 1:
+        return 0
+    g = max(1.0 - L_uni / L, alpha * gamma_t)
+    g = min(max(g, 0.0), gamma_max)
+    return min(int(math.floor(L * g + 0.5)), L - 1)
+
+
+def costs_fit(omega, phi1, phi2):
+    """Alg.2 l.1 pretest samples -> Costs (reading A-40).  Omega_1 is the extra
+    cost at the smallest pruned count n > 0 ("static space allocation
+    overhead"), clamped at 0; Omega_2(n) = extra(n) - Omega_1 (P:258
+    "proportionally increased dimension extracting cost").  Every function
+    passes through (0, 0) and is non-decreasing: samples with x <= 0 or an x
+    already seen are dropped, y is the running maximum clamped at 0; a
+    function without samples is the zero line (0,0)-(1,0)."""
+    def mono(pts):
+        xs, ys = [0.0], [0.0]
+        for x, y in sorted((float(a), float(b)) for a, b in pts):
+            if x > xs[-1]:
+                xs.append(x)
+                ys.append(max(ys[-1], y, 0.0))
+        if len(xs) < 2:
+            xs.append(1.0)
+            ys.append(0.0)
+        return (tuple(xs), tuple(ys))
+    for pts in (omega, phi1, phi2):
+        for x, y in pts:
+            if not (math.isfinite(x) and math.isfinite(y)):
+                raise OracleError("ZTP_EINVAL", "non-finite sample")
+    pos = sorted(((float(x), float(y)) for x, y in omega if x > 0), key=lambda t: t[0])
+    om1 = max(pos[0][1], 0.0) if pos else 0.0
+    return Costs(om1, mono([(x, y - om1) for x, y in pos]), mono(phi1), mono(phi2))
 
 
 # ----------------------------------------------------------------------------

@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 
 from . import _lib
 from ._lib import (ACT_GELU, ACT_GELU_D, ACT_NONE, BF16, BWD, CRIT_AVG, CRIT_MIN, F32, FWD, IMPUTE_AVERAGE, IMPUTE_SAME,  # noqa
-                   IMPUTE_ZERO, KIND_DW, KIND_DX, KIND_FWD, MIGRATE, NORMAL, RESIZE, SPLIT, Costs, Counts,
+                   IMPUTE_ZERO, KIND_DW, KIND_DX, KIND_FWD, MIGRATE, NORMAL, RESIZE, SPLIT, Costs, Counts, Ctl, CtlOpts,
                    LinearArgs, Mat, PlanOpts, PlanT, Pwl, Sel, Xfer, ZtpError, check, lib)
 
 __all__ = [
@@ -119,10 +119,79 @@ def ztp_plan_refine(prev: PlanT, fresh: PlanT, gamma_max: float = 0.9) -> PlanT:
     return out
 
 
+CTL_WINDOW, CTL_FIRST, CTL_MONITOR = 0, 1, 2
+CTL_KEEP, CTL_APPLY = 0, 1
+
+
+def ctl_opts(L_ref: float = 1.0, trigger: float = 0.10, max_refines: int = 1, **plan_kw) -> CtlOpts:
+    o = CtlOpts()
+    lib.ztp_ctl_opts_default(C.byref(o))
+    o.plan = plan_opts(**plan_kw)
+    o.L_ref, o.trigger, o.max_refines = L_ref, trigger, max_refines
+    return o
+
+
+def ztp_ctl_init(world: int) -> Ctl:
+    c = Ctl()
+    check(lib.ztp_ctl_init(C.byref(c), world))
+    return c
+
+
+def ztp_ctl_step(ctl: Ctl, opts: CtlOpts, T: Sequence[float], M: Sequence[float], costs=None) -> int:
+    """One controller step (include/ztp.h): T, M of the step just run under
+    ctl.plan (all ranks', all-gathered); returns CTL_APPLY if ctl.plan changed."""
+    e = ctl.world
+    Ta = (C.c_double * e)(*T[:e])
+    Ma = (C.c_double * e)(*M[:e])
+    if costs is None:
+        costs = make_costs()
+    c, _keep = costs if isinstance(costs, tuple) else (costs, None)
+    act = C.c_int32()
+    check(lib.ztp_ctl_step(C.byref(ctl), C.byref(opts), C.byref(c), Ta, Ma, C.byref(act)))
+    return int(act.value)
+
+
 def ztp_plan_counts(plan: PlanT, rank: int, K: int, n_units: int, unit: int = 1, is_row: bool = False) -> Counts:
     out = Counts()
     check(lib.ztp_plan_counts(C.byref(plan), rank, K, n_units, unit, int(is_row), C.byref(out)))
     return out
+
+
+SEGS = ("qkv", "o", "fc1", "fc2")
+
+
+def ztp_layer_prune_counts(plan: PlanT, rank: int, h: int, a: int, u: int) -> dict:
+    """{qkv, o, fc1, fc2} prune counts of one layer of `rank` (A-37 attention rule)."""
+    out = (C.c_int32 * 4)()
+    check(lib.ztp_layer_prune_counts(C.byref(plan), rank, h, a, u, out))
+    return dict(zip(SEGS, (int(v) for v in out)))
+
+
+def ztp_plan_uniform(world: int, gamma: float) -> PlanT:
+    out = PlanT()
+    check(lib.ztp_plan_uniform(world, gamma, C.byref(out)))
+    return out
+
+
+def ztp_pridiff_counts(L: int, L_uni: int, gamma_t: float, alpha: float = 0.8, gamma_max: float = 0.9) -> int:
+    return int(lib.ztp_pridiff_counts(L, L_uni, gamma_t, alpha, gamma_max))
+
+
+def ztp_costs_fit(omega, phi1, phi2):
+    """Pretest samples [(x, y)] -> (Costs, keepalive, plain dict) via the C fit (A-40)."""
+    def arr(pts, k):
+        return (C.c_double * max(len(pts), 1))(*[float(p[k]) for p in pts])
+    cap = max(len(omega), len(phi1), len(phi2)) + 2
+    xs, ys = (C.c_double * (3 * cap))(), (C.c_double * (3 * cap))()
+    out = Costs()
+    keep = [arr(omega, 0), arr(omega, 1), arr(phi1, 0), arr(phi1, 1), arr(phi2, 0), arr(phi2, 1), xs, ys]
+    check(lib.ztp_costs_fit(len(omega), keep[0], keep[1], len(phi1), keep[2], keep[3], len(phi2), keep[4],
+                            keep[5], cap, xs, ys, C.byref(out)))
+    plain = {"omega1": out.omega1}
+    for name in ("omega2", "phi1", "phi2"):
+        f = getattr(out, name)
+        plain[name] = (tuple(f.x[i] for i in range(f.n)), tuple(f.y[i] for i in range(f.n)))
+    return (out, keep), plain
 
 
 def ztp_allgather_stats(ctx, T_own: float, M_own: float, world: int, stream=None):

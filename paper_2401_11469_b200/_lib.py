@@ -57,6 +57,18 @@ class PlanT(C.Structure):
                 ("gamma_r", C.c_double * MAX_RANKS)]
 
 
+class CtlOpts(C.Structure):
+    _fields_ = [("plan", PlanOpts), ("L_ref", C.c_double), ("trigger", C.c_double), ("max_refines", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class Ctl(C.Structure):
+    _fields_ = [("world", C.c_int32), ("state", C.c_int32), ("refines", C.c_int32), ("_pad", C.c_int32),
+                ("plan", PlanT), ("T_ref", C.c_double * MAX_RANKS), ("T_target", C.c_double),
+                ("T_wmax", C.c_double), ("steps", C.c_int64), ("windows", C.c_int64), ("replans", C.c_int64),
+                ("refine_count", C.c_int64), ("triggers", C.c_int64)]
+
+
 class Counts(C.Structure):
     _fields_ = [("n_prune", C.c_int32), ("n_mig", C.c_int32), ("n_out", C.c_int32),
                 ("out_dst", C.c_int32 * MAX_RANKS), ("out_lo", C.c_int64 * MAX_RANKS),
@@ -111,6 +123,18 @@ def _load():
         "ztp_plan": (st, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double,
                           C.POINTER(Costs), C.POINTER(PlanOpts), C.POINTER(PlanT)]),
         "ztp_plan_refine": (st, [C.POINTER(PlanT), C.POINTER(PlanT), C.c_double, C.POINTER(PlanT)]),
+        "ztp_ctl_opts_default": (None, [C.POINTER(CtlOpts)]),
+        "ztp_ctl_init": (st, [C.POINTER(Ctl), C.c_int]),
+        "ztp_ctl_step": (st, [C.POINTER(Ctl), C.POINTER(CtlOpts), C.POINTER(Costs), C.POINTER(C.c_double),
+                              C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+        "ztp_layer_prune_counts": (st, [C.POINTER(PlanT), C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                        C.POINTER(C.c_int32)]),
+        "ztp_plan_uniform": (st, [C.c_int, C.c_double, C.POINTER(PlanT)]),
+        "ztp_pridiff_counts": (C.c_int32, [C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double]),
+        "ztp_costs_fit": (st, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int,
+                               C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double),
+                               C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                               C.POINTER(Costs)]),
         "ztp_plan_counts": (st, [C.POINTER(PlanT), C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                  C.POINTER(Counts)]),
         "ztp_allgather_stats": (st, [vp, C.c_double, C.c_double, C.POINTER(C.c_double),
@@ -146,7 +170,8 @@ lib = _load()
 # every symbol include/ztp.h declares (checked by tests/test_abi.py)
 EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_id", "ztp_ctx_create",
             "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count", "ztp_plan_opts_default", "ztp_plan", "ztp_plan_refine",
-            "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_join", "ztp_col_linear", "ztp_row_linear",
+            "ztp_ctl_opts_default", "ztp_ctl_init", "ztp_ctl_step", "ztp_plan_counts",
+            "ztp_layer_prune_counts", "ztp_plan_uniform", "ztp_pridiff_counts", "ztp_costs_fit", "ztp_allgather_stats", "ztp_select", "ztp_join", "ztp_col_linear", "ztp_row_linear",
             "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "ztp_prepare",
             "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",
             "ztp_set_profile", "ztp_read_profile")

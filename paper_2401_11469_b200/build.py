@@ -44,9 +44,15 @@ def build(force: bool = False, verbose: bool = True) -> str:
     os.makedirs(bdir, exist_ok=True)
     common = ["-std=c++17", "-O3", "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
               "-I", inc]
+    hdr_t = max(os.path.getmtime(d) for d in [os.path.join(CSRC, h) for h in HEADERS] +
+                [os.path.join(ROOT, "include", "ztp.h")])
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(bdir, s + ".o")
+        objs.append(obj)
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t)
+                and os.environ.get("ZTP_REBUILD_ALL") != "1"):
+            continue
         if s.endswith(".cu"):
             cmd = [nvcc(), "-c", src, "-o", obj, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
                    "--expt-relaxed-constexpr", "-Xptxas", "-v" if os.environ.get("ZTP_PTXAS_V") else "-O3"] + common
@@ -55,7 +61,6 @@ def build(force: bool = False, verbose: bool = True) -> str:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-        objs.append(obj)
     link = [nvcc(), "-shared", "-o", LIB] + objs + ["-gencode", "arch=compute_100a,code=sm_100a", "-L", libdir,
                                                     "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}",
                                                     "-Xcompiler", "-fPIC"]

@@ -170,9 +170,13 @@ ztp_status ensure_ws(ztp_ctx* c, size_t bytes) {
 
 bool emulating(const ztp_ctx* c) { return c->chi > 1.0 || c->stats; }
 
+// Stamp slot of a GEMM: the side stream (concurrent dW) has its own, so a
+// slowed rank keeps the concurrent dX / dW schedule of an unslowed one.
+unsigned long long* stamp_slot(ztp_ctx* c, cudaStream_t st) { return c->d_stamp + (st == c->side_stream ? 2 : 0); }
+
 ztp_status after_gemm(ztp_ctx* c, cudaStream_t st) {
   if (!emulating(c)) return ZTP_OK;
-  CUDA_TRY(c, ztp::delay_launch(c->d_stamp, c->chi, c->d_gemm_ns, st));
+  CUDA_TRY(c, ztp::delay_launch(stamp_slot(c, st), c->chi, c->d_gemm_ns, st));
   ++c->launches;
   return ZTP_OK;
 }
@@ -289,7 +293,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     // identity row map: compact outputs, or a dense lineage (S = 0..K-1)
     p.out_dense = out_compact || (kind == ztp::KIND_FWD ? out_pos == nullptr
                                                         : (kept == c->d_iota && pruned == nullptr && M <= nk));
-    p.stamp = emulating(c) ? c->d_stamp : nullptr;
+    p.stamp = emulating(c) ? stamp_slot(c, st) : nullptr;
     p.dbg = c->dbg_epi;
     p.col_pos = col_pos;
     p.n_full = n_full;
@@ -610,11 +614,10 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("g_t", g));
   const int64_t N = g.cols;
   if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
-  // dW concurrently with dX on the side stream (not while emulating a
-  // straggler -- the slowdown stamps one GEMM at a time -- nor while profiling,
-  // which times each GEMM alone)
-  const bool conc = c->conc_bwd && c->prof_on != 1 && a->dx_t.ptr && a->dw_t.ptr && !emulating(c) &&
-                    dtype == ZTP_BF16;
+  // dW concurrently with dX on the side stream (also on an emulated
+  // straggler: each GEMM is stretched from its own stamp slot; not while
+  // profiling with events, which times each GEMM alone)
+  const bool conc = c->conc_bwd && c->prof_on != 1 && a->dx_t.ptr && a->dw_t.ptr && dtype == ZTP_BF16;
   cudaStream_t sw = st;
   int cap_dx = 0, cap_dw = 0;
   if (conc) {
@@ -780,12 +783,12 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
     ztp_ctx_destroy(c);
     return s;
   };
-  if (cudaMalloc(&c->d_flags, 64) != cudaSuccess || cudaMalloc(&c->d_stamp, 16) != cudaSuccess ||
+  if (cudaMalloc(&c->d_flags, 64) != cudaSuccess || cudaMalloc(&c->d_stamp, 32) != cudaSuccess ||
       cudaMalloc(&c->d_gemm_ns, 16) != cudaSuccess || cudaMalloc(&c->d_stats, 2 * (ZTP_MAX_RANKS + 1) * sizeof(double)) != cudaSuccess)
     return cleanup(fail(nullptr, ZTP_ECUDA, "ztp_ctx_create: device allocation failed"));
   cudaMemset(c->d_flags, 0, 64);
-  unsigned long long init_stamp[2] = {~0ull, 0ull};
-  cudaMemcpy(c->d_stamp, init_stamp, 16, cudaMemcpyHostToDevice);
+  unsigned long long init_stamp[4] = {~0ull, 0ull, ~0ull, 0ull};
+  cudaMemcpy(c->d_stamp, init_stamp, 32, cudaMemcpyHostToDevice);
   cudaMemset(c->d_gemm_ns, 0, 16);
   if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming) != cudaSuccess ||
@@ -890,6 +893,10 @@ ztp_status ztp_select(ztp_ctx* c, int nseg, const int32_t* h_len, const int32_t*
     po += h_np[i];
   }
   if (so > INT32_MAX) return fail(c, ZTP_EINVAL, "ztp_select: too many columns");
+  {  // a pending concurrent dW still reads the lineage lists this call rewrites
+    ztp_status js = join_side(c, (cudaStream_t)stream);
+    if (js != ZTP_OK) return js;
+  }
   for (int b = 0; b < nseg; b += ztp::SELECT_MAX_SEGS) {
     ztp::SelectParams p{};
     p.nseg = std::min(ztp::SELECT_MAX_SEGS, nseg - b);
@@ -910,6 +917,10 @@ ztp_status ztp_priority_update(ztp_ctx* c, const ztp_mat* w, const ztp_mat* wo, 
       wo->dtype != ZTP_BF16)
     return fail(c, ZTP_ESHAPE, "ztp_priority_update: " + shp("w_t", *w) + " vs " + shp("w_old_t", *wo) + " (bf16)");
   cudaStream_t st = (cudaStream_t)stream;
+  {  // the selection (pos_prev) and scores may still be read by a pending dW
+    ztp_status js = join_side(c, st);
+    if (js != ZTP_OK) return js;
+  }
   const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
   CUDA_TRY(c, ztp::priority_update_launch(w->ptr, w->ld, wo->ptr, wo->ld, w->rows, w->cols, pos_prev, delta,
                                           count_above, theta, st));
@@ -928,6 +939,10 @@ double ztp_pridiff_gamma(int64_t L, int64_t L_uni, double gamma_t, double alpha)
 ztp_status ztp_prepare(ztp_ctx* c, int n, const ztp_linear_args* const* args, const int32_t* what, void* stream) {
   if (!c || n < 0 || (n > 0 && (!args || !what))) return fail(c, ZTP_EINVAL, "ztp_prepare: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
+  {  // the compact copies this call rewrites may still be read by a pending dW
+    ztp_status js = join_side(c, st);
+    if (js != ZTP_OK) return js;
+  }
   ztp::GatherJobs J{};
   auto add = [&](const void* src, int64_t ld_src, const int32_t* rows, int nr, const int32_t* cols, int nc,
                  const ztp_mat& dst, int src_cols) -> ztp_status {

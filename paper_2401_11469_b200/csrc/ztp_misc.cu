@@ -15,7 +15,11 @@ namespace ztp {
 // ------------------------------------------------------------ emulation
 // The GEMM stamped [start_min, end_max] of its CTAs; spin until
 // start + chi (end - start) so the rank's GEMM takes chi times longer (A-32),
-// accumulate the (stretched) GEMM time into acc_ns (M_i, A-6), reset stamps.
+// accumulate the (stretched) GEMM time into acc_ns[0] (M_i, A-6), reset stamps.
+// Concurrent GEMMs (dX / dW on two streams, two stamp slots) are counted
+// once where they overlap: acc_ns[1] is the latest end already accounted, and
+// each delay adds only the part of [start, now] after it (the union of the
+// GEMM intervals, up to the order in which two overlapping delays finish).
 __global__ void ztp_delay_kernel(unsigned long long* stamp, double chi, unsigned long long* acc_ns) {
   pdl_wait();
   pdl_trigger();
@@ -28,7 +32,11 @@ __global__ void ztp_delay_kernel(unsigned long long* stamp, double chi, unsigned
       __nanosleep(256);
       now = globaltimer();
     }
-    if (acc_ns) atomicAdd(acc_ns, now - s);
+    if (acc_ns) {
+      const unsigned long long seen = atomicMax(acc_ns + 1, now);
+      const unsigned long long from = seen > s ? seen : s;
+      if (now > from) atomicAdd(acc_ns, now - from);
+    }
   }
   stamp[0] = ~0ull;
   stamp[1] = 0ull;

@@ -8,6 +8,8 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/ztp.h"
 
@@ -208,11 +210,24 @@ extern "C" ztp_status ztp_plan_refine(const ztp_plan_t* prev, const ztp_plan_t* 
   }
   ztp_plan_t o = *fresh;
   o.x = 0;
+  o.z = prev->z;
   if (semi) {   // keep the migration group and its sender order (A-42)
     o.x = prev->x;
     for (int i = 0; i < ZTP_MAX_RANKS; ++i) o.order[i] = prev->order[i];
   }
   for (int r = 0; r < e; ++r) {
+    if (prev->role[r] == ZTP_NORMAL) {
+      // A-43: a refresh refines the plan's stragglers only.  A normal task
+      // keeps its full shard (Alg.2 resizes only the z - x stragglers, P:284;
+      // a receiver's extra runtime is received work, which migration makes
+      // loss-free); only a new statistics window can re-plan it.
+      o.gamma[r] = 0.0;
+      o.gamma_r[r] = 0.0;
+      o.beta[r] = 0.0;
+      o.phi[r] = 0.0;
+      o.role[r] = ZTP_NORMAL;
+      continue;
+    }
     if (prev->role[r] == ZTP_MIGRATE || prev->role[r] == ZTP_SPLIT) {
       // A-42: compose the rank's whole shed fraction, keep its Eq.2 split
       const double keep = (1.0 - prev->gamma[r]) * (1.0 - fresh->gamma_r[r]);
@@ -238,6 +253,147 @@ extern "C" ztp_status ztp_plan_refine(const ztp_plan_t* prev, const ztp_plan_t* 
     o.role[r] = g > 0.0 ? ZTP_RESIZE : ZTP_NORMAL;
   }
   *out = o;
+  return ZTP_OK;
+}
+
+extern "C" ztp_status ztp_plan_uniform(int e, double gamma, ztp_plan_t* out) {
+  if (!out || e < 1 || e > ZTP_MAX_RANKS || !(gamma >= 0.0) || !(gamma < 1.0)) {
+    set_thread_error("ztp_plan_uniform: world outside 1..8 or gamma outside [0, 1)");
+    return ZTP_EINVAL;
+  }
+  std::memset(out, 0, sizeof(*out));
+  out->world = e;
+  for (int r = 0; r < e; ++r) {
+    out->order[r] = r;
+    out->gamma[r] = gamma;
+    out->gamma_r[r] = gamma;
+    out->role[r] = gamma > 0.0 ? ZTP_RESIZE : ZTP_NORMAL;
+  }
+  return ZTP_OK;
+}
+
+namespace {
+
+bool plan_is_dense(const ztp_plan_t& p) {
+  for (int r = 0; r < p.world; ++r)
+    if (p.role[r] != ZTP_NORMAL) return false;
+  return true;
+}
+
+void plan_dense(ztp_plan_t* p, int e) {
+  std::memset(p, 0, sizeof(*p));
+  p->world = e;
+  for (int r = 0; r < e; ++r) p->order[r] = r;
+}
+
+bool plans_equal(const ztp_plan_t& a, const ztp_plan_t& b) {
+  if (a.world != b.world || a.x != b.x) return false;
+  for (int r = 0; r < a.world; ++r)
+    if (a.role[r] != b.role[r] || a.gamma[r] != b.gamma[r] || a.gamma_r[r] != b.gamma_r[r] ||
+        a.beta[r] != b.beta[r] || a.phi[r] != b.phi[r])
+      return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" void ztp_ctl_opts_default(ztp_ctl_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  ztp_plan_opts_default(&o->plan);
+  o->L_ref = 1.0;
+  o->trigger = 0.10;
+  o->max_refines = 1;
+}
+
+extern "C" ztp_status ztp_ctl_init(ztp_ctl* c, int world) {
+  if (!c || world < 1 || world > ZTP_MAX_RANKS) {
+    set_thread_error("ztp_ctl_init: null controller or world outside 1..8");
+    return ZTP_EINVAL;
+  }
+  std::memset(c, 0, sizeof(*c));
+  c->world = world;
+  c->state = ZTP_CTL_WINDOW;
+  plan_dense(&c->plan, world);
+  return ZTP_OK;
+}
+
+extern "C" ztp_status ztp_ctl_step(ztp_ctl* c, const ztp_ctl_opts* o, const ztp_costs* costs, const double* T,
+                                   const double* M, int32_t* action) {
+  if (!c || !o || !T || !M || !action || c->world < 1 || c->world > ZTP_MAX_RANKS) {
+    set_thread_error("ztp_ctl_step: null argument or uninitialised controller");
+    return ZTP_EINVAL;
+  }
+  const int e = c->world;
+  for (int r = 0; r < e; ++r)
+    if (!std::isfinite(T[r]) || !(T[r] > 0.0)) {
+      set_thread_error("ztp_ctl_step: T[" + std::to_string(r) + "] must be finite and > 0");
+      return ZTP_EINVAL;
+    }
+  *action = ZTP_CTL_KEEP;
+  const double trig = o->trigger;
+  c->steps = c->steps + 1;
+  double Tmin = T[0], Tmax = T[0];
+  for (int r = 1; r < e; ++r) {
+    if (T[r] < Tmin) Tmin = T[r];
+    if (T[r] > Tmax) Tmax = T[r];
+  }
+  auto lift = [&]() {   // next step is a statistics window on the un-resized layer
+    if (!plan_is_dense(c->plan)) *action = ZTP_CTL_APPLY;
+    plan_dense(&c->plan, e);
+    c->state = ZTP_CTL_WINDOW;
+  };
+  if (c->state == ZTP_CTL_WINDOW) {
+    // Alg.1 l.1-2 / Alg.2 l.2-24 on the window's un-resized runtimes
+    ztp_plan_t p;
+    const ztp_status s = ztp_plan(e, T, M, o->L_ref, costs, &o->plan, &p);
+    if (s != ZTP_OK) return s;
+    c->windows = c->windows + 1;
+    if (!plan_is_dense(p)) {
+      c->plan = p;
+      c->replans = c->replans + 1;
+      *action = ZTP_CTL_APPLY;
+    }
+    c->T_target = Tmin;
+    c->T_wmax = Tmax;
+    c->refines = 0;
+    c->state = ZTP_CTL_FIRST;
+    return ZTP_OK;
+  }
+  if (c->state == ZTP_CTL_FIRST) {
+    if (!plan_is_dense(c->plan) && (Tmin < (1.0 - trig) * c->T_target || Tmax > (1.0 + trig) * c->T_wmax)) {
+      // the slowdowns changed while the plan was applied: a new window (A-41)
+      lift();
+      return ZTP_OK;
+    }
+    if (!plan_is_dense(c->plan) && c->refines < o->max_refines) {
+      ztp_plan_opts zo = o->plan;
+      zo.enable_migration = 0;
+      zo.zero_crit = ZTP_CRIT_MIN;
+      ztp_plan_t fresh, ref;
+      ztp_status s = ztp_plan(e, T, M, o->L_ref, nullptr, &zo, &fresh);
+      if (s != ZTP_OK) return s;
+      s = ztp_plan_refine(&c->plan, &fresh, o->plan.gamma_max, &ref);
+      if (s != ZTP_OK) return s;
+      c->refines = c->refines + 1;
+      if (!plans_equal(ref, c->plan)) {
+        c->plan = ref;
+        c->refine_count = c->refine_count + 1;
+        *action = ZTP_CTL_APPLY;
+        return ZTP_OK;   // still FIRST: the refined plan's first step is judged next
+      }
+    }
+    for (int r = 0; r < e; ++r) c->T_ref[r] = T[r];
+    c->state = ZTP_CTL_MONITOR;
+    return ZTP_OK;
+  }
+  // MONITOR: P:178's over-10% change (either direction, A-8) opens a window
+  for (int r = 0; r < e; ++r)
+    if (std::fabs(T[r] - c->T_ref[r]) / c->T_ref[r] > trig) {
+      c->triggers = c->triggers + 1;
+      lift();
+      return ZTP_OK;
+    }
   return ZTP_OK;
 }
 
@@ -300,5 +456,123 @@ extern "C" ztp_status ztp_plan_counts(const ztp_plan_t* p, int rank, int64_t K, 
       lo += cnt;
     }
   }
+  return ZTP_OK;
+}
+
+extern "C" ztp_status ztp_layer_prune_counts(const ztp_plan_t* p, int rank, int64_t h, int64_t a, int64_t u,
+                                             int32_t out[4]) {
+  if (!p || !out || rank < 0 || rank >= p->world || h < 1 || a < 1 || u < 1) {
+    set_thread_error("ztp_layer_prune_counts: bad plan / rank / sizes");
+    return ZTP_EINVAL;
+  }
+  // A-37: heads do not migrate (A-26), so a rank that sheds MLP units
+  // resizes its attention by its Eq.1 gamma; others by gamma_r.
+  ztp_plan_t att = *p;
+  if (p->role[rank] == ZTP_MIGRATE || p->role[rank] == ZTP_SPLIT) att.gamma_r[rank] = p->gamma[rank];
+  att.role[rank] = ZTP_RESIZE;
+  att.phi[rank] = 0.0;
+  ztp_counts c;
+  ztp_status s;
+  if ((s = ztp_plan_counts(&att, rank, h, h, 1, 0, &c)) != ZTP_OK) return s;
+  out[0] = c.n_prune;
+  if ((s = ztp_plan_counts(&att, rank, a, a, 1, 0, &c)) != ZTP_OK) return s;
+  out[1] = c.n_prune;
+  if ((s = ztp_plan_counts(p, rank, h, u, 1, 0, &c)) != ZTP_OK) return s;
+  out[2] = c.n_prune;
+  if ((s = ztp_plan_counts(p, rank, u, u, 1, 1, &c)) != ZTP_OK) return s;
+  out[3] = c.n_prune;
+  return ZTP_OK;
+}
+
+extern "C" int32_t ztp_pridiff_counts(int64_t L, int64_t L_uni, double gamma_t, double alpha, double gamma_max) {
+  if (L < 1) return 0;
+  // Alg.1 l.10-11, then A-4 (clamp, >= 1 survives) and A-3 (rounding)
+  double g = 1.0 - (double)L_uni / (double)L;
+  const double f = alpha * gamma_t;
+  if (f > g) g = f;
+  if (g > gamma_max) g = gamma_max;
+  if (g < 0.0) g = 0.0;
+  int64_t n = (int64_t)std::floor((double)L * g + 0.5);
+  if (n > L - 1) n = L - 1;
+  return (int32_t)n;
+}
+
+namespace {
+
+// Samples -> a non-decreasing piecewise-linear function through (0, 0) (A-40):
+// x ascending, duplicates and x <= 0 dropped, y = running max clamped at 0 (a
+// cost cannot shrink when more units move; a dip is timing noise).  Writes at
+// most n + 2 points.
+int monotone_fit(int n, const double* x, const double* y, double* ox, double* oy) {
+  std::vector<std::pair<double, double>> pts;
+  for (int i = 0; i < n; ++i) pts.emplace_back(x[i], y[i]);
+  std::sort(pts.begin(), pts.end());
+  int m = 0;
+  ox[m] = 0.0;
+  oy[m] = 0.0;
+  ++m;
+  for (const auto& pt : pts) {
+    if (!(pt.first > ox[m - 1])) continue;
+    double v = pt.second > 0.0 ? pt.second : 0.0;
+    if (oy[m - 1] > v) v = oy[m - 1];
+    ox[m] = pt.first;
+    oy[m] = v;
+    ++m;
+  }
+  if (m < 2) {
+    ox[m] = 1.0;
+    oy[m] = 0.0;
+    ++m;
+  }
+  return m;
+}
+
+}  // namespace
+
+extern "C" ztp_status ztp_costs_fit(int n_omega, const double* omega_x, const double* omega_y, int n_phi1,
+                                    const double* phi1_x, const double* phi1_y, int n_phi2, const double* phi2_x,
+                                    const double* phi2_y, int cap, double* xs, double* ys, ztp_costs* out) {
+  if (!out || !xs || !ys || n_omega < 0 || n_phi1 < 0 || n_phi2 < 0 || (n_omega && (!omega_x || !omega_y)) ||
+      (n_phi1 && (!phi1_x || !phi1_y)) || (n_phi2 && (!phi2_x || !phi2_y))) {
+    set_thread_error("ztp_costs_fit: null argument");
+    return ZTP_EINVAL;
+  }
+  const int need = std::max(std::max(n_omega, n_phi1), n_phi2) + 2;
+  if (cap < need) {
+    set_thread_error("ztp_costs_fit: cap " + std::to_string(cap) + " < " + std::to_string(need) + " points");
+    return ZTP_EINVAL;
+  }
+  auto finite = [](int n, const double* x, const double* y) {
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(x[i]) || !std::isfinite(y[i])) return false;
+    return true;
+  };
+  if (!finite(n_omega, omega_x, omega_y) || !finite(n_phi1, phi1_x, phi1_y) || !finite(n_phi2, phi2_x, phi2_y)) {
+    set_thread_error("ztp_costs_fit: non-finite sample");
+    return ZTP_EINVAL;
+  }
+  // Omega_1 = the extra cost at the smallest pruned count > 0 ("static
+  // space allocation overhead"), Omega_2(n) = extra(n) - Omega_1
+  std::vector<double> px, py;
+  int first = -1;
+  for (int i = 0; i < n_omega; ++i)
+    if (omega_x[i] > 0.0 && (first < 0 || omega_x[i] < omega_x[first])) first = i;
+  double omega1 = 0.0;
+  if (first >= 0) omega1 = omega_y[first] > 0.0 ? omega_y[first] : 0.0;
+  for (int i = 0; i < n_omega; ++i)
+    if (omega_x[i] > 0.0) {
+      px.push_back(omega_x[i]);
+      py.push_back(omega_y[i] - omega1);
+    }
+  out->omega1 = omega1;
+  out->omega2.n = monotone_fit((int)px.size(), px.data(), py.data(), xs, ys);
+  out->omega2.x = xs;
+  out->omega2.y = ys;
+  out->phi1.n = monotone_fit(n_phi1, phi1_x, phi1_y, xs + cap, ys + cap);
+  out->phi1.x = xs + cap;
+  out->phi1.y = ys + cap;
+  out->phi2.n = monotone_fit(n_phi2, phi2_x, phi2_y, xs + 2 * cap, ys + 2 * cap);
+  out->phi2.x = xs + 2 * cap;
+  out->phi2.y = ys + 2 * cap;
   return ZTP_OK;
 }

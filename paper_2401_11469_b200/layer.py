@@ -73,22 +73,9 @@ def migration_io(plan, rank: int, world: int, u: int, h: int, unit: int = 1) -> 
 
 
 def layer_prune_counts(plan, rank: int, h: int, a: int, u: int) -> Dict[str, int]:
-    """Prune counts of the four linears of `rank` from a plan (host only).
-    MLP (A-26): FC1 prunes its input K = h by gamma_r, FC2 its K_rem = u -
-    n_mig own units by gamma_r (ztp_plan_counts).  Attention (A-37): heads do
-    not migrate in this build, so QKV / O prune K = h / a by gamma_r, and a
-    rank that sheds MLP units (MIGRATE / SPLIT) resizes its attention by its
-    Eq.1 gamma instead -- its remaining attention work is (1 - gamma), as is
-    the MLP's after migration."""
-    att = Z.PlanT.from_buffer_copy(plan)
-    if int(plan.role[rank]) in (Z.MIGRATE, Z.SPLIT):
-        att.gamma_r[rank] = plan.gamma[rank]
-    att.role[rank] = Z.RESIZE
-    att.phi[rank] = 0.0
-    return {"qkv": Z.ztp_plan_counts(att, rank, h, h, 1, False).n_prune,
-            "o": Z.ztp_plan_counts(att, rank, a, a, 1, False).n_prune,
-            "fc1": Z.ztp_plan_counts(plan, rank, h, u, 1, False).n_prune,
-            "fc2": Z.ztp_plan_counts(plan, rank, u, u, 1, True).n_prune}
+    """Prune counts of the four linears of `rank` from a plan: the library's
+    ztp_layer_prune_counts (MLP by gamma_r, attention by the A-37 rule)."""
+    return Z.ztp_layer_prune_counts(plan, rank, h, a, u)
 
 
 def xfer_specs(mio: MigrationIO, u: int, h: int, grads: bool) -> List[dict]:
@@ -249,9 +236,7 @@ class ZtpLayer:
         l_uni = cnt.cpu().tolist()                 # epoch boundary: one host sync
         n_prune = {}
         for i, s in enumerate(SEGS):
-            L = lens[s]
-            g = min(Z.ztp_pridiff_gamma(L, l_uni[i], gamma_t, alpha), 0.9)        # A-4 clamp
-            n_prune[s] = min(int(g * L + 0.5), L - 1)                              # A-3 rounding
+            n_prune[s] = Z.ztp_pridiff_counts(lens[s], l_uni[i], gamma_t, alpha, 0.9)   # l.10-11, A-3, A-4
         scores = {s: self._scores[offs[s]:offs[s] + lens[s]].clone() for s in SEGS}
         self.set_selection(n_prune, scores, stream)
         return n_prune

@@ -36,38 +36,13 @@ GAMMAS = (0.0, 0.125, 0.25, 0.5, 0.75)
 FRACS = (0.0, 0.125, 0.25, 0.5, 1.0)
 
 
-def _monotone(points: Sequence[Tuple[float, float]]) -> Tuple[Tuple[float, ...], Tuple[float, ...]]:
-    """Samples -> a non-decreasing piecewise-linear function through (0, 0):
-    x ascending, duplicates dropped, y clamped at 0 and made non-decreasing
-    (running max) -- a cost cannot shrink when more units are moved or pruned,
-    so a dip is timing noise."""
-    pts = sorted((float(x), float(y)) for x, y in points)
-    xs, ys = [0.0], [0.0]
-    for x, y in pts:
-        if x <= xs[-1]:
-            continue
-        xs.append(x)
-        ys.append(max(ys[-1], y, 0.0))
-    if len(xs) < 2:                      # ztp_pwl needs >= 2 samples
-        xs.append(1.0)
-        ys.append(0.0)
-    return tuple(xs), tuple(ys)
-
-
 def fit_costs(omega: Sequence[Tuple[float, float]], phi1: Sequence[Tuple[float, float]],
               phi2: Sequence[Tuple[float, float]]):
-    """Raw pretest samples -> (ztp_costs keepalive tuple, plain dict).
-    omega: (pruned units n, extra non-GEMM ms vs the dense step) for n >= 0;
-    Omega_1 = the extra at the smallest n > 0, Omega_2(n) = extra(n) - Omega_1
-    (a static part plus a part proportional to the pruned data).
-    phi1: (migrated units, ms); phi2: (units received by one helper, ms)."""
-    pos = sorted((x, y) for x, y in omega if x > 0)
-    omega1 = max(pos[0][1], 0.0) if pos else 0.0
-    o2 = _monotone([(x, y - omega1) for x, y in pos])
-    p1 = _monotone(phi1)
-    p2 = _monotone(phi2)
-    plain = {"omega1": omega1, "omega2": o2, "phi1": p1, "phi2": p2}
-    return Z.make_costs(omega1, o2, p1, p2), plain
+    """Raw pretest samples -> (ztp_costs keepalive tuple, plain dict), fitted
+    by the library (ztp_costs_fit, A-40): omega = (pruned units n, extra
+    non-GEMM ms vs the dense step), phi1 = (migrated units, ms), phi2 =
+    (units received by one helper, ms)."""
+    return Z.ztp_costs_fit(list(omega), list(phi1), list(phi2))
 
 
 # ----------------------------------------------------------------- GPU side
@@ -111,12 +86,8 @@ def gemm_ms(L, ctx, steps: int = 5) -> float:
 
 
 def _homog_counts(L, g: float) -> Dict[str, int]:
-    """A-3 rounding, A-4 (at least one kept) of one ratio on all four linears."""
-    out = {}
-    for s in ("qkv", "o", "fc1", "fc2"):
-        K = {"qkv": L.h, "o": L.a, "fc1": L.h, "fc2": L.u}[s]
-        out[s] = min(int(K * g + 0.5), K - 1)
-    return out
+    """The four prune counts of one homogeneous ratio (library: A-3, A-4)."""
+    return Z.ztp_layer_prune_counts(Z.ztp_plan_uniform(1, g), 0, L.h, L.a, L.u)
 
 
 def pretest(L, ctx, scores: Dict, *, gammas: Sequence[float] = GAMMAS, fracs: Sequence[float] = FRACS,

@@ -260,3 +260,131 @@ def test_layer_prune_counts_attention_rule():
             assert c["fc2"] == Z.ztp_plan_counts(plan, r, u, u, 1, True).n_prune
             if role == Z.MIGRATE:            # a migrating rank still sheds its attention excess
                 assert c["qkv"] > 0 and c["o"] > 0
+
+
+def _plan_bits_equal(zp, op, e):
+    assert zp.world == op.world and zp.z == op.z and zp.x == op.x
+    assert list(zp.role)[:e] == list(op.role[:e])
+    assert list(zp.order)[:e] == list(op.order[:e])
+    for k in ("gamma", "beta", "phi", "gamma_r"):
+        for r in range(e):
+            assert _bits(getattr(zp, k)[r]) == _bits(getattr(op, k)[r]), (k, r)
+
+
+@pytest.mark.parametrize("semi", [0, 1])
+def test_controller_matches_oracle_randomized(Z, semi):
+    """ztp_ctl_step (the P:178 re-planning loop, A-41/A-43) bit-exact against
+    the oracle's Controller on random runtime sequences: every plan, state,
+    action and counter after every step."""
+    rng = random.Random(17 + semi)
+    seen = {"refine": 0, "trigger": 0, "apply": 0}
+    for trial in range(60):
+        e = rng.randint(1, 8)
+        zc, oc = _costs_pair(Z, rng) if semi else (Z.make_costs(), O.Costs())
+        kw = dict(enable_migration=semi, zero_crit=1 if semi else rng.randint(0, 1),
+                  gamma_max=rng.choice([0.9, 1.0]), eps=rng.choice([0.0, 0.02, 0.05]))
+        L = float(rng.choice([512, 1376, 2560]))
+        trig = rng.choice([0.1, 0.05, 0.2])
+        mr = rng.randint(0, 3)
+        zo = Z.ctl_opts(L_ref=L, trigger=trig, max_refines=mr, **kw)
+        oo = O.CtlOpts(plan=O.PlanOpts(**kw), L_ref=L, trigger=trig, max_refines=mr)
+        zctl, octl = Z.ztp_ctl_init(e), O.Controller(e)
+        chis = [1.0] * e
+        for k in range(25):
+            if rng.random() < 0.15:                     # the slowdowns change
+                chis = [rng.choice([1.0, 1.0, 1.0, 2.0, 3.0, 8.0]) for _ in range(e)]
+            T = [c * rng.uniform(0.9, 1.1) + rng.uniform(0.1, 0.3) for c in chis]
+            M = [t * rng.uniform(0.5, 0.9) for t in T]
+            try:
+                oa = octl.step(T, M, oo, oc)
+                oerr = None
+            except O.OracleError as ex:
+                oerr = ex.code
+            try:
+                za = Z.ztp_ctl_step(zctl, zo, T, M, zc)
+                zerr = None
+            except Z.ZtpError as ex:
+                zerr = ex.name
+            assert oerr == zerr, (trial, k)
+            if oerr:
+                break
+            assert za == oa and zctl.state == octl.state and zctl.refines == octl.refines, (trial, k)
+            _plan_bits_equal(zctl.plan, octl.plan, e)
+            assert (zctl.windows, zctl.replans, zctl.refine_count, zctl.triggers) == \
+                (octl.windows, octl.replans, octl.refine_count, octl.triggers)
+            assert _bits(zctl.T_target) == _bits(octl.T_target) and _bits(zctl.T_wmax) == _bits(octl.T_wmax)
+            seen["apply"] += za
+        seen["refine"] += octl.refine_count
+        seen["trigger"] += octl.triggers
+    assert all(v > 0 for v in seen.values()), seen
+
+
+def test_controller_errors_abi(Z):
+    ctl = Z.ztp_ctl_init(2)
+    with pytest.raises(Z.ZtpError) as ei:
+        Z.ztp_ctl_step(ctl, Z.ctl_opts(), [1.0, float("nan")], [1.0, 1.0])
+    assert ei.value.name == "ZTP_EINVAL"
+    with pytest.raises(Z.ZtpError) as ei:
+        Z.ztp_ctl_step(ctl, Z.ctl_opts(), [1.0, 2.0], [1.0, 0.0])
+    assert ei.value.name == "ZTP_ENOBASELINE"
+    with pytest.raises(Z.ZtpError):
+        Z.ztp_ctl_init(9)
+
+
+def test_layer_prune_counts_matches_oracle(Z):
+    """ztp_layer_prune_counts (A-37 + MLP counts) equals the oracle's on random
+    SEMI / ZERO plans for every rank; ztp_plan_uniform likewise."""
+    rng = random.Random(23)
+    for _ in range(200):
+        e = rng.randint(1, 8)
+        T = [rng.uniform(1, 1.2) for _ in range(e)]
+        for s in rng.sample(range(e), rng.randint(0, max(0, e - 1))):
+            T[s] = rng.uniform(1.5, 6.0)
+        M = [t * rng.uniform(0.6, 0.9) for t in T]
+        zc, oc = _costs_pair(Z, rng)
+        kw = dict(enable_migration=rng.randint(0, 1) if e > 1 else 0, zero_crit=1)
+        h = rng.choice([64, 1024, 4096])
+        a, u = h // e, rng.choice([128, 1376, 2560])
+        try:
+            op = O.plan(T, M, float(u), oc, O.PlanOpts(**kw))
+        except O.OracleError:
+            continue
+        zp = Z.ztp_plan(T, M, float(u), zc, Z.plan_opts(**kw))
+        for r in range(e):
+            assert Z.ztp_layer_prune_counts(zp, r, h, a, u) == O.layer_prune_counts(op, r, h, a, u)
+    for g in (0.0, 0.25, 0.5, 0.9, 0.999):
+        up, oup = Z.ztp_plan_uniform(4, g), O.plan_uniform(4, g)
+        assert Z.ztp_layer_prune_counts(up, 2, 1024, 256, 1024) == O.layer_prune_counts(oup, 2, 1024, 256, 1024)
+    with pytest.raises(Z.ZtpError):
+        Z.ztp_plan_uniform(2, 1.0)
+
+
+def test_pridiff_counts_matches_oracle(Z):
+    rng = random.Random(29)
+    for _ in range(500):
+        L = rng.randint(1, 20000)
+        L_uni = rng.randint(0, L)
+        g, a, gm = rng.random(), rng.choice([0.5, 0.8, 1.0]), rng.choice([0.9, 1.0])
+        assert Z.ztp_pridiff_counts(L, L_uni, g, a, gm) == O.pridiff_counts(L, L_uni, g, a, gm)
+    assert Z.ztp_pridiff_counts(0, 0, 0.5) == 0
+
+
+def test_costs_fit_matches_oracle(Z):
+    """ztp_costs_fit (A-40) bit-exact vs the oracle's fit on random noisy
+    samples (duplicates, negatives, dips)."""
+    rng = random.Random(31)
+    for _ in range(300):
+        def pts(n, lo):
+            return [(float(rng.choice([0, rng.randint(lo, 3000)])), rng.uniform(-0.01, 0.05)) for _ in range(n)]
+        om, p1, p2 = pts(rng.randint(0, 7), 1), pts(rng.randint(0, 6), 1), pts(rng.randint(0, 6), 1)
+        if rng.random() < 0.2 and om:
+            om.append((om[0][0], om[0][1] + 0.001))          # repeated x
+        (zc, _), plain = Z.ztp_costs_fit(om, p1, p2)
+        oc = O.costs_fit(om, p1, p2)
+        assert _bits(plain["omega1"]) == _bits(oc.omega1)
+        for k in ("omega2", "phi1", "phi2"):
+            zx, zy = plain[k]
+            ox, oy = getattr(oc, k)
+            assert len(zx) == len(ox) and all(_bits(p) == _bits(q) for p, q in zip(zx + zy, ox + oy)), k
+    with pytest.raises(Z.ZtpError):
+        Z.ztp_costs_fit([(1.0, float("nan"))], [], [])

@@ -9,12 +9,19 @@ import pytest
 from oracle import ztp_oracle as O
 
 
-def test_fit_costs_shape_and_monotone():
+@pytest.mark.parametrize("which", ["library", "oracle"])
+def test_fit_costs_shape_and_monotone(which):
     """Omega_1 = extra cost at the smallest pruned count; Omega_2 / Phi_1 /
     Phi_2 pass through (0, 0), are non-decreasing (noise dips removed) and
-    clamped at 0."""
+    clamped at 0.  Hand-computed values (A-40), for the library's fit and the
+    oracle's."""
     from paper_2401_11469_b200.pretest import fit_costs
-    _, c = fit_costs([(0, 0.0), (128, 0.010), (256, 0.012), (512, 0.011), (768, 0.020)],
+
+    def oracle_fit(om, p1, p2):
+        oc = O.costs_fit(om, p1, p2)
+        return None, {"omega1": oc.omega1, "omega2": oc.omega2, "phi1": oc.phi1, "phi2": oc.phi2}
+    fit = fit_costs if which == "library" else oracle_fit
+    _, c = fit([(0, 0.0), (128, 0.010), (256, 0.012), (512, 0.011), (768, 0.020)],
                      [(128, 0.004), (64, 0.003), (1024, 0.020)],
                      [(0, 0.0), (128, -0.001), (256, 0.006), (512, 0.012)])
     assert c["omega1"] == pytest.approx(0.010)
@@ -34,6 +41,8 @@ def test_fit_costs_degenerate():
     from paper_2401_11469_b200.pretest import fit_costs
     costs, c = fit_costs([(0, 0.0)], [], [])
     assert c["omega1"] == 0.0
+    oc = O.costs_fit([(0, 0.0)], [], [])
+    assert oc.omega1 == 0.0 and oc.phi1 == ((0.0, 1.0), (0.0, 0.0))
     for k in ("omega2", "phi1", "phi2"):
         assert len(c[k][0]) >= 2
 
