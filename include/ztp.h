@@ -42,6 +42,7 @@ extern "C" {
 
 #define ZTP_MAX_RANKS 8
 #define ZTP_UID_BYTES 128
+#define ZTP_IPC_BYTES 128
 
 typedef enum ztp_status {
   ZTP_OK = 0,
@@ -84,6 +85,8 @@ const char* ztp_version(void);
  * every rank (e.g. torch.distributed.broadcast); every rank then calls
  * ztp_ctx_create with its own rank and the CUDA device it owns.  Collective:
  * all ranks must call it.  The communicator is NCCL over NVLink/NVSwitch.
+ * world > 1 with uid == NULL creates a context without NCCL whose data plane
+ * is the peer-memory transport below (ztp_window_*).
  * ------------------------------------------------------------------------- */
 ztp_status ztp_get_unique_id(unsigned char uid[ZTP_UID_BYTES]);
 ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world,
@@ -94,6 +97,42 @@ ztp_status ztp_ctx_destroy(ztp_ctx* ctx);
 ztp_status ztp_sync(ztp_ctx* ctx, void* stream);
 /* Number of kernels this context launched so far (own kernels only). */
 int64_t ztp_launch_count(const ztp_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * Peer-memory data plane (SURVEY §8(b) ztp_sym_alloc).
+ * Every rank owns one symmetric window: ztp_window_create allocates it
+ * (bytes + 64 KB of barrier flags) and writes a ZTP_IPC_BYTES handle (CUDA
+ * IPC handle, pointer, pid, device, size); the caller all-gathers the handles
+ * of every rank (rank order, e.g. torch.distributed.all_gather_object) and
+ * calls ztp_window_open on every rank, which maps each peer's window (CUDA IPC
+ * across processes, the pointer itself for contexts of one process, NVLink
+ * P2P between GPUs).  ztp_sym_alloc carves caller tensors out of the window
+ * (bump allocation, 256-byte aligned; the same call sequence on every rank
+ * gives the same offsets, so a peer's copy of a tensor is found at the same
+ * offset -- the library owns the memory, valid until ztp_ctx_destroy).
+ * With ZTP_TRANSPORT_PEER (default for contexts created without an NCCL id):
+ *   all-reduce (row FWD, col BWD) = two-shot over peer loads, summed
+ *     in rank order 0..e-1 in fp32 (deterministic; the oracle's left fold);
+ *   all-gather (unpaired mode) = pulls of the peers' row blocks;
+ *   ztp_migrate = one-sided pulls of the source rank's slice, no
+ *     staging copies;
+ *   ztp_allgather_stats = stores into every peer's stats slot;
+ * each a kernel whose CTA b meets CTA b of every peer at device-side
+ * barriers (release / acquire, system scope), so it is graph-capturable; the
+ * tensors involved must be window tensors (EINVAL otherwise).  A barrier not
+ * met within 10 s raises a flag that ztp_sync reports as ZTP_ECUDA.
+ * ZTP_TRANSPORT_NCCL: NCCL collectives and grouped send/recv.
+ * Errors: EINVAL (no window / not open / exhausted / tensor outside it),
+ * ESHAPE (window sizes differ across ranks), ECUDA.
+ * ------------------------------------------------------------------------- */
+enum { ZTP_TRANSPORT_NCCL = 0, ZTP_TRANSPORT_PEER = 1 };
+ztp_status ztp_window_create(ztp_ctx* ctx, size_t bytes, unsigned char handle[ZTP_IPC_BYTES]);
+ztp_status ztp_window_open(ztp_ctx* ctx, const unsigned char* handles /* world x ZTP_IPC_BYTES */);
+ztp_status ztp_sym_alloc(ztp_ctx* ctx, size_t bytes, void** ptr);
+ztp_status ztp_set_transport(ztp_ctx* ctx, int transport);
+/* Device-side barrier of all ranks on `stream` (NCCL: a 1-element
+ * all-reduce; peer: one barrier round).  Collective. */
+ztp_status ztp_barrier(ztp_ctx* ctx, void* stream);
 
 /* ---------------------------------------------------------------------------
  * (1) Plan -- pure host, deterministic, no context, no device work.
@@ -470,10 +509,16 @@ ztp_status ztp_core(ztp_ctx* ctx, ztp_phase phase, const ztp_mat* qkv_t, const z
  * Each transfer copies the sub-matrix src[r0:r0+nr, c0:c0+nc] held by
  * src_rank into dst[dr0:dr0+nr, dc0:dc0+nc] held by dst_rank.  Every rank
  * calls ztp_migrate with the SAME list; a rank acts only on transfers naming
- * it (all transfers are issued inside one NCCL group, so any pattern is
- * deadlock-free).  src_rank == dst_rank is a local device copy.  The slice is
- * moved exactly once over NVLink (the straggler's egress is the scarce
- * resource; helpers receive disjoint slices instead of full broadcasts).
+ * it.  src_rank == dst_rank is a local device copy.  The slice is moved
+ * exactly once over NVLink (the straggler's egress is the scarce resource;
+ * helpers receive disjoint slices instead of full broadcasts).
+ * Peer transport: the destination PULLS from the source rank's window --
+ * `src` must be a window tensor, and on the destination rank `src` is its
+ * OWN symmetric counterpart (same ztp_sym_alloc slot), whose window offset
+ * locates the source's copy; one kernel per 24 pulls per rank, with device
+ * barriers before (sources final) and after (sources not yet reused).
+ * NCCL transport: the slices are staged through a workspace and moved by
+ * grouped ncclSend / ncclRecv (any pattern is deadlock-free).
  * ------------------------------------------------------------------------- */
 typedef struct ztp_xfer {
   ztp_mat src;                 /* meaningful on src_rank only */

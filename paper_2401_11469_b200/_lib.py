@@ -11,6 +11,8 @@ LIB_PATH = os.path.join(HERE, "libztp.so")
 
 MAX_RANKS = 8
 UID_BYTES = 128
+IPC_BYTES = 128
+TRANSPORT_NCCL, TRANSPORT_PEER = 0, 1
 
 # status codes (ztp_status)
 STATUS = ["ZTP_OK", "ZTP_EINVAL", "ZTP_ESHAPE", "ZTP_EINDEX", "ZTP_EDEGENERATE", "ZTP_ELINEAGE", "ZTP_EHISTORY",
@@ -156,6 +158,11 @@ def _load():
         "ztp_read_stamps": (C.c_int, [vp, vp, C.POINTER(C.c_uint64), C.c_int]),
         "ztp_pridiff_gamma": (C.c_double, [C.c_int64, C.c_int64, C.c_double, C.c_double]),
         "ztp_set_profile": (st, [vp, C.c_int]),
+        "ztp_window_create": (st, [vp, C.c_size_t, C.c_char_p]),
+        "ztp_window_open": (st, [vp, C.c_char_p]),
+        "ztp_sym_alloc": (st, [vp, C.c_size_t, C.POINTER(vp)]),
+        "ztp_set_transport": (st, [vp, C.c_int]),
+        "ztp_barrier": (st, [vp, vp]),
         "ztp_read_profile": (st, [vp, vp, C.POINTER(Profile)]),
     }
     for name, (res, args) in sig.items():
@@ -174,7 +181,8 @@ EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_i
             "ztp_layer_prune_counts", "ztp_plan_uniform", "ztp_pridiff_counts", "ztp_costs_fit", "ztp_allgather_stats", "ztp_select", "ztp_join", "ztp_col_linear", "ztp_row_linear",
             "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "ztp_prepare",
             "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",
-            "ztp_set_profile", "ztp_read_profile")
+            "ztp_set_profile", "ztp_read_profile", "ztp_window_create", "ztp_window_open", "ztp_sym_alloc",
+            "ztp_set_transport", "ztp_barrier")
 
 
 def check(code: int, ctx=None):

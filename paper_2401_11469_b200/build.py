@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libztp.so")
-SOURCES = ["ztp_api.cu", "ztp_gemm.cu", "ztp_select.cu", "ztp_misc.cu", "ztp_plan.cpp"]
+SOURCES = ["ztp_api.cu", "ztp_gemm.cu", "ztp_select.cu", "ztp_misc.cu", "ztp_peer.cu", "ztp_plan.cpp"]
 HEADERS = ["ztp_internal.h", "ztp_ptx.cuh"]
 
 

@@ -3,6 +3,7 @@
 // Host-side validation runs before anything is enqueued.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -87,6 +88,15 @@ struct ztp_ctx {
   static constexpr int PSTAMP_CAP = 4096;
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
+  // peer-memory data plane (ztp_window_*, ztp_sym_alloc; ztp_peer.cu)
+  int transport = ZTP_TRANSPORT_NCCL;
+  char* win = nullptr;                 // own symmetric window (cudaMalloc)
+  size_t win_bytes = 0, win_used = 0;
+  bool win_open = false;
+  void* win_ipc[ZTP_MAX_RANKS] = {};   // peer windows opened through CUDA IPC (closed on destroy)
+  ztp::PeerWin pw{};
+  int peer_ctas = 32;                  // CTAs per peer collective (same on every rank)
+  float* d_one = nullptr;              // NCCL barrier scratch
 };
 
 enum { PROF_GEMM = 0, PROF_OTHER = 1, PROF_COMM = 2 };
@@ -392,11 +402,57 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
   return s;
 }
 
+// Window offset of a tensor of `bytes` (peer transport): it must lie inside
+// this rank's symmetric window, so every peer holds it at the same offset.
+ztp_status win_offset(ztp_ctx* c, const void* p, size_t bytes, const char* what, int64_t* off) {
+  if (!c->win_open) return fail(c, ZTP_EINVAL, std::string(what) + ": the peer transport needs ztp_window_open first");
+  const char* q = static_cast<const char*>(p);
+  if (q < c->win + ztp::PEER_RESERVED || q + bytes > c->win + c->win_bytes)
+    return fail(c, ZTP_EINVAL, std::string(what) + ": tensor is not inside the symmetric window (ztp_sym_alloc)");
+  *off = q - c->win;
+  return ZTP_OK;
+}
+
 ztp_status allreduce(ztp_ctx* c, const ztp_mat& m, cudaStream_t st) {
   if (c->world == 1) return ZTP_OK;
   if (m.ld != m.cols) return fail(c, ZTP_ESHAPE, "all-reduce needs a contiguous tensor: " + shp("t", m));
+  const size_t es = m.dtype == ZTP_F32 ? 4 : 2;
+  const size_t bytes = (size_t)(m.rows * m.cols) * es;
   const int pe = prof_begin(c, st, PROF_COMM, 0.0);
-  NCCL_TRY(c, ncclAllReduce(m.ptr, m.ptr, (size_t)(m.rows * m.cols), nccl_type(m.dtype), ncclSum, c->comm, st));
+  if (c->transport == ZTP_TRANSPORT_PEER) {
+    int64_t off;
+    ztp_status s = win_offset(c, m.ptr, bytes, "all-reduce", &off);
+    if (s != ZTP_OK) return s;
+    if (bytes % 16) return fail(c, ZTP_ESHAPE, "peer all-reduce: payload must be a multiple of 16 bytes");
+    CUDA_TRY(c, ztp::peer_allreduce_launch(c->pw, off, (int64_t)bytes, m.dtype == ZTP_F32, c->peer_ctas, st));
+    ++c->launches;
+  } else {
+    NCCL_TRY(c, ncclAllReduce(m.ptr, m.ptr, (size_t)(m.rows * m.cols), nccl_type(m.dtype), ncclSum, c->comm, st));
+  }
+  prof_end(c, pe, st);
+  return ZTP_OK;
+}
+
+// In-place all-gather of `full` [world * blk_rows, cols] whose row block
+// `rank` this rank has written (unpaired mode).
+ztp_status allgather_rows(ztp_ctx* c, const ztp_mat& full, int64_t blk_rows, cudaStream_t st) {
+  if (c->world == 1) return ZTP_OK;
+  if (full.ld != full.cols) return fail(c, ZTP_ESHAPE, "all-gather needs a contiguous tensor: " + shp("t", full));
+  const size_t es = full.dtype == ZTP_F32 ? 4 : 2;
+  const size_t blk = (size_t)(blk_rows * full.cols) * es;
+  const int pe = prof_begin(c, st, PROF_COMM, 0.0);
+  if (c->transport == ZTP_TRANSPORT_PEER) {
+    int64_t off;
+    ztp_status s = win_offset(c, full.ptr, blk * c->world, "all-gather", &off);
+    if (s != ZTP_OK) return s;
+    if (blk % 16) return fail(c, ZTP_ESHAPE, "peer all-gather: block must be a multiple of 16 bytes");
+    CUDA_TRY(c, ztp::peer_allgather_launch(c->pw, off, (int64_t)blk, c->peer_ctas, st));
+    ++c->launches;
+  } else {
+    char* base = static_cast<char*>(full.ptr);
+    NCCL_TRY(c, ncclAllGather(base + c->rank * blk, base, (size_t)(blk_rows * full.cols), nccl_type(full.dtype),
+                              c->comm, st));
+  }
   prof_end(c, pe, st);
   return ZTP_OK;
 }
@@ -525,8 +581,73 @@ ztp_status join_side(ztp_ctx* c, cudaStream_t st) {
   return ZTP_OK;
 }
 
+ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args* a, cudaStream_t st);
+
+ztp_mat row_block(const ztp_mat& m, int64_t r0, int64_t nr) {
+  ztp_mat o = m;
+  const size_t es = m.dtype == ZTP_F32 ? 4 : 2;
+  o.ptr = static_cast<char*>(m.ptr) + (size_t)(r0 * m.ld) * es;
+  o.rows = nr;
+  return o;
+}
+
+// Unpaired mode (a column-parallel FWD whose output is needed whole,
+// a row-parallel layer whose input is not split): the rank computes its row
+// block of the full tensor and an all-gather completes it.
+//   col FWD gather_output: y_t is [world n_out, N]; rows [rank n_out, ...) are
+//     this rank's outputs, then all-gather of y_t.
+//   row input_is_parallel = 0: x_t (and pre_in_t) are the full input [world K,
+//     N], the rank uses rows [rank K, ...); BWD dx_t is [world K, N], the rank
+//     computes its block (imputed rows P included, A-14), then all-gather.
 ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args* a, cudaStream_t st) {
   if (!c || !a) return fail(c, ZTP_EINVAL, "linear: null ctx/args");
+  const bool gat = layer == LAYER_COL && a->gather_output;
+  const bool unsplit_in = layer == LAYER_ROW && !a->input_is_parallel;
+  if (!gat && !unsplit_in) return linear_impl(c, layer, phase, a, st);
+  if (a->skip_collective) return fail(c, ZTP_EINVAL, "unpaired all-gather mode with skip_collective");
+  if (a->out_sel || a->y_pos || a->x_compact || a->dx_compact || a->impute == ZTP_IMPUTE_SAME)
+    return fail(c, ZTP_EUNSUPPORTED, "unpaired all-gather mode: no out_sel / y_pos / compact operands / Same");
+  if (!mat_ok(a->w_t)) return fail(c, ZTP_ESHAPE, "linear: bad " + shp("w_t", a->w_t));
+  ztp_linear_args b = *a;
+  b.gather_output = 0;
+  b.input_is_parallel = 1;
+  const int e = c->world, r = c->rank;
+  if (gat && phase == ZTP_BWD) {   // the gradient of a gathered output: this rank's row block of g_t
+    const int64_t n_out = a->n_out > 0 ? a->n_out : a->w_t.cols;
+    if (!mat_ok(a->g_t) || a->g_t.rows != e * n_out)
+      return fail(c, ZTP_ESHAPE, "gather_output BWD: " + shp("g_t", a->g_t) + " must have world x n_out rows");
+    b.g_t = row_block(a->g_t, r * n_out, n_out);
+    return linear_impl(c, layer, phase, &b, st);
+  }
+  if (gat) {
+    const int64_t n_out = a->n_out > 0 ? a->n_out : a->w_t.cols;
+    if (!mat_ok(a->y_t) || a->y_t.rows != e * n_out)
+      return fail(c, ZTP_ESHAPE, "gather_output: " + shp("y_t", a->y_t) + " must have world x n_out rows");
+    b.y_t = row_block(a->y_t, r * n_out, n_out);
+    ztp_status s = linear_impl(c, layer, phase, &b, st);
+    if (s != ZTP_OK) return s;
+    return allgather_rows(c, a->y_t, n_out, st);
+  }
+  const int64_t K = a->w_t.rows;
+  if (!mat_ok(a->x_t) || a->x_t.rows != e * K)
+    return fail(c, ZTP_ESHAPE, "input_is_parallel = 0: " + shp("x_t", a->x_t) + " must have world x K rows");
+  b.x_t = row_block(a->x_t, r * K, K);
+  if (a->pre_in_t.ptr) {
+    if (a->pre_in_t.rows != e * K) return fail(c, ZTP_ESHAPE, "input_is_parallel = 0: " + shp("pre_in_t", a->pre_in_t));
+    b.pre_in_t = row_block(a->pre_in_t, r * K, K);
+  }
+  if (phase == ZTP_BWD && a->dx_t.ptr) {
+    if (!mat_ok(a->dx_t) || a->dx_t.rows != e * K)
+      return fail(c, ZTP_ESHAPE, "input_is_parallel = 0: " + shp("dx_t", a->dx_t) + " must have world x K rows");
+    b.dx_t = row_block(a->dx_t, r * K, K);
+  }
+  ztp_status s = linear_impl(c, layer, phase, &b, st);
+  if (s != ZTP_OK) return s;
+  if (phase == ZTP_BWD && a->dx_t.ptr) return allgather_rows(c, a->dx_t, K, st);
+  return ZTP_OK;
+}
+
+ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args* a, cudaStream_t st) {
   if (phase == ZTP_FWD) {
     ztp_status js = join_side(c, st);   // a new step: earlier concurrent dW work is ordered before it
     if (js != ZTP_OK) return js;
@@ -540,8 +661,6 @@ ztp_status linear(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_args*
     return fail(c, ZTP_EINVAL, std::string(nm) + ": unknown imputation policy " + std::to_string(a->impute));
   if (a->impute != ZTP_IMPUTE_ZERO && (a->dx_compact || a->out_sel))
     return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + ": dx_compact / out_sel imply Zero imputation (A-35)");
-  if (a->gather_output || (phase == ZTP_BWD && layer == LAYER_ROW && !a->input_is_parallel))
-    return fail(c, ZTP_EUNSUPPORTED, std::string(nm) + ": unpaired all-gather mode not built yet");
   const int dtype = a->w_t.dtype;
   const int32_t* kept;
   const int32_t* pruned;
@@ -759,7 +878,6 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   *out = nullptr;
   if (world < 1 || world > ZTP_MAX_RANKS || rank < 0 || rank >= world)
     return fail(nullptr, ZTP_EINVAL, "ztp_ctx_create: rank/world out of range");
-  if (world > 1 && !uid) return fail(nullptr, ZTP_EINVAL, "ztp_ctx_create: world > 1 needs an NCCL unique id");
   CUDA_TRY(nullptr, cudaSetDevice(device));
   cudaDeviceProp prop;
   CUDA_TRY(nullptr, cudaGetDeviceProperties(&prop, device));
@@ -798,7 +916,9 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
       cudaEventCreateWithFlags(&c->ev_d, cudaEventDisableTiming) != cudaSuccess)
     return cleanup(fail(nullptr, ZTP_ECUDA, "ztp_ctx_create: stream/event creation failed"));
   if (ensure_iota(c, 1 << 16) != ZTP_OK) return cleanup(ZTP_ECUDA);
-  if (world > 1) {
+  c->transport = (world > 1 && !uid) ? ZTP_TRANSPORT_PEER : ZTP_TRANSPORT_NCCL;
+  if (const char* pc = getenv("ZTP_PEER_CTAS")) c->peer_ctas = std::max(1, std::min(ztp::PEER_MAX_CTAS, atoi(pc)));
+  if (world > 1 && uid) {
     ncclUniqueId id;
     std::memcpy(&id, uid, ZTP_UID_BYTES);
     ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
@@ -812,6 +932,11 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
 ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   if (!c) return ZTP_OK;
   if (c->comm) ncclCommDestroy(c->comm);
+  for (int q = 0; q < ZTP_MAX_RANKS; ++q)
+    if (c->win_ipc[q]) cudaIpcCloseMemHandle(c->win_ipc[q]);
+  if (c->win) cudaFree(c->win);
+  if (c->pw.ep) cudaFree(c->pw.ep);
+  if (c->d_one) cudaFree(c->d_one);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
@@ -841,9 +966,13 @@ ztp_status ztp_sync(ztp_ctx* c, void* stream) {
   if (!c) return fail(nullptr, ZTP_EINVAL, "ztp_sync: null ctx");
   CUDA_TRY(c, cudaStreamSynchronize((cudaStream_t)stream));
   CUDA_TRY(c, cudaGetLastError());
-  int32_t flags = 0;
-  CUDA_TRY(c, cudaMemcpy(&flags, c->d_flags, 4, cudaMemcpyDeviceToHost));
-  if (flags) {
+  int32_t flags[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpy(flags, c->d_flags, 8, cudaMemcpyDeviceToHost));
+  if (flags[1]) {
+    cudaMemset(c->d_flags + 1, 0, 4);
+    return fail(c, ZTP_ECUDA, "peer barrier timed out (a rank did not reach the same collective within 10 s)");
+  }
+  if (flags[0]) {
     cudaMemset(c->d_flags, 0, 4);
     return fail(c, ZTP_EINVAL, "ztp_select saw a NaN score");
   }
@@ -863,9 +992,17 @@ ztp_status ztp_allgather_stats(ztp_ctx* c, double T_own, double M_own, double* T
   }
   double* d_send = c->d_stats + 2 * ZTP_MAX_RANKS;  // scratch after the gathered block
   std::vector<double> host(2 * c->world);
-  CUDA_TRY(c, cudaMemcpyAsync(d_send, mine, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
-  NCCL_TRY(c, ncclAllGather(d_send, c->d_stats, 2, ncclDouble, c->comm, st));
-  CUDA_TRY(c, cudaMemcpyAsync(host.data(), c->d_stats, 2 * c->world * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (c->transport == ZTP_TRANSPORT_PEER) {
+    if (!c->win_open) return fail(c, ZTP_EINVAL, "ztp_allgather_stats: open the peer window first");
+    CUDA_TRY(c, ztp::peer_stats_launch(c->pw, T_own, M_own, st));
+    ++c->launches;
+    CUDA_TRY(c, cudaMemcpyAsync(host.data(), c->win + ztp::PEER_STATS_OFF, 2 * c->world * sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+  } else {
+    CUDA_TRY(c, cudaMemcpyAsync(d_send, mine, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+    NCCL_TRY(c, ncclAllGather(d_send, c->d_stats, 2, ncclDouble, c->comm, st));
+    CUDA_TRY(c, cudaMemcpyAsync(host.data(), c->d_stats, 2 * c->world * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
   CUDA_TRY(c, cudaStreamSynchronize(st));
   for (int r = 0; r < c->world; ++r) {
     T_all[r] = host[2 * r];
@@ -1088,7 +1225,8 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
     const int dt = me_src ? x.src.dtype : x.dst.dtype;
     const size_t es = dt == ZTP_F32 ? 4 : 2;
     off[i] = total;
-    if ((me_src || me_dst) && x.src_rank != x.dst_rank) total += ((size_t)x.nr * x.nc * es + 255) & ~size_t(255);
+    if ((me_src || me_dst) && x.src_rank != x.dst_rank && c->transport == ZTP_TRANSPORT_NCCL)
+      total += ((size_t)x.nr * x.nc * es + 255) & ~size_t(255);
   }
   if (total && ensure_ws(c, total) != ZTP_OK) return ZTP_ECUDA;
   char* ws = (char*)c->ws;
@@ -1101,10 +1239,43 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
       CUDA_TRY(c, cudaMemcpy2DAsync((char*)x.dst.ptr + (x.dr0 * x.dst.ld + x.dc0) * es, x.dst.ld * es,
                                     (const char*)x.src.ptr + (x.r0 * x.src.ld + x.c0) * es, x.src.ld * es, x.nc * es,
                                     x.nr, cudaMemcpyDeviceToDevice, st));
-    } else if (x.src_rank == c->rank) {
+    } else if (x.src_rank == c->rank && c->transport == ZTP_TRANSPORT_NCCL) {
       CUDA_TRY(c, cudaMemcpy2DAsync(ws + off[i], x.nc * es, (const char*)x.src.ptr + (x.r0 * x.src.ld + x.c0) * es,
                                     x.src.ld * es, x.nc * es, x.nr, cudaMemcpyDeviceToDevice, st));
     }
+  }
+  if (c->world > 1 && c->transport == ZTP_TRANSPORT_PEER) {
+    // one-sided pulls (P:237 peer copies): the destination reads the source
+    // rank's window at the symmetric offset of its own counterpart of `src`;
+    // no packing, no staging.  Every rank launches the same number of pull
+    // rounds (computed from the common list) since they carry barriers.
+    int per_rank[ZTP_MAX_RANKS] = {0};
+    for (int i = 0; i < n; ++i)
+      if (xs[i].nr > 0 && xs[i].nc > 0 && xs[i].src_rank != xs[i].dst_rank) ++per_rank[xs[i].dst_rank];
+    int rounds = 0;
+    for (int q = 0; q < c->world; ++q)
+      rounds = std::max(rounds, (per_rank[q] + ztp::PEER_MAX_PULLS - 1) / ztp::PEER_MAX_PULLS);
+    std::vector<ztp::PeerPull> mine;
+    for (int i = 0; i < n; ++i) {
+      const ztp_xfer& x = xs[i];
+      if (x.nr == 0 || x.nc == 0 || x.src_rank == x.dst_rank || x.dst_rank != c->rank) continue;
+      if (!mat_ok(x.src) || x.r0 + x.nr > x.src.rows || x.c0 + x.nc > x.src.cols || x.src.dtype != x.dst.dtype)
+        return fail(c, ZTP_ESHAPE, "ztp_migrate (peer): the destination rank passes its own symmetric counterpart "
+                                   "of the source, " + shp("src", x.src) + " does not cover the slice");
+      const size_t es = x.dst.dtype == ZTP_F32 ? 4 : 2;
+      int64_t off;
+      ztp_status s = win_offset(c, x.src.ptr, (size_t)(x.src.rows * x.src.ld) * es, "ztp_migrate", &off);
+      if (s != ZTP_OK) return s;
+      mine.push_back(ztp::PeerPull{x.src_rank, (int32_t)es, off, x.r0, x.c0, x.nr, x.nc, x.src.ld, x.dst.ptr, x.dr0,
+                                   x.dc0, x.dst.ld});
+    }
+    for (int rd = 0; rd < rounds; ++rd) {
+      ztp::PeerPulls P{};
+      for (int k = rd * ztp::PEER_MAX_PULLS; k < (int)mine.size() && P.n < ztp::PEER_MAX_PULLS; ++k) P.x[P.n++] = mine[k];
+      CUDA_TRY(c, ztp::peer_pull_launch(c->pw, P, c->peer_ctas, st));
+      ++c->launches;
+    }
+    return ZTP_OK;
   }
   if (c->world > 1) {
     NCCL_TRY(c, ncclGroupStart());
@@ -1125,6 +1296,116 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
     CUDA_TRY(c, cudaMemcpy2DAsync((char*)x.dst.ptr + (x.dr0 * x.dst.ld + x.dc0) * es, x.dst.ld * es, ws + off[i],
                                   x.nc * es, x.nc * es, x.nr, cudaMemcpyDeviceToDevice, st));
   }
+  return ZTP_OK;
+}
+
+ztp_status ztp_window_create(ztp_ctx* c, size_t bytes, unsigned char handle[ZTP_IPC_BYTES]) {
+  if (!c || !handle) return fail(c, ZTP_EINVAL, "ztp_window_create: null argument");
+  if (c->win) return fail(c, ZTP_EINVAL, "ztp_window_create: the context already has a window");
+  bytes = ((bytes + 4095) & ~size_t(4095)) + ztp::PEER_RESERVED;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMalloc(&c->win, bytes));
+  CUDA_TRY(c, cudaMemset(c->win, 0, bytes));
+  CUDA_TRY(c, cudaMalloc(&c->pw.ep, ztp::PEER_MAX_CTAS * sizeof(uint32_t)));
+  CUDA_TRY(c, cudaMemset(c->pw.ep, 0, ztp::PEER_MAX_CTAS * sizeof(uint32_t)));
+  c->win_bytes = bytes;
+  c->win_used = ztp::PEER_RESERVED;
+  std::memset(handle, 0, ZTP_IPC_BYTES);
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->win));
+  static_assert(sizeof(cudaIpcMemHandle_t) <= 64, "IPC handle size");
+  std::memcpy(handle, &h, sizeof h);
+  const uint64_t raw = reinterpret_cast<uint64_t>(c->win);
+  const int32_t pid = (int32_t)getpid(), dev = c->device;
+  const uint64_t nb = bytes;
+  std::memcpy(handle + 64, &raw, 8);
+  std::memcpy(handle + 72, &pid, 4);
+  std::memcpy(handle + 76, &dev, 4);
+  std::memcpy(handle + 80, &nb, 8);
+  return ZTP_OK;
+}
+
+ztp_status ztp_window_open(ztp_ctx* c, const unsigned char* handles) {
+  if (!c || !handles) return fail(c, ZTP_EINVAL, "ztp_window_open: null argument");
+  if (!c->win) return fail(c, ZTP_EINVAL, "ztp_window_open: create the window first");
+  if (c->win_open) return fail(c, ZTP_EINVAL, "ztp_window_open: already open");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int32_t mypid = (int32_t)getpid();
+  ztp::PeerWin w{};
+  w.rank = c->rank;
+  w.world = c->world;
+  for (int q = 0; q < c->world; ++q) {
+    const unsigned char* h = handles + (size_t)q * ZTP_IPC_BYTES;
+    uint64_t raw, nb;
+    int32_t pid, dev;
+    std::memcpy(&raw, h + 64, 8);
+    std::memcpy(&pid, h + 72, 4);
+    std::memcpy(&dev, h + 76, 4);
+    std::memcpy(&nb, h + 80, 8);
+    if (nb != c->win_bytes)
+      return fail(c, ZTP_ESHAPE, "ztp_window_open: rank " + std::to_string(q) + "'s window has " +
+                                     std::to_string(nb) + " bytes, mine " + std::to_string(c->win_bytes));
+    if (q == c->rank) {
+      w.base[q] = c->win;
+    } else if (pid == mypid) {   // another context of this process: the pointer itself
+      if (dev != c->device) {
+        const cudaError_t pe = cudaDeviceEnablePeerAccess(dev, 0);
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(c, ZTP_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(pe));
+        cudaGetLastError();
+      }
+      w.base[q] = reinterpret_cast<char*>(raw);
+    } else {
+      cudaIpcMemHandle_t ih;
+      std::memcpy(&ih, h, sizeof ih);
+      void* p = nullptr;
+      CUDA_TRY(c, cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+      c->win_ipc[q] = p;
+      w.base[q] = static_cast<char*>(p);
+    }
+    w.flags[q] = reinterpret_cast<uint32_t*>(w.base[q] + ztp::PEER_FLAGS_OFF);
+  }
+  w.ep = c->pw.ep;
+  w.err = c->d_flags + 1;
+  c->pw = w;
+  c->win_open = true;
+  return ZTP_OK;
+}
+
+ztp_status ztp_sym_alloc(ztp_ctx* c, size_t bytes, void** ptr) {
+  if (!c || !ptr) return fail(c, ZTP_EINVAL, "ztp_sym_alloc: null argument");
+  *ptr = nullptr;
+  if (!c->win) return fail(c, ZTP_EINVAL, "ztp_sym_alloc: create the window first");
+  const size_t at = (c->win_used + 255) & ~size_t(255);
+  if (at + bytes > c->win_bytes)
+    return fail(c, ZTP_EINVAL, "ztp_sym_alloc: window exhausted (" + std::to_string(c->win_bytes - at) + " bytes left, " +
+                                   std::to_string(bytes) + " asked)");
+  c->win_used = at + bytes;
+  *ptr = c->win + at;
+  return ZTP_OK;
+}
+
+ztp_status ztp_set_transport(ztp_ctx* c, int transport) {
+  if (!c || (transport != ZTP_TRANSPORT_NCCL && transport != ZTP_TRANSPORT_PEER))
+    return fail(c, ZTP_EINVAL, "ztp_set_transport: unknown transport");
+  if (transport == ZTP_TRANSPORT_NCCL && c->world > 1 && !c->comm)
+    return fail(c, ZTP_EINVAL, "ztp_set_transport: this context has no NCCL communicator");
+  c->transport = transport;
+  return ZTP_OK;
+}
+
+ztp_status ztp_barrier(ztp_ctx* c, void* stream) {
+  if (!c) return fail(c, ZTP_EINVAL, "ztp_barrier: null ctx");
+  if (c->world == 1) return ZTP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c->transport == ZTP_TRANSPORT_PEER) {
+    if (!c->win_open) return fail(c, ZTP_EINVAL, "ztp_barrier: open the peer window first");
+    CUDA_TRY(c, ztp::peer_barrier_launch(c->pw, 1, st));
+    ++c->launches;
+    return ZTP_OK;
+  }
+  if (!c->d_one) CUDA_TRY(c, cudaMalloc(&c->d_one, 16));
+  NCCL_TRY(c, ncclAllReduce(c->d_one, c->d_one, 1, ncclFloat, ncclSum, c->comm, st));
   return ZTP_OK;
 }
 

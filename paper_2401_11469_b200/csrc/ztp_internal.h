@@ -188,4 +188,34 @@ cudaError_t priority_update_launch(const void* w, int64_t ld_w, const void* w_ol
 cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
                              cudaStream_t st);
 
+// Peer-memory data plane (ztp_peer.cu): the symmetric window of every rank
+// mapped into this process, per-(rank, CTA) barrier flags at its start.
+constexpr int PEER_MAX_CTAS = 256;
+constexpr int64_t PEER_FLAGS_OFF = 0;         // u32 flags[ZTP_MAX_RANKS][PEER_MAX_CTAS]
+constexpr int64_t PEER_STATS_OFF = 8192;      // double stats[ZTP_MAX_RANKS][2]
+constexpr int64_t PEER_RESERVED = 65536;      // ztp_sym_alloc starts here
+struct PeerWin {
+  int rank, world;
+  char* base[8];         // window base of every rank, mapped here (base[rank] = own)
+  uint32_t* flags[8];    // = base[q] + PEER_FLAGS_OFF
+  uint32_t* ep;          // local: barrier epoch per CTA slot [PEER_MAX_CTAS]
+  int32_t* err;          // local: 2 = peer barrier timeout
+};
+struct PeerPull {        // dst[dr0 +, dc0 +] <- window of src_rank at src_off [r0 +, c0 +], nr x nc elements
+  int32_t src_rank, es;
+  int64_t src_off, r0, c0, nr, nc, ld_src;
+  void* dst;
+  int64_t dr0, dc0, ld_dst;
+};
+constexpr int PEER_MAX_PULLS = 24;
+struct PeerPulls {
+  int n;
+  PeerPull x[PEER_MAX_PULLS];
+};
+cudaError_t peer_allreduce_launch(const PeerWin& w, int64_t off, int64_t bytes, int f32, int nctas, cudaStream_t st);
+cudaError_t peer_allgather_launch(const PeerWin& w, int64_t off, int64_t blk_bytes, int nctas, cudaStream_t st);
+cudaError_t peer_pull_launch(const PeerWin& w, const PeerPulls& p, int nctas, cudaStream_t st);
+cudaError_t peer_stats_launch(const PeerWin& w, double T, double M, cudaStream_t st);
+cudaError_t peer_barrier_launch(const PeerWin& w, int nctas, cudaStream_t st);
+
 }  // namespace ztp

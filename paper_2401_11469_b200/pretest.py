@@ -51,9 +51,9 @@ def time_step(L, ctx, chi: float = 1.0, steps: int = 30, reps: int = 3) -> float
     import torch
     stream = torch.cuda.Stream()
     Z.ztp_set_slowdown(ctx, chi)
-    L.step(stream)
+    L.step(stream, select=False)          # selection: once per plan, not per step
     torch.cuda.synchronize()
-    g = L.capture(stream)
+    g = L.capture(stream, select=False)
     with torch.cuda.stream(stream):      # replay() issues on the current stream
         for _ in range(3):
             g.replay()
@@ -79,7 +79,7 @@ def gemm_ms(L, ctx, steps: int = 5) -> float:
     Z.ztp_set_stats(ctx, True)
     Z.ztp_read_gemm_ns(ctx)
     for _ in range(steps):
-        L.step()
+        L.step(select=False)
     m = Z.ztp_read_gemm_ns(ctx) / steps / 1e6
     Z.ztp_set_stats(ctx, False)
     return m
