@@ -20,8 +20,10 @@ __all__ = [
     "ztp_version", "ztp_get_unique_id", "ztp_ctx_create", "ztp_ctx_destroy", "ztp_sync", "ztp_launch_count",
     "ztp_plan", "ztp_plan_refine", "ztp_plan_counts", "ztp_allgather_stats", "ztp_select", "ztp_join", "ztp_col_linear", "ztp_row_linear",
     "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "mat",
-    "make_costs", "plan_opts", "ZtpError",
+    "make_costs", "plan_opts", "ZtpError", "ztp_window_create", "ztp_window_open", "ztp_sym_alloc",
+    "ztp_set_transport", "ztp_barrier", "TRANSPORT_NCCL", "TRANSPORT_PEER",
 ]
+from ._lib import TRANSPORT_NCCL, TRANSPORT_PEER  # noqa: E402
 
 
 def _stream(stream) -> Optional[int]:
@@ -228,7 +230,8 @@ def linear_args(x_t=None, w_t=None, y_t=None, pre_t=None, g_t=None, dx_t=None, d
                 sel_: Optional[Sel] = None, n_out: int = 0, impute: int = IMPUTE_ZERO, act: int = ACT_NONE,
                 act_in: int = ACT_NONE, skip_collective: int = 0, xs_t=None, ws_t=None, y_pos=None,
                 x_compact: bool = False, dx_compact: bool = False, out_sel: Optional[Sel] = None,
-                hist_dx=None, hist_dw=None) -> LinearArgs:
+                hist_dx=None, hist_dw=None, gather_output: bool = False, input_is_parallel: bool = True
+                ) -> LinearArgs:
     a = LinearArgs()
     a.x_t, a.w_t, a.y_t, a.pre_t = mat(x_t), mat(w_t), mat(y_t), mat(pre_t)
     a.g_t, a.dx_t, a.dw_t, a.pre_in_t = mat(g_t), mat(dx_t), mat(dw_t), mat(pre_in_t)
@@ -244,8 +247,8 @@ def linear_args(x_t=None, w_t=None, y_t=None, pre_t=None, g_t=None, dx_t=None, d
     a.impute = impute
     a.act = act
     a.act_in = act_in
-    a.gather_output = 0
-    a.input_is_parallel = 1
+    a.gather_output = int(gather_output)
+    a.input_is_parallel = int(input_is_parallel)
     a.skip_collective = skip_collective
     return a
 
@@ -300,6 +303,58 @@ def ztp_migrate(ctx, xfers: Sequence[Xfer], stream=None) -> None:
 
 def xfer(src=None, dst=None, r0=0, c0=0, nr=0, nc=0, dr0=0, dc0=0, src_rank=0, dst_rank=0) -> Xfer:
     return Xfer(mat(src), mat(dst), r0, c0, nr, nc, dr0, dc0, src_rank, dst_rank)
+
+
+# ------------------------------------------------------- peer-memory data plane
+
+def ztp_window_create(ctx, nbytes: int) -> bytes:
+    """Allocate this rank's symmetric window; returns its IPC_BYTES handle."""
+    buf = C.create_string_buffer(_lib.IPC_BYTES)
+    check(lib.ztp_window_create(ctx, int(nbytes), buf), ctx)
+    return buf.raw
+
+
+def ztp_window_open(ctx, handles: Sequence[bytes]) -> None:
+    """Map every rank's window (handles in rank order)."""
+    blob = b"".join(handles)
+    if len(blob) != len(handles) * _lib.IPC_BYTES:
+        raise ValueError("ztp_window_open: every handle must be IPC_BYTES long")
+    check(lib.ztp_window_open(ctx, blob), ctx)
+
+
+class _DevPtr:
+    """__cuda_array_interface__ of library-owned device memory (a window
+    slice), so torch can view it without copying."""
+
+    def __init__(self, ptr: int, nelem: int, typestr: str, device: int):
+        self.__cuda_array_interface__ = {"shape": (nelem,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+        self.device = device
+
+
+def ztp_sym_alloc(ctx, rows: int, cols: int, dtype=None, device: int = 0):
+    """A [rows, cols] tensor (row pitch padded to 16 bytes) carved out of the
+    symmetric window: the same call sequence on every rank yields the same
+    window offsets.  The library owns the memory (valid until
+    ztp_ctx_destroy)."""
+    import torch
+    dtype = dtype or torch.bfloat16
+    es = {torch.bfloat16: 2, torch.float32: 4}[dtype]
+    ld = (cols * es + 15) // 16 * 16 // es
+    p = C.c_void_p()
+    n = max(rows, 1) * ld
+    check(lib.ztp_sym_alloc(ctx, n * es, C.byref(p)), ctx)
+    raw = torch.as_tensor(_DevPtr(p.value, n, "<i2" if es == 2 else "<f4", device), device=f"cuda:{device}")
+    t = raw.view(dtype) if es == 2 else raw
+    return t.view(max(rows, 1), ld)[:, :cols]
+
+
+def ztp_set_transport(ctx, transport: int) -> None:
+    check(lib.ztp_set_transport(ctx, transport), ctx)
+
+
+def ztp_barrier(ctx, stream=None) -> None:
+    check(lib.ztp_barrier(ctx, _stream(stream)), ctx)
 
 
 def ztp_set_slowdown(ctx, chi: float) -> None:

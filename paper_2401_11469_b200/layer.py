@@ -43,6 +43,12 @@ def _buf(r, c, dtype=torch.bfloat16, fill=0.0):
     return t[:, :c]
 
 
+def sym_allocator(ctx, device: int = 0):
+    """Allocator of window tensors (ztp_sym_alloc; zero-filled at window
+    creation) for ZtpLayer(alloc=...) under the peer transport."""
+    return lambda r, c, dtype: Z.ztp_sym_alloc(ctx, r, c, dtype, device)
+
+
 @dataclass
 class MigrationIO:
     """This rank's migration ranges from ztp_plan_counts (FC1/FC2 units)."""
@@ -95,8 +101,12 @@ def xfer_specs(mio: MigrationIO, u: int, h: int, grads: bool) -> List[dict]:
 
 
 class ZtpLayer:
-    def __init__(self, ctx, h: int, f: int, N: int, rank: int, world: int, shards: Dict[str, torch.Tensor],
-                 mig_cap: int = 0, dtype=torch.bfloat16, layer_id: int = 0):
+    def __init__(self, ctx, h: int, f: int, N: int, rank: int, world: int, shards: Optional[Dict[str, torch.Tensor]],
+                 mig_cap: int = 0, dtype=torch.bfloat16, layer_id: int = 0, alloc=None):
+        """alloc(rows, cols, dtype) -> zero-filled tensor: where the layer's
+        buffers live (default torch; `sym_allocator(ctx)` for the peer
+        transport, whose all-reduce and migration operands must be window
+        tensors at the same offsets on every rank)."""
         self.ctx, self.h, self.f, self.N = ctx, h, f, N
         self.rank, self.world = rank, world
         self.a = h // world                  # attention features per rank
@@ -104,42 +114,15 @@ class ZtpLayer:
         self.cap = mig_cap
         self.dtype = dtype
         self.layer_id = layer_id
+        self.alloc = alloc
         a, u, cap = self.a, self.u, mig_cap
-        # weights (W^T), MLP ones with migration capacity
-        self.qkv_t = _buf(h, 3 * a, dtype)
-        self.o_t = _buf(a, h, dtype)
-        self.w1_t = _buf(h, u + cap, dtype)
-        self.w2_t = _buf(u + cap, h, dtype)
-        self.qkv_t.copy_(shards["qkv"])
-        self.o_t.copy_(shards["o"])
-        self.w1_t[:, :u].copy_(shards["w1"])
-        self.w2_t[:u].copy_(shards["w2"])
-        # activations
-        self.X = _buf(h, N, dtype)
-        self.Xc = _buf(h, N, dtype)              # compact X rows S_qkv
-        self.QKV = _buf(3 * a, N, dtype)
-        self.ctxC = _buf(a, N, dtype)            # compact ctx rows S_o
-        self.Y1 = _buf(h, N, dtype)
-        self.Y1c = _buf(h, N, dtype)             # compact Y1 rows S_fc1
-        self.PreC = _buf(u + cap, N, dtype)      # compact GeLU'(pre) rows S_fc2 (ACT_GELU_D)
-        self.HC = _buf(u + cap, N, dtype)        # compact H rows S_fc2
-        self.Y = _buf(h, N, dtype)
-        # gradients
-        self.G = _buf(h, N, dtype)
-        self.G1 = _buf(u + cap, N, dtype)        # dH * GeLU'(pre), compact rows S_fc2 (P_fc2 Zero, implied)
-        self.dY1 = _buf(h, N, dtype)
-        self.dctx = _buf(a, N, dtype)
-        self.gQKV = _buf(3 * a, N, dtype)
-        self.dX = _buf(h, N, dtype)
-        self.dqkv = _buf(h, 3 * a, dtype)
-        self.do = _buf(a, h, dtype)
-        self.dw1 = _buf(h, u + cap, dtype)
-        self.dw2 = _buf(u + cap, h, dtype)
-        # compact weights
-        self.Wqkv_c = _buf(h, 3 * a, dtype)
-        self.Wo_c = _buf(a, h, dtype)
-        self.W1_c = _buf(h, u + cap, dtype)
-        self.W2_c = _buf(u + cap, h, dtype)
+        for name, r, c in self.buffer_specs(h, f, N, world, mig_cap):
+            setattr(self, name, self._new(r, c))
+        if shards is not None:
+            self.qkv_t.copy_(shards["qkv"])
+            self.o_t.copy_(shards["o"])
+            self.w1_t[:, :u].copy_(shards["w1"])
+            self.w2_t[:u].copy_(shards["w2"])
         # selection buffers (lineage)
         self.K = {"qkv": h, "o": a, "fc1": h, "fc2": u + cap}
         total = sum(self.K.values()) + 3 * a        # + the derived V-output segment (A-36)
@@ -149,6 +132,40 @@ class ZtpLayer:
         self.mig = MigrationIO()
         self.n_fc = u                            # FC1 output units computed / FC2 K
         self.set_selection({s: 0 for s in SEGS}, None)
+
+    @staticmethod
+    def buffer_specs(h: int, f: int, N: int, world: int, cap: int):
+        """(attribute, rows, cols) of every device buffer, in allocation order
+        (identical on every rank, so window offsets are symmetric)."""
+        a, u = h // world, f // world
+        return [
+            # weights (W^T), MLP ones with migration capacity
+            ("qkv_t", h, 3 * a), ("o_t", a, h), ("w1_t", h, u + cap), ("w2_t", u + cap, h),
+            # activations: X, compact X rows S_qkv, QKV, compact ctx rows S_o, Y1,
+            # compact Y1 rows S_fc1, compact GeLU'(pre) / H rows S_fc2, Y
+            ("X", h, N), ("Xc", h, N), ("QKV", 3 * a, N), ("ctxC", a, N), ("Y1", h, N), ("Y1c", h, N),
+            ("PreC", u + cap, N), ("HC", u + cap, N), ("Y", h, N),
+            # gradients (G1 = dH * GeLU'(pre), compact rows S_fc2)
+            ("G", h, N), ("G1", u + cap, N), ("dY1", h, N), ("dctx", a, N), ("gQKV", 3 * a, N), ("dX", h, N),
+            ("dqkv", h, 3 * a), ("do", a, h), ("dw1", h, u + cap), ("dw2", u + cap, h),
+            # compact weights
+            ("Wqkv_c", h, 3 * a), ("Wo_c", a, h), ("W1_c", h, u + cap), ("W2_c", u + cap, h),
+        ]
+
+    @staticmethod
+    def window_bytes(h: int, f: int, N: int, world: int, cap: int = 0, es: int = 2) -> int:
+        """Symmetric-window bytes the layer's buffers take (ztp_sym_alloc
+        rounds every allocation to 256 bytes)."""
+        tot = 0
+        for _, r, c in ZtpLayer.buffer_specs(h, f, N, world, cap):
+            ld = (c * es + 15) // 16 * 16 // es
+            tot += (max(r, 1) * ld * es + 255) // 256 * 256
+        return tot
+
+    def _new(self, r, c):
+        if self.alloc is not None:
+            return self.alloc(r, c, self.dtype)
+        return _buf(r, c, self.dtype)
 
     # ------------------------------------------------------------------ plan
     def set_migration(self, mio: MigrationIO):
@@ -318,7 +335,11 @@ class ZtpLayer:
         xs = []
         for d in xfer_specs(self.mig, self.u, self.h, grads):
             t = tens[d["t"]]
-            xs.append(Z.xfer(t if self.rank == d["src"] else None, t if self.rank == d["dst"] else None,
+            # every rank passes its own tensor as both ends: the source rank's
+            # is read (NCCL: packed and sent), the destination rank's is written,
+            # and under the peer transport the destination's own counterpart of
+            # the source locates the slice in the source rank's window
+            xs.append(Z.xfer(t, t,
                              r0=d["r0"], c0=d["c0"], nr=d["nr"], nc=d["nc"], dr0=d["dr0"], dc0=d["dc0"],
                              src_rank=d["src"], dst_rank=d["dst"]))
         return xs
