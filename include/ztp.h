@@ -512,12 +512,14 @@ ztp_status ztp_core(ztp_ctx* ctx, ztp_phase phase, const ztp_mat* qkv_t, const z
  * it.  src_rank == dst_rank is a local device copy.  The slice is moved
  * exactly once over NVLink (the straggler's egress is the scarce resource;
  * helpers receive disjoint slices instead of full broadcasts).
- * Peer transport: the destination PULLS from the source rank's window --
+ * Peer pulls (the peer transport, or any context whose window is open --
+ * the NCCL transport then carries only the collectives): the destination
+ * PULLS from the source rank's window --
  * `src` must be a window tensor, and on the destination rank `src` is its
  * OWN symmetric counterpart (same ztp_sym_alloc slot), whose window offset
  * locates the source's copy; one kernel per 24 pulls per rank, with device
  * barriers before (sources final) and after (sources not yet reused).
- * NCCL transport: the slices are staged through a workspace and moved by
+ * NCCL transport without a window: the slices are staged through a workspace and moved by
  * grouped ncclSend / ncclRecv (any pattern is deadlock-free).
  * ------------------------------------------------------------------------- */
 typedef struct ztp_xfer {

@@ -1210,6 +1210,9 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
     ztp_status js = join_side(c, st);   // returned dW slices must be complete
     if (js != ZTP_OK) return js;
   }
+  // one-sided peer pulls whenever the symmetric window is open (also under
+  // the NCCL transport for the collectives): no staging copies
+  const bool peer = c->world > 1 && (c->transport == ZTP_TRANSPORT_PEER || c->win_open);
   std::vector<size_t> off(n, 0);
   size_t total = 0;
   for (int i = 0; i < n; ++i) {
@@ -1225,7 +1228,7 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
     const int dt = me_src ? x.src.dtype : x.dst.dtype;
     const size_t es = dt == ZTP_F32 ? 4 : 2;
     off[i] = total;
-    if ((me_src || me_dst) && x.src_rank != x.dst_rank && c->transport == ZTP_TRANSPORT_NCCL)
+    if ((me_src || me_dst) && x.src_rank != x.dst_rank && !peer)
       total += ((size_t)x.nr * x.nc * es + 255) & ~size_t(255);
   }
   if (total && ensure_ws(c, total) != ZTP_OK) return ZTP_ECUDA;
@@ -1239,12 +1242,12 @@ ztp_status ztp_migrate(ztp_ctx* c, int n, const ztp_xfer* xs, void* stream) {
       CUDA_TRY(c, cudaMemcpy2DAsync((char*)x.dst.ptr + (x.dr0 * x.dst.ld + x.dc0) * es, x.dst.ld * es,
                                     (const char*)x.src.ptr + (x.r0 * x.src.ld + x.c0) * es, x.src.ld * es, x.nc * es,
                                     x.nr, cudaMemcpyDeviceToDevice, st));
-    } else if (x.src_rank == c->rank && c->transport == ZTP_TRANSPORT_NCCL) {
+    } else if (x.src_rank == c->rank && !peer) {
       CUDA_TRY(c, cudaMemcpy2DAsync(ws + off[i], x.nc * es, (const char*)x.src.ptr + (x.r0 * x.src.ld + x.c0) * es,
                                     x.src.ld * es, x.nc * es, x.nr, cudaMemcpyDeviceToDevice, st));
     }
   }
-  if (c->world > 1 && c->transport == ZTP_TRANSPORT_PEER) {
+  if (peer) {
     // one-sided pulls (P:237 peer copies): the destination reads the source
     // rank's window at the symmetric offset of its own counterpart of `src`;
     // no packing, no staging.  Every rank launches the same number of pull

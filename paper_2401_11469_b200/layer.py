@@ -427,10 +427,58 @@ class ZtpLayer:
         self._graph.replay()
 
     # ------------------------------------------------------------ accounting
-    def executed_flops(self) -> float:
-        """FLOPs of the resized layer: 6 N n K' per linear (fwd + dX + dW),
-        SURVEY §8(d).  The method's count -- output pruning (FC1 computing only
-        FC2's kept units) executes fewer for the same result."""
+    def method_flops(self) -> float:
+        """FLOPs of the resized layer by the method's count: 6 N n K' per
+        linear (fwd + dX + dW), SURVEY §8(d)."""
         N, a, h = self.N, self.a, self.h
         nk = self.nk
         return 6.0 * N * (3 * a * nk["qkv"] + h * nk["o"] + self.n_fc * nk["fc1"] + h * nk["fc2"])
+
+    def executed_flops(self) -> float:
+        """FLOPs the GEMMs of one step execute: as method_flops, except that
+        FC1 computes only the units FC2 keeps (A-35) and QKV computes V only
+        for O's kept features (A-36) -- same results, less work."""
+        N, a, h = self.N, self.a, self.h
+        nk = self.nk
+        n_qkv = 2 * a + nk["o"] if self.vsel is not None else 3 * a
+        n_fc1 = nk["fc2"] if self.sels["fc2"] is not None else self.n_fc
+        return 6.0 * N * (n_qkv * nk["qkv"] + h * nk["o"] + n_fc1 * nk["fc1"] + h * nk["fc2"])
+
+
+class ZtpStack:
+    """Several layers of one rank run as one step: per layer the weight
+    migration pulls (SEMI plans), then the forward of every layer, the
+    backward in reverse order, and the migrated dW slices returned.  The
+    selection runs once per plan (set_selection; the priority list is
+    epoch-granular), not inside the step."""
+
+    def __init__(self, layers: List[ZtpLayer]):
+        self.layers = layers
+
+    def step(self, stream=None, select: bool = False):
+        for L in self.layers:
+            if select:
+                L.run_select(stream)
+            L.migrate_weights(stream)
+        for L in self.layers:
+            L.forward(stream)
+        for L in reversed(self.layers):
+            L.backward(stream)
+        for L in self.layers:
+            L.return_grads(stream)
+
+    def capture(self, stream, select: bool = False, pre=None, post=None):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            if pre is not None:
+                pre()
+            self.step(stream, select=select)
+            if post is not None:
+                post()
+        return g
+
+    def method_flops(self) -> float:
+        return sum(L.method_flops() for L in self.layers)
+
+    def executed_flops(self) -> float:
+        return sum(L.executed_flops() for L in self.layers)

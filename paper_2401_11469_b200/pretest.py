@@ -91,7 +91,7 @@ def _homog_counts(L, g: float) -> Dict[str, int]:
 
 
 def pretest(L, ctx, scores: Dict, *, gammas: Sequence[float] = GAMMAS, fracs: Sequence[float] = FRACS,
-            steps: int = 30, link_gbs: Optional[float] = None, ctx_rank: int = 0):
+            steps: int = 30, link_gbs: Optional[float] = None, ctx_rank: int = 0, world_pull: bool = False):
     """Run the pretest on this rank's layer `L` (a ZtpLayer built with
     mig_cap >= L.u * max(fracs)) and return (costs, report).
 
@@ -101,6 +101,8 @@ def pretest(L, ctx, scores: Dict, *, gammas: Sequence[float] = GAMMAS, fracs: Se
     additionally modelled as bytes / link_gbs + the measured per-call fixed
     cost, and the MODEL is what the returned costs use (a one-GPU run cannot
     time NVLink; report["phi1_measured"] keeps the local copies).
+    world_pull (TP > 1, every rank calls pretest in lockstep): Phi_1 is timed
+    on real peer pulls between ranks (ztp_migrate), no model.
     The layer is left dense, without migration."""
     import torch
     from paper_2401_11469_b200.layer import MigrationIO
@@ -143,11 +145,15 @@ def pretest(L, ctx, scores: Dict, *, gammas: Sequence[float] = GAMMAS, fracs: Se
         if n == 0 or n > L.cap:
             continue
         xs = []
-        for t_src, t_dst, r0, c0, nr, nc, dr0, dc0 in (
-                (L.w1_t, L.w1_t, 0, 0, h, n, 0, u), (L.w2_t, L.w2_t, 0, 0, n, h, u, 0),
-                (L.dw1, L.dw1, 0, u, h, n, 0, 0), (L.dw2, L.dw2, u, 0, n, h, 0, 0)):
-            xs.append(Z.xfer(t_src, t_dst, r0=r0, c0=c0, nr=nr, nc=nc, dr0=dr0, dc0=dc0,
-                             src_rank=ctx_rank, dst_rank=ctx_rank))
+        # one GPU: local copies; TP > 1 (world_pull): every rank d pulls the
+        # slices of rank d+1 -- n units cross every link, as they cross the
+        # straggler's egress in a plan (collective: all ranks run it)
+        pairs = ([((d + 1) % L.world, d) for d in range(L.world)] if world_pull and L.world > 1
+                 else [(ctx_rank, ctx_rank)])
+        for src_r, dst_r in pairs:
+            for t, r0, c0, nr, nc, dr0, dc0 in ((L.w1_t, 0, 0, h, n, 0, u), (L.w2_t, 0, 0, n, h, u, 0),
+                                               (L.dw1, 0, u, h, n, 0, 0), (L.dw2, u, 0, n, h, 0, 0)):
+                xs.append(Z.xfer(t, t, r0=r0, c0=c0, nr=nr, nc=nc, dr0=dr0, dc0=dc0, src_rank=src_r, dst_rank=dst_r))
         for _ in range(3):
             Z.ztp_migrate(ctx, xs, stream)
         torch.cuda.synchronize()
