@@ -448,7 +448,10 @@ def plan_counts(p: Plan, rank: int, K: int, n_units: int, unit: int, is_row: boo
     if npr < 0:
         npr = 0
     c.n_prune = npr
-    receivers = [r for r in range(e) if p.role[r] not in (MIGRATE, SPLIT)]
+    # receivers: the NORMAL tasks ("evenly distributed across other
+    # normal tasks"; reading A-44) -- never resized, so migration stays
+    # loss-free
+    receivers = [r for r in range(e) if p.role[r] == NORMAL]
     for s in p.order:
         nm = nmig(s)
         if nm == 0:
@@ -620,6 +623,40 @@ def impute_rows(out_S: np.ndarray, S, P, K: int, policy: str = "zero", hist=None
     return out
 
 
+# Summation order of every contraction of the layer ("fp64,
+# naive loops ... every output element keeps one fixed summation order").
+# "blas": numpy's product (fast, any order; results within the fp64 bound
+# K 2^-53 sum|terms| of the exact sum).  "fixed": the naive loop over the
+# contraction index in ascending order, each product and each add rounded
+# once (no FMA) -- bit-reproducible, used where a pin needs exact equality.
+_ORDER = ["blas"]
+
+
+class fixed_order:
+    """with fixed_order(): every contraction is the naive k-ascending loop."""
+
+    def __enter__(self):
+        self._prev = _ORDER[0]
+        _ORDER[0] = "fixed"
+        return self
+
+    def __exit__(self, *exc):
+        _ORDER[0] = self._prev
+        return False
+
+
+def contract(A, B):
+    """A^T B = sum over the rows k of A and B (ascending) of outer(A[k], B[k])."""
+    A = np.asarray(A, dtype=np.float64)
+    B = np.asarray(B, dtype=np.float64)
+    if _ORDER[0] == "blas":
+        return A.T @ B
+    acc = np.zeros((A.shape[1], B.shape[1]), dtype=np.float64)
+    for k in range(A.shape[0]):
+        acc = acc + np.multiply.outer(A[k], B[k])
+    return acc
+
+
 def linear_fwd(Wt, Xt, S=None):
     """Forward with dual pruning: drop rows P of Wt [K,n] and Xt [K,N]
     (the paper's columns), concatenate survivors in ascending order, multiply.
@@ -627,9 +664,9 @@ def linear_fwd(Wt, Xt, S=None):
     Wt = np.asarray(Wt, dtype=np.float64)
     Xt = np.asarray(Xt, dtype=np.float64)
     if S is None:
-        return Wt.T @ Xt
+        return contract(Wt, Xt)
     S = np.asarray(S, dtype=np.int64)
-    return Wt[S].T @ Xt[S]
+    return contract(Wt[S], Xt[S])
 
 
 def linear_bwd_dx(Wt, Gt, S=None, P=None, policy="zero", hist=None):
@@ -638,8 +675,8 @@ def linear_bwd_dx(Wt, Gt, S=None, P=None, policy="zero", hist=None):
     Wt = np.asarray(Wt, dtype=np.float64)
     Gt = np.asarray(Gt, dtype=np.float64)
     if S is None:
-        return Wt @ Gt
-    return impute_rows(Wt[np.asarray(S)] @ Gt, S, P, Wt.shape[0], policy, hist)
+        return contract(Wt.T, Gt)
+    return impute_rows(contract(Wt[np.asarray(S)].T, Gt), S, P, Wt.shape[0], policy, hist)
 
 
 def linear_bwd_dw(Xt, Gt, S=None, P=None, policy="zero", hist=None):
@@ -648,8 +685,8 @@ def linear_bwd_dw(Xt, Gt, S=None, P=None, policy="zero", hist=None):
     Xt = np.asarray(Xt, dtype=np.float64)
     Gt = np.asarray(Gt, dtype=np.float64)
     if S is None:
-        return Xt @ Gt.T
-    return impute_rows(Xt[np.asarray(S)] @ Gt.T, S, P, Xt.shape[0], policy, hist)
+        return contract(Xt.T, Gt.T)
+    return impute_rows(contract(Xt[np.asarray(S)].T, Gt.T), S, P, Xt.shape[0], policy, hist)
 
 
 def fold(parts):
@@ -695,25 +732,40 @@ def shard_layer(WQt, WKt, WVt, WOt, W1t, W2t, e: int) -> LayerShards:
     return LayerShards(qkv, o, w1, w2)
 
 
-def dense_layer_step(Xt, Gt, WQt, WKt, WVt, WOt, W1t, W2t):
+def dense_layer_step(Xt, Gt, WQt, WKt, WVt, WOt, W1t, W2t, blocks: int = 1):
     """The unsplit, unpruned layer written directly (no TP): the reference the
-    TP layer must reproduce at gamma = 0 (BASELINE north_star)."""
-    q, k, v = WQt.T @ Xt, WKt.T @ Xt, WVt.T @ Xt
-    ctx = q + k + v
-    Y1 = WOt.T @ ctx
-    pre = W1t.T @ Y1
+    TP layer must reproduce at gamma = 0 (BASELINE north_star).
+
+    blocks = e: every contraction over a dimension 1D TP splits -- the O and
+    FC2 forward inputs, FC1's and QKV's grad_output contractions -- is summed
+    per block of e contiguous parts and the block sums are added in block
+    order (the summation order of e ranks and a left-fold all-reduce).  With
+    fixed_order() the TP layer at gamma = 0 equals this bit-for-bit; any two
+    block counts agree within the fp64 bound."""
+    h = Xt.shape[0]
+    f = W1t.shape[1]
+    a, u = h // blocks, f // blocks
+    Fb = [slice(r * a, (r + 1) * a) for r in range(blocks)]
+    Ub = [slice(r * u, (r + 1) * u) for r in range(blocks)]
+    q, k, v = contract(WQt, Xt), contract(WKt, Xt), contract(WVt, Xt)
+    ctx = (q + k) + v
+    Y1 = fold([contract(WOt[F], ctx[F]) for F in Fb])
+    pre = contract(W1t, Y1)
     H = gelu_tanh(pre)
-    Y = W2t.T @ H
+    Y = fold([contract(W2t[U], H[U]) for U in Ub])
     # backward
-    dW2t = H @ Gt.T
-    dH = W2t @ Gt
+    dW2t = contract(H.T, Gt.T)
+    dH = contract(W2t.T, Gt)
     G1 = dH * gelu_tanh_grad(pre)
-    dW1t = Y1 @ G1.T
-    dY1 = W1t @ G1
-    dWOt = ctx @ dY1.T
-    dctx = WOt @ dY1
-    dWQt = Xt @ dctx.T
-    dX = (WQt @ dctx + WKt @ dctx) + WVt @ dctx
+    dW1t = contract(Y1.T, G1.T)
+    dY1 = fold([contract(W1t[:, U].T, G1[U]) for U in Ub])
+    dWOt = contract(ctx.T, dY1.T)
+    dctx = contract(WOt.T, dY1)
+    dWQt = contract(Xt.T, dctx.T)
+    # the QKV grad_output contracts over the concatenated [Q | K | V] outputs;
+    # block r = [Q_r | K_r | V_r] (one rank's column shard)
+    dX = fold([contract(np.concatenate([WQt[:, F], WKt[:, F], WVt[:, F]], axis=1).T,
+                        np.concatenate([dctx[F], dctx[F], dctx[F]], axis=0)) for F in Fb])
     return dict(Y=Y, dX=dX, dWQt=dWQt, dWKt=dWQt.copy(), dWVt=dWQt.copy(),
                 dWOt=dWOt, dW1t=dW1t, dW2t=dW2t)
 
@@ -795,7 +847,7 @@ def layer_step(Xt, Gt, sh: LayerShards, sel=None, mig=None, merged=True, policy=
         pj = linear_fwd(sh.w1_t[s][:, lo:hi], Y1, Sr)
         preJ[(s, r)] = pj
         HJ[(s, r)] = gelu_tanh(pj)
-        contrib = sh.w2_t[s][lo:hi].T @ HJ[(s, r)]
+        contrib = contract(sh.w2_t[s][lo:hi], HJ[(s, r)])
         flops[r] += 2.0 * (hi - lo) * N * (kept_count(r, "fc1", h) + h)
         if merged:
             y_parts[r] = y_parts[r] + contrib          # local reduce merged
@@ -824,8 +876,8 @@ def layer_step(Xt, Gt, sh: LayerShards, sel=None, mig=None, merged=True, policy=
         dW1[r][:, :nown] = linear_bwd_dw(Y1, G1, S, P, policy)
         flops[r] += 2.0 * 2.0 * kept_count(r, "fc1", h) * nown * N
     for (s, r, lo, hi) in mig:
-        dHJ = sh.w2_t[s][lo:hi] @ Gt
-        dW2[s][lo:hi] = HJ[(s, r)] @ Gt.T                  # returned to the owner
+        dHJ = contract(sh.w2_t[s][lo:hi].T, Gt)
+        dW2[s][lo:hi] = contract(HJ[(s, r)].T, Gt.T)       # returned to the owner
         G1J = dHJ * gelu_tanh_grad(preJ[(s, r)])
         Sr, Pr = S_of(r, "fc1")
         contrib = linear_bwd_dx(sh.w1_t[s][:, lo:hi], G1J, Sr, Pr, policy)

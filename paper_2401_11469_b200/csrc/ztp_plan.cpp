@@ -421,8 +421,11 @@ extern "C" ztp_status ztp_plan_counts(const ztp_plan_t* p, int rank, int64_t K, 
   out->n_prune = (int32_t)npr;
   int recv[ZTP_MAX_RANKS];
   int nrecv = 0;
+  // receivers: the NORMAL tasks ("evenly distributed across other
+  // normal tasks"; A-44) -- they never resize, so migrated work stays
+  // loss-free
   for (int r = 0; r < e; ++r)
-    if (!migrating(r)) recv[nrecv++] = r;
+    if (p->role[r] == ZTP_NORMAL) recv[nrecv++] = r;
   for (int i = 0; i < e; ++i) {
     const int s = p->order[i];
     const int64_t nm = nmig(s);
@@ -467,16 +470,18 @@ extern "C" ztp_status ztp_layer_prune_counts(const ztp_plan_t* p, int rank, int6
   }
   // A-37: heads do not migrate (A-26), so a rank that sheds MLP units
   // resizes its attention by its Eq.1 gamma; others by gamma_r.
-  ztp_plan_t att = *p;
-  if (p->role[rank] == ZTP_MIGRATE || p->role[rank] == ZTP_SPLIT) att.gamma_r[rank] = p->gamma[rank];
-  att.role[rank] = ZTP_RESIZE;
-  att.phi[rank] = 0.0;
+  const double g_att =
+      (p->role[rank] == ZTP_MIGRATE || p->role[rank] == ZTP_SPLIT) ? p->gamma[rank] : p->gamma_r[rank];
+  auto att = [&](int64_t K) -> int32_t {   // A-3 rounding, A-4 clamp
+    int64_t n = (int64_t)std::floor((double)K * g_att + 0.5);
+    if (n > K - 1) n = K - 1;
+    if (n < 0) n = 0;
+    return (int32_t)n;
+  };
+  out[0] = att(h);
+  out[1] = att(a);
   ztp_counts c;
   ztp_status s;
-  if ((s = ztp_plan_counts(&att, rank, h, h, 1, 0, &c)) != ZTP_OK) return s;
-  out[0] = c.n_prune;
-  if ((s = ztp_plan_counts(&att, rank, a, a, 1, 0, &c)) != ZTP_OK) return s;
-  out[1] = c.n_prune;
   if ((s = ztp_plan_counts(p, rank, h, u, 1, 0, &c)) != ZTP_OK) return s;
   out[2] = c.n_prune;
   if ((s = ztp_plan_counts(p, rank, u, u, 1, 1, &c)) != ZTP_OK) return s;

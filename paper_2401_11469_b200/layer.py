@@ -102,11 +102,15 @@ def xfer_specs(mio: MigrationIO, u: int, h: int, grads: bool) -> List[dict]:
 
 class ZtpLayer:
     def __init__(self, ctx, h: int, f: int, N: int, rank: int, world: int, shards: Optional[Dict[str, torch.Tensor]],
-                 mig_cap: int = 0, dtype=torch.bfloat16, layer_id: int = 0, alloc=None):
+                 mig_cap: int = 0, dtype=torch.bfloat16, layer_id: int = 0, alloc=None, plain: bool = False):
         """alloc(rows, cols, dtype) -> zero-filled tensor: where the layer's
         buffers live (default torch; `sym_allocator(ctx)` for the peer
         transport, whose all-reduce and migration operands must be window
-        tensors at the same offsets on every rank)."""
+        tensors at the same offsets on every rank).
+        plain (always so for dtype float32, the verification mode A-30): no
+        producer-side compaction and no output pruning -- every activation
+        is kept at full size, the GEMMs read kept rows through the lineage
+        and the epilogues write / zero-impute rows at their positions."""
         self.ctx, self.h, self.f, self.N = ctx, h, f, N
         self.rank, self.world = rank, world
         self.a = h // world                  # attention features per rank
@@ -115,6 +119,7 @@ class ZtpLayer:
         self.dtype = dtype
         self.layer_id = layer_id
         self.alloc = alloc
+        self.plain = plain or dtype == torch.float32
         a, u, cap = self.a, self.u, mig_cap
         for name, r, c in self.buffer_specs(h, f, N, world, mig_cap):
             setattr(self, name, self._new(r, c))
@@ -191,7 +196,7 @@ class ZtpLayer:
         # selection is a derived segment over the 3a QKV outputs -- Q and K
         # scored +inf (never pruned), V scored like O's inputs -- selected in
         # the same launch, so it is exactly O's (S_o, P_o) shifted by 2a.
-        self.v_prune = self.n_prune["o"] > 0 and os.environ.get("ZTP_V_PRUNE", "1") != "0"
+        self.v_prune = self.n_prune["o"] > 0 and os.environ.get("ZTP_V_PRUNE", "1") != "0" and not self.plain
         segs = SEGS + (("vo",) if self.v_prune else ())
         if self.v_prune:
             self.seg_len["vo"], self.append["vo"], self.n_prune["vo"] = 3 * self.a, 0, self.n_prune["o"]
@@ -272,9 +277,30 @@ class ZtpLayer:
         p = self.P[s] if self.n_prune[s] > 0 else self.kept
         return Z.sel(self.S[s], self.nk[s], p, self.n_prune[s], self.layer_id, mid)
 
+    def _build_args_plain(self):
+        """Argument structs of the plain arrangement (see __init__)."""
+        h, a, N, nfc = self.h, self.a, self.N, self.n_fc
+        L = Z.linear_args
+        self.vsel, self.y1_direct, self._prep = None, False, []
+        sl = self.sels
+        self.f_qkv = L(x_t=self.X, w_t=self.qkv_t, y_t=self.QKV, sel_=sl["qkv"], n_out=3 * a)
+        self.f_o = L(x_t=self.ctxC, w_t=self.o_t, y_t=self.Y1, sel_=sl["o"])
+        self.f_fc1 = L(x_t=self.Y1, w_t=self.w1_t, y_t=self.HC[:nfc], pre_t=self.PreC[:nfc], sel_=sl["fc1"],
+                       n_out=nfc, act=Z.ACT_GELU_D)
+        self.f_fc2 = L(x_t=self.HC[:nfc], w_t=self.w2_t[:nfc], y_t=self.Y, sel_=sl["fc2"])
+        self.b_fc2 = L(x_t=self.HC[:nfc], w_t=self.w2_t[:nfc], g_t=self.G, dx_t=self.G1[:nfc], dw_t=self.dw2[:nfc],
+                       pre_in_t=self.PreC[:nfc], sel_=sl["fc2"], act_in=Z.ACT_GELU_D)
+        self.b_fc1 = L(x_t=self.Y1, w_t=self.w1_t, g_t=self.G1[:nfc], dx_t=self.dY1, dw_t=self.dw1, sel_=sl["fc1"],
+                       n_out=nfc)
+        self.b_o = L(x_t=self.ctxC, w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx, dw_t=self.do, sel_=sl["o"])
+        self.b_qkv = L(x_t=self.X, w_t=self.qkv_t, g_t=self.gQKV, dx_t=self.dX, dw_t=self.dqkv, sel_=sl["qkv"],
+                       n_out=3 * a)
+
     def _build_args(self):
         h, a, N, nfc = self.h, self.a, self.N, self.n_fc
         self.sels = {s: self._sel(s, i) for i, s in enumerate(SEGS)}
+        if self.plain:
+            return self._build_args_plain()
         vsel = self._sel("vo", 4) if self.v_prune else None
         self.vsel = vsel
         L = Z.linear_args
@@ -364,8 +390,11 @@ class ZtpLayer:
         c = self.ctx
         self.prepare(stream)
         Z.ztp_col_linear(c, Z.FWD, self.f_qkv, stream)
-        Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, self.S["o"], self.nk["o"], stream,
-                   v_compact=self.vsel is not None)
+        if self.plain:     # ctx at full size, O reads its kept rows through the lineage
+            Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, None, 0, stream)
+        else:              # ctx written compact in O's kept order
+            Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, self.S["o"], self.nk["o"], stream,
+                       v_compact=self.vsel is not None)
         Z.ztp_row_linear(c, Z.FWD, self.f_o, stream)          # + all-reduce of Y1
 
     def fwd_mlp(self, stream=None):

@@ -474,3 +474,47 @@ def test_priority_update_next1(env, K, n):
     S2, P2 = O.select(got, npr)
     assert np.array_equal(kept.cpu().numpy()[:K - npr], S2)
     assert np.array_equal(pr.cpu().numpy()[:npr], P2)
+
+
+@pytest.mark.parametrize("incremental", [True, False])
+def test_anti_endless_loop_on_gpu_S410(env, incremental):
+    """S:410 / P:190 scenario of tests/test_oracle_select.py driven through the
+    GPU kernels (ztp_priority_update + ztp_select, bf16 weights): every
+    epoch's GPU scores match the oracle's on the same weights (1e-4), its
+    selection equals the oracle's select on the GPU scores bit for bit, and
+    the incremental rule rotates the pruned set (>= 3 distinct in 10 epochs)
+    where the naive update freezes on the first one."""
+    Z, torch, ctx = env
+    K, n, npr = 64, 32, 16
+    rng = np.random.default_rng(410)
+    W = I.round_bf16(rng.standard_normal((K, n)))
+    d0 = rng.random(K).astype(np.float32)
+    delta = torch.tensor(d0, device="cuda")
+    kept = torch.empty(K, dtype=torch.int32, device="cuda")
+    pr = torch.empty(npr, dtype=torch.int32, device="cuda")
+    pos = torch.empty(K, dtype=torch.int32, device="cuda")
+    Z.ztp_select(ctx, [K], [npr], delta, kept, pr, pos=pos)
+    Z.ztp_sync(ctx)
+    sets = [tuple(pr.cpu().tolist())]
+    assert list(sets[0]) == list(O.select(d0, npr)[1])
+    for _ in range(9):
+        W_old = W
+        scale = rng.lognormal(-3.0, 1.0, size=K)
+        upd = rng.standard_normal((K, n)) * scale[:, None]
+        upd[np.asarray(sets[-1])] = 0.0
+        W = I.round_bf16(W + upd)
+        prev = delta.cpu().numpy().astype(np.float64)
+        Z.ztp_priority_update(ctx, dev(torch, W), dev(torch, W_old), delta,
+                              pos_prev=pos if incremental else None)
+        Z.ztp_sync(ctx)
+        got = delta.cpu().numpy()
+        ref = O.priority_update(prev, W, W_old, list(sets[-1]) if incremental else None)
+        assert np.allclose(got, ref, rtol=1e-4, atol=1e-12)
+        Z.ztp_select(ctx, [K], [npr], delta, kept, pr, pos=pos)
+        Z.ztp_sync(ctx)
+        sets.append(tuple(pr.cpu().tolist()))
+        assert list(sets[-1]) == list(O.select(got, npr)[1])
+    if incremental:
+        assert len(set(sets)) >= 3
+    else:
+        assert all(sset == sets[0] for sset in sets)

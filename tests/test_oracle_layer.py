@@ -150,6 +150,53 @@ def test_tp_equivalence_gamma0(e):
     assert out["allreduce_count"] == 4          # 2 per layer per direction (A-29)
 
 
+@pytest.mark.parametrize("e", [1, 2, 4])
+def test_tp_gamma0_reproduces_unsplit_bitexact_fixed_order(e):
+    """BJ north_star "ratio 0 and no migration reproduce the unsplit full GEMM
+    exactly" (SURVEY §8(c) pin 1): with every contraction the naive
+    k-ascending loop, the e-rank layer at gamma = 0 equals, bit for bit, the
+    unsplit dense layer summed per shard block and over blocks in rank order;
+    and the block order differs from the textbook one-block order by no more
+    than the fp64 bound."""
+    Xt, Gt, W, sh = _make(e, h=16, f=32, N=6, seed=3 + e)
+    with O.fixed_order():
+        out = O.layer_step(Xt, Gt, sh)
+        ref = O.dense_layer_step(Xt, Gt, *W, blocks=e)
+        one = O.dense_layer_step(Xt, Gt, *W, blocks=1)
+    h, f = Xt.shape[0], W[4].shape[1]
+    a, u = h // e, f // e
+    assert np.array_equal(out["Y"], ref["Y"]) and np.array_equal(out["dX"], ref["dX"])
+    for r in range(e):
+        assert np.array_equal(out["dW1"][r], ref["dW1t"][:, r * u:(r + 1) * u])
+        assert np.array_equal(out["dW2"][r], ref["dW2t"][r * u:(r + 1) * u])
+        assert np.array_equal(out["dWo"][r], ref["dWOt"][r * a:(r + 1) * a])
+        assert np.array_equal(out["dWqkv"][r][:, :a], ref["dWQt"][:, r * a:(r + 1) * a])
+    for k in ("Y", "dX"):
+        sc = np.max(np.abs(one[k]))
+        assert np.max(np.abs(ref[k] - one[k])) <= (h + f) * 2.0 ** -52 * sc * 8
+    # the BLAS order agrees with the fixed order within the fp64 bound
+    blas = O.layer_step(Xt, Gt, sh)
+    for k in ("Y", "dX"):
+        assert np.max(np.abs(blas[k] - out[k])) <= 1e-12 * np.max(np.abs(out[k]))
+
+
+def test_fixed_order_contract_against_exact_sums():
+    """The fixed-order contraction is the k-ascending loop: against math.fsum
+    (exactly rounded) within K 2^-53 sum|terms|, and it reproduces a hand
+    evaluation of the same loop bit for bit."""
+    A, B = _rand((7, 3), 41), _rand((7, 4), 42)
+    with O.fixed_order():
+        C = O.contract(A, B)
+    for j in range(3):
+        for t in range(4):
+            acc = 0.0
+            for k in range(7):
+                acc = acc + A[k, j] * B[k, t]
+            assert C[j, t] == acc
+            ex = math.fsum(A[k, j] * B[k, t] for k in range(7))
+            assert abs(C[j, t] - ex) <= 7 * 2 ** -53 * sum(abs(A[k, j] * B[k, t]) for k in range(7))
+
+
 def _loss(Xt, Gt, sh, sel=None, mig=None):
     return float(np.sum(O.layer_step(Xt, Gt, sh, sel, mig)["Y"] * Gt))
 
@@ -167,7 +214,7 @@ def _random_sel(e, h, f, seed, gamma=0.5):
     return sel
 
 
-@pytest.mark.parametrize("mode", ["dense", "pruned", "migrated"])
+@pytest.mark.parametrize("mode", ["dense", "pruned", "migrated", "pruned+migrated"])
 def test_gradient_check_central_differences_S301(mode):
     """analytic gradients vs central differences (step 1e-5,
     rel 1e-5) on 32 coordinates.  The pruned layer is a function of its
@@ -175,8 +222,21 @@ def test_gradient_check_central_differences_S301(mode):
     imputation produces.  Migration is lossless."""
     e, h, f, N = 2, 8, 32, 6
     Xt, Gt, W, sh = _make(e, h, f, N, seed=11)
-    sel = _random_sel(e, h, f, 5) if mode == "pruned" else None
-    mig = [(1, 0, 12, 16)] if mode == "migrated" else None
+    mig = [(1, 0, 12, 16)] if "migrated" in mode else None
+    if mode == "pruned":
+        sel = _random_sel(e, h, f, 5)
+    elif mode == "pruned+migrated":
+        # SEMI split on the straggler (rank 1): units [12, 16) migrate to the
+        # NORMAL helper (rank 0, unpruned, A-44) and the straggler resizes
+        # its four linears, FC2 over its remaining 12 units
+        sel = [{seg: (list(range(K)), []) for seg, K in (("qkv", h), ("o", h // e), ("fc1", h), ("fc2", f // e))}]
+        rng = np.random.default_rng(6)
+        d = {}
+        for seg, K in (("qkv", h), ("o", h // e), ("fc1", h), ("fc2", 12)):
+            d[seg] = O.select(rng.random(K).astype(np.float32), K // 2)
+        sel.append(d)
+    else:
+        sel = None
     out = O.layer_step(Xt, Gt, sh, sel, mig)
     rng = random.Random(3)
     step = 1e-5

@@ -345,3 +345,25 @@ def test_pwl_eval_interpolation_S552():
     assert O.pwl_eval(fn, 6.0) == 9.0          # extrapolation of the last segment
     with pytest.raises(O.OracleError):
         O.pwl_eval(((0.0,), (0.0,)), 1.0)
+
+
+def test_receivers_are_normal_tasks_A44():
+    """A-44 (P:235 "evenly distributed across other normal tasks", P:233
+    loss-free migration): in a multi-straggler plan (Eq.3 x migrators, z - x
+    resizers) the migrated units go to NORMAL tasks only, which prune
+    nothing; resize-group stragglers receive nothing."""
+    e = 8
+    T = [1.0, 8.0, 1.0, 6.0, 1.0, 4.0, 1.0, 2.0]     # c5 phase 3 (P:457): ranks 1,3,5,7 x8,6,4,2
+    M = [0.8 * t for t in T]
+    costs = O.Costs(phi1=((0.0, 1.0), (0.0, 1e-4)))
+    p = O.plan(T, M, 100.0, costs, O.PlanOpts(enable_migration=1, zero_crit=O.CRIT_MIN))
+    assert p.x >= 1 and p.z == 4
+    resizers = [r for r in range(e) if p.role[r] == O.RESIZE]
+    normals = [r for r in range(e) if p.role[r] == O.NORMAL]
+    assert normals == [0, 2, 4, 6]
+    got = {r: O.plan_counts(p, r, 100, 100, 1, True) for r in range(e)}
+    received = {r: sum(hi - lo for (_, lo, hi) in got[r].inc) for r in range(e)}
+    sent = sum(got[r].n_mig for r in range(e))
+    assert sum(received.values()) == sent > 0
+    assert all(received[r] == 0 for r in resizers) and all(received[r] > 0 for r in normals)
+    assert all(got[r].n_prune == 0 for r in normals)

@@ -1,5 +1,6 @@
 """Pins of the oracle priority select (Alg.1 l.12-14, A-1/A-2)."""
 import itertools
+import math
 import random
 
 import numpy as np
@@ -110,3 +111,41 @@ def test_pridiff_gamma_rules():
     assert O.pridiff_gamma(np.zeros(8), theta, 0.5) == 1.0
     with pytest.raises(O.OracleError):
         O.pridiff_gamma(np.zeros(0), theta, 0.5)
+
+
+def anti_endless_loop_run(incremental: bool, epochs: int = 10, K: int = 64, n: int = 32, gamma: float = 0.25,
+                          seed: int = 410):
+    """Seeded scenario of S:410 / P:190: each epoch "trains" the weight W^T
+    [K, n] by an update of per-row scale drawn fresh every epoch (the rows'
+    real variation), except that rows pruned this epoch receive none (their
+    Zero-imputed gradient rows, leave them unchanged under SGD).  At
+    the epoch end delta is updated (incrementally, or naively: every
+    row recomputed) and the next pruned set is selected (Alg.1 l.12-14).
+    Returns the pruned sets of every epoch."""
+    rng = np.random.default_rng(seed)
+    W = rng.standard_normal((K, n))
+    npr = int(math.floor(K * gamma + 0.5))
+    delta = rng.random(K).astype(np.float32)          # epoch-0 scores
+    _, P = O.select(delta, npr)
+    sets = [tuple(P)]
+    for _ in range(epochs - 1):
+        W_old = W.copy()
+        scale = rng.lognormal(-3.0, 1.0, size=K)
+        upd = rng.standard_normal((K, n)) * scale[:, None]
+        upd[np.asarray(P)] = 0.0
+        W = W + upd
+        delta = O.priority_update(delta, W, W_old, P if incremental else None).astype(np.float32)
+        _, P = O.select(delta, npr)
+        sets.append(tuple(P))
+    return sets
+
+
+def test_anti_endless_loop_S410():
+    """S:410 invariant: with the incremental rule the pruned set rotates (>= 3
+    distinct sets in 10 epochs); the naive full update freezes on a fixed set
+    by epoch 3 (pruned rows show zero variation and are pruned again)."""
+    inc = anti_endless_loop_run(True)
+    naive = anti_endless_loop_run(False)
+    assert len(set(inc)) >= 3
+    assert all(sset == naive[2] for sset in naive[2:])
+    assert naive[1] == naive[2]
