@@ -15,7 +15,7 @@ from synth.configs import CONFIGS  # noqa: E402
 from synth import inputs as I  # noqa: E402
 import bench  # noqa: E402
 
-cfg = CONFIGS["c2"]
+cfg = CONFIGS[os.environ.get("CFG", "c2")]
 h, f, N = cfg.h, cfg.f, cfg.N
 ctx = Z.ztp_ctx_create(0, 1, None, 0)
 sh = bench.rank_shards(cfg, 1, 0)
@@ -32,10 +32,10 @@ n_prune = {s: Z.ztp_plan_counts(p, 0, K, f, 1, s in ("o", "fc2")).n_prune
            for s, K in (("qkv", h), ("o", h), ("fc1", h), ("fc2", f))}
 L.set_selection(n_prune, sc)
 for _ in range(3):
-    L.step(stream)
+    L.step(stream, select=False)
 torch.cuda.synchronize()
 Z.ztp_set_profile(ctx, 2)
-g = L.capture(stream)
+g = L.capture(stream, select=False)   # selection once per plan
 for _ in range(300):
     g.replay()
 Z.ztp_read_profile(ctx, stream)

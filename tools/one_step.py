@@ -32,4 +32,4 @@ L.set_selection(n_prune, sc)
 for _ in range(2 + int(os.environ.get("STEPS", "1"))):
     L.step()
 torch.cuda.synchronize()
-print("flops", L.executed_flops())
+print("flops", L.method_flops(), L.executed_flops())
