@@ -49,6 +49,11 @@ struct ztp_ctx {
   // not start on the SMs its predecessor frees (ZTP_SQUAT_GUARD=0: PDL anyway;
   // the same guard on the side stream's split-K reduces measured no better)
   int squat_guard = 1;
+  // ZTP_GROUP: a linear's dX and dW as one grouped persistent launch on every
+  // SM (ztp::gemm_group_launch) instead of two concurrent kernels (TP = 1 /
+  // row layers; a col layer at TP > 1 keeps the concurrent pair so the dX
+  // all-reduce overlaps its dW)
+  int group_bwd = 0;
   int sm_cap = 0;                      // > 0: SMs a GEMM launch may use (concurrent dX / dW partition)
   bool side_pending = false;           // side-stream work not yet joined into a caller stream
   void* skws_side = nullptr;           // split-K partials of side-stream GEMMs
@@ -225,6 +230,138 @@ struct Src {
   bool compact;
 };
 
+// Kernel parameters of one bf16 resized GEMM (operands, lineage, epilogue,
+// split-K workspace).  force_splits > 0 overrides the split-K choice.
+ztp_status gemm_build_bf16(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t* kept,
+                           const int32_t* pruned, int nk, const ztp_mat& out, const ztp_mat* out2, const ztp_mat* aux,
+                           int aux_by_m, const int32_t* out_pos, int epi, cudaStream_t st, bool out_compact,
+                           const int32_t* col_pos, int n_full, bool indep_of_prev, int M, int N, int kdim,
+                           int force_splits, ztp::GemmOperands* po, ztp::GemmParams* pp) {
+  const ztp_mat& a = *A.m;
+  const ztp_mat& b = *B.m;
+  ztp::GemmOperands o{};
+  o.a = a.ptr;
+  o.a_ld = a.ld;
+  o.a_gather = !A.compact;
+  o.a_rows = A.compact ? nk : a.rows;
+  o.a_cols = kind == ztp::KIND_DW ? a.cols : n_out;
+  o.b = b.ptr;
+  o.b_ld = b.ld;
+  if (kind == ztp::KIND_FWD) {
+    o.b_gather = !B.compact;
+    o.b_rows = B.compact ? nk : b.rows;
+    o.b_cols = b.cols;
+  } else {
+    o.b_gather = false;
+    o.b_rows = n_out;
+    o.b_cols = b.cols;
+  }
+  ztp::GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.kdim = kdim;
+  p.n_kept = nk;
+  p.kept = kept;
+  p.pruned = pruned;
+  p.epi = epi;
+  p.out = (__nv_bfloat16*)out.ptr;
+  p.ld_out = out.ld;
+  p.out_rows = (int)out.rows;
+  if (out2 && out2->rows != out.rows)
+    return fail(c, ZTP_ESHAPE, "gemm: " + shp("out2", *out2) + " must have the rows of " + shp("out", out));
+  p.out2 = out2 ? (__nv_bfloat16*)out2->ptr : nullptr;
+  p.ld_out2 = out2 ? out2->ld : 0;
+  p.aux = aux ? (const __nv_bfloat16*)aux->ptr : nullptr;
+  p.ld_aux = aux ? aux->ld : 0;
+  p.aux_by_m = aux_by_m;
+  p.out_pos = out_pos;
+  // identity row map: compact outputs, or a dense lineage (S = 0..K-1)
+  p.out_dense = out_compact || (kind == ztp::KIND_FWD ? out_pos == nullptr
+                                                      : (kept == c->d_iota && pruned == nullptr && M <= nk));
+  p.stamp = emulating(c) ? stamp_slot(c, st) : nullptr;
+  p.dbg = c->dbg_epi;
+  p.col_pos = col_pos;
+  p.n_full = n_full;
+  // early start (PDL wait at exit) only when nothing between the launches
+  // depends on stamps (emulation) and the workspaces are disjoint (dW uses
+  // its own split-K workspace)
+  p.pdl_late = indep_of_prev && !emulating(c) && ztp::pdl_enabled();
+  // split-K over the contraction when the output has too few tiles for 148 SMs
+  const int nsm = c->sm_cap > 0 ? c->sm_cap : c->num_sms;
+  p.splits = force_splits > 0 ? force_splits
+                              : (c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, nsm) : 1);
+  if (p.splits > 1) {
+    const int num_kb = (kdim + 63) / 64;
+    // dW: the K-slices of a tile as one cluster reduced through DSMEM
+    const int cs = force_splits > 0 ? 0 : ztp::gemm_cluster_splits(kind, epi, M, N, nk, p.splits, nsm);
+    if (cs >= 2) p.splits = cs;
+    p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
+    p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
+    p.cs = (cs >= 2 && p.splits == cs) ? cs : 0;
+  }
+  if (p.splits > 1 && p.cs > 1) {
+    p.ws = nullptr;      // no workspace: partials never leave the cluster
+  } else if (p.splits > 1) {
+    const int num_kb = (kdim + 63) / 64;
+    p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
+    p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
+    const size_t bytes = ztp::gemm_ws_bytes(kind, M, N, nk, p.splits);
+    const bool side = st == c->side_stream || kind == ztp::KIND_DW;   // dW: its own workspace
+    void*& wsp = side ? c->skws_side : c->skws;
+    size_t& wcap = side ? c->skws_side_cap : c->skws_cap;
+    if (wcap < bytes) {
+      if (wsp) cudaFree(wsp);
+      wsp = nullptr;
+      wcap = 0;
+      CUDA_TRY(c, cudaMalloc(&wsp, bytes));
+      wcap = bytes;
+    }
+    p.ws = (float*)wsp;
+    p.ld_ws = (N + 7) / 8 * 8;
+    p.ws_split_stride = (int64_t)(kind == ztp::KIND_FWD ? M : std::min(M, nk)) * p.ld_ws;
+  } else {
+    p.splits = 1;
+    p.kb_per_split = (kdim + 63) / 64;
+  }
+  *po = o;
+  *pp = p;
+  return ZTP_OK;
+}
+
+// Output rows M, columns N and contraction length of a GEMM of `kind`.
+void gemm_dims(int kind, const ztp_mat& a, const ztp_mat& b, const ztp_mat& out, int64_t n_out, int nk, int* M,
+               int* N, int* kdim) {
+  if (kind == ztp::KIND_FWD) {
+    *M = (int)n_out;
+    *N = (int)b.cols;
+    *kdim = nk;
+  } else if (kind == ztp::KIND_DX) {
+    *M = (int)out.rows;
+    *N = (int)b.cols;
+    *kdim = (int)n_out;
+  } else {
+    *M = (int)out.rows;
+    *N = (int)n_out;
+    *kdim = (int)a.cols;
+  }
+}
+
+ztp_status gemm_check(ztp_ctx* c, int kind, Src A, Src B, int nk, const ztp_mat& out, const ztp_mat* out2,
+                      const ztp_mat* aux) {
+  const int dtype = A.m->dtype;
+  const ztp_mat* need[3] = {A.m, B.m, &out};
+  for (const ztp_mat* m : need)
+    if (!mat_ok(*m) || m->dtype != dtype)
+      return fail(c, ZTP_ESHAPE, "gemm: operand " + shp("m", *m) +
+                                     " must be non-empty, 16-byte aligned with ld a multiple of 16 bytes, dtype "
+                                     "matching");
+  if (out2 && (!mat_ok(*out2) || out2->dtype != dtype)) return fail(c, ZTP_ESHAPE, "gemm: bad " + shp("out2", *out2));
+  if (aux && (!mat_ok(*aux) || aux->dtype != dtype)) return fail(c, ZTP_ESHAPE, "gemm: bad " + shp("aux", *aux));
+  if ((A.compact && A.m->rows < nk) || (kind == ztp::KIND_FWD && B.compact && B.m->rows < nk))
+    return fail(c, ZTP_ESHAPE, "gemm: compact operand has fewer rows than n_kept");
+  return ZTP_OK;
+}
+
 // One resized GEMM + (optional) emulated slowdown.
 //   FWD: A = W^T source, B = X^T source     DX: A = W^T source, B = G^T
 //   DW : A = X^T source, B = G^T
@@ -234,124 +371,27 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
                 const int32_t* col_pos = nullptr, int n_full = 0, bool indep_of_prev = false) {
   const int dtype = A.m->dtype;
   {
-    const ztp_mat* need[3] = {A.m, B.m, &out};
-    for (const ztp_mat* m : need)
-      if (!mat_ok(*m) || m->dtype != dtype)
-        return fail(c, ZTP_ESHAPE, "gemm: operand " + shp("m", *m) +
-                                       " must be non-empty, 16-byte aligned with ld a multiple of 16 bytes, dtype "
-                                       "matching");
-    if (out2 && (!mat_ok(*out2) || out2->dtype != dtype)) return fail(c, ZTP_ESHAPE, "gemm: bad " + shp("out2", *out2));
-    if (aux && (!mat_ok(*aux) || aux->dtype != dtype)) return fail(c, ZTP_ESHAPE, "gemm: bad " + shp("aux", *aux));
-    if ((A.compact && A.m->rows < nk) || (kind == ztp::KIND_FWD && B.compact && B.m->rows < nk))
-      return fail(c, ZTP_ESHAPE, "gemm: compact operand has fewer rows than n_kept");
+    const ztp_status cs = gemm_check(c, kind, A, B, nk, out, out2, aux);
+    if (cs != ZTP_OK) return cs;
   }
   const ztp_mat& a = *A.m;
   const ztp_mat& b = *B.m;
   int M, N, kdim;
-  if (kind == ztp::KIND_FWD) {
-    M = (int)n_out;
-    N = (int)b.cols;
-    kdim = nk;
-  } else if (kind == ztp::KIND_DX) {
-    M = (int)out.rows;
-    N = (int)b.cols;
-    kdim = (int)n_out;
-  } else {
-    M = (int)out.rows;
-    N = (int)n_out;
-    kdim = (int)a.cols;
-  }
+  gemm_dims(kind, a, b, out, n_out, nk, &M, &N, &kdim);
   const double tokens = (double)(kind == ztp::KIND_DW ? a.cols : b.cols);
   const int pe = prof_begin(c, st, PROF_GEMM, 2.0 * (double)nk * (double)n_out * tokens);
   if (dtype == ZTP_BF16) {
     ztp::GemmOperands o{};
-    o.a = a.ptr;
-    o.a_ld = a.ld;
-    o.a_gather = !A.compact;
-    o.a_rows = A.compact ? nk : a.rows;
-    o.a_cols = kind == ztp::KIND_DW ? a.cols : n_out;
-    o.b = b.ptr;
-    o.b_ld = b.ld;
-    if (kind == ztp::KIND_FWD) {
-      o.b_gather = !B.compact;
-      o.b_rows = B.compact ? nk : b.rows;
-      o.b_cols = b.cols;
-    } else {
-      o.b_gather = false;
-      o.b_rows = n_out;
-      o.b_cols = b.cols;
-    }
     ztp::GemmParams p{};
-    p.M = M;
-    p.N = N;
-    p.kdim = kdim;
-    p.n_kept = nk;
-    p.kept = kept;
-    p.pruned = pruned;
-    p.epi = epi;
-    p.out = (__nv_bfloat16*)out.ptr;
-    p.ld_out = out.ld;
-    p.out_rows = (int)out.rows;
-    if (out2 && out2->rows != out.rows)
-      return fail(c, ZTP_ESHAPE, "gemm: " + shp("out2", *out2) + " must have the rows of " + shp("out", out));
-    p.out2 = out2 ? (__nv_bfloat16*)out2->ptr : nullptr;
-    p.ld_out2 = out2 ? out2->ld : 0;
-    p.aux = aux ? (const __nv_bfloat16*)aux->ptr : nullptr;
-    p.ld_aux = aux ? aux->ld : 0;
-    p.aux_by_m = aux_by_m;
-    p.out_pos = out_pos;
-    // identity row map: compact outputs, or a dense lineage (S = 0..K-1)
-    p.out_dense = out_compact || (kind == ztp::KIND_FWD ? out_pos == nullptr
-                                                        : (kept == c->d_iota && pruned == nullptr && M <= nk));
-    p.stamp = emulating(c) ? stamp_slot(c, st) : nullptr;
-    p.dbg = c->dbg_epi;
-    p.col_pos = col_pos;
-    p.n_full = n_full;
-    // early start (PDL wait at exit) only when nothing between the launches
-    // depends on stamps (emulation) and the workspaces are disjoint (dW uses
-    // its own split-K workspace)
-    p.pdl_late = indep_of_prev && !emulating(c) && ztp::pdl_enabled();
+    ztp_status bs = gemm_build_bf16(c, kind, A, B, n_out, kept, pruned, nk, out, out2, aux, aux_by_m, out_pos, epi, st,
+                                    out_compact, col_pos, n_full, indep_of_prev, M, N, kdim, 0, &o, &p);
+    if (bs != ZTP_OK) return bs;
     if (c->prof_on && c->d_pstamp && c->pstamp_used < ztp_ctx::PSTAMP_CAP) {
       c->pstamp_flops.resize((size_t)c->pstamp_used + 1);
       c->pstamp_flops[c->pstamp_used] = 2.0 * (double)nk * (double)n_out * tokens;
       p.prof_stamp = c->d_pstamp + 2 * (c->pstamp_used++);
     }
-    // split-K over the contraction when the output has too few tiles for 148 SMs
     const int nsm = c->sm_cap > 0 ? c->sm_cap : c->num_sms;
-    p.splits = c->allow_splitk ? ztp::gemm_choose_splits(kind, M, N, kdim, nk, nsm) : 1;
-    if (p.splits > 1) {
-      const int num_kb = (kdim + 63) / 64;
-      // dW: the K-slices of a tile as one cluster reduced through DSMEM
-      const int cs = ztp::gemm_cluster_splits(kind, epi, M, N, nk, p.splits, nsm);
-      if (cs >= 2) p.splits = cs;
-      p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
-      p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
-      p.cs = (cs >= 2 && p.splits == cs) ? cs : 0;
-    }
-    if (p.splits > 1 && p.cs > 1) {
-      p.ws = nullptr;      // no workspace: partials never leave the cluster
-    } else if (p.splits > 1) {
-      const int num_kb = (kdim + 63) / 64;
-      p.kb_per_split = (num_kb + p.splits - 1) / p.splits;
-      p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
-      const size_t bytes = ztp::gemm_ws_bytes(kind, M, N, nk, p.splits);
-      const bool side = st == c->side_stream || kind == ztp::KIND_DW;   // dW: its own workspace
-      void*& wsp = side ? c->skws_side : c->skws;
-      size_t& wcap = side ? c->skws_side_cap : c->skws_cap;
-      if (wcap < bytes) {
-        if (wsp) cudaFree(wsp);
-        wsp = nullptr;
-        wcap = 0;
-        CUDA_TRY(c, cudaMalloc(&wsp, bytes));
-        wcap = bytes;
-      }
-      p.ws = (float*)wsp;
-      p.ld_ws = (N + 7) / 8 * 8;
-      p.ws_split_stride = (int64_t)(kind == ztp::KIND_FWD ? M : std::min(M, nk)) * p.ld_ws;
-    } else {
-      p.splits = 1;
-      p.kb_per_split = (kdim + 63) / 64;
-    }
     if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, nsm, st));
     if ((p.splits > 1 && p.cs <= 1) || p.col_pos) ++c->launches;   // split-K reduce or column expansion
   } else {
@@ -397,6 +437,68 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     CUDA_TRY(c, ztp::gemm_f32_launch(p, st));
   }
   ++c->launches;
+  const ztp_status s = after_gemm(c, st);
+  prof_end(c, pe, st);
+  return s;
+}
+
+// A linear's dX and dW GEMMs as ONE grouped persistent launch (bf16): the
+// two problems' work units share every CTA pair (ztp::gemm_group_launch).
+// Returns ZTP_EUNSUPPORTED (nothing enqueued) when the pair does not qualify.
+struct GemmSpec {
+  int kind;
+  Src A, B;
+  int64_t n_out;
+  const int32_t *kept, *pruned;
+  int nk;
+  ztp_mat out;
+  const ztp_mat* aux;
+  int aux_by_m, epi;
+  bool out_compact;
+  const int32_t* col_pos;
+  int n_full;
+};
+ztp_status gemm_group(ztp_ctx* c, const GemmSpec& x, const GemmSpec& w, cudaStream_t st) {
+  for (const GemmSpec* g : {&x, &w}) {
+    const ztp_status cs = gemm_check(c, g->kind, g->A, g->B, g->nk, g->out, nullptr, g->aux);
+    if (cs != ZTP_OK) return cs;
+    if (!g->A.compact || g->A.m->dtype != ZTP_BF16) return ZTP_EUNSUPPORTED;
+  }
+  int M0, N0, k0, M1, N1, k1;
+  gemm_dims(x.kind, *x.A.m, *x.B.m, x.out, x.n_out, x.nk, &M0, &N0, &k0);
+  gemm_dims(w.kind, *w.A.m, *w.B.m, w.out, w.n_out, w.nk, &M1, &N1, &k1);
+  if (ztp::gemm_choose_cg(x.kind, M0, x.nk) != ztp::gemm_choose_cg(w.kind, M1, w.nk)) return ZTP_EUNSUPPORTED;
+  const int sw = ztp::gemm_group_splits(M0, N0, k0, x.nk, M1, N1, k1, w.nk, c->num_sms);
+  ztp::GemmOperands o0{}, o1{};
+  ztp::GemmParams p0{}, p1{};
+  ztp_status bs = gemm_build_bf16(c, x.kind, x.A, x.B, x.n_out, x.kept, x.pruned, x.nk, x.out, nullptr, x.aux,
+                                  x.aux_by_m, nullptr, x.epi, st, x.out_compact, nullptr, 0, false, M0, N0, k0, 1, &o0,
+                                  &p0);
+  if (bs == ZTP_OK)
+    bs = gemm_build_bf16(c, w.kind, w.A, w.B, w.n_out, w.kept, w.pruned, w.nk, w.out, nullptr, nullptr, 0, nullptr,
+                         w.epi, st, false, w.col_pos, w.n_full, false, M1, N1, k1, sw, &o1, &p1);
+  if (bs != ZTP_OK) return bs;
+  const double tok0 = (double)x.B.m->cols, tok1 = (double)w.A.m->cols;
+  const double fl = 2.0 * x.nk * (double)x.n_out * tok0 + 2.0 * w.nk * (double)w.n_out * tok1;
+  const int pe = prof_begin(c, st, PROF_GEMM, fl);
+  if (c->prof_on && c->d_pstamp && c->pstamp_used < ztp_ctx::PSTAMP_CAP) {
+    c->pstamp_flops.resize((size_t)c->pstamp_used + 1);
+    c->pstamp_flops[c->pstamp_used] = fl;
+    p0.prof_stamp = p1.prof_stamp = c->d_pstamp + 2 * (c->pstamp_used++);
+  }
+  if (!(c->dbg_skip & 16)) {
+    const cudaError_t e = ztp::gemm_group_launch(x.kind, o0, p0, w.kind, o1, p1, c->num_sms, st);
+    if (e == cudaErrorInvalidConfiguration) {   // too many units per pair: nothing enqueued, use the pair
+      if (p0.prof_stamp) --c->pstamp_used;
+      prof_end(c, pe, st);
+      return ZTP_EUNSUPPORTED;
+    }
+    if (e == cudaErrorStreamCaptureUnsupported)
+      return fail(c, ZTP_EUNSUPPORTED, "grouped dX/dW: unit schedule of this shape not built before capture "
+                                       "(run the step once eagerly first)");
+    CUDA_TRY(c, e);
+  }
+  c->launches += 1 + ((p1.splits > 1 || p1.col_pos) ? 1 : 0) + ((p0.splits > 1 || p0.col_pos) ? 1 : 0);
   const ztp_status s = after_gemm(c, st);
   prof_end(c, pe, st);
   return s;
@@ -733,6 +835,52 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
     return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("g_t", g));
   const int64_t N = g.cols;
   if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
+  const bool reduce_dx0 = layer == LAYER_COL && a->dx_t.ptr && !a->skip_collective && c->world > 1;
+  if (c->group_bwd && a->dx_t.ptr && a->dw_t.ptr && dtype == ZTP_BF16 && !reduce_dx0 && !c->use_gather4 &&
+      !(a->act_in != ZTP_ACT_NONE && layer != LAYER_ROW)) {
+    // ---- grouped: dX and dW units in one persistent launch on every SM
+    const ztp_mat& x = a->x_t;
+    if (!mat_ok(a->dx_t) || (dxc ? a->dx_t.rows < nk : a->dx_t.rows != K) || a->dx_t.cols != N ||
+        a->dx_t.dtype != dtype)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dx_t", a->dx_t) + " vs K " + std::to_string(K));
+    if (dxc && a->act_in != ZTP_ACT_NONE && !xc)
+      return fail(c, ZTP_EINVAL, std::string(nm) + " BWD: dx_compact with GeLU' needs x_compact pre_in_t");
+    if (!mat_ok(x) || x.rows < x_rows_need || x.cols != N || x.dtype != dtype || (!xc && x.rows != K))
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("x_t", x) + " vs " + shp("g_t", g));
+    if (!mat_ok(a->dw_t) || a->dw_t.rows != K || a->dw_t.cols < n_out || a->dw_t.dtype != dtype)
+      return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD: " + shp("dw_t", a->dw_t));
+    int epi = ztp::EPI_NONE;
+    const ztp_mat* aux = nullptr;
+    if (layer == LAYER_ROW && (a->act_in == ZTP_ACT_GELU || a->act_in == ZTP_ACT_GELU_D)) {
+      if (!mat_ok(a->pre_in_t) || a->pre_in_t.rows < x_rows_need || a->pre_in_t.cols != N)
+        return fail(c, ZTP_ESHAPE, std::string(nm) + " BWD GeLU': " + shp("pre_in_t", a->pre_in_t));
+      epi = a->act_in == ZTP_ACT_GELU_D ? ztp::EPI_MUL : ztp::EPI_GELU_GRAD;
+      aux = &a->pre_in_t;
+    }
+    if (os)
+      s = weight_2d(c, a->w_t, dense_sel ? nullptr : kept, nk, os->kept, (int)n_y, a->ws_t, false, &tmpw, &W, st);
+    else
+      s = operand_src(c, dense_sel, false, a->w_t, a->ws_t, false, kept, nk, 1, &tmpw, &W, st);
+    if (s != ZTP_OK) return s;
+    s = operand_src(c, dense_sel, xc, x, a->xs_t, false, kept, nk, 0, &tmpx, &X, st);
+    if (s != ZTP_OK) return s;
+    ztp_mat dx = a->dx_t;
+    if (dxc) dx.rows = nk;   // rows P implied Zero, not written
+    const GemmSpec sx{ztp::KIND_DX, W, Src{&g, true}, n_y, kept, dxc ? nullptr : pruned, nk, dx, aux, xc ? 1 : 0,
+                      epi, dxc, nullptr, 0};
+    const GemmSpec sw{ztp::KIND_DW, X, Src{&g, true}, n_y, kept, pruned, nk, a->dw_t, nullptr, 0, ztp::EPI_NONE,
+                      false, os ? a->y_pos : nullptr, (int)n_out};
+    s = gemm_group(c, sx, sw, st);
+    if (s != ZTP_EUNSUPPORTED) {
+      if (s != ZTP_OK) return s;
+      if (!dense_sel) s = impute(c, a->impute, a->dx_t, N, kept, nk, pruned, np, a->hist_dx, st);
+      if (s == ZTP_OK && !dense_sel) s = impute(c, a->impute, a->dw_t, n_out, kept, nk, pruned, np, a->hist_dw, st);
+      if (s != ZTP_OK) return s;
+      if (layer == LAYER_COL && !a->skip_collective && c->world > 1) return allreduce(c, a->dx_t, st);
+      return ZTP_OK;
+    }
+    // not groupable (shapes): fall through to the concurrent pair
+  }
   // dW concurrently with dX on the side stream (also on an emulated
   // straggler: each GEMM is stretched from its own stamp slot; not while
   // profiling with events, which times each GEMM alone)
@@ -895,6 +1043,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* cc = getenv("ZTP_CONC")) c->conc_bwd = atoi(cc) != 0;
   if (const char* ds = getenv("ZTP_DW_SHARE")) c->dw_share = atof(ds);
   if (const char* sg = getenv("ZTP_SQUAT_GUARD")) c->squat_guard = atoi(sg) != 0;
+  if (const char* gb = getenv("ZTP_GROUP")) c->group_bwd = atoi(gb) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
   auto cleanup = [&](ztp_status s) {

@@ -28,7 +28,10 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstdint>
+#include <vector>
 
 #include "ztp_internal.h"
 #include "ztp_ptx.cuh"
@@ -160,39 +163,355 @@ struct Sched {
   }
 };
 
+// Pipeline state a CTA's roles carry from one work unit to the next.
+struct Pipe {
+  int stage = 0;       // smem ring slot (producer / MMA)
+  uint32_t phase = 0;
+  int acc = 0;         // TMEM accumulator buffer (MMA / epilogue)
+  uint32_t aphase = 0;
+  int sk = 0;          // epilogue staging buffers used so far (ping-pong)
+};
+
+// ---- TMA producer of one work unit (warp 0).
 // AG / BG: operand A / B gathered row-by-row with TMA gather4 through the
 // lineage list (true) or loaded as dense TMA boxes from a compact, already
 // row-selected tensor (false; rows past the compact extent are zero-filled).
 template <int KIND, int CG, bool AG, bool BG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    ztp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
-                    const __grid_constant__ CUtensorMap tmW, const GemmParams p) {
+__device__ __forceinline__ void produce_unit(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmParams& p,
+                                             const Work& wk, int rank, bool leader, int lane, uint8_t* ring,
+                                             uint64_t* full, uint64_t* empty, Pipe& ps) {
   using C = Cfg<CG>;
-  constexpr int STAGES = C::STAGES;
   constexpr int BNL = C::BNL;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* ring = smem;
-  uint8_t* staging = smem + C::RING;
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::STAGING);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int am0 = wk.m0 + BM * rank;   // this CTA's 128 rows of the tile (A)
+  const int bn0 = wk.n0 + BNL * rank;  // this CTA's columns of B
+  int ar0 = 0, ar1 = 0, ar2 = 0, ar3 = 0;
+  if (KIND != KIND_FWD && AG) {
+    const int mb = am0 + 4 * lane;
+    ar0 = (mb + 0 < p.n_kept) ? __ldg(p.kept + mb + 0) : p.oob_row;
+    ar1 = (mb + 1 < p.n_kept) ? __ldg(p.kept + mb + 1) : p.oob_row;
+    ar2 = (mb + 2 < p.n_kept) ? __ldg(p.kept + mb + 2) : p.oob_row;
+    ar3 = (mb + 3 < p.n_kept) ? __ldg(p.kept + mb + 3) : p.oob_row;
+  }
+  for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
+    mbar_wait(&empty[ps.stage], ps.phase ^ 1);
+    uint8_t* sa = ring + ps.stage * C::STAGE_BYTES;
+    uint8_t* sb = sa + A_BYTES;
+    uint64_t* fb = &full[ps.stage];
+    if (leader && lane == 0) mbar_expect_tx(fb, CG * C::STAGE_BYTES);
+    __syncwarp();
+    auto load = [&](const CUtensorMap* tm, void* dst, int c0, int c1) {
+      if (CG == 2)
+        tma_load_2d_cg2(tm, fb, dst, c0, c1);
+      else
+        tma_load_2d(tm, fb, dst, c0, c1);
+    };
+    auto gather = [&](const CUtensorMap* tm, void* dst, int col, int r0, int r1, int r2, int r3) {
+      if (CG == 2)
+        tma_gather4_cg2(tm, fb, dst, col, r0, r1, r2, r3);
+      else
+        tma_gather4(tm, fb, dst, col, r0, r1, r2, r3);
+    };
+    if (KIND == KIND_FWD) {
+      // both operands MN-major (contraction rows outer)
+      if (AG || BG) {
+        const int g = lane & 15, half = lane >> 4;
+        const int kbase = kb * BK + 4 * g;
+        int r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = kbase + i;
+          r[i] = (k < p.n_kept) ? __ldg(p.kept + k) : p.oob_row;
+        }
+        if (AG) gather(tmA, sa + half * 8192 + g * 512, am0 + 64 * half, r[0], r[1], r[2], r[3]);
+        if (BG) {
+          constexpr int NB = BNL / 64, PER = NB / 2;
+#pragma unroll
+          for (int b = half * PER; b < (half + 1) * PER; ++b)
+            gather(tmB, sb + b * 8192 + g * 512, bn0 + 64 * b, r[0], r[1], r[2], r[3]);
+        }
+      }
+      if (lane == 0) {
+        if (!AG) {
+          load(tmA, sa, am0, kb * BK);
+          load(tmA, sa + 8192, am0 + 64, kb * BK);
+        }
+        if (!BG) {
+#pragma unroll
+          for (int b = 0; b < BNL / 64; ++b) load(tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
+        }
+      }
+    } else {
+      // A: K-major rows (m) x 64 contraction columns
+      if (AG) gather(tmA, sa + lane * 512, kb * BK, ar0, ar1, ar2, ar3);
+      if (lane == 0) {
+        if (!AG) load(tmA, sa, kb * BK, am0);
+        if (KIND == KIND_DX) {
+          // B = G^T [n, N] MN-major dense: 64 contraction rows x BNL columns
+#pragma unroll
+          for (int b = 0; b < BNL / 64; ++b) load(tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
+        } else {
+          // B = G^T [n, N] K-major dense: BNL rows (output cols j) x 64 tokens
+          load(tmB, sb, kb * BK, bn0);
+        }
+      }
+    }
+    if (++ps.stage == C::STAGES) {
+      ps.stage = 0;
+      ps.phase ^= 1;
+    }
+  }
+}
 
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t crank = (CG == 2 || p.cs > 1) ? cluster_ctarank() : 0u;   // rank in the cluster
-  const int rank = CG == 2 ? (int)(crank & 1u) : 0;                         // CTA rank in the pair
-  const bool leader = rank == 0;
-  const uint16_t pmask = (uint16_t)(0x3u << (crank & ~1u));   // this pair's CTAs (commit multicast)
-  const int csplit = p.cs > 1 ? (int)crank / CG : 0;          // cluster split-K: this pair's K-slice
-  const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
+// ---- MMA issuer of one work unit (warp 1 of the even CTA; lane 0 issues).
+template <int KIND, int CG>
+__device__ __forceinline__ void mma_unit(const Work& wk, int lane, uint16_t pmask, uint8_t* ring, uint64_t* full,
+                                         uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
+                                         Pipe& ps) {
+  using C = Cfg<CG>;
+  constexpr uint32_t IDESC = make_idesc_bf16(C::TM, BN, KIND == KIND_FWD ? 1 : 0, KIND == KIND_DW ? 0 : 1);
+  mbar_wait(&tempty[ps.acc], ps.aphase ^ 1);
+  tc_fence_after();
+  const uint32_t d_tmem = tmem_base + ps.acc * BN;
+  for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
+    mbar_wait(&full[ps.stage], ps.phase);
+    tc_fence_after();
+    if (lane == 0) {
+      const uint32_t sa = smem_u32(ring + ps.stage * C::STAGE_BYTES);
+      const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk) {
+        uint64_t ad, bd;
+        if (KIND == KIND_FWD)
+          ad = make_sdesc_sw128(sa + kk * 2048, 8192, 1024);  // MN-major: LBO = 64-col block stride
+        else
+          ad = make_sdesc_sw128(sa + kk * 32, 16, 1024);      // K-major: SBO = 8-row group stride
+        if (KIND == KIND_DW)
+          bd = make_sdesc_sw128(sb + kk * 32, 16, 1024);
+        else
+          bd = make_sdesc_sw128(sb + kk * 2048, 8192, 1024);
+        const uint32_t accum = (kb > wk.kb0 || kk > 0) ? 1u : 0u;
+        if (CG == 2)
+          umma_bf16_cg2(d_tmem, ad, bd, IDESC, accum);
+        else
+          umma_bf16(d_tmem, ad, bd, IDESC, accum);
+      }
+      if (CG == 2)
+        umma_commit_mc(&empty[ps.stage], pmask);
+      else
+        umma_commit(&empty[ps.stage]);
+    }
+    __syncwarp();
+    if (++ps.stage == C::STAGES) {
+      ps.stage = 0;
+      ps.phase ^= 1;
+    }
+  }
+  if (lane == 0) {
+    if (CG == 2)
+      umma_commit_mc(&tfull[ps.acc], pmask);
+    else
+      umma_commit(&tfull[ps.acc]);
+  }
+  __syncwarp();
+  if (++ps.acc == 2) {
+    ps.acc = 0;
+    ps.aphase ^= 1;
+  }
+}
 
+// ---- Epilogue of one work unit (warps 4-11: TMEM lane quarter x column half).
+template <int KIND, int CG>
+__device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUtensorMap* tmO2, const CUtensorMap* tmW,
+                                              const GemmParams& p, int S, const Work& wk, int rank, int ew, int lane,
+                                              uint8_t* staging, uint64_t* tfull, uint64_t* tempty,
+                                              uint32_t tmem_base, Pipe& ps) {
+  const int lq = ew & 3;               // TMEM lane quarter == warp % 4 (rows lq*32 .. +31)
+  const int ch = ew >> 2;              // column half of the 256-column accumulator
+  uint8_t* const stg_base = staging + ew * 2 * STAGING_PER_WARP;
+  uint8_t* stg = stg_base;
+  auto release = [&]() {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (CG == 2)
+        mbar_arrive_leader(&tempty[ps.acc]);
+      else
+        mbar_arrive(&tempty[ps.acc]);
+    }
+    if (++ps.acc == 2) {
+      ps.acc = 0;
+      ps.aphase ^= 1;
+    }
+  };
+  const int m0 = wk.m0 + BM * rank, n0 = wk.n0;
+  const bool zt = wk.zero;
+  const uint32_t tbase = tmem_base + ((uint32_t)(lq * 32) << 16) + ps.acc * BN + ch * (BN / 2);
+  const int nc0 = n0 + ch * (BN / 2);   // first output column of this warp
+  // Two staging buffers per warp alternate: before refilling one, the
+  // lanes that issued TMA stores wait until at most the other buffer's
+  // store is still reading (bulk wait_group.read 1).
+  auto staging_free = [&]() {
+    if (lane < 8) bulk_wait_read1();
+    __syncwarp();
+    stg = stg_base + (ps.sk & 1) * STAGING_PER_WARP;
+    ++ps.sk;
+  };
+  if (S > 1) {
+    // ---- split-K partial: fp32 tile -> ws[split] via TMA box stores
+    //      (rows >= n_kept / cols >= N are outside the ws map: not written)
+    mbar_wait(&tfull[ps.acc], ps.aphase);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tbase + c * 32, v);
+      tmem_ld_wait();
+      if (c == BN / 64 - 1) release();   // accumulator fully in registers: TMEM free
+      staging_free();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        st_shared_v4(stg + lane * 128 + ((q ^ (lane & 7)) << 4),
+                     make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(tmW, stg, nc0 + c * 32, m0 + lq * 32, wk.split);
+        bulk_commit();
+      }
+    }
+    return;
+  }
+  // this lane owns tile row m = m0 + lq*32 + lane; its output row index
+  const int m = m0 + lq * 32 + lane;
+  int orow = p.oob_out;                       // rows outside the output are not written
+  int arow = 0;
+  if (m < p.M) {
+    int o;
+    if (p.out_dense)
+      o = m;                                      // compact output (row i <- unit i of the list)
+    else if (KIND == KIND_FWD)
+      o = p.out_pos ? __ldg(p.out_pos + m) : m;   // producer-side compaction for the next layer
+    else
+      o = (m < p.n_kept) ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
+    if (o >= 0) orow = o;
+    arow = p.aux_by_m ? m : o;
+  }
+  const bool dense_out = p.out_dense;
+  // rows of the 4-row scatter group this lane issues (lanes 0..7)
+  int sr[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sr[j] = __shfl_sync(0xFFFFFFFFu, orow, (4 * lane + j) & 31);
+  if (!zt) {
+    mbar_wait(&tfull[ps.acc], ps.aphase);
+    tc_fence_after();
+  }
+  if (p.dbg & 2) {
+    if (!zt) release();
+    return;
+  }
+  // one TMA store of a staged 32 x 64 bf16 plane (dense box or 4-row scatter)
+  auto store_plane = [&](const CUtensorMap* tm, uint8_t* buf, int col0) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (p.dbg & 1) return;
+    if (dense_out) {
+      if (lane == 0) {
+        tma_store_2d(tm, buf, col0, m0 + lq * 32);
+        bulk_commit();
+      }
+    } else if (lane < 8) {
+      tma_scatter4(tm, buf + lane * 512, col0, sr[0], sr[1], sr[2], sr[3]);
+      bulk_commit();
+    }
+  };
+  const bool two_planes = p.epi == EPI_GELU || p.epi == EPI_GELU_D;
+  const bool has_aux = (p.epi == EPI_GELU_GRAD || p.epi == EPI_MUL) && !zt;
+#pragma unroll 1
+  for (int c = 0; c < BN / 128; ++c) {
+    const int col0 = nc0 + c * 64;
+    uint32_t v[64];
+    // GeLU' operand (pre-activation, or GeLU'(pre) itself for EPI_MUL):
+    // this lane's row, loaded before the TMEM load so the two overlap
+    uint4 pin[8];
+    if (has_aux) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        pin[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (m < p.n_kept && col0 + 8 * i < p.N)
+          pin[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (int64_t)arow * p.ld_aux + col0 + 8 * i));
+      }
+    }
+    if (!zt) {
+      tmem_ld_32x32b_x32(tbase + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+      tmem_ld_32x32b_x32(tbase + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      tmem_ld_wait();
+      if (c == BN / 128 - 1) release();   // accumulator fully in registers: TMEM free for tile i+2
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = 0u;
+    }
+    if (two_planes) {
+      // out <- pre (EPI_GELU) or GeLU'(pre) (EPI_GELU_D); out2 <- GeLU(pre).
+      // Both staging buffers are filled in one pass (tanh shared).
+      if (lane < 8) bulk_wait_read0();
+      __syncwarp();
+      uint8_t* const b0 = stg_base;
+      uint8_t* const b1 = stg_base + STAGING_PER_WARP;
+      const bool want_d = p.epi == EPI_GELU_D;
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        uint32_t w0[4], w1[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 x = make_float2(__uint_as_float(v[qq * 8 + 2 * j]), __uint_as_float(v[qq * 8 + 2 * j + 1]));
+          float2 hv, dv;
+          gelu2(x, hv, dv, want_d);
+          w0[j] = want_d ? pack2(dv) : pack2(x);
+          w1[j] = pack2(hv);
+        }
+        const uint32_t off = lane * 128 + ((qq ^ (lane & 7)) << 4);
+        st_shared_v4(b0 + off, make_uint4(w0[0], w0[1], w0[2], w0[3]));
+        st_shared_v4(b1 + off, make_uint4(w1[0], w1[1], w1[2], w1[3]));
+      }
+      store_plane(tmO, b0, col0);
+      store_plane(tmO2, b1, col0);
+    } else {
+      staging_free();
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        uint32_t w[4];
+        const uint32_t a4[4] = {pin[qq].x, pin[qq].y, pin[qq].z, pin[qq].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 x = make_float2(__uint_as_float(v[qq * 8 + 2 * j]), __uint_as_float(v[qq * 8 + 2 * j + 1]));
+          if (has_aux) {
+            // G1 = dH * GeLU'(pre_in)  (EPI_MUL: aux already holds GeLU'(pre))
+            const float2 a = unpack2(a4[j]);
+            if (p.epi == EPI_GELU_GRAD) {
+              float2 hv, dv;
+              gelu2(a, hv, dv, true);
+              x = __fmul2_rn(x, dv);
+            } else {
+              x = __fmul2_rn(x, a);
+            }
+          }
+          w[j] = pack2(x);
+        }
+        st_shared_v4(stg + lane * 128 + ((qq ^ (lane & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
+      }
+      store_plane(tmO, stg, col0);
+    }
+  }
+}
 
+// Shared prologue of both kernels: barriers, TMEM allocation, then the PDL
+// handshake.  Returns the TMEM base address.
+template <int CG>
+__device__ __forceinline__ uint32_t kernel_prologue(uint64_t* full, uint64_t* empty, uint64_t* tfull, uint64_t* tempty,
+                                                    uint32_t* tmem_slot, int warp) {
+  using C = Cfg<CG>;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -201,10 +520,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tempty[s], EPI_WARPS * CG);
     }
     fence_barrier_init();
-  }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
   }
   if (warp == 2) {
     if (CG == 2)
@@ -218,7 +533,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else
     __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  return *tmem_slot;
+}
+
+template <int CG>
+__device__ __forceinline__ void kernel_teardown(uint32_t tmem_base, int warp) {
+  tc_fence_before();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    if (CG == 2)
+      tmem_dealloc_cg2(tmem_base, 512);
+    else
+      tmem_dealloc(tmem_base, 512);
+  }
+}
+
+template <int KIND, int CG, bool AG, bool BG>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    ztp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
+                    const __grid_constant__ CUtensorMap tmW, const GemmParams p) {
+  using C = Cfg<CG>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  uint8_t* staging = smem + C::RING;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::STAGING);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = (CG == 2 || p.cs > 1) ? cluster_ctarank() : 0u;   // rank in the cluster
+  const int rank = CG == 2 ? (int)(crank & 1u) : 0;                         // CTA rank in the pair
+  const bool leader = rank == 0;
+  const uint16_t pmask = (uint16_t)(0x3u << (crank & ~1u));   // this pair's CTAs (commit multicast)
+  const int csplit = p.cs > 1 ? (int)crank / CG : 0;          // cluster split-K: this pair's K-slice
+  const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  const uint32_t tmem_base = kernel_prologue<CG>(full, empty, tfull, tempty, tmem_slot, warp);
   // prologue done (barriers, TMEM, descriptor prefetch): wait for the
   // preceding kernel's results, let the next kernel begin its own prologue.
   // pdl_late (a dW GEMM right after the dX GEMM it does not depend on): run
@@ -237,341 +600,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     u_first = csplit * sc.tiles_c + (int)(blockIdx.x / (CG * p.cs));
     u_step = sc.num_units;
   }
-
+  Pipe ps;
   if (warp == 0) {
-    // ============================ TMA producer ============================
-    int stage = 0;
-    uint32_t phase = 0;
     for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
-      if (wk.zero) continue;
-      const int am0 = wk.m0 + BM * rank;   // this CTA's 128 rows of the tile (A)
-      const int bn0 = wk.n0 + BNL * rank;  // this CTA's columns of B
-      int ar0 = 0, ar1 = 0, ar2 = 0, ar3 = 0;
-      if (KIND != KIND_FWD && AG) {
-        const int mb = am0 + 4 * lane;
-        ar0 = (mb + 0 < p.n_kept) ? __ldg(p.kept + mb + 0) : p.oob_row;
-        ar1 = (mb + 1 < p.n_kept) ? __ldg(p.kept + mb + 1) : p.oob_row;
-        ar2 = (mb + 2 < p.n_kept) ? __ldg(p.kept + mb + 2) : p.oob_row;
-        ar3 = (mb + 3 < p.n_kept) ? __ldg(p.kept + mb + 3) : p.oob_row;
-      }
-      for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = ring + stage * C::STAGE_BYTES;
-        uint8_t* sb = sa + A_BYTES;
-        if (leader && lane == 0) mbar_expect_tx(&full[stage], CG * C::STAGE_BYTES);
-        __syncwarp();
-        auto load = [&](const CUtensorMap* tm, void* dst, int c0, int c1) {
-          if (CG == 2)
-            tma_load_2d_cg2(tm, &full[stage], dst, c0, c1);
-          else
-            tma_load_2d(tm, &full[stage], dst, c0, c1);
-        };
-        auto gather = [&](const CUtensorMap* tm, void* dst, int col, int r0, int r1, int r2, int r3) {
-          if (CG == 2)
-            tma_gather4_cg2(tm, &full[stage], dst, col, r0, r1, r2, r3);
-          else
-            tma_gather4(tm, &full[stage], dst, col, r0, r1, r2, r3);
-        };
-        if (KIND == KIND_FWD) {
-          // both operands MN-major (contraction rows outer)
-          if (AG || BG) {
-            const int g = lane & 15, half = lane >> 4;
-            const int kbase = kb * BK + 4 * g;
-            int r[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int k = kbase + i;
-              r[i] = (k < p.n_kept) ? __ldg(p.kept + k) : p.oob_row;
-            }
-            if (AG) gather(&tmA, sa + half * 8192 + g * 512, am0 + 64 * half, r[0], r[1], r[2], r[3]);
-            if (BG) {
-              constexpr int NB = BNL / 64, PER = NB / 2;
-#pragma unroll
-              for (int b = half * PER; b < (half + 1) * PER; ++b)
-                gather(&tmB, sb + b * 8192 + g * 512, bn0 + 64 * b, r[0], r[1], r[2], r[3]);
-            }
-          }
-          if (lane == 0) {
-            if (!AG) {
-              load(&tmA, sa, am0, kb * BK);
-              load(&tmA, sa + 8192, am0 + 64, kb * BK);
-            }
-            if (!BG) {
-#pragma unroll
-              for (int b = 0; b < BNL / 64; ++b) load(&tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
-            }
-          }
-        } else {
-          // A: K-major rows (m) x 64 contraction columns
-          if (AG) gather(&tmA, sa + lane * 512, kb * BK, ar0, ar1, ar2, ar3);
-          if (lane == 0) {
-            if (!AG) load(&tmA, sa, kb * BK, am0);
-            if (KIND == KIND_DX) {
-              // B = G^T [n, N] MN-major dense: 64 contraction rows x BNL columns
-#pragma unroll
-              for (int b = 0; b < BNL / 64; ++b) load(&tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
-            } else {
-              // B = G^T [n, N] K-major dense: BNL rows (output cols j) x 64 tokens
-              load(&tmB, sb, kb * BK, bn0);
-            }
-          }
-        }
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
+      if (!wk.zero) produce_unit<KIND, CG, AG, BG>(&tmA, &tmB, p, wk, rank, leader, lane, ring, full, empty, ps);
     }
   } else if (warp == 1 && leader) {
-    // ============================ MMA issuer ==============================
-    constexpr uint32_t IDESC = make_idesc_bf16(C::TM, BN, KIND == KIND_FWD ? 1 : 0, KIND == KIND_DW ? 0 : 1);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t aphase = 0;
     for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
-      if (wk.zero) continue;
-      mbar_wait(&tempty[acc], aphase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sa = smem_u32(ring + stage * C::STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            uint64_t ad, bd;
-            if (KIND == KIND_FWD)
-              ad = make_sdesc_sw128(sa + kk * 2048, 8192, 1024);  // MN-major: LBO = 64-col block stride
-            else
-              ad = make_sdesc_sw128(sa + kk * 32, 16, 1024);      // K-major: SBO = 8-row group stride
-            if (KIND == KIND_DW)
-              bd = make_sdesc_sw128(sb + kk * 32, 16, 1024);
-            else
-              bd = make_sdesc_sw128(sb + kk * 2048, 8192, 1024);
-            const uint32_t accum = (kb > wk.kb0 || kk > 0) ? 1u : 0u;
-            if (CG == 2)
-              umma_bf16_cg2(d_tmem, ad, bd, IDESC, accum);
-            else
-              umma_bf16(d_tmem, ad, bd, IDESC, accum);
-          }
-          if (CG == 2)
-            umma_commit_mc(&empty[stage], pmask);
-          else
-            umma_commit(&empty[stage]);
-        }
-        __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      if (lane == 0) {
-        if (CG == 2)
-          umma_commit_mc(&tfull[acc], pmask);
-        else
-          umma_commit(&tfull[acc]);
-      }
-      __syncwarp();
-      if (++acc == 2) {
-        acc = 0;
-        aphase ^= 1;
-      }
+      if (!wk.zero) mma_unit<KIND, CG>(wk, lane, pmask, ring, full, empty, tfull, tempty, tmem_base, ps);
     }
   } else if (warp >= 4 && p.cs > 1) {
     // cluster split-K: this pair's K-slice is accumulated; reduced below
     mbar_wait(&tfull[0], 0);
     tc_fence_after();
   } else if (warp >= 4) {
-    // ============================ epilogue ================================
-    const int ew = warp - 4;
-    const int lq = ew & 3;               // TMEM lane quarter == warp % 4 (rows lq*32 .. +31)
-    const int ch = ew >> 2;              // column half of the 256-column accumulator
-    uint8_t* const stg_base = staging + ew * 2 * STAGING_PER_WARP;
-    uint8_t* stg = stg_base;
-    int sk = 0;                          // staging buffers used so far (ping-pong)
-    int acc = 0;
-    uint32_t aphase = 0;
-    auto release = [&]() {
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CG == 2)
-          mbar_arrive_leader(&tempty[acc]);
-        else
-          mbar_arrive(&tempty[acc]);
-      }
-      if (++acc == 2) {
-        acc = 0;
-        aphase ^= 1;
-      }
-    };
-    for (int u = u_first; u < sc.num_units; u += u_step) {
-      const Work wk = sc.get(u);
-      const int m0 = wk.m0 + BM * rank, n0 = wk.n0;
-      const bool zt = wk.zero;
-      const uint32_t tbase = tmem_base + ((uint32_t)(lq * 32) << 16) + acc * BN + ch * (BN / 2);
-      const int nc0 = n0 + ch * (BN / 2);   // first output column of this warp
-      // Two staging buffers per warp alternate: before refilling one, the
-      // lanes that issued TMA stores wait until at most the other buffer's
-      // store is still reading (bulk wait_group.read 1).
-      auto staging_free = [&]() {
-        if (lane < 8) bulk_wait_read1();
-        __syncwarp();
-        stg = stg_base + (sk & 1) * STAGING_PER_WARP;
-        ++sk;
-      };
-      if (sc.S > 1) {
-        // ---- split-K partial: fp32 tile -> ws[split] via TMA box stores
-        //      (rows >= n_kept / cols >= N are outside the ws map: not written)
-        mbar_wait(&tfull[acc], aphase);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tbase + c * 32, v);
-          tmem_ld_wait();
-          if (c == BN / 64 - 1) release();   // accumulator fully in registers: TMEM free
-          staging_free();
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            st_shared_v4(stg + lane * 128 + ((q ^ (lane & 7)) << 4),
-                         make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&tmW, stg, nc0 + c * 32, m0 + lq * 32, wk.split);
-            bulk_commit();
-          }
-        }
-        continue;
-      }
-      // this lane owns tile row m = m0 + lq*32 + lane; its output row index
-      const int m = m0 + lq * 32 + lane;
-      int orow = p.oob_out;                       // rows outside the output are not written
-      int arow = 0;
-      if (m < p.M) {
-        int o;
-        if (p.out_dense)
-          o = m;                                      // compact output (row i <- unit i of the list)
-        else if (KIND == KIND_FWD)
-          o = p.out_pos ? __ldg(p.out_pos + m) : m;   // producer-side compaction for the next layer
-        else
-          o = (m < p.n_kept) ? __ldg(p.kept + m) : __ldg(p.pruned + (m - p.n_kept));
-        if (o >= 0) orow = o;
-        arow = p.aux_by_m ? m : o;
-      }
-      const bool dense_out = p.out_dense;
-      // rows of the 4-row scatter group this lane issues (lanes 0..7)
-      int sr[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sr[j] = __shfl_sync(0xFFFFFFFFu, orow, (4 * lane + j) & 31);
-      if (!zt) {
-        mbar_wait(&tfull[acc], aphase);
-        tc_fence_after();
-      }
-      if (p.dbg & 2) {
-        if (!zt) release();
-        continue;
-      }
-      // one TMA store of a staged 32 x 64 bf16 plane (dense box or 4-row scatter)
-      auto store_plane = [&](const CUtensorMap* tm, uint8_t* buf, int col0) {
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (p.dbg & 1) return;
-        if (dense_out) {
-          if (lane == 0) {
-            tma_store_2d(tm, buf, col0, m0 + lq * 32);
-            bulk_commit();
-          }
-        } else if (lane < 8) {
-          tma_scatter4(tm, buf + lane * 512, col0, sr[0], sr[1], sr[2], sr[3]);
-          bulk_commit();
-        }
-      };
-      const bool two_planes = p.epi == EPI_GELU || p.epi == EPI_GELU_D;
-      const bool has_aux = (p.epi == EPI_GELU_GRAD || p.epi == EPI_MUL) && !zt;
-#pragma unroll 1
-      for (int c = 0; c < BN / 128; ++c) {
-        const int col0 = nc0 + c * 64;
-        uint32_t v[64];
-        // GeLU' operand (pre-activation, or GeLU'(pre) itself for EPI_MUL):
-        // this lane's row, loaded before the TMEM load so the two overlap
-        uint4 pin[8];
-        if (has_aux) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            pin[i] = make_uint4(0u, 0u, 0u, 0u);
-            if (m < p.n_kept && col0 + 8 * i < p.N)
-              pin[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (int64_t)arow * p.ld_aux + col0 + 8 * i));
-          }
-        }
-        if (!zt) {
-          tmem_ld_32x32b_x32(tbase + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-          tmem_ld_32x32b_x32(tbase + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-          tmem_ld_wait();
-          if (c == BN / 128 - 1) release();   // accumulator fully in registers: TMEM free for tile i+2
-        } else {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) v[i] = 0u;
-        }
-        if (two_planes) {
-          // out <- pre (EPI_GELU) or GeLU'(pre) (EPI_GELU_D); out2 <- GeLU(pre).
-          // Both staging buffers are filled in one pass (tanh shared).
-          if (lane < 8) bulk_wait_read0();
-          __syncwarp();
-          uint8_t* const b0 = stg_base;
-          uint8_t* const b1 = stg_base + STAGING_PER_WARP;
-          const bool want_d = p.epi == EPI_GELU_D;
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq) {
-            uint32_t w0[4], w1[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 x = make_float2(__uint_as_float(v[qq * 8 + 2 * j]), __uint_as_float(v[qq * 8 + 2 * j + 1]));
-              float2 hv, dv;
-              gelu2(x, hv, dv, want_d);
-              w0[j] = want_d ? pack2(dv) : pack2(x);
-              w1[j] = pack2(hv);
-            }
-            const uint32_t off = lane * 128 + ((qq ^ (lane & 7)) << 4);
-            st_shared_v4(b0 + off, make_uint4(w0[0], w0[1], w0[2], w0[3]));
-            st_shared_v4(b1 + off, make_uint4(w1[0], w1[1], w1[2], w1[3]));
-          }
-          store_plane(&tmO, b0, col0);
-          store_plane(&tmO2, b1, col0);
-        } else {
-          staging_free();
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq) {
-            uint32_t w[4];
-            const uint32_t a4[4] = {pin[qq].x, pin[qq].y, pin[qq].z, pin[qq].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float2 x = make_float2(__uint_as_float(v[qq * 8 + 2 * j]), __uint_as_float(v[qq * 8 + 2 * j + 1]));
-              if (has_aux) {
-                // G1 = dH * GeLU'(pre_in)  (EPI_MUL: aux already holds GeLU'(pre))
-                const float2 a = unpack2(a4[j]);
-                if (p.epi == EPI_GELU_GRAD) {
-                  float2 hv, dv;
-                  gelu2(a, hv, dv, true);
-                  x = __fmul2_rn(x, dv);
-                } else {
-                  x = __fmul2_rn(x, a);
-                }
-              }
-              w[j] = pack2(x);
-            }
-            st_shared_v4(stg + lane * 128 + ((qq ^ (lane & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
-          }
-          store_plane(&tmO, stg, col0);
-        }
-      }
-    }
+    for (int u = u_first; u < sc.num_units; u += u_step)
+      epilogue_unit<KIND, CG>(&tmO, &tmO2, &tmW, p, sc.S, sc.get(u), rank, warp - 4, lane, staging, tfull, tempty,
+                              tmem_base, ps);
     if (lane < 8) bulk_wait0();   // all output writes performed before the CTA exits
   }
 
@@ -664,21 +711,97 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
 
-  tc_fence_before();
-  if (CG == 2)
-    cluster_sync();
-  else
-    __syncthreads();
-  tc_fence_after();
-  if (warp == 2) {
-    if (CG == 2)
-      tmem_dealloc_cg2(tmem_base, 512);
-    else
-      tmem_dealloc(tmem_base, 512);
-  }
+  kernel_teardown<CG>(tmem_base, warp);
   if (p.pdl_late) pdl_wait();
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMax(p.stamp + 1, (unsigned long long)globaltimer());
   if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp + 1, (unsigned long long)globaltimer());
+}
+
+// Two GEMM problems in ONE persistent launch (a linear's dX and dW, P:146:
+// both need only G and the FWD operands): their work units share every CTA
+// pair under a static longest-processing-time schedule built on the host,
+// so neither GEMM's fill, tail or wave quantisation is exposed on its own
+// and no SM split between two concurrent kernels is needed.
+constexpr int GROUP_LIST_MAX = 256;   // work units of one pair in a grouped launch (smem-staged list)
+
+struct GroupArgs {
+  CUtensorMap a[2], b[2], o[2], o2[2], w[2];
+  GemmParams p[2];
+  const int32_t* sched;   // units of pair q: sched[off[q] .. off[q+1]), entry = problem << 24 | unit
+  const int32_t* off;
+};
+
+template <int K0, int K1, int CG>
+__global__ void __launch_bounds__(NUM_THREADS, 1) ztp_gemm_group_kernel(const __grid_constant__ GroupArgs g) {
+  using C = Cfg<CG>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  uint8_t* staging = smem + C::RING;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::STAGING);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;
+  const int rank = CG == 2 ? (int)(crank & 1u) : 0;
+  const bool leader = rank == 0;
+  const uint16_t pmask = (uint16_t)(0x3u << (crank & ~1u));
+  const int pair = blockIdx.x / CG;
+  // this pair's unit list into shared memory (host-written before the
+  // launch, so read before the PDL wait; made visible by the prologue's sync)
+  int32_t* slist = reinterpret_cast<int32_t*>(smem + C::TOTAL - 1024);
+  const int i0 = __ldg(g.off + pair), nu = __ldg(g.off + pair + 1) - i0;
+  for (int i = threadIdx.x; i < nu; i += blockDim.x) slist[i] = __ldg(g.sched + i0 + i);
+  if (warp == 0 && lane < 4) tma_prefetch_desc(lane < 2 ? &g.a[lane & 1] : &g.b[lane & 1]);
+  const uint32_t tmem_base = kernel_prologue<CG>(full, empty, tfull, tempty, tmem_slot, warp);
+  pdl_wait();
+  pdl_trigger();
+  const GemmParams& p0 = g.p[0];
+  if (p0.stamp != nullptr && threadIdx.x == 0) atomicMin(p0.stamp, (unsigned long long)globaltimer());
+  if (p0.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p0.prof_stamp, ~(unsigned long long)globaltimer());
+  const Sched<K0, C::TM> s0(g.p[0]);
+  const Sched<K1, C::TM> s1(g.p[1]);
+  Pipe ps;
+  if (warp == 0) {
+    for (int i = 0; i < nu; ++i) {
+      const int e = slist[i], u = e & 0xFFFFFF;
+      if ((e >> 24) == 0) {
+        const Work wk = s0.get(u);
+        if (!wk.zero) produce_unit<K0, CG, false, false>(&g.a[0], &g.b[0], g.p[0], wk, rank, leader, lane, ring, full, empty, ps);
+      } else {
+        const Work wk = s1.get(u);
+        if (!wk.zero) produce_unit<K1, CG, false, false>(&g.a[1], &g.b[1], g.p[1], wk, rank, leader, lane, ring, full, empty, ps);
+      }
+    }
+  } else if (warp == 1 && leader) {
+    for (int i = 0; i < nu; ++i) {
+      const int e = slist[i], u = e & 0xFFFFFF;
+      if ((e >> 24) == 0) {
+        const Work wk = s0.get(u);
+        if (!wk.zero) mma_unit<K0, CG>(wk, lane, pmask, ring, full, empty, tfull, tempty, tmem_base, ps);
+      } else {
+        const Work wk = s1.get(u);
+        if (!wk.zero) mma_unit<K1, CG>(wk, lane, pmask, ring, full, empty, tfull, tempty, tmem_base, ps);
+      }
+    }
+  } else if (warp >= 4) {
+    for (int i = 0; i < nu; ++i) {
+      const int e = slist[i], u = e & 0xFFFFFF;
+      if ((e >> 24) == 0)
+        epilogue_unit<K0, CG>(&g.o[0], &g.o2[0], &g.w[0], g.p[0], s0.S, s0.get(u), rank, warp - 4, lane, staging,
+                              tfull, tempty, tmem_base, ps);
+      else
+        epilogue_unit<K1, CG>(&g.o[1], &g.o2[1], &g.w[1], g.p[1], s1.S, s1.get(u), rank, warp - 4, lane, staging,
+                              tfull, tempty, tmem_base, ps);
+    }
+    if (lane < 8) bulk_wait0();
+  }
+  kernel_teardown<CG>(tmem_base, warp);
+  if (p0.stamp != nullptr && threadIdx.x == 0) atomicMax(p0.stamp + 1, (unsigned long long)globaltimer());
+  if (p0.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p0.prof_stamp + 1, (unsigned long long)globaltimer());
 }
 
 // Split-K reduction (fixed split order -> deterministic) fused with the
@@ -905,6 +1028,28 @@ static int units_of(int kind, int cg, const GemmParams& p) {
   return mc * n_tiles * p.splits + (p.splits == 1 ? (m_tiles - mc) * n_tiles : 0);
 }
 
+// After a GEMM launch: the split-K reduce (fixed split order, the epilogue
+// of the unsplit kernel), or the column spread of output pruning.
+template <int KIND>
+static cudaError_t post_launch(const GemmParams& p, int num_sms, cudaStream_t st) {
+  if (p.splits == 1 || p.cs > 1) {
+    if (p.col_pos)   // compact columns written by the epilogue: spread them, Zero the rest
+      return expand_cols_launch(p.out, p.ld_out, p.out_rows, p.col_pos, p.N, p.n_full, st);
+    return cudaSuccess;
+  }
+  const int64_t chunks = (int64_t)p.M * (((p.col_pos ? p.n_full : p.N) + 7) / 8);
+  const int blocks = (int)std::min<int64_t>((chunks + 255) / 256, (int64_t)num_sms * 8);
+  if (KIND == KIND_DW && p.epi == EPI_NONE) {
+    switch (p.splits) {
+      case 2: return dw_reduce_launch<2>(p, blocks, st);
+      case 3: return dw_reduce_launch<3>(p, blocks, st);
+      case 4: return dw_reduce_launch<4>(p, blocks, st);
+      default: break;   // more splits: the generic loop (measured faster at S = 8)
+    }
+  }
+  return launch_k(ztp_splitk_reduce<KIND>, blocks, 256, 0, st, p);
+}
+
 template <int KIND, int CG, bool AG, bool BG>
 static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms, cudaStream_t st) {
   static bool attr_set = false;
@@ -935,22 +1080,7 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, mp.w, p);
     if (e != cudaSuccess) return e;
   }
-  if (p.splits == 1 || p.cs > 1) {
-    if (p.col_pos)   // compact columns written by the epilogue: spread them, Zero the rest
-      return expand_cols_launch(p.out, p.ld_out, p.out_rows, p.col_pos, p.N, p.n_full, st);
-    return cudaSuccess;
-  }
-  const int64_t chunks = (int64_t)p.M * (((p.col_pos ? p.n_full : p.N) + 7) / 8);
-  const int blocks = (int)std::min<int64_t>((chunks + 255) / 256, (int64_t)num_sms * 8);
-  if (KIND == KIND_DW && p.epi == EPI_NONE) {
-    switch (p.splits) {
-      case 2: return dw_reduce_launch<2>(p, blocks, st);
-      case 3: return dw_reduce_launch<3>(p, blocks, st);
-      case 4: return dw_reduce_launch<4>(p, blocks, st);
-      default: break;   // more splits: the generic loop (measured faster at S = 8)
-    }
-  }
-  return launch_k(ztp_splitk_reduce<KIND>, blocks, 256, 0, st, p);
+  return post_launch<KIND>(p, num_sms, st);
 }
 
 int gemm_choose_cg(int kind, int M, int n_kept) {
@@ -1034,11 +1164,9 @@ static cudaError_t dispatch(bool ag, bool bg, const Maps& mp, const GemmParams& 
 }
 
 // Operand, output and workspace tensor maps per kind (see the file header).
-cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_sms, cudaStream_t st) {
-  Maps mp;
+static bool build_maps(int kind, const GemmOperands& o, GemmParams& p, int cg, Maps& mp) {
   bool ok = true;
   const bool ag = o.a_gather, bg = o.b_gather;
-  const int cg = gemm_choose_cg(kind, p.M, p.n_kept);
   const uint32_t bnl = BN / cg;
   p.oob_row = (int)(o.a_rows > o.b_rows ? o.a_rows : o.b_rows);  // outside every gathered tensor
   p.oob_out = p.out_rows;                                        // TMA stores skip this row
@@ -1068,12 +1196,214 @@ cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_s
   } else {
     mp.w = mp.o;
   }
-  if (!ok) return cudaErrorInvalidValue;
+  return ok;
+}
+
+cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_sms, cudaStream_t st) {
+  Maps mp;
+  const bool ag = o.a_gather, bg = o.b_gather;
+  const int cg = gemm_choose_cg(kind, p.M, p.n_kept);
+  if (!build_maps(kind, o, p, cg, mp)) return cudaErrorInvalidValue;
   if (kind == KIND_FWD)
     return cg == 2 ? dispatch<KIND_FWD, 2>(ag, bg, mp, p, num_sms, st) : dispatch<KIND_FWD, 1>(ag, bg, mp, p, num_sms, st);
   if (kind == KIND_DX)
     return cg == 2 ? dispatch<KIND_DX, 2>(ag, bg, mp, p, num_sms, st) : dispatch<KIND_DX, 1>(ag, bg, mp, p, num_sms, st);
   return cg == 2 ? dispatch<KIND_DW, 2>(ag, bg, mp, p, num_sms, st) : dispatch<KIND_DW, 1>(ag, bg, mp, p, num_sms, st);
+}
+
+// ------------------------------------------------------- grouped dX + dW launch
+
+// Host mirror of Sched: the work units of one problem and their cost in
+// 64-deep k-blocks (+ an epilogue allowance: bf16 tile 2, fp32 split-K
+// partial 3; an all-pruned Zero tile costs 1).
+static void unit_costs(int kind, int cg, const GemmParams& p, std::vector<int>& cost, std::vector<char>& zero) {
+  const int tm = BM * cg;
+  const int m_tiles = (p.M + tm - 1) / tm, n_tiles = (p.N + BN - 1) / BN;
+  const int num_kb = (p.kdim + BK - 1) / BK;
+  int mc = m_tiles;
+  if (kind != KIND_FWD) mc = std::min(m_tiles, (p.n_kept + tm - 1) / tm);
+  const int tiles_c = mc * n_tiles, S = p.splits, kbs = p.kb_per_split;
+  const int nz = S == 1 ? (m_tiles - mc) * n_tiles : 0;
+  cost.clear();
+  zero.clear();
+  for (int u = 0; u < nz; ++u) {
+    cost.push_back(1);
+    zero.push_back(1);
+  }
+  for (int u = 0; u < tiles_c * S; ++u) {
+    const int s = u / tiles_c;
+    const int kb0 = s * kbs, kb1 = std::min(num_kb, kb0 + kbs);
+    cost.push_back(std::max(0, kb1 - kb0) + (S > 1 ? 3 : 2));
+    zero.push_back(0);
+  }
+}
+
+// Static schedule of a grouped launch: Zero tiles (epilogue only, ~3 k-blocks
+// of time each) first, one per pair in turn -- LPT would pile the cheap ones
+// onto the idle pairs -- then the computed units, longest first, each onto
+// the least-loaded pair.  Returns the makespan in k-blocks.
+struct GUnit {
+  int cost, prob, idx;
+  bool zero;
+};
+static int64_t lpt_schedule(std::vector<GUnit> us, int pairs, std::vector<std::vector<int32_t>>* lists) {
+  std::stable_sort(us.begin(), us.end(), [](const GUnit& a, const GUnit& b) { return a.cost > b.cost; });
+  std::vector<int64_t> load(pairs, 0);
+  std::vector<std::vector<int32_t>> zl(pairs), rl(pairs);
+  int zq = 0;
+  for (const GUnit& u : us)
+    if (u.zero) {
+      zl[zq].push_back((u.prob << 24) | u.idx);
+      load[zq] += 3;
+      zq = (zq + 1) % pairs;
+    }
+  for (const GUnit& u : us) {
+    if (u.zero) continue;
+    int q = 0;
+    for (int j = 1; j < pairs; ++j)
+      if (load[j] < load[q]) q = j;
+    load[q] += u.cost;
+    rl[q].push_back((u.prob << 24) | u.idx);
+  }
+  if (lists) {
+    lists->assign(pairs, {});
+    for (int q = 0; q < pairs; ++q) {
+      (*lists)[q] = zl[q];
+      (*lists)[q].insert((*lists)[q].end(), rl[q].begin(), rl[q].end());
+    }
+  }
+  return *std::max_element(load.begin(), load.end());
+}
+
+static std::vector<GUnit> group_units(int k0, const GemmParams& p0, int k1, const GemmParams& p1, int cg) {
+  std::vector<int> c0, c1;
+  std::vector<char> z0, z1;
+  unit_costs(k0, cg, p0, c0, z0);
+  unit_costs(k1, cg, p1, c1, z1);
+  std::vector<GUnit> us;
+  for (int i = 0; i < (int)c0.size(); ++i) us.push_back({c0[i], 0, i, z0[i] != 0});
+  for (int i = 0; i < (int)c1.size(); ++i) us.push_back({c1[i], 1, i, z1[i] != 0});
+  return us;
+}
+
+int gemm_group_splits(int M_dx, int N_dx, int kdim_dx, int n_kept_dx, int M_dw, int N_dw, int kdim_dw,
+                      int n_kept_dw, int num_sms) {
+  // the dW split count whose LPT schedule has the smallest makespan (fp32
+  // partials and the reduce grow with the splits: ties go to fewer)
+  const int cg = gemm_choose_cg(KIND_DX, M_dx, n_kept_dx);
+  GemmParams px{}, pw{};
+  px.M = M_dx; px.N = N_dx; px.kdim = kdim_dx; px.n_kept = n_kept_dx; px.splits = 1;
+  px.kb_per_split = (kdim_dx + BK - 1) / BK;
+  pw.M = M_dw; pw.N = N_dw; pw.kdim = kdim_dw; pw.n_kept = n_kept_dw;
+  const int kb_dw = (kdim_dw + BK - 1) / BK;
+  int best = 1;
+  int64_t best_t = -1;
+  for (int s = 1; s <= std::min(16, std::max(1, kb_dw / 8)); ++s) {
+    pw.kb_per_split = (kb_dw + s - 1) / s;
+    pw.splits = (kb_dw + pw.kb_per_split - 1) / pw.kb_per_split;
+    if (pw.splits != s) continue;
+    const auto us = group_units(KIND_DX, px, KIND_DW, pw, cg);
+    const int pairs = std::max(1, std::min((int)us.size(), num_sms / cg));
+    // each extra split adds the reduce's re-read of one fp32 partial (~1 k-block per pair)
+    const int64_t t = lpt_schedule(us, pairs, nullptr) + (s > 1 ? s : 0);
+    if (best_t < 0 || t < best_t) {
+      best_t = t;
+      best = s;
+    }
+  }
+  return best;
+}
+
+namespace {
+struct SchedEntry {
+  std::vector<int64_t> key;
+  int32_t* d = nullptr;   // sched entries then offsets (device; kept for the process: captured graphs use it)
+  int n = 0, pairs = 0;
+};
+std::vector<SchedEntry>& sched_cache() {
+  static std::vector<SchedEntry> v;
+  return v;
+}
+}  // namespace
+
+cudaError_t gemm_group_launch(int k0, const GemmOperands& o0, GemmParams p0, int k1, const GemmOperands& o1,
+                              GemmParams p1, int num_sms, cudaStream_t st) {
+  if (k0 != KIND_DX || k1 != KIND_DW || o0.a_gather || o0.b_gather || o1.a_gather || o1.b_gather || p0.cs > 1 ||
+      p1.cs > 1)
+    return cudaErrorInvalidValue;
+  const int cg = gemm_choose_cg(k0, p0.M, p0.n_kept);
+  if (cg != gemm_choose_cg(k1, p1.M, p1.n_kept)) return cudaErrorInvalidValue;
+  GroupArgs ga;
+  Maps m0, m1;
+  if (!build_maps(k0, o0, p0, cg, m0) || !build_maps(k1, o1, p1, cg, m1)) return cudaErrorInvalidValue;
+  ga.a[0] = m0.a; ga.b[0] = m0.b; ga.o[0] = m0.o; ga.o2[0] = m0.o2; ga.w[0] = m0.w;
+  ga.a[1] = m1.a; ga.b[1] = m1.b; ga.o[1] = m1.o; ga.o2[1] = m1.o2; ga.w[1] = m1.w;
+  ga.p[0] = p0;
+  ga.p[1] = p1;
+  const int total = (int)group_units(k0, p0, k1, p1, cg).size();
+  const int pairs = std::max(1, std::min(total, num_sms / cg));
+  std::vector<int64_t> key = {k0, k1, cg, pairs, p0.M, p0.N, p0.kdim, p0.n_kept, p0.splits, p0.kb_per_split,
+                              p1.M, p1.N, p1.kdim, p1.n_kept, p1.splits, p1.kb_per_split};
+  SchedEntry* hit = nullptr;
+  for (auto& e : sched_cache())
+    if (e.key == key) hit = &e;
+  if (!hit) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return cudaErrorStreamCaptureUnsupported;   // schedules are built by an eager (warm-up) call
+    std::vector<std::vector<int32_t>> lists;
+    lpt_schedule(group_units(k0, p0, k1, p1, cg), pairs, &lists);
+    std::vector<int32_t> h;
+    std::vector<int32_t> off(pairs + 1, 0);
+    for (int q = 0; q < pairs; ++q) {
+      off[q] = (int32_t)h.size();
+      h.insert(h.end(), lists[q].begin(), lists[q].end());
+    }
+    off[pairs] = (int32_t)h.size();
+    for (int q = 0; q < pairs; ++q)
+      if (off[q + 1] - off[q] > GROUP_LIST_MAX) return cudaErrorInvalidConfiguration;   // caller: concurrent pair
+    SchedEntry e;
+    e.key = key;
+    e.n = (int)h.size();
+    e.pairs = pairs;
+    cudaError_t err = cudaMalloc(&e.d, (h.size() + off.size()) * sizeof(int32_t));
+    if (err != cudaSuccess) return err;
+    err = cudaMemcpy(e.d, h.data(), h.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess)
+      err = cudaMemcpy(e.d + h.size(), off.data(), off.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (err != cudaSuccess) return err;
+    sched_cache().push_back(e);
+    hit = &sched_cache().back();
+  }
+  ga.sched = hit->d;
+  ga.off = hit->d + hit->n;
+  const int smem = (cg == 2 ? Cfg<2>::TOTAL : Cfg<1>::TOTAL) + GROUP_LIST_MAX * 4;
+  auto kern = cg == 2 ? ztp_gemm_group_kernel<KIND_DX, KIND_DW, 2> : ztp_gemm_group_kernel<KIND_DX, KIND_DW, 1>;
+  static bool attr_set[3] = {false, false, false};
+  if (!attr_set[cg]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[cg] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pairs * cg);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cg;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ga);
+  if (e != cudaSuccess) return e;
+  e = post_launch<KIND_DX>(p0, num_sms, st);
+  if (e != cudaSuccess) return e;
+  return post_launch<KIND_DW>(p1, num_sms, st);
 }
 
 }  // namespace ztp

@@ -107,6 +107,16 @@ struct GemmOperands {
 };
 
 cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_sms, cudaStream_t st);
+// A linear's dX (k0 = KIND_DX) and dW (k1 = KIND_DW) as ONE persistent launch
+// (grouped, static LPT unit schedule), then their split-K reduces / column
+// spreads.  Both must use the same CTA-group size and compact operands.  The
+// unit schedule of a shape is built by the first (eager) call and cached;
+// a cache miss during stream capture returns cudaErrorStreamCaptureUnsupported.
+cudaError_t gemm_group_launch(int k0, const GemmOperands& o0, GemmParams p0, int k1, const GemmOperands& o1,
+                              GemmParams p1, int num_sms, cudaStream_t st);
+int gemm_choose_cg(int kind, int M, int n_kept);
+int gemm_group_splits(int M_dx, int N_dx, int kdim_dx, int n_kept_dx, int M_dw, int N_dw, int kdim_dw,
+                      int n_kept_dw, int num_sms);
 
 // fp32 verification GEMM (SIMT FFMA), same lineage semantics, fp32 tensors.
 struct GemmParamsF32 {

@@ -225,7 +225,7 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None, f32=False, pl
         Z.ztp_ctx_destroy(ctx)
 
 
-@pytest.mark.parametrize("env", [{"ZTP_CONC": "0"},
+@pytest.mark.parametrize("env", [{"ZTP_GROUP": "1"}, {"ZTP_GROUP": "0"}, {"ZTP_CONC": "0"},
                                  {"ZTP_SQUAT_GUARD": "0"},
                                  {"ZTP_DW_SHARE": "0.8"},
                                  {"ZTP_DW_SHARE": "1.6"}])
