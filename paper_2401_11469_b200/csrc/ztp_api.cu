@@ -53,7 +53,7 @@ struct ztp_ctx {
   // SM (ztp::gemm_group_launch) instead of two concurrent kernels (TP = 1 /
   // row layers; a col layer at TP > 1 keeps the concurrent pair so the dX
   // all-reduce overlaps its dW)
-  int group_bwd = 0;
+  int group_bwd = 0;                   // 0 never (default), 1 always, 2 small pairs only (measured: no net gain)
   int sm_cap = 0;                      // > 0: SMs a GEMM launch may use (concurrent dX / dW partition)
   bool side_pending = false;           // side-stream work not yet joined into a caller stream
   void* skws_side = nullptr;           // split-K partials of side-stream GEMMs
@@ -467,6 +467,7 @@ ztp_status gemm_group(ztp_ctx* c, const GemmSpec& x, const GemmSpec& w, cudaStre
   int M0, N0, k0, M1, N1, k1;
   gemm_dims(x.kind, *x.A.m, *x.B.m, x.out, x.n_out, x.nk, &M0, &N0, &k0);
   gemm_dims(w.kind, *w.A.m, *w.B.m, w.out, w.n_out, w.nk, &M1, &N1, &k1);
+
   if (ztp::gemm_choose_cg(x.kind, M0, x.nk) != ztp::gemm_choose_cg(w.kind, M1, w.nk)) return ZTP_EUNSUPPORTED;
   const int sw = ztp::gemm_group_splits(M0, N0, k0, x.nk, M1, N1, k1, w.nk, c->num_sms);
   ztp::GemmOperands o0{}, o1{};
@@ -837,7 +838,9 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
   if (dtype == ZTP_BF16 && N % 8 != 0) return fail(c, ZTP_ESHAPE, "tokens N must be a multiple of 8");
   const bool reduce_dx0 = layer == LAYER_COL && a->dx_t.ptr && !a->skip_collective && c->world > 1;
   if (c->group_bwd && a->dx_t.ptr && a->dw_t.ptr && dtype == ZTP_BF16 && !reduce_dx0 && !c->use_gather4 &&
-      !(a->act_in != ZTP_ACT_NONE && layer != LAYER_ROW)) {
+      !(a->act_in != ZTP_ACT_NONE && layer != LAYER_ROW) &&
+      (c->group_bwd == 1 || ztp::gemm_group_pays((int)(dxc ? nk : K), (int)N, (int)n_y, nk, (int)K, (int)n_y,
+                                                 (int)N, nk, c->num_sms))) {
     // ---- grouped: dX and dW units in one persistent launch on every SM
     const ztp_mat& x = a->x_t;
     if (!mat_ok(a->dx_t) || (dxc ? a->dx_t.rows < nk : a->dx_t.rows != K) || a->dx_t.cols != N ||
@@ -1043,7 +1046,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* cc = getenv("ZTP_CONC")) c->conc_bwd = atoi(cc) != 0;
   if (const char* ds = getenv("ZTP_DW_SHARE")) c->dw_share = atof(ds);
   if (const char* sg = getenv("ZTP_SQUAT_GUARD")) c->squat_guard = atoi(sg) != 0;
-  if (const char* gb = getenv("ZTP_GROUP")) c->group_bwd = atoi(gb) != 0;
+  if (const char* gb = getenv("ZTP_GROUP")) c->group_bwd = atoi(gb);
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
   auto cleanup = [&](ztp_status s) {

@@ -1314,6 +1314,19 @@ int gemm_group_splits(int M_dx, int N_dx, int kdim_dx, int n_kept_dx, int M_dw, 
   return best;
 }
 
+bool gemm_group_pays(int M_dx, int N_dx, int kdim_dx, int n_kept_dx, int M_dw, int N_dw, int kdim_dw, int n_kept_dw,
+                     int num_sms) {
+  // measured (profiles/r02_grouped_dx_dw_ab.txt): the grouped launch wins
+  // only for small pairs (the O projection at c2: ~28 k-blocks per CTA pair),
+  // where two concurrent kernels each run about one partial wave
+  const int cg = gemm_choose_cg(KIND_DX, M_dx, n_kept_dx);
+  const int tm = BM * cg;
+  auto tiles = [&](int M, int N, int nk) { return ((std::min(M, nk) + tm - 1) / tm) * ((N + BN - 1) / BN); };
+  const double total = (double)tiles(M_dx, N_dx, n_kept_dx) * ((kdim_dx + BK - 1) / BK) +
+                       (double)tiles(M_dw, N_dw, n_kept_dw) * ((kdim_dw + BK - 1) / BK);
+  return total / std::max(1, num_sms / cg) <= 32.0;
+}
+
 namespace {
 struct SchedEntry {
   std::vector<int64_t> key;

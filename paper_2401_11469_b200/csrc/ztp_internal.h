@@ -115,6 +115,8 @@ cudaError_t gemm_launch(int kind, const GemmOperands& o, GemmParams p, int num_s
 cudaError_t gemm_group_launch(int k0, const GemmOperands& o0, GemmParams p0, int k1, const GemmOperands& o1,
                               GemmParams p1, int num_sms, cudaStream_t st);
 int gemm_choose_cg(int kind, int M, int n_kept);
+bool gemm_group_pays(int M_dx, int N_dx, int kdim_dx, int n_kept_dx, int M_dw, int N_dw, int kdim_dw, int n_kept_dw,
+                     int num_sms);
 int gemm_group_splits(int M_dx, int N_dx, int kdim_dx, int n_kept_dx, int M_dw, int N_dw, int kdim_dw,
                       int n_kept_dw, int num_sms);
 
