@@ -79,6 +79,8 @@ struct ztp_ctx {
   int dbg_skip = 0;                    // ZTP_DEBUG_SKIP bitmask (timing experiments only, results invalid):
                                        // 1 select, 2 compaction copies, 4 core, 16 GEMMs
   void* skws = nullptr;                // split-K fp32 partials
+  void* xws[2] = {nullptr, nullptr};   // compact dW columns before the spread (main, side stream)
+  size_t xws_cap[2] = {0, 0};
   size_t skws_cap = 0;
   // profiling (ztp_set_profile): event pairs around every kernel class
   struct ProfEv {
@@ -236,7 +238,8 @@ ztp_status gemm_build_bf16(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, co
                            const int32_t* pruned, int nk, const ztp_mat& out, const ztp_mat* out2, const ztp_mat* aux,
                            int aux_by_m, const int32_t* out_pos, int epi, cudaStream_t st, bool out_compact,
                            const int32_t* col_pos, int n_full, bool indep_of_prev, int M, int N, int kdim,
-                           int force_splits, ztp::GemmOperands* po, ztp::GemmParams* pp) {
+                           int force_splits, ztp::GemmOperands* po, ztp::GemmParams* pp,
+                           const int32_t* col_kept = nullptr) {
   const ztp_mat& a = *A.m;
   const ztp_mat& b = *B.m;
   ztp::GemmOperands o{};
@@ -323,6 +326,27 @@ ztp_status gemm_build_bf16(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, co
     p.splits = 1;
     p.kb_per_split = (kdim + 63) / 64;
   }
+  (void)col_kept;
+  if (col_pos && p.splits == 1) {
+    // output pruning without split-K: the epilogue writes the compact
+    // columns to a scratch (one per stream), the column spread writes dW in
+    // full, Zero units included.  (Spreading inside the epilogue, by
+    // row segments of full columns, measured slower: c4 step 0.87 -> 1.02 ms.)
+    const int64_t ldc = (N + 7) / 8 * 8;
+    const size_t bytes = (size_t)out.rows * ldc * 2;
+    const int k = st == c->side_stream ? 1 : 0;
+    if (c->xws_cap[k] < bytes) {
+      if (c->xws[k]) cudaFree(c->xws[k]);
+      c->xws[k] = nullptr;
+      c->xws_cap[k] = 0;
+      CUDA_TRY(c, cudaMalloc(&c->xws[k], bytes));
+      c->xws_cap[k] = bytes;
+    }
+    p.full_out = p.out;
+    p.ld_full = p.ld_out;
+    p.out = (__nv_bfloat16*)c->xws[k];
+    p.ld_out = ldc;
+  }
   *po = o;
   *pp = p;
   return ZTP_OK;
@@ -368,7 +392,8 @@ ztp_status gemm_check(ztp_ctx* c, int kind, Src A, Src B, int nk, const ztp_mat&
 ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t* kept, const int32_t* pruned,
                 int nk, const ztp_mat& out, const ztp_mat* out2, const ztp_mat* aux, int aux_by_m,
                 const int32_t* out_pos, int epi, cudaStream_t st, bool out_compact = false,
-                const int32_t* col_pos = nullptr, int n_full = 0, bool indep_of_prev = false) {
+                const int32_t* col_pos = nullptr, int n_full = 0, bool indep_of_prev = false,
+                const int32_t* col_kept = nullptr) {
   const int dtype = A.m->dtype;
   {
     const ztp_status cs = gemm_check(c, kind, A, B, nk, out, out2, aux);
@@ -384,7 +409,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     ztp::GemmOperands o{};
     ztp::GemmParams p{};
     ztp_status bs = gemm_build_bf16(c, kind, A, B, n_out, kept, pruned, nk, out, out2, aux, aux_by_m, out_pos, epi, st,
-                                    out_compact, col_pos, n_full, indep_of_prev, M, N, kdim, 0, &o, &p);
+                                    out_compact, col_pos, n_full, indep_of_prev, M, N, kdim, 0, &o, &p, col_kept);
     if (bs != ZTP_OK) return bs;
     if (c->prof_on && c->d_pstamp && c->pstamp_used < ztp_ctx::PSTAMP_CAP) {
       c->pstamp_flops.resize((size_t)c->pstamp_used + 1);
@@ -393,7 +418,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     }
     const int nsm = c->sm_cap > 0 ? c->sm_cap : c->num_sms;
     if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, nsm, st));
-    if ((p.splits > 1 && p.cs <= 1) || p.col_pos) ++c->launches;   // split-K reduce or column expansion
+    if ((p.splits > 1 && p.cs <= 1) || p.col_pos) ++c->launches;   // split-K reduce or column spread
   } else {
     if (col_pos) return fail(c, ZTP_EUNSUPPORTED, "f32 path: output pruning");
     ztp::GemmParamsF32 p{};
@@ -457,6 +482,7 @@ struct GemmSpec {
   bool out_compact;
   const int32_t* col_pos;
   int n_full;
+  const int32_t* col_kept;
 };
 ztp_status gemm_group(ztp_ctx* c, const GemmSpec& x, const GemmSpec& w, cudaStream_t st) {
   for (const GemmSpec* g : {&x, &w}) {
@@ -477,7 +503,7 @@ ztp_status gemm_group(ztp_ctx* c, const GemmSpec& x, const GemmSpec& w, cudaStre
                                   &p0);
   if (bs == ZTP_OK)
     bs = gemm_build_bf16(c, w.kind, w.A, w.B, w.n_out, w.kept, w.pruned, w.nk, w.out, nullptr, nullptr, 0, nullptr,
-                         w.epi, st, false, w.col_pos, w.n_full, false, M1, N1, k1, sw, &o1, &p1);
+                         w.epi, st, false, w.col_pos, w.n_full, false, M1, N1, k1, sw, &o1, &p1, w.col_kept);
   if (bs != ZTP_OK) return bs;
   const double tok0 = (double)x.B.m->cols, tok1 = (double)w.A.m->cols;
   const double fl = 2.0 * x.nk * (double)x.n_out * tok0 + 2.0 * w.nk * (double)w.n_out * tok1;
@@ -870,9 +896,9 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
     ztp_mat dx = a->dx_t;
     if (dxc) dx.rows = nk;   // rows P implied Zero, not written
     const GemmSpec sx{ztp::KIND_DX, W, Src{&g, true}, n_y, kept, dxc ? nullptr : pruned, nk, dx, aux, xc ? 1 : 0,
-                      epi, dxc, nullptr, 0};
+                      epi, dxc, nullptr, 0, nullptr};
     const GemmSpec sw{ztp::KIND_DW, X, Src{&g, true}, n_y, kept, pruned, nk, a->dw_t, nullptr, 0, ztp::EPI_NONE,
-                      false, os ? a->y_pos : nullptr, (int)n_out};
+                      false, os ? a->y_pos : nullptr, (int)n_out, os ? os->kept : nullptr};
     s = gemm_group(c, sx, sw, st);
     if (s != ZTP_EUNSUPPORTED) {
       if (s != ZTP_OK) return s;
@@ -963,7 +989,8 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
     s = gemm(c, ztp::KIND_DW, X, Src{&g, true}, n_y, kept, pruned, nk, a->dw_t, nullptr, nullptr, 0, nullptr,
              ztp::EPI_NONE, sw, false, os ? a->y_pos : nullptr, (int)n_out,
              /*indep_of_prev=*/a->dx_t.ptr != nullptr && !copied && !conc && !reduce_dx &&
-                 a->impute == ZTP_IMPUTE_ZERO);
+                 a->impute == ZTP_IMPUTE_ZERO,
+             os ? os->kept : nullptr);
     c->sm_cap = 0;
     if (s != ZTP_OK) return s;
     if (!dense_sel) s = impute(c, a->impute, a->dw_t, n_out, kept, nk, pruned, np, a->hist_dw, sw);
@@ -1106,6 +1133,8 @@ ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   cudaFree(c->skws);
   cudaFree(c->cws[0]);
   cudaFree(c->cws[1]);
+  cudaFree(c->xws[0]);
+  cudaFree(c->xws[1]);
   for (auto& e : c->prof) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);

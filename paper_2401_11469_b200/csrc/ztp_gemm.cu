@@ -1029,12 +1029,13 @@ static int units_of(int kind, int cg, const GemmParams& p) {
 }
 
 // After a GEMM launch: the split-K reduce (fixed split order, the epilogue
-// of the unsplit kernel), or the column spread of output pruning.
+// of the unsplit kernel; it also spreads output-pruned dW columns), or the
+// column spread of an unsplit output-pruned dW.
 template <int KIND>
 static cudaError_t post_launch(const GemmParams& p, int num_sms, cudaStream_t st) {
   if (p.splits == 1 || p.cs > 1) {
-    if (p.col_pos)   // compact columns written by the epilogue: spread them, Zero the rest
-      return expand_cols_launch(p.out, p.ld_out, p.out_rows, p.col_pos, p.N, p.n_full, st);
+    if (p.col_pos)   // compact columns written by the epilogue (scratch): spread them, Zero the rest
+      return expand_cols_launch(p.out, p.ld_out, p.full_out, p.ld_full, p.out_rows, p.col_pos, p.n_full, st);
     return cudaSuccess;
   }
   const int64_t chunks = (int64_t)p.M * (((p.col_pos ? p.n_full : p.N) + 7) / 8);

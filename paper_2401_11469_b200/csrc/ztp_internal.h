@@ -82,6 +82,8 @@ struct GemmParams {
   const int32_t* col_pos;  // DW output pruning: full column j <- compact column col_pos[j] (< 0: Zero)
   int n_full;              // full output columns when col_pos is set (N = compact columns)
   int pdl_late;            // inputs do not depend on the preceding kernel: PDL wait deferred to exit
+  __nv_bfloat16* full_out; // DW output pruning without split-K: the epilogue writes compact columns to `out`
+  int64_t ld_full;         // (a scratch) and the column spread writes full_out [out_rows, n_full]
   int cs;                  // DW cluster split-K: the `splits` K-slices of a tile run as one cluster and
                            // are reduced through distributed shared memory (no workspace, no reduce kernel)
 };
@@ -188,7 +190,7 @@ struct GatherJobs {
   GatherJob job[GATHER_MAX_JOBS];
 };
 cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st);
-cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, int nc, int n_full, cudaStream_t st);
+
 // Average / Same imputation of rows P (NEXT-2): mode 1 = per-column
 // mean over rows S of `out` (A-10), mode 2 = rows P copied from `hist` (A-11).
 cudaError_t impute_rows_launch(void* out, int64_t ld, int64_t cols, const int32_t* kept, int nk, const int32_t* pruned,
@@ -197,6 +199,9 @@ cudaError_t impute_rows_launch(void* out, int64_t ld, int64_t cols, const int32_
 cudaError_t priority_update_launch(const void* w, int64_t ld_w, const void* w_old, int64_t ld_old, int64_t K,
                                    int64_t n, const int32_t* pos_prev, float* delta, int32_t* count_above,
                                    float theta, cudaStream_t st);
+// out-of-place column spread: dst[r, j] = pos[j] >= 0 ? src[r, pos[j]] : 0, r < n, j < n_full
+cudaError_t expand_cols_launch(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int n, const int32_t* pos,
+                               int n_full, cudaStream_t st);
 cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
                              cudaStream_t st);
 

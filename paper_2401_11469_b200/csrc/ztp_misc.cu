@@ -253,164 +253,152 @@ cudaError_t gather_2d_launch(const void* src, int64_t ld_src, const int32_t* row
                   ld_dst);
 }
 
-// Batched compaction of several operands (ztp_prepare): one launch, one warp
-// per output row (rows of all jobs concatenated).  Row copies stream 16-byte
-// vectors, UNROLL in flight per lane.  2D jobs (a weight block W^T[S, S'],
-// output pruning) first stage the source row in the warp's shared-memory slot
-// with 16-byte loads, then pick the kept columns from shared memory, so HBM
-// sees only coalesced full-row reads.
-__global__ void ztp_gather_multi(const GatherJobs J, int slot_elems) {
+// Batched compaction of several operands (ztp_prepare): one launch over work
+// items of (job, row, 1024-column chunk), one warp per item, so every SM
+// keeps many independent 2 KB copies in flight (no shared memory: full
+// occupancy).  Row copies stream 16-byte vectors, 4 per lane in flight; 2D
+// jobs (a weight block W^T[S, S'], output pruning) gather the kept columns
+// of the source row with 2-byte loads (the chunk's source window is a few KB,
+// served by L1 after its first touch) and store 16-byte vectors.
+constexpr int GM_CHUNK = 1024;   // output elements per work item
+
+__device__ __forceinline__ uint32_t gm_pick2(const uint16_t* s, int a, int b) {
+  return (uint32_t)__ldg(s + a) | ((uint32_t)__ldg(s + b) << 16);
+}
+
+__global__ void __launch_bounds__(256) ztp_gather_multi(const GatherJobs J) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __align__(16) uint16_t gm_slot[];
-  constexpr int UNROLL = 4;
-  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-  uint16_t* slot = gm_slot + (int64_t)(threadIdx.x >> 5) * slot_elems;
-  const int64_t nw = (int64_t)gridDim.x * wpb;
-  for (int64_t row = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); row < J.total; row += nw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t it = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < J.total; it += nw) {
     int j = 0;
 #pragma unroll 1
-    while (j + 1 < J.njobs && row >= J.job[j + 1].rbegin) ++j;
+    while (j + 1 < J.njobs && it >= J.job[j + 1].rbegin) ++j;
     const GatherJob& g = J.job[j];
-    const int r = (int)(row - g.rbegin);
+    const int64_t li = it - g.rbegin;
+    const int cpr = (g.nc + GM_CHUNK - 1) / GM_CHUNK;
+    const int r = (int)(li / cpr), c0 = (int)(li % cpr) * GM_CHUNK;
+    const int c1 = min(g.nc, c0 + GM_CHUNK);
     const uint16_t* s = g.src + (int64_t)(g.rows ? __ldg(g.rows + r) : r) * g.ld_src;
     uint16_t* d = g.dst + (int64_t)r * g.ld_dst;
+    const int v1 = c0 + (c1 - c0) / 8 * 8;         // end of the 8-column groups
     if (!g.cols) {
-      const int nv = g.nc / 8;
-      for (int v0 = lane; v0 < nv; v0 += 32 * UNROLL) {
-        uint4 w[UNROLL];
+      uint4 w[4];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-          if (v0 + 32 * u < nv) w[u] = __ldg(reinterpret_cast<const uint4*>(s) + v0 + 32 * u);
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-          if (v0 + 32 * u < nv) reinterpret_cast<uint4*>(d)[v0 + 32 * u] = w[u];
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 8 * (lane + 32 * u);
+        if (c < v1) w[u] = __ldg(reinterpret_cast<const uint4*>(s + c));
       }
-      for (int c = nv * 8 + lane; c < g.nc; c += 32) d[c] = __ldg(s + c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 8 * (lane + 32 * u);
+        if (c < v1) *reinterpret_cast<uint4*>(d + c) = w[u];
+      }
+      for (int c = v1 + lane; c < c1; c += 32) d[c] = __ldg(s + c);
       continue;
     }
-    const int sv = (g.src_cols + 7) / 8;            // source vectors staged (pitch is 16-byte padded)
-    for (int v0 = lane; v0 < sv; v0 += 32 * UNROLL) {
-      uint4 w[UNROLL];
+    uint4 w[4];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u)
-        if (v0 + 32 * u < sv) w[u] = __ldg(reinterpret_cast<const uint4*>(s) + v0 + 32 * u);
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u)
-        if (v0 + 32 * u < sv) reinterpret_cast<uint4*>(slot)[v0 + 32 * u] = w[u];
-    }
-    __syncwarp();
-    for (int c0 = lane * 8; c0 < g.nc; c0 += 256) {
-      if (c0 + 8 <= g.nc) {
-        uint32_t q[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          q[k] = (uint32_t)slot[__ldg(g.cols + c0 + 2 * k)] | ((uint32_t)slot[__ldg(g.cols + c0 + 2 * k + 1)] << 16);
-        *reinterpret_cast<uint4*>(d + c0) = make_uint4(q[0], q[1], q[2], q[3]);
-      } else {
-        for (int c = c0; c < g.nc; ++c) d[c] = slot[__ldg(g.cols + c)];
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 8 * (lane + 32 * u);
+      if (c < v1) {
+        int4 q0, q1;
+        if ((reinterpret_cast<uintptr_t>(g.cols) & 15) == 0) {
+          q0 = __ldg(reinterpret_cast<const int4*>(g.cols + c));
+          q1 = __ldg(reinterpret_cast<const int4*>(g.cols + c + 4));
+        } else {
+          q0 = make_int4(__ldg(g.cols + c), __ldg(g.cols + c + 1), __ldg(g.cols + c + 2), __ldg(g.cols + c + 3));
+          q1 = make_int4(__ldg(g.cols + c + 4), __ldg(g.cols + c + 5), __ldg(g.cols + c + 6), __ldg(g.cols + c + 7));
+        }
+        w[u] = make_uint4(gm_pick2(s, q0.x, q0.y), gm_pick2(s, q0.z, q0.w), gm_pick2(s, q1.x, q1.y),
+                          gm_pick2(s, q1.z, q1.w));
       }
     }
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 8 * (lane + 32 * u);
+      if (c < v1) *reinterpret_cast<uint4*>(d + c) = w[u];
+    }
+    for (int c = v1 + lane; c < c1; c += 32) d[c] = __ldg(s + __ldg(g.cols + c));
   }
 }
 
 cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st) {
   if (j.total <= 0) return cudaSuccess;
-  int slot = 0;                                   // elements per warp slot (largest 2D source row)
-  for (int i = 0; i < j.njobs; ++i) {
-    const GatherJob& g = j.job[i];
+  GatherJobs J = j;   // work items instead of rows
+  int64_t items = 0;
+  for (int i = 0; i < J.njobs; ++i) {
+    GatherJob& g = J.job[i];
     if ((reinterpret_cast<uintptr_t>(g.src) & 15) || (reinterpret_cast<uintptr_t>(g.dst) & 15) || g.ld_src % 8 ||
         g.ld_dst % 8)
       return cudaErrorMisalignedAddress;
-    if (g.cols) {
-      if (g.src_cols <= 0 || (g.src_cols + 7) / 8 * 8 > g.ld_src) return cudaErrorInvalidValue;
-      slot = std::max(slot, (g.src_cols + 7) / 8 * 8);
-    }
+    if (g.cols && (g.src_cols <= 0 || g.src_cols > g.ld_src)) return cudaErrorInvalidValue;
+    g.rbegin = items;
+    items += (int64_t)g.n * ((g.nc + GM_CHUNK - 1) / GM_CHUNK);
   }
-  int wpb = 8;
-  while (wpb > 1 && (size_t)wpb * slot * 2 > 96 * 1024) wpb >>= 1;
-  const size_t smem = (size_t)wpb * slot * 2;
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  static size_t max_set = 48 * 1024;
-  if (smem > max_set) {
-    cudaError_t e = cudaFuncSetAttribute(ztp_gather_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    max_set = smem;
-  }
-  const int64_t need = (j.total + wpb - 1) / wpb;
-  const int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / std::max<size_t>(smem, 1))));
-  const int blocks = (int)std::min<int64_t>(need, (int64_t)148 * per_sm);
-  return launch_k(ztp_gather_multi, blocks, 32 * wpb, smem, st, j, slot);
+  J.total = items;
+  const int64_t need = (items + 7) / 8;
+  const int blocks = (int)std::min<int64_t>(need, (int64_t)148 * 8);
+  return launch_k(ztp_gather_multi, blocks, 256, 0, st, J);
 }
 
-// In-place column expansion (output pruning, bf16): row r of t holds nc
-// compact columns; afterwards t[r, j] = pos[j] >= 0 ? old[r, pos[j]] : 0 for
-// j < n_full (the Zero gradient of the consumer-pruned units).  One
-// warp per row: the compact row is staged in the warp's shared-memory slot
-// with 16-byte loads first, so the in-place overwrite never reads a written
-// element; several rows per CTA are in flight at once.
-__global__ void ztp_expand_cols(uint16_t* t, int64_t ld, int n, const int32_t* __restrict__ pos, int nc, int n_full,
-                                int row_slot, int pos_vec) {
+// Column expansion (output pruning, bf16), out of place: dst[r, j] =
+// pos[j] >= 0 ? src[r, pos[j]] : 0 for j < n_full (the Zero gradient of the
+// consumer-pruned units).  Work items of (row, 1024 output columns),
+// one warp each: 8-column groups, pos read as 16-byte vectors, the compact
+// source window gathered with 2-byte loads (L1), 16-byte stores.
+__global__ void __launch_bounds__(256) ztp_expand_cols(const uint16_t* __restrict__ src, int64_t ld_src,
+                                                       uint16_t* __restrict__ dst, int64_t ld_dst, int n,
+                                                       const int32_t* __restrict__ pos, int n_full) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __align__(16) uint16_t rows_s[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-  uint16_t* row = rows_s + (int64_t)w * row_slot;
-  const int nv = nc / 8;
-  for (int r = blockIdx.x * wpb + w; r < n; r += gridDim.x * wpb) {
-    uint16_t* p = t + (int64_t)r * ld;
-    for (int c = lane; c < nv; c += 32)
-      reinterpret_cast<uint4*>(row)[c] = reinterpret_cast<const uint4*>(p)[c];
-    for (int c = nv * 8 + lane; c < nc; c += 32) row[c] = p[c];
-    __syncwarp();
-    for (int j0 = lane * 8; j0 < n_full; j0 += 256) {
-      if (j0 + 8 <= n_full) {
-        int q[8];
-        if (pos_vec) {
-          const int4 q0 = __ldg(reinterpret_cast<const int4*>(pos + j0));
-          const int4 q1 = __ldg(reinterpret_cast<const int4*>(pos + j0 + 4));
-          q[0] = q0.x, q[1] = q0.y, q[2] = q0.z, q[3] = q0.w, q[4] = q1.x, q[5] = q1.y, q[6] = q1.z, q[7] = q1.w;
+  const int lane = threadIdx.x & 31;
+  const int cpr = (n_full + GM_CHUNK - 1) / GM_CHUNK;
+  const int64_t items = (int64_t)n * cpr;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const bool pv = (reinterpret_cast<uintptr_t>(pos) & 15) == 0;
+  for (int64_t it = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += nw) {
+    const int r = (int)(it / cpr), c0 = (int)(it % cpr) * GM_CHUNK;
+    const int c1 = min(n_full, c0 + GM_CHUNK);
+    const int v1 = c0 + (c1 - c0) / 8 * 8;
+    const uint16_t* s = src + (int64_t)r * ld_src;
+    uint16_t* d = dst + (int64_t)r * ld_dst;
+    auto pick = [&](int q) -> uint32_t { return q >= 0 ? (uint32_t)__ldg(s + q) : 0u; };
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 8 * (lane + 32 * u);
+      if (c < v1) {
+        int4 q0, q1;
+        if (pv) {
+          q0 = __ldg(reinterpret_cast<const int4*>(pos + c));
+          q1 = __ldg(reinterpret_cast<const int4*>(pos + c + 4));
         } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) q[k] = __ldg(pos + j0 + k);
+          q0 = make_int4(__ldg(pos + c), __ldg(pos + c + 1), __ldg(pos + c + 2), __ldg(pos + c + 3));
+          q1 = make_int4(__ldg(pos + c + 4), __ldg(pos + c + 5), __ldg(pos + c + 6), __ldg(pos + c + 7));
         }
-        uint32_t o[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          o[k] = (q[2 * k] >= 0 ? (uint32_t)row[q[2 * k]] : 0u) |
-                 ((q[2 * k + 1] >= 0 ? (uint32_t)row[q[2 * k + 1]] : 0u) << 16);
-        *reinterpret_cast<uint4*>(p + j0) = make_uint4(o[0], o[1], o[2], o[3]);
-      } else {
-        for (int j = j0; j < n_full; ++j) {
-          const int q = __ldg(pos + j);
-          p[j] = q >= 0 ? row[q] : (uint16_t)0;
-        }
+        w[u] = make_uint4(pick(q0.x) | (pick(q0.y) << 16), pick(q0.z) | (pick(q0.w) << 16),
+                          pick(q1.x) | (pick(q1.y) << 16), pick(q1.z) | (pick(q1.w) << 16));
       }
     }
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 8 * (lane + 32 * u);
+      if (c < v1) *reinterpret_cast<uint4*>(d + c) = w[u];
+    }
+    for (int c = v1 + lane; c < c1; c += 32) d[c] = (uint16_t)pick(__ldg(pos + c));
   }
 }
 
-cudaError_t expand_cols_launch(void* t, int64_t ld, int n, const int32_t* pos, int nc, int n_full, cudaStream_t st) {
+cudaError_t expand_cols_launch(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int n, const int32_t* pos,
+                               int n_full, cudaStream_t st) {
   if (n <= 0 || n_full <= 0) return cudaSuccess;
-  if ((reinterpret_cast<uintptr_t>(t) & 15) != 0 || ld % 8 != 0) return cudaErrorMisalignedAddress;
-  const int pos_vec = (reinterpret_cast<uintptr_t>(pos) & 15) == 0;
-  const int row_slot = (nc + 7) / 8 * 8;                    // elements per warp slot (16-byte multiple)
-  int wpb = 8;
-  while (wpb > 1 && (size_t)wpb * row_slot * 2 > 96 * 1024) wpb >>= 1;
-  const size_t smem = (size_t)wpb * row_slot * 2;
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  static int max_set = 48 * 1024;
-  if ((int)smem > max_set) {
-    cudaError_t e = cudaFuncSetAttribute(ztp_expand_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    max_set = (int)smem;
-  }
-  const int need = (n + wpb - 1) / wpb;
-  const int blocks = need < 148 * 4 ? need : 148 * 4;
-  return launch_k(ztp_expand_cols, blocks, 32 * wpb, smem, st, (uint16_t*)t, ld, n, pos, nc, n_full, row_slot,
-                  pos_vec);
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) != 0 || ld_dst % 8 != 0) return cudaErrorMisalignedAddress;
+  const int64_t items = (int64_t)n * ((n_full + GM_CHUNK - 1) / GM_CHUNK);
+  const int blocks = (int)std::min<int64_t>((items + 7) / 8, (int64_t)148 * 8);
+  return launch_k(ztp_expand_cols, blocks, 256, 0, st, (const uint16_t*)src, ld_src, (uint16_t*)dst, ld_dst, n, pos,
+                  n_full);
 }
 
 // ------------------------------------------ Average / Same imputation (NEXT-2)
