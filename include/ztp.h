@@ -135,6 +135,33 @@ ztp_status ztp_set_transport(ztp_ctx* ctx, int transport);
 ztp_status ztp_barrier(ztp_ctx* ctx, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Execution options of a context (performance scheduling only; results are
+ * the same up to fp32 summation order within the stated tolerances).  Each
+ * starts from its environment variable (read once by ztp_ctx_create) or the
+ * default below; ztp_set_option overrides it for later calls.  Values are
+ * doubles (integers for switches).  EINVAL on an unknown option / bad value.
+ *   ZTP_OPT_CONC        (ZTP_CONC, 1)        dW GEMM on a side stream, concurrent with dX
+ *   ZTP_OPT_DW_SHARE    (ZTP_DW_SHARE, 1.2)  weight of dW's MMA work in the dX / dW SM split
+ *   ZTP_OPT_SQUAT_GUARD (ZTP_SQUAT_GUARD, 1) core kernel in stream order while a dW is pending
+ *   ZTP_OPT_GATHER4     (ZTP_GATHER4, 0)     operand rows gathered by TMA gather4 inside the GEMM
+ *   ZTP_OPT_SPLITK      (ZTP_SPLITK, 1)      split-K for few-tile GEMMs
+ *   ZTP_OPT_GROUP       (ZTP_GROUP, 0)       0 / 1 / 2: dX + dW as one grouped launch never /
+ *                                            always / only for small pairs
+ *   ZTP_OPT_PEER_CTAS   (ZTP_PEER_CTAS, 32)  CTAs of a peer collective (same on every rank)
+ * ------------------------------------------------------------------------- */
+typedef enum ztp_option {
+  ZTP_OPT_CONC = 0,
+  ZTP_OPT_DW_SHARE = 1,
+  ZTP_OPT_SQUAT_GUARD = 2,
+  ZTP_OPT_GATHER4 = 3,
+  ZTP_OPT_SPLITK = 4,
+  ZTP_OPT_GROUP = 5,
+  ZTP_OPT_PEER_CTAS = 6
+} ztp_option;
+ztp_status ztp_set_option(ztp_ctx* ctx, ztp_option opt, double value);
+ztp_status ztp_get_option(const ztp_ctx* ctx, ztp_option opt, double* value);
+
+/* ---------------------------------------------------------------------------
  * (1) Plan -- pure host, deterministic, no context, no device work.
  *
  * ztp_plan: per-rank runtimes T[e] and GEMM times M[e] (A-5, A-6) of the last

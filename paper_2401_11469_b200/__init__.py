@@ -23,7 +23,8 @@ __all__ = [
     "make_costs", "plan_opts", "ZtpError", "ztp_window_create", "ztp_window_open", "ztp_sym_alloc",
     "ztp_set_transport", "ztp_barrier", "TRANSPORT_NCCL", "TRANSPORT_PEER",
 ]
-from ._lib import TRANSPORT_NCCL, TRANSPORT_PEER  # noqa: E402
+from ._lib import (TRANSPORT_NCCL, TRANSPORT_PEER, OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4,  # noqa: E402
+                   OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS)
 
 
 def _stream(stream) -> Optional[int]:
@@ -351,6 +352,16 @@ def ztp_sym_alloc(ctx, rows: int, cols: int, dtype=None, device: int = 0):
 
 def ztp_set_transport(ctx, transport: int) -> None:
     check(lib.ztp_set_transport(ctx, transport), ctx)
+
+
+def ztp_set_option(ctx, opt: int, value: float) -> None:
+    check(lib.ztp_set_option(ctx, int(opt), float(value)), ctx)
+
+
+def ztp_get_option(ctx, opt: int) -> float:
+    v = C.c_double()
+    check(lib.ztp_get_option(ctx, int(opt), C.byref(v)), ctx)
+    return v.value
 
 
 def ztp_barrier(ctx, stream=None) -> None:

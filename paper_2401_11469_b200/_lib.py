@@ -24,6 +24,7 @@ ACT_NONE, ACT_GELU, ACT_GELU_D = 0, 1, 2
 CRIT_AVG, CRIT_MIN = 0, 1
 NORMAL, RESIZE, MIGRATE, SPLIT = 0, 1, 2, 3
 KIND_FWD, KIND_DX, KIND_DW = 0, 1, 2
+OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4, OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS = range(7)
 
 
 class ZtpError(RuntimeError):
@@ -163,6 +164,8 @@ def _load():
         "ztp_sym_alloc": (st, [vp, C.c_size_t, C.POINTER(vp)]),
         "ztp_set_transport": (st, [vp, C.c_int]),
         "ztp_barrier": (st, [vp, vp]),
+        "ztp_set_option": (st, [vp, C.c_int, C.c_double]),
+        "ztp_get_option": (st, [vp, C.c_int, C.POINTER(C.c_double)]),
         "ztp_read_profile": (st, [vp, vp, C.POINTER(Profile)]),
     }
     for name, (res, args) in sig.items():
@@ -182,7 +185,7 @@ EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_i
             "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "ztp_prepare",
             "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",
             "ztp_set_profile", "ztp_read_profile", "ztp_window_create", "ztp_window_open", "ztp_sym_alloc",
-            "ztp_set_transport", "ztp_barrier")
+            "ztp_set_transport", "ztp_barrier", "ztp_set_option", "ztp_get_option")
 
 
 def check(code: int, ctx=None):

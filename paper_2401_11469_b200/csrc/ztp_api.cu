@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <string>
@@ -1576,6 +1577,45 @@ ztp_status ztp_set_transport(ztp_ctx* c, int transport) {
     return fail(c, ZTP_EINVAL, "ztp_set_transport: this context has no NCCL communicator");
   c->transport = transport;
   return ZTP_OK;
+}
+
+ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
+  if (!c) return fail(c, ZTP_EINVAL, "ztp_set_option: null ctx");
+  if (!std::isfinite(v)) return fail(c, ZTP_EINVAL, "ztp_set_option: value must be finite");
+  const int iv = (int)v;
+  switch (opt) {
+    case ZTP_OPT_CONC: c->conc_bwd = iv != 0; return ZTP_OK;
+    case ZTP_OPT_DW_SHARE:
+      if (!(v > 0.0)) return fail(c, ZTP_EINVAL, "ztp_set_option: dW share must be > 0");
+      c->dw_share = v;
+      return ZTP_OK;
+    case ZTP_OPT_SQUAT_GUARD: c->squat_guard = iv != 0; return ZTP_OK;
+    case ZTP_OPT_GATHER4: c->use_gather4 = iv != 0; return ZTP_OK;
+    case ZTP_OPT_SPLITK: c->allow_splitk = iv != 0; return ZTP_OK;
+    case ZTP_OPT_GROUP:
+      if (iv < 0 || iv > 2) return fail(c, ZTP_EINVAL, "ztp_set_option: group mode is 0, 1 or 2");
+      c->group_bwd = iv;
+      return ZTP_OK;
+    case ZTP_OPT_PEER_CTAS:
+      if (iv < 1 || iv > ztp::PEER_MAX_CTAS) return fail(c, ZTP_EINVAL, "ztp_set_option: peer CTAs out of range");
+      c->peer_ctas = iv;
+      return ZTP_OK;
+  }
+  return fail(c, ZTP_EINVAL, "ztp_set_option: unknown option " + std::to_string((int)opt));
+}
+
+ztp_status ztp_get_option(const ztp_ctx* c, ztp_option opt, double* v) {
+  if (!c || !v) return fail(nullptr, ZTP_EINVAL, "ztp_get_option: null argument");
+  switch (opt) {
+    case ZTP_OPT_CONC: *v = c->conc_bwd; return ZTP_OK;
+    case ZTP_OPT_DW_SHARE: *v = c->dw_share; return ZTP_OK;
+    case ZTP_OPT_SQUAT_GUARD: *v = c->squat_guard; return ZTP_OK;
+    case ZTP_OPT_GATHER4: *v = c->use_gather4; return ZTP_OK;
+    case ZTP_OPT_SPLITK: *v = c->allow_splitk; return ZTP_OK;
+    case ZTP_OPT_GROUP: *v = c->group_bwd; return ZTP_OK;
+    case ZTP_OPT_PEER_CTAS: *v = c->peer_ctas; return ZTP_OK;
+  }
+  return fail(nullptr, ZTP_EINVAL, "ztp_get_option: unknown option " + std::to_string((int)opt));
 }
 
 ztp_status ztp_barrier(ztp_ctx* c, void* stream) {

@@ -225,25 +225,24 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None, f32=False, pl
         Z.ztp_ctx_destroy(ctx)
 
 
-@pytest.mark.parametrize("env", [{"ZTP_GROUP": "1"}, {"ZTP_GROUP": "0"}, {"ZTP_CONC": "0"},
-                                 {"ZTP_SQUAT_GUARD": "0"},
-                                 {"ZTP_DW_SHARE": "0.8"},
-                                 {"ZTP_DW_SHARE": "1.6"}])
-def test_layer_schedule_variants_graph(tz, monkeypatch, env):
-    """The scheduling choices (concurrent vs serial dX / dW, the SM split
-    weight -- it changes the dW split-K counts -- and the core's stream-order
-    guard) change launch order and summation splits only: a captured step
-    under each still matches the oracle.  The knobs are read when a context
-    is created."""
+@pytest.mark.parametrize("opts", [{"GROUP": 1}, {"GROUP": 2}, {"CONC": 0}, {"SQUAT_GUARD": 0},
+                                  {"DW_SHARE": 0.8}, {"DW_SHARE": 1.6}, {"SPLITK": 0}])
+def test_layer_schedule_variants_graph(tz, opts):
+    """The scheduling options (ztp_set_option: grouped or concurrent or
+    serial dX / dW, the SM split weight -- it changes the dW split-K counts --,
+    split-K off, the core's stream-order guard) change launch order and
+    summation splits only: a captured step under each still matches the
+    oracle."""
     torch, Z, ZtpLayer, _ = tz
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
     h, f, N = 512, 2048, 1032
     X, G, sh = make_inputs(h, f, N, 1, 17)
     gam = [dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)]
     sel, scores, nps = selections(1, h, f, N, 17, gam)
     ref = O.layer_step(X, G, sh, sel)
     ctx, L = build(tz, sh, 0, 1, h, f, N)
+    for k, v in opts.items():
+        Z.ztp_set_option(ctx, getattr(Z, "OPT_" + k), v)
+        assert Z.ztp_get_option(ctx, getattr(Z, "OPT_" + k)) == v
     L.set_selection(nps[0], {s: torch.from_numpy(v).cuda() for s, v in scores[0].items()})
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):

@@ -116,3 +116,22 @@ def test_profile_counters(env):
     assert p["n_gemm"] == 3
     assert p["gemm_flops"] == pytest.approx(3 * 2.0 * K * n * N, rel=1e-12)
     assert 0 < p["gemm_kernel_ms"] <= p["gemm_ms"] * 1.05
+
+
+def test_options_round_trip_and_errors():
+    """ztp_set_option / ztp_get_option (include/ztp.h): values round-trip,
+    bad values and unknown options are EINVAL and leave the option as it was."""
+    import paper_2401_11469_b200 as Z
+    ctx = Z.ztp_ctx_create(0, 1, None, 0)
+    try:
+        for opt, val in ((Z.OPT_CONC, 0), (Z.OPT_DW_SHARE, 1.5), (Z.OPT_SQUAT_GUARD, 0), (Z.OPT_GATHER4, 1),
+                         (Z.OPT_SPLITK, 0), (Z.OPT_GROUP, 2), (Z.OPT_PEER_CTAS, 16)):
+            Z.ztp_set_option(ctx, opt, val)
+            assert Z.ztp_get_option(ctx, opt) == val
+        for opt, bad in ((Z.OPT_DW_SHARE, 0.0), (Z.OPT_GROUP, 3), (Z.OPT_PEER_CTAS, 0), (99, 1.0)):
+            with pytest.raises(Z.ZtpError) as ei:
+                Z.ztp_set_option(ctx, opt, bad)
+            assert ei.value.name == "ZTP_EINVAL"
+        assert Z.ztp_get_option(ctx, Z.OPT_GROUP) == 2
+    finally:
+        Z.ztp_ctx_destroy(ctx)
