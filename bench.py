@@ -477,6 +477,60 @@ class Case:
         self.Z.ztp_ctx_destroy(self.ctx)
 
 
+def table1(D, args, stream):
+    """Table I analog on this box's ranks: the
+    paper-literal sending-collecting migration of one column linear (c4's FC1
+    at TP = e: K = h, n = f / e, N tokens) in a homogeneous setting -- nu
+    ranks each migrate a fraction gamma of their contraction rows to the
+    normal ranks, broadcast-reduce (NCCL broadcast / reduce) vs
+    scatter-gather (point-to-point) -- step (FWD + BWD) ms, max over ranks,
+    and its ratio to gamma = 0."""
+    import torch
+    import paper_2401_11469_b200 as Z
+    from paper_2401_11469_b200.kmig import KMigColLinear
+    from paper_2401_11469_b200.layer import sym_allocator
+    from synth.configs import CONFIGS
+    e, r = D.world, D.rank
+    cfg = CONFIGS["c4"]
+    K, n, N = cfg.h, cfg.f // e, cfg.N
+    use_nccl = args.transport == "nccl" and not args.share_gpu
+    uid = D.bcast_obj(Z.ztp_get_unique_id() if (use_nccl and r == 0) else None) if use_nccl else None
+    ctx = Z.ztp_ctx_create(r, e, uid, D.device)
+    Z.ztp_window_open(ctx, D.allgather_obj(Z.ztp_window_create(ctx, 8 << 30)))
+    alloc = sym_allocator(ctx, D.device)
+    nus = sorted({1, min(4, e - 1)})
+    rows = []
+    for nu in nus:
+        migr = list(range(e - nu, e))
+        for mode, mname in ((Z.COLL_TREE, "broadcast-reduce"), (Z.COLL_P2P, "scatter-gather")):
+            row = {"policy": mname, "nu": nu, "ms": {}}
+            for g in (0.0, 0.25, 0.5, 0.75, 1.0):
+                k = min(int(round(g * K)), K - 64)       # >= 64 contraction rows stay (A-4 analog)
+                Lk = KMigColLinear(ctx, r, e, K, n, N, migr if k else [], k, mode, alloc=alloc)
+                Lk.X.normal_()
+                Lk.W.uniform_(-K ** -0.5, K ** -0.5)
+                Lk.G.normal_()
+                for _ in range(2):
+                    Lk.step(stream)
+                torch.cuda.synchronize()
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    Lk.step(stream)
+                for _ in range(3):
+                    gr.replay()
+                row["ms"][str(g)] = timed(D, gr.replay, 20, stream)
+                del gr, Lk
+            base = row["ms"]["0.0"]
+            row["ratio"] = {gk: v / base for gk, v in row["ms"].items()}
+            rows.append(row)
+    D.barrier()
+    Z.ztp_ctx_destroy(ctx)
+    return {"workload": f"c4 FC1 column linear at TP={e}: K={K}, n={n}, N={N}, fwd+bwd, homogeneous",
+            "transport": "nccl collectives + peer pulls" if use_nccl else "peer", "rows": rows,
+            "paper_v100_ratio_gamma1": {"broadcast-reduce(1)": 500 / 373, "scatter-gather(1)": 963 / 373,
+                                        "broadcast-reduce(4)": 1113 / 373, "scatter-gather(4)": 1436 / 373}}
+
+
 def plan_summary(plan, e):
     if plan is None:
         return {"roles": "N" * e}
@@ -738,6 +792,8 @@ def main():
             matrix.append(case_summary(M, mc["name"], res, peak_burst))
             M.destroy()
             torch.cuda.empty_cache()
+        extra["table1"] = table1(D, args, stream)
+        torch.cuda.empty_cache()
     h2d = 2 * h * N * 2
     d2h = h * N * 2
     line = {

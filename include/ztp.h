@@ -135,6 +135,33 @@ ztp_status ztp_set_transport(ztp_ctx* ctx, int transport);
 ztp_status ztp_barrier(ztp_ctx* ctx, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Rooted collectives and the local reduce of the paper-literal migration
+ * (NEXT-3; "sending-collecting migration", Table I).
+ * Collective: every rank calls with the same root / shape / mode.
+ * ztp_broadcast: every rank's t <- root's t.  ztp_reduce: root's t <- sum over
+ * ranks of t (other ranks' t unchanged).  mode ZTP_COLL_TREE = the NCCL
+ * collective (ncclBroadcast / ncclReduce: ring / tree / NVLS, many de facto
+ * senders); ZTP_COLL_P2P = point to point (grouped ncclSend / ncclRecv: the
+ * root sends the whole tensor to every rank / receives every rank's tensor
+ * into the ctx workspace and sums them in rank order).  Under the peer
+ * transport both modes are pulls (broadcast: every rank pulls the root's
+ * window tensor; reduce: the root pulls every rank's and sums in rank order
+ * 0..e-1 in fp32) and t must be a window tensor.  Contiguous t only (ld ==
+ * cols).  Errors: EINVAL (root / mode / not in the window), ESHAPE, ENCCL.
+ * ztp_accumulate: dst += src elementwise (same shape, fp32 add, one
+ * rounding) -- a helper's migrated contribution merged into its own partial
+ * before the all-reduce (the "reduce-merging" of P:248).
+ * ------------------------------------------------------------------------- */
+enum { ZTP_COLL_TREE = 0, ZTP_COLL_P2P = 1 };
+ztp_status ztp_broadcast(ztp_ctx* ctx, int root, const ztp_mat* t, int mode, void* stream);
+ztp_status ztp_reduce(ztp_ctx* ctx, int root, const ztp_mat* t, int mode, void* stream);
+ztp_status ztp_accumulate(ztp_ctx* ctx, const ztp_mat* dst, const ztp_mat* src, void* stream);
+/* The all-reduce (sum) the linears issue, for a caller that merges
+ * extra contributions into its partial first (skip_collective = 1, then
+ * ztp_accumulate, then this).  Contiguous t; peer transport: a window tensor. */
+ztp_status ztp_allreduce(ztp_ctx* ctx, const ztp_mat* t, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Execution options of a context (performance scheduling only; results are
  * the same up to fp32 summation order within the stated tolerances).  Each
  * starts from its environment variable (read once by ztp_ctx_create) or the

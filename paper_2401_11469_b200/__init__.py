@@ -23,7 +23,7 @@ __all__ = [
     "make_costs", "plan_opts", "ZtpError", "ztp_window_create", "ztp_window_open", "ztp_sym_alloc",
     "ztp_set_transport", "ztp_barrier", "TRANSPORT_NCCL", "TRANSPORT_PEER",
 ]
-from ._lib import (TRANSPORT_NCCL, TRANSPORT_PEER, OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4,  # noqa: E402
+from ._lib import (TRANSPORT_NCCL, TRANSPORT_PEER, COLL_TREE, COLL_P2P, OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4,  # noqa: E402
                    OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS)
 
 
@@ -352,6 +352,26 @@ def ztp_sym_alloc(ctx, rows: int, cols: int, dtype=None, device: int = 0):
 
 def ztp_set_transport(ctx, transport: int) -> None:
     check(lib.ztp_set_transport(ctx, transport), ctx)
+
+
+def ztp_broadcast(ctx, root: int, t, mode: int = 0, stream=None) -> None:
+    m = mat(t)
+    check(lib.ztp_broadcast(ctx, root, C.byref(m), mode, _stream(stream)), ctx)
+
+
+def ztp_reduce(ctx, root: int, t, mode: int = 0, stream=None) -> None:
+    m = mat(t)
+    check(lib.ztp_reduce(ctx, root, C.byref(m), mode, _stream(stream)), ctx)
+
+
+def ztp_accumulate(ctx, dst, src, stream=None) -> None:
+    d, s_ = mat(dst), mat(src)
+    check(lib.ztp_accumulate(ctx, C.byref(d), C.byref(s_), _stream(stream)), ctx)
+
+
+def ztp_allreduce(ctx, t, stream=None) -> None:
+    m = mat(t)
+    check(lib.ztp_allreduce(ctx, C.byref(m), _stream(stream)), ctx)
 
 
 def ztp_set_option(ctx, opt: int, value: float) -> None:

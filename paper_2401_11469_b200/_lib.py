@@ -13,6 +13,7 @@ MAX_RANKS = 8
 UID_BYTES = 128
 IPC_BYTES = 128
 TRANSPORT_NCCL, TRANSPORT_PEER = 0, 1
+COLL_TREE, COLL_P2P = 0, 1
 
 # status codes (ztp_status)
 STATUS = ["ZTP_OK", "ZTP_EINVAL", "ZTP_ESHAPE", "ZTP_EINDEX", "ZTP_EDEGENERATE", "ZTP_ELINEAGE", "ZTP_EHISTORY",
@@ -165,6 +166,10 @@ def _load():
         "ztp_set_transport": (st, [vp, C.c_int]),
         "ztp_barrier": (st, [vp, vp]),
         "ztp_set_option": (st, [vp, C.c_int, C.c_double]),
+        "ztp_broadcast": (st, [vp, C.c_int, C.POINTER(Mat), C.c_int, vp]),
+        "ztp_reduce": (st, [vp, C.c_int, C.POINTER(Mat), C.c_int, vp]),
+        "ztp_accumulate": (st, [vp, C.POINTER(Mat), C.POINTER(Mat), vp]),
+        "ztp_allreduce": (st, [vp, C.POINTER(Mat), vp]),
         "ztp_get_option": (st, [vp, C.c_int, C.POINTER(C.c_double)]),
         "ztp_read_profile": (st, [vp, vp, C.POINTER(Profile)]),
     }
@@ -185,7 +190,8 @@ EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_i
             "ztp_core", "ztp_migrate", "ztp_set_slowdown", "ztp_set_stats", "ztp_read_gemm_ns", "ztp_gemm", "ztp_prepare",
             "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",
             "ztp_set_profile", "ztp_read_profile", "ztp_window_create", "ztp_window_open", "ztp_sym_alloc",
-            "ztp_set_transport", "ztp_barrier", "ztp_set_option", "ztp_get_option")
+            "ztp_set_transport", "ztp_barrier", "ztp_set_option", "ztp_get_option", "ztp_broadcast", "ztp_reduce",
+            "ztp_accumulate", "ztp_allreduce")
 
 
 def check(code: int, ctx=None):

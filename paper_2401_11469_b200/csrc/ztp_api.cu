@@ -1579,6 +1579,99 @@ ztp_status ztp_set_transport(ztp_ctx* c, int transport) {
   return ZTP_OK;
 }
 
+ztp_status ztp_broadcast(ztp_ctx* c, int root, const ztp_mat* t, int mode, void* stream) {
+  if (!c || !t) return fail(c, ZTP_EINVAL, "ztp_broadcast: null argument");
+  if (root < 0 || root >= c->world || (mode != ZTP_COLL_TREE && mode != ZTP_COLL_P2P))
+    return fail(c, ZTP_EINVAL, "ztp_broadcast: bad root / mode");
+  if (!mat_ok(*t) || t->ld != t->cols) return fail(c, ZTP_ESHAPE, "ztp_broadcast: contiguous tensor needed, " + shp("t", *t));
+  if (c->world == 1) return ZTP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = t->dtype == ZTP_F32 ? 4 : 2;
+  const size_t n = (size_t)(t->rows * t->cols), bytes = n * es;
+  const int pe = prof_begin(c, st, PROF_COMM, 0.0);
+  if (c->transport == ZTP_TRANSPORT_PEER) {
+    int64_t off;
+    ztp_status s = win_offset(c, t->ptr, bytes, "ztp_broadcast", &off);
+    if (s != ZTP_OK) return s;
+    if (bytes % 16) return fail(c, ZTP_ESHAPE, "peer broadcast: payload must be a multiple of 16 bytes");
+    CUDA_TRY(c, ztp::peer_bcast_launch(c->pw, root, off, (int64_t)bytes, c->peer_ctas, st));
+    ++c->launches;
+  } else if (mode == ZTP_COLL_TREE) {
+    NCCL_TRY(c, ncclBroadcast(t->ptr, t->ptr, n, nccl_type(t->dtype), root, c->comm, st));
+  } else {
+    NCCL_TRY(c, ncclGroupStart());
+    if (c->rank == root) {
+      for (int q = 0; q < c->world; ++q)
+        if (q != root) NCCL_TRY(c, ncclSend(t->ptr, n, nccl_type(t->dtype), q, c->comm, st));
+    } else {
+      NCCL_TRY(c, ncclRecv(t->ptr, n, nccl_type(t->dtype), root, c->comm, st));
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+  }
+  prof_end(c, pe, st);
+  return ZTP_OK;
+}
+
+ztp_status ztp_reduce(ztp_ctx* c, int root, const ztp_mat* t, int mode, void* stream) {
+  if (!c || !t) return fail(c, ZTP_EINVAL, "ztp_reduce: null argument");
+  if (root < 0 || root >= c->world || (mode != ZTP_COLL_TREE && mode != ZTP_COLL_P2P))
+    return fail(c, ZTP_EINVAL, "ztp_reduce: bad root / mode");
+  if (!mat_ok(*t) || t->ld != t->cols) return fail(c, ZTP_ESHAPE, "ztp_reduce: contiguous tensor needed, " + shp("t", *t));
+  if (c->world == 1) return ZTP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = t->dtype == ZTP_F32 ? 4 : 2;
+  const size_t n = (size_t)(t->rows * t->cols), bytes = n * es;
+  const int pe = prof_begin(c, st, PROF_COMM, 0.0);
+  if (c->transport == ZTP_TRANSPORT_PEER) {
+    int64_t off;
+    ztp_status s = win_offset(c, t->ptr, bytes, "ztp_reduce", &off);
+    if (s != ZTP_OK) return s;
+    if (bytes % 16) return fail(c, ZTP_ESHAPE, "peer reduce: payload must be a multiple of 16 bytes");
+    CUDA_TRY(c, ztp::peer_reduce_launch(c->pw, root, off, (int64_t)bytes, t->dtype == ZTP_F32, c->peer_ctas, st));
+    ++c->launches;
+  } else if (mode == ZTP_COLL_TREE) {
+    NCCL_TRY(c, ncclReduce(t->ptr, t->ptr, n, nccl_type(t->dtype), ncclSum, root, c->comm, st));
+  } else {
+    // gather every rank's tensor into the root's workspace, then the root
+    // sums them in rank order (its own copy included) into t
+    if (c->rank == root && ensure_ws(c, bytes * c->world) != ZTP_OK) return ZTP_ECUDA;
+    char* ws = (char*)c->ws;
+    if (c->rank == root)
+      CUDA_TRY(c, cudaMemcpyAsync(ws + (size_t)root * bytes, t->ptr, bytes, cudaMemcpyDeviceToDevice, st));
+    NCCL_TRY(c, ncclGroupStart());
+    if (c->rank == root) {
+      for (int q = 0; q < c->world; ++q)
+        if (q != root) NCCL_TRY(c, ncclRecv(ws + (size_t)q * bytes, n, nccl_type(t->dtype), q, c->comm, st));
+    } else {
+      NCCL_TRY(c, ncclSend(t->ptr, n, nccl_type(t->dtype), root, c->comm, st));
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+    if (c->rank == root) {
+      CUDA_TRY(c, ztp::accumulate_launch(t->ptr, t->cols, ws, t->cols, t->rows, t->cols, t->dtype, c->world, t->rows,
+                                         1, st));
+      ++c->launches;
+    }
+  }
+  prof_end(c, pe, st);
+  return ZTP_OK;
+}
+
+ztp_status ztp_allreduce(ztp_ctx* c, const ztp_mat* t, void* stream) {
+  if (!c || !t) return fail(c, ZTP_EINVAL, "ztp_allreduce: null argument");
+  if (!mat_ok(*t)) return fail(c, ZTP_ESHAPE, "ztp_allreduce: bad " + shp("t", *t));
+  return allreduce(c, *t, (cudaStream_t)stream);
+}
+
+ztp_status ztp_accumulate(ztp_ctx* c, const ztp_mat* dst, const ztp_mat* src, void* stream) {
+  if (!c || !dst || !src) return fail(c, ZTP_EINVAL, "ztp_accumulate: null argument");
+  if (!mat_ok(*dst) || !mat_ok(*src) || dst->rows != src->rows || dst->cols != src->cols || dst->dtype != src->dtype)
+    return fail(c, ZTP_ESHAPE, "ztp_accumulate: " + shp("dst", *dst) + " vs " + shp("src", *src));
+  CUDA_TRY(c, ztp::accumulate_launch(dst->ptr, dst->ld, src->ptr, src->ld, dst->rows, dst->cols, dst->dtype, 1, 0, 0,
+                                     (cudaStream_t)stream));
+  ++c->launches;
+  return ZTP_OK;
+}
+
 ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
   if (!c) return fail(c, ZTP_EINVAL, "ztp_set_option: null ctx");
   if (!std::isfinite(v)) return fail(c, ZTP_EINVAL, "ztp_set_option: value must be finite");

@@ -230,6 +230,12 @@ struct PeerPulls {
   PeerPull x[PEER_MAX_PULLS];
 };
 cudaError_t peer_allreduce_launch(const PeerWin& w, int64_t off, int64_t bytes, int f32, int nctas, cudaStream_t st);
+cudaError_t peer_bcast_launch(const PeerWin& w, int root, int64_t off, int64_t bytes, int nctas, cudaStream_t st);
+cudaError_t peer_reduce_launch(const PeerWin& w, int root, int64_t off, int64_t bytes, int f32, int nctas,
+                               cudaStream_t st);
+// dst += src (bf16 / f32 rows, fp32 add) and dst = sum of `nparts` row blocks of src (rank order)
+cudaError_t accumulate_launch(void* dst, int64_t ld_dst, const void* src, int64_t ld_src, int64_t rows, int64_t cols,
+                              int dtype, int nparts, int64_t part_stride, int overwrite, cudaStream_t st);
 cudaError_t peer_allgather_launch(const PeerWin& w, int64_t off, int64_t blk_bytes, int nctas, cudaStream_t st);
 cudaError_t peer_pull_launch(const PeerWin& w, const PeerPulls& p, int nctas, cudaStream_t st);
 cudaError_t peer_stats_launch(const PeerWin& w, double T, double M, cudaStream_t st);

@@ -419,6 +419,25 @@ __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return
 template <>
 __device__ __forceinline__ float from_f<float>(float v) { return v; }
 
+// Local reduce (NEXT-3 migration: a helper's migrated contribution merged
+// into its partial before the all-reduce; the root's sum of gathered
+// partials): dst[r, c] (+)= sum_{q < nparts} src[q * part_stride + r, c], the
+// parts added in order q = 0.. in fp32, one rounding.
+template <typename T>
+__global__ void __launch_bounds__(256) ztp_accumulate(T* dst, int64_t ld_dst, const T* src, int64_t ld_src,
+                                                      int64_t rows, int64_t cols, int nparts, int64_t part_stride,
+                                                      int overwrite) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    float a = overwrite ? 0.f : to_f<T>(dst[r * ld_dst + c]);
+    for (int q = 0; q < nparts; ++q) a += to_f<T>(src[(q * part_stride + r) * ld_src + c]);
+    dst[r * ld_dst + c] = from_f<T>(a);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) ztp_impute_average(T* out, int64_t ld, int64_t cols, const int32_t* kept, int nk,
                                                           const int32_t* pruned, int np) {
@@ -645,4 +664,18 @@ cudaError_t gemm_f32_launch(const GemmParamsF32& p, cudaStream_t st) {
   return launch_k(ztp_gemm_f32_kernel, grid, 256, 0, st, p);
 }
 
+}  // namespace ztp
+
+namespace ztp {
+cudaError_t accumulate_launch(void* dst, int64_t ld_dst, const void* src, int64_t ld_src, int64_t rows, int64_t cols,
+                              int dtype, int nparts, int64_t part_stride, int overwrite, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  const int64_t total = rows * cols;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)148 * 16);
+  if (dtype == 0)
+    return launch_k(ztp_accumulate<__nv_bfloat16>, blocks, 256, 0, st, (__nv_bfloat16*)dst, ld_dst,
+                    (const __nv_bfloat16*)src, ld_src, rows, cols, nparts, part_stride, overwrite);
+  return launch_k(ztp_accumulate<float>, blocks, 256, 0, st, (float*)dst, ld_dst, (const float*)src, ld_src, rows,
+                  cols, nparts, part_stride, overwrite);
+}
 }  // namespace ztp

@@ -156,6 +156,57 @@ __global__ void __launch_bounds__(512) ztp_peer_allgather(const PeerWin w, int64
   pdl_trigger();
 }
 
+// broadcast from `root`: every other rank pulls root's tensor (nvec 16-byte
+// vectors at window offset `off`) into its own copy
+__global__ void __launch_bounds__(512) ztp_peer_bcast(const PeerWin w, int root, int64_t off, int64_t nvec) {
+  pdl_wait();
+  const int b = blockIdx.x, nb = gridDim.x;
+  peer_barrier(w, b);                       // root's tensor is final
+  if (w.rank != root) {
+    const int4* src = reinterpret_cast<const int4*>(w.base[root] + off);
+    int4* dst = reinterpret_cast<int4*>(w.base[w.rank] + off);
+    for (int64_t i = (int64_t)b * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)nb * blockDim.x)
+      dst[i] = ld_cg(src + i);
+  }
+  peer_barrier(w, b);                       // the root's copy is not reused while a peer reads it
+  pdl_trigger();
+}
+
+// reduce (sum) to `root`: root sums every rank's tensor in rank order 0..e-1
+// in fp32 (the oracle's left fold) into its own copy
+template <bool F32>
+__global__ void __launch_bounds__(512) ztp_peer_reduce(const PeerWin w, int root, int64_t off, int64_t nvec) {
+  pdl_wait();
+  const int b = blockIdx.x, nb = gridDim.x;
+  peer_barrier(w, b);                       // every rank's partial is complete
+  if (w.rank == root) {
+    int4* mine = reinterpret_cast<int4*>(w.base[root] + off);
+    for (int64_t i = (int64_t)b * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)nb * blockDim.x) {
+      if constexpr (F32) {
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int q = 0; q < w.world; ++q) {
+          const int4 x = ld_cg(reinterpret_cast<const int4*>(w.base[q] + off) + i);
+          const float* f = reinterpret_cast<const float*>(&x);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) a[k] += f[k];
+        }
+        int4 o;
+        float* fo = reinterpret_cast<float*>(&o);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fo[k] = a[k];
+        mine[i] = o;
+      } else {
+        Bf16x8Acc acc;
+        acc.zero();
+        for (int q = 0; q < w.world; ++q) acc.add(ld_cg(reinterpret_cast<const int4*>(w.base[q] + off) + i));
+        mine[i] = acc.pack();
+      }
+    }
+  }
+  peer_barrier(w, b);                       // no rank overwrites its partial while the root reads it
+  pdl_trigger();
+}
+
 // one-sided pulls of shard slices (ztp_migrate): every transfer whose
 // destination is this rank reads the source rank's window at the source's
 // symmetric offset; one warp per destination row.
@@ -214,6 +265,14 @@ cudaError_t peer_allreduce_launch(const PeerWin& w, int64_t off, int64_t bytes, 
 }
 cudaError_t peer_allgather_launch(const PeerWin& w, int64_t off, int64_t blk_bytes, int nctas, cudaStream_t st) {
   return launch_k(ztp_peer_allgather, nctas, 512, 0, st, w, off, blk_bytes / 16);
+}
+cudaError_t peer_bcast_launch(const PeerWin& w, int root, int64_t off, int64_t bytes, int nctas, cudaStream_t st) {
+  return launch_k(ztp_peer_bcast, nctas, 512, 0, st, w, root, off, bytes / 16);
+}
+cudaError_t peer_reduce_launch(const PeerWin& w, int root, int64_t off, int64_t bytes, int f32, int nctas,
+                               cudaStream_t st) {
+  if (f32) return launch_k(ztp_peer_reduce<true>, nctas, 512, 0, st, w, root, off, bytes / 16);
+  return launch_k(ztp_peer_reduce<false>, nctas, 512, 0, st, w, root, off, bytes / 16);
 }
 cudaError_t peer_pull_launch(const PeerWin& w, const PeerPulls& p, int nctas, cudaStream_t st) {
   return launch_k(ztp_peer_pull, nctas, 256, 0, st, w, p);

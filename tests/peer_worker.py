@@ -135,6 +135,33 @@ def main():
                 g.replay()
             Z.ztp_sync(ctx, st)
             res.update(Y_graph=host(L.Y), dX_graph=host(L.dX), dw1_graph=host(L.dw1[:, :u]))
+    elif case == "kmig":
+        # paper-literal K-dim migration of a column linear (NEXT-3): ranks in
+        # PEER_MIGRATORS shed k contraction rows each, both policies
+        from paper_2401_11469_b200.kmig import KMigColLinear
+        K, n, N, seed = 256, 64, 136, 77
+        migr = [int(v) for v in os.environ["PEER_MIGRATORS"].split(",")]
+        k = int(os.environ["PEER_K"])
+        mode = {"tree": Z.COLL_TREE, "p2p": Z.COLL_P2P}[os.environ["PEER_MODE"]]
+        open_window(16 << 20)
+        Lk = KMigColLinear(ctx, rank, world, K, n, N, migr, k, mode, alloc=sym_allocator(ctx))
+        Lk.X.copy_(dev(I.normal(seed, "x", K, N)))
+        Lk.W.copy_(dev(I.uniform_sym(seed, "w", K, world * n, 0.1, c0=rank * n, c1=(rank + 1) * n)))
+        Lk.G.copy_(dev(I.normal(seed, "g", world * n, N, r0=rank * n, r1=(rank + 1) * n)))
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            Lk.step(st)
+            Z.ztp_sync(ctx, st)
+            res.update(Y=host(Lk.output()), dX=host(Lk.dX), dW=host(Lk.dW))
+            # replayed as a CUDA graph
+            Lk.dX.zero_()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                Lk.step(st)
+            for _ in range(2):
+                g.replay()
+            Z.ztp_sync(ctx, st)
+            res.update(Y_graph=host(Lk.output()), dX_graph=host(Lk.dX), dW_graph=host(Lk.dW))
     else:
         raise SystemExit(f"unknown case {case}")
     np.savez(os.path.join(out, f"{case}_{rank}.npz"), **res)

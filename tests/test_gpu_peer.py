@@ -142,3 +142,31 @@ def test_peer_layer_step_semi(tmp_path, world, mig, gamma):
         P = sel[s][sg][1]
         if len(P):
             assert np.all(res[s][key][np.asarray(P)][:, :cols] == 0), sg
+
+
+@pytest.mark.parametrize("world,migr,k,mode", [
+    (3, "2", 96, "tree"), (3, "2", 96, "p2p"),        # one migrating rank, two helpers
+    (4, "1,3", 130, "tree"), (4, "1,3", 250, "p2p"),  # nu = 2, ragged helper ranges
+])
+def test_peer_kdim_migration_lossless(tmp_path, world, migr, k, mode):
+    """NEXT-3, the paper-literal sending-collecting migration of a column
+    linear: migrating ranks shed k contraction rows to the normal
+    ranks; outputs, dX (helpers' rows merged into the all-reduce) and
+    every rank's dW (returned slices) equal the unsplit linear (P:233
+    loss-free), eager and graph-replayed, under both policies."""
+    res = run_ranks(world, "kmig", tmp_path, env={"PEER_MIGRATORS": migr, "PEER_K": str(k), "PEER_MODE": mode})
+    K, n, N, seed = 256, 64, 136, 77
+    X = I.normal(seed, "x", K, N)
+    W = I.uniform_sym(seed, "w", K, world * n, 0.1)
+    G = I.normal(seed, "g", world * n, N)
+    dX = O.fold([O.linear_bwd_dx(W[:, r * n:(r + 1) * n], G[r * n:(r + 1) * n]) for r in range(world)])
+
+    def close(got, want, name):
+        err = np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-30)
+        assert np.isfinite(got).all() and err <= TOL, f"{name}: {err:.3e}"
+    for r in range(world):
+        Wr, Gr = W[:, r * n:(r + 1) * n], G[r * n:(r + 1) * n]
+        for sfx in ("", "_graph"):
+            close(res[r]["Y" + sfx], O.linear_fwd(Wr, X), f"Y{sfx}[{r}]")
+            close(res[r]["dX" + sfx], dX, f"dX{sfx}[{r}]")
+            close(res[r]["dW" + sfx], O.linear_bwd_dw(X, Gr), f"dW{sfx}[{r}]")
