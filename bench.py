@@ -305,7 +305,7 @@ class Case:
     """One config at TP = D.world on this rank: a context (+ symmetric window
     at N > 1), the rank's layer stack, graphs and timings."""
 
-    def __init__(self, D, args, cfg, semi: bool, stream):
+    def __init__(self, D, args, cfg, semi: bool, stream, cap_units: float = 1.0):
         import torch
         import paper_2401_11469_b200 as Z
         from paper_2401_11469_b200.layer import ZtpLayer, ZtpStack, sym_allocator
@@ -320,7 +320,9 @@ class Case:
         uid = Z.ztp_get_unique_id() if (use_nccl and r == 0) else None
         uid = D.bcast_obj(uid) if use_nccl else None
         self.ctx = Z.ztp_ctx_create(r, e, uid, D.device)
-        self.cap = self.u if semi else 0
+        # receive capacity (MLP units) for migrated work: one straggler's whole
+        # shard by default; forced plans (lambda sweep) can pile more on a rank
+        self.cap = int(self.u * cap_units) if semi else 0
         nl = cfg.layers
         alloc = None
         if e > 1:
@@ -531,6 +533,41 @@ def table1(D, args, stream):
                                         "broadcast-reduce(4)": 1113 / 373, "scatter-gather(4)": 1436 / 373}}
 
 
+def lambda_sweep(D, args, stream):
+    """NEXT-4's multi-straggler study: c4 at TP = 8
+    with ranks 1, 3, 5, 7 slowed x8, x6, x4, x2 (the paper's setting), one
+    statistics window, then the plan with Eq.3's migration bound forced to
+    lambda = 0 .. 4 (force_lambda; lambda = 0 is ZERO for all four
+    stragglers, lambda = 4 migration for all), each applied and timed; the
+    automatic Eq.3 choice alongside."""
+    import paper_2401_11469_b200 as Z
+    from synth.configs import CONFIGS
+    e = D.world
+    C = Case(D, args, CONFIGS["c4"], True, stream, cap_units=2.0)
+    chis = [1.0] * e
+    for q, c in zip((1, 3, 5, 7), (8.0, 6.0, 4.0, 2.0)):
+        if q < e:
+            chis[q] = c
+    C.set_chi(1.0)
+    t_free = C.run(30, 3)
+    costs, cplain = C.costs()
+    C.set_chi(chis[D.rank])
+    t_unbal = C.run(20, 3)
+    T, M = C.stats_window()
+    rows = []
+    for lam in (-1, 0, 1, 2, 3, 4):
+        opts = Z.plan_opts(enable_migration=1, zero_crit=Z.CRIT_MIN, eps=args.eps, force_lambda=lam)
+        plan = Z.ztp_plan(T, M, float(C.u), costs, opts)
+        C.apply(plan)
+        ms = C.run(20, 3)
+        rows.append({"lambda": "auto (Eq.3)" if lam < 0 else lam, "x": int(plan.x), "ms": ms,
+                     "recovery": t_free / ms, "speedup": t_unbal / ms, "plan": plan_summary(plan, e)})
+    C.destroy()
+    return {"workload": f"c4 at TP={e}, ranks 1,3,5,7 (those < TP) slowed x8,x6,x4,x2", "T_free_ms": t_free,
+            "T_unbal_ms": t_unbal,
+            "window_T_ms": T, "rows": rows, "pretest_costs": cplain}
+
+
 def plan_summary(plan, e):
     if plan is None:
         return {"roles": "N" * e}
@@ -616,6 +653,8 @@ def main():
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"])
     ap.add_argument("--share-gpu", action="store_true", help="N>1 on one GPU (path validation only)")
     ap.add_argument("--no-matrix", action="store_true")
+    ap.add_argument("--extras", default="all", choices=["all", "table1", "lambda", "none"],
+                    help="N>1 extras: Table I analog, forced-lambda sweep (N=8)")
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -781,7 +820,7 @@ def main():
     matrix = []
     C.destroy()
     if e > 1 and not args.no_matrix:
-        for mc in matrix_cases(e):
+        for mc in (matrix_cases(e) if args.extras == "all" else []):
             mcfg = CONFIGS[mc["cfg"]]
             M = Case(D, args, mcfg, mc["semi"], stream)
             if mc.get("schedule") == "c5":
@@ -792,7 +831,10 @@ def main():
             matrix.append(case_summary(M, mc["name"], res, peak_burst))
             M.destroy()
             torch.cuda.empty_cache()
-        extra["table1"] = table1(D, args, stream)
+        if args.extras in ("all", "table1"):
+            extra["table1"] = table1(D, args, stream)
+        if (e == 8 and args.extras == "all") or args.extras == "lambda":
+            extra["lambda_sweep"] = lambda_sweep(D, args, stream)
         torch.cuda.empty_cache()
     h2d = 2 * h * N * 2
     d2h = h * N * 2
