@@ -770,7 +770,64 @@ def dense_layer_step(Xt, Gt, WQt, WKt, WVt, WOt, W1t, W2t, blocks: int = 1):
                 dWOt=dWOt, dW1t=dW1t, dW2t=dW2t)
 
 
-def layer_step(Xt, Gt, sh: LayerShards, sel=None, mig=None, merged=True, policy="zero"):
+@dataclass
+class AttnCore:
+    """The real attention core (NEXT-4; A-31's stand-in replaced): per rank
+    heads = a / head_dim, tokens t = b * seq + s (batch-major), softmax
+    attention per (batch, head) with scale 1/sqrt(head_dim), causal or not."""
+    head_dim: int
+    seq: int
+    causal: bool = True
+
+
+def attention_fwd(Qt, Kt, Vt, core: AttnCore):
+    """ctx^T = per (batch, head): softmax(Q K^T / sqrt(d) [+ causal mask]) V,
+    written out per query row in fp64 (feature-major [a, N] in and out).
+    Returns ctx^T and the probabilities P[b][h] for the backward."""
+    a, N = Qt.shape
+    d, S = core.head_dim, core.seq
+    H, B = a // d, N // S
+    ctx = np.zeros((a, N))
+    probs = {}
+    for b in range(B):
+        cols = slice(b * S, (b + 1) * S)
+        for hh in range(H):
+            rows = slice(hh * d, (hh + 1) * d)
+            q, k, v = Qt[rows, cols].T, Kt[rows, cols].T, Vt[rows, cols].T        # [S, d]
+            sc = (q @ k.T) / math.sqrt(d)
+            if core.causal:
+                sc = np.where(np.tril(np.ones((S, S), dtype=bool)), sc, -np.inf)
+            m = sc.max(axis=1, keepdims=True)
+            ex = np.exp(sc - m)
+            P = ex / ex.sum(axis=1, keepdims=True)
+            probs[(b, hh)] = P
+            ctx[rows, cols] = (P @ v).T
+    return ctx, probs
+
+
+def attention_bwd(Qt, Kt, Vt, dctx, probs, core: AttnCore):
+    """Gradients of attention_fwd: dV = P^T dO, dP = dO V^T,
+    dS = P * (dP - rowsum(dP * P)), dQ = dS K / sqrt(d), dK = dS^T Q / sqrt(d)."""
+    a, N = Qt.shape
+    d, S = core.head_dim, core.seq
+    H, B = a // d, N // S
+    dQ, dK, dV = np.zeros((a, N)), np.zeros((a, N)), np.zeros((a, N))
+    for b in range(B):
+        cols = slice(b * S, (b + 1) * S)
+        for hh in range(H):
+            rows = slice(hh * d, (hh + 1) * d)
+            q, k, v, do = Qt[rows, cols].T, Kt[rows, cols].T, Vt[rows, cols].T, dctx[rows, cols].T
+            P = probs[(b, hh)]
+            dv = P.T @ do
+            dp = do @ v.T
+            ds = P * (dp - (dp * P).sum(axis=1, keepdims=True))
+            dQ[rows, cols] = (ds @ k / math.sqrt(d)).T
+            dK[rows, cols] = (ds.T @ q / math.sqrt(d)).T
+            dV[rows, cols] = dv.T
+    return dQ, dK, dV
+
+
+def layer_step(Xt, Gt, sh: LayerShards, sel=None, mig=None, merged=True, policy="zero", core=None):
     """One TP layer step (fwd + bwd) simulated for all e ranks in-process.
 
     sel[r][seg] = (S, P) per segment (None = dense) -- the lineage table
@@ -808,12 +865,17 @@ def layer_step(Xt, Gt, sh: LayerShards, sel=None, mig=None, merged=True, policy=
         own_hi[s] = min(own_hi[s], lo)
     # ---------------- forward: attention-projection block -------------------
     ctx = []
+    attn_saved = []
     y1_parts = []
     for r in range(e):
         S, _ = S_of(r, "qkv")
         qkv = linear_fwd(sh.qkv_t[r], Xt, S)
         flops[r] += 2.0 * qkv.shape[0] * N * kept_count(r, "qkv", h)
-        c = (qkv[:a] + qkv[a:2 * a]) + qkv[2 * a:]
+        if core is None:
+            c = (qkv[:a] + qkv[a:2 * a]) + qkv[2 * a:]          # stand-in core (A-31)
+        else:
+            c, pr = attention_fwd(qkv[:a], qkv[a:2 * a], qkv[2 * a:], core)
+            attn_saved.append((qkv, pr))
         ctx.append(c)
         So, _ = S_of(r, "o")
         y1_parts.append(linear_fwd(sh.o_t[r], c, So))
@@ -898,7 +960,11 @@ def layer_step(Xt, Gt, sh: LayerShards, sel=None, mig=None, merged=True, policy=
         dctx = linear_bwd_dx(sh.o_t[r], dY1, So, Po, policy)
         dWo[r] = linear_bwd_dw(ctx[r], dY1, So, Po, policy)
         flops[r] += 2.0 * 2.0 * kept_count(r, "o", a) * h * N
-        gq = np.concatenate([dctx, dctx, dctx], axis=0)       # core bwd: dQ=dK=dV=dctx
+        if core is None:
+            gq = np.concatenate([dctx, dctx, dctx], axis=0)   # stand-in core bwd: dQ=dK=dV=dctx
+        else:
+            qkv_r, pr = attn_saved[r]
+            gq = np.concatenate(attention_bwd(qkv_r[:a], qkv_r[a:2 * a], qkv_r[2 * a:], dctx, pr, core), axis=0)
         S, P = S_of(r, "qkv")
         dx_parts.append(linear_bwd_dx(sh.qkv_t[r], gq, S, P, policy))
         dWqkv[r] = linear_bwd_dw(Xt, gq, S, P, policy)

@@ -326,3 +326,58 @@ def test_synth_shards_concatenate_to_dense():
     z = I.normal(5, "x", 6, 10)
     assert np.array_equal(I.normal(5, "x", 6, 10, r0=2, r1=5), z[2:5])
     assert np.array_equal(I.round_bf16(z), z)
+
+
+# ------------------------------------------------- real attention core (NEXT-4)
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_attention_core_closed_forms(causal):
+    """Q = 0 makes every allowed score equal: each query's output is the plain
+    mean of V over the keys it may see -- the prefix mean (causal) or the
+    sequence mean -- per batch and head; one-token sequences return V."""
+    d, S, B, H = 4, 5, 2, 2
+    core = O.AttnCore(head_dim=d, seq=S, causal=causal)
+    V = _rand((H * d, B * S), 3)
+    ctx, P = O.attention_fwd(np.zeros((H * d, B * S)), _rand((H * d, B * S), 4), V, core)
+    for b in range(B):
+        for i in range(S):
+            lo, hi = b * S, b * S + (i + 1 if causal else S)
+            np.testing.assert_allclose(ctx[:, b * S + i], V[:, lo:hi].mean(axis=1), rtol=0, atol=1e-15)
+    for p in P.values():
+        np.testing.assert_allclose(p.sum(axis=1), 1.0, rtol=0, atol=1e-15)
+        if causal:
+            assert np.all(np.triu(p, 1) == 0.0)
+    one = O.AttnCore(head_dim=d, seq=1, causal=causal)
+    Q1, K1, V1 = _rand((H * d, 3), 5), _rand((H * d, 3), 6), _rand((H * d, 3), 7)
+    np.testing.assert_allclose(O.attention_fwd(Q1, K1, V1, one)[0], V1, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("mode", ["dense", "pruned"])
+def test_attention_layer_gradient_check(mode):
+    """The layer with the real attention core: analytic gradients of every
+    weight and of X vs central differences (S:248/S:301 protocol)."""
+    e, h, f, N = 2, 8, 16, 6
+    core = O.AttnCore(head_dim=2, seq=3, causal=True)
+    Xt, Gt, W, sh = _make(e, h, f, N, seed=13)
+    sel = _random_sel(e, h, f, 8) if mode == "pruned" else None
+    out = O.layer_step(Xt, Gt, sh, sel, core=core)
+    loss = lambda: float(np.sum(O.layer_step(Xt, Gt, sh, sel, core=core)["Y"] * Gt))  # noqa: E731
+    rng = random.Random(17)
+    step = 1e-5
+    for _ in range(24):
+        which = rng.choice(["qkv", "o", "w1", "w2", "x"])
+        r = rng.randrange(e)
+        if which == "x":
+            arr, grad = Xt, out["dX"]
+        else:
+            arr = {"qkv": sh.qkv_t, "o": sh.o_t, "w1": sh.w1_t, "w2": sh.w2_t}[which][r]
+            grad = {"qkv": out["dWqkv"], "o": out["dWo"], "w1": out["dW1"], "w2": out["dW2"]}[which][r]
+        i, j = rng.randrange(arr.shape[0]), rng.randrange(arr.shape[1])
+        old = arr[i, j]
+        arr[i, j] = old + step
+        lp = loss()
+        arr[i, j] = old - step
+        lm = loss()
+        arr[i, j] = old
+        fd = (lp - lm) / (2 * step)
+        assert abs(fd - grad[i, j]) <= 1e-5 * max(1.0, abs(grad[i, j])), (which, r, i, j, fd, grad[i, j])
