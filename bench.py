@@ -346,7 +346,11 @@ class Case:
                        "w1": (torch.rand(h, u, device="cuda", generator=gen) * 2 - 1) * h ** -0.5,
                        "w2": (torch.rand(u, h, device="cuda", generator=gen) * 2 - 1) * f ** -0.5}
                 dev = {k: v.to(torch.bfloat16) for k, v in dev.items()}
-            L = ZtpLayer(self.ctx, h, f, N, r, e, dev, mig_cap=self.cap, layer_id=li, alloc=alloc)
+            attn = None
+            if getattr(args, "attention", "standin") == "real":
+                from paper_2401_11469_b200.layer import AttnSpec
+                attn = AttnSpec(cfg.head_dim, cfg.seq, cfg.causal)
+            L = ZtpLayer(self.ctx, h, f, N, r, e, dev, mig_cap=self.cap, layer_id=li, alloc=alloc, attn=attn)
             if li == 0:
                 L.X.copy_(torch.from_numpy(I.normal(cfg.seed, "x", h, N).astype(np.float32)).cuda().to(torch.bfloat16))
                 L.G.copy_(torch.from_numpy(I.normal(cfg.seed, "g", h, N).astype(np.float32)).cuda().to(torch.bfloat16))
@@ -653,6 +657,8 @@ def main():
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"])
     ap.add_argument("--share-gpu", action="store_true", help="N>1 on one GPU (path validation only)")
     ap.add_argument("--no-matrix", action="store_true")
+    ap.add_argument("--attention", default="standin", choices=["standin", "real"],
+                    help="attention core: A-31's stand-in (default) or real fused attention (NEXT-4)")
     ap.add_argument("--extras", default="all", choices=["all", "table1", "lambda", "none"],
                     help="N>1 extras: Table I analog, forced-lambda sweep (N=8)")
     ap.add_argument("--ref-tokens", type=int, default=256)
@@ -847,6 +853,8 @@ def main():
                    "mode": ("homogeneous ZERO-Pri gamma=%.2f" % args.gamma) if e == 1 else
                            f"rank {e - 1} slowed {args.chi}x, ZERO-resizing (T_min), ztp_ctl_step controller",
                    "selection": "ztp_select once per plan (P:187 epoch granularity), not in the step",
+                   "attention_core": ("real: cuDNN fused attention (torch SDPA) between ztp_transpose layout changes"
+                                      if args.attention == "real" else "stand-in ctx = Q + K + V (A-31)"),
                    "l2": "no flush: per-step working set > 126 MB L2 (activations ~%d MB)" %
                          int((2 * h * N * 2 * 6 + 2 * (f // e) * N * 2 * 2) / 1e6)},
         "method_tflops": flops_method / (ms_bal * 1e-3) / 1e12,

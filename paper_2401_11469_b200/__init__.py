@@ -374,6 +374,15 @@ def ztp_allreduce(ctx, t, stream=None) -> None:
     check(lib.ztp_allreduce(ctx, C.byref(m), _stream(stream)), ctx)
 
 
+def ztp_transpose(ctx, src, dst, cols=None, n: Optional[int] = None, stream=None) -> None:
+    """dst[i, r] = src[r, cols[i] if cols is not None else i] for i < n."""
+    s_, d = mat(src), mat(dst)
+    if n is None:
+        n = int(cols.numel()) if cols is not None else src.shape[1]
+    check(lib.ztp_transpose(ctx, C.byref(s_), C.byref(d), cols.data_ptr() if cols is not None else None, n,
+                            _stream(stream)), ctx)
+
+
 def ztp_set_option(ctx, opt: int, value: float) -> None:
     check(lib.ztp_set_option(ctx, int(opt), float(value)), ctx)
 

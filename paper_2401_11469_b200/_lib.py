@@ -170,6 +170,7 @@ def _load():
         "ztp_reduce": (st, [vp, C.c_int, C.POINTER(Mat), C.c_int, vp]),
         "ztp_accumulate": (st, [vp, C.POINTER(Mat), C.POINTER(Mat), vp]),
         "ztp_allreduce": (st, [vp, C.POINTER(Mat), vp]),
+        "ztp_transpose": (st, [vp, C.POINTER(Mat), C.POINTER(Mat), vp, C.c_int64, vp]),
         "ztp_get_option": (st, [vp, C.c_int, C.POINTER(C.c_double)]),
         "ztp_read_profile": (st, [vp, vp, C.POINTER(Profile)]),
     }
@@ -191,7 +192,7 @@ EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_i
             "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",
             "ztp_set_profile", "ztp_read_profile", "ztp_window_create", "ztp_window_open", "ztp_sym_alloc",
             "ztp_set_transport", "ztp_barrier", "ztp_set_option", "ztp_get_option", "ztp_broadcast", "ztp_reduce",
-            "ztp_accumulate", "ztp_allreduce")
+            "ztp_accumulate", "ztp_allreduce", "ztp_transpose")
 
 
 def check(code: int, ctx=None):

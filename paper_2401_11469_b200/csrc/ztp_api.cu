@@ -1672,6 +1672,20 @@ ztp_status ztp_accumulate(ztp_ctx* c, const ztp_mat* dst, const ztp_mat* src, vo
   return ZTP_OK;
 }
 
+ztp_status ztp_transpose(ztp_ctx* c, const ztp_mat* src, const ztp_mat* dst, const int32_t* cols, int64_t n,
+                         void* stream) {
+  if (!c || !src || !dst) return fail(c, ZTP_EINVAL, "ztp_transpose: null argument");
+  if (!mat_ok(*src) || !mat_ok(*dst) || src->dtype != ZTP_BF16 || dst->dtype != ZTP_BF16 || n < 0 ||
+      dst->rows < n || dst->cols < src->rows || (!cols && n > src->cols))
+    return fail(c, ZTP_ESHAPE, "ztp_transpose: " + shp("src", *src) + " -> " + shp("dst", *dst) + " n " +
+                                   std::to_string(n));
+  const int pe = prof_begin(c, (cudaStream_t)stream, PROF_OTHER, 0.0);
+  CUDA_TRY(c, ztp::transpose_launch(src->ptr, src->ld, src->rows, cols, n, dst->ptr, dst->ld, (cudaStream_t)stream));
+  prof_end(c, pe, (cudaStream_t)stream);
+  ++c->launches;
+  return ZTP_OK;
+}
+
 ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
   if (!c) return fail(c, ZTP_EINVAL, "ztp_set_option: null ctx");
   if (!std::isfinite(v)) return fail(c, ZTP_EINVAL, "ztp_set_option: value must be finite");

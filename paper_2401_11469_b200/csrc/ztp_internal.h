@@ -202,6 +202,9 @@ cudaError_t priority_update_launch(const void* w, int64_t ld_w, const void* w_ol
 // out-of-place column spread: dst[r, j] = pos[j] >= 0 ? src[r, pos[j]] : 0, r < n, j < n_full
 cudaError_t expand_cols_launch(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int n, const int32_t* pos,
                                int n_full, cudaStream_t st);
+// dst[i, r] = src[r, cols ? cols[i] : i], i < n, r < R (16-bit elements)
+cudaError_t transpose_launch(const void* src, int64_t ld_src, int64_t R, const int32_t* cols, int64_t n, void* dst,
+                             int64_t ld_dst, cudaStream_t st);
 cudaError_t fill_rows_launch(void* out, int64_t ld, const int32_t* rows, int nrows, int64_t cols, int dtype,
                              cudaStream_t st);
 

@@ -679,3 +679,39 @@ cudaError_t accumulate_launch(void* dst, int64_t ld_dst, const void* src, int64_
                   cols, nparts, part_stride, overwrite);
 }
 }  // namespace ztp
+
+namespace ztp {
+// Transpose with column selection (the real attention core's layout changes,
+// NEXT-4): dst[i, r] = src[r, cols ? cols[i] : i] for i < n, r < R.  32 x 32
+// tiles through shared memory (+1 padding: conflict-free), 16-bit elements,
+// coalesced reads along src rows and writes along dst rows.
+__global__ void __launch_bounds__(256) ztp_transpose_k(const uint16_t* __restrict__ src, int64_t ld_src, int64_t R,
+                                                       const int32_t* __restrict__ cols, int64_t n,
+                                                       uint16_t* __restrict__ dst, int64_t ld_dst) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint16_t tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 8 rows of 32 lanes
+  const int64_t i = i0 + tx;
+  const int64_t c = i < n ? (cols ? (int64_t)__ldg(cols + i) : i) : -1;
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t r = r0 + k;
+    tile[k][tx] = (r < R && c >= 0) ? src[r * ld_src + c] : (uint16_t)0;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t di = i0 + k, r = r0 + tx;
+    if (di < n && r < R) dst[di * ld_dst + r] = tile[tx][k];
+  }
+}
+
+cudaError_t transpose_launch(const void* src, int64_t ld_src, int64_t R, const int32_t* cols, int64_t n, void* dst,
+                             int64_t ld_dst, cudaStream_t st) {
+  if (R <= 0 || n <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((R + 31) / 32));
+  if (grid.y > 65535) return cudaErrorInvalidValue;
+  return launch_k(ztp_transpose_k, grid, 256, 0, st, (const uint16_t*)src, ld_src, R, cols, n, (uint16_t*)dst,
+                  ld_dst);
+}
+}  // namespace ztp

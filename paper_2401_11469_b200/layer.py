@@ -43,10 +43,28 @@ def _buf(r, c, dtype=torch.bfloat16, fill=0.0):
     return t[:, :c]
 
 
+def _on(stream):
+    """torch work on the library's stream (the fused attention core)."""
+    import contextlib
+    return torch.cuda.stream(stream) if isinstance(stream, torch.cuda.Stream) else contextlib.nullcontext()
+
+
 def sym_allocator(ctx, device: int = 0):
     """Allocator of window tensors (ztp_sym_alloc; zero-filled at window
     creation) for ZtpLayer(alloc=...) under the peer transport."""
     return lambda r, c, dtype: Z.ztp_sym_alloc(ctx, r, c, dtype, device)
+
+
+@dataclass
+class AttnSpec:
+    """The real attention core (NEXT-4; replaces A-31's stand-in): heads of
+    head_dim features, tokens t = batch * seq + s, causal or not.  The fused
+    attention itself is cuDNN's (through torch SDPA: a library kernel like
+    cuBLAS, the core being outside the method, A-31); the layout changes
+    around it are libztp's ztp_transpose."""
+    head_dim: int
+    seq: int
+    causal: bool = True
 
 
 @dataclass
@@ -102,7 +120,8 @@ def xfer_specs(mio: MigrationIO, u: int, h: int, grads: bool) -> List[dict]:
 
 class ZtpLayer:
     def __init__(self, ctx, h: int, f: int, N: int, rank: int, world: int, shards: Optional[Dict[str, torch.Tensor]],
-                 mig_cap: int = 0, dtype=torch.bfloat16, layer_id: int = 0, alloc=None, plain: bool = False):
+                 mig_cap: int = 0, dtype=torch.bfloat16, layer_id: int = 0, alloc=None, plain: bool = False,
+                 attn: Optional[AttnSpec] = None):
         """alloc(rows, cols, dtype) -> zero-filled tensor: where the layer's
         buffers live (default torch; `sym_allocator(ctx)` for the peer
         transport, whose all-reduce and migration operands must be window
@@ -120,6 +139,13 @@ class ZtpLayer:
         self.layer_id = layer_id
         self.alloc = alloc
         self.plain = plain or dtype == torch.float32
+        self.attn = attn
+        if attn is not None:
+            if dtype != torch.bfloat16 or (h // world) % attn.head_dim or N % attn.seq:
+                raise ValueError("attention core: bf16, whole heads per rank, whole sequences")
+            # token-major copies for the fused attention ([batch, seq, heads, head_dim])
+            self.QKVt = torch.zeros(N, 3 * (h // world), dtype=dtype, device="cuda")
+            self.dOt = torch.zeros(N, h // world, dtype=dtype, device="cuda")
         a, u, cap = self.a, self.u, mig_cap
         for name, r, c in self.buffer_specs(h, f, N, world, mig_cap):
             setattr(self, name, self._new(r, c))
@@ -196,7 +222,8 @@ class ZtpLayer:
         # selection is a derived segment over the 3a QKV outputs -- Q and K
         # scored +inf (never pruned), V scored like O's inputs -- selected in
         # the same launch, so it is exactly O's (S_o, P_o) shifted by 2a.
-        self.v_prune = self.n_prune["o"] > 0 and os.environ.get("ZTP_V_PRUNE", "1") != "0" and not self.plain
+        self.v_prune = (self.n_prune["o"] > 0 and os.environ.get("ZTP_V_PRUNE", "1") != "0" and not self.plain
+                        and self.attn is None)
         segs = SEGS + (("vo",) if self.v_prune else ())
         if self.v_prune:
             self.seg_len["vo"], self.append["vo"], self.n_prune["vo"] = 3 * self.a, 0, self.n_prune["o"]
@@ -390,7 +417,9 @@ class ZtpLayer:
         c = self.ctx
         self.prepare(stream)
         Z.ztp_col_linear(c, Z.FWD, self.f_qkv, stream)
-        if self.plain:     # ctx at full size, O reads its kept rows through the lineage
+        if self.attn is not None:
+            self._attn_fwd(stream)
+        elif self.plain:   # ctx at full size, O reads its kept rows through the lineage
             Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, None, 0, stream)
         else:              # ctx written compact in O's kept order
             Z.ztp_core(c, Z.FWD, self.QKV, self.ctxC, self.a, self.a, self.S["o"], self.nk["o"], stream,
@@ -407,10 +436,45 @@ class ZtpLayer:
         Z.ztp_row_linear(c, Z.BWD, self.b_fc2, stream)        # dH -> G1 = dH * GeLU'(pre), dW2
         Z.ztp_col_linear(c, Z.BWD, self.b_fc1, stream)        # dY1 (+ all-reduce), dW1
 
+    def _heads(self, t):
+        """[N, k * a] token-major -> k views [batch, heads, seq, head_dim]."""
+        sp = self.attn
+        B, S, H, D = self.N // sp.seq, sp.seq, self.a // sp.head_dim, sp.head_dim
+        k = t.shape[1] // self.a
+        v = t.view(B, S, k, H, D)
+        return [v[:, :, i].transpose(1, 2) for i in range(k)]
+
+    def _attn_fwd(self, stream=None):
+        """Real core FWD: QKV^T -> token-major (ztp_transpose), fused causal /
+        bidirectional attention (cuDNN), output -> ctx^T in O's kept order S_o."""
+        import torch.nn.functional as F
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        c, N, a = self.ctx, self.N, self.a
+        Z.ztp_transpose(c, self.QKV, self.QKVt, None, N, stream)
+        self._qkv_leaf = self.QKVt.detach().requires_grad_(True)
+        q, k, v = self._heads(self._qkv_leaf)
+        with _on(stream), torch.enable_grad(), sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+            self._o = F.scaled_dot_product_attention(q, k, v, is_causal=self.attn.causal)
+            ot = self._o.transpose(1, 2).reshape(N, a)
+        Z.ztp_transpose(c, ot, self.ctxC, self.S["o"], self.nk["o"], stream)
+
+    def _attn_bwd(self, stream=None):
+        """Real core BWD: dctx^T -> token-major dO, the fused attention
+        backward (cuDNN) -> dQKV token-major -> gQKV^T (ztp_transpose)."""
+        c, N = self.ctx, self.N
+        Z.ztp_transpose(c, self.dctx, self.dOt, None, N, stream)
+        do = self._heads(self.dOt)[0]
+        with _on(stream):
+            (dqkv,) = torch.autograd.grad(self._o, self._qkv_leaf, do)
+        Z.ztp_transpose(c, dqkv, self.gQKV, None, 3 * self.a, stream)
+        self._o = self._qkv_leaf = None
+
     def bwd_attn(self, stream=None):
         c = self.ctx
         Z.ztp_row_linear(c, Z.BWD, self.b_o, stream)          # dctx, dWo
-        if self.vsel is not None:
+        if self.attn is not None:
+            self._attn_bwd(stream)
+        elif self.vsel is not None:
             Z.ztp_core(c, Z.BWD, self.gQKV, self.dctx, self.a, self.a, self.S["o"], self.nk["o"], stream,
                        v_compact=True)
         else:

@@ -65,13 +65,13 @@ def tz():
     return torch, Z, ZtpLayer, MigrationIO
 
 
-def build(tz, sh, r, e, h, f, N, cap=0, dtype=None, plain=False):
+def build(tz, sh, r, e, h, f, N, cap=0, dtype=None, plain=False, attn=None):
     torch, Z, ZtpLayer, _ = tz
     dtype = dtype or torch.bfloat16
     ctx = Z.ztp_ctx_create(0, 1, None, 0)
     d = lambda a: to_dev(torch, a, dtype)  # noqa: E731
     L = ZtpLayer(ctx, h, f, N, r, e, {"qkv": d(sh.qkv_t[r]), "o": d(sh.o_t[r]), "w1": d(sh.w1_t[r]),
-                                      "w2": d(sh.w2_t[r])}, mig_cap=cap, dtype=dtype, plain=plain)
+                                      "w2": d(sh.w2_t[r])}, mig_cap=cap, dtype=dtype, plain=plain, attn=attn)
     return ctx, L
 
 
@@ -135,7 +135,7 @@ def test_layer_cuda_graph_replay(tz):
     Z.ztp_ctx_destroy(ctx)
 
 
-def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None, f32=False, plain=False):
+def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None, f32=False, plain=False, attn=None):
     """e ranks on one GPU; the test sums partials where NCCL all-reduces.
     sampled = k: full-size run checked on k token columns (Y, dX) against the
     oracle computed for those columns only (layer_step_sampled).
@@ -157,9 +157,10 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None, f32=False, pl
         cols = np.unique(np.concatenate([np.linspace(0, N - 1, sampled).astype(np.int64), [N - 1]]))
         ref = O.layer_step_sampled(X, G, sh, sel, cols, mig)
     else:
-        ref = O.layer_step(X, G, sh, sel, mig)
+        core = O.AttnCore(attn.head_dim, attn.seq, attn.causal) if attn is not None else None
+        ref = O.layer_step(X, G, sh, sel, mig, core=core)
     cap = max([sum(hi - lo for (_, lo, hi) in inc[r]) for r in range(e)] + [0])
-    ranks = [build(tz, sh, r, e, h, f, N, cap, dt, plain) for r in range(e)]
+    ranks = [build(tz, sh, r, e, h, f, N, cap, dt, plain, attn) for r in range(e)]
     offs = {}
     for r, (ctx, L) in enumerate(ranks):
         off = 0
@@ -425,3 +426,32 @@ def test_layer_plain_bf16_matches_oracle(tz):
     g = _zeros(2)
     g[1] = dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)
     _simulate(tz, 2, 128, 512, 264, g, seed=55, plain=True)
+
+
+@pytest.mark.parametrize("e,causal,gam", [
+    (1, True, [dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)]),
+    (1, False, [dict(qkv=0.0, o=0.0, fc1=0.0, fc2=0.0)]),
+    (2, True, [dict(qkv=0.0, o=0.0, fc1=0.0, fc2=0.0), dict(qkv=0.25, o=0.5, fc1=0.3, fc2=0.25)]),
+])
+def test_layer_real_attention_core(tz, e, causal, gam):
+    """NEXT-4: the layer with the real attention core (ztp_transpose around
+    cuDNN's fused attention; heads whole per rank) vs the oracle's fp64
+    softmax attention -- Y, dX and every dW, resized ranks included."""
+    from paper_2401_11469_b200.layer import AttnSpec
+    _simulate(tz, e, 256, 1024, 256, gam, seed=90 + e, attn=AttnSpec(head_dim=64, seq=64, causal=causal))
+
+
+def test_transpose_with_column_selection(tz):
+    """ztp_transpose: dst[i, r] = src[r, cols[i]] exactly (bf16 moves bits)."""
+    torch, Z, _, _ = tz
+    ctx = Z.ztp_ctx_create(0, 1, None, 0)
+    src = torch.randn(77, 304, device="cuda").bfloat16()[:, :300]     # rows padded to 16 bytes (TMA rule)
+    cols = torch.tensor([299, 0, 5, 17, 150, 151, 64, 33], dtype=torch.int32, device="cuda")
+    dst = torch.zeros(8, 80, device="cuda", dtype=torch.bfloat16)
+    Z.ztp_transpose(ctx, src, dst[:, :77], cols)
+    full = torch.zeros(300, 80, device="cuda", dtype=torch.bfloat16)
+    Z.ztp_transpose(ctx, src, full[:, :77])
+    Z.ztp_sync(ctx)
+    assert torch.equal(dst[:, :77], src[:, cols.long()].t())
+    assert torch.equal(full[:, :77], src.t()) and torch.all(full[:, 77:] == 0)
+    Z.ztp_ctx_destroy(ctx)
