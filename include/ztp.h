@@ -162,6 +162,18 @@ ztp_status ztp_accumulate(ztp_ctx* ctx, const ztp_mat* dst, const ztp_mat* src, 
 ztp_status ztp_allreduce(ztp_ctx* ctx, const ztp_mat* t, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Layout change for a token-major library kernel (the real attention core,
+ * NEXT-4, runs cuDNN fused attention on [batch, seq, heads, head_dim]):
+ *   dst[i, r] = src[r, cols ? cols[i] : i]   for i < n, r < src->rows
+ * src [R, C], dst [>= n, >= R], bf16; cols (device, nullable) selects and
+ * orders the source columns (e.g. the O projection's kept features S_o, so
+ * the core's output lands compact in O's kept order).  Indices are not
+ * range-checked on the device.  Errors: ESHAPE, ECUDA.
+ * ------------------------------------------------------------------------- */
+ztp_status ztp_transpose(ztp_ctx* ctx, const ztp_mat* src, const ztp_mat* dst, const int32_t* cols, int64_t n,
+                         void* stream);
+
+/* ---------------------------------------------------------------------------
  * Execution options of a context (performance scheduling only; results are
  * the same up to fp32 summation order within the stated tolerances).  Each
  * starts from its environment variable (read once by ztp_ctx_create) or the
@@ -208,6 +220,10 @@ ztp_status ztp_get_option(const ztp_ctx* ctx, ztp_option opt, double* value);
  * so results are bit-identical on every rank and to the oracle.
  * Errors: EINVAL (world not in 1..8, T not finite / negative, cost function
  * with < 2 samples), ENOBASELINE (M_r <= 0 where Eq.1 is evaluated).
+ * A-48: with costs given, a RESIZE rank whose Eq.1 saving gamma_r * M[r]
+ * does not exceed costs->omega1 (the static resizing overhead) is
+ * returned NORMAL with gamma 0 (timing noise above eps does not resize a
+ * healthy task); costs == NULL or omega1 == 0 leaves the plan unfiltered.
  * ------------------------------------------------------------------------- */
 typedef struct ztp_pwl {       /* piecewise linear, x ascending, linear extrapolation */
   int32_t n;

@@ -220,6 +220,21 @@ def eq3_scan(T: list, order: list, z: int, T_min: float, L: float, costs: Costs)
 
 
 def plan(T, M, L_ref: float, costs: Costs, opts: PlanOpts) -> Plan:
+    """Alg.2 (below, plan_core) followed by reading A-48: a RESIZE rank whose
+    Eq.1 saving gamma_r M does not exceed the static resizing overhead
+    Omega_1 stays NORMAL with gamma 0.  No costs / Omega_1 = 0:
+    unchanged."""
+    p = plan_core(T, M, L_ref, costs, opts)
+    if costs is not None and costs.omega1 > 0.0:
+        for r in range(p.world):
+            if p.role[r] == RESIZE and p.gamma_r[r] * M[r] <= costs.omega1:
+                p.role[r] = NORMAL
+                p.gamma[r] = 0.0
+                p.gamma_r[r] = 0.0
+    return p
+
+
+def plan_core(T, M, L_ref: float, costs: Costs, opts: PlanOpts) -> Plan:
     """Alg.1 l.1-2 (ZERO-only) and Alg.2 (SEMI).
 
     Evaluation order is fixed (fp64, no FMA) so the GPU host planner must

@@ -1053,13 +1053,11 @@ static cudaError_t post_launch(const GemmParams& p, int num_sms, cudaStream_t st
 
 template <int KIND, int CG, bool AG, bool BG>
 static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms, cudaStream_t st) {
-  static bool attr_set = false;
   const int smem = Cfg<CG>::TOTAL;
   auto kern = ztp_gemm_kernel<KIND, CG, AG, BG>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem_optin((const void*)kern, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int units = units_of(KIND, CG, p);
   const int pairs = p.cs > 1 ? units : std::min(units, num_sms / CG);   // cluster split-K: one unit per pair
@@ -1124,7 +1122,7 @@ int gemm_cluster_splits(int kind, int epi, int M, int N, int n_kept, int splits,
       const int smem = cg == 2 ? Cfg<2>::TOTAL : Cfg<1>::TOTAL;
       const void* kern = cg == 2 ? (const void*)ztp_gemm_kernel<KIND_DW, 2, false, false>
                                  : (const void*)ztp_gemm_kernel<KIND_DW, 1, false, false>;
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+      if (ensure_smem_optin(kern, smem) != cudaSuccess) return 0;
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(cg * cs * 64);
       cfg.blockDim = dim3(NUM_THREADS);
@@ -1393,11 +1391,9 @@ cudaError_t gemm_group_launch(int k0, const GemmOperands& o0, GemmParams p0, int
   ga.off = hit->d + hit->n;
   const int smem = (cg == 2 ? Cfg<2>::TOTAL : Cfg<1>::TOTAL) + GROUP_LIST_MAX * 4;
   auto kern = cg == 2 ? ztp_gemm_group_kernel<KIND_DX, KIND_DW, 2> : ztp_gemm_group_kernel<KIND_DX, KIND_DW, 1>;
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[cg]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem_optin((const void*)kern, smem);
     if (e != cudaSuccess) return e;
-    attr_set[cg] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pairs * cg);

@@ -47,6 +47,10 @@ inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
+// Raise a kernel's dynamic shared-memory opt-in to >= bytes on the CURRENT
+// device (function attributes are per device; cached per (device, kernel)).
+cudaError_t ensure_smem_optin(const void* kernel, int bytes);
+
 enum { KIND_FWD = 0, KIND_DX = 1, KIND_DW = 2 };
 // EPI_GELU: out <- pre, out2 <- GeLU(pre).  EPI_GELU_D: out <- GeLU'(pre), out2 <- GeLU(pre).
 // EPI_GELU_GRAD: out <- acc * GeLU'(aux).  EPI_MUL: out <- acc * aux (aux = GeLU'(pre)).

@@ -715,3 +715,21 @@ cudaError_t transpose_launch(const void* src, int64_t ld_src, int64_t R, const i
                   ld_dst);
 }
 }  // namespace ztp
+
+#include <map>
+#include <mutex>
+namespace ztp {
+cudaError_t ensure_smem_optin(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = done[{dev, kernel}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+}  // namespace ztp

@@ -69,8 +69,30 @@ extern "C" void ztp_plan_opts_default(ztp_plan_opts* o) {
   o->force_lambda = -1;
 }
 
+static ztp_status plan_core(int e, const double* T, const double* M, double L_ref, const ztp_costs* costs,
+                            const ztp_plan_opts* opts, ztp_plan_t* out);
+
+// A-48: a rank is resized only when it pays.  Resizing costs a rank the
+// static overhead Omega_1 (measured by the pretest) as soon as it
+// resizes at all; Eq.1 sheds gamma M of its GEMM time.  A RESIZE rank with
+// gamma_r M <= Omega_1 stays NORMAL (gamma 0) -- timing noise just above the
+// detection tolerance no longer resizes a healthy task.  Without costs (or
+// Omega_1 = 0) nothing changes (paper-literal).
 extern "C" ztp_status ztp_plan(int e, const double* T, const double* M, double L_ref, const ztp_costs* costs,
                                const ztp_plan_opts* opts, ztp_plan_t* out) {
+  const ztp_status s = plan_core(e, T, M, L_ref, costs, opts, out);
+  if (s != ZTP_OK || !costs || !(costs->omega1 > 0.0)) return s;
+  for (int r = 0; r < e; ++r)
+    if (out->role[r] == ZTP_RESIZE && out->gamma_r[r] * M[r] <= costs->omega1) {
+      out->role[r] = ZTP_NORMAL;
+      out->gamma[r] = 0.0;
+      out->gamma_r[r] = 0.0;
+    }
+  return ZTP_OK;
+}
+
+static ztp_status plan_core(int e, const double* T, const double* M, double L_ref, const ztp_costs* costs,
+                            const ztp_plan_opts* opts, ztp_plan_t* out) {
   if (!out || !T || !M || !opts) {
     set_thread_error("ztp_plan: null argument");
     return ZTP_EINVAL;

@@ -333,7 +333,6 @@ __global__ void __launch_bounds__(1024) ztp_select_kernel(const SelectParams p, 
 
 cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* kept, int32_t* pruned, int32_t* pos,
                           int32_t* err_flag, cudaStream_t st) {
-  static int smem_set = 0;
   SelectParams q = p;
   int maxlen = 0;
   for (int i = 0; i < p.nseg; ++i) maxlen = p.seg[i].len > maxlen ? p.seg[i].len : maxlen;
@@ -343,10 +342,9 @@ cudaError_t select_launch(const SelectParams& p, const float* scores, int32_t* k
   // the opt-in covers dynamic + static shared memory: raise it for any staged
   // launch (a 12288-key segment is exactly 48 KB dynamic, over the default
   // 48 KB limit once the kernel's static arrays are added)
-  if (smem > 0 && smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(ztp_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (smem > 0) {
+    cudaError_t e = ensure_smem_optin((const void*)ztp_select_kernel, smem);
     if (e != cudaSuccess) return e;
-    smem_set = smem;
   }
   cudaError_t e = launch_k(ztp_select_kernel, p.nseg, 1024, smem, st, q, scores, kept, pruned, pos, err_flag);
   if (e != cudaSuccess) return e;

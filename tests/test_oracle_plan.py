@@ -367,3 +367,27 @@ def test_receivers_are_normal_tasks_A44():
     assert sum(received.values()) == sent > 0
     assert all(received[r] == 0 for r in resizers) and all(received[r] > 0 for r in normals)
     assert all(got[r].n_prune == 0 for r in normals)
+
+
+def test_resize_only_when_it_pays_A48():
+    """A-48: a rank just above the detection tolerance (timing noise) has an
+    Eq.1 saving gamma M below the static resizing overhead Omega_1
+    and stays NORMAL; the real straggler resizes as before; Omega_1 = 0 is
+    the unfiltered plan."""
+    T = [1.0, 1.06, 2.0]
+    M = [0.8 * t for t in T]
+    opts = O.PlanOpts(enable_migration=0, zero_crit=O.CRIT_MIN, eps=0.05)
+    p0 = O.plan(T, M, 100.0, O.Costs(omega1=0.0), opts)
+    assert p0.role[1] == O.RESIZE and p0.gamma_r[1] * M[1] == pytest.approx(0.06)
+    p1 = O.plan(T, M, 100.0, O.Costs(omega1=0.1), opts)
+    assert p1.role == [O.NORMAL, O.NORMAL, O.RESIZE] and p1.gamma[1] == 0.0
+    assert p1.gamma[2] == p0.gamma[2] == pytest.approx(1.0 / 1.6)
+    # SEMI multi-straggler: the noise rank drops out of the resize group, and
+    # becomes a receiver (A-44)
+    T = [1.0, 1.06, 1.0, 6.0, 1.0, 4.0, 1.0, 1.0]
+    M = [0.8 * t for t in T]
+    costs = O.Costs(omega1=0.1, phi1=((0.0, 1.0), (0.0, 1e-4)))
+    p = O.plan(T, M, 100.0, costs, O.PlanOpts(enable_migration=1, zero_crit=O.CRIT_MIN, eps=0.05))
+    assert p.role[1] == O.NORMAL and p.role[3] in (O.MIGRATE, O.SPLIT)
+    got = {r: O.plan_counts(p, r, 100, 100, 1, True) for r in range(8)}
+    assert sum(hi - lo for (_, lo, hi) in got[1].inc) > 0 or p.x == 0
