@@ -63,6 +63,7 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.times = []
         self._stop = threading.Event()
         self._t = None
 
@@ -80,11 +81,18 @@ class ClockSampler:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == len(self.FIELDS):
                 self.samples.append(parts)
+                self.times.append(time.time())
         p.kill()
 
     def start(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+
+    def median_mhz(self, t0: float, t1: float):
+        """Median SM clock of the samples taken in [t0, t1] (None if none)."""
+        v = [float(s[0]) for s, t in zip(self.samples, self.times) if t0 <= t <= t1 and
+             s[0].replace(".", "").isdigit()]
+        return float(np.median(v)) if v else None
 
     def stop(self):
         self._stop.set()
@@ -722,7 +730,9 @@ def main():
     flops_exec = D.sum(flops_exec_rank)
     flops_method = D.sum(C.stack.method_flops())
     value = flops_exec / (ms_bal * 1e-3) / 1e12
-    gemm_ms, gemm_fl = C.ingraph_gemm()
+    t_g0 = time.time()
+    gemm_ms, gemm_fl = C.ingraph_gemm(40)
+    clk_gemm = sampler.median_mhz(t_g0, time.time())
     # the same measurement after 1 s idle: the board's power cap lowers SM
     # clocks during long replay runs, so the GEMM class is
     # also reported from a cool start (frac_after_idle); `frac` stays the
@@ -818,6 +828,8 @@ def main():
             "gemm_share_of_step": gemm_ms / ms_bal if ms_bal else None,
             "gemm_kernel_ms_per_step": gemm_ms, "gemm_executed_gflop_per_step": gemm_fl / 1e9,
             "frac_after_idle": (gemm_fl_cool / (gemm_ms_cool * 1e-3) / 1e12 / peak) if gemm_ms_cool > 0 else None,
+            "sm_mhz_during_measure": clk_gemm,
+            "frac_clock_normalized": (achieved / (peak * clk_gemm / 1965.0)) if (achieved and clk_gemm) else None,
             "gemm_kernel_ms_per_step_after_idle": gemm_ms_cool,
             "measured": "executed GEMM FLOPs / GEMM kernel time from the kernels' own %globaltimer stamps (first "
                         "CTA start after its PDL wait to last CTA end, split-K reduce included), union per step, "
