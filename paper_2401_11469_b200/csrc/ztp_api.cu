@@ -81,6 +81,8 @@ struct ztp_ctx {
                                        // 1 select, 2 compaction copies, 4 core, 16 GEMMs
   void* skws = nullptr;                // split-K fp32 partials
   void* xws[2] = {nullptr, nullptr};   // compact dW columns before the spread (main, side stream)
+  void* mws[2] = {nullptr, nullptr};   // Average imputation's column means (main, side stream)
+  size_t mws_cap[2] = {0, 0};
   size_t xws_cap[2] = {0, 0};
   size_t skws_cap = 0;
   // profiling (ztp_set_profile): event pairs around every kernel class
@@ -664,12 +666,25 @@ ztp_status impute(ztp_ctx* c, int policy, const ztp_mat& out, int64_t cols, cons
     if (!mat_ok(*hist) || hist->rows != out.rows || hist->cols < cols || hist->dtype != out.dtype)
       return fail(c, ZTP_ESHAPE, "Same imputation: " + shp("hist", *hist) + " vs " + shp("out", out));
   }
+  void* means = nullptr;
+  if (policy == ZTP_IMPUTE_AVERAGE) {   // column means (fp32), a workspace per stream
+    const int k = st == c->side_stream ? 1 : 0;
+    const size_t bytes = (size_t)cols * sizeof(float);
+    if (c->mws_cap[k] < bytes) {
+      if (c->mws[k]) cudaFree(c->mws[k]);
+      c->mws[k] = nullptr;
+      c->mws_cap[k] = 0;
+      CUDA_TRY(c, cudaMalloc(&c->mws[k], bytes));
+      c->mws_cap[k] = bytes;
+    }
+    means = c->mws[k];
+  }
   const int pe = prof_begin(c, st, PROF_OTHER, 0.0);
   CUDA_TRY(c, ztp::impute_rows_launch(out.ptr, out.ld, cols, kept, nk, pruned, np,
                                       policy == ZTP_IMPUTE_AVERAGE ? 1 : 2, hist ? hist->ptr : nullptr,
-                                      hist ? hist->ld : 0, out.dtype, st));
+                                      hist ? hist->ld : 0, out.dtype, means, st));
   prof_end(c, pe, st);
-  ++c->launches;
+  c->launches += policy == ZTP_IMPUTE_AVERAGE ? 2 : 1;
   return ZTP_OK;
 }
 
@@ -1136,6 +1151,8 @@ ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   cudaFree(c->cws[1]);
   cudaFree(c->xws[0]);
   cudaFree(c->xws[1]);
+  cudaFree(c->mws[0]);
+  cudaFree(c->mws[1]);
   for (auto& e : c->prof) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);

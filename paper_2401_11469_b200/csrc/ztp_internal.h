@@ -198,7 +198,8 @@ cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st);
 // Average / Same imputation of rows P (NEXT-2): mode 1 = per-column
 // mean over rows S of `out` (A-10), mode 2 = rows P copied from `hist` (A-11).
 cudaError_t impute_rows_launch(void* out, int64_t ld, int64_t cols, const int32_t* kept, int nk, const int32_t* pruned,
-                               int np, int mode, const void* hist, int64_t ld_hist, int dtype, cudaStream_t st);
+                               int np, int mode, const void* hist, int64_t ld_hist, int dtype, void* ws,
+                               cudaStream_t st);   // ws: cols floats (Average's column means)
 // NEXT-1 column delta with carry-over (ztp_priority_update).
 cudaError_t priority_update_launch(const void* w, int64_t ld_w, const void* w_old, int64_t ld_old, int64_t K,
                                    int64_t n, const int32_t* pos_prev, float* delta, int32_t* count_above,

@@ -402,10 +402,9 @@ cudaError_t expand_cols_launch(const void* src, int64_t ld_src, void* dst, int64
 }
 
 // ------------------------------------------ Average / Same imputation (NEXT-2)
-// Average (A-10): one CTA per 8-column group; its threads stride over
-// the kept rows S, partial sums in fp32 are combined in a fixed tree order
-// (deterministic), mean = sum / |S|, written to every row p in P.  Zero rows
-// P written by the GEMM are overwritten.  Same (A-11): out[p] <- hist[p].
+// Average (A-10): the per-column mean over the kept rows S, in fp32
+// with a fixed summation tree (deterministic), written to every row p in P
+// (the GEMM's Zero rows are overwritten).  Same (A-11): out[p] <- hist[p].
 template <typename T>
 __device__ __forceinline__ float to_f(T v);
 template <>
@@ -438,64 +437,150 @@ __global__ void __launch_bounds__(256) ztp_accumulate(T* dst, int64_t ld_dst, co
   }
 }
 
+// Average, pass 1: one CTA per 32 columns; its 256 threads are 4 groups of 8
+// columns x 64 row slices striding the kept rows S (4 loads in flight per
+// thread); the 64 slices' fp32 partial sums are combined by a fixed tree
+// (deterministic) and mean = sum / |S| is stored per column (fp32 workspace).
 template <typename T>
-__global__ void __launch_bounds__(256) ztp_impute_average(T* out, int64_t ld, int64_t cols, const int32_t* kept, int nk,
-                                                          const int32_t* pruned, int np) {
+__global__ void __launch_bounds__(256) ztp_impute_means(const T* out, int64_t ld, int64_t cols, const int32_t* kept,
+                                                        int nk, float* means) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float part[8][256];
-  const int64_t c0 = (int64_t)blockIdx.x * 8;
+  __shared__ float part[64][33];
+  const int cg = threadIdx.x & 3, sl = threadIdx.x >> 2;      // column group, row slice
+  const int64_t c0 = (int64_t)blockIdx.x * 32 + cg * 8;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int i = threadIdx.x; i < nk; i += blockDim.x) {
-    const T* row = out + (int64_t)__ldg(kept + i) * ld + c0;
+  const bool full = c0 + 8 <= cols;
+  for (int i0 = sl; i0 < nk; i0 += 64 * 4) {
+    T v[4][8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (c0 + q < cols) acc[q] += to_f<T>(row[q]);
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + 64 * u;
+      if (i < nk) {
+        const T* row = out + (int64_t)__ldg(kept + i) * ld + c0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[u][q] = (full || c0 + q < cols) ? row[q] : from_f<T>(0.f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + 64 * u < nk)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += to_f<T>(v[u][q]);
   }
 #pragma unroll
-  for (int q = 0; q < 8; ++q) part[q][threadIdx.x] = acc[q];
+  for (int q = 0; q < 8; ++q) part[sl][cg * 8 + q] = acc[q];
   __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) part[q][threadIdx.x] += part[q][threadIdx.x + w];
+  for (int w = 32; w > 0; w >>= 1) {           // fixed-order tree over the 64 row slices
+    for (int j = threadIdx.x; j < w * 32; j += blockDim.x) part[j / 32][j % 32] += part[j / 32 + w][j % 32];
     __syncthreads();
   }
-  for (int j = threadIdx.x; j < np * 8; j += blockDim.x) {
-    const int r = j / 8, q = j % 8;
-    if (c0 + q < cols) out[(int64_t)__ldg(pruned + r) * ld + c0 + q] = from_f<T>(part[q][0] / (float)nk);
+  if (threadIdx.x < 32) {
+    const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+    if (c < cols) means[c] = part[0][threadIdx.x] * (1.0f / (float)nk);
   }
 }
 
+// Average, pass 2: rows P <- the column means, one warp per (row, 256
+// columns), 8 columns per lane, 16-byte stores where the row allows.
 template <typename T>
-__global__ void ztp_impute_same(T* out, int64_t ld, int64_t cols, const int32_t* pruned, int np, const T* hist,
-                                int64_t ld_hist) {
+__global__ void __launch_bounds__(256) ztp_impute_fill(T* out, int64_t ld, int64_t cols, const int32_t* pruned, int np,
+                                                       const float* means) {
   pdl_wait();
   pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int64_t cpr = (cols + 255) / 256, items = (int64_t)np * cpr;
+  const bool vec = (sizeof(T) == 2) && ((ld * 2) % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  for (int64_t it = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); it < items; it += (int64_t)gridDim.x * 8) {
+    const int64_t r = __ldg(pruned + it / cpr), c = (it % cpr) * 256 + lane * 8;
+    T* o = out + r * ld + c;
+    if (vec && c + 8 <= cols) {
+      const float4 a = *reinterpret_cast<const float4*>(means + c), b = *reinterpret_cast<const float4*>(means + c + 4);
+      const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      T v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = from_f<T>(f[q]);
+      *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(v);
+    } else {
+      for (int q = 0; q < 8 && c + q < cols; ++q) o[q] = from_f<T>(means[c + q]);
+    }
+  }
+}
+
+// Same: rows P copied from the history, 16-byte vectors (4 in flight per
+// thread) when the row widths allow, else element-wise.
+template <typename T>
+__global__ void __launch_bounds__(256) ztp_impute_same(T* out, int64_t ld, int64_t cols, const int32_t* pruned, int np,
+                                                       const T* hist, int64_t ld_hist, int vec) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    constexpr int E = 16 / sizeof(T);
+    const int64_t vpr = cols / E, total = (int64_t)np * vpr;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < total; i0 += 4 * stride) {
+      uint4 w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < total) {
+          const int64_t r = __ldg(pruned + i / vpr), c = (i % vpr) * E;
+          w[u] = __ldg(reinterpret_cast<const uint4*>(hist + r * ld_hist + c));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < total) {
+          const int64_t r = __ldg(pruned + i / vpr), c = (i % vpr) * E;
+          *reinterpret_cast<uint4*>(out + r * ld + c) = w[u];
+        }
+      }
+    }
+    return;
+  }
   const int64_t total = (int64_t)np * cols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
     const int64_t r = __ldg(pruned + i / cols), c = i % cols;
     out[r * ld + c] = hist[r * ld_hist + c];
   }
 }
 
 cudaError_t impute_rows_launch(void* out, int64_t ld, int64_t cols, const int32_t* kept, int nk, const int32_t* pruned,
-                               int np, int mode, const void* hist, int64_t ld_hist, int dtype, cudaStream_t st) {
+                               int np, int mode, const void* hist, int64_t ld_hist, int dtype, void* ws,
+                               cudaStream_t st) {
   if (np <= 0 || cols <= 0) return cudaSuccess;
   if (mode == 1) {
-    const int blocks = (int)((cols + 7) / 8);
-    if (dtype == 0)
-      return launch_k(ztp_impute_average<__nv_bfloat16>, blocks, 256, 0, st, (__nv_bfloat16*)out, ld, cols, kept, nk,
-                      pruned, np);
-    return launch_k(ztp_impute_average<float>, blocks, 256, 0, st, (float*)out, ld, cols, kept, nk, pruned, np);
+    if (!ws) return cudaErrorInvalidValue;
+    float* means = static_cast<float*>(ws);
+    const int blocks = (int)((cols + 31) / 32);
+    const int64_t items = (int64_t)np * ((cols + 255) / 256);
+    const int fb = (int)std::min<int64_t>((items + 7) / 8, (int64_t)148 * 8);
+    cudaError_t e;
+    if (dtype == 0) {
+      e = launch_k(ztp_impute_means<__nv_bfloat16>, blocks, 256, 0, st, (const __nv_bfloat16*)out, ld, cols, kept, nk,
+                   means);
+      if (e == cudaSuccess)
+        e = launch_k(ztp_impute_fill<__nv_bfloat16>, fb, 256, 0, st, (__nv_bfloat16*)out, ld, cols, pruned, np,
+                     (const float*)means);
+      return e;
+    }
+    e = launch_k(ztp_impute_means<float>, blocks, 256, 0, st, (const float*)out, ld, cols, kept, nk, means);
+    if (e == cudaSuccess)
+      e = launch_k(ztp_impute_fill<float>, fb, 256, 0, st, (float*)out, ld, cols, pruned, np, (const float*)means);
+    return e;
   }
-  int blocks = (int)(((int64_t)np * cols + 255) / 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  const int64_t es = dtype == 0 ? 2 : 4;
+  const int vec = ((cols * es) % 16 == 0) && ((ld * es) % 16 == 0) && ((ld_hist * es) % 16 == 0) &&
+                  ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(hist)) & 15) == 0;
+  const int64_t work = vec ? (int64_t)np * cols / (16 / es) / 4 : (int64_t)np * cols;
+  int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)148 * 8);
+  blocks = std::max(blocks, 1);
   if (dtype == 0)
     return launch_k(ztp_impute_same<__nv_bfloat16>, blocks, 256, 0, st, (__nv_bfloat16*)out, ld, cols, pruned, np,
-                    (const __nv_bfloat16*)hist, ld_hist);
+                    (const __nv_bfloat16*)hist, ld_hist, vec);
   return launch_k(ztp_impute_same<float>, blocks, 256, 0, st, (float*)out, ld, cols, pruned, np, (const float*)hist,
-                  ld_hist);
+                  ld_hist, vec);
 }
 
 // ------------------------------------------- NEXT-1 priority maintenance
