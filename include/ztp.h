@@ -187,6 +187,13 @@ ztp_status ztp_transpose(ztp_ctx* ctx, const ztp_mat* src, const ztp_mat* dst, c
  *   ZTP_OPT_GROUP       (ZTP_GROUP, 0)       0 / 1 / 2: dX + dW as one grouped launch never /
  *                                            always / only for small pairs
  *   ZTP_OPT_PEER_CTAS   (ZTP_PEER_CTAS, 32)  CTAs of a peer collective (same on every rank)
+ *   ZTP_OPT_A_EARLY     (ZTP_A_EARLY, 1)     a GEMM right after a GEMM whose outputs do not overlap
+ *                                            its A operand issues its first stages' A loads before
+ *                                            the PDL wait (only B waits for the predecessor)
+ *   ZTP_OPT_PART        (ZTP_PART, 1)        dX / dW SM partition: 0 work-proportional,
+ *                                            1 wave-quantised (minimises the later finish)
+ *   ZTP_OPT_AUX_WEIGHT  (ZTP_AUX_WEIGHT, 1.4) dX work factor in that partition when its epilogue
+ *                                            reads an aux operand (GeLU')
  * ------------------------------------------------------------------------- */
 typedef enum ztp_option {
   ZTP_OPT_CONC = 0,
@@ -195,7 +202,10 @@ typedef enum ztp_option {
   ZTP_OPT_GATHER4 = 3,
   ZTP_OPT_SPLITK = 4,
   ZTP_OPT_GROUP = 5,
-  ZTP_OPT_PEER_CTAS = 6
+  ZTP_OPT_PEER_CTAS = 6,
+  ZTP_OPT_A_EARLY = 7,
+  ZTP_OPT_PART = 8,
+  ZTP_OPT_AUX_WEIGHT = 9
 } ztp_option;
 ztp_status ztp_set_option(ztp_ctx* ctx, ztp_option opt, double value);
 ztp_status ztp_get_option(const ztp_ctx* ctx, ztp_option opt, double* value);
@@ -646,6 +656,13 @@ ztp_status ztp_read_profile(ztp_ctx* ctx, void* stream, ztp_profile* out);
  * GEMM launches (profiling on), in launch order, without resetting them;
  * returns how many pairs were written to out[2 * max_launches], -1 on error. */
 int ztp_read_stamps(ztp_ctx* ctx, void* stream, unsigned long long* out, int max_launches);
+/* Profiling mode 3 (ztp_set_profile(ctx, 3)): as mode 2, and every GEMM
+ * launch (first 64) also records per CTA (<= 160) eight %globaltimer stamps:
+ * CTA start, after the PDL wait, first operand stage ready (MMA issuer), last
+ * MMA commit, first accumulator ready (epilogue), last tile's stores issued,
+ * stores complete, CTA end; 0 = not recorded by that CTA.  Copies launches x
+ * 160 x 8 values into out; returns the launch count or -1. */
+int ztp_read_cta_stamps(ztp_ctx* ctx, void* stream, unsigned long long* out, int max_launches);
 
 /* Raw resized GEMM (test / benchmark entry; the linears use it internally).
  * kind 0 = FWD (y = w[S]^T x[S]), 1 = dX (dx rows by sel), 2 = dW. */

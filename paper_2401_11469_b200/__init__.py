@@ -24,7 +24,7 @@ __all__ = [
     "ztp_set_transport", "ztp_barrier", "TRANSPORT_NCCL", "TRANSPORT_PEER",
 ]
 from ._lib import (TRANSPORT_NCCL, TRANSPORT_PEER, COLL_TREE, COLL_P2P, OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4,  # noqa: E402
-                   OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS)
+                   OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS, OPT_A_EARLY, OPT_PART, OPT_AUX_WEIGHT)
 
 
 def _stream(stream) -> Optional[int]:
@@ -422,6 +422,16 @@ def ztp_read_stamps(ctx, stream=None, max_launches: int = 256):
     if n < 0:
         raise ZtpError(-1, "ztp_read_stamps failed")
     return [(buf[2 * i], buf[2 * i + 1]) for i in range(n)]
+
+
+def ztp_read_cta_stamps(ctx, stream=None, max_launches: int = 64):
+    """Profiling mode 3: numpy [launches, 160, 8] per-CTA %globaltimer stamps."""
+    import numpy as np
+    buf = (C.c_uint64 * (max_launches * 160 * 8))()
+    n = lib.ztp_read_cta_stamps(ctx, _stream(stream), buf, max_launches)
+    if n < 0:
+        raise ZtpError(-1, "ztp_read_cta_stamps failed (profiling mode 3 not enabled?)")
+    return np.frombuffer(buf, dtype=np.uint64)[:n * 160 * 8].reshape(n, 160, 8).copy()
 
 
 def ztp_read_gemm_ns(ctx, stream=None) -> float:

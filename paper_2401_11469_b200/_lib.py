@@ -25,7 +25,8 @@ ACT_NONE, ACT_GELU, ACT_GELU_D = 0, 1, 2
 CRIT_AVG, CRIT_MIN = 0, 1
 NORMAL, RESIZE, MIGRATE, SPLIT = 0, 1, 2, 3
 KIND_FWD, KIND_DX, KIND_DW = 0, 1, 2
-OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4, OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS = range(7)
+(OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4, OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS, OPT_A_EARLY, OPT_PART,
+ OPT_AUX_WEIGHT) = range(10)
 
 
 class ZtpError(RuntimeError):
@@ -158,6 +159,7 @@ def _load():
         "ztp_prepare": (st, [vp, C.c_int, C.POINTER(C.POINTER(LinearArgs)), C.POINTER(C.c_int32), vp]),
         "ztp_priority_update": (st, [vp, C.POINTER(Mat), C.POINTER(Mat), vp, vp, vp, C.c_float, vp]),
         "ztp_read_stamps": (C.c_int, [vp, vp, C.POINTER(C.c_uint64), C.c_int]),
+        "ztp_read_cta_stamps": (C.c_int, [vp, vp, C.POINTER(C.c_uint64), C.c_int]),
         "ztp_pridiff_gamma": (C.c_double, [C.c_int64, C.c_int64, C.c_double, C.c_double]),
         "ztp_set_profile": (st, [vp, C.c_int]),
         "ztp_window_create": (st, [vp, C.c_size_t, C.c_char_p]),
@@ -192,7 +194,8 @@ EXPORTED = ("ztp_status_str", "ztp_last_error", "ztp_version", "ztp_get_unique_i
             "ztp_priority_update", "ztp_pridiff_gamma", "ztp_read_stamps",
             "ztp_set_profile", "ztp_read_profile", "ztp_window_create", "ztp_window_open", "ztp_sym_alloc",
             "ztp_set_transport", "ztp_barrier", "ztp_set_option", "ztp_get_option", "ztp_broadcast", "ztp_reduce",
-            "ztp_accumulate", "ztp_allreduce", "ztp_transpose")
+            "ztp_accumulate", "ztp_allreduce", "ztp_transpose",
+            "ztp_read_cta_stamps")
 
 
 def check(code: int, ctx=None):

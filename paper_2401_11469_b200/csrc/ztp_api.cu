@@ -44,6 +44,8 @@ struct ztp_ctx {
   // it gets more SMs than its MMA share: 1.2 measured best (1.0 / 1.2 / 1.3 /
   // 1.4 / 1.5 / 1.6 / 0.8 swept, profiles/r01_dw_share_sweep_v*.txt)
   double dw_share = 1.2;
+  int part_model = 1;                  // ZTP_PART: 0 work-proportional dX / dW partition, 1 wave-quantised
+  double aux_weight = 1.4;             // ZTP_AUX_WEIGHT: dX work factor when its epilogue reads an aux operand
   // While a concurrent dW is pending, the (non-persistent) core kernel is
   // launched in plain stream order: under PDL its CTAs would sit resident on
   // every free SM waiting for the dX GEMM, and the side-stream dW GEMM could
@@ -54,6 +56,13 @@ struct ztp_ctx {
   // SM (ztp::gemm_group_launch) instead of two concurrent kernels (TP = 1 /
   // row layers; a col layer at TP > 1 keeps the concurrent pair so the dX
   // all-reduce overlaps its dW)
+  // A-operand loads before the PDL wait when the preceding library launch was
+  // a GEMM on the same stream whose outputs do not overlap A (ZTP_A_EARLY, default 1)
+  int a_early = 1;
+  int64_t lg_id = -1;                  // ztp::launch_seq() right after the last eligible GEMM launch (-1: none)
+  cudaStream_t lg_stream = nullptr;
+  const char* lg_out[2] = {nullptr, nullptr};
+  size_t lg_bytes[2] = {0, 0};
   int group_bwd = 0;                   // 0 never (default), 1 always, 2 small pairs only (measured: no net gain)
   int sm_cap = 0;                      // > 0: SMs a GEMM launch may use (concurrent dX / dW partition)
   bool side_pending = false;           // side-stream work not yet joined into a caller stream
@@ -96,6 +105,8 @@ struct ztp_ctx {
   int pstamp_used = 0;
   std::vector<double> pstamp_flops;         // algorithmic FLOPs of each stamped launch
   static constexpr int PSTAMP_CAP = 4096;
+  static constexpr int CTASTAMP_LAUNCHES = 64, CTASTAMP_PER_LAUNCH = 160 * 8;   // mode 3: per-CTA stamps
+  unsigned long long* d_ctastamp = nullptr;
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
   // peer-memory data plane (ztp_window_*, ztp_sym_alloc; ztp_peer.cu)
@@ -417,11 +428,37 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     if (c->prof_on && c->d_pstamp && c->pstamp_used < ztp_ctx::PSTAMP_CAP) {
       c->pstamp_flops.resize((size_t)c->pstamp_used + 1);
       c->pstamp_flops[c->pstamp_used] = 2.0 * (double)nk * (double)n_out * tokens;
+      if (c->prof_on == 3 && c->d_ctastamp && c->pstamp_used < ztp_ctx::CTASTAMP_LAUNCHES)
+        p.cta_stamps = c->d_ctastamp + (size_t)c->pstamp_used * ztp_ctx::CTASTAMP_PER_LAUNCH;
       p.prof_stamp = c->d_pstamp + 2 * (c->pstamp_used++);
     }
     const int nsm = c->sm_cap > 0 ? c->sm_cap : c->num_sms;
+    {
+      // A untouched by the immediately preceding kernel: a GEMM of this stream
+      // with nothing launched since (so it waited on ITS predecessor before it
+      // triggered this launch) whose outputs are disjoint from A
+      const char* a0 = static_cast<const char*>(a.ptr);
+      const char* a1 = a0 + (size_t)(A.compact ? nk : a.rows) * a.ld * 2;
+      bool ok = c->a_early && c->lg_id == (int64_t)ztp::launch_seq().load() && c->lg_stream == st &&
+                !o.a_gather && !o.b_gather && !p.pdl_late;
+      for (int k = 0; ok && k < 2; ++k)
+        if (c->lg_out[k] && a0 < c->lg_out[k] + c->lg_bytes[k] && c->lg_out[k] < a1) ok = false;
+      p.a_early = ok ? 1 : 0;
+    }
+    const uint64_t seq0 = ztp::launch_seq().load();
     if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, nsm, st));
-    if ((p.splits > 1 && p.cs <= 1) || p.col_pos) ++c->launches;   // split-K reduce or column spread
+    const bool extra = (p.splits > 1 && p.cs <= 1) || p.col_pos;
+    if (extra) ++c->launches;   // split-K reduce or column spread
+    c->lg_id = -1;
+    if (!extra && !p.pdl_late && !emulating(c) && ztp::launch_seq().load() == seq0 + 1) {   // exactly the GEMM
+      // the launch the next GEMM may prefetch its A behind
+      c->lg_id = (int64_t)ztp::launch_seq().load();
+      c->lg_stream = st;
+      c->lg_out[0] = static_cast<const char*>(out.ptr);
+      c->lg_bytes[0] = (size_t)out.rows * out.ld * 2;
+      c->lg_out[1] = out2 ? static_cast<const char*>(out2->ptr) : nullptr;
+      c->lg_bytes[1] = out2 ? (size_t)out2->rows * out2->ld * 2 : 0;
+    }
   } else {
     if (col_pos) return fail(c, ZTP_EUNSUPPORTED, "f32 path: output pruning");
     ztp::GemmParamsF32 p{};
@@ -941,11 +978,41 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
     // at once and each one's fill and tail overlap the other's mainloop
     const double rows = (double)std::min<int64_t>(nk, dxc ? nk : K);
     const double t_rows = std::ceil(rows / 256.0);
-    const double w_dx = t_rows * std::ceil((double)N / 256.0) * std::ceil((double)n_y / 64.0);
+    // a GeLU' epilogue (reads pre_in_t per output element) costs dX more per
+    // tile: weighted by aux_weight
+    const bool dx_aux = layer == LAYER_ROW && (a->act_in == ZTP_ACT_GELU || a->act_in == ZTP_ACT_GELU_D);
+    const double w_dx = t_rows * std::ceil((double)N / 256.0) * std::ceil((double)n_y / 64.0) *
+                        (dx_aux ? c->aux_weight : 1.0);
     const double w_dw = t_rows * std::ceil((double)n_y / 256.0) * std::ceil((double)N / 64.0);
     const int pairs = c->num_sms / 2;
     int px = (int)std::lround(pairs * w_dx / (w_dx + c->dw_share * w_dw));
     px = std::max(1, std::min(pairs - 1, px));
+    if (c->part_model == 1) {
+      // wave-quantised: each GEMM's time ~ ceil(units / CTA slots) x k-blocks
+      // per unit (its split-K as gemm() will choose it for that many SMs);
+      // the partition minimising the later finish, ties to the proportional one
+      auto cost = [&](int kind, int M_, int N_, int kdim_, int nsm, double wgt) {
+        const int cg = ztp::gemm_choose_cg(kind, M_, nk);
+        const int tm = 128 * cg;
+        const int mc = std::min((M_ + tm - 1) / tm, (nk + tm - 1) / tm), nt = (N_ + 255) / 256;
+        const int sp = c->allow_splitk ? ztp::gemm_choose_splits(kind, M_, N_, kdim_, nk, nsm) : 1;
+        const int kb = (kdim_ + 63) / 64, kps = (kb + sp - 1) / sp;
+        const int slots = std::max(1, nsm / cg);
+        return std::ceil((double)mc * nt * sp / slots) * kps * wgt;
+      };
+      const int Mx = (int)(dxc ? nk : K);
+      double best = 1e300;
+      int bp = px;
+      for (int q = 1; q < pairs; ++q) {
+        const double t = std::max(cost(ztp::KIND_DX, Mx, (int)N, (int)n_y, 2 * q, dx_aux ? c->aux_weight : 1.0),
+                                  cost(ztp::KIND_DW, (int)K, (int)n_y, (int)N, 2 * (pairs - q), c->dw_share));
+        if (t < best - 1e-9 || (t < best + 1e-9 && std::abs(q - px) < std::abs(bp - px))) {
+          best = std::min(best, t);
+          bp = q;
+        }
+      }
+      px = bp;
+    }
     cap_dx = 2 * px;
     cap_dw = 2 * (pairs - px);
   }
@@ -1088,8 +1155,11 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* sk = getenv("ZTP_SPLITK")) c->allow_splitk = atoi(sk) != 0;
   if (const char* cc = getenv("ZTP_CONC")) c->conc_bwd = atoi(cc) != 0;
   if (const char* ds = getenv("ZTP_DW_SHARE")) c->dw_share = atof(ds);
+  if (const char* aw = getenv("ZTP_AUX_WEIGHT")) c->aux_weight = atof(aw);
+  if (const char* pm = getenv("ZTP_PART")) c->part_model = atoi(pm);
   if (const char* sg = getenv("ZTP_SQUAT_GUARD")) c->squat_guard = atoi(sg) != 0;
   if (const char* gb = getenv("ZTP_GROUP")) c->group_bwd = atoi(gb);
+  if (const char* ae = getenv("ZTP_A_EARLY")) c->a_early = atoi(ae) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
   auto cleanup = [&](ztp_status s) {
@@ -1140,6 +1210,7 @@ ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   if (c->ev_d) cudaEventDestroy(c->ev_d);
   if (c->skws_side) cudaFree(c->skws_side);
   if (c->d_pstamp) cudaFree(c->d_pstamp);
+  if (c->d_ctastamp) cudaFree(c->d_ctastamp);
   cudaFree(c->d_flags);
   cudaFree(c->d_stamp);
   cudaFree(c->d_gemm_ns);
@@ -1724,6 +1795,15 @@ ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
       if (iv < 1 || iv > ztp::PEER_MAX_CTAS) return fail(c, ZTP_EINVAL, "ztp_set_option: peer CTAs out of range");
       c->peer_ctas = iv;
       return ZTP_OK;
+    case ZTP_OPT_A_EARLY: c->a_early = iv != 0; return ZTP_OK;
+    case ZTP_OPT_PART:
+      if (iv < 0 || iv > 1) return fail(c, ZTP_EINVAL, "ztp_set_option: partition model is 0 or 1");
+      c->part_model = iv;
+      return ZTP_OK;
+    case ZTP_OPT_AUX_WEIGHT:
+      if (!(v > 0.0)) return fail(c, ZTP_EINVAL, "ztp_set_option: aux weight must be > 0");
+      c->aux_weight = v;
+      return ZTP_OK;
   }
   return fail(c, ZTP_EINVAL, "ztp_set_option: unknown option " + std::to_string((int)opt));
 }
@@ -1738,6 +1818,9 @@ ztp_status ztp_get_option(const ztp_ctx* c, ztp_option opt, double* v) {
     case ZTP_OPT_SPLITK: *v = c->allow_splitk; return ZTP_OK;
     case ZTP_OPT_GROUP: *v = c->group_bwd; return ZTP_OK;
     case ZTP_OPT_PEER_CTAS: *v = c->peer_ctas; return ZTP_OK;
+    case ZTP_OPT_A_EARLY: *v = c->a_early; return ZTP_OK;
+    case ZTP_OPT_PART: *v = c->part_model; return ZTP_OK;
+    case ZTP_OPT_AUX_WEIGHT: *v = c->aux_weight; return ZTP_OK;
   }
   return fail(nullptr, ZTP_EINVAL, "ztp_get_option: unknown option " + std::to_string((int)opt));
 }
@@ -1759,7 +1842,12 @@ ztp_status ztp_barrier(ztp_ctx* c, void* stream) {
 
 ztp_status ztp_set_profile(ztp_ctx* c, int on) {
   if (!c) return fail(c, ZTP_EINVAL, "ztp_set_profile: null ctx");
-  c->prof_on = (on == 2) ? 2 : (on ? 1 : 0);
+  c->prof_on = (on == 2 || on == 3) ? on : (on ? 1 : 0);
+  if (on == 3 && !c->d_ctastamp) {
+    const size_t bytes = (size_t)ztp_ctx::CTASTAMP_LAUNCHES * ztp_ctx::CTASTAMP_PER_LAUNCH * sizeof(unsigned long long);
+    CUDA_TRY(c, cudaMalloc(&c->d_ctastamp, bytes));
+    CUDA_TRY(c, cudaMemset(c->d_ctastamp, 0, bytes));
+  }
   if (!on) c->pstamp_used = 0;
   if (on && !c->d_pstamp) CUDA_TRY(c, cudaMalloc(&c->d_pstamp, 2 * ztp_ctx::PSTAMP_CAP * sizeof(unsigned long long)));
   if (on) {
@@ -1801,7 +1889,7 @@ ztp_status ztp_read_profile(ztp_ctx* c, void* stream, ztp_profile* out) {
       const unsigned long long t0 = ~h[2 * i], t1 = h[2 * i + 1];
       if (h[2 * i] != 0 && t1 >= t0) {
         iv.emplace_back(t0, t1);
-        if (c->prof_on == 2) {
+        if (c->prof_on >= 2) {
           out->gemm_flops += c->pstamp_flops[i];
           ++out->n_gemm;
         }
@@ -1823,7 +1911,7 @@ ztp_status ztp_read_profile(ztp_ctx* c, void* stream, ztp_profile* out) {
     }
     CUDA_TRY(c, cudaMemset(c->d_pstamp, 0, h.size() * sizeof(unsigned long long)));
     // mode 2 keeps its slots: a captured graph writes the same ones every replay
-    if (c->prof_on != 2) c->pstamp_used = 0;
+    if (c->prof_on < 2) c->pstamp_used = 0;
   }
   return ZTP_OK;
 }
@@ -1849,6 +1937,17 @@ ztp_status ztp_set_stats(ztp_ctx* c, int on) {
   if (!c) return fail(c, ZTP_EINVAL, "ztp_set_stats: null ctx");
   c->stats = on ? 1 : 0;
   return ZTP_OK;
+}
+
+int ztp_read_cta_stamps(ztp_ctx* c, void* stream, unsigned long long* out, int max_launches) {
+  if (!c || !out || max_launches < 0 || !c->d_ctastamp) return -1;
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return -1;
+  const int n = std::min(std::min(c->pstamp_used, max_launches), ztp_ctx::CTASTAMP_LAUNCHES);
+  if (n <= 0) return 0;
+  const size_t cnt = (size_t)n * ztp_ctx::CTASTAMP_PER_LAUNCH;
+  if (cudaMemcpy(out, c->d_ctastamp, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return n;
 }
 
 ztp_status ztp_read_gemm_ns(ztp_ctx* c, void* stream, double* ns) {

@@ -262,11 +262,73 @@ __device__ __forceinline__ void produce_unit(const CUtensorMap* tmA, const CUten
   }
 }
 
+// ---- The first unit's first stages with the A loads issued BEFORE the PDL
+// wait (p.a_early: A -- weights, or FWD activations for dW -- is not written
+// by the preceding kernel), the B loads after it; dense boxes only.  The ring
+// is empty at kernel start, so the stages' empty barriers pass at once.
+template <int KIND, int CG>
+__device__ __forceinline__ void produce_unit_early(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmParams& p,
+                                                   Work wk, int rank, bool leader, int lane, uint8_t* ring,
+                                                   uint64_t* full, uint64_t* empty, Pipe& ps) {
+  using C = Cfg<CG>;
+  constexpr int BNL = C::BNL;
+  const int am0 = wk.m0 + BM * rank, bn0 = wk.n0 + BNL * rank;
+  const int n = min(C::STAGES, wk.kb1 - wk.kb0);
+  auto load = [&](const CUtensorMap* tm, uint64_t* fb, void* dst, int c0, int c1) {
+    if (CG == 2)
+      tma_load_2d_cg2(tm, fb, dst, c0, c1);
+    else
+      tma_load_2d(tm, fb, dst, c0, c1);
+  };
+  const int st0 = ps.stage;
+  const uint32_t ph0 = ps.phase;
+  for (int i = 0; i < n; ++i) {
+    const int kb = wk.kb0 + i;
+    mbar_wait(&empty[ps.stage], ps.phase ^ 1);
+    uint8_t* sa = ring + ps.stage * C::STAGE_BYTES;
+    uint64_t* fb = &full[ps.stage];
+    if (leader && lane == 0) mbar_expect_tx(fb, CG * C::STAGE_BYTES);
+    __syncwarp();
+    if (lane == 0) {
+      if (KIND == KIND_FWD) {
+        load(tmA, fb, sa, am0, kb * BK);
+        load(tmA, fb, sa + 8192, am0 + 64, kb * BK);
+      } else {
+        load(tmA, fb, sa, kb * BK, am0);
+      }
+    }
+    if (++ps.stage == C::STAGES) {
+      ps.stage = 0;
+      ps.phase ^= 1;
+    }
+  }
+  pdl_wait();   // B (the predecessor's output) from here on
+  pdl_trigger();   // only after the wait: a dependent launched off this trigger may itself prefetch early
+  int stg = st0;
+  for (int i = 0; i < n; ++i) {
+    const int kb = wk.kb0 + i;
+    uint8_t* sb = ring + stg * C::STAGE_BYTES + A_BYTES;
+    uint64_t* fb = &full[stg];
+    if (lane == 0) {
+      if (KIND == KIND_DW) {
+        load(tmB, fb, sb, kb * BK, bn0);
+      } else {
+#pragma unroll
+        for (int b = 0; b < BNL / 64; ++b) load(tmB, fb, sb + b * 8192, bn0 + 64 * b, kb * BK);
+      }
+    }
+    if (++stg == C::STAGES) stg = 0;
+  }
+  (void)ph0;
+  wk.kb0 += n;
+  if (wk.kb0 < wk.kb1) produce_unit<KIND, CG, false, false>(tmA, tmB, p, wk, rank, leader, lane, ring, full, empty, ps);
+}
+
 // ---- MMA issuer of one work unit (warp 1 of the even CTA; lane 0 issues).
 template <int KIND, int CG>
 __device__ __forceinline__ void mma_unit(const Work& wk, int lane, uint16_t pmask, uint8_t* ring, uint64_t* full,
                                          uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
-                                         Pipe& ps) {
+                                         Pipe& ps, unsigned long long** first = nullptr) {
   using C = Cfg<CG>;
   constexpr uint32_t IDESC = make_idesc_bf16(C::TM, BN, KIND == KIND_FWD ? 1 : 0, KIND == KIND_DW ? 0 : 1);
   mbar_wait(&tempty[ps.acc], ps.aphase ^ 1);
@@ -275,6 +337,10 @@ __device__ __forceinline__ void mma_unit(const Work& wk, int lane, uint16_t pmas
   for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
     mbar_wait(&full[ps.stage], ps.phase);
     tc_fence_after();
+    if (first && *first) {
+      if (lane == 0) **first = globaltimer();
+      *first = nullptr;
+    }
     if (lane == 0) {
       const uint32_t sa = smem_u32(ring + ps.stage * C::STAGE_BYTES);
       const uint32_t sb = sa + A_BYTES;
@@ -324,7 +390,7 @@ template <int KIND, int CG>
 __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUtensorMap* tmO2, const CUtensorMap* tmW,
                                               const GemmParams& p, int S, const Work& wk, int rank, int ew, int lane,
                                               uint8_t* staging, uint64_t* tfull, uint64_t* tempty,
-                                              uint32_t tmem_base, Pipe& ps) {
+                                              uint32_t tmem_base, Pipe& ps, unsigned long long** first = nullptr) {
   const int lq = ew & 3;               // TMEM lane quarter == warp % 4 (rows lq*32 .. +31)
   const int ch = ew >> 2;              // column half of the 256-column accumulator
   uint8_t* const stg_base = staging + ew * 2 * STAGING_PER_WARP;
@@ -404,6 +470,10 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
   if (!zt) {
     mbar_wait(&tfull[ps.acc], ps.aphase);
     tc_fence_after();
+    if (first && *first) {
+      if (lane == 0) **first = globaltimer();
+      *first = nullptr;
+    }
   }
   if (p.dbg & 2) {
     if (!zt) release();
@@ -576,6 +646,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint16_t pmask = (uint16_t)(0x3u << (crank & ~1u));   // this pair's CTAs (commit multicast)
   const int csplit = p.cs > 1 ? (int)crank / CG : 0;          // cluster split-K: this pair's K-slice
   const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
+  unsigned long long* const cst = p.cta_stamps ? p.cta_stamps + (size_t)blockIdx.x * 8 : nullptr;
+  if (cst && threadIdx.x == 0) cst[0] = globaltimer();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -587,8 +659,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // pdl_late (a dW GEMM right after the dX GEMM it does not depend on): run
   // now, wait for the predecessor only before exiting, so successors still
   // see it complete (its own inputs were complete before the dX started).
-  if (!p.pdl_late) pdl_wait();
-  pdl_trigger();
+  const bool early = p.a_early && !AG && !BG && !p.pdl_late && p.cs <= 1;   // producer waits inside its first unit
+  if (!p.pdl_late && !(early && warp == 0)) pdl_wait();
+  if (!(early && warp == 0)) pdl_trigger();
+  if (cst && threadIdx.x == 0) cst[1] = globaltimer();
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMin(p.stamp, (unsigned long long)globaltimer());
   if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp, ~(unsigned long long)globaltimer());
 
@@ -602,24 +676,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   Pipe ps;
   if (warp == 0) {
+    bool waited = !early;
     for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
-      if (!wk.zero) produce_unit<KIND, CG, AG, BG>(&tmA, &tmB, p, wk, rank, leader, lane, ring, full, empty, ps);
+      if (wk.zero) continue;
+      if (!waited) {
+        if constexpr (!AG && !BG)
+          produce_unit_early<KIND, CG>(&tmA, &tmB, p, wk, rank, leader, lane, ring, full, empty, ps);
+        waited = true;
+      } else {
+        produce_unit<KIND, CG, AG, BG>(&tmA, &tmB, p, wk, rank, leader, lane, ring, full, empty, ps);
+      }
+    }
+    if (!waited) {
+      pdl_wait();
+      pdl_trigger();
     }
   } else if (warp == 1 && leader) {
+    unsigned long long* f = cst ? cst + 2 : nullptr;
     for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
-      if (!wk.zero) mma_unit<KIND, CG>(wk, lane, pmask, ring, full, empty, tfull, tempty, tmem_base, ps);
+      if (!wk.zero) mma_unit<KIND, CG>(wk, lane, pmask, ring, full, empty, tfull, tempty, tmem_base, ps, &f);
     }
+    if (cst && lane == 0) cst[3] = globaltimer();
   } else if (warp >= 4 && p.cs > 1) {
     // cluster split-K: this pair's K-slice is accumulated; reduced below
     mbar_wait(&tfull[0], 0);
     tc_fence_after();
   } else if (warp >= 4) {
+    unsigned long long* f = (cst && warp == 4) ? cst + 4 : nullptr;
     for (int u = u_first; u < sc.num_units; u += u_step)
       epilogue_unit<KIND, CG>(&tmO, &tmO2, &tmW, p, sc.S, sc.get(u), rank, warp - 4, lane, staging, tfull, tempty,
-                              tmem_base, ps);
+                              tmem_base, ps, &f);
+    if (cst && warp == 4 && lane == 0) cst[5] = globaltimer();
     if (lane < 8) bulk_wait0();   // all output writes performed before the CTA exits
+    if (cst && warp == 4 && lane == 0) cst[6] = globaltimer();
   }
 
   if (p.cs > 1) {
@@ -713,6 +804,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   kernel_teardown<CG>(tmem_base, warp);
   if (p.pdl_late) pdl_wait();
+  if (cst && threadIdx.x == 0) cst[7] = globaltimer();
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMax(p.stamp + 1, (unsigned long long)globaltimer());
   if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp + 1, (unsigned long long)globaltimer());
 }
@@ -1076,6 +1168,7 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    launch_seq().fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, mp.w, p);
     if (e != cudaSuccess) return e;
   }
@@ -1409,6 +1502,7 @@ cudaError_t gemm_group_launch(int k0, const GemmOperands& o0, GemmParams p0, int
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  launch_seq().fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ga);
   if (e != cudaSuccess) return e;
   e = post_launch<KIND_DX>(p0, num_sms, st);

@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <utility>
 
@@ -13,6 +14,14 @@ namespace ztp {
 // griddepcontrol.wait before touching memory (ztp_ptx.cuh pdl_wait).  Kept in
 // CUDA graphs as programmatic edges.  ZTP_PDL=0 turns it off (A/B timing).
 bool pdl_enabled();
+// Every kernel launch of the library (all four launch sites) bumps this
+// process-wide sequence: a GEMM may prefetch its A operand before its PDL wait
+// only if the launch right before it (no other launch since) was a GEMM whose
+// outputs are disjoint from that A (ztp_api.cu gemm, GemmParams::a_early).
+inline std::atomic<uint64_t>& launch_seq() {
+  static std::atomic<uint64_t> s{0};
+  return s;
+}
 // launch_k_pdl(pdl = false): plain stream order.  Used where an early-
 // launched elementwise kernel would occupy (squat) SMs while it waits: its
 // CTAs would take the SMs a concurrent side-stream GEMM is waiting for.
@@ -29,6 +38,7 @@ inline cudaError_t launch_k_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 b
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  launch_seq().fetch_add(1, std::memory_order_relaxed);
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>
@@ -44,6 +54,7 @@ inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t s
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  launch_seq().fetch_add(1, std::memory_order_relaxed);
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
@@ -83,9 +94,14 @@ struct GemmParams {
   int out_rows;  // rows of the output tensor(s)
   int out_dense; // the row map is the identity on m < M (set by the host): dense TMA box stores
   unsigned long long* prof_stamp;  // profiling: [max ~start, max end] %globaltimer (nullable)
+  unsigned long long* cta_stamps;  // profiling mode 3: per CTA 8 %globaltimer stamps (CTA start, after the
+                                   // PDL wait, first operand stage ready, last MMA commit, first accumulator
+                                   // ready, last tile's stores issued, stores complete, CTA end) (nullable)
   const int32_t* col_pos;  // DW output pruning: full column j <- compact column col_pos[j] (< 0: Zero)
   int n_full;              // full output columns when col_pos is set (N = compact columns)
   int pdl_late;            // inputs do not depend on the preceding kernel: PDL wait deferred to exit
+  int a_early;             // A is not written by the preceding kernel: the producer issues the first stages'
+                           // A loads before the PDL wait (only B waits for the predecessor)
   __nv_bfloat16* full_out; // DW output pruning without split-K: the epilogue writes compact columns to `out`
   int64_t ld_full;         // (a scratch) and the column spread writes full_out [out_rows, n_full]
   int cs;                  // DW cluster split-K: the `splits` K-slices of a tile run as one cluster and

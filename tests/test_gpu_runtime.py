@@ -125,13 +125,73 @@ def test_options_round_trip_and_errors():
     ctx = Z.ztp_ctx_create(0, 1, None, 0)
     try:
         for opt, val in ((Z.OPT_CONC, 0), (Z.OPT_DW_SHARE, 1.5), (Z.OPT_SQUAT_GUARD, 0), (Z.OPT_GATHER4, 1),
-                         (Z.OPT_SPLITK, 0), (Z.OPT_GROUP, 2), (Z.OPT_PEER_CTAS, 16)):
+                         (Z.OPT_SPLITK, 0), (Z.OPT_GROUP, 2), (Z.OPT_PEER_CTAS, 16), (Z.OPT_A_EARLY, 0),
+                         (Z.OPT_PART, 0), (Z.OPT_AUX_WEIGHT, 2.0)):
             Z.ztp_set_option(ctx, opt, val)
             assert Z.ztp_get_option(ctx, opt) == val
-        for opt, bad in ((Z.OPT_DW_SHARE, 0.0), (Z.OPT_GROUP, 3), (Z.OPT_PEER_CTAS, 0), (99, 1.0)):
+        for opt, bad in ((Z.OPT_DW_SHARE, 0.0), (Z.OPT_GROUP, 3), (Z.OPT_PEER_CTAS, 0), (Z.OPT_PART, 2),
+                         (Z.OPT_AUX_WEIGHT, -1.0), (99, 1.0)):
             with pytest.raises(Z.ZtpError) as ei:
                 Z.ztp_set_option(ctx, opt, bad)
             assert ei.value.name == "ZTP_EINVAL"
         assert Z.ztp_get_option(ctx, Z.OPT_GROUP) == 2
+    finally:
+        Z.ztp_ctx_destroy(ctx)
+
+
+@pytest.mark.parametrize("early", [1, 0])
+def test_gemm_chain_a_early(early):
+    """A-operand prefetch before the PDL wait (ZTP_OPT_A_EARLY): a chain of
+    FWD GEMMs where (2) reads the output of (1) as B with an untouched A
+    (prefetched early), (3) takes (1)'s output -- two launches back -- as its
+    A (prefetched early: (2) triggers its dependents only after its own
+    wait), (4) takes (3)'s output as A (not prefetched: the predecessor
+    writes it).  Eager results match a plain fp32 matmul; 20 graph replays
+    reproduce them bit for bit (a stale early read would differ)."""
+    import torch
+    import paper_2401_11469_b200 as Z
+    ctx = Z.ztp_ctx_create(0, 1, None, 0)
+    try:
+        Z.ztp_set_option(ctx, Z.OPT_A_EARLY, early)
+        g = torch.Generator(device="cpu").manual_seed(5)
+        rnd = lambda r, c, s=1.0: ((torch.rand(r, c, generator=g) - 0.5) * s).cuda().to(torch.bfloat16)  # noqa
+        K, n, N = 768, 512, 1536
+        X, W1, W2, B3, B4 = rnd(K, N), rnd(K, n, 0.1), rnd(n, n, 0.2), rnd(n, n), rnd(N, n, 0.1)
+        Y1 = torch.empty(n, N, device="cuda", dtype=torch.bfloat16)
+        Y2 = torch.empty(n, N, device="cuda", dtype=torch.bfloat16)
+        Y3 = torch.empty(N, n, device="cuda", dtype=torch.bfloat16)
+        Y4 = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
+        L = Z.linear_args
+        steps = [L(x_t=X, w_t=W1, y_t=Y1),        # Y1^T = W1^T' X^T          (A = W1)
+                 L(x_t=Y1, w_t=W2, y_t=Y2),       # Y2 = W2' Y1                (A = W2, B = Y1)
+                 L(x_t=B3, w_t=Y1, y_t=Y3),       # Y3 = Y1' B3                (A = Y1: two launches back)
+                 L(x_t=B4, w_t=Y3, y_t=Y4)]       # Y4 = Y3' B4                (A = Y3: the predecessor's output)
+        s = torch.cuda.Stream()
+
+        def run():
+            for a in steps:
+                Z.ztp_gemm(ctx, Z.KIND_FWD, a, s)
+        with torch.cuda.stream(s):
+            run()
+        torch.cuda.synchronize()
+        f = lambda t: t.float().cpu()  # noqa: E731
+        r1 = f(W1).t() @ f(X)
+        r2 = f(W2).t() @ f(Y1)
+        r3 = f(Y1).t() @ f(B3)
+        r4 = f(Y3).t() @ f(B4)
+        for got, ref in ((Y1, r1), (Y2, r2), (Y3, r3), (Y4, r4)):
+            err = (f(got) - ref).abs().max().item()
+            assert err <= 0.02 * ref.abs().max().item() + 1e-3, err
+        eager = [t.clone() for t in (Y1, Y2, Y3, Y4)]
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            run()
+        for _ in range(20):
+            for t in (Y1, Y2, Y3, Y4):
+                t.fill_(7.0)
+            gr.replay()
+            torch.cuda.synchronize()
+            for t, e in zip((Y1, Y2, Y3, Y4), eager):
+                assert torch.equal(t, e)
     finally:
         Z.ztp_ctx_destroy(ctx)

@@ -1,12 +1,9 @@
 #!/bin/bash
-# concurrent dX/dW SM split: modelled (ZTP_PART=1) vs proportional with dW weight 1.2 / 1.0
+# dX/dW partition model A/B (interleaved bench rounds) + graph timelines
 mkdir -p gpurun_out
-for i in 1 2; do
-for v in "ZTP_PART=1" "ZTP_DW_SHARE=1.2" "ZTP_DW_SHARE=1.0"; do
-env $v timeout -s KILL 300 python bench.py --no-cpu 2>&1 | tail -1 > gpurun_out/bench_part.txt
-python -c "
-import json;d=json.loads(open('gpurun_out/bench_part.txt').read());print('$v run $i', 'ms/step %.4f'%d['ms_per_step'], 'gemm_frac %.3f'%d['roofline']['frac'], 'gemm_ms %.4f'%d['roofline']['gemm_kernel_ms_per_step'])"
-done; done | tee gpurun_out/part_ab.txt
-ZTP_PART=1 timeout -s KILL 120 python tools/graph_timeline.py > gpurun_out/timeline_part1.txt 2>&1
-ZTP_DW_SHARE=1.2 timeout -s KILL 120 python tools/graph_timeline.py > gpurun_out/timeline_share12.txt 2>&1
-tail -13 gpurun_out/timeline_part1.txt; tail -13 gpurun_out/timeline_share12.txt
+for v in "ZTP_AUX_WEIGHT=1.4" "ZTP_AUX_WEIGHT=1.4 ZTP_PART=1" "ZTP_AUX_WEIGHT=1.7 ZTP_PART=1"; do
+  tag=$(echo $v | tr ' =' '_-')
+  env $v timeout -s KILL 300 python tools/graph_timeline.py > gpurun_out/part_graph_$tag.txt 2>&1
+done
+R=3 bash tools/gpu_ab2.sh "ZTP_AUX_WEIGHT=1.4" "ZTP_AUX_WEIGHT=1.0 ZTP_PART=1" "ZTP_AUX_WEIGHT=1.4 ZTP_PART=1" "ZTP_AUX_WEIGHT=1.7 ZTP_PART=1" "ZTP_AUX_WEIGHT=1.4 ZTP_PART=1 ZTP_DW_SHARE=1.0"
+cat gpurun_out/ab2.txt
