@@ -192,7 +192,7 @@ ztp_status ztp_transpose(ztp_ctx* ctx, const ztp_mat* src, const ztp_mat* dst, c
  *                                            the PDL wait (only B waits for the predecessor)
  *   ZTP_OPT_PART        (ZTP_PART, 1)        dX / dW SM partition: 0 work-proportional,
  *                                            1 wave-quantised (minimises the later finish)
- *   ZTP_OPT_AUX_WEIGHT  (ZTP_AUX_WEIGHT, 1.4) dX work factor in that partition when its epilogue
+ *   ZTP_OPT_AUX_WEIGHT  (ZTP_AUX_WEIGHT, 1.0) dX work factor in that partition when its epilogue
  *                                            reads an aux operand (GeLU')
  * ------------------------------------------------------------------------- */
 typedef enum ztp_option {

@@ -45,7 +45,7 @@ struct ztp_ctx {
   // 1.4 / 1.5 / 1.6 / 0.8 swept, profiles/r01_dw_share_sweep_v*.txt)
   double dw_share = 1.2;
   int part_model = 1;                  // ZTP_PART: 0 work-proportional dX / dW partition, 1 wave-quantised
-  double aux_weight = 1.4;             // ZTP_AUX_WEIGHT: dX work factor when its epilogue reads an aux operand
+  double aux_weight = 1.0;             // ZTP_AUX_WEIGHT: dX work factor when its epilogue reads an aux operand
   // While a concurrent dW is pending, the (non-persistent) core kernel is
   // launched in plain stream order: under PDL its CTAs would sit resident on
   // every free SM waiting for the dX GEMM, and the side-stream dW GEMM could

@@ -467,6 +467,25 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
   int sr[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) sr[j] = __shfl_sync(0xFFFFFFFFu, orow, (4 * lane + j) & 31);
+  const bool has_aux = (p.epi == EPI_GELU_GRAD || p.epi == EPI_MUL) && !zt;
+  // GeLU' operand (pre-activation, or GeLU'(pre) itself for EPI_MUL) of this
+  // lane's row: the first chunk into registers and the rest of the row's
+  // segment into L2 BEFORE waiting for the accumulator, so its HBM latency
+  // hides behind this tile's mainloop
+  uint4 pin[8];
+  auto load_aux = [&](int col0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      pin[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (m < p.n_kept && col0 + 8 * i < p.N)
+        pin[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (int64_t)arow * p.ld_aux + col0 + 8 * i));
+    }
+  };
+  if (has_aux) {
+    if (m < p.n_kept && nc0 + 72 <= p.N)
+      prefetch_l2_bulk(p.aux + (int64_t)arow * p.ld_aux + nc0 + 64, (uint32_t)min(64, p.N - nc0 - 64) / 8 * 16);
+    load_aux(nc0);
+  }
   if (!zt) {
     mbar_wait(&tfull[ps.acc], ps.aphase);
     tc_fence_after();
@@ -495,22 +514,11 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
     }
   };
   const bool two_planes = p.epi == EPI_GELU || p.epi == EPI_GELU_D;
-  const bool has_aux = (p.epi == EPI_GELU_GRAD || p.epi == EPI_MUL) && !zt;
 #pragma unroll 1
   for (int c = 0; c < BN / 128; ++c) {
     const int col0 = nc0 + c * 64;
     uint32_t v[64];
-    // GeLU' operand (pre-activation, or GeLU'(pre) itself for EPI_MUL):
-    // this lane's row, loaded before the TMEM load so the two overlap
-    uint4 pin[8];
-    if (has_aux) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        pin[i] = make_uint4(0u, 0u, 0u, 0u);
-        if (m < p.n_kept && col0 + 8 * i < p.N)
-          pin[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (int64_t)arow * p.ld_aux + col0 + 8 * i));
-      }
-    }
+    if (has_aux && c > 0) load_aux(col0);   // before the TMEM load so the two overlap (L2 hit)
     if (!zt) {
       tmem_ld_32x32b_x32(tbase + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
       tmem_ld_32x32b_x32(tbase + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
@@ -928,7 +936,7 @@ __device__ __forceinline__ void splitk_reduce_body(const GemmParams& p) {
       for (int s = 0; s < p.splits; ++s, src += p.ws_split_stride) {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (cc[q] >= 0) v[q] += __ldcg(src + cc[q]);
+          if (cc[q] >= 0) v[q] += __ldg(src + cc[q]);   // L1: the 8 gathers of a group share sectors
       }
     } else if (computed) {
       const float* src = p.ws + (int64_t)m * p.ld_ws + col;
@@ -1022,7 +1030,7 @@ __global__ void __launch_bounds__(256) ztp_dw_reduce(const GemmParams p) {
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
-          for (int q = 0; q < 8; ++q) t[s][q] = cc[q] >= 0 ? __ldcg(src + s * p.ws_split_stride + cc[q]) : 0.f;
+          for (int q = 0; q < 8; ++q) t[s][q] = cc[q] >= 0 ? __ldg(src + s * p.ws_split_stride + cc[q]) : 0.f;
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
