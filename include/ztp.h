@@ -194,6 +194,10 @@ ztp_status ztp_transpose(ztp_ctx* ctx, const ztp_mat* src, const ztp_mat* dst, c
  *                                            1 wave-quantised (minimises the later finish)
  *   ZTP_OPT_AUX_WEIGHT  (ZTP_AUX_WEIGHT, 1.0) dX work factor in that partition when its epilogue
  *                                            reads an aux operand (GeLU')
+ *   ZTP_OPT_FLAGS       (ZTP_FLAGS, 0)       a GEMM whose B operand is the output of the GEMM just
+ *                                            before it on the stream waits per 256-column block
+ *                                            on that GEMM's tile-completion counters instead of
+ *                                            its PDL wait (measured slower: off by default)
  * ------------------------------------------------------------------------- */
 typedef enum ztp_option {
   ZTP_OPT_CONC = 0,
@@ -205,7 +209,8 @@ typedef enum ztp_option {
   ZTP_OPT_PEER_CTAS = 6,
   ZTP_OPT_A_EARLY = 7,
   ZTP_OPT_PART = 8,
-  ZTP_OPT_AUX_WEIGHT = 9
+  ZTP_OPT_AUX_WEIGHT = 9,
+  ZTP_OPT_FLAGS = 10
 } ztp_option;
 ztp_status ztp_set_option(ztp_ctx* ctx, ztp_option opt, double value);
 ztp_status ztp_get_option(const ztp_ctx* ctx, ztp_option opt, double* value);

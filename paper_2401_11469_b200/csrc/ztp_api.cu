@@ -63,6 +63,21 @@ struct ztp_ctx {
   cudaStream_t lg_stream = nullptr;
   const char* lg_out[2] = {nullptr, nullptr};
   size_t lg_bytes[2] = {0, 0};
+  int64_t lg_ld[2] = {0, 0}, lg_cols[2] = {0, 0};
+  const char* lg_in[3] = {nullptr, nullptr, nullptr};   // its A, B and aux operands
+  size_t lg_in_bytes[3] = {0, 0, 0};
+  unsigned long long* lg_slot = nullptr;                // its tile-completion flag slot (nullptr: none)
+  // Tile-completion flags between consecutive GEMMs of a stream (ZTP_FLAGS,
+  // ZTP_OPT_FLAGS): slots of [target, FLAG_NB column-block counters],
+  // cumulative (never reset), used round-robin
+  // Each stream owns a partition of 16 slots (4 streams; further streams get
+  // no flags), so two producers sharing a slot are always ordered on one
+  // stream: a consumer's wait can only be on its own producer's tiles.
+  int flags_opt = 0;
+  static constexpr int FLAG_SLOTS = 64, FLAG_PART = 16;
+  unsigned long long* d_tflags = nullptr;
+  cudaStream_t flag_stream[FLAG_SLOTS / FLAG_PART] = {};
+  int flag_next[FLAG_SLOTS / FLAG_PART] = {};
   int group_bwd = 0;                   // 0 never (default), 1 always, 2 small pairs only (measured: no net gain)
   int sm_cap = 0;                      // > 0: SMs a GEMM launch may use (concurrent dX / dW partition)
   bool side_pending = false;           // side-stream work not yet joined into a caller stream
@@ -433,17 +448,74 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
       p.prof_stamp = c->d_pstamp + 2 * (c->pstamp_used++);
     }
     const int nsm = c->sm_cap > 0 ? c->sm_cap : c->num_sms;
+    // byte ranges this GEMM reads and writes
+    const char* a0 = static_cast<const char*>(a.ptr);
+    const size_t a_bytes = (size_t)(A.compact ? nk : a.rows) * a.ld * 2;
+    const char* b0 = static_cast<const char*>(b.ptr);
+    const int64_t b_rows = (kind == ztp::KIND_FWD && B.compact) ? nk : b.rows;
+    const size_t b_bytes = (size_t)b_rows * b.ld * 2;
+    const char* x0 = aux ? static_cast<const char*>(aux->ptr) : nullptr;
+    const size_t x_bytes = aux ? (size_t)aux->rows * aux->ld * 2 : 0;
+    const char* o0 = static_cast<const char*>(out.ptr);
+    const size_t o_bytes = (size_t)out.rows * out.ld * 2;
+    const char* o1 = out2 ? static_cast<const char*>(out2->ptr) : nullptr;
+    const size_t o1_bytes = out2 ? (size_t)out2->rows * out2->ld * 2 : 0;
+    auto ovl = [](const char* u, size_t nu, const char* v, size_t nv) { return u && v && u < v + nv && v < u + nu; };
     {
-      // A untouched by the immediately preceding kernel: a GEMM of this stream
-      // with nothing launched since (so it waited on ITS predecessor before it
-      // triggered this launch) whose outputs are disjoint from A
-      const char* a0 = static_cast<const char*>(a.ptr);
-      const char* a1 = a0 + (size_t)(A.compact ? nk : a.rows) * a.ld * 2;
-      bool ok = c->a_early && c->lg_id == (int64_t)ztp::launch_seq().load() && c->lg_stream == st &&
-                !o.a_gather && !o.b_gather && !p.pdl_late;
-      for (int k = 0; ok && k < 2; ++k)
-        if (c->lg_out[k] && a0 < c->lg_out[k] + c->lg_bytes[k] && c->lg_out[k] < a1) ok = false;
-      p.a_early = ok ? 1 : 0;
+      // the previous launch on this stream -- the kernel this one is
+      // programmatically dependent on -- is the GEMM recorded below (it
+      // triggered this launch only after ITS predecessor completed)
+      const bool chain = c->lg_id >= 0 && c->lg_stream == st && c->lg_id == (int64_t)ztp::last_launch_on(st) &&
+                         !o.a_gather && !o.b_gather && !p.pdl_late;
+      bool a_ok = chain;   // A untouched by that GEMM
+      for (int k = 0; a_ok && k < 2; ++k)
+        if (ovl(a0, a_bytes, c->lg_out[k], c->lg_bytes[k])) a_ok = false;
+      // flag consumer: B is (a row range of) one of its outputs with the same
+      // column origin and column blocks; nothing else read here is written
+      // there, nothing written here is touched there
+      int src = -1;
+      if (chain && a_ok && c->flags_opt && c->lg_slot && kind != ztp::KIND_DW && p.cs <= 1)
+        for (int k = 0; k < 2; ++k)
+          if (c->lg_out[k] && b.ld == c->lg_ld[k] && b0 >= c->lg_out[k] &&
+              b0 + b_bytes <= c->lg_out[k] + c->lg_bytes[k] && (size_t)(b0 - c->lg_out[k]) % (size_t)(b.ld * 2) == 0 &&
+              b.cols <= c->lg_cols[k])
+            src = k;
+      bool fl = src >= 0;
+      for (int k = 0; fl && k < 2; ++k)
+        if (ovl(x0, x_bytes, c->lg_out[k], c->lg_bytes[k])) fl = false;
+      for (int k = 0; fl && k < 3; ++k)
+        if (ovl(o0, o_bytes, c->lg_in[k], c->lg_in_bytes[k]) || ovl(o1, o1_bytes, c->lg_in[k], c->lg_in_bytes[k]))
+          fl = false;
+      for (int k = 0; fl && k < 2; ++k)
+        if (ovl(o0, o_bytes, c->lg_out[k], c->lg_bytes[k]) || ovl(o1, o1_bytes, c->lg_out[k], c->lg_bytes[k]))
+          fl = false;
+      if (fl) {
+        p.fi_target = c->lg_slot;
+        p.fi_flags = c->lg_slot + 1;
+      }
+      p.a_early = (c->a_early && a_ok && !fl) ? 1 : 0;
+    }
+    // a possible flag producer for the next GEMM of this stream (the launcher
+    // drops the flags if its split-K / spread / width rules out a producer)
+    const bool fprod = c->flags_opt && kind != ztp::KIND_DW && !p.pdl_late && !emulating(c) && p.splits == 1 &&
+                       p.cs <= 1 && !p.col_pos && (N + 255) / 256 <= ztp::FLAG_NB;
+    unsigned long long* slot = nullptr;
+    if (fprod) {
+      constexpr int NP = ztp_ctx::FLAG_SLOTS / ztp_ctx::FLAG_PART;
+      int part = -1;
+      for (int q = 0; q < NP && part < 0; ++q)
+        if (c->flag_stream[q] == st && c->flag_next[q] > 0) part = q;
+      for (int q = 0; q < NP && part < 0; ++q)
+        if (c->flag_next[q] == 0) {
+          part = q;
+          c->flag_stream[q] = st;
+        }
+      if (part >= 0) {
+        const int k = part * ztp_ctx::FLAG_PART + (c->flag_next[part]++ % ztp_ctx::FLAG_PART);
+        slot = c->d_tflags + (size_t)k * (1 + ztp::FLAG_NB);
+        p.fo_target = slot;
+        p.fo_flags = slot + 1;
+      }
     }
     const uint64_t seq0 = ztp::launch_seq().load();
     if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, nsm, st));
@@ -451,13 +523,24 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     if (extra) ++c->launches;   // split-K reduce or column spread
     c->lg_id = -1;
     if (!extra && !p.pdl_late && !emulating(c) && ztp::launch_seq().load() == seq0 + 1) {   // exactly the GEMM
-      // the launch the next GEMM may prefetch its A behind
-      c->lg_id = (int64_t)ztp::launch_seq().load();
+      // the launch the next GEMM may prefetch its A behind / wait on per column block
+      c->lg_id = (int64_t)ztp::last_launch_on(st);
       c->lg_stream = st;
-      c->lg_out[0] = static_cast<const char*>(out.ptr);
-      c->lg_bytes[0] = (size_t)out.rows * out.ld * 2;
-      c->lg_out[1] = out2 ? static_cast<const char*>(out2->ptr) : nullptr;
-      c->lg_bytes[1] = out2 ? (size_t)out2->rows * out2->ld * 2 : 0;
+      c->lg_out[0] = o0;
+      c->lg_bytes[0] = o_bytes;
+      c->lg_ld[0] = out.ld;
+      c->lg_cols[0] = out.cols;
+      c->lg_out[1] = o1;
+      c->lg_bytes[1] = o1_bytes;
+      c->lg_ld[1] = out2 ? out2->ld : 0;
+      c->lg_cols[1] = out2 ? out2->cols : 0;
+      c->lg_in[0] = a0;
+      c->lg_in_bytes[0] = a_bytes;
+      c->lg_in[1] = b0;
+      c->lg_in_bytes[1] = b_bytes;
+      c->lg_in[2] = x0;
+      c->lg_in_bytes[2] = x_bytes;
+      c->lg_slot = slot;
     }
   } else {
     if (col_pos) return fail(c, ZTP_EUNSUPPORTED, "f32 path: output pruning");
@@ -1160,13 +1243,16 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* sg = getenv("ZTP_SQUAT_GUARD")) c->squat_guard = atoi(sg) != 0;
   if (const char* gb = getenv("ZTP_GROUP")) c->group_bwd = atoi(gb);
   if (const char* ae = getenv("ZTP_A_EARLY")) c->a_early = atoi(ae) != 0;
+  if (const char* fl = getenv("ZTP_FLAGS")) c->flags_opt = atoi(fl) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
   auto cleanup = [&](ztp_status s) {
     ztp_ctx_destroy(c);
     return s;
   };
-  if (cudaMalloc(&c->d_flags, 64) != cudaSuccess || cudaMalloc(&c->d_stamp, 32) != cudaSuccess ||
+  if (cudaMalloc(&c->d_tflags, sizeof(unsigned long long) * ztp_ctx::FLAG_SLOTS * (1 + ztp::FLAG_NB)) != cudaSuccess ||
+      cudaMemset(c->d_tflags, 0, sizeof(unsigned long long) * ztp_ctx::FLAG_SLOTS * (1 + ztp::FLAG_NB)) != cudaSuccess ||
+      cudaMalloc(&c->d_flags, 64) != cudaSuccess || cudaMalloc(&c->d_stamp, 32) != cudaSuccess ||
       cudaMalloc(&c->d_gemm_ns, 16) != cudaSuccess || cudaMalloc(&c->d_stats, 2 * (ZTP_MAX_RANKS + 1) * sizeof(double)) != cudaSuccess)
     return cleanup(fail(nullptr, ZTP_ECUDA, "ztp_ctx_create: device allocation failed"));
   cudaMemset(c->d_flags, 0, 64);
@@ -1212,6 +1298,7 @@ ztp_status ztp_ctx_destroy(ztp_ctx* c) {
   if (c->d_pstamp) cudaFree(c->d_pstamp);
   if (c->d_ctastamp) cudaFree(c->d_ctastamp);
   cudaFree(c->d_flags);
+  cudaFree(c->d_tflags);
   cudaFree(c->d_stamp);
   cudaFree(c->d_gemm_ns);
   cudaFree(c->d_stats);
@@ -1804,6 +1891,7 @@ ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
       if (!(v > 0.0)) return fail(c, ZTP_EINVAL, "ztp_set_option: aux weight must be > 0");
       c->aux_weight = v;
       return ZTP_OK;
+    case ZTP_OPT_FLAGS: c->flags_opt = iv != 0; return ZTP_OK;
   }
   return fail(c, ZTP_EINVAL, "ztp_set_option: unknown option " + std::to_string((int)opt));
 }
@@ -1821,6 +1909,7 @@ ztp_status ztp_get_option(const ztp_ctx* c, ztp_option opt, double* v) {
     case ZTP_OPT_A_EARLY: *v = c->a_early; return ZTP_OK;
     case ZTP_OPT_PART: *v = c->part_model; return ZTP_OK;
     case ZTP_OPT_AUX_WEIGHT: *v = c->aux_weight; return ZTP_OK;
+    case ZTP_OPT_FLAGS: *v = c->flags_opt; return ZTP_OK;
   }
   return fail(nullptr, ZTP_EINVAL, "ztp_get_option: unknown option " + std::to_string((int)opt));
 }

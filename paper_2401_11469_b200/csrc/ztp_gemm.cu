@@ -173,13 +173,29 @@ struct Pipe {
 };
 
 // ---- TMA producer of one work unit (warp 0).
+// A consumer's wait for a column block of its producer's output (ZTP_FLAGS):
+// acquire the block's completion count, then order the TMA loads after it.
+// A count that never arrives (a broken dependency) traps after 2 s instead
+// of hanging the device.
+__device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned long long tgt) {
+  if (ld_acquire_u64(f) < tgt) {
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_u64(f) < tgt) {
+      __nanosleep(64);
+      if (globaltimer() - t0 > 2000000000ull) __trap();
+    }
+  }
+  fence_proxy_async_global();
+}
+
 // AG / BG: operand A / B gathered row-by-row with TMA gather4 through the
 // lineage list (true) or loaded as dense TMA boxes from a compact, already
 // row-selected tensor (false; rows past the compact extent are zero-filled).
 template <int KIND, int CG, bool AG, bool BG>
 __device__ __forceinline__ void produce_unit(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmParams& p,
                                              const Work& wk, int rank, bool leader, int lane, uint8_t* ring,
-                                             uint64_t* full, uint64_t* empty, Pipe& ps) {
+                                             uint64_t* full, uint64_t* empty, Pipe& ps,
+                                             unsigned long long ftgt = 0) {
   using C = Cfg<CG>;
   constexpr int BNL = C::BNL;
   const int am0 = wk.m0 + BM * rank;   // this CTA's 128 rows of the tile (A)
@@ -235,6 +251,7 @@ __device__ __forceinline__ void produce_unit(const CUtensorMap* tmA, const CUten
           load(tmA, sa, am0, kb * BK);
           load(tmA, sa + 8192, am0 + 64, kb * BK);
         }
+        if (p.fi_flags && kb == wk.kb0) flag_wait(p.fi_flags + wk.n0 / BN, ftgt);
         if (!BG) {
 #pragma unroll
           for (int b = 0; b < BNL / 64; ++b) load(tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
@@ -245,6 +262,7 @@ __device__ __forceinline__ void produce_unit(const CUtensorMap* tmA, const CUten
       if (AG) gather(tmA, sa + lane * 512, kb * BK, ar0, ar1, ar2, ar3);
       if (lane == 0) {
         if (!AG) load(tmA, sa, kb * BK, am0);
+        if (p.fi_flags && kb == wk.kb0) flag_wait(p.fi_flags + wk.n0 / BN, ftgt);
         if (KIND == KIND_DX) {
           // B = G^T [n, N] MN-major dense: 64 contraction rows x BNL columns
 #pragma unroll
@@ -661,15 +679,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
+  if (p.fo_target && blockIdx.x == 0 && threadIdx.x == 0) {
+    // this launch's share of the slot's cumulative target, also added to the
+    // column blocks it does not produce (so every block of the slot keeps
+    // pace with the target); before CTA 0 can trigger a consumer
+    atomicAdd(p.fo_target, p.fo_T);
+    for (int nb = p.fo_nb; nb < FLAG_NB; ++nb) atomicAdd(p.fo_flags + nb, p.fo_T);
+    __threadfence();
+  }
   const uint32_t tmem_base = kernel_prologue<CG>(full, empty, tfull, tempty, tmem_slot, warp);
   // prologue done (barriers, TMEM, descriptor prefetch): wait for the
   // preceding kernel's results, let the next kernel begin its own prologue.
   // pdl_late (a dW GEMM right after the dX GEMM it does not depend on): run
   // now, wait for the predecessor only before exiting, so successors still
   // see it complete (its own inputs were complete before the dX started).
-  const bool early = p.a_early && !AG && !BG && !p.pdl_late && p.cs <= 1;   // producer waits inside its first unit
-  if (!p.pdl_late && !(early && warp == 0)) pdl_wait();
-  if (!(early && warp == 0)) pdl_trigger();
+  // flag consumer: only B comes from the preceding kernel, and it is waited
+  // for per column block; the PDL wait (and, after it, the trigger -- so a
+  // successor launched off it sees everything up to the producer complete)
+  // is left to warp 3
+  const bool fcons = !AG && !BG && p.fi_flags != nullptr;
+  const bool early = !fcons && p.a_early && !AG && !BG && !p.pdl_late && p.cs <= 1;   // producer waits in unit 1
+  if (fcons) {
+    if (warp == 3) {
+      pdl_wait();
+      pdl_trigger();
+    }
+  } else {
+    if (!p.pdl_late && !(early && warp == 0)) pdl_wait();
+    if (!(early && warp == 0)) pdl_trigger();
+  }
   if (cst && threadIdx.x == 0) cst[1] = globaltimer();
   if (p.stamp != nullptr && threadIdx.x == 0) atomicMin(p.stamp, (unsigned long long)globaltimer());
   if (p.prof_stamp != nullptr && threadIdx.x == 0) atomicMax(p.prof_stamp, ~(unsigned long long)globaltimer());
@@ -685,6 +723,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   Pipe ps;
   if (warp == 0) {
     bool waited = !early;
+    const unsigned long long ftgt = fcons ? ld_acquire_u64(p.fi_target) : 0ull;
     for (int u = u_first; u < sc.num_units; u += u_step) {
       const Work wk = sc.get(u);
       if (wk.zero) continue;
@@ -693,7 +732,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           produce_unit_early<KIND, CG>(&tmA, &tmB, p, wk, rank, leader, lane, ring, full, empty, ps);
         waited = true;
       } else {
-        produce_unit<KIND, CG, AG, BG>(&tmA, &tmB, p, wk, rank, leader, lane, ring, full, empty, ps);
+        produce_unit<KIND, CG, AG, BG>(&tmA, &tmB, p, wk, rank, leader, lane, ring, full, empty, ps, ftgt);
       }
     }
     if (!waited) {
@@ -713,11 +752,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
   } else if (warp >= 4) {
     unsigned long long* f = (cst && warp == 4) ? cst + 4 : nullptr;
-    for (int u = u_first; u < sc.num_units; u += u_step)
-      epilogue_unit<KIND, CG>(&tmO, &tmO2, &tmW, p, sc.S, sc.get(u), rank, warp - 4, lane, staging, tfull, tempty,
+    // flag producer: a unit's column block is counted once its stores are
+    // performed -- checked one unit later (at most the last unit's bulk
+    // groups still pending), so the epilogue never stalls on its own stores
+    int pend0 = -1, pend1 = -1;
+    const bool two = p.epi == EPI_GELU || p.epi == EPI_GELU_D;
+    for (int u = u_first; u < sc.num_units; u += u_step) {
+      const Work wk = sc.get(u);
+      if (p.fo_flags && pend1 >= 0) {
+        if (lane < 8) {
+          if (two)
+            bulk_wait_n<4>();
+          else
+            bulk_wait_n<2>();
+        }
+        __syncwarp();
+        if (lane == 0) {
+          fence_proxy_async_global();
+          red_release_add_u64(p.fo_flags + pend1, 1ull);
+        }
+      }
+      epilogue_unit<KIND, CG>(&tmO, &tmO2, &tmW, p, sc.S, wk, rank, warp - 4, lane, staging, tfull, tempty,
                               tmem_base, ps, &f);
+      pend1 = pend0;
+      pend0 = wk.n0 / BN;
+    }
     if (cst && warp == 4 && lane == 0) cst[5] = globaltimer();
     if (lane < 8) bulk_wait0();   // all output writes performed before the CTA exits
+    if (p.fo_flags) {
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async_global();
+        if (pend1 >= 0) red_release_add_u64(p.fo_flags + pend1, 1ull);
+        if (pend0 >= 0) red_release_add_u64(p.fo_flags + pend0, 1ull);
+      }
+    }
     if (cst && warp == 4 && lane == 0) cst[6] = globaltimer();
   }
 
@@ -1161,6 +1230,17 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
   }
   const int units = units_of(KIND, CG, p);
   const int pairs = p.cs > 1 ? units : std::min(units, num_sms / CG);   // cluster split-K: one unit per pair
+  GemmParams pl = p;
+  if (pl.fo_flags) {
+    const int n_tiles = (p.N + BN - 1) / BN;
+    if (p.splits != 1 || p.cs > 1 || p.col_pos || n_tiles > FLAG_NB || units % n_tiles) {
+      pl.fo_flags = nullptr;   // not a flag producer
+      pl.fo_target = nullptr;
+    } else {
+      pl.fo_nb = n_tiles;
+      pl.fo_T = (unsigned long long)(units / n_tiles) * EPI_WARPS * CG;
+    }
+  }
   if (pairs > 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(pairs * CG);
@@ -1176,8 +1256,8 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    launch_seq().fetch_add(1, std::memory_order_relaxed);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, mp.w, p);
+    note_launch(st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, mp.w, pl);
     if (e != cudaSuccess) return e;
   }
   return post_launch<KIND>(p, num_sms, st);
@@ -1510,7 +1590,7 @@ cudaError_t gemm_group_launch(int k0, const GemmOperands& o0, GemmParams p0, int
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  launch_seq().fetch_add(1, std::memory_order_relaxed);
+  note_launch(cfg.stream);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ga);
   if (e != cudaSuccess) return e;
   e = post_launch<KIND_DX>(p0, num_sms, st);

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <utility>
 
 namespace ztp {
@@ -22,6 +23,39 @@ inline std::atomic<uint64_t>& launch_seq() {
   static std::atomic<uint64_t> s{0};
   return s;
 }
+// ... and the sequence number of the last launch per stream: the kernel a
+// launch on `st` is programmatically dependent on is the previous launch on
+// `st` (other streams' launches do not matter for PDL).
+struct StreamSeqs {
+  std::mutex mu;
+  cudaStream_t s[32];
+  uint64_t seq[32];
+  int n = 0;
+};
+inline StreamSeqs& stream_seqs() {
+  static StreamSeqs x;
+  return x;
+}
+inline void note_launch(cudaStream_t st) {
+  const uint64_t q = launch_seq().fetch_add(1, std::memory_order_relaxed) + 1;
+  StreamSeqs& x = stream_seqs();
+  std::lock_guard<std::mutex> g(x.mu);
+  for (int i = 0; i < x.n; ++i)
+    if (x.s[i] == st) {
+      x.seq[i] = q;
+      return;
+    }
+  const int i = x.n < 32 ? x.n++ : (int)(q % 32);   // evicted streams read 0 (never a match)
+  x.s[i] = st;
+  x.seq[i] = q;
+}
+inline uint64_t last_launch_on(cudaStream_t st) {
+  StreamSeqs& x = stream_seqs();
+  std::lock_guard<std::mutex> g(x.mu);
+  for (int i = 0; i < x.n; ++i)
+    if (x.s[i] == st) return x.seq[i];
+  return 0;
+}
 // launch_k_pdl(pdl = false): plain stream order.  Used where an early-
 // launched elementwise kernel would occupy (squat) SMs while it waits: its
 // CTAs would take the SMs a concurrent side-stream GEMM is waiting for.
@@ -38,7 +72,7 @@ inline cudaError_t launch_k_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 b
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
-  launch_seq().fetch_add(1, std::memory_order_relaxed);
+  note_launch(st);
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>
@@ -54,7 +88,7 @@ inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t s
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  launch_seq().fetch_add(1, std::memory_order_relaxed);
+  note_launch(st);
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
@@ -67,6 +101,7 @@ enum { KIND_FWD = 0, KIND_DX = 1, KIND_DW = 2 };
 // EPI_GELU_GRAD: out <- acc * GeLU'(aux).  EPI_MUL: out <- acc * aux (aux = GeLU'(pre)).
 enum { EPI_NONE = 0, EPI_GELU = 1, EPI_GELU_GRAD = 2, EPI_GELU_D = 3, EPI_MUL = 4 };
 
+constexpr int FLAG_NB = 64;   // column blocks (256 tokens) a flag slot covers
 struct GemmParams {
   int M, N;            // output rows (M) and columns (N)
   int kdim;            // contraction length (FWD: n_kept; DX: n_out; DW: tokens)
@@ -102,6 +137,18 @@ struct GemmParams {
   int pdl_late;            // inputs do not depend on the preceding kernel: PDL wait deferred to exit
   int a_early;             // A is not written by the preceding kernel: the producer issues the first stages'
                            // A loads before the PDL wait (only B waits for the predecessor)
+  // Tile-completion flags between consecutive GEMMs of a stream (ZTP_FLAGS):
+  // a producer counts, per 256-column block of its output, the epilogue
+  // warps whose stores of a tile are complete (fo_flags[nb] += 1 each, and
+  // fo_target += fo_T once per launch: cumulative, never reset); a consumer
+  // whose B operand is that output waits for fo_flags[nb] >= target before
+  // loading B for a tile of column block nb, instead of the PDL wait.
+  unsigned long long* fo_flags;
+  unsigned long long* fo_target;
+  unsigned long long fo_T;     // set by the launcher: units per column block x EPI_WARPS x CG
+  int fo_nb;                   // column blocks of this launch
+  const unsigned long long* fi_flags;
+  const unsigned long long* fi_target;
   __nv_bfloat16* full_out; // DW output pruning without split-K: the epilogue writes compact columns to `out`
   int64_t ld_full;         // (a scratch) and the column spread writes full_out [out_rows, n_full]
   int cs;                  // DW cluster split-K: the `splits` K-slices of a tile run as one cluster and

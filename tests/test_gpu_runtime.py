@@ -126,7 +126,7 @@ def test_options_round_trip_and_errors():
     try:
         for opt, val in ((Z.OPT_CONC, 0), (Z.OPT_DW_SHARE, 1.5), (Z.OPT_SQUAT_GUARD, 0), (Z.OPT_GATHER4, 1),
                          (Z.OPT_SPLITK, 0), (Z.OPT_GROUP, 2), (Z.OPT_PEER_CTAS, 16), (Z.OPT_A_EARLY, 0),
-                         (Z.OPT_PART, 0), (Z.OPT_AUX_WEIGHT, 2.0)):
+                         (Z.OPT_PART, 0), (Z.OPT_AUX_WEIGHT, 2.0), (Z.OPT_FLAGS, 1)):
             Z.ztp_set_option(ctx, opt, val)
             assert Z.ztp_get_option(ctx, opt) == val
         for opt, bad in ((Z.OPT_DW_SHARE, 0.0), (Z.OPT_GROUP, 3), (Z.OPT_PEER_CTAS, 0), (Z.OPT_PART, 2),
@@ -139,8 +139,8 @@ def test_options_round_trip_and_errors():
         Z.ztp_ctx_destroy(ctx)
 
 
-@pytest.mark.parametrize("early", [1, 0])
-def test_gemm_chain_a_early(early):
+@pytest.mark.parametrize("early,flags", [(1, 0), (0, 0), (1, 1)])
+def test_gemm_chain_a_early(early, flags):
     """A-operand prefetch before the PDL wait (ZTP_OPT_A_EARLY): a chain of
     FWD GEMMs where (2) reads the output of (1) as B with an untouched A
     (prefetched early), (3) takes (1)'s output -- two launches back -- as its
@@ -153,6 +153,7 @@ def test_gemm_chain_a_early(early):
     ctx = Z.ztp_ctx_create(0, 1, None, 0)
     try:
         Z.ztp_set_option(ctx, Z.OPT_A_EARLY, early)
+        Z.ztp_set_option(ctx, Z.OPT_FLAGS, flags)   # (2) then waits on (1)'s tile-completion counters
         g = torch.Generator(device="cpu").manual_seed(5)
         rnd = lambda r, c, s=1.0: ((torch.rand(r, c, generator=g) - 0.5) * s).cuda().to(torch.bfloat16)  # noqa
         K, n, N = 768, 512, 1536
