@@ -198,6 +198,12 @@ ztp_status ztp_transpose(ztp_ctx* ctx, const ztp_mat* src, const ztp_mat* dst, c
  *                                            before it on the stream waits per 256-column block
  *                                            on that GEMM's tile-completion counters instead of
  *                                            its PDL wait (measured slower: off by default)
+ *   ZTP_OPT_SPREAD_EPI  (ZTP_SPREAD_EPI, 0)  an output-pruned dW without split-K (out_sel set) is
+ *                                            written in full by the GEMM epilogue (lane = row: kept
+ *                                            columns from the staged row, Zero units in between,
+ *                                            16-byte stores); 0: compact scratch + a column-spread
+ *                                            pass (measured: on par at c4, slower at c5 -- the
+ *                                            scattered row stores make the epilogue L1-bound)
  * ------------------------------------------------------------------------- */
 typedef enum ztp_option {
   ZTP_OPT_CONC = 0,
@@ -210,7 +216,8 @@ typedef enum ztp_option {
   ZTP_OPT_A_EARLY = 7,
   ZTP_OPT_PART = 8,
   ZTP_OPT_AUX_WEIGHT = 9,
-  ZTP_OPT_FLAGS = 10
+  ZTP_OPT_FLAGS = 10,
+  ZTP_OPT_SPREAD_EPI = 11
 } ztp_option;
 ztp_status ztp_set_option(ztp_ctx* ctx, ztp_option opt, double value);
 ztp_status ztp_get_option(const ztp_ctx* ctx, ztp_option opt, double* value);

@@ -59,6 +59,7 @@ struct ztp_ctx {
   // A-operand loads before the PDL wait when the preceding library launch was
   // a GEMM on the same stream whose outputs do not overlap A (ZTP_A_EARLY, default 1)
   int a_early = 1;
+  int spread_epi = 0;         // output-pruned unsplit dW: column spread inside the GEMM epilogue (opt-in)
   int64_t lg_id = -1;                  // ztp::launch_seq() right after the last eligible GEMM launch (-1: none)
   cudaStream_t lg_stream = nullptr;
   const char* lg_out[2] = {nullptr, nullptr};
@@ -355,8 +356,14 @@ ztp_status gemm_build_bf16(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, co
     p.splits = 1;
     p.kb_per_split = (kdim + 63) / 64;
   }
-  (void)col_kept;
-  if (col_pos && p.splits == 1) {
+  if (col_pos && p.splits == 1 && c->spread_epi && col_kept) {
+    // output pruning without split-K: the epilogue writes dW in full, its
+    // kept columns from the staged tile and the Zero units in between
+    p.spread = 1;
+    p.col_kept = col_kept;
+    p.full_out = p.out;
+    p.ld_full = p.ld_out;
+  } else if (col_pos && p.splits == 1) {
     // output pruning without split-K: the epilogue writes the compact
     // columns to a scratch (one per stream), the column spread writes dW in
     // full, Zero units included.  (Spreading inside the epilogue, by
@@ -519,7 +526,7 @@ ztp_status gemm(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, const int32_t
     }
     const uint64_t seq0 = ztp::launch_seq().load();
     if (!(c->dbg_skip & 16)) CUDA_TRY(c, ztp::gemm_launch(kind, o, p, nsm, st));
-    const bool extra = (p.splits > 1 && p.cs <= 1) || p.col_pos;
+    const bool extra = (p.splits > 1 && p.cs <= 1) || (p.col_pos && !p.spread);
     if (extra) ++c->launches;   // split-K reduce or column spread
     c->lg_id = -1;
     if (!extra && !p.pdl_late && !emulating(c) && ztp::launch_seq().load() == seq0 + 1) {   // exactly the GEMM
@@ -648,7 +655,8 @@ ztp_status gemm_group(ztp_ctx* c, const GemmSpec& x, const GemmSpec& w, cudaStre
                                        "(run the step once eagerly first)");
     CUDA_TRY(c, e);
   }
-  c->launches += 1 + ((p1.splits > 1 || p1.col_pos) ? 1 : 0) + ((p0.splits > 1 || p0.col_pos) ? 1 : 0);
+  c->launches += 1 + ((p1.splits > 1 || (p1.col_pos && !p1.spread)) ? 1 : 0) +
+                 ((p0.splits > 1 || (p0.col_pos && !p0.spread)) ? 1 : 0);
   const ztp_status s = after_gemm(c, st);
   prof_end(c, pe, st);
   return s;
@@ -1243,6 +1251,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* sg = getenv("ZTP_SQUAT_GUARD")) c->squat_guard = atoi(sg) != 0;
   if (const char* gb = getenv("ZTP_GROUP")) c->group_bwd = atoi(gb);
   if (const char* ae = getenv("ZTP_A_EARLY")) c->a_early = atoi(ae) != 0;
+  if (const char* se = getenv("ZTP_SPREAD_EPI")) c->spread_epi = atoi(se) != 0;
   if (const char* fl = getenv("ZTP_FLAGS")) c->flags_opt = atoi(fl) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
@@ -1892,6 +1901,7 @@ ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
       c->aux_weight = v;
       return ZTP_OK;
     case ZTP_OPT_FLAGS: c->flags_opt = iv != 0; return ZTP_OK;
+    case ZTP_OPT_SPREAD_EPI: c->spread_epi = iv != 0; return ZTP_OK;
   }
   return fail(c, ZTP_EINVAL, "ztp_set_option: unknown option " + std::to_string((int)opt));
 }
@@ -1910,6 +1920,7 @@ ztp_status ztp_get_option(const ztp_ctx* c, ztp_option opt, double* v) {
     case ZTP_OPT_PART: *v = c->part_model; return ZTP_OK;
     case ZTP_OPT_AUX_WEIGHT: *v = c->aux_weight; return ZTP_OK;
     case ZTP_OPT_FLAGS: *v = c->flags_opt; return ZTP_OK;
+    case ZTP_OPT_SPREAD_EPI: *v = c->spread_epi; return ZTP_OK;
   }
   return fail(nullptr, ZTP_EINVAL, "ztp_get_option: unknown option " + std::to_string((int)opt));
 }

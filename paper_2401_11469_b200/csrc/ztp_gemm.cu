@@ -531,6 +531,76 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
       bulk_commit();
     }
   };
+  // Output-pruned dW written in full (p.spread).  The chunk's compact
+  // columns [col0, col0 + 64) own the full columns [F0, F1) from their first
+  // kept column up to the next chunk's (chunk 0 from column 0, the last one
+  // to n_full), so every full column -- kept value or Zero unit --
+  // is written by exactly one chunk.  Lane = row: each lane parks its packed
+  // row in the warp's staging (8 KB, both ping-pong buffers: no TMA store is
+  // in flight here) at a 136-byte pitch (2-way bank conflicts at most), the
+  // span's col_pos entries go to shared memory once as byte offsets, then
+  // every 8-column group is one uniform step: 8 shared loads from the lane's
+  // own row, masked packing, one 16-byte store per row (a group shared with
+  // the neighbouring chunk goes out element-wise).
+  constexpr int SP_PITCH = 136, SP_POS = 32 * SP_PITCH, SP_PIECE = 64;   // pos staging: 64 groups (2 KB)
+  auto spread_chunk = [&](const uint32_t (&pk)[32], int col0) {
+    const uint32_t sb = smem_u32(stg_base);
+    __syncwarp();   // previous chunk's reads of this buffer are done
+    if (!zt) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(sb + lane * SP_PITCH + 8 * i), "r"(pk[2 * i]),
+                     "r"(pk[2 * i + 1])
+                     : "memory");
+    }
+    if ((p.dbg & 1) || col0 >= p.N) return;
+    const int F0 = col0 == 0 ? 0 : __ldg(p.col_kept + col0);
+    const int F1 = col0 + 64 >= p.N ? p.n_full : __ldg(p.col_kept + col0 + 64);
+    const int V0 = F0 >> 3, nvec = ((F1 + 7) >> 3) - V0;
+    const bool row_ok = orow >= 0 && orow < p.out_rows;
+    __nv_bfloat16* const drow = p.full_out + (int64_t)(row_ok ? orow : 0) * p.ld_full;
+    const uint32_t rb = sb + lane * SP_PITCH;
+#pragma unroll 1
+    for (int v0 = 0; v0 < nvec; v0 += SP_PIECE) {
+      const int nv = min(SP_PIECE, nvec - v0);
+      __syncwarp();   // the previous piece's offsets are consumed
+      for (int k = lane; k < 8 * nv; k += 32) {
+        const int j = 8 * (V0 + v0) + k;
+        int o = -1;   // byte offset of the kept value in the lane's row, -1: Zero unit, -2: not owned
+        if (j < F0 || j >= F1) {
+          o = -2;
+        } else if (!zt) {
+          const int q = __ldg(p.col_pos + j) - col0;
+          if ((unsigned)q < 64u) o = 2 * q;   // ascending lists: kept columns of the span are this chunk's
+        }
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(sb + SP_POS + 4 * k), "r"(o) : "memory");
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int g = 0; g < nv; ++g) {
+        const uint4 qa = ld_shared_v4(sb + SP_POS + 32 * g);
+        const uint4 qb = ld_shared_v4(sb + SP_POS + 32 * g + 16);
+        const int q[8] = {(int)qa.x, (int)qa.y, (int)qa.z, (int)qa.w, (int)qb.x, (int)qb.y, (int)qb.z, (int)qb.w};
+        uint32_t x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          uint16_t h = 0;
+          if (q[e] >= 0) asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(rb + q[e]) : "memory");
+          x[e] = h;
+        }
+        if (!row_ok) continue;
+        __nv_bfloat16* dst = drow + 8 * (V0 + v0 + g);
+        if (q[0] != -2 && q[7] != -2) {   // the whole group is this chunk's ([F0, F1) is contiguous)
+          st_global_v4(dst, make_uint4(x[0] | (x[1] << 16), x[2] | (x[3] << 16), x[4] | (x[5] << 16),
+                                       x[6] | (x[7] << 16)));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (q[e] != -2) reinterpret_cast<uint16_t*>(dst)[e] = (uint16_t)x[e];
+        }
+      }
+    }
+  };
   const bool two_planes = p.epi == EPI_GELU || p.epi == EPI_GELU_D;
 #pragma unroll 1
   for (int c = 0; c < BN / 128; ++c) {
@@ -571,6 +641,11 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
       }
       store_plane(tmO, b0, col0);
       store_plane(tmO2, b1, col0);
+    } else if (p.spread) {   // dW (no epilogue math): packed row -> full-column spread
+      uint32_t pk[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+      spread_chunk(pk, col0);
     } else {
       staging_free();
 #pragma unroll
@@ -1203,7 +1278,7 @@ static int units_of(int kind, int cg, const GemmParams& p) {
 template <int KIND>
 static cudaError_t post_launch(const GemmParams& p, int num_sms, cudaStream_t st) {
   if (p.splits == 1 || p.cs > 1) {
-    if (p.col_pos)   // compact columns written by the epilogue (scratch): spread them, Zero the rest
+    if (p.col_pos && !p.spread)   // compact columns written by the epilogue (scratch): spread them, Zero the rest
       return expand_cols_launch(p.out, p.ld_out, p.full_out, p.ld_full, p.out_rows, p.col_pos, p.n_full, st);
     return cudaSuccess;
   }

@@ -153,6 +153,10 @@ struct GemmParams {
   int64_t ld_full;         // (a scratch) and the column spread writes full_out [out_rows, n_full]
   int cs;                  // DW cluster split-K: the `splits` K-slices of a tile run as one cluster and
                            // are reduced through distributed shared memory (no workspace, no reduce kernel)
+  int spread;              // DW output pruning without split-K, written by the epilogue itself: each warp's
+                           // staged 32 x 64 compact chunk goes out as the full-column row segments it owns
+                           // (pruned units Zero) -- no scratch, no column-spread pass
+  const int32_t* col_kept; // spread: compact column i -> full column col_kept[i] (ascending; col_pos inverse)
 };
 // Cluster split-K choice for a dW launch with `splits` K-slices: the split
 // count to run as clusters (<= splits, cluster of cg x cs CTAs fits and every

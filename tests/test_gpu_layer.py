@@ -228,7 +228,9 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None, f32=False, pl
 
 @pytest.mark.parametrize("opts", [{"GROUP": 1}, {"GROUP": 2}, {"CONC": 0}, {"SQUAT_GUARD": 0}, {"A_EARLY": 0},
                                   {"PART": 0}, {"AUX_WEIGHT": 2.5}, {"FLAGS": 1},
-                                  {"DW_SHARE": 0.8}, {"DW_SHARE": 1.6}, {"SPLITK": 0}])
+                                  {"DW_SHARE": 0.8}, {"DW_SHARE": 1.6}, {"SPLITK": 0},
+                                  {"SPLITK": 0, "SPREAD_EPI": 1}, {"SPLITK": 0, "SPREAD_EPI": 1, "GROUP": 1},
+                                  {"SPREAD_EPI": 1}])
 def test_layer_schedule_variants_graph(tz, opts):
     """The scheduling options (ztp_set_option: grouped or concurrent or
     serial dX / dW, the SM split weight -- it changes the dW split-K counts --,
@@ -406,6 +408,14 @@ def test_config_c2_full_size_all_outputs(tz):
     gradients (split-K dW reduce with the dW1 column spread of output
     pruning, A-35, at production shapes)."""
     _simulate(tz, 1, 1024, 4096, 8192, [dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)], seed=241)
+
+
+def test_config_c4_tp1_all_outputs(tz):
+    """c4's bench workload (h = 4096, f = 11008, N = 2048, TP = 1, gamma = 0.5)
+    on EVERY output against the full fp64 oracle step: at these shapes the
+    output-pruned dWqkv (V pruning, A-36) and dW1 (A-35) run unsplit, their
+    compact columns spread by ztp_expand_cols."""
+    _simulate(tz, 1, 4096, 11008, 2048, [dict(qkv=0.5, o=0.5, fc1=0.5, fc2=0.5)], seed=243)
 
 
 @pytest.mark.parametrize("e,gam,mig", [
