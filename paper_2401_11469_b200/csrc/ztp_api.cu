@@ -382,6 +382,7 @@ ztp_status gemm_build_bf16(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, co
     p.ld_full = p.ld_out;
     p.out = (__nv_bfloat16*)c->xws[k];
     p.ld_out = ldc;
+    p.skip_zero = 1;   // the spread writes the Zero rows P (no all-pruned units, no scratch reads for them)
   }
   *po = o;
   *pp = p;

@@ -135,7 +135,7 @@ struct Sched {
     kbs = p.kb_per_split;
     units_c = tiles_c * S;
     zero_m = m_tiles - mc;
-    num_units = units_c + (S == 1 ? zero_m * n_tiles : 0);
+    num_units = units_c + (S == 1 && !p.skip_zero ? zero_m * n_tiles : 0);
   }
   // all-pruned (zero) units come FIRST: the epilogue warps write them while
   // the producer / MMA warps, which skip them, already stream the first tile.
@@ -1269,7 +1269,7 @@ static int units_of(int kind, int cg, const GemmParams& p) {
   const int m_tiles = (p.M + tm - 1) / tm, n_tiles = (p.N + BN - 1) / BN;
   int mc = m_tiles;
   if (kind != KIND_FWD) mc = std::min(m_tiles, (p.n_kept + tm - 1) / tm);
-  return mc * n_tiles * p.splits + (p.splits == 1 ? (m_tiles - mc) * n_tiles : 0);
+  return mc * n_tiles * p.splits + (p.splits == 1 && !p.skip_zero ? (m_tiles - mc) * n_tiles : 0);
 }
 
 // After a GEMM launch: the split-K reduce (fixed split order, the epilogue
@@ -1279,7 +1279,8 @@ template <int KIND>
 static cudaError_t post_launch(const GemmParams& p, int num_sms, cudaStream_t st) {
   if (p.splits == 1 || p.cs > 1) {
     if (p.col_pos && !p.spread)   // compact columns written by the epilogue (scratch): spread them, Zero the rest
-      return expand_cols_launch(p.out, p.ld_out, p.full_out, p.ld_full, p.out_rows, p.col_pos, p.n_full, st);
+      return expand_cols_launch(p.out, p.ld_out, p.full_out, p.ld_full, p.kept, std::min(p.n_kept, p.M), p.pruned,
+                                std::max(0, p.M - p.n_kept), p.col_pos, p.n_full, st);
     return cudaSuccess;
   }
   const int64_t chunks = (int64_t)p.M * (((p.col_pos ? p.n_full : p.N) + 7) / 8);
@@ -1478,7 +1479,7 @@ static void unit_costs(int kind, int cg, const GemmParams& p, std::vector<int>& 
   int mc = m_tiles;
   if (kind != KIND_FWD) mc = std::min(m_tiles, (p.n_kept + tm - 1) / tm);
   const int tiles_c = mc * n_tiles, S = p.splits, kbs = p.kb_per_split;
-  const int nz = S == 1 ? (m_tiles - mc) * n_tiles : 0;
+  const int nz = S == 1 && !p.skip_zero ? (m_tiles - mc) * n_tiles : 0;
   cost.clear();
   zero.clear();
   for (int u = 0; u < nz; ++u) {

@@ -157,6 +157,7 @@ struct GemmParams {
                            // staged 32 x 64 compact chunk goes out as the full-column row segments it owns
                            // (pruned units Zero) -- no scratch, no column-spread pass
   const int32_t* col_kept; // spread: compact column i -> full column col_kept[i] (ascending; col_pos inverse)
+  int skip_zero;           // no all-pruned (Zero) units: the column-spread pass writes the Zero rows P itself
 };
 // Cluster split-K choice for a dW launch with `splits` K-slices: the split
 // count to run as clusters (<= splits, cluster of cg x cs CTAs fits and every
@@ -271,9 +272,11 @@ cudaError_t impute_rows_launch(void* out, int64_t ld, int64_t cols, const int32_
 cudaError_t priority_update_launch(const void* w, int64_t ld_w, const void* w_old, int64_t ld_old, int64_t K,
                                    int64_t n, const int32_t* pos_prev, float* delta, int32_t* count_above,
                                    float theta, cudaStream_t st);
-// out-of-place column spread: dst[r, j] = pos[j] >= 0 ? src[r, pos[j]] : 0, r < n, j < n_full
-cudaError_t expand_cols_launch(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int n, const int32_t* pos,
-                               int n_full, cudaStream_t st);
+// out-of-place column spread over the lineage rows: for r = kept[i] (i < nk; kept NULL = identity)
+// dst[r, j] = pos[j] >= 0 ? src[r, pos[j]] : 0, for r = pruned[i] (i < np) dst[r, :] = 0; j < n_full
+cudaError_t expand_cols_launch(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, const int32_t* kept,
+                               int nk, const int32_t* pruned, int np, const int32_t* pos, int n_full,
+                               cudaStream_t st);
 // dst[i, r] = src[r, cols ? cols[i] : i], i < n, r < R (16-bit elements)
 cudaError_t transpose_launch(const void* src, int64_t ld_src, int64_t R, const int32_t* cols, int64_t n, void* dst,
                              int64_t ld_dst, cudaStream_t st);

@@ -343,27 +343,45 @@ cudaError_t gather_multi_launch(const GatherJobs& j, cudaStream_t st) {
   return launch_k(ztp_gather_multi, blocks, 256, 0, st, J);
 }
 
-// Column expansion (output pruning, bf16), out of place: dst[r, j] =
-// pos[j] >= 0 ? src[r, pos[j]] : 0 for j < n_full (the Zero gradient of the
-// consumer-pruned units).  Work items of (row, 1024 output columns),
-// one warp each: 8-column groups, pos read as 16-byte vectors, the compact
-// source window gathered with 2-byte loads (L1), 16-byte stores.
+// Column expansion (output pruning, bf16), out of place, over the lineage
+// rows: a kept row r = kept[i] gets dst[r, j] = pos[j] >= 0 ? src[r, pos[j]]
+// : 0 (the Zero gradient of the consumer-pruned units), a pruned row
+// r = pruned[i] (the Zero rows P) is written 0 without reading the
+// scratch -- the dW GEMM computes no all-pruned units in this mode.  Work
+// items of (row, 1024 output columns), one warp each: 8-column groups, pos
+// read as 16-byte vectors, the compact source window gathered with 2-byte
+// loads (L1), 16-byte stores.  (Within 1.1-1.6x of a device memcpy of the
+// same bytes; CTA-tiled variants staging the windows in shared memory were
+// slower: tools/bench_src/expand_bench.cu, profiles/r02_expand_variants.txt.)
 __global__ void __launch_bounds__(256) ztp_expand_cols(const uint16_t* __restrict__ src, int64_t ld_src,
-                                                       uint16_t* __restrict__ dst, int64_t ld_dst, int n,
+                                                       uint16_t* __restrict__ dst, int64_t ld_dst,
+                                                       const int32_t* __restrict__ kept, int nk,
+                                                       const int32_t* __restrict__ pruned, int np,
                                                        const int32_t* __restrict__ pos, int n_full) {
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int cpr = (n_full + GM_CHUNK - 1) / GM_CHUNK;
-  const int64_t items = (int64_t)n * cpr;
+  const int64_t items = (int64_t)(nk + np) * cpr;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const bool pv = (reinterpret_cast<uintptr_t>(pos) & 15) == 0;
   for (int64_t it = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += nw) {
-    const int r = (int)(it / cpr), c0 = (int)(it % cpr) * GM_CHUNK;
+    const int i = (int)(it / cpr), c0 = (int)(it % cpr) * GM_CHUNK;
     const int c1 = min(n_full, c0 + GM_CHUNK);
     const int v1 = c0 + (c1 - c0) / 8 * 8;
+    const bool zero_row = i >= nk;
+    const int r = zero_row ? __ldg(pruned + (i - nk)) : (kept ? __ldg(kept + i) : i);
     const uint16_t* s = src + (int64_t)r * ld_src;
     uint16_t* d = dst + (int64_t)r * ld_dst;
+    if (zero_row) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 8 * (lane + 32 * u);
+        if (c < v1) *reinterpret_cast<uint4*>(d + c) = make_uint4(0u, 0u, 0u, 0u);
+      }
+      for (int c = v1 + lane; c < c1; c += 32) d[c] = 0;
+      continue;
+    }
     auto pick = [&](int q) -> uint32_t { return q >= 0 ? (uint32_t)__ldg(s + q) : 0u; };
     uint4 w[4];
 #pragma unroll
@@ -391,14 +409,16 @@ __global__ void __launch_bounds__(256) ztp_expand_cols(const uint16_t* __restric
   }
 }
 
-cudaError_t expand_cols_launch(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int n, const int32_t* pos,
-                               int n_full, cudaStream_t st) {
-  if (n <= 0 || n_full <= 0) return cudaSuccess;
+cudaError_t expand_cols_launch(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, const int32_t* kept,
+                               int nk, const int32_t* pruned, int np, const int32_t* pos, int n_full,
+                               cudaStream_t st) {
+  if (nk + np <= 0 || n_full <= 0) return cudaSuccess;
   if ((reinterpret_cast<uintptr_t>(dst) & 15) != 0 || ld_dst % 8 != 0) return cudaErrorMisalignedAddress;
-  const int64_t items = (int64_t)n * ((n_full + GM_CHUNK - 1) / GM_CHUNK);
+  if (np > 0 && !pruned) return cudaErrorInvalidValue;
+  const int64_t items = (int64_t)(nk + np) * ((n_full + GM_CHUNK - 1) / GM_CHUNK);
   const int blocks = (int)std::min<int64_t>((items + 7) / 8, (int64_t)148 * 8);
-  return launch_k(ztp_expand_cols, blocks, 256, 0, st, (const uint16_t*)src, ld_src, (uint16_t*)dst, ld_dst, n, pos,
-                  n_full);
+  return launch_k(ztp_expand_cols, blocks, 256, 0, st, (const uint16_t*)src, ld_src, (uint16_t*)dst, ld_dst, kept,
+                  nk, pruned, np, pos, n_full);
 }
 
 // ------------------------------------------ Average / Same imputation (NEXT-2)
