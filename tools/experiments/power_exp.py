@@ -10,7 +10,7 @@ import time
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2401_11469_b200 as Z  # noqa: E402
 from paper_2401_11469_b200.layer import ZtpLayer, SEGS  # noqa: E402
 from synth.configs import CONFIGS  # noqa: E402
