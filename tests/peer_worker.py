@@ -30,14 +30,28 @@ def main():
     from synth import inputs as I
 
     dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
-    torch.cuda.set_device(0)
-    ctx = Z.ztp_ctx_create(rank, world, None, 0)           # no NCCL id -> peer transport
+    # PEER_MULTIDEV=1 (>= world GPUs): rank r on cuda:r with an NCCL communicator
+    # (collectives and grouped send / recv over NVLink) and the window mapped
+    # across devices (peer pulls over NVLink); default: every rank on cuda:0,
+    # peer transport over CUDA IPC
+    multidev = os.environ.get("PEER_MULTIDEV") == "1"
+    device = rank if multidev else 0
+    torch.cuda.set_device(device)
+    uid = None
+    if multidev:
+        box = [Z.ztp_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = box[0]
+    ctx = Z.ztp_ctx_create(rank, world, uid, device)      # no NCCL id -> peer transport
+    sym_alloc = lambda r, c, dt=torch.bfloat16: Z.ztp_sym_alloc(ctx, r, c, dt, device)  # noqa: E731
 
     def open_window(nbytes):
         h = Z.ztp_window_create(ctx, nbytes)
         hs = [None] * world
         dist.all_gather_object(hs, h)
         Z.ztp_window_open(ctx, hs)
+        if multidev and os.environ.get("PEER_TRANSPORT", "nccl") == "peer":
+            Z.ztp_set_transport(ctx, Z.TRANSPORT_PEER)   # the library's own peer kernels across GPUs
 
     res = {}
     dev = lambda a, dt=torch.bfloat16: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda().to(dt)  # noqa
@@ -50,7 +64,7 @@ def main():
             Wt = I.uniform_sym(seed, "w", world * K, n, 0.1, r0=rank * K, r1=(rank + 1) * K)
             Xt = I.normal(seed, "x", world * K, N, r0=rank * K, r1=(rank + 1) * K)
             w, x = dev(Wt, dt), dev(Xt, dt)
-            y = Z.ztp_sym_alloc(ctx, n, N, dt)
+            y = sym_alloc(n, N, dt)
             a = Z.linear_args(x_t=x, w_t=w, y_t=y, skip_collective=1)
             Z.ztp_row_linear(ctx, Z.FWD, a)
             torch.cuda.synchronize()
@@ -62,7 +76,7 @@ def main():
         # unpaired column FWD (gather_output): my block, then the all-gathered tensor
         Wt = I.uniform_sym(seed, "wc", K, world * n, 0.1, c0=rank * n, c1=(rank + 1) * n)
         Xt = I.normal(seed, "xc", K, N)
-        yfull = Z.ztp_sym_alloc(ctx, world * n, N)
+        yfull = sym_alloc(world * n, N)
         a = Z.linear_args(x_t=dev(Xt), w_t=dev(Wt), y_t=yfull, gather_output=True)
         Z.ztp_col_linear(ctx, Z.FWD, a)
         Z.ztp_sync(ctx)
@@ -72,8 +86,8 @@ def main():
         res["T"], res["M"] = np.array(T), np.array(M)
         # one-sided pulls: every rank's window tensor A holds rank-coded values;
         # rank r pulls a slice of rank (r+1) % world into its own B
-        A = Z.ztp_sym_alloc(ctx, 64, 96)
-        B = Z.ztp_sym_alloc(ctx, 64, 96)
+        A = sym_alloc(64, 96)
+        B = sym_alloc(64, 96)
         A.copy_(dev(I.normal(seed, "a", 64, 96, rank=rank)))
         B.zero_()
         xs = []
@@ -102,7 +116,7 @@ def main():
         shards = {"qkv": dev(qkv), "o": dev(I.uniform_sym(seed, "wo", h, h, bq, r0=F0, r1=F1)),
                   "w1": dev(I.uniform_sym(seed, "w1", h, f, bq, c0=U0, c1=U1)),
                   "w2": dev(I.uniform_sym(seed, "w2", f, h, 1 / math.sqrt(f), r0=U0, r1=U1))}
-        L = ZtpLayer(ctx, h, f, N, rank, e, shards, mig_cap=cap, alloc=sym_allocator(ctx))
+        L = ZtpLayer(ctx, h, f, N, rank, e, shards, mig_cap=cap, alloc=sym_allocator(ctx, device))
         own = u - (u - mig[0][2] if rank == s else 0)
         all_x, inc = [], []
         for (src, dst, lo, hi) in mig:
@@ -144,7 +158,7 @@ def main():
         k = int(os.environ["PEER_K"])
         mode = {"tree": Z.COLL_TREE, "p2p": Z.COLL_P2P}[os.environ["PEER_MODE"]]
         open_window(16 << 20)
-        Lk = KMigColLinear(ctx, rank, world, K, n, N, migr, k, mode, alloc=sym_allocator(ctx))
+        Lk = KMigColLinear(ctx, rank, world, K, n, N, migr, k, mode, alloc=sym_allocator(ctx, device))
         Lk.X.copy_(dev(I.normal(seed, "x", K, N)))
         Lk.W.copy_(dev(I.uniform_sym(seed, "w", K, world * n, 0.1, c0=rank * n, c1=(rank + 1) * n)))
         Lk.G.copy_(dev(I.normal(seed, "g", world * n, N, r0=rank * n, r1=(rank + 1) * n)))

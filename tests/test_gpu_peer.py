@@ -55,7 +55,10 @@ def bf16(x):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_peer_collectives_bit_exact(tmp_path, world):
-    res = run_ranks(world, "collectives", tmp_path)
+    _check_collectives(run_ranks(world, "collectives", tmp_path), world)
+
+
+def _check_collectives(res, world):
     # all-reduce: sum of the ranks' partials in rank order in fp32, one RNE
     # rounding for bf16 (the oracle's left fold)
     for tag in ("bf16", "f32"):
@@ -97,7 +100,11 @@ def test_peer_layer_step_semi(tmp_path, world, mig, gamma):
     """A whole TP layer step (select + FWD + BWD) with a SEMI plan through the
     peer transport, eager and replayed as a CUDA graph: Y, dX and every
     rank's weight gradients in the owner's view match the oracle."""
-    res = run_ranks(world, "layer", tmp_path, env={"PEER_MIG": mig, "PEER_GAMMA": gamma})
+    _check_layer_semi(tmp_path, world, mig, gamma)
+
+
+def _check_layer_semi(tmp_path, world, mig, gamma, env=None):
+    res = run_ranks(world, "layer", tmp_path, env=dict({"PEER_MIG": mig, "PEER_GAMMA": gamma}, **(env or {})))
     h, f, N, seed = 128, 512, 264, 31
     e = world
     a, u = h // e, f // e
@@ -170,3 +177,36 @@ def test_peer_kdim_migration_lossless(tmp_path, world, migr, k, mode):
             close(res[r]["Y" + sfx], O.linear_fwd(Wr, X), f"Y{sfx}[{r}]")
             close(res[r]["dX" + sfx], dX, f"dX{sfx}[{r}]")
             close(res[r]["dW" + sfx], O.linear_bwd_dw(X, Gr), f"dW{sfx}[{r}]")
+
+
+# ------------------------------------------------ one rank per GPU (>= 2 GPUs)
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_multidev_peer_collectives_bit_exact(tmp_path, world):
+    """Rank r on cuda:r (NVLink P2P between GPUs): the library's peer
+    transport -- two-shot all-reduce in rank order, all-gather, statistics,
+    one-sided pulls -- bit-exact as in the one-GPU run.  Skipped below
+    `world` GPUs (the driver's boxes have one)."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    res = run_ranks(world, "collectives", tmp_path, env={"PEER_MULTIDEV": "1", "PEER_TRANSPORT": "peer"})
+    _check_collectives(res, world)
+
+
+@pytest.mark.parametrize("world,mig,gamma", [
+    (2, "192,256", "0.5,0.25,0.3,0.3"),
+    (4, "80,96,96,112,112,128", "0.25,0.5,0.4,0.2"),
+])
+def test_multidev_nccl_layer_step_semi(tmp_path, world, mig, gamma):
+    """The SEMI layer step of test_peer_layer_step_semi with one rank per GPU
+    and an NCCL communicator (collectives over NVLink / NVSwitch), migration
+    pulls through the window: every output against the oracle.  Skipped
+    below `world` GPUs."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    _check_layer_semi(tmp_path, world, mig, gamma, env={"PEER_MULTIDEV": "1", "PEER_TRANSPORT": "nccl"})
