@@ -50,11 +50,17 @@ template <int CG>
 struct Cfg {
   static constexpr int BNL = BN / CG;                    // B columns staged by one CTA
   static constexpr int TM = BM * CG;                     // tile rows
-  static constexpr int STAGES = CG == 2 ? 5 : 3;
+#ifndef ZTP_STG3
+#define ZTP_STG3 0
+#endif
+  // 2-CTA: a 4-stage operand ring and three epilogue staging buffers per warp
+  // (stores of two chunks in flight while the third is filled); 1-CTA: 3 + 2
+  static constexpr int STAGES = CG == 2 ? (ZTP_STG3 ? 4 : 5) : 3;
+  static constexpr int STG_BUFS = (CG == 2 && ZTP_STG3) ? 3 : 2;
   static constexpr int B_BYTES = BNL * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
   static constexpr int RING = STAGES * STAGE_BYTES;
-  static constexpr int STAGING = EPI_WARPS * 2 * STAGING_PER_WARP;   // ping-pong per warp
+  static constexpr int STAGING = EPI_WARPS * STG_BUFS * STAGING_PER_WARP;   // rotating per warp
   static constexpr int BARS = (2 * STAGES + 4) * 8 + 16;
   static constexpr int TOTAL = 1024 + RING + STAGING + BARS;
 };
@@ -411,7 +417,8 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
                                               uint32_t tmem_base, Pipe& ps, unsigned long long** first = nullptr) {
   const int lq = ew & 3;               // TMEM lane quarter == warp % 4 (rows lq*32 .. +31)
   const int ch = ew >> 2;              // column half of the 256-column accumulator
-  uint8_t* const stg_base = staging + ew * 2 * STAGING_PER_WARP;
+  constexpr int NBUF = Cfg<CG>::STG_BUFS;
+  uint8_t* const stg_base = staging + ew * NBUF * STAGING_PER_WARP;
   uint8_t* stg = stg_base;
   auto release = [&]() {
     tc_fence_before();
@@ -435,9 +442,9 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
   // lanes that issued TMA stores wait until at most the other buffer's
   // store is still reading (bulk wait_group.read 1).
   auto staging_free = [&]() {
-    if (lane < 8) bulk_wait_read1();
+    if (lane < 8) bulk_wait_read_n<NBUF - 1>();
     __syncwarp();
-    stg = stg_base + (ps.sk & 1) * STAGING_PER_WARP;
+    stg = stg_base + (ps.sk % NBUF) * STAGING_PER_WARP;
     ++ps.sk;
   };
   if (S > 1) {
@@ -1374,6 +1381,7 @@ int gemm_cluster_splits(int kind, int epi, int M, int N, int n_kept, int splits,
   static int max_cl[3][9] = {};
   for (int cs = std::min(splits, 8 / cg); cs >= 2; --cs) {
     if (tiles_c * cs * cg > num_sms) continue;
+    if (cs * ((8 + cs - 1) / cs) * BM * 128 > (cg == 2 ? Cfg<2>::RING : Cfg<1>::RING)) continue;   // DSMEM slots
     int& mc = max_cl[cg][cs];
     if (mc == 0) {
       const int smem = cg == 2 ? Cfg<2>::TOTAL : Cfg<1>::TOTAL;
