@@ -599,7 +599,7 @@ def controller_run(C, args, schedule, semi, final_steps=0):
     t_free = C.run(args.steps if final_steps else 30, args.warmup)
     costs, cplain = (C.costs() if semi else (None, None))
     opts = Z.ctl_opts(L_ref=float(C.u), trigger=0.10, max_refines=2, enable_migration=int(semi),
-                      zero_crit=Z.CRIT_MIN, eps=args.eps)
+                      zero_crit=Z.CRIT_AVG if args.criterion == "avg" else Z.CRIT_MIN, eps=args.eps)
     ctl = Z.ztp_ctl_init(e)
     phases, series = [], []
     for ph, (chis, nsteps) in enumerate(schedule):
@@ -661,6 +661,8 @@ def main():
     ap.add_argument("--gamma", type=float, default=0.5, help="N=1 homogeneous prune ratio")
     ap.add_argument("--chi", type=float, default=2.0, help="straggler slowdown (N>1)")
     ap.add_argument("--eps", type=float, default=0.05, help="A-17 straggler tolerance above timing noise")
+    ap.add_argument("--criterion", default="min", choices=["min", "avg"],
+                    help="N>1 Eq.1 criterion: T_min (A-7, headline) or the paper-literal T_avg")
     ap.add_argument("--ctl-steps", type=int, default=6, help="controller steps per phase (N>1)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"])
     ap.add_argument("--share-gpu", action="store_true", help="N>1 on one GPU (path validation only)")
@@ -707,7 +709,7 @@ def main():
         ms_free, ms_bal = res["T_free_ms"], res["T_bal_ms"]
         ph = res["phases"][0]
         flops_dense = None
-        plan_info = {"final": ph["final_plan"], "controller": res["controller"], "criterion": "T_min (A-7)",
+        plan_info = {"final": ph["final_plan"], "controller": res["controller"], "criterion": "T_avg (paper-literal Eq.1)" if args.criterion == "avg" else "T_min (A-7)",
                      "eps": args.eps, "series": [{k: v for k, v in s.items() if k not in ("T_ms", "M_ms")}
                                                  for s in res["series"]]}
         extra = {"ms_unbal": ph["T_unbal_ms"], "recovery": ms_free / ms_bal, "speedup": ph["T_unbal_ms"] / ms_bal}
