@@ -43,6 +43,9 @@ CONFIGS = {
     # c4: Llama-2-7B-shaped layer h=4096 f=11008 seq2048
     "c4": LayerConfig("c4", 3, h=4096, f=11008, heads=32, N=2048,
                       note="Llama-2-7B-shaped layer (h=4096, ffn=11008, seq=2048)", seq=2048),
+    # c0 (optional, the paper's own shape): ViT-1B layer h=2048 f=8192, 65 tokens x batch 64
+    "c0": LayerConfig("c0", 5, h=2048, f=8192, heads=16, N=4160,
+                      note="ViT-1B layer (h=2048, ffn=8192, 65 tokens, batch=64)", seq=65, causal=False),
     # c5: GPT-13B-shaped 4-layer stack h=5120 f=20480 seq2048
     "c5": LayerConfig("c5", 4, h=5120, f=20480, heads=40, N=2048, layers=4,
                       note="GPT 13B-shaped 4-layer stack (h=5120, ffn=20480, seq=2048)", seq=2048),

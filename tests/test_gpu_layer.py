@@ -397,6 +397,15 @@ def test_config_c5_layer_full_size_all_outputs(tz):
     _simulate(tz, 8, 5120, 20480, 2048, g, seed=244)
 
 
+def test_config_c0_paper_shape_all_outputs(tz):
+    """c0 (optional, the paper's ViT-1B layer: h = 2048, f = 8192, 65 x 64 =
+    4160 tokens) at TP = 8, rank 7 a 4x straggler resized at 0.75: every
+    output of every rank against the full fp64 oracle step."""
+    g = _zeros(8)
+    g[7] = dict(qkv=0.75, o=0.75, fc1=0.75, fc2=0.75)
+    _simulate(tz, 8, 2048, 8192, 4160, g, seed=245)
+
+
 def test_config_c1_exact_shape(tz):
     """c1 (single FFN-block config of BASELINE.json: h = 64, f = 256, seq 16 x
     batch 2 -> N = 32) at TP = 2, rank 1 slowed 2x -> T_avg ratio 0.25 on every

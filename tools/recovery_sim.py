@@ -9,7 +9,9 @@ Per case: T_free (chi = 1, dense), T_unbal (chi on the straggler, dense),
 then STEPS steps under ztp_ctl_step (window -> plan -> refresh -> monitor,
 A-41/A-43) with the slowdown held; T_bal = mean of the monitored steps.
 Usage: CASES=c2:2:2,c2:4:2,c3:4:2,c4:8:2,c4:8:3s python tools/recovery_sim.py
-(cfg:e:chi, suffix s = SEMI plans with the pretest costs)."""
+(cfg:e:chi, suffix s = SEMI plans with the pretest costs).  The E4 analog
+(a chi sweep of one straggler on the paper's ViT-1B shape):
+CASES=c0:8:1,c0:8:2,c0:8:3,c0:8:4,c0:8:6,c0:8:8,c0:8:4s,c0:8:8s."""
 import json
 import os
 import sys
@@ -22,9 +24,9 @@ from synth.configs import CONFIGS  # noqa: E402
 from tp_sim import SimTP, NVLINK_GBS, plan_summary  # noqa: E402
 
 STEPS = int(os.environ.get("STEPS", "8"))
-EPS = float(os.environ.get("EPS", "0.05"))
+EPS = float(os.environ.get("EPS", "0.05"))     # A-17 tolerance above the one-GPU timing noise (~3%)
 # Eq.1's criterion: T_min (A-7, the build's headline) or the paper-literal T_avg (CRIT=avg)
-CRIT = {"min": Z.CRIT_MIN, "avg": Z.CRIT_AVG}[os.environ.get("CRIT", "min")]     # A-17 tolerance above the one-GPU timing noise (~3%)
+CRIT = {"min": Z.CRIT_MIN, "avg": Z.CRIT_AVG}[os.environ.get("CRIT", "min")]
 
 
 def run_case(name, e, chi, semi):
