@@ -14,7 +14,8 @@ timed alone, step = max over ranks + modelled all-reduces and per-step
 migration copies at 770 GB/s).  Every step's T_i, M_i go to ztp_ctl_step
 (SEMI plans, T_min criterion, the Alg.2 l.1 pretest costs measured at
 start-up); the plan it returns is applied before the next step.
-Env: STEPS_PER_PHASE (10), REPLAYS (10), EPS (0.05), OUT, CFG (c5), TP (8)."""
+Env: STEPS_PER_PHASE (10), REPLAYS (10), EPS (0.05), OUT, CFG (c5), TP (8),
+SCHED=roundrobin (c0's schedule: rank 1 x2, rank 3 x4, rank 5 x8, homogeneous)."""
 import json
 import os
 import sys
@@ -34,6 +35,11 @@ EPS = float(os.environ.get("EPS", "0.05"))
 def schedule(step, e):
     ph = step // PER
     chi = [1.0] * e
+    if os.environ.get("SCHED") == "roundrobin":
+        # c0: the straggler rotates over the ranks with chi 2, 4, 8, then homogeneous
+        if ph < 3:
+            chi[(2 * ph + 1) % e] = (2.0, 4.0, 8.0)[ph]
+        return chi
     if ph == 0:
         chi[0] = 2.0
     elif ph == 1:
