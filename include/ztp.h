@@ -191,7 +191,9 @@ ztp_status ztp_transpose(ztp_ctx* ctx, const ztp_mat* src, const ztp_mat* dst, c
  *                                            its A operand issues its first stages' A loads before
  *                                            the PDL wait (only B waits for the predecessor)
  *   ZTP_OPT_PART        (ZTP_PART, 1)        dX / dW SM partition: 0 work-proportional,
- *                                            1 wave-quantised (minimises the later finish)
+ *                                            1 wave-quantised (minimises the later finish of
+ *                                            max(MMA k-blocks, epilogue incl. Zero tiles)),
+ *                                            2 wave-quantised on MMA k-blocks only
  *   ZTP_OPT_AUX_WEIGHT  (ZTP_AUX_WEIGHT, 1.0) dX work factor in that partition when its epilogue
  *                                            reads an aux operand (GeLU')
  *   ZTP_OPT_FLAGS       (ZTP_FLAGS, 0)       a GEMM whose B operand is the output of the GEMM just
@@ -204,6 +206,10 @@ ztp_status ztp_transpose(ztp_ctx* ctx, const ztp_mat* src, const ztp_mat* dst, c
  *                                            16-byte stores); 0: compact scratch + a column-spread
  *                                            pass (measured: on par at c4, slower at c5 -- the
  *                                            scattered row stores make the epilogue L1-bound)
+ *   ZTP_OPT_ZERO_GENERIC (ZTP_ZERO_GENERIC, 1) all-pruned (Zero) tiles of a dX / dW at a lineage row
+ *                                            map are written by generic 16-byte stores (eight
+ *                                            lanes per 128-byte row segment) instead of TMA
+ *                                            scatter4 boxes
  * ------------------------------------------------------------------------- */
 typedef enum ztp_option {
   ZTP_OPT_CONC = 0,
@@ -217,7 +223,8 @@ typedef enum ztp_option {
   ZTP_OPT_PART = 8,
   ZTP_OPT_AUX_WEIGHT = 9,
   ZTP_OPT_FLAGS = 10,
-  ZTP_OPT_SPREAD_EPI = 11
+  ZTP_OPT_SPREAD_EPI = 11,
+  ZTP_OPT_ZERO_GENERIC = 12
 } ztp_option;
 ztp_status ztp_set_option(ztp_ctx* ctx, ztp_option opt, double value);
 ztp_status ztp_get_option(const ztp_ctx* ctx, ztp_option opt, double* value);

@@ -60,6 +60,7 @@ struct ztp_ctx {
   // a GEMM on the same stream whose outputs do not overlap A (ZTP_A_EARLY, default 1)
   int a_early = 1;
   int spread_epi = 0;         // output-pruned unsplit dW: column spread inside the GEMM epilogue (opt-in)
+  int zero_generic = 1;       // Zero units at a lineage row map: generic stores instead of TMA scatter4
   int64_t lg_id = -1;                  // ztp::launch_seq() right after the last eligible GEMM launch (-1: none)
   cudaStream_t lg_stream = nullptr;
   const char* lg_out[2] = {nullptr, nullptr};
@@ -315,6 +316,7 @@ ztp_status gemm_build_bf16(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, co
   p.dbg = c->dbg_epi;
   p.col_pos = col_pos;
   p.n_full = n_full;
+  p.zero_generic = c->zero_generic;
   // early start (PDL wait at exit) only when nothing between the launches
   // depends on stamps (emulation) and the workspaces are disjoint (dW uses
   // its own split-K workspace)
@@ -1079,25 +1081,38 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
     const int pairs = c->num_sms / 2;
     int px = (int)std::lround(pairs * w_dx / (w_dx + c->dw_share * w_dw));
     px = std::max(1, std::min(pairs - 1, px));
-    if (c->part_model == 1) {
+    if (c->part_model >= 1) {
       // wave-quantised: each GEMM's time ~ ceil(units / CTA slots) x k-blocks
       // per unit (its split-K as gemm() will choose it for that many SMs);
       // the partition minimising the later finish, ties to the proportional one
-      auto cost = [&](int kind, int M_, int N_, int kdim_, int nsm, double wgt) {
+      // The epilogue warps run beside the MMA: a pair's time is the longer
+      // of its MMA k-blocks and its epilogue work -- computed tiles (~2 us,
+      // EW k-blocks) plus the all-pruned Zero tiles, which have no MMA but
+      // write a whole output tile (~2.5 us, ZW; the c0 TP = 8 gamma = 0.9
+      // timeline, profiles/r02_zero_units_partition.txt).  Without the
+      // epilogue term a heavily resized dX (few computed tiles, many Zero
+      // rows) got few SMs and its Zero rows ran long after its MMAs.
+      constexpr double EW = 5.0, ZW = 6.0;
+      auto cost = [&](int kind, int M_, int N_, int kdim_, int nsm, double wgt, bool zero_units) {
         const int cg = ztp::gemm_choose_cg(kind, M_, nk);
         const int tm = 128 * cg;
-        const int mc = std::min((M_ + tm - 1) / tm, (nk + tm - 1) / tm), nt = (N_ + 255) / 256;
+        const int mt = (M_ + tm - 1) / tm;
+        const int mc = std::min(mt, (nk + tm - 1) / tm), nt = (N_ + 255) / 256;
         const int sp = c->allow_splitk ? ztp::gemm_choose_splits(kind, M_, N_, kdim_, nk, nsm) : 1;
         const int kb = (kdim_ + 63) / 64, kps = (kb + sp - 1) / sp;
         const int slots = std::max(1, nsm / cg);
-        return std::ceil((double)mc * nt * sp / slots) * kps * wgt;
+        const double rounds = std::ceil((double)mc * nt * sp / slots);
+        const double zu = (zero_units && sp == 1) ? (double)(mt - mc) * nt : 0.0;
+        if (c->part_model == 2) return rounds * kps * wgt;   // MMA work only (the model before the Zero term)
+        return std::max(rounds * kps * wgt, rounds * EW + std::ceil(zu / slots) * ZW);
       };
       const int Mx = (int)(dxc ? nk : K);
       double best = 1e300;
       int bp = px;
       for (int q = 1; q < pairs; ++q) {
-        const double t = std::max(cost(ztp::KIND_DX, Mx, (int)N, (int)n_y, 2 * q, dx_aux ? c->aux_weight : 1.0),
-                                  cost(ztp::KIND_DW, (int)K, (int)n_y, (int)N, 2 * (pairs - q), c->dw_share));
+        const double t =
+            std::max(cost(ztp::KIND_DX, Mx, (int)N, (int)n_y, 2 * q, dx_aux ? c->aux_weight : 1.0, !dxc),
+                     cost(ztp::KIND_DW, (int)K, (int)n_y, (int)N, 2 * (pairs - q), c->dw_share, !os));
         if (t < best - 1e-9 || (t < best + 1e-9 && std::abs(q - px) < std::abs(bp - px))) {
           best = std::min(best, t);
           bp = q;
@@ -1253,6 +1268,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* gb = getenv("ZTP_GROUP")) c->group_bwd = atoi(gb);
   if (const char* ae = getenv("ZTP_A_EARLY")) c->a_early = atoi(ae) != 0;
   if (const char* se = getenv("ZTP_SPREAD_EPI")) c->spread_epi = atoi(se) != 0;
+  if (const char* zg = getenv("ZTP_ZERO_GENERIC")) c->zero_generic = atoi(zg) != 0;
   if (const char* fl = getenv("ZTP_FLAGS")) c->flags_opt = atoi(fl) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
@@ -1894,7 +1910,7 @@ ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
       return ZTP_OK;
     case ZTP_OPT_A_EARLY: c->a_early = iv != 0; return ZTP_OK;
     case ZTP_OPT_PART:
-      if (iv < 0 || iv > 1) return fail(c, ZTP_EINVAL, "ztp_set_option: partition model is 0 or 1");
+      if (iv < 0 || iv > 2) return fail(c, ZTP_EINVAL, "ztp_set_option: partition model is 0, 1 or 2");
       c->part_model = iv;
       return ZTP_OK;
     case ZTP_OPT_AUX_WEIGHT:
@@ -1903,6 +1919,7 @@ ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
       return ZTP_OK;
     case ZTP_OPT_FLAGS: c->flags_opt = iv != 0; return ZTP_OK;
     case ZTP_OPT_SPREAD_EPI: c->spread_epi = iv != 0; return ZTP_OK;
+    case ZTP_OPT_ZERO_GENERIC: c->zero_generic = iv != 0; return ZTP_OK;
   }
   return fail(c, ZTP_EINVAL, "ztp_set_option: unknown option " + std::to_string((int)opt));
 }
@@ -1922,6 +1939,7 @@ ztp_status ztp_get_option(const ztp_ctx* c, ztp_option opt, double* v) {
     case ZTP_OPT_AUX_WEIGHT: *v = c->aux_weight; return ZTP_OK;
     case ZTP_OPT_FLAGS: *v = c->flags_opt; return ZTP_OK;
     case ZTP_OPT_SPREAD_EPI: *v = c->spread_epi; return ZTP_OK;
+    case ZTP_OPT_ZERO_GENERIC: *v = c->zero_generic; return ZTP_OK;
   }
   return fail(nullptr, ZTP_EINVAL, "ztp_get_option: unknown option " + std::to_string((int)opt));
 }

@@ -523,6 +523,28 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
     if (!zt) release();
     return;
   }
+  if (zt && !dense_out && !p.spread && p.zero_generic) {
+    // All-pruned tile at a lineage row map (the Zero rows P): no data
+    // to stage, so no TMA scatter4 (4 rows x 128 B per op) -- generic 16-byte
+    // stores, eight lanes per 128-byte row segment, four rows per instruction.
+    if (p.dbg & 1) return;
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 1
+    for (int c = 0; c < BN / 128; ++c) {
+      const int col = nc0 + c * 64 + 8 * (lane & 7);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int orr = __shfl_sync(0xFFFFFFFFu, orow, 4 * i + (lane >> 3));
+        if (orr < 0 || orr >= p.out_rows || col >= p.N) continue;
+        __nv_bfloat16* dst = p.out + (int64_t)orr * p.ld_out + col;
+        if (col + 8 <= p.N)
+          st_global_v4(dst, z4);
+        else
+          for (int e = 0; e < p.N - col; ++e) reinterpret_cast<uint16_t*>(dst)[e] = 0;
+      }
+    }
+    return;
+  }
   // one TMA store of a staged 32 x 64 bf16 plane (dense box or 4-row scatter)
   auto store_plane = [&](const CUtensorMap* tm, uint8_t* buf, int col0) {
     fence_proxy_async_smem();

@@ -158,6 +158,7 @@ struct GemmParams {
                            // (pruned units Zero) -- no scratch, no column-spread pass
   const int32_t* col_kept; // spread: compact column i -> full column col_kept[i] (ascending; col_pos inverse)
   int skip_zero;           // no all-pruned (Zero) units: the column-spread pass writes the Zero rows P itself
+  int zero_generic;        // all-pruned units at a lineage row map written by generic 16-byte stores, not scatter4
 };
 // Cluster split-K choice for a dW launch with `splits` K-slices: the split
 // count to run as clusters (<= splits, cluster of cg x cs CTAs fits and every

@@ -18,16 +18,27 @@ import bench  # noqa: E402
 
 cfg = CONFIGS[os.environ.get("CFG", "c2")]
 h, f, N = cfg.h, cfg.f, cfg.N
+e = int(os.environ.get("TP", "1"))        # TP > 1: rank 0's shard of a TP = e layer (collectives not run)
+a, u = h // e, f // e
+gamma = float(os.environ.get("GAMMA", "0.5"))
 ctx = Z.ztp_ctx_create(0, 1, None, 0)
-sh = bench.rank_shards(cfg, 1, 0)
+sh = bench.rank_shards(cfg, e, 0)
 dev = {k: torch.from_numpy(v.astype(np.float32)).cuda().to(torch.bfloat16) for k, v in sh.items()}
-L = ZtpLayer(ctx, h, f, N, 0, 1, dev)
+L = ZtpLayer(ctx, h, f, N, 0, e, dev)
 L.X.normal_()
 L.G.normal_()
-sc = {s: torch.from_numpy(v).cuda() for s, v in bench.scores_for(cfg, 0, {"qkv": h, "o": h, "fc1": h, "fc2": f}).items()}
+sc = {s: torch.from_numpy(v).cuda() for s, v in bench.scores_for(cfg, 0, {"qkv": h, "o": a, "fc1": h, "fc2": u}).items()}
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
-L.set_selection(Z.ztp_layer_prune_counts(Z.ztp_plan_uniform(1, float(os.environ.get("GAMMA", "0.5"))), 0, h, h, f), sc)
+if e == 1:
+    L.set_selection(Z.ztp_layer_prune_counts(Z.ztp_plan_uniform(1, gamma), 0, h, h, f), sc)
+else:
+    from paper_2401_11469_b200.layer import layer_prune_counts
+    p = Z.PlanT()
+    p.world = e
+    p.role[0] = Z.RESIZE if gamma > 0 else Z.NORMAL
+    p.gamma[0] = p.gamma_r[0] = gamma
+    L.set_selection(layer_prune_counts(p, 0, h, a, u), sc)
 for _ in range(3):
     L.step(stream, select=False)
 torch.cuda.synchronize()
