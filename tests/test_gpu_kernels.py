@@ -518,3 +518,87 @@ def test_anti_endless_loop_on_gpu_S410(env, incremental):
         assert len(set(sets)) >= 3
     else:
         assert all(sset == sets[0] for sset in sets)
+
+
+# ------------------------------------------------------ guard bands (no OOB writes)
+
+def _guarded(torch, r, c, dtype):
+    """[r, c] view of a NaN-filled buffer with 3 extra rows and >= 24 extra
+    columns of padding (ld a multiple of 8): writes outside the logical
+    tensor would change the padding."""
+    ld = (c + 24 + 7) // 8 * 8
+    buf = torch.full((r + 3, ld), float("nan"), device="cuda", dtype=dtype)
+    return buf, buf[:r, :c]
+
+
+def _band_intact(buf, r, c):
+    return bool(torch_isnan_all(buf[r:, :]) and torch_isnan_all(buf[:, c:]))
+
+
+def torch_isnan_all(t):
+    import torch
+    return bool(torch.isnan(t.float()).all().item())
+
+
+@pytest.mark.parametrize("opts", [{}, {"SPLITK": 0}, {"SPLITK": 0, "SPREAD_EPI": 1}, {"ZERO_GENERIC": 0},
+                                  {"SPLITK": 0, "ZERO_GENERIC": 0}])
+def test_outputs_stay_inside_their_tensors(env, opts):
+    """Every output of the FC1 -> FC2 pair (GeLU epilogues, compact and
+    lineage-mapped rows, Zero tiles, output-pruned dW1 through the split-K
+    reduce, the column-spread pass or the spreading epilogue) is a view into a
+    NaN buffer with guard rows and columns: results match the oracle and no
+    byte outside the logical tensors is written (the compute-sanitizer is
+    unavailable on the GPU pool; this is its stand-in for the write paths)."""
+    Z, torch, ctx = env
+    for k, v in opts.items():
+        Z.ztp_set_option(ctx, getattr(Z, "OPT_" + k), v)
+    try:
+        h, f, N, seed = 264, 776, 1032, 4711
+        X = I.normal(seed, "x", h, N)
+        W1 = I.uniform_sym(seed, "w1", h, f, 1 / math.sqrt(h))
+        W2 = I.uniform_sym(seed, "w2", f, h, 1 / math.sqrt(f))
+        G = I.normal(seed, "g", h, N)
+        S1, P1 = O.select(I.lognormal_scores(seed, "s1", h), int(0.6 * h))
+        S2, P2 = O.select(I.lognormal_scores(seed, "s2", f), int(0.5 * f))
+        nk2 = len(S2)
+        bf = torch.bfloat16
+        x, w1, w2, g = dev(torch, X), dev(torch, W1), dev(torch, W2), dev(torch, G)
+        s1, k1 = _sel_dev(Z, torch, S1, P1, 0, 2)
+        s2, k2 = _sel_dev(Z, torch, S2, P2, 0, 3)
+        pos = np.full(f, -1, dtype=np.int32)
+        pos[np.asarray(S2)] = np.arange(nk2, dtype=np.int32)
+        pos = torch.tensor(pos, device="cuda")
+        outs = {}
+        for name, (r, c) in {"hc": (nk2, N), "prec": (nk2, N), "y": (h, N), "g1c": (nk2, N), "dy1": (h, N),
+                             "dw1": (h, f), "dw2": (f, h)}.items():
+            outs[name] = _guarded(torch, r, c, bf) + (r, c)
+        v = {k_: t[1] for k_, t in outs.items()}
+        ws1 = empty(torch, h, f, bf)
+        a1 = Z.linear_args(x_t=x, w_t=w1, y_t=v["hc"], pre_t=v["prec"], ws_t=ws1, sel_=s1, act=Z.ACT_GELU,
+                           y_pos=pos, out_sel=s2)
+        a2 = Z.linear_args(x_t=v["hc"], w_t=w2, y_t=v["y"], g_t=g, dx_t=v["g1c"], dw_t=v["dw2"], pre_in_t=v["prec"],
+                           sel_=s2, act_in=Z.ACT_GELU, x_compact=True, dx_compact=True)
+        b1 = Z.linear_args(x_t=x, w_t=w1, g_t=v["g1c"], dx_t=v["dy1"], dw_t=v["dw1"], ws_t=ws1, sel_=s1, y_pos=pos,
+                           out_sel=s2)
+        Z.ztp_col_linear(ctx, Z.FWD, a1)
+        Z.ztp_row_linear(ctx, Z.FWD, a2)
+        Z.ztp_row_linear(ctx, Z.BWD, a2)
+        Z.ztp_col_linear(ctx, Z.BWD, b1)
+        Z.ztp_join(ctx)
+        Z.ztp_sync(ctx)
+        S2a = np.asarray(S2)
+        pre_ref = O.linear_fwd(W1, X, S1)
+        H_ref = O.gelu_tanh(pre_ref)
+        G1_full = O.linear_bwd_dx(W2, G, S2, P2) * O.gelu_tanh_grad(pre_ref)
+        refs = {"prec": pre_ref[S2a], "hc": H_ref[S2a], "y": O.linear_fwd(W2, H_ref, S2), "g1c": G1_full[S2a],
+                "dw2": O.linear_bwd_dw(H_ref, G, S2, P2), "dy1": O.linear_bwd_dx(W1, G1_full, S1, P1),
+                "dw1": O.linear_bwd_dw(X, G1_full, S1, P1)}
+        for name, (buf, view, r, c) in outs.items():
+            gh = host(view)
+            assert np.isfinite(gh).all(), f"{name}: unwritten (NaN) elements"
+            ok, e = err_ok(gh, refs[name], TOL_BF16)
+            assert ok, f"{name}: max|err|/||ref|| = {e:.3e}"
+            assert _band_intact(buf, r, c), f"{name}: a write landed outside the tensor"
+    finally:
+        for k in opts:
+            Z.ztp_set_option(ctx, getattr(Z, "OPT_" + k), {"SPLITK": 1, "SPREAD_EPI": 0, "ZERO_GENERIC": 1}[k])
