@@ -3,7 +3,12 @@ inside the captured step graph (profiling mode 3): for each launch the
 median / max over CTAs of  wait = PDL wait end - CTA start,  fill = first
 operand stage ready - PDL wait end,  main = last MMA commit - first stage,
 tail = stores complete - last MMA commit,  end = CTA end - stores complete,
-and the launch span (first PDL-wait end .. last CTA end)."""
+and the launch span (first PDL-wait end .. last CTA end).  Under the A-operand
+prefetch (ZTP_OPT_A_EARLY) the producer warp waits for the predecessor only
+after issuing its first A loads, and thread 0 stamps the wait end before
+that: such a launch's remaining PDL wait shows up in `fill` (e.g. FC2 FWD
+right after FC1 FWD's long two-plane tail).
+TP = e > 1 (env TP, GAMMA): rank 0's shard of a TP = e layer, collectives not run."""
 import os
 import sys
 
