@@ -210,6 +210,9 @@ ztp_status ztp_transpose(ztp_ctx* ctx, const ztp_mat* src, const ztp_mat* dst, c
  *                                            map are written by generic 16-byte stores (eight
  *                                            lanes per 128-byte row segment) instead of TMA
  *                                            scatter4 boxes
+ *   ZTP_OPT_TAIL_HALVES (ZTP_TAIL_HALVES, 1) a FWD GEMM whose last round of 256 x 256 tiles fills at
+ *                                            most half of the CTA pairs runs those tiles as two
+ *                                            128-column halves each, on twice as many pairs
  * ------------------------------------------------------------------------- */
 typedef enum ztp_option {
   ZTP_OPT_CONC = 0,
@@ -224,7 +227,8 @@ typedef enum ztp_option {
   ZTP_OPT_AUX_WEIGHT = 9,
   ZTP_OPT_FLAGS = 10,
   ZTP_OPT_SPREAD_EPI = 11,
-  ZTP_OPT_ZERO_GENERIC = 12
+  ZTP_OPT_ZERO_GENERIC = 12,
+  ZTP_OPT_TAIL_HALVES = 13
 } ztp_option;
 ztp_status ztp_set_option(ztp_ctx* ctx, ztp_option opt, double value);
 ztp_status ztp_get_option(const ztp_ctx* ctx, ztp_option opt, double* value);

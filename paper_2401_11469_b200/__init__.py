@@ -25,7 +25,7 @@ __all__ = [
 ]
 from ._lib import (TRANSPORT_NCCL, TRANSPORT_PEER, COLL_TREE, COLL_P2P, OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4,  # noqa: E402
                    OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS, OPT_A_EARLY, OPT_PART, OPT_AUX_WEIGHT, OPT_FLAGS,
-                   OPT_SPREAD_EPI, OPT_ZERO_GENERIC)
+                   OPT_SPREAD_EPI, OPT_ZERO_GENERIC, OPT_TAIL_HALVES)
 
 
 def _stream(stream) -> Optional[int]:

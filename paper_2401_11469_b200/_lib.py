@@ -26,7 +26,7 @@ CRIT_AVG, CRIT_MIN = 0, 1
 NORMAL, RESIZE, MIGRATE, SPLIT = 0, 1, 2, 3
 KIND_FWD, KIND_DX, KIND_DW = 0, 1, 2
 (OPT_CONC, OPT_DW_SHARE, OPT_SQUAT_GUARD, OPT_GATHER4, OPT_SPLITK, OPT_GROUP, OPT_PEER_CTAS, OPT_A_EARLY, OPT_PART,
- OPT_AUX_WEIGHT, OPT_FLAGS, OPT_SPREAD_EPI, OPT_ZERO_GENERIC) = range(13)
+ OPT_AUX_WEIGHT, OPT_FLAGS, OPT_SPREAD_EPI, OPT_ZERO_GENERIC, OPT_TAIL_HALVES) = range(14)
 
 
 class ZtpError(RuntimeError):

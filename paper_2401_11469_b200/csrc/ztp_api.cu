@@ -61,6 +61,7 @@ struct ztp_ctx {
   int a_early = 1;
   int spread_epi = 0;         // output-pruned unsplit dW: column spread inside the GEMM epilogue (opt-in)
   int zero_generic = 1;       // Zero units at a lineage row map: generic stores instead of TMA scatter4
+  int tail_halves = 1;        // FWD: a last round filling <= half the pairs runs as 128-column halves
   int64_t lg_id = -1;                  // ztp::launch_seq() right after the last eligible GEMM launch (-1: none)
   cudaStream_t lg_stream = nullptr;
   const char* lg_out[2] = {nullptr, nullptr};
@@ -317,6 +318,7 @@ ztp_status gemm_build_bf16(ztp_ctx* c, int kind, Src A, Src B, int64_t n_out, co
   p.col_pos = col_pos;
   p.n_full = n_full;
   p.zero_generic = c->zero_generic;
+  p.tail_ok = c->tail_halves;
   // early start (PDL wait at exit) only when nothing between the launches
   // depends on stamps (emulation) and the workspaces are disjoint (dW uses
   // its own split-K workspace)
@@ -1269,6 +1271,7 @@ ztp_status ztp_ctx_create(ztp_ctx** out, int rank, int world, const unsigned cha
   if (const char* ae = getenv("ZTP_A_EARLY")) c->a_early = atoi(ae) != 0;
   if (const char* se = getenv("ZTP_SPREAD_EPI")) c->spread_epi = atoi(se) != 0;
   if (const char* zg = getenv("ZTP_ZERO_GENERIC")) c->zero_generic = atoi(zg) != 0;
+  if (const char* th = getenv("ZTP_TAIL_HALVES")) c->tail_halves = atoi(th) != 0;
   if (const char* fl = getenv("ZTP_FLAGS")) c->flags_opt = atoi(fl) != 0;
   if (const char* de = getenv("ZTP_DEBUG_EPI")) c->dbg_epi = atoi(de);
   if (const char* ds = getenv("ZTP_DEBUG_SKIP")) c->dbg_skip = atoi(ds);
@@ -1920,6 +1923,7 @@ ztp_status ztp_set_option(ztp_ctx* c, ztp_option opt, double v) {
     case ZTP_OPT_FLAGS: c->flags_opt = iv != 0; return ZTP_OK;
     case ZTP_OPT_SPREAD_EPI: c->spread_epi = iv != 0; return ZTP_OK;
     case ZTP_OPT_ZERO_GENERIC: c->zero_generic = iv != 0; return ZTP_OK;
+    case ZTP_OPT_TAIL_HALVES: c->tail_halves = iv != 0; return ZTP_OK;
   }
   return fail(c, ZTP_EINVAL, "ztp_set_option: unknown option " + std::to_string((int)opt));
 }
@@ -1940,6 +1944,7 @@ ztp_status ztp_get_option(const ztp_ctx* c, ztp_option opt, double* v) {
     case ZTP_OPT_FLAGS: *v = c->flags_opt; return ZTP_OK;
     case ZTP_OPT_SPREAD_EPI: *v = c->spread_epi; return ZTP_OK;
     case ZTP_OPT_ZERO_GENERIC: *v = c->zero_generic; return ZTP_OK;
+    case ZTP_OPT_TAIL_HALVES: *v = c->tail_halves; return ZTP_OK;
   }
   return fail(nullptr, ZTP_EINVAL, "ztp_get_option: unknown option " + std::to_string((int)opt));
 }

@@ -122,6 +122,7 @@ __device__ __forceinline__ float2 unpack2(uint32_t u) { return make_float2(bf16_
 struct Work {
   int m0, n0, kb0, kb1, split;
   bool zero;
+  int half;   // -1: the whole 256-column tile; 0 / 1: a 128-column half (2-CTA FWD tail, GemmParams::tail_r)
 };
 
 template <int KIND, int TM>
@@ -142,15 +143,25 @@ struct Sched {
     units_c = tiles_c * S;
     zero_m = m_tiles - mc;
     num_units = units_c + (S == 1 && !p.skip_zero ? zero_m * n_tiles : 0);
+    tail_r = (KIND == KIND_FWD && S == 1) ? p.tail_r : 0;
+    num_units += tail_r;   // the last tail_r tiles run as two 128-column halves each
   }
+  int tail_r;
   // all-pruned (zero) units come FIRST: the epilogue warps write them while
   // the producer / MMA warps, which skip them, already stream the first tile.
   __device__ __forceinline__ Work get(int u0) const {
     Work w;
-    const int nz = num_units - units_c;
+    const int nz = num_units - units_c - tail_r;   // all-pruned units (the tail halves are computed ones)
+    w.half = -1;
     if (u0 >= nz) {
       const int u = u0 - nz;
-      const int s = u / tiles_c, t = u - s * tiles_c;
+      int s = u / tiles_c, t = u - s * tiles_c;
+      if (tail_r > 0 && u >= tiles_c - tail_r) {   // FWD tail: last round's tiles as halves, one per pair
+        const int v = u - (tiles_c - tail_r);
+        s = 0;
+        t = tiles_c - tail_r + (v >> 1);
+        w.half = v & 1;
+      }
       w.m0 = (t % mc) * TM;
       w.n0 = (t / mc) * BN;
       w.split = s;
@@ -219,7 +230,7 @@ __device__ __forceinline__ void produce_unit(const CUtensorMap* tmA, const CUten
     uint8_t* sa = ring + ps.stage * C::STAGE_BYTES;
     uint8_t* sb = sa + A_BYTES;
     uint64_t* fb = &full[ps.stage];
-    if (leader && lane == 0) mbar_expect_tx(fb, CG * C::STAGE_BYTES);
+    if (leader && lane == 0) mbar_expect_tx(fb, CG * (wk.half < 0 ? C::STAGE_BYTES : A_BYTES + 8192));
     __syncwarp();
     auto load = [&](const CUtensorMap* tm, void* dst, int c0, int c1) {
       if (CG == 2)
@@ -259,8 +270,12 @@ __device__ __forceinline__ void produce_unit(const CUtensorMap* tmA, const CUten
         }
         if (p.fi_flags && kb == wk.kb0) flag_wait(p.fi_flags + wk.n0 / BN, ftgt);
         if (!BG) {
+          if (wk.half >= 0) {   // a 128-column half: this CTA's h-th 64-column box into block 0
+            load(tmB, sb, bn0 + 64 * wk.half, kb * BK);
+          } else {
 #pragma unroll
-          for (int b = 0; b < BNL / 64; ++b) load(tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
+            for (int b = 0; b < BNL / 64; ++b) load(tmB, sb + b * 8192, bn0 + 64 * b, kb * BK);
+          }
         }
       }
     } else {
@@ -311,7 +326,7 @@ __device__ __forceinline__ void produce_unit_early(const CUtensorMap* tmA, const
     mbar_wait(&empty[ps.stage], ps.phase ^ 1);
     uint8_t* sa = ring + ps.stage * C::STAGE_BYTES;
     uint64_t* fb = &full[ps.stage];
-    if (leader && lane == 0) mbar_expect_tx(fb, CG * C::STAGE_BYTES);
+    if (leader && lane == 0) mbar_expect_tx(fb, CG * (wk.half < 0 ? C::STAGE_BYTES : A_BYTES + 8192));
     __syncwarp();
     if (lane == 0) {
       if (KIND == KIND_FWD) {
@@ -336,6 +351,8 @@ __device__ __forceinline__ void produce_unit_early(const CUtensorMap* tmA, const
     if (lane == 0) {
       if (KIND == KIND_DW) {
         load(tmB, fb, sb, kb * BK, bn0);
+      } else if (wk.half >= 0) {
+        load(tmB, fb, sb, bn0 + 64 * wk.half, kb * BK);
       } else {
 #pragma unroll
         for (int b = 0; b < BNL / 64; ++b) load(tmB, fb, sb + b * 8192, bn0 + 64 * b, kb * BK);
@@ -354,7 +371,9 @@ __device__ __forceinline__ void mma_unit(const Work& wk, int lane, uint16_t pmas
                                          uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
                                          Pipe& ps, unsigned long long** first = nullptr) {
   using C = Cfg<CG>;
-  constexpr uint32_t IDESC = make_idesc_bf16(C::TM, BN, KIND == KIND_FWD ? 1 : 0, KIND == KIND_DW ? 0 : 1);
+  constexpr uint32_t IDESC_F = make_idesc_bf16(C::TM, BN, KIND == KIND_FWD ? 1 : 0, KIND == KIND_DW ? 0 : 1);
+  constexpr uint32_t IDESC_H = make_idesc_bf16(C::TM, BN / 2, KIND == KIND_FWD ? 1 : 0, KIND == KIND_DW ? 0 : 1);
+  const uint32_t IDESC = wk.half >= 0 ? IDESC_H : IDESC_F;
   mbar_wait(&tempty[ps.acc], ps.aphase ^ 1);
   tc_fence_after();
   const uint32_t d_tmem = tmem_base + ps.acc * BN;
@@ -436,8 +455,12 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
   };
   const int m0 = wk.m0 + BM * rank, n0 = wk.n0;
   const bool zt = wk.zero;
-  const uint32_t tbase = tmem_base + ((uint32_t)(lq * 32) << 16) + ps.acc * BN + ch * (BN / 2);
-  const int nc0 = n0 + ch * (BN / 2);   // first output column of this warp
+  // a 128-column half unit (2-CTA FWD tail): accumulator columns [64 ch, +64)
+  // hold the tile's columns [128 ch + 64 h, +64) -- each CTA staged its h-th box
+  const bool hu = wk.half >= 0;
+  const int nchunks = hu ? 1 : BN / 128;
+  const uint32_t tbase = tmem_base + ((uint32_t)(lq * 32) << 16) + ps.acc * BN + ch * (hu ? BN / 4 : BN / 2);
+  const int nc0 = n0 + ch * (BN / 2) + (hu ? 64 * wk.half : 0);   // first output column of this warp
   // Two staging buffers per warp alternate: before refilling one, the
   // lanes that issued TMA stores wait until at most the other buffer's
   // store is still reading (bulk wait_group.read 1).
@@ -632,7 +655,7 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
   };
   const bool two_planes = p.epi == EPI_GELU || p.epi == EPI_GELU_D;
 #pragma unroll 1
-  for (int c = 0; c < BN / 128; ++c) {
+  for (int c = 0; c < nchunks; ++c) {
     const int col0 = nc0 + c * 64;
     uint32_t v[64];
     if (has_aux && c > 0) load_aux(col0);   // before the TMEM load so the two overlap (L2 hit)
@@ -640,7 +663,7 @@ __device__ __forceinline__ void epilogue_unit(const CUtensorMap* tmO, const CUte
       tmem_ld_32x32b_x32(tbase + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
       tmem_ld_32x32b_x32(tbase + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
       tmem_ld_wait();
-      if (c == BN / 128 - 1) release();   // accumulator fully in registers: TMEM free for tile i+2
+      if (c == nchunks - 1) release();   // accumulator fully in registers: TMEM free for tile i+2
     } else {
 #pragma unroll
       for (int i = 0; i < 64; ++i) v[i] = 0u;
@@ -1298,7 +1321,20 @@ static int units_of(int kind, int cg, const GemmParams& p) {
   const int m_tiles = (p.M + tm - 1) / tm, n_tiles = (p.N + BN - 1) / BN;
   int mc = m_tiles;
   if (kind != KIND_FWD) mc = std::min(m_tiles, (p.n_kept + tm - 1) / tm);
-  return mc * n_tiles * p.splits + (p.splits == 1 && !p.skip_zero ? (m_tiles - mc) * n_tiles : 0);
+  return mc * n_tiles * p.splits + (p.splits == 1 && !p.skip_zero ? (m_tiles - mc) * n_tiles : 0) +
+         (kind == KIND_FWD && p.splits == 1 ? p.tail_r : 0);
+}
+
+// FWD tail (2-CTA, unsplit, dense boxes): when the last round of tiles fills
+// at most half of the CTA pairs, its tiles run as two 128-column halves on
+// twice as many pairs -- the launch ends half a tile earlier (c2: QKV 320
+// tiles = 4 x 74 + 24, FC1 256 = 3 x 74 + 34).  Returns the tile count.
+static int tail_halves(int kind, int cg, const GemmParams& p, int num_sms, bool gathered) {
+  if (kind != KIND_FWD || cg != 2 || p.splits != 1 || !p.tail_ok || gathered || p.fo_flags || p.fi_flags) return 0;
+  const int m_tiles = (p.M + BM * cg - 1) / (BM * cg), n_tiles = (p.N + BN - 1) / BN;
+  const int T = m_tiles * n_tiles, P = num_sms / cg;
+  const int R = T >= P ? T % P : T;
+  return (R > 0 && 2 * R <= P) ? R : 0;
 }
 
 // After a GEMM launch: the split-K reduce (fixed split order, the epilogue
@@ -1333,9 +1369,10 @@ static cudaError_t launch_kind(const Maps& mp, const GemmParams& p, int num_sms,
     cudaError_t e = ensure_smem_optin((const void*)kern, smem);
     if (e != cudaSuccess) return e;
   }
-  const int units = units_of(KIND, CG, p);
-  const int pairs = p.cs > 1 ? units : std::min(units, num_sms / CG);   // cluster split-K: one unit per pair
   GemmParams pl = p;
+  pl.tail_r = tail_halves(KIND, CG, p, num_sms, AG || BG);
+  const int units = units_of(KIND, CG, pl);
+  const int pairs = pl.cs > 1 ? units : std::min(units, num_sms / CG);   // cluster split-K: one unit per pair
   if (pl.fo_flags) {
     const int n_tiles = (p.N + BN - 1) / BN;
     if (p.splits != 1 || p.cs > 1 || p.col_pos || n_tiles > FLAG_NB || units % n_tiles) {

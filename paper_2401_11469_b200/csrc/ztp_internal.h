@@ -159,6 +159,8 @@ struct GemmParams {
   const int32_t* col_kept; // spread: compact column i -> full column col_kept[i] (ascending; col_pos inverse)
   int skip_zero;           // no all-pruned (Zero) units: the column-spread pass writes the Zero rows P itself
   int zero_generic;        // all-pruned units at a lineage row map written by generic 16-byte stores, not scatter4
+  int tail_ok;             // FWD: the last partial round of tiles may run as 128-column halves (ZTP_OPT_TAIL_HALVES)
+  int tail_r;              // set by the launcher: that many last tiles run as two halves each (0: off)
 };
 // Cluster split-K choice for a dW launch with `splits` K-slices: the split
 // count to run as clusters (<= splits, cluster of cg x cs CTAs fits and every

@@ -230,7 +230,8 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None, f32=False, pl
                                   {"PART": 0}, {"PART": 2}, {"AUX_WEIGHT": 2.5}, {"FLAGS": 1},
                                   {"DW_SHARE": 0.8}, {"DW_SHARE": 1.6}, {"SPLITK": 0},
                                   {"SPLITK": 0, "SPREAD_EPI": 1}, {"SPLITK": 0, "SPREAD_EPI": 1, "GROUP": 1},
-                                  {"SPREAD_EPI": 1}, {"ZERO_GENERIC": 0}])
+                                  {"SPREAD_EPI": 1}, {"ZERO_GENERIC": 0},
+                                  {"TAIL_HALVES": 0}])
 def test_layer_schedule_variants_graph(tz, opts):
     """The scheduling options (ztp_set_option: grouped or concurrent or
     serial dX / dW, the SM split weight -- it changes the dW split-K counts --,

@@ -127,7 +127,8 @@ def test_options_round_trip_and_errors():
         for opt, val in ((Z.OPT_CONC, 0), (Z.OPT_DW_SHARE, 1.5), (Z.OPT_SQUAT_GUARD, 0), (Z.OPT_GATHER4, 1),
                          (Z.OPT_SPLITK, 0), (Z.OPT_GROUP, 2), (Z.OPT_PEER_CTAS, 16), (Z.OPT_A_EARLY, 0),
                          (Z.OPT_PART, 0), (Z.OPT_AUX_WEIGHT, 2.0), (Z.OPT_FLAGS, 1),
-                         (Z.OPT_SPREAD_EPI, 1), (Z.OPT_ZERO_GENERIC, 0)):
+                         (Z.OPT_SPREAD_EPI, 1), (Z.OPT_ZERO_GENERIC, 0),
+                         (Z.OPT_TAIL_HALVES, 0)):
             Z.ztp_set_option(ctx, opt, val)
             assert Z.ztp_get_option(ctx, opt) == val
         for opt, bad in ((Z.OPT_DW_SHARE, 0.0), (Z.OPT_GROUP, 3), (Z.OPT_PEER_CTAS, 0), (Z.OPT_PART, 3),
