@@ -537,7 +537,12 @@ typedef struct ztp_linear_args {
   /* FWD: compact copies already written by ztp_prepare for this lineage
    * entry -- bit 0: xs_t, bit 1: ws_t -- so this call does not refill them. */
   int32_t prepared;
-  int32_t _pad1;
+  /* BWD with dw_t but no dx_t: 1 = run this dW GEMM on the context's side
+   * stream, after the caller stream's current position, and return at once
+   * (joined like a concurrent dW: ztp_join or the next FWD call).  The caller
+   * launches its next work beside it -- e.g. the attention projection's dW
+   * next to the QKV backward, after its dX ran alone on every SM. */
+  int32_t dw_side;
   int64_t n_out;               /* output units computed (<= w_t.cols); 0 = w_t.cols */
   int32_t impute;              /* ztp_impute (Zero is the paper's choice) */
   int32_t act;                 /* FWD activation of this layer's output */

@@ -232,8 +232,8 @@ def linear_args(x_t=None, w_t=None, y_t=None, pre_t=None, g_t=None, dx_t=None, d
                 sel_: Optional[Sel] = None, n_out: int = 0, impute: int = IMPUTE_ZERO, act: int = ACT_NONE,
                 act_in: int = ACT_NONE, skip_collective: int = 0, xs_t=None, ws_t=None, y_pos=None,
                 x_compact: bool = False, dx_compact: bool = False, out_sel: Optional[Sel] = None,
-                hist_dx=None, hist_dw=None, gather_output: bool = False, input_is_parallel: bool = True
-                ) -> LinearArgs:
+                hist_dx=None, hist_dw=None, gather_output: bool = False, input_is_parallel: bool = True,
+                dw_side: bool = False) -> LinearArgs:
     a = LinearArgs()
     a.x_t, a.w_t, a.y_t, a.pre_t = mat(x_t), mat(w_t), mat(y_t), mat(pre_t)
     a.g_t, a.dx_t, a.dw_t, a.pre_in_t = mat(g_t), mat(dx_t), mat(dw_t), mat(pre_in_t)
@@ -252,6 +252,7 @@ def linear_args(x_t=None, w_t=None, y_t=None, pre_t=None, g_t=None, dx_t=None, d
     a.gather_output = int(gather_output)
     a.input_is_parallel = int(input_is_parallel)
     a.skip_collective = skip_collective
+    a.dw_side = int(dw_side)
     return a
 
 

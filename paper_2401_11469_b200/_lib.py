@@ -90,7 +90,7 @@ class LinearArgs(C.Structure):
     _fields_ = [("x_t", Mat), ("w_t", Mat), ("y_t", Mat), ("pre_t", Mat), ("g_t", Mat), ("dx_t", Mat),
                 ("dw_t", Mat), ("pre_in_t", Mat), ("xs_t", Mat), ("ws_t", Mat), ("sel", C.POINTER(Sel)),
                 ("y_pos", C.c_void_p), ("x_compact", C.c_int32), ("dx_compact", C.c_int32),
-                ("out_sel", C.POINTER(Sel)), ("prepared", C.c_int32), ("_pad1", C.c_int32), ("n_out", C.c_int64),
+                ("out_sel", C.POINTER(Sel)), ("prepared", C.c_int32), ("dw_side", C.c_int32), ("n_out", C.c_int64),
                 ("impute", C.c_int32), ("act", C.c_int32), ("act_in", C.c_int32), ("gather_output", C.c_int32),
                 ("input_is_parallel", C.c_int32), ("skip_collective", C.c_int32),
                 ("hist_dx", C.POINTER(Mat)), ("hist_dw", C.POINTER(Mat))]

@@ -1063,8 +1063,18 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
   // straggler: each GEMM is stretched from its own stamp slot; not while
   // profiling with events, which times each GEMM alone)
   const bool conc = c->conc_bwd && c->prof_on != 1 && a->dx_t.ptr && a->dw_t.ptr && dtype == ZTP_BF16;
+  // dW alone on the side stream (dw_side): it shares the GPU with what the
+  // caller launches next on its stream (half the SMs for its persistent grid)
+  const bool side_only = a->dw_side && !a->dx_t.ptr && a->dw_t.ptr && c->conc_bwd && c->prof_on != 1 &&
+                         dtype == ZTP_BF16;
   cudaStream_t sw = st;
   int cap_dx = 0, cap_dw = 0;
+  if (side_only) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_c, st));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_c, 0));
+    sw = c->side_stream;
+    cap_dw = 2 * ((c->num_sms / 2) / 2);
+  }
   if (conc) {
     CUDA_TRY(c, cudaEventRecord(c->ev_c, st));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_c, 0));
@@ -1191,7 +1201,7 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
   // the dW outputs feed nothing later in the step: the side stream is joined
   // by ztp_join (or the next FWD call), not here, so the next linear's dX
   // does not wait for this dW
-  if (conc) c->side_pending = true;
+  if (conc || side_only) c->side_pending = true;
   if (reduce_dx) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_b, 0));
   return ZTP_OK;
 }

@@ -132,6 +132,9 @@ class ZtpLayer:
         and the epilogues write / zero-impute rows at their positions."""
         self.ctx, self.h, self.f, self.N = ctx, h, f, N
         self.rank, self.world = rank, world
+        # the O projection's dW after the core (beside the QKV backward) instead of beside its own dX
+        # (dw_side): O dX then runs alone on every SM; profiles/r02_late_o_dw_ab.txt
+        self.late_o_dw = os.environ.get("ZTP_LATE_O_DW", "0") != "0"   # measured slower at c2: opt-in
         self.a = h // world                  # attention features per rank
         self.u = f // world                  # MLP hidden units per rank
         self.cap = mig_cap
@@ -320,6 +323,7 @@ class ZtpLayer:
         self.b_fc1 = L(x_t=self.Y1, w_t=self.w1_t, g_t=self.G1[:nfc], dx_t=self.dY1, dw_t=self.dw1, sel_=sl["fc1"],
                        n_out=nfc)
         self.b_o = L(x_t=self.ctxC, w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx, dw_t=self.do, sel_=sl["o"])
+        self.b_o_dx = self.b_o_dw = None
         self.b_qkv = L(x_t=self.X, w_t=self.qkv_t, g_t=self.gQKV, dx_t=self.dX, dw_t=self.dqkv, sel_=sl["qkv"],
                        n_out=3 * a)
 
@@ -379,6 +383,11 @@ class ZtpLayer:
                        **y1_kw)
         self.b_o = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx, dw_t=self.do,
                      ws_t=self.Wo_c, sel_=self.sels["o"], x_compact=True)
+        # late O dW: dX alone on every SM, the core, then dW on the side stream beside the QKV backward
+        self.b_o_dx = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, g_t=self.dY1, dx_t=self.dctx,
+                        ws_t=self.Wo_c, sel_=self.sels["o"], x_compact=True)
+        self.b_o_dw = L(x_t=self.ctxC[:nk["o"]], w_t=self.o_t, g_t=self.dY1, dw_t=self.do,
+                        ws_t=self.Wo_c, sel_=self.sels["o"], x_compact=True, dw_side=True)
         self.b_qkv = L(x_t=self.X, w_t=self.qkv_t, g_t=self.gQKV[:ngq], dx_t=self.dX, dw_t=self.dqkv, xs_t=self.Xc,
                        ws_t=self.Wqkv_c, sel_=self.sels["qkv"], n_out=3 * a, **vkw)
 
@@ -471,7 +480,8 @@ class ZtpLayer:
 
     def bwd_attn(self, stream=None):
         c = self.ctx
-        Z.ztp_row_linear(c, Z.BWD, self.b_o, stream)          # dctx, dWo
+        late = self.late_o_dw and self.b_o_dw is not None
+        Z.ztp_row_linear(c, Z.BWD, self.b_o_dx if late else self.b_o, stream)   # dctx (+ dWo beside it)
         if self.attn is not None:
             self._attn_bwd(stream)
         elif self.vsel is not None:
@@ -479,6 +489,8 @@ class ZtpLayer:
                        v_compact=True)
         else:
             Z.ztp_core(c, Z.BWD, self.gQKV, self.dctx, self.a, self.a, None, 0, stream)
+        if late:
+            Z.ztp_row_linear(c, Z.BWD, self.b_o_dw, stream)   # dWo on the side stream
         Z.ztp_col_linear(c, Z.BWD, self.b_qkv, stream)        # dX (+ all-reduce), dWqkv
         Z.ztp_join(c, stream)                                  # concurrent dW work (ZTP_CONC) ends the step
 

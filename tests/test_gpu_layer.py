@@ -231,7 +231,7 @@ def _simulate(tz, e, h, f, N, gam, mig=None, seed=7, sampled=None, f32=False, pl
                                   {"DW_SHARE": 0.8}, {"DW_SHARE": 1.6}, {"SPLITK": 0},
                                   {"SPLITK": 0, "SPREAD_EPI": 1}, {"SPLITK": 0, "SPREAD_EPI": 1, "GROUP": 1},
                                   {"SPREAD_EPI": 1}, {"ZERO_GENERIC": 0},
-                                  {"TAIL_HALVES": 0}])
+                                  {"TAIL_HALVES": 0}, {"LATE_O_DW": 1}])
 def test_layer_schedule_variants_graph(tz, opts):
     """The scheduling options (ztp_set_option: grouped or concurrent or
     serial dX / dW, the SM split weight -- it changes the dW split-K counts --,
@@ -246,6 +246,9 @@ def test_layer_schedule_variants_graph(tz, opts):
     ref = O.layer_step(X, G, sh, sel)
     ctx, L = build(tz, sh, 0, 1, h, f, N)
     for k, v in opts.items():
+        if k == "LATE_O_DW":       # layer call order: O dW after the core on the side stream (dw_side)
+            L.late_o_dw = bool(v)
+            continue
         Z.ztp_set_option(ctx, getattr(Z, "OPT_" + k), v)
         assert Z.ztp_get_option(ctx, getattr(Z, "OPT_" + k)) == v
     L.set_selection(nps[0], {s: torch.from_numpy(v).cuda() for s, v in scores[0].items()})
