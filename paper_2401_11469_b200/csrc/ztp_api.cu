@@ -62,6 +62,9 @@ struct ztp_ctx {
   int spread_epi = 0;         // output-pruned unsplit dW: column spread inside the GEMM epilogue (opt-in)
   int zero_generic = 1;       // Zero units at a lineage row map: generic stores instead of TMA scatter4
   int tail_halves = 1;        // FWD: a last round filling <= half the pairs runs as 128-column halves
+  // MMA work queued on the side stream by a dw_side call and not yet part of
+  // a dX / dW partition: work units, k-blocks per unit, CTA pairs it may use
+  int side_bl_units = 0, side_bl_kps = 0, side_bl_pairs = 0;
   int64_t lg_id = -1;                  // ztp::launch_seq() right after the last eligible GEMM launch (-1: none)
   cudaStream_t lg_stream = nullptr;
   const char* lg_out[2] = {nullptr, nullptr};
@@ -856,6 +859,7 @@ ztp_status join_side(ztp_ctx* c, cudaStream_t st) {
     CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_d, 0));
     c->side_pending = false;
   }
+  c->side_bl_units = c->side_bl_kps = c->side_bl_pairs = 0;
   return ZTP_OK;
 }
 
@@ -1074,6 +1078,15 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
     CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_c, 0));
     sw = c->side_stream;
     cap_dw = 2 * ((c->num_sms / 2) / 2);
+    // its work, for the next dX / dW partition (the side stream runs it first)
+    const int cg = ztp::gemm_choose_cg(ztp::KIND_DW, (int)K, nk);
+    const int tm = 128 * cg;
+    const int mc = std::min(((int)K + tm - 1) / tm, (nk + tm - 1) / tm), nt = ((int)n_y + 255) / 256;
+    const int sp = c->allow_splitk ? ztp::gemm_choose_splits(ztp::KIND_DW, (int)K, (int)n_y, (int)N, nk, cap_dw) : 1;
+    const int kb = ((int)N + 63) / 64;
+    c->side_bl_units += mc * nt * sp;
+    c->side_bl_kps = std::max(c->side_bl_kps, (kb + sp - 1) / sp);
+    c->side_bl_pairs = cap_dw / cg;
   }
   if (conc) {
     CUDA_TRY(c, cudaEventRecord(c->ev_c, st));
@@ -1122,9 +1135,14 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
       double best = 1e300;
       int bp = px;
       for (int q = 1; q < pairs; ++q) {
+        // a dw_side GEMM queued on the side stream runs before this dW
+        const double bl = c->side_bl_units > 0
+                              ? std::ceil((double)c->side_bl_units / std::max(1, std::min(c->side_bl_pairs, pairs - q))) *
+                                    c->side_bl_kps * c->dw_share
+                              : 0.0;
         const double t =
             std::max(cost(ztp::KIND_DX, Mx, (int)N, (int)n_y, 2 * q, dx_aux ? c->aux_weight : 1.0, !dxc),
-                     cost(ztp::KIND_DW, (int)K, (int)n_y, (int)N, 2 * (pairs - q), c->dw_share, !os));
+                     bl + cost(ztp::KIND_DW, (int)K, (int)n_y, (int)N, 2 * (pairs - q), c->dw_share, !os));
         if (t < best - 1e-9 || (t < best + 1e-9 && std::abs(q - px) < std::abs(bp - px))) {
           best = std::min(best, t);
           bp = q;
@@ -1134,6 +1152,7 @@ ztp_status linear_impl(ztp_ctx* c, int layer, ztp_phase phase, const ztp_linear_
     }
     cap_dx = 2 * px;
     cap_dw = 2 * (pairs - px);
+    c->side_bl_units = c->side_bl_kps = c->side_bl_pairs = 0;   // accounted
   }
   if (a->dx_t.ptr) {
     if (!mat_ok(a->dx_t) || (dxc ? a->dx_t.rows < nk : a->dx_t.rows != K) || a->dx_t.cols != N ||

@@ -1,7 +1,7 @@
 #!/bin/bash
 # O projection's dW after the core, beside the QKV backward (ZTP_LATE_O_DW=1) vs beside its own dX (=0)
 mkdir -p gpurun_out
-timeout -s KILL 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -2 | tee gpurun_out/lateo_tests.txt
+timeout -s KILL 600 python -m pytest tests/test_gpu_layer.py -x -q -m gpu -k "schedule" 2>&1 | tail -2 | tee gpurun_out/lateo_tests.txt
 for rep in 1 2 3; do for v in 1 0; do
   ZTP_LATE_O_DW=$v CONFIGS="c2 c4" bash tools/gpu_configs.sh > /dev/null 2>&1
   sed "s/^/late$v rep$rep /" gpurun_out/configs.txt >> gpurun_out/lateo_ab.txt
