@@ -1222,15 +1222,38 @@ __global__ void __launch_bounds__(256) ztp_dw_reduce(const GemmParams p) {
         int cc[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) cc[q] = q < nv ? __ldg(p.col_pos + col + q) : -1;
-        float t[S][8];
+        // eight kept columns in a row (col_pos ascends on kept columns), e.g.
+        // the Q / K blocks of dWqkv under V pruning: two float4 loads per split
+        if (cc[0] >= 0 && cc[7] == cc[0] + 7 && (cc[0] & 3) == 0) {
+          float4 a[S], b[S];
 #pragma unroll
-        for (int s = 0; s < S; ++s)
+          for (int s = 0; s < S; ++s) {
+            const float* q = src + s * p.ws_split_stride + cc[0];
+            a[s] = __ldcg(reinterpret_cast<const float4*>(q));
+            b[s] = __ldcg(reinterpret_cast<const float4*>(q + 4));
+          }
 #pragma unroll
-          for (int q = 0; q < 8; ++q) t[s][q] = cc[q] >= 0 ? __ldg(src + s * p.ws_split_stride + cc[q]) : 0.f;
+          for (int s = 0; s < S; ++s) {
+            v[0] += a[s].x;
+            v[1] += a[s].y;
+            v[2] += a[s].z;
+            v[3] += a[s].w;
+            v[4] += b[s].x;
+            v[5] += b[s].y;
+            v[6] += b[s].z;
+            v[7] += b[s].w;
+          }
+        } else {
+          float t[S][8];
 #pragma unroll
-        for (int s = 0; s < S; ++s)
+          for (int s = 0; s < S; ++s)
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] += t[s][q];
+            for (int q = 0; q < 8; ++q) t[s][q] = cc[q] >= 0 ? __ldg(src + s * p.ws_split_stride + cc[q]) : 0.f;
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] += t[s][q];
+        }
       } else {
         float4 a[S], b[S];
 #pragma unroll

@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(256) ztp_expand_cols(const uint16_t* __restric
   const int64_t items = (int64_t)(nk + np) * cpr;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const bool pv = (reinterpret_cast<uintptr_t>(pos) & 15) == 0;
+  const bool sv = (reinterpret_cast<uintptr_t>(src) & 15) == 0 && ld_src % 8 == 0;   // 16-byte runs of src
   for (int64_t it = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += nw) {
     const int i = (int)(it / cpr), c0 = (int)(it % cpr) * GM_CHUNK;
     const int c1 = min(n_full, c0 + GM_CHUNK);
@@ -396,8 +397,11 @@ __global__ void __launch_bounds__(256) ztp_expand_cols(const uint16_t* __restric
           q0 = make_int4(__ldg(pos + c), __ldg(pos + c + 1), __ldg(pos + c + 2), __ldg(pos + c + 3));
           q1 = make_int4(__ldg(pos + c + 4), __ldg(pos + c + 5), __ldg(pos + c + 6), __ldg(pos + c + 7));
         }
-        w[u] = make_uint4(pick(q0.x) | (pick(q0.y) << 16), pick(q0.z) | (pick(q0.w) << 16),
-                          pick(q1.x) | (pick(q1.y) << 16), pick(q1.z) | (pick(q1.w) << 16));
+        if (q0.x >= 0 && q1.w == q0.x + 7 && (q0.x & 7) == 0 && sv)   // eight kept columns in a row
+          w[u] = __ldg(reinterpret_cast<const uint4*>(s + q0.x));
+        else
+          w[u] = make_uint4(pick(q0.x) | (pick(q0.y) << 16), pick(q0.z) | (pick(q0.w) << 16),
+                            pick(q1.x) | (pick(q1.y) << 16), pick(q1.z) | (pick(q1.w) << 16));
       }
     }
 #pragma unroll
