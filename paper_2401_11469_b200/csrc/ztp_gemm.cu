@@ -1222,9 +1222,12 @@ __global__ void __launch_bounds__(256) ztp_dw_reduce(const GemmParams p) {
         int cc[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) cc[q] = q < nv ? __ldg(p.col_pos + col + q) : -1;
-        // eight kept columns in a row (col_pos ascends on kept columns), e.g.
-        // the Q / K blocks of dWqkv under V pruning: two float4 loads per split
-        if (cc[0] >= 0 && cc[7] == cc[0] + 7 && (cc[0] & 3) == 0) {
+        // eight consecutive kept columns, e.g. the Q / K blocks of dWqkv under
+        // V pruning: two float4 loads per split instead of eight gathers
+        bool run = cc[0] >= 0 && (cc[0] & 3) == 0;
+#pragma unroll
+        for (int q = 1; q < 8; ++q) run = run && cc[q] == cc[0] + q;
+        if (run) {
           float4 a[S], b[S];
 #pragma unroll
           for (int s = 0; s < S; ++s) {

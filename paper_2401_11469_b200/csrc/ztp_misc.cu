@@ -311,8 +311,12 @@ __global__ void __launch_bounds__(256) ztp_gather_multi(const GatherJobs J) {
           q0 = make_int4(__ldg(g.cols + c), __ldg(g.cols + c + 1), __ldg(g.cols + c + 2), __ldg(g.cols + c + 3));
           q1 = make_int4(__ldg(g.cols + c + 4), __ldg(g.cols + c + 5), __ldg(g.cols + c + 6), __ldg(g.cols + c + 7));
         }
-        w[u] = make_uint4(gm_pick2(s, q0.x, q0.y), gm_pick2(s, q0.z, q0.w), gm_pick2(s, q1.x, q1.y),
-                          gm_pick2(s, q1.z, q1.w));
+        if ((q0.x & 7) == 0 && q0.y == q0.x + 1 && q0.z == q0.x + 2 && q0.w == q0.x + 3 && q1.x == q0.x + 4 &&
+            q1.y == q0.x + 5 && q1.z == q0.x + 6 && q1.w == q0.x + 7)   // eight consecutive columns: one 16-byte load
+          w[u] = __ldg(reinterpret_cast<const uint4*>(s + q0.x));
+        else
+          w[u] = make_uint4(gm_pick2(s, q0.x, q0.y), gm_pick2(s, q0.z, q0.w), gm_pick2(s, q1.x, q1.y),
+                            gm_pick2(s, q1.z, q1.w));
       }
     }
 #pragma unroll
@@ -397,7 +401,8 @@ __global__ void __launch_bounds__(256) ztp_expand_cols(const uint16_t* __restric
           q0 = make_int4(__ldg(pos + c), __ldg(pos + c + 1), __ldg(pos + c + 2), __ldg(pos + c + 3));
           q1 = make_int4(__ldg(pos + c + 4), __ldg(pos + c + 5), __ldg(pos + c + 6), __ldg(pos + c + 7));
         }
-        if (q0.x >= 0 && q1.w == q0.x + 7 && (q0.x & 7) == 0 && sv)   // eight kept columns in a row
+        if (sv && q0.x >= 0 && (q0.x & 7) == 0 && q0.y == q0.x + 1 && q0.z == q0.x + 2 && q0.w == q0.x + 3 &&
+            q1.x == q0.x + 4 && q1.y == q0.x + 5 && q1.z == q0.x + 6 && q1.w == q0.x + 7)   // eight kept columns in a row
           w[u] = __ldg(reinterpret_cast<const uint4*>(s + q0.x));
         else
           w[u] = make_uint4(pick(q0.x) | (pick(q0.y) << 16), pick(q0.z) | (pick(q0.w) << 16),
